@@ -1,0 +1,256 @@
+/* sidp.h — C ABI of the B200-native SiDP decode hot path (libsidp.so).
+ *
+ * SiDP ("Memory-Efficient Data Parallelism for Offline LLM Inference", PAPER.md): inside a
+ * data-parallel group of d GPUs every transformer layer's pooled weights are owned by exactly
+ * one rank (§4.2); other ranks either stream the layer over NVLink into a small
+ * HBM cache ring (Weight-as-a-Service, WaS) or ship activations to the owner
+ * (Compute-as-a-Service, CaS).  Both modes compute exactly what replicated
+ * DP computes.
+ *
+ * Conventions (all functions):
+ *  - Every pointer argument is a plain host or device pointer as documented per argument;
+ *    no framework types cross this boundary.  Streams are cudaStream_t passed as void*.
+ *  - All device work is enqueued asynchronously on the caller's stream (plus the library's
+ *    internal fetch stream for WaS).  Nothing blocks the host except sidp_alloc, the
+ *    synthetic init helpers' error checks, sidp_import_handles and sidp_destroy.
+ *  - Return value: SIDP_OK or a negative sidp_status; nothing throws across the ABI.
+ *    SIDP_EINVAL means no work was enqueued.  CUDA failures are sticky (SIDP_ECUDA for the
+ *    rest of the context's life).  sidp_last_error() gives a thread-local message.
+ *  - Ownership: the library owns what it allocates (owned-weight arena, cache slots, CaS
+ *    staging/flags, workspaces, peer mappings, schedule tables) and frees it in
+ *    sidp_destroy.  The caller owns activations, KV caches, token/position buffers.
+ *  - One host thread per context; a context is not thread-safe.
+ */
+#ifndef SIDP_H_
+#define SIDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sidp_ctx sidp_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  SIDP_OK = 0,
+  SIDP_EINVAL = -1,   /* bad argument; nothing enqueued */
+  SIDP_ECUDA = -2,    /* CUDA runtime/driver error (sticky) */
+  SIDP_ENOMEM = -3,   /* device allocation failed */
+  SIDP_ESTATE = -4,   /* call out of protocol order (e.g. layer order, not allocated) */
+  SIDP_EPEER = -5,    /* peer handle import failed */
+  SIDP_ETIMEOUT = -6  /* a device-side flag wait timed out (CaS peer did not arrive) */
+} sidp_status;
+
+typedef enum {
+  SIDP_WAS = 0,        /* Weight-as-a-Service: stream remote layers into the cache ring */
+  SIDP_CAS = 1,        /* Compute-as-a-Service: ship activations to the owner */
+  SIDP_REPLICATED = 2  /* baseline: every layer local (requires world == 1) */
+} sidp_mode;
+
+typedef enum {
+  SIDP_ORDER_EXEC = 0,  /* remote layers in execution order (+ C-S7 stagger); any S >= 1 */
+  SIDP_ORDER_PAPER = 1  /* peak-shifting cycles of PAPER.md:200; requires S >= d-1 */
+} sidp_order;
+
+typedef enum {
+  SIDP_POOL_LAYER = 0,  /* pool QKV, O, gate/up, down (north_star; per-GPU ~W/d) */
+  SIDP_POOL_FFN = 1     /* pool gate/up/down only, attention replicated */
+} sidp_pool;
+
+typedef enum {
+  SIDP_FETCH_SM = 0,    /* hand-written SM copy kernel over peer memory (K1) */
+  SIDP_FETCH_CE = 1     /* copy-engine cudaMemcpyAsync (the paper's mechanism; baseline) */
+} sidp_fetch_engine;
+
+/* Decoder model dimensions (HF-Llama block; Qwen3 qk_norm and Qwen2.5 QKV-bias variants).
+ * Constraints: hidden, intermediate, n_q_heads*head_dim multiples of 64; head_dim 64 or 128;
+ * n_q_heads % n_kv_heads == 0 and n_q_heads/n_kv_heads <= 16. */
+typedef struct {
+  int32_t num_layers, hidden, n_q_heads, n_kv_heads, head_dim, intermediate, vocab;
+  int32_t qkv_bias; /* 0/1 */
+  int32_t qk_norm;  /* 0/1 */
+  float rms_eps, rope_theta;
+} sidp_model_desc;
+
+/* Group / runtime configuration.  PAPER.md:164 (init: assign owners, load only owned
+ * weights, register buffers and export handles), PAPER.md:238 (slot budgets). */
+typedef struct {
+  int32_t rank, world;          /* this rank r in [0, d), d = DP group size */
+  const int32_t* layer_owner;   /* host int32[num_layers], each in [0, world); NULL => l % world
+                                   (exactly one owner per layer) */
+  int32_t was_slots;            /* S >= 1 cache slots (north_star default 2; paper d-1) */
+  int32_t cas_slots;            /* CaS staging buffers >= 1 (2) */
+  int32_t order;                /* sidp_order */
+  int32_t pool_scope;           /* sidp_pool */
+  int32_t max_batch;            /* max rows per rank per step */
+  int32_t max_ctx;              /* KV positions per sequence; a step needs pos + 1 <= max_ctx */
+  int32_t fetch_sms;            /* CTAs used by the SM fetch kernel (0 => 16) */
+  int32_t fetch_engine;         /* sidp_fetch_engine */
+  int32_t stagger;              /* 1 => C-S7 start offsets t_r = (-r) mod (d-1) fetch ticks */
+  int32_t device;               /* CUDA device ordinal the context lives on */
+  uint64_t seed;                /* seed of the synthetic (counter-hash) weights, K12 */
+} sidp_config;
+
+/* Caller-owned KV cache of this rank (never pooled).
+ * k_cache / v_cache: device bf16 [num_layers][max_batch][n_kv_heads][max_ctx][head_dim].
+ * pos: device int32[batch], tokens already cached per row; the step writes the new k/v at
+ * position pos[b] and attends over [0, pos[b]].  max_pos: host hint >= max_b pos[b]. */
+typedef struct {
+  void* k_cache;
+  void* v_cache;
+  const int32_t* pos;
+  int32_t max_pos;
+} sidp_kv;
+
+/* One decode step of this rank. tokens/next: device int32[batch].  batch == 0 marks a
+ * dummy step: no data movement and no compute in CaS; the owner still
+ * serves peers.  logits (optional): device fp32 [batch][vocab].  layer_inputs (optional):
+ * device bf16 [num_layers][batch][hidden], receives each layer's input x (teacher-forcing
+ * parity dumps). */
+typedef struct {
+  const int32_t* tokens;
+  int32_t* next;
+  int32_t batch;
+  sidp_kv kv;
+  float* logits;
+  void* layer_inputs;
+} sidp_batch;
+
+typedef struct {
+  uint64_t steps;           /* completed sidp_step calls */
+  uint64_t fetches;         /* remote-layer fetches enqueued */
+  uint64_t bytes_fetched;   /* verbatim bytes copied into slots */
+  uint64_t launches;        /* device kernels (and copy-engine copies) enqueued */
+  uint64_t cas_round_trips; /* CaS round trips this rank took part in */
+  int32_t mode;             /* current sidp_mode */
+  int32_t timeouts;         /* device flag-wait timeouts observed */
+  uint64_t layer_bytes;     /* pooled bytes of one layer (what one fetch moves) */
+  uint64_t local_layer_bytes;  /* un-pooled per-layer bytes every rank keeps */
+  uint64_t owned_bytes;     /* owned-weight arena */
+  uint64_t slot_bytes;      /* S x layer_bytes */
+  uint64_t replicated_bytes;   /* embedding + final norm + LM head + local layer parts */
+  uint64_t workspace_bytes; /* activations, split-K / split-KV workspaces, staging */
+  double timed_ms;          /* sum of timed-kernel durations (sidp_set_timing) */
+  uint64_t timed_launches;  /* launches of the timed kernel class */
+} sidp_stats_t;
+
+/* ---- lifecycle --------------------------------------------------------------------- */
+
+/* Validate model + config, build the owner map, prefetch plan and FIFO slot recurrence
+ * (host only; no device work, callable without a GPU).  SIDP_EINVAL on: bad dims, rank not
+ * in [0, world), owner not in [0, world), was_slots < 1, SIDP_ORDER_PAPER with
+ * was_slots < world-1 (deadlock), max_batch/max_ctx < 1.
+ * *out receives a context owned by the library (free with sidp_destroy). */
+sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp_ctx** out);
+
+/* Allocate device state on cfg->device: owned-weight arena (owned layers only; non-owned
+ * layers get no memory — the paper's "placeholders"), S cache slots,
+ * replicated tensors, CaS staging + flags, workspaces, the fetch stream and events. */
+sidp_status sidp_alloc(sidp_ctx* ctx);
+
+/* K12: fill owned layers, local layer parts and replicated tensors with the counter-hash
+ * synthetic values (same function as sidp_inputs/gen.py), on `stream`. */
+sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream);
+
+/* Export this rank's owned arena / staging / flag handles into blob (host buffer of
+ * *len bytes; on return *len = bytes written; pass blob = NULL to query the size). */
+sidp_status sidp_export_handles(sidp_ctx* ctx, void* blob, size_t* len);
+
+/* Import all ranks' blobs (host pointers, rank order, world entries; this rank's own entry
+ * is ignored).  Same-process blobs map directly; others via CUDA IPC (peer access enabled).
+ * SIDP_EPEER if a handle cannot be opened. */
+sidp_status sidp_import_handles(sidp_ctx* ctx, const void* const* blobs, const size_t* lens);
+
+void sidp_destroy(sidp_ctx* ctx);
+
+/* ---- the hot path ------------------------------------------------------------------- */
+
+/* One decoder layer on x (device bf16 [batch][hidden], in/out), §4.2 / §4.3:
+ * RMSNorm -> QKV (+bias) -> (qk-norm) RoPE, KV append -> GQA attention -> O + residual ->
+ * RMSNorm -> gate/up + SiLU*mul -> down + residual.
+ *  mode SIDP_WAS: an owned layer runs from the arena; a remote layer waits for its slot
+ *    (filled by the fetch stream in plan order) and frees it after the down GEMM.  Layers
+ *    must be called in execution order (0..L-1, step after step): else SIDP_ESTATE.
+ *  mode SIDP_CAS: collective per layer — every rank of the group calls it for every layer
+ *    in order; batch == 0 (dummy) returns after serving peers if this rank owns the layer.
+ *  mode SIDP_REPLICATED: world == 1 only.
+ * batch > max_batch, layer out of range, or pos out of range => SIDP_EINVAL. */
+sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t layer,
+                              int32_t mode, const sidp_kv* kv, void* stream);
+
+/* One full decode step: embedding gather -> L layers in the current
+ * mode -> final RMSNorm -> LM head GEMM with fused argmax (ties -> lowest index). */
+sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* batch, void* stream);
+
+/* Globally consistent mode directive: must be called with identical
+ * arguments on every rank.  Takes effect at the start of step `effective_step`
+ * (0-based count of sidp_step calls).  Switching drains the WaS ring and resets the plan. */
+sidp_status sidp_set_mode(sidp_ctx* ctx, int32_t mode, int64_t effective_step);
+
+/* Control plane for CaS: per-rank rows of the coming step (host int32[world], identical on
+ * all ranks; 0 = dummy).  Sets the fused-GEMM offsets (exclusive prefix sums). */
+sidp_status sidp_set_batches(sidp_ctx* ctx, const int32_t* batches);
+
+/* ---- introspection (host only; no GPU needed) ------------------------------------------ */
+
+sidp_status sidp_owner_of(const sidp_ctx* ctx, int32_t layer, int32_t* owner);
+
+/* This rank's per-pass prefetch plan (layers in fetch order). */
+sidp_status sidp_get_plan(const sidp_ctx* ctx, int32_t* layers, int32_t capacity, int32_t* n);
+
+/* The (step, layer, slot) fetch schedule of the first `steps` passes from the FIFO
+ * free-list recurrence — compared bit-exactly with the oracle. */
+sidp_status sidp_get_schedule(const sidp_ctx* ctx, int32_t steps, int32_t* fetch_step,
+                              int32_t* fetch_layer, int32_t* fetch_slot, int32_t capacity,
+                              int32_t* n);
+
+/* Fetch-tick offset of this rank's fetch stream (C-S7 stagger). */
+sidp_status sidp_stagger_ticks(const sidp_ctx* ctx, int32_t* ticks);
+
+/* Device-side log of fetches actually issued by the runtime (step, layer, slot) since the
+ * last reset of the plan (for protocol parity). */
+sidp_status sidp_get_fetch_log(const sidp_ctx* ctx, int32_t* fetch_step, int32_t* fetch_layer,
+                               int32_t* fetch_slot, int32_t capacity, int32_t* n);
+
+sidp_status sidp_stats(const sidp_ctx* ctx, sidp_stats_t* out);
+
+/* Time every launch of one kernel class with CUDA events on its own stream:
+ * 0 off, 1 gate/up GEMM, 2 attention, 3 fetch, 4 down GEMM, 5 QKV GEMM, 6 O GEMM,
+ * 7 LM head.  sidp_stats().timed_ms sums them (host-synchronising read). */
+sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t kernel_class);
+
+const char* sidp_last_error(void);
+
+/* ---- test hooks (parity tests of single kernels; same kernels as the hot path) ---------- */
+
+/* tcgen05 GEMM: out = epilogue(x[M,K] . w[N,K]^T).  epi: 0 fp32, 1 bf16, 2 bf16 + resid,
+ * 3 SiLU(gate)*up over 128-row [gate 64 | up 64] tiles, 4 fused argmax (u64 packed; call
+ * with out zeroed).  k_splits 0 = auto.  Device pointers; enqueued on stream. */
+sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ldw, int32_t M,
+                           int32_t N, int32_t K, int32_t epi, void* out, int32_t ldo,
+                           const void* resid, int32_t ldr, const void* bias, int32_t k_splits,
+                           void* stream);
+
+/* K12 on an arbitrary buffer: dst[r*ld + c] = value(seed, tensor, layer, (row0+r)*lcols + c)
+ * with kind 0 weight (scale from scale_k), 1 gain, 2 bias, 3 unit; row_map 1 = packed
+ * gate/up interleave. */
+sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
+                          int32_t tensor, int32_t layer, int32_t kind, int32_t scale_k,
+                          int64_t row0, int64_t lcols, int32_t row_map, void* stream);
+
+/* Synthetic KV cache fill: cache[b][g][t][d] (b < B, t < T) from logical b_global = b0 + b. */
+sidp_status sidp_test_gen_kv(void* cache, int32_t B, int32_t nkv, int32_t smax, int32_t hd,
+                             int32_t T, int64_t b0, uint64_t seed, int32_t tensor, int32_t layer,
+                             void* stream);
+
+/* Pointer to layer `layer`'s pooled blob as resident on this rank (owned arena, else NULL)
+ * and the byte offsets of its components. */
+sidp_status sidp_layer_ptr(const sidp_ctx* ctx, int32_t layer, void** pooled, void** local);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SIDP_H_ */

@@ -1,0 +1,207 @@
+"""Thin Python binding over libsidp.so: same names as the C ABI, marshalling only.
+
+torch is used for device memory (caller-owned activations, KV caches, tokens) and
+streams; every step of the hot path runs in the library's CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _abi as A
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def model_desc(m) -> A.ModelDesc:
+    return A.ModelDesc(m.num_layers, m.hidden, m.n_q_heads, m.n_kv_heads, m.head_dim,
+                       m.intermediate, m.vocab, int(m.qkv_bias), int(m.qk_norm),
+                       float(m.rms_eps), float(m.rope_theta))
+
+
+class KVCache:
+    """Caller-owned KV cache of one rank: bf16 [L][max_batch][n_kv][max_ctx][head_dim] x 2."""
+
+    def __init__(self, m, max_batch: int, max_ctx: int, device="cuda"):
+        import torch
+        shape = (m.num_layers, max_batch, m.n_kv_heads, max_ctx, m.head_dim)
+        self.k = torch.empty(shape, dtype=torch.bfloat16, device=device)
+        self.v = torch.empty(shape, dtype=torch.bfloat16, device=device)
+        self.pos = torch.zeros(max_batch, dtype=torch.int32, device=device)
+        self.max_pos = 0
+        self.max_batch, self.max_ctx = max_batch, max_ctx
+
+    def set_pos(self, pos):
+        import torch
+        p = torch.as_tensor(pos, dtype=torch.int32)
+        self.pos[:p.numel()].copy_(p)
+        self.max_pos = int(p.max()) if p.numel() else 0
+
+    def advance(self, n: int = 1, batch: int | None = None):
+        b = self.max_batch if batch is None else batch
+        self.pos[:b] += n
+        self.max_pos += n
+
+    def c(self) -> A.KV:
+        return A.KV(self.k.data_ptr(), self.v.data_ptr(), self.pos.data_ptr(), self.max_pos)
+
+    def fill_synthetic(self, seed: int, b0: int, batch: int, T: int, stream=None):
+        """K12 fill of positions [0, T) for rows [0, batch) (logical rows b0 + b)."""
+        L = self.k.shape[0]
+        nkv, smax, hd = self.k.shape[2], self.k.shape[3], self.k.shape[4]
+        for l in range(L):
+            for t_id, buf in ((18, self.k), (19, self.v)):   # gen.KCACHE / gen.VCACHE
+                A.check(A.lib().sidp_test_gen_kv(_ptr(buf[l]), batch, nkv, smax, hd, T, b0, seed,
+                                                 t_id, l, _stream_ptr(stream)), "gen_kv")
+
+
+class Context:
+    def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
+                 max_batch=8, max_ctx=128, fetch_sms=16, fetch_engine="sm", stagger=True,
+                 device=0, seed=20261017, layer_owner=None, alloc=True):
+        self.m = m
+        self.rank, self.world = rank, world
+        self._owner_arr = None
+        own_ptr = None
+        if layer_owner is not None:
+            self._owner_arr = (C.c_int32 * m.num_layers)(*layer_owner)
+            own_ptr = C.cast(self._owner_arr, C.POINTER(C.c_int32))
+        self.cfg = A.Config(rank, world, own_ptr, slots, cas_slots,
+                            A.ORDER_EXEC if order == "exec" else A.ORDER_PAPER,
+                            A.POOL_LAYER if pool == "layer" else A.POOL_FFN,
+                            max_batch, max_ctx, fetch_sms,
+                            A.FETCH_SM if fetch_engine == "sm" else A.FETCH_CE,
+                            int(bool(stagger)), device, seed)
+        self.desc = model_desc(m)
+        h = C.c_void_p()
+        A.check(A.lib().sidp_init(C.byref(self.desc), C.byref(self.cfg), C.byref(h)), "sidp_init")
+        self.h = h
+        self.max_batch, self.max_ctx = max_batch, max_ctx
+        if alloc:
+            self.alloc()
+
+    # ---- lifecycle
+    def alloc(self):
+        A.check(A.lib().sidp_alloc(self.h), "sidp_alloc")
+
+    def init_weights_synthetic(self, stream=None):
+        A.check(A.lib().sidp_init_weights_synthetic(self.h, _stream_ptr(stream)),
+                "sidp_init_weights_synthetic")
+
+    def export_handles(self) -> bytes:
+        n = C.c_size_t(0)
+        A.check(A.lib().sidp_export_handles(self.h, None, C.byref(n)), "export(size)")
+        buf = (C.c_char * n.value)()
+        A.check(A.lib().sidp_export_handles(self.h, C.cast(buf, C.c_void_p), C.byref(n)), "export")
+        return bytes(buf[:n.value])
+
+    def import_handles(self, blobs):
+        bufs = [C.create_string_buffer(b, len(b)) for b in blobs]
+        ptrs = (C.c_void_p * len(bufs))(*[C.cast(b, C.c_void_p) for b in bufs])
+        lens = (C.c_size_t * len(bufs))(*[len(b) for b in blobs])
+        A.check(A.lib().sidp_import_handles(self.h, ptrs, lens), "sidp_import_handles")
+
+    def destroy(self):
+        if self.h:
+            A.lib().sidp_destroy(self.h)
+            self.h = None
+
+    close = destroy
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    # ---- hot path
+    def decode_layer(self, x, layer, mode, kv: KVCache, batch=None, stream=None):
+        b = x.shape[0] if batch is None else batch
+        kvc = kv.c()
+        A.check(A.lib().sidp_decode_layer(self.h, _ptr(x), b, layer, mode, C.byref(kvc),
+                                          _stream_ptr(stream)), "sidp_decode_layer")
+
+    def step(self, tokens, nxt, kv: KVCache, batch=None, logits=None, layer_inputs=None,
+             stream=None):
+        b = tokens.shape[0] if batch is None else batch
+        bt = A.Batch(tokens.data_ptr() if b else None, nxt.data_ptr() if b else None, b, kv.c(),
+                     logits.data_ptr() if logits is not None else None,
+                     layer_inputs.data_ptr() if layer_inputs is not None else None)
+        A.check(A.lib().sidp_step(self.h, C.byref(bt), _stream_ptr(stream)), "sidp_step")
+
+    def set_mode(self, mode, effective_step):
+        A.check(A.lib().sidp_set_mode(self.h, mode, effective_step), "sidp_set_mode")
+
+    def set_batches(self, batches):
+        arr = (C.c_int32 * len(batches))(*batches)
+        A.check(A.lib().sidp_set_batches(self.h, arr), "sidp_set_batches")
+
+    # ---- introspection
+    def owner_of(self, layer) -> int:
+        o = C.c_int32()
+        A.check(A.lib().sidp_owner_of(self.h, layer, C.byref(o)), "sidp_owner_of")
+        return o.value
+
+    def plan(self) -> list[int]:
+        n = C.c_int32()
+        A.check(A.lib().sidp_get_plan(self.h, None, 0, C.byref(n)), "plan")
+        arr = (C.c_int32 * max(1, n.value))()
+        A.check(A.lib().sidp_get_plan(self.h, arr, n.value, C.byref(n)), "plan")
+        return list(arr[:n.value])
+
+    def schedule(self, steps: int) -> list[tuple[int, int, int]]:
+        n = C.c_int32()
+        A.check(A.lib().sidp_get_schedule(self.h, steps, None, None, None, 0, C.byref(n)), "sched")
+        k = max(1, n.value)
+        t, l, s = (C.c_int32 * k)(), (C.c_int32 * k)(), (C.c_int32 * k)()
+        A.check(A.lib().sidp_get_schedule(self.h, steps, t, l, s, k, C.byref(n)), "sched")
+        return list(zip(t[:n.value], l[:n.value], s[:n.value]))
+
+    def fetch_log(self) -> list[tuple[int, int, int]]:
+        n = C.c_int32()
+        A.check(A.lib().sidp_get_fetch_log(self.h, None, None, None, 0, C.byref(n)), "log")
+        k = max(1, n.value)
+        t, l, s = (C.c_int32 * k)(), (C.c_int32 * k)(), (C.c_int32 * k)()
+        A.check(A.lib().sidp_get_fetch_log(self.h, t, l, s, k, C.byref(n)), "log")
+        return list(zip(t[:n.value], l[:n.value], s[:n.value]))
+
+    def stagger_ticks(self) -> int:
+        v = C.c_int32()
+        A.check(A.lib().sidp_stagger_ticks(self.h, C.byref(v)), "stagger")
+        return v.value
+
+    def stats(self) -> dict:
+        s = A.Stats()
+        A.check(A.lib().sidp_stats(self.h, C.byref(s)), "sidp_stats")
+        return {f: getattr(s, f) for f, _ in A.Stats._fields_}
+
+    def set_timing(self, kernel_class: int):
+        A.check(A.lib().sidp_set_timing(self.h, kernel_class), "sidp_set_timing")
+
+    def layer_ptr(self, layer):
+        p, q = C.c_void_p(), C.c_void_p()
+        A.check(A.lib().sidp_layer_ptr(self.h, layer, C.byref(p), C.byref(q)), "layer_ptr")
+        return p.value, q.value
+
+
+# ---- single-kernel test hooks (same kernels as the hot path) ----
+def test_gemm(x, w, out, M, N, K, epi, resid=None, bias=None, k_splits=0, ldo=None, stream=None):
+    A.check(A.lib().sidp_test_gemm(_ptr(x), x.stride(0), _ptr(w), w.stride(0), M, N, K, epi,
+                                   _ptr(out), out.stride(0) if ldo is None else ldo, _ptr(resid),
+                                   resid.stride(0) if resid is not None else 0, _ptr(bias),
+                                   k_splits, _stream_ptr(stream)), "sidp_test_gemm")
+
+
+def test_gen(dst, seed, tensor, layer, kind, scale_k=0, row0=0, lcols=None, row_map=0, stream=None):
+    rows, cols = dst.shape
+    A.check(A.lib().sidp_test_gen(_ptr(dst), dst.stride(0), rows, cols, seed, tensor, layer, kind,
+                                  scale_k, row0, cols if lcols is None else lcols, row_map,
+                                  _stream_ptr(stream)), "sidp_test_gen")

@@ -1,0 +1,111 @@
+// kernels.h — internal launchers of the SiDP device kernels (below the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sidp {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------- tcgen05 decode GEMM
+// Y[m, n] = sum_k X[m, k] * W[n, k]  (X [M,K] bf16 row-major, W [N,K] bf16 row-major)
+// computed swap-AB: W tiles are the UMMA "A" operand (128 features per tile), the
+// tokens are the UMMA "N" dimension, accumulators live in TMEM.
+enum GemmEpilogue : int {
+  EPI_F32 = 0,        // out fp32 = acc (+ bias)
+  EPI_BF16 = 1,       // out bf16 = acc (+ bias)
+  EPI_RESID = 2,      // out bf16 = acc + resid (bf16); out may alias resid
+  EPI_SILU_MUL = 3,   // W rows interleaved per 128-row tile: [gate 64 | up 64];
+                      // out[m, f] bf16 = silu(gate) * up, f = tile*64 + i
+  EPI_ARGMAX = 4,     // fused argmax over n: packed (value, lowest index) into out u64[M]
+};
+
+struct GemmArgs {
+  const bf16* x; int ldx;      // [M, K]
+  const bf16* w; int ldw;      // [N, K]
+  int M, N, K;
+  int epi;
+  void* out; int ldo;
+  const bf16* resid; int ldr;
+  const bf16* bias;            // [N] or null
+  int k_splits;                // 0 = auto
+  int max_ctas;                // 0 = all SMs
+};
+
+struct GemmWorkspace {
+  float* ws; size_t ws_bytes;  // split-K partials
+  int* counters; int n_counters;
+};
+
+cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t s);
+int gemm_pick_splits(int tiles, int nkb, int sms);
+
+// ---------------------------------------------------------------- element-wise / small kernels
+cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf16* y, int ldy,
+                           int rows, int h, cudaStream_t s);
+cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
+                         cudaStream_t s);
+// qkv fp32 [B, (nq+2nkv)*hd] -> q bf16 [B, nq, hd]; k, v appended to caches at pos[b]
+struct QkvPostArgs {
+  const float* qkv; int B, nq, nkv, hd;
+  const bf16* gq; const bf16* gk; float eps;    // qk_norm gains (null = off)
+  const float2* rope;                           // [max_pos, hd/2] (cos, sin)
+  const int32_t* pos;
+  bf16* q;
+  bf16* kc; bf16* vc;                           // [Bmax, nkv, Smax, hd]
+  int smax;
+};
+cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s);
+
+struct AttnArgs {
+  const bf16* q;              // [B, nq, hd]
+  const bf16* kc; const bf16* vc;   // [Bmax, nkv, Smax, hd]
+  const int32_t* pos;         // attend over [0, pos_b]
+  bf16* o;                    // [B, nq*hd]
+  int B, nq, nkv, hd, smax;
+  int max_tokens;             // host hint: max_b (pos_b + 1) <= smax (sizes the split)
+  float* ws; size_t ws_bytes; // split-KV partials
+};
+cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s);
+
+cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next, int rows,
+                                   cudaStream_t s);
+cudaError_t argmax_reset_launch(unsigned long long* packed, int rows, cudaStream_t s);
+
+// ---------------------------------------------------------------- K12 synthetic init
+// dst[i] = value(seed, tensor, layer, logical(i)) for a strided 2-D block of a logical
+// [rows, cols] tensor: logical index = (row0 + r) * lcols + c; dst = base + r*ld + c.
+enum GenKind : int { GEN_WEIGHT = 0, GEN_GAIN = 1, GEN_BIAS = 2, GEN_UNIT = 3 };
+struct GenArgs {
+  bf16* dst; int64_t ld;
+  int64_t rows, cols;
+  uint64_t seed; int tensor; int layer;
+  int kind; int scale_k;          // GEN_WEIGHT scale from K = scale_k
+  int64_t row0, lcols;            // logical row offset and logical row length
+  int row_map;                    // 0: identity; 1: gate/up interleave (see init.cu)
+  int inter;                      // intermediate size for row_map 1
+};
+cudaError_t gen_launch(const GenArgs& a, cudaStream_t s);
+// KV cache: cache[b, g, t, d] for b < B, t < T (logical b_global = b0 + b)
+cudaError_t gen_kv_launch(bf16* cache, int B, int nkv, int smax, int hd, int T, int64_t b0,
+                          uint64_t seed, int tensor, int layer, cudaStream_t s);
+
+// ---------------------------------------------------------------- WaS fetch
+// Verbatim copy of one pooled layer, owner HBM (possibly a peer VA) -> local slot.
+cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s);
+cudaError_t delay_launch(uint64_t ns, cudaStream_t s);
+
+// ---------------------------------------------------------------- CaS signalling
+struct FlagSet {
+  uint64_t* p[16];
+  int n;
+};
+cudaError_t signal_launch(uint64_t* flag, uint64_t value, cudaStream_t s);
+cudaError_t wait_launch(const FlagSet& flags, uint64_t value, uint64_t timeout_ns, int* err,
+                        cudaStream_t s);
+cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int rows, int row_bytes,
+                             cudaStream_t s);
+
+}  // namespace sidp

@@ -1,0 +1,128 @@
+// fetch.cu — K1 remote-weight fetch and the CaS signalling kernels.
+//
+// WaS fetch ("non-owner issues non-blocking device-to-device copies from
+// r(l)'s HBM into its local cache"): a verbatim copy of one packed pooled layer from the
+// owner's arena (a peer VA imported over CUDA IPC, NVLink/NVSwitch) into a local slot.
+// SM-issued, coalesced 16-byte loads with 4 loads in flight per thread before the stores
+// (L1::no_allocate: streamed once), on a bounded number of CTAs so the concurrently
+// running GEMMs keep the rest of the SMs.
+#include "../common.cuh"
+#include "../kernels.h"
+
+namespace sidp {
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_nc_v4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_na_v4(uint4* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+constexpr int kUnroll = 4;
+
+__global__ void __launch_bounds__(512) fetch_kernel(uint4* __restrict__ dst,
+                                                    const uint4* __restrict__ src, size_t nvec) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_nc_v4(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_na_v4(dst + i + u * stride, v[u]);
+  }
+  for (; i < nvec; i += stride) st_na_v4(dst + i, ld_nc_v4(src + i));
+}
+
+__global__ void delay_kernel(uint64_t ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) {
+  }
+}
+
+// Post a flag after all prior work of this stream (kernel boundary orders the data).
+__global__ void signal_kernel(uint64_t* flag, uint64_t value) {
+  __threadfence_system();
+  st_release_sys(flag, value);
+}
+
+// Wait until every flag >= value (system-scope acquire); bounded by timeout_ns, after
+// which *err is set and the kernel returns (surfaced as SIDP_ETIMEOUT by the host).
+__global__ void wait_kernel(const FlagSet flags, uint64_t value, uint64_t timeout_ns, int* err) {
+  const int i = threadIdx.x;
+  if (i < flags.n) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(flags.p[i]) < value) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void copy_rows_kernel(uint8_t* dst, int ldd, const uint8_t* src, int lds, int rows,
+                                 int row_bytes) {
+  const int nvec = row_bytes / 16;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)r * lds);
+    uint4* d = reinterpret_cast<uint4*>(dst + (size_t)r * ldd);
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x)
+      d[v] = s[v];
+  }
+}
+
+}  // namespace
+
+cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if ((bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) ||
+      (reinterpret_cast<uintptr_t>(src) & 15))
+    return cudaErrorInvalidValue;
+  if (ctas <= 0) ctas = 32;
+  fetch_kernel<<<ctas, 512, 0, s>>>(reinterpret_cast<uint4*>(dst),
+                                    reinterpret_cast<const uint4*>(src), bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t delay_launch(uint64_t ns, cudaStream_t s) {
+  if (ns == 0) return cudaSuccess;
+  delay_kernel<<<1, 32, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
+cudaError_t signal_launch(uint64_t* flag, uint64_t value, cudaStream_t s) {
+  signal_kernel<<<1, 1, 0, s>>>(flag, value);
+  return cudaGetLastError();
+}
+
+cudaError_t wait_launch(const FlagSet& flags, uint64_t value, uint64_t timeout_ns, int* err,
+                        cudaStream_t s) {
+  if (flags.n <= 0) return cudaSuccess;
+  if (flags.n > 16) return cudaErrorInvalidValue;
+  wait_kernel<<<1, 32, 0, s>>>(flags, value, timeout_ns, err);
+  return cudaGetLastError();
+}
+
+cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int rows, int row_bytes,
+                             cudaStream_t s) {
+  if (rows <= 0 || row_bytes <= 0) return cudaSuccess;
+  if (row_bytes % 16) return cudaErrorInvalidValue;
+  dim3 grid((row_bytes / 16 + 255) / 256, rows < 1024 ? rows : 1024);
+  copy_rows_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<uint8_t*>(dst), ldd,
+                                        reinterpret_cast<const uint8_t*>(src), lds, rows,
+                                        row_bytes);
+  return cudaGetLastError();
+}
+
+}  // namespace sidp

@@ -1,0 +1,100 @@
+// norm.cu — RMSNorm, embedding gather, argmax finalisation.
+// HBM-bound row kernels: 16-byte vector loads, fp32 statistics, one bf16 rounding.
+#include "../common.cuh"
+#include "../kernels.h"
+
+namespace sidp {
+
+namespace {
+
+// y = bf16( x * rsqrt(mean(x^2) + eps) * g ), one CTA per row, h % 8 == 0
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ x, int ldx,
+                                                      const bf16* __restrict__ g, float eps,
+                                                      bf16* __restrict__ y, int ldy, int h) {
+  const int row = blockIdx.x;
+  const bf16* xr = x + (size_t)row * ldx;
+  bf16* yr = y + (size_t)row * ldy;
+  const int nvec = h / 8;
+  float ss = 0.0f;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(xr + v * 8);
+    const bf16* e = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float f = bf16_to_f(e[i]);
+      ss += f * f;
+    }
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)h + eps);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(xr + v * 8);
+    const uint4 graw = *reinterpret_cast<const uint4*>(g + v * 8);
+    const bf16* e = reinterpret_cast<const bf16*>(&raw);
+    const bf16* ge = reinterpret_cast<const bf16*>(&graw);
+    uint4 out;
+    bf16* o = reinterpret_cast<bf16*>(&out);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = f_to_bf16(bf16_to_f(e[i]) * r * bf16_to_f(ge[i]));
+    *reinterpret_cast<uint4*>(yr + v * 8) = out;
+  }
+}
+
+__global__ void embed_kernel(const bf16* __restrict__ E, int h, const int32_t* __restrict__ tok,
+                             bf16* __restrict__ x) {
+  const int row = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[row] * h);
+  uint4* dst = reinterpret_cast<uint4*>(x + (size_t)row * h);
+  for (int v = threadIdx.x; v < h / 8; v += blockDim.x) dst[v] = src[v];
+}
+
+__global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* next, int rows) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) next[i] = (int32_t)(0xFFFFFFFFu - (uint32_t)(packed[i] & 0xFFFFFFFFull));
+}
+
+__global__ void argmax_reset_kernel(unsigned long long* packed, int rows) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) packed[i] = 0ull;
+}
+
+}  // namespace
+
+cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf16* y, int ldy,
+                           int rows, int h, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (h % 8) return cudaErrorInvalidValue;
+  rmsnorm_kernel<<<rows, 256, 0, s>>>(x, ldx, g, eps, y, ldy, h);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
+                         cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  embed_kernel<<<rows, 128, 0, s>>>(E, h, tokens, x);
+  return cudaGetLastError();
+}
+
+cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next, int rows,
+                                   cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  argmax_finalize_kernel<<<(rows + 255) / 256, 256, 0, s>>>(packed, next, rows);
+  return cudaGetLastError();
+}
+
+cudaError_t argmax_reset_launch(unsigned long long* packed, int rows, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  argmax_reset_kernel<<<(rows + 255) / 256, 256, 0, s>>>(packed, rows);
+  return cudaGetLastError();
+}
+
+}  // namespace sidp

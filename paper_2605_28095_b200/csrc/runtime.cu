@@ -1,0 +1,1180 @@
+// runtime.cu — host runtime behind the C ABI (include/sidp.h).
+//
+// Owns: the layer->owner map and per-rank prefetch plan, the WaS cache
+// ring driven by a FIFO free-list, the internal fetch
+// stream + CUDA events replacing the paper's housekeeper thread ("notifications
+// ... driven by CUDA events"), owner-only weight placement + IPC export/import
+// (PAPER.md:164, 186, 236), the CaS staging/flag protocol and the
+// globally consistent mode directive.  Device work is in kernels/*.cu.
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sidp.h"
+#include "kernels.h"
+
+using sidp::bf16;
+
+namespace {
+
+thread_local std::string g_err;
+
+sidp_status fail(sidp_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+// Packed per-layer components.  Each lives either in the pooled blob (owned by one rank,
+// fetched verbatim by the others) or in the local blob every rank keeps.
+enum Comp { C_WQKV = 0, C_WO, C_WGU, C_WD, C_GATTN, C_GMLP, C_GQ, C_GK, C_BQKV, C_N };
+
+constexpr uint32_t kMagic = 0x53694450;  // "SiDP"
+constexpr int kTimingPool = 8192;
+
+struct HandleBlob {
+  uint32_t magic;
+  int32_t rank;
+  int32_t pid;
+  int32_t device;
+  uint64_t arena_ptr, cas_ptr;
+  uint64_t arena_bytes, cas_bytes;
+  cudaIpcMemHandle_t arena_h, cas_h;
+  int32_t has_arena, has_cas;
+};
+
+}  // namespace
+
+struct sidp_ctx {
+  sidp_model_desc m{};
+  sidp_config c{};
+  int L = 0, d = 1, r = 0, S = 1;
+  std::vector<int> owner, plan, sorted_plan, plan_pos, owned_index, owned_layers;
+  int R = 0;                       // remote layers per pass
+  // layout (elements)
+  size_t comp_off[C_N]{}, comp_elems[C_N]{};
+  bool comp_pooled[C_N]{};
+  size_t pooled_elems = 0, local_elems = 0;
+  int qdim = 0, kvdim = 0, qkvdim = 0;
+  // device state
+  bool allocated = false;
+  int sticky = 0;
+  bf16* arena = nullptr;           // owned pooled blobs
+  bf16* local = nullptr;           // L local blobs
+  bf16* slots = nullptr;           // S pooled blobs
+  bf16 *embed = nullptr, *g_final = nullptr, *wlm = nullptr;
+  float2* rope = nullptr;
+  int rows_max = 0;                // activation rows (max_batch, or world*max_batch for CaS)
+  bf16 *xbuf = nullptr, *u = nullptr, *q = nullptr, *o = nullptr, *act = nullptr;
+  bf16* cas_out = nullptr;         // owner-side CaS result rows
+  float* qkv = nullptr;
+  unsigned long long* amax = nullptr;
+  float* gemm_ws = nullptr;
+  size_t gemm_ws_bytes = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+  float* attn_ws = nullptr;
+  size_t attn_ws_bytes = 0;
+  cudaStream_t fetch_stream = nullptr;
+  std::vector<cudaEvent_t> ready_ev, free_ev;
+  std::vector<char> free_recorded;
+  std::vector<const bf16*> peer_arena;
+  std::vector<void*> ipc_opened;
+  // CaS state (library-owned, exported): [flags | stage slots | recv]
+  uint8_t* cas = nullptr;
+  size_t cas_bytes = 0, cas_stage_off = 0, cas_recv_off = 0, cas_stage_bytes = 0;
+  int stage_width = 0;             // bf16 elements per staged row
+  size_t recv_row_bytes = 0;
+  std::vector<uint8_t*> peer_cas;
+  int* dev_err = nullptr;
+  std::vector<int> batches;        // per-rank rows (control plane)
+  int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
+  std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
+  // WaS schedule state
+  int64_t fetch_j = 0, compute_k = 0;
+  std::vector<int> push, slot_of_fetch;
+  std::vector<int32_t> log_t, log_l, log_s;
+  int next_layer = 0;
+  int64_t step = 0;
+  bool stagger_pending = false;
+  // mode
+  int mode = SIDP_WAS;
+  int pending_mode = -1;
+  int64_t pending_step = 0;
+  // stats + timing
+  sidp_stats_t st{};
+  int timed_class = 0;
+  std::vector<cudaEvent_t> tev;
+  int tev_used = 0;
+  double timed_acc_ms = 0.0;
+};
+
+namespace {
+
+bool ck(sidp_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  c->sticky = 1;
+  fail(SIDP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return false;
+}
+#define CK(call)                                   \
+  do {                                             \
+    if (!ck(ctx, (call), #call)) return SIDP_ECUDA; \
+  } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+void build_layout(sidp_ctx* c) {
+  const auto& m = c->m;
+  c->qdim = m.n_q_heads * m.head_dim;
+  c->kvdim = m.n_kv_heads * m.head_dim;
+  c->qkvdim = c->qdim + 2 * c->kvdim;
+  c->comp_elems[C_WQKV] = (size_t)c->qkvdim * m.hidden;
+  c->comp_elems[C_WO] = (size_t)m.hidden * c->qdim;
+  c->comp_elems[C_WGU] = (size_t)2 * m.intermediate * m.hidden;
+  c->comp_elems[C_WD] = (size_t)m.hidden * m.intermediate;
+  c->comp_elems[C_GATTN] = m.hidden;
+  c->comp_elems[C_GMLP] = m.hidden;
+  c->comp_elems[C_GQ] = m.qk_norm ? m.head_dim : 0;
+  c->comp_elems[C_GK] = m.qk_norm ? m.head_dim : 0;
+  c->comp_elems[C_BQKV] = m.qkv_bias ? c->qkvdim : 0;
+  // Pooled: the weight matrices (LAYER: QKV, O, gate/up, down; FFN: gate/up, down).  Norm
+  // gains and biases (< 0.01% of a layer) stay replicated so CaS requesters can normalise
+  // locally and the owner can apply the bias in its fused GEMM.
+  const bool ffn = c->c.pool_scope == SIDP_POOL_FFN;
+  for (int i = 0; i < C_N; ++i)
+    c->comp_pooled[i] = ffn ? (i == C_WGU || i == C_WD) : (i <= C_WD);
+  c->pooled_elems = c->local_elems = 0;
+  for (int i = 0; i < C_N; ++i) {
+    size_t& acc = c->comp_pooled[i] ? c->pooled_elems : c->local_elems;
+    c->comp_off[i] = acc;
+    acc += align_up(c->comp_elems[i], 128);   // 256-byte aligned components
+  }
+}
+
+// ---- schedule (host, reading C-A3 for the truncated cycle) ----
+std::vector<int> build_plan(const std::vector<int>& owner, int d, int r, int order) {
+  const int L = (int)owner.size();
+  std::vector<int> pl;
+  if (order == SIDP_ORDER_EXEC) {
+    for (int l = 0; l < L; ++l)
+      if (owner[l] != r) pl.push_back(l);
+    return pl;
+  }
+  for (int c0 = 0; c0 < L; c0 += d) {
+    const int w = std::min(d, L - c0);
+    const int start = r < w ? r : 0;
+    for (int k = 0; k < w; ++k) {
+      const int l = c0 + (start + k) % w;
+      if (owner[l] != r) pl.push_back(l);
+    }
+  }
+  return pl;
+}
+
+int plan_lag(const std::vector<int>& pl) {
+  std::vector<int> sorted = pl;
+  std::sort(sorted.begin(), sorted.end());
+  int lag = 0;
+  for (size_t p = 0; p < pl.size(); ++p) {
+    const int q = (int)(std::lower_bound(sorted.begin(), sorted.end(), pl[p]) - sorted.begin());
+    lag = std::max(lag, (int)p - q);
+  }
+  return lag;
+}
+
+// FIFO free-list recurrence: slot(fetch j) = push[j]; push[S + k] = slot of the k-th
+// remote compute entry (whose fetch index is p(k) = t*R + pos_in_plan(layer)).
+int64_t fetch_index_of_compute(const sidp_ctx* c, int64_t k) {
+  const int64_t t = k / c->R;
+  const int l = c->sorted_plan[k % c->R];
+  return t * c->R + c->plan_pos[l];
+}
+
+void schedule_reset(sidp_ctx* c) {
+  c->fetch_j = c->compute_k = 0;
+  c->push.clear();
+  for (int s = 0; s < c->S; ++s) c->push.push_back(s);
+  c->slot_of_fetch.clear();
+  c->log_t.clear();
+  c->log_l.clear();
+  c->log_s.clear();
+  c->next_layer = 0;
+  c->stagger_pending = true;
+}
+
+int stagger_ticks_of(const sidp_ctx* c) {
+  if (!c->c.stagger || c->c.order != SIDP_ORDER_EXEC || c->d < 3) return 0;
+  return ((-c->r) % (c->d - 1) + (c->d - 1)) % (c->d - 1);
+}
+
+void count_launch(sidp_ctx* c, int n = 1) { c->st.launches += n; }
+
+// ---- optional per-class kernel timing ----
+void timing_begin(sidp_ctx* c, int cls, cudaStream_t s) {
+  if (c->timed_class != cls || c->tev_used + 2 > (int)c->tev.size()) return;
+  cudaEventRecord(c->tev[c->tev_used], s);
+}
+void timing_end(sidp_ctx* c, int cls, cudaStream_t s) {
+  if (c->timed_class != cls || c->tev_used + 2 > (int)c->tev.size()) return;
+  cudaEventRecord(c->tev[c->tev_used + 1], s);
+  c->tev_used += 2;
+  c->st.timed_launches++;
+}
+
+struct LayerW {
+  const bf16 *wqkv, *wo, *wgu, *wd, *g_attn, *g_mlp, *g_q, *g_k, *b_qkv;
+};
+
+LayerW layer_weights(const sidp_ctx* c, const bf16* pooled, const bf16* local) {
+  auto P = [&](int comp) -> const bf16* {
+    if (c->comp_elems[comp] == 0) return nullptr;
+    return (c->comp_pooled[comp] ? pooled : local) + c->comp_off[comp];
+  };
+  return LayerW{P(C_WQKV), P(C_WO), P(C_WGU), P(C_WD), P(C_GATTN),
+                P(C_GMLP), P(C_GQ), P(C_GK), P(C_BQKV)};
+}
+
+sidp::GemmWorkspace gws(sidp_ctx* c) {
+  return sidp::GemmWorkspace{c->gemm_ws, c->gemm_ws_bytes, c->counters, c->n_counters};
+}
+
+cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, int M, int N, int K,
+                 int epi, void* out, int ldo, const bf16* resid, int ldr, const bf16* bias,
+                 cudaStream_t s) {
+  sidp::GemmArgs a{};
+  a.x = x; a.ldx = ldx; a.w = w; a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = epi;
+  a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias;
+  timing_begin(c, cls, s);
+  cudaError_t e = sidp::gemm_launch(a, gws(c), s);
+  timing_end(c, cls, s);
+  count_launch(c);
+  return e;
+}
+
+// ---- the layer's kernels ----------------------------------------------------------
+// Attention half up to o (C-N2 steps 1-6).  When `qkv_in` is given (CaS RT1 returned it),
+// the RMSNorm + QKV GEMM are skipped.
+sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int layer,
+                      const sidp_kv* kv, const float* qkv_in, cudaStream_t s) {
+  const auto& m = ctx->m;
+  const float* qkv = qkv_in;
+  if (!qkv) {
+    CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+    count_launch(ctx);
+    CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_F32, ctx->qkv,
+            ctx->qkvdim, nullptr, 0, W.b_qkv, s));
+    qkv = ctx->qkv;
+  }
+  const size_t lstride = (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
+  bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
+  bf16* vc = reinterpret_cast<bf16*>(kv->v_cache) + (size_t)layer * lstride;
+  sidp::QkvPostArgs qa{};
+  qa.qkv = qkv; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
+  qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;
+  qa.q = ctx->q; qa.kc = kc; qa.vc = vc; qa.smax = ctx->c.max_ctx;
+  CK(sidp::qkv_post_launch(qa, s));
+  count_launch(ctx);
+  sidp::AttnArgs aa{};
+  aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.pos = kv->pos; aa.o = ctx->o; aa.B = B;
+  aa.nq = m.n_q_heads; aa.nkv = m.n_kv_heads; aa.hd = m.head_dim; aa.smax = ctx->c.max_ctx;
+  aa.max_tokens = kv->max_pos + 1; aa.ws = ctx->attn_ws; aa.ws_bytes = ctx->attn_ws_bytes;
+  timing_begin(ctx, 2, s);
+  CK(sidp::attention_launch(aa, s));
+  timing_end(ctx, 2, s);
+  count_launch(ctx);
+  return SIDP_OK;
+}
+
+// C-N2 steps 7-10 on rows of (o, x); writes out (may alias x).
+sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf16* x, int ldx,
+                     bf16* out, int B, cudaStream_t s) {
+  const auto& m = ctx->m;
+  // x2 = x + o W_o^T  (into out)
+  CK(gemm(ctx, 6, o, ldo_, W.wo, B, m.hidden, ctx->qdim, sidp::EPI_RESID, out, m.hidden, x, ldx,
+          nullptr, s));
+  CK(sidp::rmsnorm_launch(out, m.hidden, W.g_mlp, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+  count_launch(ctx);
+  CK(gemm(ctx, 1, ctx->u, m.hidden, W.wgu, B, 2 * m.intermediate, m.hidden, sidp::EPI_SILU_MUL,
+          ctx->act, m.intermediate, nullptr, 0, nullptr, s));
+  CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, m.hidden, m.intermediate, sidp::EPI_RESID,
+          out, m.hidden, out, m.hidden, nullptr, s));
+  return SIDP_OK;
+}
+
+sidp_status full_layer(sidp_ctx* ctx, const LayerW& W, bf16* x, int B, int layer,
+                       const sidp_kv* kv, cudaStream_t s) {
+  sidp_status st = attn_part(ctx, W, x, B, layer, kv, nullptr, s);
+  if (st != SIDP_OK) return st;
+  return mlp_part(ctx, W, ctx->o, ctx->qdim, x, ctx->m.hidden, x, B, s);
+}
+
+// ---- WaS fetch pump ----
+sidp_status enqueue_fetch(sidp_ctx* ctx) {
+  const int64_t j = ctx->fetch_j;
+  const int s = ctx->push[j];
+  const int64_t t = j / ctx->R;
+  const int l = ctx->plan[j % ctx->R];
+  if (ctx->stagger_pending) {
+    ctx->stagger_pending = false;
+    const int ticks = stagger_ticks_of(ctx);
+    if (ticks > 0) {
+      // one tick = one single-reader layer fetch at the NVLink peer-copy rate (~770 GB/s)
+      const double tick_ns = (double)ctx->pooled_elems * 2.0 / 770.0;
+      CK(sidp::delay_launch((uint64_t)(ticks * tick_ns), ctx->fetch_stream));
+      count_launch(ctx);
+    }
+  }
+  if (ctx->free_recorded[s]) CK(cudaStreamWaitEvent(ctx->fetch_stream, ctx->free_ev[s], 0));
+  const bf16* src = ctx->peer_arena[ctx->owner[l]];
+  if (!src) return fail(SIDP_ESTATE, "peer arena of rank %d not imported", ctx->owner[l]);
+  src += (size_t)ctx->owned_index[l] * ctx->pooled_elems;
+  bf16* dst = ctx->slots + (size_t)s * ctx->pooled_elems;
+  const size_t bytes = ctx->pooled_elems * 2;
+  timing_begin(ctx, 3, ctx->fetch_stream);
+  if (ctx->c.fetch_engine == SIDP_FETCH_CE) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
+  } else {
+    CK(sidp::fetch_launch(dst, src, bytes, ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 16,
+                          ctx->fetch_stream));
+  }
+  timing_end(ctx, 3, ctx->fetch_stream);
+  count_launch(ctx);
+  CK(cudaEventRecord(ctx->ready_ev[s], ctx->fetch_stream));
+  ctx->slot_of_fetch.push_back(s);
+  ctx->log_t.push_back((int32_t)t);
+  ctx->log_l.push_back(l);
+  ctx->log_s.push_back(s);
+  ctx->st.fetches++;
+  ctx->st.bytes_fetched += bytes;
+  ctx->fetch_j++;
+  return SIDP_OK;
+}
+
+sidp_status pump(sidp_ctx* ctx) {
+  while (ctx->R > 0 && ctx->fetch_j < (int64_t)ctx->push.size()) {
+    sidp_status st = enqueue_fetch(ctx);
+    if (st != SIDP_OK) return st;
+  }
+  return SIDP_OK;
+}
+
+sidp_status check_ready(sidp_ctx* ctx) {
+  if (!ctx->allocated) return fail(SIDP_ESTATE, "sidp_alloc not called");
+  if (ctx->sticky) return fail(SIDP_ECUDA, "context has a sticky CUDA error");
+  return SIDP_OK;
+}
+
+sidp_status validate_kv(sidp_ctx* ctx, const sidp_kv* kv, int B) {
+  if (!kv || !kv->k_cache || !kv->v_cache || !kv->pos) return fail(SIDP_EINVAL, "kv pointers");
+  if (B > 0 && (kv->max_pos < 0 || kv->max_pos + 1 > ctx->c.max_ctx))
+    return fail(SIDP_EINVAL, "max_pos %d out of range (max_ctx %d)", kv->max_pos, ctx->c.max_ctx);
+  return SIDP_OK;
+}
+
+sidp_status was_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* kv,
+                      cudaStream_t s) {
+  if (layer != ctx->next_layer)
+    return fail(SIDP_ESTATE, "WaS layers must run in order: expected %d got %d", ctx->next_layer,
+                layer);
+  const bf16* local = ctx->local + (size_t)layer * ctx->local_elems;
+  sidp_status st;
+  if (ctx->owner[layer] == ctx->r) {
+    st = pump(ctx);   // keep the fetch stream running ahead under owned-layer compute
+    if (st != SIDP_OK) return st;
+    const bf16* pooled = ctx->arena + (size_t)ctx->owned_index[layer] * ctx->pooled_elems;
+    st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
+  } else {
+    const int64_t k = ctx->compute_k;
+    const int64_t p = fetch_index_of_compute(ctx, k);
+    st = pump(ctx);
+    if (st != SIDP_OK) return st;
+    if (p >= ctx->fetch_j) return fail(SIDP_ESTATE, "slot ring deadlock (plan lag >= slots)");
+    const int slot = ctx->slot_of_fetch[p];
+    CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
+    const bf16* pooled = ctx->slots + (size_t)slot * ctx->pooled_elems;
+    st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
+    if (st != SIDP_OK) return st;
+    CK(cudaEventRecord(ctx->free_ev[slot], s));   // housekeeper: release after last reader
+    ctx->free_recorded[slot] = 1;
+    ctx->push.push_back(slot);
+    ctx->compute_k++;
+    st = pump(ctx);
+  }
+  if (st != SIDP_OK) return st;
+  ctx->next_layer = (layer + 1) % ctx->L;
+  return SIDP_OK;
+}
+
+// ---- CaS ---------------------------------------------------------------------------
+// Flag block at the head of each rank's CaS arena (uint64 each):
+//   arrive[world]  (owner side: source rank r posted round trip rt+1)
+//   done           (requester side: owner returned round trip rt+1)
+//   served         (owner side: finished serving round trip rt+1)
+size_t flag_off_arrive(int r) { return (size_t)r * 8; }
+size_t flag_off_done(int world) { return (size_t)world * 8; }
+size_t flag_off_served(int world) { return (size_t)world * 8 + 8; }
+
+uint64_t* flag_ptr(uint8_t* base, size_t off) { return reinterpret_cast<uint64_t*>(base + off); }
+
+// One CaS round trip: live ranks copy their rows into the owner's
+// staging slot at the exclusive-prefix-sum offset and post an arrival flag; the owner waits
+// for every live rank, runs the pooled computation once over all fused rows, copies each
+// slice back into its source rank's receive buffer and posts that rank's done flag.  Dummy
+// ranks move nothing; the owner serves even when it is itself dummy (:218).
+struct SendPart {
+  const void* src;
+  int ld_elems;      // source row stride (bf16 elements)
+  int width;         // bf16 elements copied per row
+  int col;           // destination column (bf16 elements) within the staged row
+};
+
+template <typename OwnerFn>
+sidp_status cas_round_trip(sidp_ctx* ctx, int layer, const std::vector<SendPart>& parts,
+                           size_t out_row_bytes, OwnerFn&& owner_compute, cudaStream_t s) {
+  const int d = ctx->d, me = ctx->r, o = ctx->owner[layer];
+  const int64_t rt = ctx->rt++;
+  const int slot = (int)(rt % ctx->c.cas_slots);
+  std::vector<int> off(d, 0);
+  int total = 0;
+  for (int q = 0; q < d; ++q) {
+    off[q] = total;
+    total += ctx->batches[q];
+  }
+  if (total == 0) return SIDP_OK;   // every rank dummy: nothing moves
+  const int Bme = ctx->batches[me];
+  const int64_t prev = ctx->last_rt[o][slot];
+  ctx->last_rt[o][slot] = rt;
+  uint8_t* owner_cas = ctx->peer_cas[o];
+  if (!owner_cas) return fail(SIDP_ESTATE, "CaS arena of rank %d not imported", o);
+  const uint64_t tmo = 20ull * 1000 * 1000 * 1000;   // 20 s
+  if (Bme > 0) {
+    if (prev >= 0) {   // the owner's staging slot must be free of round trip `prev`
+      sidp::FlagSet fs{};
+      fs.p[0] = flag_ptr(owner_cas, flag_off_served(d));
+      fs.n = 1;
+      CK(sidp::wait_launch(fs, (uint64_t)prev + 1, tmo, ctx->dev_err, s));
+      count_launch(ctx);
+    }
+    uint8_t* stage = owner_cas + ctx->cas_stage_off + (size_t)slot * ctx->cas_stage_bytes +
+                     (size_t)off[me] * ctx->stage_width * 2;
+    for (const SendPart& p : parts) {
+      CK(sidp::copy_rows_launch(stage + (size_t)p.col * 2, ctx->stage_width * 2, p.src,
+                                p.ld_elems * 2, Bme, p.width * 2, s));
+      count_launch(ctx);
+    }
+    CK(sidp::signal_launch(flag_ptr(owner_cas, flag_off_arrive(me)), (uint64_t)rt + 1, s));
+    count_launch(ctx);
+  }
+  if (o == me) {
+    sidp::FlagSet fs{};
+    for (int q = 0; q < d; ++q)
+      if (ctx->batches[q] > 0) fs.p[fs.n++] = flag_ptr(ctx->cas, flag_off_arrive(q));
+    CK(sidp::wait_launch(fs, (uint64_t)rt + 1, tmo, ctx->dev_err, s));
+    count_launch(ctx);
+    const bf16* stage = reinterpret_cast<const bf16*>(ctx->cas + ctx->cas_stage_off +
+                                                      (size_t)slot * ctx->cas_stage_bytes);
+    const uint8_t* result = nullptr;
+    size_t result_ld = 0;
+    sidp_status stt = owner_compute(stage, ctx->stage_width, total, &result, &result_ld);
+    if (stt != SIDP_OK) return stt;
+    for (int q = 0; q < d; ++q) {
+      if (ctx->batches[q] == 0) continue;
+      uint8_t* recv = ctx->peer_cas[q] + ctx->cas_recv_off;
+      CK(sidp::copy_rows_launch(recv, (int)out_row_bytes, result + (size_t)off[q] * result_ld,
+                                (int)result_ld, ctx->batches[q], (int)out_row_bytes, s));
+      count_launch(ctx);
+      CK(sidp::signal_launch(flag_ptr(ctx->peer_cas[q], flag_off_done(d)), (uint64_t)rt + 1, s));
+      count_launch(ctx);
+    }
+    CK(sidp::signal_launch(flag_ptr(ctx->cas, flag_off_served(d)), (uint64_t)rt + 1, s));
+    count_launch(ctx);
+  }
+  if (Bme > 0) {
+    sidp::FlagSet fs{};
+    fs.p[0] = flag_ptr(ctx->cas, flag_off_done(d));
+    fs.n = 1;
+    CK(sidp::wait_launch(fs, (uint64_t)rt + 1, tmo, ctx->dev_err, s));
+    count_launch(ctx);
+  }
+  ctx->st.cas_round_trips++;
+  return SIDP_OK;
+}
+
+sidp_status cas_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* kv,
+                      cudaStream_t s) {
+  const auto& m = ctx->m;
+  if ((int)ctx->batches.size() != ctx->d) return fail(SIDP_ESTATE, "sidp_set_batches not called");
+  if (B != ctx->batches[ctx->r])
+    return fail(SIDP_EINVAL, "batch %d != sidp_set_batches value %d", B, ctx->batches[ctx->r]);
+  const int o = ctx->owner[layer];
+  const bf16* local = ctx->local + (size_t)layer * ctx->local_elems;
+  const bf16* own_pooled =
+      o == ctx->r ? ctx->arena + (size_t)ctx->owned_index[layer] * ctx->pooled_elems : nullptr;
+  const LayerW W = layer_weights(ctx, own_pooled, local);   // pooled parts valid on the owner only
+  uint8_t* recv = ctx->cas + ctx->cas_recv_off;
+  const int h = m.hidden;
+  sidp_status st;
+  if (ctx->c.pool_scope == SIDP_POOL_LAYER) {
+    // RT1: send u = RMSNorm(x); owner returns u W_qkv^T (+b) in fp32
+    if (B > 0) {
+      CK(sidp::rmsnorm_launch(x, h, W.g_attn, m.rms_eps, ctx->u, h, B, h, s));
+      count_launch(ctx);
+    }
+    st = cas_round_trip(
+        ctx, layer, {SendPart{ctx->u, h, h, 0}}, (size_t)ctx->qkvdim * 4,
+        [&](const bf16* stage, int ld, int total, const uint8_t** res, size_t* res_ld) {
+          if (gemm(ctx, 5, stage, ld, W.wqkv, total, ctx->qkvdim, h, sidp::EPI_F32, ctx->qkv,
+                   ctx->qkvdim, nullptr, 0, W.b_qkv, s) != cudaSuccess)
+            return fail(SIDP_ECUDA, "CaS qkv gemm");
+          *res = reinterpret_cast<const uint8_t*>(ctx->qkv);
+          *res_ld = (size_t)ctx->qkvdim * 4;
+          return SIDP_OK;
+        },
+        s);
+    if (st != SIDP_OK) return st;
+    if (B > 0) {   // RoPE, KV append and attention stay local (the KV cache is local)
+      st = attn_part(ctx, W, x, B, layer, kv, reinterpret_cast<const float*>(recv), s);
+      if (st != SIDP_OK) return st;
+    }
+    // RT2: send (o, x); owner returns out = x2 + MLP(x2), x2 = x + o W_o^T
+    st = cas_round_trip(
+        ctx, layer, {SendPart{ctx->o, ctx->qdim, ctx->qdim, 0}, SendPart{x, h, h, ctx->qdim}},
+        (size_t)h * 2,
+        [&](const bf16* stage, int ld, int total, const uint8_t** res, size_t* res_ld) {
+          sidp_status s2 = mlp_part(ctx, W, stage, ld, const_cast<bf16*>(stage + ctx->qdim), ld,
+                                    ctx->cas_out, total, s);
+          *res = reinterpret_cast<const uint8_t*>(ctx->cas_out);
+          *res_ld = (size_t)h * 2;
+          return s2;
+        },
+        s);
+  } else {
+    // FFN scope (the paper's design): attention, O and the residual are local; one round
+    // trip ships (u2, x2) and returns out = x2 + SiLU(u2 W_g^T)*(u2 W_u^T) W_d^T.
+    if (B > 0) {
+      st = attn_part(ctx, W, x, B, layer, kv, nullptr, s);
+      if (st != SIDP_OK) return st;
+      CK(gemm(ctx, 6, ctx->o, ctx->qdim, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, x, h, x, h,
+              nullptr, s));
+      CK(sidp::rmsnorm_launch(x, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
+      count_launch(ctx);
+    }
+    st = cas_round_trip(
+        ctx, layer, {SendPart{ctx->u, h, h, 0}, SendPart{x, h, h, h}}, (size_t)h * 2,
+        [&](const bf16* stage, int ld, int total, const uint8_t** res, size_t* res_ld) {
+          if (gemm(ctx, 1, stage, ld, W.wgu, total, 2 * m.intermediate, h, sidp::EPI_SILU_MUL,
+                   ctx->act, m.intermediate, nullptr, 0, nullptr, s) != cudaSuccess ||
+              gemm(ctx, 4, ctx->act, m.intermediate, W.wd, total, h, m.intermediate,
+                   sidp::EPI_RESID, ctx->cas_out, h, stage + h, ld, nullptr, s) != cudaSuccess)
+            return fail(SIDP_ECUDA, "CaS ffn gemm");
+          *res = reinterpret_cast<const uint8_t*>(ctx->cas_out);
+          *res_ld = (size_t)h * 2;
+          return SIDP_OK;
+        },
+        s);
+  }
+  if (st != SIDP_OK) return st;
+  if (B > 0) CK(cudaMemcpyAsync(x, recv, (size_t)B * h * 2, cudaMemcpyDeviceToDevice, s));
+  return SIDP_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+const char* sidp_last_error(void) { return g_err.c_str(); }
+
+sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp_ctx** out) {
+  if (!model || !cfg || !out) return fail(SIDP_EINVAL, "null argument");
+  const auto& m = *model;
+  if (m.num_layers < 1 || m.hidden < 64 || m.n_q_heads < 1 || m.n_kv_heads < 1 ||
+      m.intermediate < 64 || m.vocab < 1)
+    return fail(SIDP_EINVAL, "model dimensions must be positive");
+  if (m.head_dim != 64 && m.head_dim != 128) return fail(SIDP_EINVAL, "head_dim must be 64 or 128");
+  if (m.n_q_heads % m.n_kv_heads || m.n_q_heads / m.n_kv_heads > 16)
+    return fail(SIDP_EINVAL, "n_q_heads must be a multiple of n_kv_heads (group <= 16)");
+  if (m.hidden % 64 || m.intermediate % 64 || (m.n_q_heads * m.head_dim) % 64)
+    return fail(SIDP_EINVAL, "hidden, intermediate and n_q*head_dim must be multiples of 64");
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+    return fail(SIDP_EINVAL, "rank %d not in [0, world=%d)", cfg->rank, cfg->world);
+  if (cfg->was_slots < 1) return fail(SIDP_EINVAL, "was_slots must be >= 1");
+  if (cfg->cas_slots < 1) return fail(SIDP_EINVAL, "cas_slots must be >= 1");
+  if (cfg->order != SIDP_ORDER_EXEC && cfg->order != SIDP_ORDER_PAPER)
+    return fail(SIDP_EINVAL, "bad order");
+  if (cfg->pool_scope != SIDP_POOL_LAYER && cfg->pool_scope != SIDP_POOL_FFN)
+    return fail(SIDP_EINVAL, "bad pool_scope");
+  if (cfg->max_batch < 1 || cfg->max_ctx < 1) return fail(SIDP_EINVAL, "max_batch/max_ctx >= 1");
+  std::vector<int> owner(m.num_layers);
+  for (int l = 0; l < m.num_layers; ++l) {
+    owner[l] = cfg->layer_owner ? cfg->layer_owner[l] : l % cfg->world;
+    if (owner[l] < 0 || owner[l] >= cfg->world)   // exactly one owner per layer
+      return fail(SIDP_EINVAL, "layer %d owner %d not in [0, %d)", l, owner[l], cfg->world);
+  }
+  std::vector<int> pl = build_plan(owner, cfg->world, cfg->rank, cfg->order);
+  if (cfg->order == SIDP_ORDER_PAPER && cfg->was_slots < cfg->world - 1)
+    return fail(SIDP_EINVAL, "SIDP_ORDER_PAPER needs was_slots >= world-1 (deadlock, C-S4)");
+  if (!pl.empty() && plan_lag(pl) >= cfg->was_slots)
+    return fail(SIDP_EINVAL, "plan lag %d >= was_slots %d (deadlock)", plan_lag(pl),
+                cfg->was_slots);
+  sidp_ctx* c = new sidp_ctx();
+  c->m = m;
+  c->c = *cfg;
+  c->c.layer_owner = nullptr;
+  c->L = m.num_layers;
+  c->d = cfg->world;
+  c->r = cfg->rank;
+  c->S = cfg->was_slots;
+  c->owner = owner;
+  c->plan = pl;
+  c->R = (int)pl.size();
+  c->sorted_plan = pl;
+  std::sort(c->sorted_plan.begin(), c->sorted_plan.end());
+  c->plan_pos.assign(c->L, -1);
+  for (int i = 0; i < c->R; ++i) c->plan_pos[pl[i]] = i;
+  c->owned_index.assign(c->L, -1);
+  std::vector<int> cnt(c->d, 0);
+  for (int l = 0; l < c->L; ++l) {
+    c->owned_index[l] = cnt[owner[l]]++;
+    if (owner[l] == c->r) c->owned_layers.push_back(l);
+  }
+  build_layout(c);
+  c->last_rt.assign(c->d, std::vector<int64_t>(cfg->cas_slots, -1));
+  c->mode = SIDP_WAS;
+  c->st.mode = c->mode;
+  schedule_reset(c);
+  *out = c;
+  return SIDP_OK;
+}
+
+void sidp_destroy(sidp_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->allocated) {
+    cudaSetDevice(ctx->c.device);
+    cudaDeviceSynchronize();
+    for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+    for (auto e : ctx->ready_ev) cudaEventDestroy(e);
+    for (auto e : ctx->free_ev) cudaEventDestroy(e);
+    for (auto e : ctx->tev) cudaEventDestroy(e);
+    if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
+    void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
+                    ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
+                    ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->cas, ctx->dev_err,
+                    ctx->cas_out};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  delete ctx;
+}
+
+sidp_status sidp_alloc(sidp_ctx* ctx) {
+  if (!ctx) return fail(SIDP_EINVAL, "null ctx");
+  if (ctx->allocated) return fail(SIDP_ESTATE, "already allocated");
+  CK(cudaSetDevice(ctx->c.device));
+  const auto& m = ctx->m;
+  auto dmalloc = [&](void** p, size_t bytes) -> bool {
+    if (bytes == 0) bytes = 256;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(SIDP_ENOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+      return false;
+    }
+    return true;
+  };
+#define DM(ptr, bytes)                                             \
+  do {                                                             \
+    if (!dmalloc(reinterpret_cast<void**>(&(ptr)), (bytes))) {     \
+      return SIDP_ENOMEM;                                          \
+    }                                                              \
+  } while (0)
+  const size_t pooled_b = ctx->pooled_elems * 2, local_b = ctx->local_elems * 2;
+  DM(ctx->arena, std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b);
+  DM(ctx->local, (size_t)ctx->L * local_b);
+  if (ctx->R > 0) DM(ctx->slots, (size_t)ctx->S * pooled_b);
+  DM(ctx->embed, (size_t)m.vocab * m.hidden * 2);
+  DM(ctx->g_final, (size_t)m.hidden * 2);
+  DM(ctx->wlm, (size_t)m.vocab * m.hidden * 2);
+  // RoPE table built in fp64, stored fp32 (C-N3)
+  const int half = m.head_dim / 2;
+  std::vector<float2> tab((size_t)ctx->c.max_ctx * half);
+  for (int p = 0; p < ctx->c.max_ctx; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double f = std::pow((double)m.rope_theta, -2.0 * i / m.head_dim);
+      const double a = (double)p * f;
+      tab[(size_t)p * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  DM(ctx->rope, tab.size() * sizeof(float2));
+  CK(cudaMemcpy(ctx->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  // activations: CaS owner-side fused GEMMs need world*max_batch rows
+  ctx->rows_max = ctx->c.max_batch * (ctx->d > 1 ? ctx->d : 1);
+  const size_t R = ctx->rows_max;
+  DM(ctx->xbuf, R * m.hidden * 2);
+  DM(ctx->u, R * m.hidden * 2);
+  DM(ctx->q, R * ctx->qdim * 2);
+  DM(ctx->o, R * std::max(ctx->qdim, m.hidden) * 2);
+  DM(ctx->act, R * m.intermediate * 2);
+  DM(ctx->cas_out, R * m.hidden * 2);
+  DM(ctx->qkv, R * ctx->qkvdim * 4);
+  DM(ctx->amax, R * 8);
+  ctx->gemm_ws_bytes = (size_t)3 * 148 * 128 * 256 * 4;
+  DM(ctx->gemm_ws, ctx->gemm_ws_bytes);
+  ctx->n_counters = 1 << 16;
+  DM(ctx->counters, ctx->n_counters * sizeof(int));
+  CK(cudaMemset(ctx->counters, 0, ctx->n_counters * sizeof(int)));
+  const int max_splits = std::min(64, (ctx->c.max_ctx + 255) / 256);
+  ctx->attn_ws_bytes = std::min<size_t>((size_t)R * m.n_q_heads * max_splits * (m.head_dim + 2) * 4,
+                                        (size_t)256 << 20);
+  DM(ctx->attn_ws, ctx->attn_ws_bytes);
+  // CaS arena: flags | stage slots | recv
+  ctx->stage_width = ctx->c.pool_scope == SIDP_POOL_LAYER ? ctx->qdim + m.hidden : 2 * m.hidden;
+  ctx->cas_stage_bytes = align_up((size_t)R * ctx->stage_width * 2, 256);
+  ctx->recv_row_bytes = align_up(std::max<size_t>((size_t)ctx->qkvdim * 4, (size_t)m.hidden * 2), 16);
+  ctx->cas_stage_off = 4096;
+  ctx->cas_recv_off = ctx->cas_stage_off + ctx->c.cas_slots * ctx->cas_stage_bytes;
+  ctx->cas_bytes = ctx->cas_recv_off + (size_t)ctx->c.max_batch * ctx->recv_row_bytes;
+  DM(ctx->cas, ctx->cas_bytes);
+  CK(cudaMemset(ctx->cas, 0, 4096));
+  DM(ctx->dev_err, sizeof(int));
+  CK(cudaMemset(ctx->dev_err, 0, sizeof(int)));
+  CK(cudaStreamCreateWithFlags(&ctx->fetch_stream, cudaStreamNonBlocking));
+  ctx->ready_ev.resize(ctx->S);
+  ctx->free_ev.resize(ctx->S);
+  ctx->free_recorded.assign(ctx->S, 0);
+  for (int s = 0; s < ctx->S; ++s) {
+    CK(cudaEventCreateWithFlags(&ctx->ready_ev[s], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->free_ev[s], cudaEventDisableTiming));
+  }
+  ctx->peer_arena.assign(ctx->d, nullptr);
+  ctx->peer_arena[ctx->r] = ctx->arena;
+  ctx->peer_cas.assign(ctx->d, nullptr);
+  ctx->peer_cas[ctx->r] = ctx->cas;
+  ctx->allocated = true;
+  ctx->st.layer_bytes = pooled_b;
+  ctx->st.local_layer_bytes = local_b;
+  ctx->st.owned_bytes = ctx->owned_layers.size() * pooled_b;
+  ctx->st.slot_bytes = ctx->R > 0 ? (size_t)ctx->S * pooled_b : 0;
+  ctx->st.replicated_bytes = (size_t)ctx->L * local_b + (size_t)2 * m.vocab * m.hidden * 2 + m.hidden * 2;
+  ctx->st.workspace_bytes = R * (m.hidden * 4 + ctx->qdim * 4 + m.intermediate * 2 + ctx->qkvdim * 4) +
+                            ctx->gemm_ws_bytes + ctx->attn_ws_bytes + ctx->cas_bytes;
+#undef DM
+  return SIDP_OK;
+}
+
+sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream) {
+  sidp_status st = check_ready(ctx);
+  if (st != SIDP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const auto& m = ctx->m;
+  const uint64_t seed = ctx->c.seed;
+  // tensor ids: sidp_inputs/gen.py
+  enum { EMBED = 1, WQ, WK, WV, WO, WGATE, WUP, WDOWN, G_ATTN, G_MLP, G_Q, G_K, BQ, BK, BV,
+         G_FINAL, WLM };
+  auto gen = [&](bf16* dst, int64_t rows, int64_t cols, int tensor, int layer, int kind,
+                 int scale_k, int64_t row0, int row_map) -> bool {
+    sidp::GenArgs a{};
+    a.dst = dst; a.ld = cols; a.rows = rows; a.cols = cols; a.seed = seed; a.tensor = tensor;
+    a.layer = layer; a.kind = kind; a.scale_k = scale_k; a.row0 = row0; a.lcols = cols;
+    a.row_map = row_map; a.inter = m.intermediate;
+    count_launch(ctx);
+    return ck(ctx, sidp::gen_launch(a, s), "gen");
+  };
+  auto comp_ptr = [&](int l, int comp) -> bf16* {
+    if (ctx->comp_pooled[comp]) {
+      if (ctx->owner[l] != ctx->r) return nullptr;
+      return ctx->arena + (size_t)ctx->owned_index[l] * ctx->pooled_elems + ctx->comp_off[comp];
+    }
+    return ctx->local + (size_t)l * ctx->local_elems + ctx->comp_off[comp];
+  };
+  for (int l = 0; l < ctx->L; ++l) {
+    bf16* p;
+    if ((p = comp_ptr(l, C_WQKV))) {
+      if (!gen(p, ctx->qdim, m.hidden, WQ, l, sidp::GEN_WEIGHT, m.hidden, 0, 0)) return SIDP_ECUDA;
+      if (!gen(p + (size_t)ctx->qdim * m.hidden, ctx->kvdim, m.hidden, WK, l, sidp::GEN_WEIGHT,
+               m.hidden, 0, 0)) return SIDP_ECUDA;
+      if (!gen(p + (size_t)(ctx->qdim + ctx->kvdim) * m.hidden, ctx->kvdim, m.hidden, WV, l,
+               sidp::GEN_WEIGHT, m.hidden, 0, 0)) return SIDP_ECUDA;
+    }
+    if ((p = comp_ptr(l, C_WO)) && !gen(p, m.hidden, ctx->qdim, WO, l, sidp::GEN_WEIGHT, ctx->qdim, 0, 0))
+      return SIDP_ECUDA;
+    if ((p = comp_ptr(l, C_WGU)) &&
+        !gen(p, 2 * (int64_t)m.intermediate, m.hidden, WGATE, l, sidp::GEN_WEIGHT, m.hidden, 0, 1))
+      return SIDP_ECUDA;
+    if ((p = comp_ptr(l, C_WD)) &&
+        !gen(p, m.hidden, m.intermediate, WDOWN, l, sidp::GEN_WEIGHT, m.intermediate, 0, 0))
+      return SIDP_ECUDA;
+    if ((p = comp_ptr(l, C_GATTN)) && !gen(p, 1, m.hidden, G_ATTN, l, sidp::GEN_GAIN, 0, 0, 0))
+      return SIDP_ECUDA;
+    if ((p = comp_ptr(l, C_GMLP)) && !gen(p, 1, m.hidden, G_MLP, l, sidp::GEN_GAIN, 0, 0, 0))
+      return SIDP_ECUDA;
+    if (m.qk_norm) {
+      if ((p = comp_ptr(l, C_GQ)) && !gen(p, 1, m.head_dim, G_Q, l, sidp::GEN_GAIN, 0, 0, 0))
+        return SIDP_ECUDA;
+      if ((p = comp_ptr(l, C_GK)) && !gen(p, 1, m.head_dim, G_K, l, sidp::GEN_GAIN, 0, 0, 0))
+        return SIDP_ECUDA;
+    }
+    if (m.qkv_bias && (p = comp_ptr(l, C_BQKV))) {
+      if (!gen(p, 1, ctx->qdim, BQ, l, sidp::GEN_BIAS, 0, 0, 0)) return SIDP_ECUDA;
+      if (!gen(p + ctx->qdim, 1, ctx->kvdim, BK, l, sidp::GEN_BIAS, 0, 0, 0)) return SIDP_ECUDA;
+      if (!gen(p + ctx->qdim + ctx->kvdim, 1, ctx->kvdim, BV, l, sidp::GEN_BIAS, 0, 0, 0))
+        return SIDP_ECUDA;
+    }
+  }
+  if (!gen(ctx->embed, m.vocab, m.hidden, EMBED, 0, sidp::GEN_UNIT, 0, 0, 0)) return SIDP_ECUDA;
+  if (!gen(ctx->g_final, 1, m.hidden, G_FINAL, 0, sidp::GEN_GAIN, 0, 0, 0)) return SIDP_ECUDA;
+  if (!gen(ctx->wlm, m.vocab, m.hidden, WLM, 0, sidp::GEN_WEIGHT, m.hidden, 0, 0)) return SIDP_ECUDA;
+  return SIDP_OK;
+}
+
+sidp_status sidp_export_handles(sidp_ctx* ctx, void* blob, size_t* len) {
+  if (!ctx || !len) return fail(SIDP_EINVAL, "null argument");
+  if (!blob) {
+    *len = sizeof(HandleBlob);
+    return SIDP_OK;
+  }
+  if (*len < sizeof(HandleBlob)) return fail(SIDP_EINVAL, "blob too small");
+  sidp_status st = check_ready(ctx);
+  if (st != SIDP_OK) return st;
+  HandleBlob h{};
+  h.magic = kMagic;
+  h.rank = ctx->r;
+  h.pid = (int32_t)getpid();
+  h.device = ctx->c.device;
+  h.arena_ptr = reinterpret_cast<uint64_t>(ctx->arena);
+  h.cas_ptr = reinterpret_cast<uint64_t>(ctx->cas);
+  h.arena_bytes = std::max<size_t>(1, ctx->owned_layers.size()) * ctx->pooled_elems * 2;
+  h.cas_bytes = ctx->cas_bytes;
+  h.has_arena = cudaIpcGetMemHandle(&h.arena_h, ctx->arena) == cudaSuccess;
+  h.has_cas = cudaIpcGetMemHandle(&h.cas_h, ctx->cas) == cudaSuccess;
+  cudaGetLastError();
+  std::memcpy(blob, &h, sizeof(h));
+  *len = sizeof(h);
+  return SIDP_OK;
+}
+
+sidp_status sidp_import_handles(sidp_ctx* ctx, const void* const* blobs, const size_t* lens) {
+  if (!ctx || !blobs || !lens) return fail(SIDP_EINVAL, "null argument");
+  sidp_status st = check_ready(ctx);
+  if (st != SIDP_OK) return st;
+  CK(cudaSetDevice(ctx->c.device));
+  for (int q = 0; q < ctx->d; ++q) {
+    if (q == ctx->r) continue;
+    if (lens[q] < sizeof(HandleBlob)) return fail(SIDP_EINVAL, "blob %d too small", q);
+    HandleBlob h;
+    std::memcpy(&h, blobs[q], sizeof(h));
+    if (h.magic != kMagic || h.rank != q) return fail(SIDP_EINVAL, "blob %d malformed", q);
+    if (h.pid == (int32_t)getpid()) {   // virtual ranks: same process, plain device pointers
+      ctx->peer_arena[q] = reinterpret_cast<const bf16*>(h.arena_ptr);
+      ctx->peer_cas[q] = reinterpret_cast<uint8_t*>(h.cas_ptr);
+      if (h.device != ctx->c.device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(SIDP_EPEER, "peer access to device %d: %s", h.device, cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+      continue;
+    }
+    if (!h.has_arena || !h.has_cas) return fail(SIDP_EPEER, "rank %d exported no IPC handle", q);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h.arena_h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(SIDP_EPEER, "IPC open arena of rank %d: %s", q, cudaGetErrorString(e));
+    ctx->ipc_opened.push_back(p);
+    ctx->peer_arena[q] = reinterpret_cast<const bf16*>(p);
+    e = cudaIpcOpenMemHandle(&p, h.cas_h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(SIDP_EPEER, "IPC open CaS arena of rank %d: %s", q, cudaGetErrorString(e));
+    ctx->ipc_opened.push_back(p);
+    ctx->peer_cas[q] = reinterpret_cast<uint8_t*>(p);
+  }
+  return SIDP_OK;
+}
+
+sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t layer, int32_t mode,
+                              const sidp_kv* kv, void* stream) {
+  if (!ctx) return fail(SIDP_EINVAL, "null ctx");
+  sidp_status st = check_ready(ctx);
+  if (st != SIDP_OK) return st;
+  if (layer < 0 || layer >= ctx->L) return fail(SIDP_EINVAL, "layer %d out of range", layer);
+  if (batch < 0 || batch > ctx->c.max_batch) return fail(SIDP_EINVAL, "batch %d out of range", batch);
+  if (batch > 0 && !x) return fail(SIDP_EINVAL, "null x");
+  st = validate_kv(ctx, kv, batch);
+  if (st != SIDP_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  bf16* xb = reinterpret_cast<bf16*>(x);
+  if (mode == SIDP_REPLICATED) {
+    if (ctx->d != 1) return fail(SIDP_EINVAL, "SIDP_REPLICATED needs world == 1");
+    mode = SIDP_WAS;
+  }
+  if (mode == SIDP_WAS) {
+    if (batch == 0) {   // a dummy WaS step still walks the ring so the schedule stays aligned
+      if (layer != ctx->next_layer) return fail(SIDP_ESTATE, "WaS layers must run in order");
+      if (ctx->owner[layer] != ctx->r) {
+        const int64_t p = fetch_index_of_compute(ctx, ctx->compute_k);
+        st = pump(ctx);
+        if (st != SIDP_OK) return st;
+        const int slot = ctx->slot_of_fetch[p];
+        CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
+        CK(cudaEventRecord(ctx->free_ev[slot], s));
+        ctx->free_recorded[slot] = 1;
+        ctx->push.push_back(slot);
+        ctx->compute_k++;
+        st = pump(ctx);
+        if (st != SIDP_OK) return st;
+      }
+      ctx->next_layer = (layer + 1) % ctx->L;
+      return SIDP_OK;
+    }
+    return was_layer(ctx, xb, batch, layer, kv, s);
+  }
+  if (mode == SIDP_CAS) return cas_layer(ctx, xb, batch, layer, kv, s);
+  return fail(SIDP_EINVAL, "bad mode %d", mode);
+}
+
+sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
+  if (!ctx || !b) return fail(SIDP_EINVAL, "null argument");
+  sidp_status st = check_ready(ctx);
+  if (st != SIDP_OK) return st;
+  const int B = b->batch;
+  if (B < 0 || B > ctx->c.max_batch) return fail(SIDP_EINVAL, "batch %d out of range", B);
+  if (B > 0 && (!b->tokens || !b->next)) return fail(SIDP_EINVAL, "null tokens/next");
+  st = validate_kv(ctx, &b->kv, B);
+  if (st != SIDP_OK) return st;
+  // mode directive at the step boundary
+  if (ctx->pending_mode >= 0 && ctx->step >= ctx->pending_step) {
+    if (ctx->pending_mode != ctx->mode) {
+      ctx->mode = ctx->pending_mode;
+      // drain: wait for in-flight fetches, then restart the plan (reading C-A7)
+      CK(cudaStreamSynchronize(ctx->fetch_stream));
+      std::fill(ctx->free_recorded.begin(), ctx->free_recorded.end(), 0);
+      schedule_reset(ctx);
+    }
+    ctx->pending_mode = -1;
+    ctx->st.mode = ctx->mode;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const auto& m = ctx->m;
+  bf16* x = ctx->xbuf;
+  if (B > 0) {
+    CK(sidp::embed_launch(ctx->embed, m.hidden, b->tokens, x, B, s));
+    count_launch(ctx);
+  }
+  const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
+  for (int l = 0; l < ctx->L; ++l) {
+    if (b->layer_inputs && B > 0) {
+      CK(cudaMemcpyAsync(reinterpret_cast<bf16*>(b->layer_inputs) + (size_t)l * B * m.hidden, x,
+                         (size_t)B * m.hidden * 2, cudaMemcpyDeviceToDevice, s));
+    }
+    st = sidp_decode_layer(ctx, x, B, l, mode, &b->kv, stream);
+    if (st != SIDP_OK) return st;
+  }
+  if (B > 0) {
+    CK(sidp::rmsnorm_launch(x, m.hidden, ctx->g_final, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+    count_launch(ctx);
+    CK(sidp::argmax_reset_launch(ctx->amax, B, s));
+    count_launch(ctx);
+    CK(gemm(ctx, 7, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_ARGMAX, ctx->amax,
+            0, nullptr, 0, nullptr, s));
+    CK(sidp::argmax_finalize_launch(ctx->amax, b->next, B, s));
+    count_launch(ctx);
+    if (b->logits) {
+      CK(gemm(ctx, 0, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_F32, b->logits,
+              m.vocab, nullptr, 0, nullptr, s));
+    }
+  }
+  ctx->step++;
+  ctx->st.steps++;
+  return SIDP_OK;
+}
+
+sidp_status sidp_set_mode(sidp_ctx* ctx, int32_t mode, int64_t effective_step) {
+  if (!ctx) return fail(SIDP_EINVAL, "null ctx");
+  if (mode != SIDP_WAS && mode != SIDP_CAS && mode != SIDP_REPLICATED)
+    return fail(SIDP_EINVAL, "bad mode");
+  if (mode == SIDP_REPLICATED && ctx->d != 1) return fail(SIDP_EINVAL, "REPLICATED needs world 1");
+  if (effective_step < ctx->step) return fail(SIDP_EINVAL, "effective_step in the past");
+  ctx->pending_mode = mode;
+  ctx->pending_step = effective_step;
+  return SIDP_OK;
+}
+
+sidp_status sidp_set_batches(sidp_ctx* ctx, const int32_t* batches) {
+  if (!ctx || !batches) return fail(SIDP_EINVAL, "null argument");
+  std::vector<int> b(ctx->d);
+  for (int q = 0; q < ctx->d; ++q) {
+    if (batches[q] < 0 || batches[q] > ctx->c.max_batch) return fail(SIDP_EINVAL, "batch out of range");
+    b[q] = batches[q];
+  }
+  ctx->batches = b;
+  return SIDP_OK;
+}
+
+sidp_status sidp_owner_of(const sidp_ctx* ctx, int32_t layer, int32_t* owner) {
+  if (!ctx || !owner) return fail(SIDP_EINVAL, "null argument");
+  if (layer < 0 || layer >= ctx->L) return fail(SIDP_EINVAL, "layer out of range");
+  *owner = ctx->owner[layer];
+  return SIDP_OK;
+}
+
+sidp_status sidp_get_plan(const sidp_ctx* ctx, int32_t* layers, int32_t capacity, int32_t* n) {
+  if (!ctx || !n) return fail(SIDP_EINVAL, "null argument");
+  *n = ctx->R;
+  if (layers) {
+    if (capacity < ctx->R) return fail(SIDP_EINVAL, "capacity too small");
+    for (int i = 0; i < ctx->R; ++i) layers[i] = ctx->plan[i];
+  }
+  return SIDP_OK;
+}
+
+sidp_status sidp_get_schedule(const sidp_ctx* ctx, int32_t steps, int32_t* fetch_step,
+                              int32_t* fetch_layer, int32_t* fetch_slot, int32_t capacity,
+                              int32_t* n) {
+  if (!ctx || !n || steps < 0) return fail(SIDP_EINVAL, "bad argument");
+  const int64_t total = (int64_t)steps * ctx->R;
+  *n = (int32_t)total;
+  if (!fetch_step || !fetch_layer || !fetch_slot) return SIDP_OK;
+  if (capacity < total) return fail(SIDP_EINVAL, "capacity too small");
+  // independent replay of the FIFO recurrence (same rule the runtime follows)
+  std::vector<int> push;
+  for (int s = 0; s < ctx->S; ++s) push.push_back(s);
+  std::vector<int> sof;
+  for (int64_t j = 0; j < total; ++j) {
+    while ((int64_t)push.size() <= j) {
+      const int64_t k = (int64_t)push.size() - ctx->S;
+      const int64_t p = fetch_index_of_compute(ctx, k);
+      if (p >= j) return fail(SIDP_ESTATE, "schedule deadlocks");
+      push.push_back(sof[p]);
+    }
+    sof.push_back(push[j]);
+    fetch_step[j] = (int32_t)(j / ctx->R);
+    fetch_layer[j] = ctx->plan[j % ctx->R];
+    fetch_slot[j] = push[j];
+  }
+  return SIDP_OK;
+}
+
+sidp_status sidp_stagger_ticks(const sidp_ctx* ctx, int32_t* ticks) {
+  if (!ctx || !ticks) return fail(SIDP_EINVAL, "null argument");
+  *ticks = stagger_ticks_of(ctx);
+  return SIDP_OK;
+}
+
+sidp_status sidp_get_fetch_log(const sidp_ctx* ctx, int32_t* fetch_step, int32_t* fetch_layer,
+                               int32_t* fetch_slot, int32_t capacity, int32_t* n) {
+  if (!ctx || !n) return fail(SIDP_EINVAL, "null argument");
+  *n = (int32_t)ctx->log_t.size();
+  if (!fetch_step) return SIDP_OK;
+  if (capacity < *n) return fail(SIDP_EINVAL, "capacity too small");
+  for (int32_t i = 0; i < *n; ++i) {
+    fetch_step[i] = ctx->log_t[i];
+    fetch_layer[i] = ctx->log_l[i];
+    fetch_slot[i] = ctx->log_s[i];
+  }
+  return SIDP_OK;
+}
+
+sidp_status sidp_stats(const sidp_ctx* ctx_c, sidp_stats_t* out) {
+  if (!ctx_c || !out) return fail(SIDP_EINVAL, "null argument");
+  sidp_ctx* ctx = const_cast<sidp_ctx*>(ctx_c);
+  if (ctx->allocated) {
+    int err = 0;
+    if (cudaMemcpy(&err, ctx->dev_err, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && err)
+      ctx->st.timeouts = err;
+    if (ctx->tev_used > 0) {
+      for (int i = 0; i + 1 < ctx->tev_used; i += 2) {
+        float ms = 0.0f;
+        cudaEventSynchronize(ctx->tev[i + 1]);
+        if (cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]) == cudaSuccess)
+          ctx->timed_acc_ms += ms;
+      }
+      ctx->tev_used = 0;
+    }
+  }
+  ctx->st.timed_ms = ctx->timed_acc_ms;
+  *out = ctx->st;
+  return SIDP_OK;
+}
+
+sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t kernel_class) {
+  if (!ctx) return fail(SIDP_EINVAL, "null ctx");
+  sidp_status st = check_ready(ctx);
+  if (st != SIDP_OK) return st;
+  if (ctx->tev.empty()) {
+    ctx->tev.resize(kTimingPool);
+    for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
+  }
+  ctx->timed_class = kernel_class;
+  ctx->tev_used = 0;
+  ctx->timed_acc_ms = 0.0;
+  ctx->st.timed_launches = 0;
+  return SIDP_OK;
+}
+
+sidp_status sidp_layer_ptr(const sidp_ctx* ctx, int32_t layer, void** pooled, void** local) {
+  if (!ctx || layer < 0 || layer >= ctx->L) return fail(SIDP_EINVAL, "bad argument");
+  if (!ctx->allocated) return fail(SIDP_ESTATE, "not allocated");
+  if (pooled)
+    *pooled = ctx->owner[layer] == ctx->r
+                  ? (void*)(ctx->arena + (size_t)ctx->owned_index[layer] * ctx->pooled_elems)
+                  : nullptr;
+  if (local) *local = (void*)(ctx->local + (size_t)layer * ctx->local_elems);
+  return SIDP_OK;
+}
+
+// ---- test hooks ----
+sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ldw, int32_t M,
+                           int32_t N, int32_t K, int32_t epi, void* out, int32_t ldo,
+                           const void* resid, int32_t ldr, const void* bias, int32_t k_splits,
+                           void* stream) {
+  static float* ws = nullptr;
+  static int* counters = nullptr;
+  static const size_t ws_bytes = (size_t)256 << 20;
+  if (!ws) {
+    if (cudaMalloc(&ws, ws_bytes) != cudaSuccess || cudaMalloc(&counters, (1 << 16) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(counters, 0, (1 << 16) * sizeof(int)) != cudaSuccess)
+      return fail(SIDP_ENOMEM, "test gemm workspace");
+  }
+  sidp::GemmArgs a{};
+  a.x = reinterpret_cast<const bf16*>(x); a.ldx = ldx; a.w = reinterpret_cast<const bf16*>(w);
+  a.ldw = ldw; a.M = M; a.N = N; a.K = K; a.epi = epi; a.out = out; a.ldo = ldo;
+  a.resid = reinterpret_cast<const bf16*>(resid); a.ldr = ldr;
+  a.bias = reinterpret_cast<const bf16*>(bias); a.k_splits = k_splits;
+  cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, counters, 1 << 16},
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
+sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
+                          int32_t tensor, int32_t layer, int32_t kind, int32_t scale_k,
+                          int64_t row0, int64_t lcols, int32_t row_map, void* stream) {
+  sidp::GenArgs a{};
+  a.dst = reinterpret_cast<bf16*>(dst); a.ld = ld; a.rows = rows; a.cols = cols; a.seed = seed;
+  a.tensor = tensor; a.layer = layer; a.kind = kind; a.scale_k = scale_k; a.row0 = row0;
+  a.lcols = lcols; a.row_map = row_map;
+  cudaError_t e = sidp::gen_launch(a, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "gen: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
+sidp_status sidp_test_gen_kv(void* cache, int32_t B, int32_t nkv, int32_t smax, int32_t hd,
+                             int32_t T, int64_t b0, uint64_t seed, int32_t tensor, int32_t layer,
+                             void* stream) {
+  cudaError_t e = sidp::gen_kv_launch(reinterpret_cast<bf16*>(cache), B, nkv, smax, hd, T, b0, seed,
+                                      tensor, layer, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "gen_kv: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
+}  // extern "C"

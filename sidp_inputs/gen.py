@@ -86,8 +86,13 @@ def weight_scale(K: int) -> float:
 def weight(seed: int, tensor: int, layer: int, n_rows: int, K: int, rows=None) -> np.ndarray:
     """Logical weight W[N, K] (row-major logical index n*K + k); optionally a row subset."""
     rows = np.arange(n_rows, dtype=np.uint64) if rows is None else np.asarray(rows, dtype=np.uint64)
-    idx = rows[:, None] * np.uint64(K) + np.arange(K, dtype=np.uint64)[None, :]
-    return _levels(hash_u64(seed, tensor, layer, idx)) * weight_scale(K)
+    out = np.empty((rows.shape[0], K), dtype=np.float64)
+    step = max(1, (1 << 22) // K)          # bounded temporaries for big layers
+    cols = np.arange(K, dtype=np.uint64)[None, :]
+    for i in range(0, rows.shape[0], step):
+        idx = rows[i:i + step, None] * np.uint64(K) + cols
+        out[i:i + step] = _levels(hash_u64(seed, tensor, layer, idx))
+    return out * weight_scale(K)
 
 
 def gain(seed: int, tensor: int, layer: int, n: int) -> np.ndarray:

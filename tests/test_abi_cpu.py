@@ -1,0 +1,107 @@
+"""CPU-only checks of the C-ABI library: it loads without a GPU, exports every symbol
+include/sidp.h declares, and its host-side schedule equals the oracle's bit for bit."""
+import itertools
+import os
+import re
+
+import pytest
+
+from oracle import schedule as S
+from sidp_inputs import MODELS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def sidp():
+    from paper_2605_28095_b200 import build as B
+    B.build()
+    import paper_2605_28095_b200 as P
+    return P
+
+
+def test_exports_every_declared_symbol(sidp):
+    import ctypes
+    hdr = open(os.path.join(ROOT, "include", "sidp.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = sorted(set(re.findall(r"\b(sidp_[a-z_0-9]+)\s*\(", hdr)))
+    assert "sidp_init" in names and "sidp_step" in names and "sidp_decode_layer" in names
+    L = ctypes.CDLL(sidp._abi.LIB_PATH)
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    # and the binding declares a signature for each of them
+    assert set(names) <= set(sidp._abi.SIGNATURES), set(names) - set(sidp._abi.SIGNATURES)
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(ROOT, "paper_2605_28095_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+(oracle|sidp_inputs)", txt, re.M), f
+                assert not re.search(r"#include\s+[<\"].*oracle", txt), f
+
+
+def _ctx(sidp, name="tiny", **kw):
+    return sidp.Context(MODELS[name], alloc=False, **kw)
+
+
+@pytest.mark.parametrize("order", ["exec", "paper"])
+def test_schedule_bit_exact_vs_oracle(sidp, order):
+    for d in (2, 3, 4, 8):
+        for L in (d, 2 * d, 4 * d + 1 if order == "exec" else 3 * d):
+            m = MODELS["tiny"].with_layers(L)
+            own = S.owner_map(L, d)
+            for r in range(d):
+                pl = S.plan(own, d, r, order)
+                for slots in sorted({1, 2, 3, d - 1, d}):
+                    if slots < 1:
+                        continue
+                    ok = S.deadlock_free(pl, slots) if pl else True
+                    if order == "paper" and slots < d - 1:
+                        ok = False
+                    if not ok:
+                        with pytest.raises(sidp.SidpError):
+                            sidp.Context(m, rank=r, world=d, slots=slots, order=order, alloc=False)
+                        continue
+                    c = sidp.Context(m, rank=r, world=d, slots=slots, order=order, alloc=False)
+                    assert c.plan() == pl
+                    assert [c.owner_of(l) for l in range(L)] == own
+                    if pl:
+                        assert c.schedule(3) == S.slot_schedule(pl, slots, 3)
+                    c.destroy()
+
+
+def test_stagger_ticks_match_oracle(sidp):
+    for d in range(1, 9):
+        m = MODELS["tiny"].with_layers(2 * d)
+        for r in range(d):
+            c = sidp.Context(m, rank=r, world=d, slots=2, alloc=False)
+            assert c.stagger_ticks() == S.stagger_ticks(d, r)
+            c.destroy()
+
+
+def test_custom_owner_map_and_rejections(sidp):
+    m = MODELS["tiny"]
+    c = sidp.Context(m, rank=0, world=2, layer_owner=[1, 1, 0, 0], alloc=False)
+    assert [c.owner_of(l) for l in range(4)] == [1, 1, 0, 0]
+    assert c.plan() == [0, 1]
+    c.destroy()
+    bad = [dict(layer_owner=[0, 1, 2, 0]), dict(slots=0), dict(rank=2), dict(max_batch=0)]
+    for kw in bad:
+        kw = {"rank": 0, "world": 2, **kw}
+        with pytest.raises(sidp.SidpError) as e:
+            sidp.Context(m, alloc=False, **kw)
+        assert e.value.status == -1     # SIDP_EINVAL
+    with pytest.raises(sidp.SidpError):  # PAPER order with S < d-1 deadlocks (C-S4)
+        sidp.Context(m.with_layers(8), rank=1, world=4, slots=2, order="paper", alloc=False)
+
+
+def test_host_calls_need_alloc(sidp):
+    c = _ctx(sidp)
+    import ctypes
+    kv = sidp._abi.KV(None, None, None, 0)
+    st = sidp._abi.lib().sidp_decode_layer(c.h, None, 1, 0, 0, ctypes.byref(kv), None)
+    assert st == sidp._abi.SIDP_ESTATE
+    c.destroy()

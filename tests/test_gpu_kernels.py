@@ -1,0 +1,144 @@
+"""Single-kernel parity on the GPU (through the C-ABI test hooks, same kernels as the hot path).
+
+* K12 generator: bit-exact vs sidp_inputs.gen (the shared seeded generator).
+* tcgen05 GEMM: vs the fp64 product of the same bf16 operands, over tile-spanning shapes with
+  ragged tails, forced split-K counts and every fused epilogue.
+"""
+import numpy as np
+import pytest
+import torch
+
+from sidp_inputs import gen
+
+pytestmark = pytest.mark.gpu
+SEED = 20261017
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2605_28095_b200 import build as B
+    B.build()
+    import paper_2605_28095_b200 as P
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return P
+
+
+def _lvl(shape, gen_, scale=1.0):
+    return (torch.randint(-128, 128, shape, generator=gen_).to(torch.float32) / 128 * scale).to(torch.bfloat16)
+
+
+# ------------------------------------------------------------------ K12
+def test_gen_weights_bit_exact(P):
+    dst = torch.empty(96, 5120, dtype=torch.bfloat16, device="cuda")
+    P.test_gen(dst, SEED, gen.WQ, 3, 0, scale_k=5120, row0=40)
+    ref = gen.weight(SEED, gen.WQ, 3, 136, 5120)[40:]
+    assert torch.equal(dst.cpu().double(), torch.from_numpy(ref))
+
+
+def test_gen_gate_up_interleave_bit_exact(P):
+    I, K = 192, 256
+    dst = torch.empty(2 * I, K, dtype=torch.bfloat16, device="cuda")
+    P.test_gen(dst, SEED, gen.WGATE, 1, 0, scale_k=K, row_map=1)
+    g = gen.weight(SEED, gen.WGATE, 1, I, K)
+    u = gen.weight(SEED, gen.WUP, 1, I, K)
+    ref = np.concatenate([np.concatenate([g[64 * t:64 * t + 64], u[64 * t:64 * t + 64]])
+                          for t in range(I // 64)])
+    assert torch.equal(dst.cpu().double(), torch.from_numpy(ref))
+
+
+def test_gen_gain_bias_unit_kv_bit_exact(P):
+    for kind, tid, fn in ((1, gen.G_ATTN, lambda: gen.gain(SEED, gen.G_ATTN, 2, 512)),
+                          (2, gen.BQ, lambda: gen.bias(SEED, gen.BQ, 2, 512))):
+        dst = torch.empty(1, 512, dtype=torch.bfloat16, device="cuda")
+        P.test_gen(dst, SEED, tid, 2, kind)
+        assert torch.equal(dst.cpu().double()[0], torch.from_numpy(fn()))
+    E = torch.empty(64, 256, dtype=torch.bfloat16, device="cuda")
+    P.test_gen(E, SEED, gen.EMBED, 0, 3)
+    assert torch.equal(E.cpu().double(), torch.from_numpy(gen.embed_rows(SEED, np.arange(64), 256)))
+    import ctypes
+    B, nkv, smax, hd, T = 3, 2, 40, 64, 33
+    cache = torch.zeros(B, nkv, smax, hd, dtype=torch.bfloat16, device="cuda")
+    P._abi.check(P._abi.lib().sidp_test_gen_kv(ctypes.c_void_p(cache.data_ptr()), B, nkv, smax, hd, T,
+                                               5, SEED, gen.KCACHE, 1,
+                                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "kv")
+    ref = gen.kv(SEED, gen.KCACHE, 1, np.arange(5, 5 + B), range(T), nkv, hd)     # [B, T, g, d]
+    got = cache.cpu().double().permute(0, 2, 1, 3)[:, :T]
+    assert torch.equal(got, torch.from_numpy(ref))
+
+
+# ------------------------------------------------------------------ tcgen05 GEMM
+SHAPES = [(1, 128, 64), (8, 256, 256), (16, 384, 512), (37, 1000, 320), (100, 640, 1024),
+          (256, 512, 5120), (300, 256, 512), (513, 128, 128), (64, 10240, 5120)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("splits", [1, 3, 0])
+def test_gemm_f32(P, M, N, K, splits):
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    x = _lvl((M, K), g).cuda()
+    w = _lvl((N, K), g, 2.0 ** -5).cuda()
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    P.test_gemm(x, w, out, M, N, K, 0, k_splits=splits)
+    torch.cuda.synchronize()
+    ref = x.cpu().double() @ w.cpu().double().T
+    err = (out.cpu().double() - ref).abs().max().item()
+    assert err <= 1e-5 * ref.abs().max().item() + 1e-6, err
+
+
+@pytest.mark.parametrize("M,N,K", [(8, 256, 256), (37, 1000, 320), (256, 512, 2048)])
+def test_gemm_bf16_bias_and_residual(P, M, N, K):
+    g = torch.Generator().manual_seed(1)
+    x = _lvl((M, K), g).cuda()
+    w = _lvl((N, K), g, 2.0 ** -5).cuda()
+    bias = _lvl((N,), g, 0.125).cuda()
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    P.test_gemm(x, w, out, M, N, K, 1, bias=bias, k_splits=2)
+    ref = x.cpu().double() @ w.cpu().double().T + bias.cpu().double()
+    torch.cuda.synchronize()
+    d = (out.cpu().double() - ref).abs()
+    assert (d <= ref.abs() * 2.0 ** -8 + 1e-6 * ref.abs().max()).all()
+    # residual, in place (out aliases resid)
+    r = _lvl((M, N), g).cuda()
+    ref2 = x.cpu().double() @ w.cpu().double().T + r.cpu().double()
+    P.test_gemm(x, w, r, M, N, K, 2, resid=r)
+    torch.cuda.synchronize()
+    d2 = (r.cpu().double() - ref2).abs()
+    assert (d2 <= ref2.abs() * 2.0 ** -8 + 1e-6 * ref2.abs().max()).all()
+
+
+@pytest.mark.parametrize("M,F,K,splits", [(8, 64, 256, 1), (33, 192, 512, 0), (256, 640, 1024, 4)])
+def test_gemm_silu_mul(P, M, F, K, splits):
+    g = torch.Generator().manual_seed(2)
+    x = _lvl((M, K), g).cuda()
+    wg = _lvl((F, K), g, 2.0 ** -4)
+    wu = _lvl((F, K), g, 2.0 ** -4)
+    packed = torch.cat([torch.cat([wg[64 * t:64 * t + 64], wu[64 * t:64 * t + 64]]) for t in range(F // 64)]).cuda()
+    out = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    P.test_gemm(x, packed, out, M, 2 * F, K, 3, k_splits=splits)
+    torch.cuda.synchronize()
+    xd = x.cpu().double()
+    a, b = xd @ wg.double().T, xd @ wu.double().T
+    ref = a / (1 + torch.exp(-a)) * b
+    d = (out.cpu().double() - ref).abs()
+    assert (d <= ref.abs() * 2.0 ** -7 + 1e-4 * ref.abs().max()).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1024, 256), (8, 151936 // 8, 512), (200, 2000, 256)])
+def test_gemm_fused_argmax(P, M, N, K):
+    g = torch.Generator().manual_seed(3)
+    x = _lvl((M, K), g).cuda()
+    w = _lvl((N, K), g, 2.0 ** -4).cuda()
+    packed = torch.zeros(M, dtype=torch.int64, device="cuda")
+    P.test_gemm(x, w, packed, M, N, K, 4, ldo=0)
+    logits = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    P.test_gemm(x, w, logits, M, N, K, 0)
+    torch.cuda.synchronize()
+    idx = (0xFFFFFFFF - (packed.cpu() & 0xFFFFFFFF)).numpy()
+    ref = (x.cpu().double() @ w.cpu().double().T).numpy()
+    lg = logits.cpu().numpy()
+    # the decision is taken in the kernel's fp32: must equal argmax (lowest index) of fp32 logits
+    assert (idx == np.argmax(lg, axis=1)).all()
+    top2 = np.sort(ref, axis=1)[:, -2:]
+    sure = (top2[:, 1] - top2[:, 0]) > 1e-4
+    assert (idx[sure] == np.argmax(ref, axis=1)[sure]).all()
