@@ -32,13 +32,14 @@ def P():
 
 class Rank:
     def __init__(self, P, m, *, rank=0, world=1, B=8, ctx=0, span=63, max_ctx=80, b0=0,
-                 seed=SEED, **kw):
+                 seed=SEED, max_batch=None, **kw):
         self.m, self.B, self.b0 = m, B, b0
-        self.ctx = P.Context(m, rank=rank, world=world, max_batch=max(B, 1), max_ctx=max_ctx,
+        mb = max(B, 1) if max_batch is None else max_batch
+        self.ctx = P.Context(m, rank=rank, world=world, max_batch=mb, max_ctx=max_ctx,
                              seed=seed, **kw)
         self.ctx.init_weights_synthetic()
-        self.kv = P.KVCache(m, max(B, 1), max_ctx)
-        self.kv.fill_synthetic(seed, b0, max(B, 1), max_ctx)
+        self.kv = P.KVCache(m, mb, max_ctx)          # layout uses the context's max_batch
+        self.kv.fill_synthetic(seed, b0, mb, max_ctx)
         bg = np.arange(b0, b0 + B)
         self.pos = gen.positions(seed, bg, ctx, span)
         self.kv.set_pos(self.pos if B else [0])
@@ -109,7 +110,8 @@ def test_tiny_multi_step_end_to_end(P):
 
 
 def _group(P, m, d, B, **kw):
-    ranks = [Rank(P, m, rank=r, world=d, B=B[r], b0=sum(B[:r]), **kw) for r in range(d)]
+    ranks = [Rank(P, m, rank=r, world=d, B=B[r], b0=sum(B[:r]), max_batch=max(B), **kw)
+             for r in range(d)]
     blobs = [R.ctx.export_handles() for R in ranks]
     for R in ranks:
         R.ctx.import_handles(blobs)
