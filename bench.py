@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Decode-throughput benchmark of the B200-native SiDP WaS hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload M2]
+
+N=1 runs configs[1] (Qwen3-32B shape, B=256/GPU, S_ctx=1024; 64 layers, bf16) on one GPU
+(d=1: every layer owned; the WaS ring is idle).  N>1 (torchrun, one process per GPU, NCCL
+for the control plane only) runs SiDP WaS over d=N ranks: each rank owns L/d layers and
+streams the rest over NVLink into S=2 cache slots (EXEC order + C-S7 stagger).
+
+One step = one full decode step of the whole hot path (embedding, L layers, LM head with
+fused argmax) over B rows per GPU; tokens and positions are advanced on the device by the
+library, so the timed loop launches only library kernels.  Prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s at 1/2/4/8 B200 (WaS); fraction of per-layer roofline"
+UNIT = "tokens/s"
+CLS_NAMES = {1: "gate_up_gemm", 2: "attention", 3: "fetch", 4: "down_gemm", 5: "qkv_gemm",
+             6: "o_gemm", 7: "lm_head_gemm"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="M2")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--ctx", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None, help="override (marks config reduced)")
+    ap.add_argument("--slots", type=int, default=None)
+    ap.add_argument("--order", default="exec", choices=["exec", "paper"])
+    ap.add_argument("--pool", default="layer", choices=["layer", "ffn"])
+    ap.add_argument("--fetch", default="sm", choices=["sm", "ce"])
+    ap.add_argument("--fetch-sms", type=int, default=16)
+    ap.add_argument("--no-stagger", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=8)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.idx)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- cpu oracle
+def oracle_sample(m, seed, rows, ctx_len, timed_iters=1):
+    """Time the fp64 oracle on a bounded sample: one decoder layer for `rows` rows at the
+    workload's shapes and context, plus the LM head on a 1/16 vocab slice (scaled).  Returns
+    (tokens/s extrapolated to the full L-layer step, description, cores)."""
+    import numpy as np
+    from oracle import model as OM
+    from sidp_inputs import gen
+    bg = np.arange(rows)
+    p = gen.layer_params(seed, m, 0)
+    T = ctx_len + 1
+    K = gen.kv(seed, gen.KCACHE, 0, bg, range(T), m.n_kv_heads, m.head_dim)
+    V = gen.kv(seed, gen.VCACHE, 0, bg, range(T), m.n_kv_heads, m.head_dim)
+    x = gen.activations(seed, 0, bg, m.hidden)
+    pos = np.full(rows, ctx_len)
+    vs = max(1, m.vocab // 16)
+    head = {"g_final": gen.gain(seed, gen.G_FINAL, 0, m.hidden),
+            "wlm": gen.weight(seed, gen.WLM, 0, vs, m.hidden)}
+    t_layer = []
+    for _ in range(timed_iters):
+        Kc, Vc = K.copy(), V.copy()
+        t0 = time.perf_counter()
+        OM.decoder_layer(m, p, x, pos, Kc, Vc)
+        t_layer.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    OM.lm_head(m, head, x)
+    t_head = (time.perf_counter() - t0) * (m.vocab / vs)
+    tl = min(t_layer)
+    t_step = m.num_layers * tl + t_head
+    cores = len(os.sched_getaffinity(0))
+    desc = (f"oracle fp64 (numpy BLAS) on {rows} rows: 1 decoder layer timed ({tl*1e3:.1f} ms) x "
+            f"{m.num_layers} layers + LM head on 1/16 of the vocab x16 ({t_head*1e3:.1f} ms); "
+            f"ctx {ctx_len}; extrapolated to one full decode step")
+    return rows / t_step, desc, cores, t_step
+
+
+# ----------------------------------------------------------------------------- roofline
+def kernel_work(cls, m, B, ctx_avg, layer_bytes):
+    """Algorithmic (flops, bytes) per launch of a kernel class."""
+    h, I, V = m.hidden, m.intermediate, m.vocab
+    q, kvd = m.q_dim, m.kv_dim
+    if cls == 1:
+        return 2.0 * B * 2 * I * h, 2.0 * (2 * I * h + B * h + B * I)
+    if cls == 4:
+        return 2.0 * B * h * I, 2.0 * (h * I + B * I + 2 * B * h)
+    if cls == 5:
+        return 2.0 * B * m.qkv_dim * h, 2.0 * (m.qkv_dim * h + B * h) + 4.0 * B * m.qkv_dim
+    if cls == 6:
+        return 2.0 * B * h * q, 2.0 * (h * q + B * q + 2 * B * h)
+    if cls == 7:
+        return 2.0 * B * V * h, 2.0 * (V * h + B * h)
+    if cls == 2:
+        toks = B * (ctx_avg + 1)
+        return 4.0 * m.n_q_heads * m.head_dim * toks, 2.0 * 2 * kvd * toks + 2.0 * 2 * B * q
+    if cls == 3:
+        return 0.0, float(layer_bytes)
+    raise ValueError(cls)
+
+
+def roofline_entry(cls, m, B, ctx_avg, layer_bytes, avg_ms, peaks, traffic=None):
+    flops, byts = kernel_work(cls, m, B, ctx_avg, layer_bytes)
+    t_tensor = flops / (peaks["tflops"] * 1e12) if flops else 0.0
+    t_hbm = byts / (peaks["hbm"] * 1e9)
+    if cls == 3:
+        ach = byts / (avg_ms * 1e-3) / 1e9
+        return {"kernel": CLS_NAMES[cls], "bound": "nvlink", "achieved": ach, "peak": peaks["nvl"],
+                "unit": "GB/s", "frac": ach / peaks["nvl"], "traffic": traffic}
+    if t_tensor > t_hbm:
+        ach = flops / (avg_ms * 1e-3) / 1e12
+        return {"kernel": CLS_NAMES[cls], "bound": "tensor", "achieved": ach,
+                "peak": peaks["tflops"], "unit": "TFLOP/s", "frac": ach / peaks["tflops"],
+                "traffic": traffic, "algorithmic_bytes": byts, "algorithmic_flops": flops}
+    ach = byts / (avg_ms * 1e-3) / 1e9
+    return {"kernel": CLS_NAMES[cls], "bound": "hbm", "achieved": ach, "peak": peaks["hbm"],
+            "unit": "GB/s", "frac": ach / peaks["hbm"], "traffic": traffic,
+            "algorithmic_bytes": byts, "algorithmic_flops": flops}
+
+
+def load_peaks():
+    p = {"hbm": 6549.1, "tflops": 1369.2, "tflops_burst": 1634.2, "nvl": 770.0,
+         "source": "MEASURED_PEAKS.json"}
+    try:
+        j = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        p["hbm"] = float(j["hbm_gbs"])
+        p["tflops"] = float(j.get("bf16_tflops_sustained", j["bf16_tflops"]))
+        p["tflops_burst"] = float(j["bf16_tflops"])
+    except Exception:
+        p.update({"hbm": 6650.0, "tflops": 1400.0, "tflops_burst": 1590.0,
+                  "source": "fallback (B200_PROFILING.md)"})
+    return p
+
+
+def load_traffic(workload, cls):
+    """dram bytes per launch from a committed ncu --set full capture (profiles/), or None."""
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return j.get(workload, {}).get(CLS_NAMES[cls])
+    except Exception:
+        return None
+
+
+def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms):
+    """Step-level roofline of SURVEY.md §8(d): T2 = max(sum 2PB/P_peak, sum R/BW_nvl) + T_lm;
+    T3 adds HBM weight reads and KV reads per layer."""
+    P = m.hidden * m.qkv_dim + m.q_dim * m.hidden + 3 * m.hidden * m.intermediate   # P_l
+    L = m.num_layers
+    lm = max(2.0 * B * m.vocab * m.hidden / (peaks["tflops"] * 1e12),
+             2.0 * m.vocab * m.hidden / (peaks["hbm"] * 1e9))
+    remote = (L - -(-L // d)) * P * 2.0 if d > 1 else 0.0      # (L - L/d) layers x bytes
+    t_gemm = L * 2.0 * P * B / (peaks["tflops"] * 1e12)
+    t_nvl = remote / (peaks["nvl"] * 1e9)
+    T2 = max(t_gemm, t_nvl) + lm
+    per_layer = max(2.0 * P * B / (peaks["tflops"] * 1e12), 2.0 * P / (peaks["hbm"] * 1e9)) + \
+        B * (ctx_avg + 1) * 4.0 * m.kv_dim / (peaks["hbm"] * 1e9)
+    T3 = max(L * per_layer, t_nvl) + lm
+    return {"T2_ms": T2 * 1e3, "T3_ms": T3 * 1e3, "frac_T2": T2 * 1e3 / step_ms,
+            "frac_T3": T3 * 1e3 / step_ms, "nvlink_bytes_per_step": remote,
+            "peaks": {"bf16_tflops": peaks["tflops"], "hbm_gbs": peaks["hbm"],
+                      "nvlink_gbs": peaks["nvl"]}}
+
+
+# ----------------------------------------------------------------------------- main arms
+def run_reference(args, wl, m, rank, world):
+    if rank != 0:
+        return
+    B = args.cpu_rows
+    ctx_len = wl.ctx
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, desc, cores, t_step = oracle_sample(m, wl.seed, B, ctx_len, timed_iters=1)
+        if i >= args.warmup:
+            vals.append(v)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": B / v * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args, wl, m, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+                             "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, wl, m, world):
+    B = args.batch or wl.batch
+    return {"workload": f"{wl.id}: {m.name} WaS decode, B={B}/GPU, S_ctx={args.ctx or wl.ctx}",
+            "batch_per_gpu": B, "ctx": args.ctx or wl.ctx, "layers": m.num_layers,
+            "reduced": args.layers is not None, "world": world, "slots": args.slots or wl.slots,
+            "order": args.order, "pool": args.pool, "fetch": args.fetch,
+            "stagger": not args.no_stagger,
+            "l2": "no flush needed: per-step working set (weights + KV) >> 126 MB L2",
+            "parallelism": f"sidp-dp{world}"}
+
+
+def main():
+    args = parse()
+    from sidp_inputs import MODELS, WORKLOADS
+    wl = WORKLOADS[args.workload]
+    m = MODELS[wl.model]
+    if args.layers:
+        m = m.with_layers(args.layers)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, wl, m, rank, world)
+        return
+    import numpy as np
+    import torch
+    import paper_2605_28095_b200 as P
+    from sidp_inputs import gen
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch or wl.batch
+    ctx_len = args.ctx or wl.ctx
+    slots = args.slots or wl.slots
+    e2e_steps = 0 if args.no_e2e else args.steps
+    max_ctx = ctx_len + args.warmup + args.steps + e2e_steps + 8
+    seed = wl.seed
+    ctx = P.Context(m, rank=rank, world=world, slots=slots, order=args.order, pool=args.pool,
+                    max_batch=B, max_ctx=max_ctx, fetch_sms=args.fetch_sms,
+                    fetch_engine=args.fetch, stagger=not args.no_stagger, device=local,
+                    seed=seed)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ctx.init_weights_synthetic(stream=stream)
+        kv = P.KVCache(m, B, max_ctx)
+        kv.fill_synthetic(seed, rank * B, B, ctx_len, stream=stream)
+    stream.synchronize()
+    if world > 1:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, ctx.export_handles())
+        ctx.import_handles(blobs)
+        dist.barrier()
+    bg = np.arange(rank * B, rank * B + B)
+    kv.set_pos(np.full(B, ctx_len))
+    tok = torch.from_numpy(gen.tokens(seed, bg, m.vocab)).to(torch.int32).cuda()
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.step(tok, tok, kv, batch=B, stream=stream, advance_pos=True)
+
+    # warm-up; the last warm-up step times every kernel class to find the dominant one
+    all_mask = sum(1 << c for c in CLS_NAMES)
+    for i in range(args.warmup):
+        if i == args.warmup - 1:
+            ctx.set_timing(all_mask)
+        step()
+    stream.synchronize()
+    shares = ctx.stats()["timed_ms"]
+    tot = sum(shares[1:]) or 1.0
+    kernel_shares = {CLS_NAMES[c]: shares[c] / tot for c in CLS_NAMES}
+    dom = max((c for c in CLS_NAMES if c != 3 or world > 1), key=lambda c: shares[c])
+
+    # ---------------- timed region (device-side, CUDA events, max over ranks)
+    ctx.set_timing(1 << dom)
+    launches0 = ctx.stats()["launches"]
+    pos_before = kv.max_pos
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    st = ctx.stats()
+    launches = st["launches"] - launches0
+    dom_ms = st["timed_ms"][dom] / max(1, st["timed_launches"][dom])
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        if dist.get_rank() == 0:
+            all_clk = [None] * world
+        else:
+            all_clk = None
+        gathered = [None] * world
+        dist.all_gather_object(gathered, clocks)
+        clocks = dict(gathered[0])
+        clocks["reasons"] = sorted({r for g in gathered for r in g["reasons"]})
+        clocks["per_rank_sm_mhz"] = [g["sm_mhz"] for g in gathered]
+    ms_step = ms / args.steps
+    value = B * world * args.steps / (ms / 1e3)
+    ctx_avg = pos_before + (args.steps - 1) / 2.0
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if e2e_steps:
+        h_in = torch.from_numpy(gen.tokens(seed, bg, m.vocab)).to(torch.int32).pin_memory()
+        h_out = torch.empty(B, dtype=torch.int32).pin_memory()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            with torch.cuda.stream(stream):
+                tok.copy_(h_in, non_blocking=True)
+            step()
+            with torch.cuda.stream(stream):
+                h_out.copy_(tok, non_blocking=True)
+            stream.synchronize()
+            h_in, h_out = h_out, h_in
+        t1 = time.perf_counter()
+        e_ms = (t1 - t0) * 1e3
+        if dist:
+            t = torch.tensor([e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": B * world * e2e_steps / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 4 * B,
+               "ms_per_step": e_ms / e2e_steps,
+               "note": "host tokens H2D from pinned memory, sidp_step, next tokens D2H + sync, per step"}
+
+    if rank != 0:
+        ctx.destroy()
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    roof = roofline_entry(dom, m, B, ctx_avg, st["layer_bytes"], dom_ms, peaks,
+                          load_traffic(wl.id, dom))
+    roof["avg_launch_ms"] = dom_ms
+    roof["launches_timed"] = st["timed_launches"][dom]
+    roof["peak_source"] = peaks["source"] + (" (sustained bf16)" if roof["unit"] == "TFLOP/s" else "")
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, desc, cores, _ = oracle_sample(m, seed, args.cpu_rows, ctx_len)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: counter-hash bf16 weights and KV (sidp_inputs.gen), seeded",
+        "config": _config(args, wl, m, world),
+        "roofline": roof,
+        "north_star_roofline": north_star_roofline(m, B, ctx_avg, world, peaks, ms_step),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "per_gpu_tokens_s": value / world,
+        "kernel_shares": kernel_shares,
+        "footprint_bytes_per_gpu": {"owned": st["owned_bytes"], "slots": st["slot_bytes"],
+                                    "replicated": st["replicated_bytes"],
+                                    "kv": 2 * kv.k.numel() * 2},
+    }
+    print(json.dumps(line), flush=True)
+    ctx.destroy()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -111,11 +111,13 @@ typedef struct {
  * parity dumps). */
 typedef struct {
   const int32_t* tokens;
-  int32_t* next;
+  int32_t* next;        /* may alias tokens (written after the last read of tokens) */
   int32_t batch;
   sidp_kv kv;
   float* logits;
   void* layer_inputs;
+  int32_t* pos_out;     /* optional device int32[batch]: receives pos[b] + 1 at the end of
+                           the step (may alias kv.pos) — a decode loop needs no other kernel */
 } sidp_batch;
 
 typedef struct {
@@ -132,8 +134,8 @@ typedef struct {
   uint64_t slot_bytes;      /* S x layer_bytes */
   uint64_t replicated_bytes;   /* embedding + final norm + LM head + local layer parts */
   uint64_t workspace_bytes; /* activations, split-K / split-KV workspaces, staging */
-  double timed_ms;          /* sum of timed-kernel durations (sidp_set_timing) */
-  uint64_t timed_launches;  /* launches of the timed kernel class */
+  double timed_ms[8];       /* per kernel class: summed CUDA-event durations (sidp_set_timing) */
+  uint64_t timed_launches[8];  /* per kernel class: timed launches */
 } sidp_stats_t;
 
 /* ---- lifecycle --------------------------------------------------------------------- */
@@ -216,10 +218,11 @@ sidp_status sidp_get_fetch_log(const sidp_ctx* ctx, int32_t* fetch_step, int32_t
 
 sidp_status sidp_stats(const sidp_ctx* ctx, sidp_stats_t* out);
 
-/* Time every launch of one kernel class with CUDA events on its own stream:
- * 0 off, 1 gate/up GEMM, 2 attention, 3 fetch, 4 down GEMM, 5 QKV GEMM, 6 O GEMM,
- * 7 LM head.  sidp_stats().timed_ms sums them (host-synchronising read). */
-sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t kernel_class);
+/* Time every launch of the kernel classes in `class_mask` (bit c = class c) with CUDA events
+ * on the stream each launch goes to: 1 gate/up GEMM, 2 attention, 3 fetch, 4 down GEMM,
+ * 5 QKV GEMM, 6 O GEMM, 7 LM head (0 = off).  Resets the accumulators;
+ * sidp_stats().timed_ms[c] sums them (that read synchronises on the recorded events). */
+sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t class_mask);
 
 const char* sidp_last_error(void);
 

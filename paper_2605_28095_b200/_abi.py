@@ -42,7 +42,7 @@ class KV(C.Structure):
 
 class Batch(C.Structure):
     _fields_ = [("tokens", C.c_void_p), ("next", C.c_void_p), ("batch", C.c_int32), ("kv", KV),
-                ("logits", C.c_void_p), ("layer_inputs", C.c_void_p)]
+                ("logits", C.c_void_p), ("layer_inputs", C.c_void_p), ("pos_out", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -51,8 +51,8 @@ class Stats(C.Structure):
                 ("timeouts", C.c_int32), ("layer_bytes", C.c_uint64),
                 ("local_layer_bytes", C.c_uint64), ("owned_bytes", C.c_uint64),
                 ("slot_bytes", C.c_uint64), ("replicated_bytes", C.c_uint64),
-                ("workspace_bytes", C.c_uint64), ("timed_ms", C.c_double),
-                ("timed_launches", C.c_uint64)]
+                ("workspace_bytes", C.c_uint64), ("timed_ms", C.c_double * 8),
+                ("timed_launches", C.c_uint64 * 8)]
 
 
 _P = C.c_void_p

@@ -130,12 +130,17 @@ class Context:
                                           _stream_ptr(stream)), "sidp_decode_layer")
 
     def step(self, tokens, nxt, kv: KVCache, batch=None, logits=None, layer_inputs=None,
-             stream=None):
+             stream=None, advance_pos=False):
+        """One decode step.  advance_pos=True lets the library write pos+1 back into kv.pos
+        (and the host hint kv.max_pos is bumped here), so a decode loop launches nothing else."""
         b = tokens.shape[0] if batch is None else batch
         bt = A.Batch(tokens.data_ptr() if b else None, nxt.data_ptr() if b else None, b, kv.c(),
                      logits.data_ptr() if logits is not None else None,
-                     layer_inputs.data_ptr() if layer_inputs is not None else None)
+                     layer_inputs.data_ptr() if layer_inputs is not None else None,
+                     kv.pos.data_ptr() if advance_pos else None)
         A.check(A.lib().sidp_step(self.h, C.byref(bt), _stream_ptr(stream)), "sidp_step")
+        if advance_pos:
+            kv.max_pos += 1
 
     def set_mode(self, mode, effective_step):
         A.check(A.lib().sidp_set_mode(self.h, mode, effective_step), "sidp_set_mode")
@@ -181,10 +186,16 @@ class Context:
     def stats(self) -> dict:
         s = A.Stats()
         A.check(A.lib().sidp_stats(self.h, C.byref(s)), "sidp_stats")
-        return {f: getattr(s, f) for f, _ in A.Stats._fields_}
+        d = {f: getattr(s, f) for f, _ in A.Stats._fields_}
+        d["timed_ms"] = list(s.timed_ms)
+        d["timed_launches"] = list(s.timed_launches)
+        return d
 
-    def set_timing(self, kernel_class: int):
-        A.check(A.lib().sidp_set_timing(self.h, kernel_class), "sidp_set_timing")
+    # kernel classes for set_timing (bit positions)
+    K_GATEUP, K_ATTN, K_FETCH, K_DOWN, K_QKV, K_O, K_LMHEAD = 1, 2, 3, 4, 5, 6, 7
+
+    def set_timing(self, class_mask: int):
+        A.check(A.lib().sidp_set_timing(self.h, class_mask), "sidp_set_timing")
 
     def layer_ptr(self, layer):
         p, q = C.c_void_p(), C.c_void_p()

@@ -70,8 +70,9 @@ struct AttnArgs {
 };
 cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s);
 
-cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next, int rows,
-                                   cudaStream_t s);
+// next[b] = decoded argmax; if pos_out: pos_out[b] = pos[b] + 1 (may alias pos)
+cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next,
+                                   int32_t* pos_out, const int32_t* pos, int rows, cudaStream_t s);
 cudaError_t argmax_reset_launch(unsigned long long* packed, int rows, cudaStream_t s);
 
 // ---------------------------------------------------------------- K12 synthetic init

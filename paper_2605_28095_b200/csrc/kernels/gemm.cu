@@ -1,20 +1,26 @@
 // gemm.cu — tcgen05/TMEM decode GEMM for sm_100a.
 //
-// Y[m, n] = sum_k X[m, k] W[n, k], bf16 in, fp32 accumulate (north_star: "bf16 weights
-// with fp32 accumulation").  Decode shapes have few tokens (M = batch rows) and many
-// features, so the kernel is "swap-AB": a 128-row W tile is the UMMA A operand
-// (UMMA_M = 128), the token tile is the UMMA N operand (16..256), and the fp32
-// accumulator D^T[feature, token] lives in TMEM (lane = feature, column = token).
+// Y[m, n] = sum_k X[m, k] W[n, k], bf16 in, fp32 accumulate (north_star: "bf16 weights with
+// fp32 accumulation").  Decode shapes have few tokens (M = batch rows) and many features, so the
+// kernel is swap-AB: W rows are the UMMA "M" operand, tokens the UMMA "N" operand.
 //
-// Warp roles (192 threads, one CTA per SM):
-//   warp 0      TMA producer: W tile [128 x 64] + X tile [BM x 64] per stage, 128B swizzle
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
-// Split-K (for shapes with fewer tiles than SMs): every split writes fp32 partials to a
-// workspace; the last-arriving CTA of a tile (atomic counter) sums the partials in split
-// order 0..S-1 (deterministic) and runs the epilogue.
+// Design (B200-first):
+//  * CTA pairs (cluster 2, tcgen05.mma.cta_group::2): a pair owns a 256-feature tile; each CTA
+//    TMA-loads its 128 W rows and half of the token tile, the leader issues one M=256 UMMA over
+//    both CTAs' shared memory, each CTA's TMEM holds its 128 features x all tokens.  This halves
+//    the per-SM token-tile (L2) traffic and runs the tensor core at the 2-SM rate.
+//  * Persistent: grid = (#SMs / 2) pairs walking a static list of (feature tile, token tile,
+//    k-split) units; two TMEM accumulators so the epilogue of unit i overlaps the mainloop of
+//    unit i+1.
+//  * Warp roles (192 threads / CTA): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer
+//    (leader CTA), warps 2-5 epilogue (tcgen05.ld -> smem transpose -> 16-byte coalesced stores).
+//  * Epilogue kind is a template parameter (one compact kernel per kind).
+//  * Split-K for shapes with few feature tiles: fp32 partials to a workspace; the last-arriving
+//    split of a tile half sums the partials in split order 0..S-1 (deterministic) and runs the
+//    epilogue.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../common.cuh"
 #include "../kernels.h"
@@ -23,245 +29,447 @@ namespace sidp {
 
 namespace {
 
-constexpr int BN = 128;      // features per tile (UMMA_M)
-constexpr int BK = 64;       // 64 bf16 = 128 B per row -> SWIZZLE_128B atom
+constexpr int BK = 64;          // 64 bf16 = 128 B rows -> SWIZZLE_128B atom
+constexpr int WROWS = 128;      // W rows per CTA (UMMA M = 256 per pair)
 constexpr int kThreads = 192;
-constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemBudget = 224 * 1024;
+constexpr int SROW = 132;       // padded fp32 staging row (32 tokens x 128 features)
 
 struct KParams {
   int M, N, K;
-  int BM;                    // token tile (UMMA_N)
+  int BNT;                      // token tile (UMMA N), multiple of 32, <= 256
   int stages;
-  int splits;
-  int kb_per_split;
-  int epi;
+  int splits, kb_per_split;
+  int m_tiles, n_pairs, units;
   void* out; int ldo;
   const bf16* resid; int ldr;
   const bf16* bias;
   float* ws;
   int* counters;
+  int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
 };
 
-__device__ __forceinline__ unsigned long long argmax_key(float v, int n) {
+// ---- cluster / 2-SM helpers ------------------------------------------------------
+SIDP_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+SIDP_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+SIDP_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+SIDP_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+SIDP_DEV void tma_load_2d_2sm(const CUtensorMap* m, uint32_t leader_bar, void* smem_dst, int c0,
+                              int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+SIDP_DEV void umma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+SIDP_DEV void umma2_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+SIDP_DEV void tmem_alloc2(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_dst)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+SIDP_DEV void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+
+SIDP_DEV unsigned long long argmax_key(float v, int n) {
   uint32_t u = __float_as_uint(v);
   u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
   return ((unsigned long long)u << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)n);
 }
 
-// Epilogue of one 32-column chunk for one thread (feature row `n`, tokens m0..m0+31).
-__device__ __forceinline__ void epilogue_chunk(const KParams& p, const float (&v)[32], int n,
-                                               int m0, int lane_in_tile, float* xchg,
-                                               int epi_tid) {
-  const int epi = p.epi;
-  if (epi == EPI_SILU_MUL) {
-    // rows 0..63 of the tile are gate features, rows 64..127 the matching up features
-    const bool is_up = lane_in_tile >= 64;
-    const int i = lane_in_tile & 63;
-    if (is_up) {
+SIDP_DEV void unpack_bf16x8(const uint4& raw, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) xchg[j * 64 + i] = v[j];
-    }
-    named_bar_sync(1, 128);
-    if (!is_up) {
-      const int f = (n / BN) * 64 + i;        // output feature
-      const int F = p.N / 2;
-      bf16* out = reinterpret_cast<bf16*>(p.out);
-      if (f < F) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int m = m0 + j;
-          if (m < p.M) {
-            const float g = v[j], u = xchg[j * 64 + i];
-            const float s = g / (1.0f + __expf(-g));
-            out[(size_t)m * p.ldo + f] = f_to_bf16(s * u);
-          }
-        }
-      }
-    }
-    named_bar_sync(1, 128);
-    return;
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
   }
-  if (epi == EPI_ARGMAX) {
-    unsigned long long* out = reinterpret_cast<unsigned long long*>(p.out);
+}
+SIDP_DEV uint4 pack_bf16x8(const float (&f)[8]) {
+  uint4 r;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      unsigned long long key = (n < p.N) ? argmax_key(v[j], n) : 0ull;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-        key = other > key ? other : key;
-      }
-      const int m = m0 + j;
-      if ((threadIdx.x & 31) == 0 && m < p.M) atomicMax(out + m, key);
-    }
-    return;
-  }
-  if (n >= p.N) return;
-  const float b = p.bias ? bf16_to_f(p.bias[n]) : 0.0f;
-  if (epi == EPI_F32) {
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return r;
+}
+
+// Store phase: sm holds fp32 [32 tokens][SROW] (features 0..127 of this CTA's W rows).
+// m0 = first token of the chunk, n0 = first feature (W row) of this CTA, pt = packed tile id.
+template <int EPI>
+SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int pt, int tid) {
+  if constexpr (EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(p.out);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int m = m0 + j;
-      if (m < p.M) out[(size_t)m * p.ldo + n] = v[j] + b;
-    }
-  } else if (epi == EPI_BF16) {
-    bf16* out = reinterpret_cast<bf16*>(p.out);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int m = m0 + j;
-      if (m < p.M) out[(size_t)m * p.ldo + n] = f_to_bf16(v[j] + b);
-    }
-  } else {  // EPI_RESID
-    bf16* out = reinterpret_cast<bf16*>(p.out);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int m = m0 + j;
-      if (m < p.M) {
-        const float r = bf16_to_f(p.resid[(size_t)m * p.ldr + n]);
-        out[(size_t)m * p.ldo + n] = f_to_bf16(v[j] + r);
+    for (int i = 0; i < 8; ++i) {
+      const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
+      const int m = m0 + j, n = n0 + f;
+      if (m < p.M && n < p.N) {
+        float4 x = *reinterpret_cast<const float4*>(sm + j * SROW + f);
+        if (p.bias) {
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(p.bias + n);
+          const float2 b0 = __bfloat1622float2(b2[0]), b1 = __bfloat1622float2(b2[1]);
+          x.x += b0.x; x.y += b0.y; x.z += b1.x; x.w += b1.y;
+        }
+        *reinterpret_cast<float4*>(out + (size_t)m * p.ldo + n) = x;
       }
+    }
+  } else if constexpr (EPI == EPI_BF16 || EPI == EPI_RESID) {
+    bf16* out = reinterpret_cast<bf16*>(p.out);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int v = tid + 128 * i, j = v >> 4, f = (v & 15) * 8;
+      const int m = m0 + j, n = n0 + f;
+      if (m < p.M && n < p.N) {
+        float x[8];
+        const float4 a = *reinterpret_cast<const float4*>(sm + j * SROW + f);
+        const float4 b = *reinterpret_cast<const float4*>(sm + j * SROW + f + 4);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        float y[8];
+        if constexpr (EPI == EPI_RESID) {
+          unpack_bf16x8(*reinterpret_cast<const uint4*>(p.resid + (size_t)m * p.ldr + n), y);
+        } else {
+          if (p.bias) {
+            unpack_bf16x8(*reinterpret_cast<const uint4*>(p.bias + n), y);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) y[q] = 0.0f;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] += y[q];
+        *reinterpret_cast<uint4*>(out + (size_t)m * p.ldo + n) = pack_bf16x8(x);
+      }
+    }
+  } else if constexpr (EPI == EPI_SILU_MUL) {
+    // this CTA's 128 W rows = [gate 64 | up 64] of packed tile pt -> outputs pt*64 .. +64
+    bf16* out = reinterpret_cast<bf16*>(p.out);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int v = tid + 128 * i, j = v >> 3, f = (v & 7) * 8;
+      const int m = m0 + j;
+      const int of = pt * 64 + f;
+      if (m < p.M && of < p.N / 2) {
+        float x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float g = sm[j * SROW + f + q], u = sm[j * SROW + 64 + f + q];
+          x[q] = g / (1.0f + __expf(-g)) * u;
+        }
+        *reinterpret_cast<uint4*>(out + (size_t)m * p.ldo + of) = pack_bf16x8(x);
+      }
+    }
+  } else {  // EPI_ARGMAX: warp w reduces tokens w*8 .. w*8+7 over the 128 features
+    unsigned long long* out = reinterpret_cast<unsigned long long*>(p.out);
+    const int w = tid >> 5, lane = tid & 31;
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = w * 8 + jj, m = m0 + j;
+      unsigned long long key = 0ull;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int n = n0 + lane * 4 + q;
+        if (n < p.N) {
+          const unsigned long long k2 = argmax_key(sm[j * SROW + lane * 4 + q], n);
+          key = k2 > key ? k2 : key;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+        key = other > key ? other : key;
+      }
+      if (lane == 0 && m < p.M && key) atomicMax(out + m, key);
     }
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-               const KParams p) {
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+             const KParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int stages = p.stages;
-  const int BM = p.BM;
-  const uint32_t a_bytes = BN * BK * 2;                 // 16 KB
-  const uint32_t b_bytes = (uint32_t)BM * BK * 2;
+  const int stages = p.stages, BNT = p.BNT, HALF = p.BNT / 2;
+  const uint32_t a_bytes = WROWS * BK * 2;              // 16 KB
+  const uint32_t b_bytes = (uint32_t)HALF * BK * 2;
   uint8_t* sA = smem;
   uint8_t* sB = sA + (size_t)stages * a_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)stages * b_bytes);
+  float* stg = reinterpret_cast<float*>(sB + (size_t)stages * b_bytes);   // [32][SROW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + 32 * SROW);
   uint64_t* empty = full + stages;
-  uint64_t* tmem_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + stages;                      // [2]
+  uint64_t* tempty = tfull + 2;                          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  float* xchg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_full) + 64);  // 8 KB
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int n_blk = blockIdx.x, m_blk = blockIdx.y, split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int nkb = p.K / BK;
-  const int kb0 = split * p.kb_per_split;
-  const int kb1 = min(nkb, kb0 + p.kb_per_split);
-  const int tmem_cols = BM <= 32 ? 32 : (BM <= 64 ? 64 : (BM <= 128 ? 128 : 256));
+  const uint32_t tmem_cols = BNT <= 16 ? 32 : (BNT <= 32 ? 64 : (BNT <= 64 ? 128 : (BNT <= 128 ? 256 : 512)));
 
-  if (warp == 0 && lane == 0) {
+  if (threadIdx.x == 0) {
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 1);          // leader's arrive + expect_tx(bytes of both CTAs)
+      mbar_init(&empty[s], 1);         // MMA commit (multicast to both CTAs)
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);        // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 1) tmem_alloc2(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
-      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-        const int s = i % stages;
-        const uint32_t ph = (i / stages) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
-        tma_load_2d(&tm_w, &full[s], sA + (size_t)s * a_bytes, kb * BK, n_blk * BN);
-        tma_load_2d(&tm_x, &full[s], sB + (size_t)s * b_bytes, kb * BK, m_blk * BM);
+      int it = 0;
+      for (int u = cluster; u < p.units; u += n_clusters) {
+        const int ks = u % p.splits, rest = u / p.splits;
+        const int mt = rest % p.m_tiles, ft = rest / p.m_tiles;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(nkb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
+          if (p.debug & 2) {
+            if (leader) mbar_arrive(&full[s]);
+            continue;
+          }
+          // Only the leader arrives (expecting both CTAs' bytes); the peer's TMA completes its
+          // transaction bytes on the leader's barrier directly — no per-stage remote arrive.
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
+          tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes, kb * BK, ft * 2 * WROWS + rank * WROWS);
+          tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes, kb * BK, mt * BNT + rank * HALF);
+        }
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = umma_idesc_bf16(BN, BM);
-    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-      const int s = i % stages;
-      const uint32_t ph = (i / stages) & 1;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(sA + (size_t)s * a_bytes);
-        const uint32_t b0 = smem_u32(sB + (size_t)s * b_bytes);
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      const uint32_t idesc = umma_idesc_bf16(2 * WROWS, BNT);
+      int it = 0, ui = 0;
+      for (int u = cluster; u < p.units; u += n_clusters, ++ui) {
+        const int ks = u % p.splits;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(nkb, kb0 + p.kb_per_split);
+        const int acc = ui & 1;
+        const uint32_t aph = (ui >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * BNT;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (lane == 0 && (p.debug & 1)) {
+            mbar_arrive(&empty[s]);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&empty[s]), 1));
+          } else if (lane == 0) {
+            const uint32_t a0 = smem_u32(sA + (size_t)s * a_bytes);
+            const uint32_t b0 = smem_u32(sB + (size_t)s * b_bytes);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          umma_bf16(tmem_base, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                    (i > 0 || k > 0) ? 1u : 0u);
-        }
-        umma_commit(&empty[s]);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) umma_commit(tmem_full);
-    __syncwarp();
-  } else {
-    // ---------------------------------------------------------------- epilogue warps
-    const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-    const int lane_in_tile = quarter * 32 + lane;
-    const int n = n_blk * BN + lane_in_tile;
-    const int epi_tid = (warp - 2) * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const uint32_t t_lane = tmem_base + ((uint32_t)(quarter * 32) << 16);
-    const int tile_id = m_blk * gridDim.x + n_blk;
-    const size_t tile_elems = (size_t)BN * BM;
-
-    if (p.splits == 1) {
-      for (int c = 0; c < BM; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_lane + c, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        epilogue_chunk(p, v, n, m_blk * BM + c, lane_in_tile, xchg, epi_tid);
-      }
-    } else {
-      // write this split's partial, then the last CTA of the tile reduces in split order
-      float* my = p.ws + ((size_t)tile_id * p.splits + split) * tile_elems;
-      for (int c = 0; c < BM; c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_lane + c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) my[(size_t)(c + j) * BN + lane_in_tile] = __uint_as_float(r[j]);
-      }
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (epi_tid == 0) {
-        const int old = atomicAdd(p.counters + tile_id, 1);
-        *last_flag = (old == p.splits - 1);
-        if (old == p.splits - 1) p.counters[tile_id] = 0;   // re-arm for the next launch
-      }
-      named_bar_sync(1, 128);
-      if (*last_flag) {
-        __threadfence();
-        const float* base = p.ws + (size_t)tile_id * p.splits * tile_elems;
-        for (int c = 0; c < BM; c += 32) {
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-          for (int s = 0; s < p.splits; ++s) {
-            const float* src = base + (size_t)s * tile_elems + (size_t)c * BN + lane_in_tile;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += __ldcg(src + (size_t)j * BN);
+            for (int k = 0; k < BK / 16; ++k)
+              umma2_bf16(dcol, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                         (kb > kb0 || k > 0) ? 1u : 0u);
+            umma2_commit_mc(&empty[s]);
           }
-          epilogue_chunk(p, v, n, m_blk * BM + c, lane_in_tile, xchg, epi_tid);
+          __syncwarp();
+        }
+        if (lane == 0) umma2_commit_mc(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quarter = warp & 3;                       // TMEM lane quarter of this warp
+    const int row = quarter * 32 + lane;                // W row within this CTA (feature)
+    const int tid = (warp - 2) * 32 + lane;             // 0..127
+    int ui = 0;
+    for (int u = cluster; u < p.units; u += n_clusters, ++ui) {
+      const int ks = u % p.splits, rest = u / p.splits;
+      const int mt = rest % p.m_tiles, ft = rest / p.m_tiles;
+      const int acc = ui & 1;
+      const uint32_t aph = (ui >> 1) & 1;
+      const int n0 = ft * 2 * WROWS + rank * WROWS;
+      const int pt = ft * 2 + rank;
+      const int mbase = mt * BNT;
+      const int nchunks = min(BNT, ((p.M - mbase + 31) / 32) * 32) / 32;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tl = tmem_base + acc * BNT + ((uint32_t)(quarter * 32) << 16);
+      if (p.splits == 1) {
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tl + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
+          if (c == nchunks - 1) {   // last TMEM read of this accumulator: hand it back early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          }
+          named_bar_sync(1, 128);
+          store_phase<EPI>(p, stg, mbase + c * 32, n0, pt, tid);
+          named_bar_sync(1, 128);
+        }
+        if (nchunks == 0) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        }
+      } else {
+        // split-K: fp32 partial of this k-slice -> ws[ks][m][n] (token-major, coalesced);
+        // gemm_reduce_kernel sums the slices in order 0..S-1 and runs the epilogue.
+        float* part = p.ws + (size_t)ks * p.M * p.N;
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tl + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
+          if (c == nchunks - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          }
+          named_bar_sync(1, 128);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
+            const int m = mbase + c * 32 + j, n = n0 + f;
+            if (m < p.M && n < p.N)
+              __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N + n),
+                     *reinterpret_cast<const float4*>(stg + j * SROW + f));
+          }
+          named_bar_sync(1, 128);
+        }
+        if (nchunks == 0) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
       }
     }
-    tc_fence_before();
   }
+  tc_fence_before();
   __syncthreads();
+  cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, tmem_cols);
+    tmem_dealloc2(tmem_base, tmem_cols);
+  }
+}
+
+// Split-K reduction + epilogue over all SMs: each thread sums 8 consecutive outputs of one
+// token row across the S fp32 slices in order 0..S-1 (deterministic), then applies EPI.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
+  const int n_out = EPI == EPI_SILU_MUL ? p.N / 2 : p.N;
+  const int vec_per_row = n_out / 8;
+  const size_t total = (size_t)p.M * vec_per_row;
+  const size_t slice = (size_t)p.M * p.N;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(idx / vec_per_row);
+    const int f = (int)(idx % vec_per_row) * 8;
+    float a[8], b[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = b[q] = 0.0f;
+    int na = f, nb = 0;
+    if constexpr (EPI == EPI_SILU_MUL) {
+      na = (f / 64) * 128 + (f % 64);   // gate rows of packed tile f/64
+      nb = na + 64;                     // matching up rows
+    }
+    const float* base = p.ws + (size_t)m * p.N;
+#pragma unroll 4
+    for (int s = 0; s < p.splits; ++s) {
+      const float4 x0 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + na));
+      const float4 x1 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + na + 4));
+      a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
+      a[4] += x1.x; a[5] += x1.y; a[6] += x1.z; a[7] += x1.w;
+      if constexpr (EPI == EPI_SILU_MUL) {
+        const float4 y0 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + nb));
+        const float4 y1 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + nb + 4));
+        b[0] += y0.x; b[1] += y0.y; b[2] += y0.z; b[3] += y0.w;
+        b[4] += y1.x; b[5] += y1.y; b[6] += y1.z; b[7] += y1.w;
+      }
+    }
+    if constexpr (EPI == EPI_F32) {
+      if (p.bias) {
+        float y[8];
+        unpack_bf16x8(*reinterpret_cast<const uint4*>(p.bias + f), y);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] += y[q];
+      }
+      float* out = reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo + f;
+      *reinterpret_cast<float4*>(out) = make_float4(a[0], a[1], a[2], a[3]);
+      *reinterpret_cast<float4*>(out + 4) = make_float4(a[4], a[5], a[6], a[7]);
+    } else if constexpr (EPI == EPI_BF16 || EPI == EPI_RESID) {
+      float y[8];
+      if constexpr (EPI == EPI_RESID) {
+        unpack_bf16x8(*reinterpret_cast<const uint4*>(p.resid + (size_t)m * p.ldr + f), y);
+      } else if (p.bias) {
+        unpack_bf16x8(*reinterpret_cast<const uint4*>(p.bias + f), y);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] += y[q];
+      *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.out) + (size_t)m * p.ldo + f) =
+          pack_bf16x8(a);
+    } else if constexpr (EPI == EPI_SILU_MUL) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = a[q] / (1.0f + __expf(-a[q])) * b[q];
+      *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.out) + (size_t)m * p.ldo + f) =
+          pack_bf16x8(a);
+    }
   }
 }
 
@@ -300,17 +508,24 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
 
 int g_num_sms = 0;
 
+template <int EPI>
+void set_attr() {
+  cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSmemBudget + 1024);
+}
+
 }  // namespace
 
-int gemm_pick_splits(int tiles, int nkb, int sms) {
-  if (tiles >= sms) return 1;
+int gemm_pick_splits(int tiles, int nkb, int slots) {
+  // tiles = pair-units without split; slots = concurrent pairs.  Cost ~ waves x (k-blocks + c).
+  if (tiles >= slots) return 1;
   int best = 1;
   double best_t = 1e30;
   for (int s = 1; s <= 16; ++s) {
     const int per = (nkb + s - 1) / s;
-    if (per < 2 && s > 1) break;
-    const int waves = (tiles * s + sms - 1) / sms;
-    const double t = waves * (per + 2.0);
+    if (per < 4 && s > 1) break;
+    const int waves = (tiles * s + slots - 1) / slots;
+    const double t = waves * (per + 6.0) + (s > 1 ? 2.0 : 0.0);
     if (t < best_t - 1e-9) {
       best_t = t;
       best = s;
@@ -321,48 +536,74 @@ int gemm_pick_splits(int tiles, int nkb, int sms) {
 
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t stream) {
   if (a.M <= 0) return cudaSuccess;
-  if (a.K % BK != 0 || a.N <= 0 || a.x == nullptr || a.w == nullptr) return cudaErrorInvalidValue;
-  if (a.epi == EPI_SILU_MUL && (a.N % BN) != 0) return cudaErrorInvalidValue;
+  if (a.K % BK != 0 || a.N <= 0 || a.N % 8 != 0 || a.x == nullptr || a.w == nullptr)
+    return cudaErrorInvalidValue;
+  if (a.epi == EPI_SILU_MUL && (a.N % WROWS) != 0) return cudaErrorInvalidValue;
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBudget + 1024);
+    set_attr<EPI_F32>();
+    set_attr<EPI_BF16>();
+    set_attr<EPI_RESID>();
+    set_attr<EPI_SILU_MUL>();
+    set_attr<EPI_ARGMAX>();
   }
+  static int env_bnt = getenv("SIDP_GEMM_BNT") ? atoi(getenv("SIDP_GEMM_BNT")) : 256;
+  static int env_stages = getenv("SIDP_GEMM_STAGES") ? atoi(getenv("SIDP_GEMM_STAGES")) : 12;
   const int sms = a.max_ctas > 0 ? std::min(a.max_ctas, g_num_sms) : g_num_sms;
-  int BM = std::min(256, ((a.M + 15) / 16) * 16);
-  if (BM > 32 && BM % 32) BM = ((BM + 31) / 32) * 32;   // epilogue walks 32-column chunks
-  if (BM < 32) BM = 32;
-  const int m_tiles = (a.M + BM - 1) / BM;
-  const int n_tiles = (a.N + BN - 1) / BN;
+  const int pair_slots = std::max(1, sms / 2);
+  int BNT = ((a.M + 31) / 32) * 32;
+  BNT = std::max(32, std::min(env_bnt, BNT));
+  const int m_tiles = (a.M + BNT - 1) / BNT;
+  const int n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
   const int nkb = a.K / BK;
-  int splits = a.k_splits > 0 ? a.k_splits : gemm_pick_splits(n_tiles * m_tiles, nkb, sms);
+  int splits = a.k_splits > 0 ? a.k_splits : gemm_pick_splits(n_pairs * m_tiles, nkb, pair_slots);
   splits = std::max(1, std::min(splits, nkb));
-  const int kb_per = (nkb + splits - 1) / splits;
+  if (a.epi == EPI_ARGMAX) splits = 1;                    // fused argmax needs whole dot products
+  while (splits > 1 && (size_t)splits * a.M * a.N * 4 > w.ws_bytes) --splits;
+  int kb_per = (nkb + splits - 1) / splits;
   splits = (nkb + kb_per - 1) / kb_per;                   // no empty split
-  const size_t tile_elems = (size_t)BN * BM;
-  if (splits > 1) {
-    if ((size_t)n_tiles * m_tiles * splits * tile_elems * 4 > w.ws_bytes ||
-        n_tiles * m_tiles > w.n_counters)
-      return cudaErrorMemoryAllocation;
-  }
-  const size_t stage_bytes = (size_t)BN * BK * 2 + (size_t)BM * BK * 2;
-  const size_t extra = 2048 + 64 * 32 * 4 + 64;            // barriers + epilogue exchange
-  int stages = (int)std::min<size_t>(8, (kSmemBudget - extra) / stage_bytes);
-  stages = std::max(2, std::min(stages, std::max(2, kb_per)));
+  const int units = n_pairs * m_tiles * splits;
+  const size_t stage_bytes = (size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2;
+  const size_t extra = 32 * SROW * 4 + 512;
+  int stages = (int)std::min<size_t>(env_stages, (kSmemBudget - extra) / stage_bytes);
+  stages = std::max(2, stages);
 
   CUtensorMap tw, tx;
-  if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, BN)) return cudaErrorInvalidValue;
-  if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BM)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, WROWS)) return cudaErrorInvalidValue;
+  if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) return cudaErrorInvalidValue;
 
   KParams p;
-  p.M = a.M; p.N = a.N; p.K = a.K; p.BM = BM; p.stages = stages; p.splits = splits;
-  p.kb_per_split = kb_per; p.epi = a.epi; p.out = a.out; p.ldo = a.ldo; p.resid = a.resid;
-  p.ldr = a.ldr; p.bias = a.bias; p.ws = w.ws; p.counters = w.counters;
+  p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages; p.splits = splits;
+  p.kb_per_split = kb_per; p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.units = units;
+  p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
+  p.ws = w.ws; p.counters = w.counters;
+  static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
+  p.debug = env_debug;
   const size_t smem = stages * stage_bytes + extra + 1024;
-  dim3 grid(n_tiles, m_tiles, splits);
-  gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(tw, tx, p);
+  const int clusters = std::min(units, pair_slots);
+  dim3 grid(2 * clusters);
+  switch (a.epi) {
+    case EPI_F32: gemm2_kernel<EPI_F32><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
+    case EPI_BF16: gemm2_kernel<EPI_BF16><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
+    case EPI_RESID: gemm2_kernel<EPI_RESID><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
+    case EPI_SILU_MUL: gemm2_kernel<EPI_SILU_MUL><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
+    case EPI_ARGMAX: gemm2_kernel<EPI_ARGMAX><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || splits == 1) return e;
+  const int n_out = a.epi == EPI_SILU_MUL ? a.N / 2 : a.N;
+  const size_t vecs = (size_t)a.M * (n_out / 8);
+  const int rgrid = (int)std::min<size_t>((vecs + 255) / 256, (size_t)g_num_sms * 8);
+  switch (a.epi) {
+    case EPI_F32: gemm_reduce_kernel<EPI_F32><<<rgrid, 256, 0, stream>>>(p); break;
+    case EPI_BF16: gemm_reduce_kernel<EPI_BF16><<<rgrid, 256, 0, stream>>>(p); break;
+    case EPI_RESID: gemm_reduce_kernel<EPI_RESID><<<rgrid, 256, 0, stream>>>(p); break;
+    case EPI_SILU_MUL: gemm_reduce_kernel<EPI_SILU_MUL><<<rgrid, 256, 0, stream>>>(p); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

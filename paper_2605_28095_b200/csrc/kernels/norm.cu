@@ -57,9 +57,13 @@ __global__ void embed_kernel(const bf16* __restrict__ E, int h, const int32_t* _
   for (int v = threadIdx.x; v < h / 8; v += blockDim.x) dst[v] = src[v];
 }
 
-__global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* next, int rows) {
+__global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* next,
+                                       int32_t* pos_out, const int32_t* pos, int rows) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < rows) next[i] = (int32_t)(0xFFFFFFFFu - (uint32_t)(packed[i] & 0xFFFFFFFFull));
+  if (i < rows) {
+    next[i] = (int32_t)(0xFFFFFFFFu - (uint32_t)(packed[i] & 0xFFFFFFFFull));
+    if (pos_out) pos_out[i] = pos[i] + 1;
+  }
 }
 
 __global__ void argmax_reset_kernel(unsigned long long* packed, int rows) {
@@ -84,10 +88,10 @@ cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, i
   return cudaGetLastError();
 }
 
-cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next, int rows,
-                                   cudaStream_t s) {
+cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next,
+                                   int32_t* pos_out, const int32_t* pos, int rows, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  argmax_finalize_kernel<<<(rows + 255) / 256, 256, 0, s>>>(packed, next, rows);
+  argmax_finalize_kernel<<<(rows + 255) / 256, 256, 0, s>>>(packed, next, pos_out, pos, rows);
   return cudaGetLastError();
 }
 

@@ -113,10 +113,11 @@ struct sidp_ctx {
   int64_t pending_step = 0;
   // stats + timing
   sidp_stats_t st{};
-  int timed_class = 0;
+  int timed_mask = 0;
   std::vector<cudaEvent_t> tev;
+  std::vector<int> tev_cls;
   int tev_used = 0;
-  double timed_acc_ms = 0.0;
+  double timed_acc_ms[8]{};
 };
 
 namespace {
@@ -221,15 +222,28 @@ int stagger_ticks_of(const sidp_ctx* c) {
 void count_launch(sidp_ctx* c, int n = 1) { c->st.launches += n; }
 
 // ---- optional per-class kernel timing ----
+void timing_flush(sidp_ctx* c);
 void timing_begin(sidp_ctx* c, int cls, cudaStream_t s) {
-  if (c->timed_class != cls || c->tev_used + 2 > (int)c->tev.size()) return;
+  if (!((c->timed_mask >> cls) & 1)) return;
+  if (c->tev_used + 2 > (int)c->tev.size()) timing_flush(c);
   cudaEventRecord(c->tev[c->tev_used], s);
 }
 void timing_end(sidp_ctx* c, int cls, cudaStream_t s) {
-  if (c->timed_class != cls || c->tev_used + 2 > (int)c->tev.size()) return;
+  if (!((c->timed_mask >> cls) & 1)) return;
   cudaEventRecord(c->tev[c->tev_used + 1], s);
+  c->tev_cls[c->tev_used / 2] = cls;
   c->tev_used += 2;
-  c->st.timed_launches++;
+  c->st.timed_launches[cls]++;
+}
+// Accumulate recorded pairs (synchronises on them) and recycle the pool.
+void timing_flush(sidp_ctx* c) {
+  for (int i = 0; i + 1 < c->tev_used; i += 2) {
+    float ms = 0.0f;
+    cudaEventSynchronize(c->tev[i + 1]);
+    if (cudaEventElapsedTime(&ms, c->tev[i], c->tev[i + 1]) == cudaSuccess)
+      c->timed_acc_ms[c->tev_cls[i / 2]] += ms;
+  }
+  c->tev_used = 0;
 }
 
 struct LayerW {
@@ -986,7 +1000,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
     count_launch(ctx);
     CK(gemm(ctx, 7, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_ARGMAX, ctx->amax,
             0, nullptr, 0, nullptr, s));
-    CK(sidp::argmax_finalize_launch(ctx->amax, b->next, B, s));
+    CK(sidp::argmax_finalize_launch(ctx->amax, b->next, b->pos_out, b->kv.pos, B, s));
     count_launch(ctx);
     if (b->logits) {
       CK(gemm(ctx, 0, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_F32, b->logits,
@@ -1091,33 +1105,28 @@ sidp_status sidp_stats(const sidp_ctx* ctx_c, sidp_stats_t* out) {
     int err = 0;
     if (cudaMemcpy(&err, ctx->dev_err, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && err)
       ctx->st.timeouts = err;
-    if (ctx->tev_used > 0) {
-      for (int i = 0; i + 1 < ctx->tev_used; i += 2) {
-        float ms = 0.0f;
-        cudaEventSynchronize(ctx->tev[i + 1]);
-        if (cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]) == cudaSuccess)
-          ctx->timed_acc_ms += ms;
-      }
-      ctx->tev_used = 0;
-    }
+    if (ctx->tev_used > 0) timing_flush(ctx);
   }
-  ctx->st.timed_ms = ctx->timed_acc_ms;
+  for (int i = 0; i < 8; ++i) ctx->st.timed_ms[i] = ctx->timed_acc_ms[i];
   *out = ctx->st;
   return SIDP_OK;
 }
 
-sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t kernel_class) {
+sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t class_mask) {
   if (!ctx) return fail(SIDP_EINVAL, "null ctx");
   sidp_status st = check_ready(ctx);
   if (st != SIDP_OK) return st;
   if (ctx->tev.empty()) {
     ctx->tev.resize(kTimingPool);
+    ctx->tev_cls.resize(kTimingPool / 2);
     for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
   }
-  ctx->timed_class = kernel_class;
+  ctx->timed_mask = class_mask;
   ctx->tev_used = 0;
-  ctx->timed_acc_ms = 0.0;
-  ctx->st.timed_launches = 0;
+  for (int i = 0; i < 8; ++i) {
+    ctx->timed_acc_ms[i] = 0.0;
+    ctx->st.timed_launches[i] = 0;
+  }
   return SIDP_OK;
 }
 

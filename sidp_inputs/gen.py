@@ -20,6 +20,8 @@ layouts are permutations of these logical arrays.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 # ---- tensor ids (logical tensors of the model and workload) ----
@@ -87,12 +89,23 @@ def weight(seed: int, tensor: int, layer: int, n_rows: int, K: int, rows=None) -
     """Logical weight W[N, K] (row-major logical index n*K + k); optionally a row subset."""
     rows = np.arange(n_rows, dtype=np.uint64) if rows is None else np.asarray(rows, dtype=np.uint64)
     out = np.empty((rows.shape[0], K), dtype=np.float64)
-    step = max(1, (1 << 22) // K)          # bounded temporaries for big layers
+    step = max(1, (1 << 20) // K)          # bounded temporaries for big layers
     cols = np.arange(K, dtype=np.uint64)[None, :]
-    for i in range(0, rows.shape[0], step):
+    scale = weight_scale(K)
+
+    def fill(i):
         idx = rows[i:i + step, None] * np.uint64(K) + cols
-        out[i:i + step] = _levels(hash_u64(seed, tensor, layer, idx))
-    return out * weight_scale(K)
+        out[i:i + step] = _levels(hash_u64(seed, tensor, layer, idx)) * scale
+
+    starts = range(0, rows.shape[0], step)
+    if rows.shape[0] * K >= (1 << 23):     # numpy ufuncs release the GIL: chunk over threads
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for i in starts:
+            fill(i)
+    return out
 
 
 def gain(seed: int, tensor: int, layer: int, n: int) -> np.ndarray:
