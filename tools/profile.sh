@@ -1,0 +1,14 @@
+#!/bin/bash
+# Run on the GPU box (gpurun): launch list of the bench command + ncu --set full captures of the
+# top kernels.  Outputs under gpurun_out/.
+set -x
+mkdir -p gpurun_out
+B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
+   --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
+S="python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e --no-cpu-baseline"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 8 -c 1 \
+   -o gpurun_out/prof_attn $S > gpurun_out/ncu_attn.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm2_kernel -s 32 -c 5 \
+   -o gpurun_out/prof_gemm $S > gpurun_out/ncu_gemm.log 2>&1
+ls -la gpurun_out
