@@ -41,6 +41,7 @@ struct GemmWorkspace {
 
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t s);
 int gemm_pick_splits(int tiles, int nkb, int sms);
+int gemm_last_launch_count();   // kernels enqueued by the last gemm_launch on this thread
 
 // ---------------------------------------------------------------- element-wise / small kernels
 cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf16* y, int ldy,
@@ -69,6 +70,7 @@ struct AttnArgs {
   float* ws; size_t ws_bytes; // split-KV partials
 };
 cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s);
+int attention_last_launch_count();
 
 // next[b] = decoded argmax; if pos_out: pos_out[b] = pos[b] + 1 (may alias pos)
 cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next,

@@ -332,6 +332,7 @@ __global__ void attn_combine_kernel(const float* ws, bf16* o, int nq, int splits
 }
 
 int g_sms = 0;
+thread_local int g_attn_launches = 0;
 
 }  // namespace
 
@@ -341,6 +342,8 @@ cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s) {
   qkv_post_kernel<<<a.B, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
+
+int attention_last_launch_count() { return g_attn_launches; }
 
 cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
   if (a.B <= 0) return cudaSuccess;
@@ -379,7 +382,9 @@ cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
   else
     attn_kernel<64><<<grid, 128, smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
+  g_attn_launches = 1;
   if (e != cudaSuccess || splits == 1) return e;
+  g_attn_launches = 2;
   if (a.hd == 128)
     attn_combine_kernel<128><<<a.B * a.nq, 128, 0, s>>>(a.ws, a.o, a.nq, splits);
   else

@@ -507,6 +507,7 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
 }
 
 int g_num_sms = 0;
+thread_local int g_last_launches = 0;
 
 template <int EPI>
 void set_attr() {
@@ -534,7 +535,10 @@ int gemm_pick_splits(int tiles, int nkb, int slots) {
   return best;
 }
 
+int gemm_last_launch_count() { return g_last_launches; }
+
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t stream) {
+  g_last_launches = 0;
   if (a.M <= 0) return cudaSuccess;
   if (a.K % BK != 0 || a.N <= 0 || a.N % 8 != 0 || a.x == nullptr || a.w == nullptr)
     return cudaErrorInvalidValue;
@@ -593,7 +597,9 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     default: return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaGetLastError();
+  g_last_launches = 1;
   if (e != cudaSuccess || splits == 1) return e;
+  g_last_launches = 2;
   const int n_out = a.epi == EPI_SILU_MUL ? a.N / 2 : a.N;
   const size_t vecs = (size_t)a.M * (n_out / 8);
   const int rgrid = (int)std::min<size_t>((vecs + 255) / 256, (size_t)g_num_sms * 8);

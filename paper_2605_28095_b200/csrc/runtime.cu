@@ -272,7 +272,7 @@ cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, in
   timing_begin(c, cls, s);
   cudaError_t e = sidp::gemm_launch(a, gws(c), s);
   timing_end(c, cls, s);
-  count_launch(c);
+  count_launch(c, sidp::gemm_last_launch_count());
   return e;
 }
 
@@ -306,7 +306,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   timing_begin(ctx, 2, s);
   CK(sidp::attention_launch(aa, s));
   timing_end(ctx, 2, s);
-  count_launch(ctx);
+  count_launch(ctx, sidp::attention_last_launch_count());
   return SIDP_OK;
 }
 
