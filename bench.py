@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=8)
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="all ranks on cuda:0 with a gloo control plane (functional multi-process "
+                         "test of the IPC path on a 1-GPU box; not a scaling number)")
     return ap.parse_args()
 
 
@@ -281,11 +284,16 @@ def main():
     import torch
     import paper_2605_28095_b200 as P
     from sidp_inputs import gen
+    if args.share_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch or wl.batch
     ctx_len = args.ctx or wl.ctx
     slots = args.slots or wl.slots
@@ -303,9 +311,8 @@ def main():
         kv.fill_synthetic(seed, rank * B, B, ctx_len, stream=stream)
     stream.synchronize()
     if world > 1:
-        blobs = [None] * world
-        dist.all_gather_object(blobs, ctx.export_handles())
-        ctx.import_handles(blobs)
+        from paper_2605_28095_b200.orchestrator import exchange_handles
+        exchange_handles(ctx, dist)
         dist.barrier()
     bg = np.arange(rank * B, rank * B + B)
     kv.set_pos(np.full(B, ctx_len))
@@ -350,13 +357,9 @@ def main():
     launches = st["launches"] - launches0
     dom_ms = st["timed_ms"][dom] / max(1, st["timed_launches"][dom])
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if args.share_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        if dist.get_rank() == 0:
-            all_clk = [None] * world
-        else:
-            all_clk = None
         gathered = [None] * world
         dist.all_gather_object(gathered, clocks)
         clocks = dict(gathered[0])
@@ -386,7 +389,7 @@ def main():
         t1 = time.perf_counter()
         e_ms = (t1 - t0) * 1e3
         if dist:
-            t = torch.tensor([e_ms], device="cuda")
+            t = torch.tensor([e_ms], device="cpu" if args.share_gpu else "cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": B * world * e2e_steps / (e_ms / 1e3), "unit": UNIT,

@@ -1,0 +1,151 @@
+"""Real multi-process SiDP group on ONE GPU: two processes (gloo control plane) exchange CUDA IPC
+handles, run WaS (peer arena fetches across processes) and CaS (cross-process staging + flags).
+This exercises the exact N>1 data path except NVLink bandwidth (both ranks share cuda:0).
+
+WaS logits must be BITWISE equal to a single-process replicated run; CaS within tolerance.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+SEED = 20261019
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run_rank(rank, world, port, mode, pool, batches, steps, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2605_28095_b200 as P
+        from paper_2605_28095_b200.orchestrator import exchange_handles
+        from sidp_inputs import MODELS, gen
+        torch.cuda.set_device(0)
+        m = MODELS["tiny"].with_layers(8)
+        B = batches[rank]
+        mb, max_ctx = max(batches), 80
+        b0 = sum(batches[:rank])
+        ctx = P.Context(m, rank=rank, world=world, max_batch=mb, max_ctx=max_ctx, seed=SEED,
+                        pool=pool, slots=2)
+        ctx.init_weights_synthetic()
+        kv = P.KVCache(m, mb, max_ctx)
+        kv.fill_synthetic(SEED, b0, mb, max_ctx)
+        bg = np.arange(b0, b0 + B)
+        pos = gen.positions(SEED, bg, 0, 63)
+        kv.set_pos(pos if B else [0])
+        toks = torch.from_numpy(gen.tokens(SEED, bg, m.vocab)).to(torch.int32).cuda()
+        nxt = torch.zeros(mb, dtype=torch.int32, device="cuda")
+        logits = torch.zeros(mb, m.vocab, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        exchange_handles(ctx, dist)
+        if mode == "cas":
+            ctx.set_batches(batches)
+            ctx.set_mode(1, 0)
+        dist.barrier()
+        out = []
+        for s in range(steps):
+            ctx.step(toks, nxt, kv, batch=B, logits=logits)
+            torch.cuda.synchronize()
+            out.append((nxt[:B].cpu().numpy().copy(), logits[:B].cpu().numpy().copy()))
+            if B:
+                toks = nxt[:B].clone()
+                kv.advance(1, B)
+        st = ctx.stats()
+        log = ctx.fetch_log()
+        dist.barrier()
+        ctx.destroy()
+        q.put((rank, out, st["timeouts"], log))
+    finally:
+        dist.destroy_process_group()
+
+
+def _replicated(batches, r, steps, pool):
+    import paper_2605_28095_b200 as P
+    from sidp_inputs import MODELS, gen
+    m = MODELS["tiny"].with_layers(8)
+    B, mb, b0 = batches[r], max(batches), sum(batches[:r])
+    ctx = P.Context(m, rank=0, world=1, max_batch=mb, max_ctx=80, seed=SEED, pool=pool)
+    ctx.init_weights_synthetic()
+    kv = P.KVCache(m, mb, 80)
+    kv.fill_synthetic(SEED, b0, mb, 80)
+    bg = np.arange(b0, b0 + B)
+    kv.set_pos(gen.positions(SEED, bg, 0, 63))
+    toks = torch.from_numpy(gen.tokens(SEED, bg, m.vocab)).to(torch.int32).cuda()
+    nxt = torch.zeros(mb, dtype=torch.int32, device="cuda")
+    logits = torch.zeros(mb, m.vocab, dtype=torch.float32, device="cuda")
+    out = []
+    for s in range(steps):
+        ctx.step(toks, nxt, kv, batch=B, logits=logits)
+        torch.cuda.synchronize()
+        out.append((nxt[:B].cpu().numpy().copy(), logits[:B].cpu().numpy().copy()))
+        toks = nxt[:B].clone()
+        kv.advance(1, B)
+    ctx.destroy()
+    return out
+
+
+def _launch(mode, pool, batches, steps):
+    world = len(batches)
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_run_rank, args=(r, world, port, mode, pool, batches, steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, timeouts, log = q.get(timeout=300)
+        res[r] = (out, timeouts, log)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("pool", ["layer", "ffn"])
+def test_was_two_processes_ipc(pool):
+    from oracle import schedule as OS
+    batches = [3, 5]
+    res = _launch("was", pool, batches, 3)
+    own = OS.owner_map(8, 2)
+    for r in range(2):
+        out, timeouts, log = res[r]
+        ref = _replicated(batches, r, 3, pool)
+        for s in range(3):
+            assert np.array_equal(out[s][1], ref[s][1]), (r, s)      # bitwise: verbatim fetch
+            assert np.array_equal(out[s][0], ref[s][0])
+        full = OS.slot_schedule(OS.plan_exec(own, r), 2, 4)
+        assert [tuple(x) for x in log] == full[:len(log)]
+
+
+@pytest.mark.parametrize("pool", ["layer", "ffn"])
+@pytest.mark.parametrize("batches", [[3, 5], [4, 0]])
+def test_cas_two_processes_ipc(pool, batches):
+    res = _launch("cas", pool, batches, 2)
+    for r in range(2):
+        out, timeouts, _ = res[r]
+        assert timeouts == 0
+        if batches[r] == 0:
+            continue
+        ref = _replicated(batches, r, 2, pool)
+        for s in range(2):
+            got, exp = out[s][1], ref[s][1]
+            err = np.abs(got - exp).max() / np.abs(exp).max()
+            assert err <= 1e-2, (r, s, err)
