@@ -3,7 +3,7 @@
 // WaS fetch ("non-owner issues non-blocking device-to-device copies from
 // r(l)'s HBM into its local cache"): a verbatim copy of one packed pooled layer from the
 // owner's arena (a peer VA imported over CUDA IPC, NVLink/NVSwitch) into a local slot.
-// SM-issued, coalesced 16-byte loads with 4 loads in flight per thread before the stores
+// SM-issued, coalesced 16-byte loads with 8 loads in flight per thread before the stores
 // (L1::no_allocate: streamed once), on a bounded number of CTAs so the concurrently
 // running GEMMs keep the rest of the SMs.
 #include "../common.cuh"
@@ -26,7 +26,7 @@ __device__ __forceinline__ void st_na_v4(uint4* p, const uint4& v) {
                : "memory");
 }
 
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;   // 128 B in flight per thread (NVLink peer latency ~2 us)
 
 __global__ void __launch_bounds__(512) fetch_kernel(uint4* __restrict__ dst,
                                                     const uint4* __restrict__ src, size_t nvec) {

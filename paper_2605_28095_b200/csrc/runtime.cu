@@ -42,6 +42,11 @@ enum Comp { C_WQKV = 0, C_WO, C_WGU, C_WD, C_GATTN, C_GMLP, C_GQ, C_GK, C_BQKV, 
 constexpr uint32_t kMagic = 0x53694450;  // "SiDP"
 constexpr int kTimingPool = 8192;
 
+struct GraphKey {
+  int batch;
+  const void *tokens, *next, *k_cache, *v_cache, *pos, *pos_out;
+};
+
 struct HandleBlob {
   uint32_t magic;
   int32_t rank;
@@ -114,6 +119,15 @@ struct sidp_ctx {
   // stats + timing
   sidp_stats_t st{};
   int timed_mask = 0;
+  // CUDA graph of an all-local step
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{};
+  int gmask = -1;
+  bool capturing = false;
+  uint64_t graph_launches = 0;
+  int graph_tev_pairs = 0;
+  bool graph_timed_pending = false;
+  uint64_t graph_timed_count[8]{};
   std::vector<cudaEvent_t> tev;
   std::vector<int> tev_cls;
   int tev_used = 0;
@@ -220,6 +234,7 @@ int stagger_ticks_of(const sidp_ctx* c) {
 }
 
 void count_launch(sidp_ctx* c, int n = 1) { c->st.launches += n; }
+void graph_harvest(sidp_ctx* c);
 
 // ---- optional per-class kernel timing ----
 void timing_flush(sidp_ctx* c);
@@ -235,15 +250,30 @@ void timing_end(sidp_ctx* c, int cls, cudaStream_t s) {
   c->tev_used += 2;
   c->st.timed_launches[cls]++;
 }
-// Accumulate recorded pairs (synchronises on them) and recycle the pool.
+// Graph replays re-record the same captured event pairs: accumulate them after each replay.
+void graph_harvest(sidp_ctx* c) {
+  for (int i = 0; i < c->graph_tev_pairs; ++i) {
+    float ms = 0.0f;
+    cudaEventSynchronize(c->tev[2 * i + 1]);
+    if (cudaEventElapsedTime(&ms, c->tev[2 * i], c->tev[2 * i + 1]) == cudaSuccess)
+      c->timed_acc_ms[c->tev_cls[i]] += ms;
+  }
+  for (int k = 0; k < 8; ++k) c->st.timed_launches[k] += c->graph_timed_count[k];
+  c->graph_timed_pending = false;
+}
+
+// Accumulate recorded pairs (synchronises on them) and recycle the pool.  Pairs owned by a
+// live graph (the first graph_tev_pairs) are harvested per replay instead.
 void timing_flush(sidp_ctx* c) {
-  for (int i = 0; i + 1 < c->tev_used; i += 2) {
+  const int first = c->gexec ? 2 * c->graph_tev_pairs : 0;
+  if (c->gexec && c->graph_timed_pending) graph_harvest(c);
+  for (int i = first; i + 1 < c->tev_used; i += 2) {
     float ms = 0.0f;
     cudaEventSynchronize(c->tev[i + 1]);
     if (cudaEventElapsedTime(&ms, c->tev[i], c->tev[i + 1]) == cudaSuccess)
       c->timed_acc_ms[c->tev_cls[i / 2]] += ms;
   }
-  c->tev_used = 0;
+  c->tev_used = first;
 }
 
 struct LayerW {
@@ -302,7 +332,9 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   sidp::AttnArgs aa{};
   aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.pos = kv->pos; aa.o = ctx->o; aa.B = B;
   aa.nq = m.n_q_heads; aa.nkv = m.n_kv_heads; aa.hd = m.head_dim; aa.smax = ctx->c.max_ctx;
-  aa.max_tokens = kv->max_pos + 1; aa.ws = ctx->attn_ws; aa.ws_bytes = ctx->attn_ws_bytes;
+  // the split is sized from max_ctx (not the per-step max_pos) so the launch configuration is
+  // step-invariant and a captured CUDA graph stays valid; empty splits exit immediately
+  aa.max_tokens = ctx->c.max_ctx; aa.ws = ctx->attn_ws; aa.ws_bytes = ctx->attn_ws_bytes;
   timing_begin(ctx, 2, s);
   CK(sidp::attention_launch(aa, s));
   timing_end(ctx, 2, s);
@@ -679,6 +711,7 @@ void sidp_destroy(sidp_ctx* ctx) {
   if (ctx->allocated) {
     cudaSetDevice(ctx->c.device);
     cudaDeviceSynchronize();
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     for (auto e : ctx->ready_ev) cudaEventDestroy(e);
     for (auto e : ctx->free_ev) cudaEventDestroy(e);
@@ -956,6 +989,68 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
   return fail(SIDP_EINVAL, "bad mode %d", mode);
 }
 
+// Body of one decode step (enqueue only).
+static sidp_status step_body(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s) {
+  const int B = b->batch;
+  const auto& m = ctx->m;
+  sidp_status st;
+  bf16* x = ctx->xbuf;
+  if (B > 0) {
+    CK(sidp::embed_launch(ctx->embed, m.hidden, b->tokens, x, B, s));
+    count_launch(ctx);
+  }
+  const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
+  for (int l = 0; l < ctx->L; ++l) {
+    if (b->layer_inputs && B > 0) {
+      CK(cudaMemcpyAsync(reinterpret_cast<bf16*>(b->layer_inputs) + (size_t)l * B * m.hidden, x,
+                         (size_t)B * m.hidden * 2, cudaMemcpyDeviceToDevice, s));
+    }
+    st = sidp_decode_layer(ctx, x, B, l, mode, &b->kv, s);
+    if (st != SIDP_OK) return st;
+  }
+  if (B > 0) {
+    CK(sidp::rmsnorm_launch(x, m.hidden, ctx->g_final, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+    count_launch(ctx);
+    CK(sidp::argmax_reset_launch(ctx->amax, B, s));
+    count_launch(ctx);
+    CK(gemm(ctx, 7, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_ARGMAX, ctx->amax,
+            0, nullptr, 0, nullptr, s));
+    CK(sidp::argmax_finalize_launch(ctx->amax, b->next, b->pos_out, b->kv.pos, B, s));
+    count_launch(ctx);
+    if (b->logits) {
+      CK(gemm(ctx, 0, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_F32, b->logits,
+              m.vocab, nullptr, 0, nullptr, s));
+    }
+  }
+  return SIDP_OK;
+}
+
+// CUDA graphs (launch-bound inner loop: ~700 kernels per step).  A step is replayable when it
+// touches no WaS ring (every layer local) and its pointers / batch / timing mask are unchanged;
+// kernel parameters never depend on the step index (positions live on the device).
+static bool graph_eligible(const sidp_ctx* ctx, const sidp_batch* b) {
+  static const bool enabled = !(getenv("SIDP_GRAPH") && atoi(getenv("SIDP_GRAPH")) == 0);
+  const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
+  return enabled && mode == SIDP_WAS && ctx->R == 0 && b->batch > 0 && !b->logits &&
+         !b->layer_inputs;
+}
+
+static void graph_drop(sidp_ctx* ctx) {
+  if (!ctx->gexec) return;
+  if (ctx->graph_timed_pending) graph_harvest(ctx);
+  cudaGraphExecDestroy(ctx->gexec);
+  ctx->gexec = nullptr;
+  ctx->graph_tev_pairs = 0;
+  ctx->tev_used = 0;
+}
+
+static bool graph_key_matches(const sidp_ctx* ctx, const sidp_batch* b) {
+  const auto& k = ctx->gkey;
+  return ctx->gexec && k.batch == b->batch && k.tokens == b->tokens && k.next == b->next &&
+         k.k_cache == b->kv.k_cache && k.v_cache == b->kv.v_cache && k.pos == b->kv.pos &&
+         k.pos_out == b->pos_out && ctx->gmask == ctx->timed_mask;
+}
+
 sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
   if (!ctx || !b) return fail(SIDP_EINVAL, "null argument");
   sidp_status st = check_ready(ctx);
@@ -978,35 +1073,48 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
     ctx->st.mode = ctx->mode;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const auto& m = ctx->m;
-  bf16* x = ctx->xbuf;
-  if (B > 0) {
-    CK(sidp::embed_launch(ctx->embed, m.hidden, b->tokens, x, B, s));
-    count_launch(ctx);
-  }
-  const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
-  for (int l = 0; l < ctx->L; ++l) {
-    if (b->layer_inputs && B > 0) {
-      CK(cudaMemcpyAsync(reinterpret_cast<bf16*>(b->layer_inputs) + (size_t)l * B * m.hidden, x,
-                         (size_t)B * m.hidden * 2, cudaMemcpyDeviceToDevice, s));
+  if (s != nullptr && graph_eligible(ctx, b)) {   // capture needs a non-default stream
+    if (!graph_key_matches(ctx, b)) {
+      graph_drop(ctx);
+      if (ctx->tev_used > 0) timing_flush(ctx);
+      const uint64_t l0 = ctx->st.launches;
+      uint64_t t0[8];
+      for (int i = 0; i < 8; ++i) t0[i] = ctx->st.timed_launches[i];
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      ctx->capturing = true;
+      st = step_body(ctx, b, s);
+      ctx->capturing = false;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(s, &g);
+      if (st != SIDP_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      CK(e);
+      CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+      cudaGraphDestroy(g);
+      ctx->graph_launches = ctx->st.launches - l0;
+      ctx->st.launches = l0;
+      ctx->gkey = GraphKey{B, b->tokens, b->next, b->kv.k_cache, b->kv.v_cache, b->kv.pos, b->pos_out};
+      ctx->gmask = ctx->timed_mask;
+      ctx->graph_tev_pairs = ctx->tev_used / 2;
+      ctx->graph_timed_pending = false;
+      for (int i = 0; i < 8; ++i) {
+        ctx->graph_timed_count[i] = ctx->st.timed_launches[i] - t0[i];
+        ctx->st.timed_launches[i] = t0[i];
+      }
     }
-    st = sidp_decode_layer(ctx, x, B, l, mode, &b->kv, stream);
-    if (st != SIDP_OK) return st;
+    // harvest the previous replay's kernel timings before the events are re-recorded
+    if (ctx->graph_timed_pending) graph_harvest(ctx);
+    CK(cudaGraphLaunch(ctx->gexec, s));
+    ctx->st.launches += ctx->graph_launches;
+    ctx->graph_timed_pending = ctx->graph_tev_pairs > 0;
+    ctx->step++;
+    ctx->st.steps++;
+    return SIDP_OK;
   }
-  if (B > 0) {
-    CK(sidp::rmsnorm_launch(x, m.hidden, ctx->g_final, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
-    count_launch(ctx);
-    CK(sidp::argmax_reset_launch(ctx->amax, B, s));
-    count_launch(ctx);
-    CK(gemm(ctx, 7, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_ARGMAX, ctx->amax,
-            0, nullptr, 0, nullptr, s));
-    CK(sidp::argmax_finalize_launch(ctx->amax, b->next, b->pos_out, b->kv.pos, B, s));
-    count_launch(ctx);
-    if (b->logits) {
-      CK(gemm(ctx, 0, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_F32, b->logits,
-              m.vocab, nullptr, 0, nullptr, s));
-    }
-  }
+  st = step_body(ctx, b, s);
+  if (st != SIDP_OK) return st;
   ctx->step++;
   ctx->st.steps++;
   return SIDP_OK;
@@ -1121,6 +1229,7 @@ sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t class_mask) {
     ctx->tev_cls.resize(kTimingPool / 2);
     for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
   }
+  graph_drop(ctx);
   ctx->timed_mask = class_mask;
   ctx->tev_used = 0;
   for (int i = 0; i < 8; ++i) {

@@ -241,3 +241,22 @@ def test_big_shapes_sampled_rows(P, name, B, ctx):
     ref = OM.lm_head(m, om.head, out)
     assert rel_err(logits[rows].double().numpy(), ref) <= TOL
     R.ctx.destroy()
+
+
+def test_cuda_graph_replay_matches_eager(P):
+    """An all-local step is captured once and replayed as a CUDA graph; the decoded tokens of
+    several replays equal an eager run (logits requested => no graph) bit for bit."""
+    m = MODELS["tiny"]
+    A = Rank(P, m, B=8, span=63, max_ctx=80)
+    Bq = Rank(P, m, B=8, span=63, max_ctx=80)
+    for s in range(4):
+        with torch.cuda.stream(A.stream):          # graph path: no logits / dumps
+            A.ctx.step(A.toks, A.toks, A.kv, batch=8, stream=A.stream, advance_pos=True)
+        A.stream.synchronize()
+        A.history.append(A.toks.clone().cpu())
+        Bq.step(); Bq.finish_step()                # eager path (logits requested)
+        assert torch.equal(A.history[-1], Bq.history[-1][0]), s
+    st = A.ctx.stats()
+    assert st["steps"] == 4 and st["launches"] > 4 * (1 + m.num_layers * 6)
+    A.ctx.destroy()
+    Bq.ctx.destroy()
