@@ -7,6 +7,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #define SIDP_DEV __device__ __forceinline__
 
@@ -157,6 +160,14 @@ SIDP_DEV uint64_t globaltimer_ns() {
   return t;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the decode chain are launched with programmatic stream serialization: a kernel
+// triggers its dependents early and waits (griddepcontrol.wait) for its predecessor's grid to
+// complete and flush before touching global data, so launch latency and prologues (barrier
+// init, TMEM alloc, descriptor prefetch) overlap the predecessor's tail.
+SIDP_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SIDP_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- small math
 SIDP_DEV float bf16_to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 SIDP_DEV __nv_bfloat16 f_to_bf16(float v) { return __float2bfloat16_rn(v); }
@@ -170,6 +181,27 @@ SIDP_DEV float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+inline bool pdl_enabled() {
+  static const int v = getenv("SIDP_PDL") ? atoi(getenv("SIDP_PDL")) : 1;
+  return v != 0;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace sidp

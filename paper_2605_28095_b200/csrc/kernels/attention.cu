@@ -21,6 +21,8 @@ namespace {
 
 // ---------------------------------------------------------------- qkv post
 __global__ void qkv_post_kernel(QkvPostArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int hd = a.hd, half = hd / 2;
@@ -127,6 +129,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int CPR = HD / 8;                         // 16-byte chunks per row
   constexpr int TILE = kChunk * HD;                   // elements per K (or V) chunk
+  pdl_trigger();
+  pdl_wait();
   const int g = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tq = lane & 3;
@@ -313,6 +317,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
 
 template <int HD>
 __global__ void attn_combine_kernel(const float* ws, bf16* o, int nq, int splits) {
+  pdl_trigger();
+  pdl_wait();
   const int bh = blockIdx.x;   // b * nq + head
   const float* part = ws + (size_t)bh * splits * (HD + 2);
   float M = -INFINITY;
@@ -339,8 +345,7 @@ thread_local int g_attn_launches = 0;
 cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s) {
   if (a.B <= 0) return cudaSuccess;
   if (a.hd != 64 && a.hd != 128) return cudaErrorInvalidValue;
-  qkv_post_kernel<<<a.B, 256, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(qkv_post_kernel, dim3(a.B), dim3(256), 0, s, a);
 }
 
 int attention_last_launch_count() { return g_attn_launches; }
@@ -377,19 +382,16 @@ cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.hd));
   dim3 grid(a.nkv, a.B, splits);
   const size_t smem = (size_t)kWarps * 4 * kChunk * a.hd * 2;
-  if (a.hd == 128)
-    attn_kernel<128><<<grid, 128, smem, s>>>(p);
-  else
-    attn_kernel<64><<<grid, 128, smem, s>>>(p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = a.hd == 128 ? launch_pdl(attn_kernel<128>, grid, dim3(128), smem, s, p)
+                              : launch_pdl(attn_kernel<64>, grid, dim3(128), smem, s, p);
   g_attn_launches = 1;
   if (e != cudaSuccess || splits == 1) return e;
   g_attn_launches = 2;
-  if (a.hd == 128)
-    attn_combine_kernel<128><<<a.B * a.nq, 128, 0, s>>>(a.ws, a.o, a.nq, splits);
-  else
-    attn_combine_kernel<64><<<a.B * a.nq, 64, 0, s>>>(a.ws, a.o, a.nq, splits);
-  return cudaGetLastError();
+  const float* wsc = a.ws;
+  bf16* oc = a.o;
+  const int nq = a.nq;
+  return a.hd == 128 ? launch_pdl(attn_combine_kernel<128>, dim3(a.B * a.nq), dim3(128), 0, s, wsc, oc, nq, splits)
+                     : launch_pdl(attn_combine_kernel<64>, dim3(a.B * a.nq), dim3(64), 0, s, wsc, oc, nq, splits);
 }
 
 }  // namespace sidp

@@ -39,8 +39,10 @@ struct KParams {
   int M, N, K;
   int BNT;                      // token tile (UMMA N), multiple of 32, <= 256
   int stages;
-  int splits, kb_per_split;
-  int m_tiles, n_pairs, units;
+  int m_tiles, n_pairs, tiles;
+  int streamk;                  // 1: k-block ranges split evenly over clusters; 0: whole tiles
+  long long total_kb;           // tiles * nkb
+  int clusters;                 // concurrent CTA pairs (fixed per launch configuration)
   void* out; int ldo;
   const bf16* resid; int ldr;
   const bf16* bias;
@@ -103,6 +105,63 @@ SIDP_DEV void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
                : "memory");
 }
+
+// ---- work decomposition ---------------------------------------------------------
+// Stream-K: the tiles*nkb k-blocks (tile-major, tokens fastest within a feature tile so W
+// tiles are re-read from L2 across token tiles) are split into `clusters` equal contiguous
+// ranges; cluster c owns [b_c, b_{c+1}), b_c = floor(c * total / C).  A range crossing tile
+// boundaries yields several units; a tile covered by one unit is finished in the GEMM
+// epilogue, otherwise each covering unit writes its fp32 partial to slice `seg` and
+// gemm_reduce_kernel sums slices 0..nseg-1 in order (deterministic: depends only on shapes
+// and C).  Whole-tile mode (fused argmax) walks tiles round-robin.
+SIDP_DEV int cluster_of_kb(long long g, long long total, int C) {
+  return (int)(((g + 1) * (long long)C + total - 1) / total) - 1;
+}
+__host__ __device__ inline long long range_begin(int c, long long total, int C) {
+  return (long long)c * total / C;
+}
+
+struct Unit {
+  int ft, mt, kb0, kb1, seg, nseg;
+};
+
+struct UnitIter {
+  long long g, end;   // stream-K cursor
+  int u;              // whole-tile cursor
+  SIDP_DEV void init(const KParams& p, int cluster) {
+    g = range_begin(cluster, p.total_kb, p.clusters);
+    end = range_begin(cluster + 1, p.total_kb, p.clusters);
+    u = cluster;
+  }
+  SIDP_DEV bool next(const KParams& p, int cluster, Unit& x) {
+    const int nkb = p.K / 64;
+    int t;
+    if (p.streamk) {
+      if (g >= end) return false;
+      t = (int)(g / nkb);
+      const long long tile_end = (long long)(t + 1) * nkb;
+      const long long seg_end = end < tile_end ? end : tile_end;
+      x.kb0 = (int)(g - (long long)t * nkb);
+      x.kb1 = x.kb0 + (int)(seg_end - g);
+      const int first = cluster_of_kb((long long)t * nkb, p.total_kb, p.clusters);
+      const int last = cluster_of_kb(tile_end - 1, p.total_kb, p.clusters);
+      x.seg = cluster - first;
+      x.nseg = last - first + 1;
+      g = seg_end;
+    } else {
+      if (u >= p.tiles) return false;
+      t = u;
+      u += p.clusters;
+      x.kb0 = 0;
+      x.kb1 = nkb;
+      x.seg = 0;
+      x.nseg = 1;
+    }
+    x.mt = t % p.m_tiles;
+    x.ft = t / p.m_tiles;
+    return true;
+  }
+};
 
 SIDP_DEV unsigned long long argmax_key(float v, int n) {
   uint32_t u = __float_as_uint(v);
@@ -262,16 +321,19 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: let the next kernel of the chain launch, then wait for our inputs
+  pdl_trigger();
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int it = 0;
-      for (int u = cluster; u < p.units; u += n_clusters) {
-        const int ks = u % p.splits, rest = u / p.splits;
-        const int mt = rest % p.m_tiles, ft = rest / p.m_tiles;
-        const int kb0 = ks * p.kb_per_split, kb1 = min(nkb, kb0 + p.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+      UnitIter ui;
+      ui.init(p, cluster);
+      Unit x;
+      while (ui.next(p, cluster, x)) {
+        for (int kb = x.kb0; kb < x.kb1; ++kb, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -283,8 +345,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           // Only the leader arrives (expecting both CTAs' bytes); the peer's TMA completes its
           // transaction bytes on the leader's barrier directly — no per-stage remote arrive.
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
-          tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes, kb * BK, ft * 2 * WROWS + rank * WROWS);
-          tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes, kb * BK, mt * BNT + rank * HALF);
+          tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes, kb * BK, x.ft * 2 * WROWS + rank * WROWS);
+          tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes, kb * BK, x.mt * BNT + rank * HALF);
         }
       }
     }
@@ -292,16 +354,18 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     // ------------------------------------------------------------ MMA issuer (leader only)
     if (leader) {
       const uint32_t idesc = umma_idesc_bf16(2 * WROWS, BNT);
-      int it = 0, ui = 0;
-      for (int u = cluster; u < p.units; u += n_clusters, ++ui) {
-        const int ks = u % p.splits;
-        const int kb0 = ks * p.kb_per_split, kb1 = min(nkb, kb0 + p.kb_per_split);
-        const int acc = ui & 1;
-        const uint32_t aph = (ui >> 1) & 1;
+      int it = 0, un = 0;
+      UnitIter ui;
+      ui.init(p, cluster);
+      Unit x;
+      while (ui.next(p, cluster, x)) {
+        const int acc = un & 1;
+        const uint32_t aph = (un >> 1) & 1;
+        ++un;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem_base + acc * BNT;
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int kb = x.kb0; kb < x.kb1; ++kb, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(&full[s], ph);
@@ -315,7 +379,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               umma2_bf16(dcol, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                         (kb > kb0 || k > 0) ? 1u : 0u);
+                         (kb > x.kb0 || k > 0) ? 1u : 0u);
             umma2_commit_mc(&empty[s]);
           }
           __syncwarp();
@@ -329,56 +393,38 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int quarter = warp & 3;                       // TMEM lane quarter of this warp
     const int row = quarter * 32 + lane;                // W row within this CTA (feature)
     const int tid = (warp - 2) * 32 + lane;             // 0..127
-    int ui = 0;
-    for (int u = cluster; u < p.units; u += n_clusters, ++ui) {
-      const int ks = u % p.splits, rest = u / p.splits;
-      const int mt = rest % p.m_tiles, ft = rest / p.m_tiles;
-      const int acc = ui & 1;
-      const uint32_t aph = (ui >> 1) & 1;
-      const int n0 = ft * 2 * WROWS + rank * WROWS;
-      const int pt = ft * 2 + rank;
-      const int mbase = mt * BNT;
+    int un = 0;
+    UnitIter ui;
+    ui.init(p, cluster);
+    Unit x;
+    while (ui.next(p, cluster, x)) {
+      const int acc = un & 1;
+      const uint32_t aph = (un >> 1) & 1;
+      ++un;
+      const int n0 = x.ft * 2 * WROWS + rank * WROWS;
+      const int pt = x.ft * 2 + rank;
+      const int mbase = x.mt * BNT;
       const int nchunks = min(BNT, ((p.M - mbase + 31) / 32) * 32) / 32;
+      float* part = p.ws + (size_t)x.seg * p.M * p.N;   // partial slice (nseg > 1 only)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tl = tmem_base + acc * BNT + ((uint32_t)(quarter * 32) << 16);
-      if (p.splits == 1) {
-        for (int c = 0; c < nchunks; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tl + c * 32, r);
-          tmem_ld_wait();
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tl + c * 32, r);
+        tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
-          if (c == nchunks - 1) {   // last TMEM read of this accumulator: hand it back early
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-          }
-          named_bar_sync(1, 128);
-          store_phase<EPI>(p, stg, mbase + c * 32, n0, pt, tid);
-          named_bar_sync(1, 128);
-        }
-        if (nchunks == 0) {
+        for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
+        if (c == nchunks - 1) {   // last TMEM read of this accumulator: hand it back early
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
-      } else {
-        // split-K: fp32 partial of this k-slice -> ws[ks][m][n] (token-major, coalesced);
-        // gemm_reduce_kernel sums the slices in order 0..S-1 and runs the epilogue.
-        float* part = p.ws + (size_t)ks * p.M * p.N;
-        for (int c = 0; c < nchunks; ++c) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tl + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
-          if (c == nchunks - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-          }
-          named_bar_sync(1, 128);
+        named_bar_sync(1, 128);
+        if (x.nseg == 1) {
+          store_phase<EPI>(p, stg, mbase + c * 32, n0, pt, tid);
+        } else {
+          // partial of this k-range -> ws[seg][m][n] (token-major, coalesced 16-byte stores)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
@@ -387,13 +433,13 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
               __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N + n),
                      *reinterpret_cast<const float4*>(stg + j * SROW + f));
           }
-          named_bar_sync(1, 128);
         }
-        if (nchunks == 0) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-        }
+        named_bar_sync(1, 128);
+      }
+      if (nchunks == 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
       }
     }
   }
@@ -406,18 +452,35 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   }
 }
 
-// Split-K reduction + epilogue over all SMs: each thread sums 8 consecutive outputs of one
-// token row across the S fp32 slices in order 0..S-1 (deterministic), then applies EPI.
+// Stream-K fix-up over all SMs: for tiles covered by several k-range segments, each thread sums
+// 8 consecutive outputs of one token row across the segment slices in order 0..nseg-1
+// (deterministic), then applies EPI.  Tiles finished inside the GEMM are skipped.
 template <int EPI>
 __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
+  pdl_trigger();
+  pdl_wait();
+  // blockIdx.y = cluster boundary c (1..C-1); the tile containing b_c strictly inside is fixed
+  // up by the block row of the first boundary that splits it.
+  const long long nkb = p.K / 64;
+  const int c = blockIdx.y + 1;
+  const long long bc = range_begin(c, p.total_kb, p.clusters);
+  const int t = (int)(bc / nkb);
+  if (bc % nkb == 0) return;                                  // boundary on a tile edge
+  if (c > 1 && range_begin(c - 1, p.total_kb, p.clusters) > (long long)t * nkb) return;
+  const int nseg = cluster_of_kb((long long)(t + 1) * nkb - 1, p.total_kb, p.clusters) -
+                   cluster_of_kb((long long)t * nkb, p.total_kb, p.clusters) + 1;
+  const int mt = t % p.m_tiles, ft = t / p.m_tiles;
+  const int m0 = mt * p.BNT, rows = min(p.BNT, p.M - m0);
+  const int tile_out = EPI == EPI_SILU_MUL ? 2 * WROWS / 2 : 2 * WROWS;   // outputs per row
+  const int out0 = EPI == EPI_SILU_MUL ? ft * WROWS : ft * 2 * WROWS;
   const int n_out = EPI == EPI_SILU_MUL ? p.N / 2 : p.N;
-  const int vec_per_row = n_out / 8;
-  const size_t total = (size_t)p.M * vec_per_row;
+  const int vec_per_row = tile_out / 8;
   const size_t slice = (size_t)p.M * p.N;
-  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const int m = (int)(idx / vec_per_row);
-    const int f = (int)(idx % vec_per_row) * 8;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < rows * vec_per_row;
+       idx += gridDim.x * blockDim.x) {
+    const int m = m0 + idx / vec_per_row;
+    const int f = out0 + (idx % vec_per_row) * 8;
+    if (f >= n_out) continue;
     float a[8], b[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) a[q] = b[q] = 0.0f;
@@ -428,7 +491,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
     }
     const float* base = p.ws + (size_t)m * p.N;
 #pragma unroll 4
-    for (int s = 0; s < p.splits; ++s) {
+    for (int s = 0; s < nseg; ++s) {
       const float4 x0 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + na));
       const float4 x1 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + na + 4));
       a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
@@ -562,13 +625,19 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   const int m_tiles = (a.M + BNT - 1) / BNT;
   const int n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
   const int nkb = a.K / BK;
-  int splits = a.k_splits > 0 ? a.k_splits : gemm_pick_splits(n_pairs * m_tiles, nkb, pair_slots);
-  splits = std::max(1, std::min(splits, nkb));
-  if (a.epi == EPI_ARGMAX) splits = 1;                    // fused argmax needs whole dot products
-  while (splits > 1 && (size_t)splits * a.M * a.N * 4 > w.ws_bytes) --splits;
-  int kb_per = (nkb + splits - 1) / splits;
-  splits = (nkb + kb_per - 1) / kb_per;                   // no empty split
-  const int units = n_pairs * m_tiles * splits;
+  const int tiles = n_pairs * m_tiles;
+  // stream-K over all pairs unless the epilogue needs whole dot products (fused argmax) or the
+  // caller pins whole tiles (k_splits == 1); max segments per tile bounds the workspace
+  int clusters = pair_slots;
+  int streamk = (a.epi != EPI_ARGMAX && a.k_splits != 1 && tiles % clusters != 0) ? 1 : 0;
+  if (streamk) {
+    const long long total = (long long)tiles * nkb;
+    const long long per = total / clusters;
+    if (per < 2) clusters = (int)std::max<long long>(1, total / 2);   // tiny problems
+    const int max_seg = (int)((nkb + per - 1) / std::max<long long>(per, 1)) + 1;
+    if ((size_t)max_seg * a.M * a.N * 4 > w.ws_bytes) streamk = 0;
+  }
+  if (!streamk) clusters = std::min(tiles, pair_slots);
   const size_t stage_bytes = (size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2;
   const size_t extra = 32 * SROW * 4 + 512;
   int stages = (int)std::min<size_t>(env_stages, (kSmemBudget - extra) / stage_bytes);
@@ -579,38 +648,36 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) return cudaErrorInvalidValue;
 
   KParams p;
-  p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages; p.splits = splits;
-  p.kb_per_split = kb_per; p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.units = units;
+  p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
+  p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.tiles = tiles; p.streamk = streamk;
+  p.total_kb = (long long)tiles * nkb; p.clusters = clusters;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
   const size_t smem = stages * stage_bytes + extra + 1024;
-  const int clusters = std::min(units, pair_slots);
   dim3 grid(2 * clusters);
+  cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
   switch (a.epi) {
-    case EPI_F32: gemm2_kernel<EPI_F32><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
-    case EPI_BF16: gemm2_kernel<EPI_BF16><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
-    case EPI_RESID: gemm2_kernel<EPI_RESID><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
-    case EPI_SILU_MUL: gemm2_kernel<EPI_SILU_MUL><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
-    case EPI_ARGMAX: gemm2_kernel<EPI_ARGMAX><<<grid, kThreads, smem, stream>>>(tw, tx, p); break;
+    case EPI_F32: e0 = launch_pdl(gemm2_kernel<EPI_F32>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
+    case EPI_BF16: e0 = launch_pdl(gemm2_kernel<EPI_BF16>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
+    case EPI_RESID: e0 = launch_pdl(gemm2_kernel<EPI_RESID>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
+    case EPI_SILU_MUL: e0 = launch_pdl(gemm2_kernel<EPI_SILU_MUL>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
+    case EPI_ARGMAX: e0 = launch_pdl(gemm2_kernel<EPI_ARGMAX>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
     default: return cudaErrorInvalidValue;
   }
-  cudaError_t e = cudaGetLastError();
   g_last_launches = 1;
-  if (e != cudaSuccess || splits == 1) return e;
+  if (e0 != cudaSuccess || !streamk) return e0;
   g_last_launches = 2;
-  const int n_out = a.epi == EPI_SILU_MUL ? a.N / 2 : a.N;
-  const size_t vecs = (size_t)a.M * (n_out / 8);
-  const int rgrid = (int)std::min<size_t>((vecs + 255) / 256, (size_t)g_num_sms * 8);
+  dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, clusters - 1));
   switch (a.epi) {
-    case EPI_F32: gemm_reduce_kernel<EPI_F32><<<rgrid, 256, 0, stream>>>(p); break;
-    case EPI_BF16: gemm_reduce_kernel<EPI_BF16><<<rgrid, 256, 0, stream>>>(p); break;
-    case EPI_RESID: gemm_reduce_kernel<EPI_RESID><<<rgrid, 256, 0, stream>>>(p); break;
-    case EPI_SILU_MUL: gemm_reduce_kernel<EPI_SILU_MUL><<<rgrid, 256, 0, stream>>>(p); break;
+    case EPI_F32: e1 = launch_pdl(gemm_reduce_kernel<EPI_F32>, rgrid, dim3(256), 0, stream, p); break;
+    case EPI_BF16: e1 = launch_pdl(gemm_reduce_kernel<EPI_BF16>, rgrid, dim3(256), 0, stream, p); break;
+    case EPI_RESID: e1 = launch_pdl(gemm_reduce_kernel<EPI_RESID>, rgrid, dim3(256), 0, stream, p); break;
+    case EPI_SILU_MUL: e1 = launch_pdl(gemm_reduce_kernel<EPI_SILU_MUL>, rgrid, dim3(256), 0, stream, p); break;
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
+  return e1;
 }
 
 }  // namespace sidp

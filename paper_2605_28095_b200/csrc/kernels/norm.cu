@@ -11,6 +11,8 @@ namespace {
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ x, int ldx,
                                                       const bf16* __restrict__ g, float eps,
                                                       bf16* __restrict__ y, int ldy, int h) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const bf16* xr = x + (size_t)row * ldx;
   bf16* yr = y + (size_t)row * ldy;
@@ -51,6 +53,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const bf16* __restrict__ x
 
 __global__ void embed_kernel(const bf16* __restrict__ E, int h, const int32_t* __restrict__ tok,
                              bf16* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(E + (size_t)tok[row] * h);
   uint4* dst = reinterpret_cast<uint4*>(x + (size_t)row * h);
@@ -59,6 +63,8 @@ __global__ void embed_kernel(const bf16* __restrict__ E, int h, const int32_t* _
 
 __global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t* next,
                                        int32_t* pos_out, const int32_t* pos, int rows) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows) {
     next[i] = (int32_t)(0xFFFFFFFFu - (uint32_t)(packed[i] & 0xFFFFFFFFull));
@@ -67,6 +73,8 @@ __global__ void argmax_finalize_kernel(const unsigned long long* packed, int32_t
 }
 
 __global__ void argmax_reset_kernel(unsigned long long* packed, int rows) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows) packed[i] = 0ull;
 }
@@ -77,28 +85,25 @@ cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf1
                            int rows, int h, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
   if (h % 8) return cudaErrorInvalidValue;
-  rmsnorm_kernel<<<rows, 256, 0, s>>>(x, ldx, g, eps, y, ldy, h);
-  return cudaGetLastError();
+  return launch_pdl(rmsnorm_kernel, dim3(rows), dim3(256), 0, s, x, ldx, g, eps, y, ldy, h);
 }
 
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
                          cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  embed_kernel<<<rows, 128, 0, s>>>(E, h, tokens, x);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(rows), dim3(128), 0, s, E, h, tokens, x);
 }
 
 cudaError_t argmax_finalize_launch(const unsigned long long* packed, int32_t* next,
                                    int32_t* pos_out, const int32_t* pos, int rows, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  argmax_finalize_kernel<<<(rows + 255) / 256, 256, 0, s>>>(packed, next, pos_out, pos, rows);
-  return cudaGetLastError();
+  return launch_pdl(argmax_finalize_kernel, dim3((rows + 255) / 256), dim3(256), 0, s, packed, next,
+                    pos_out, pos, rows);
 }
 
 cudaError_t argmax_reset_launch(unsigned long long* packed, int rows, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  argmax_reset_kernel<<<(rows + 255) / 256, 256, 0, s>>>(packed, rows);
-  return cudaGetLastError();
+  return launch_pdl(argmax_reset_kernel, dim3((rows + 255) / 256), dim3(256), 0, s, packed, rows);
 }
 
 }  // namespace sidp

@@ -238,14 +238,22 @@ void graph_harvest(sidp_ctx* c);
 
 // ---- optional per-class kernel timing ----
 void timing_flush(sidp_ctx* c);
+// Inside stream capture a plain cudaEventRecord only expresses a dependency; an "external"
+// record becomes an event-record node that every graph replay re-records.
+void record_timing_event(sidp_ctx* c, cudaEvent_t e, cudaStream_t s) {
+  if (c->capturing)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
 void timing_begin(sidp_ctx* c, int cls, cudaStream_t s) {
   if (!((c->timed_mask >> cls) & 1)) return;
   if (c->tev_used + 2 > (int)c->tev.size()) timing_flush(c);
-  cudaEventRecord(c->tev[c->tev_used], s);
+  record_timing_event(c, c->tev[c->tev_used], s);
 }
 void timing_end(sidp_ctx* c, int cls, cudaStream_t s) {
   if (!((c->timed_mask >> cls) & 1)) return;
-  cudaEventRecord(c->tev[c->tev_used + 1], s);
+  record_timing_event(c, c->tev[c->tev_used + 1], s);
   c->tev_cls[c->tev_used / 2] = cls;
   c->tev_used += 2;
   c->st.timed_launches[cls]++;
@@ -257,6 +265,8 @@ void graph_harvest(sidp_ctx* c) {
     cudaEventSynchronize(c->tev[2 * i + 1]);
     if (cudaEventElapsedTime(&ms, c->tev[2 * i], c->tev[2 * i + 1]) == cudaSuccess)
       c->timed_acc_ms[c->tev_cls[i]] += ms;
+    else
+      cudaGetLastError();   // never leave a benign query error as the sticky last error
   }
   for (int k = 0; k < 8; ++k) c->st.timed_launches[k] += c->graph_timed_count[k];
   c->graph_timed_pending = false;
@@ -272,6 +282,8 @@ void timing_flush(sidp_ctx* c) {
     cudaEventSynchronize(c->tev[i + 1]);
     if (cudaEventElapsedTime(&ms, c->tev[i], c->tev[i + 1]) == cudaSuccess)
       c->timed_acc_ms[c->tev_cls[i / 2]] += ms;
+    else
+      cudaGetLastError();
   }
   c->tev_used = first;
 }

@@ -258,5 +258,14 @@ def test_cuda_graph_replay_matches_eager(P):
         assert torch.equal(A.history[-1], Bq.history[-1][0]), s
     st = A.ctx.stats()
     assert st["steps"] == 4 and st["launches"] > 4 * (1 + m.num_layers * 6)
+    # per-class kernel timing survives graph capture (external event-record nodes)
+    A.ctx.set_timing(1 << 2)
+    for s in range(3):
+        with torch.cuda.stream(A.stream):
+            A.ctx.step(A.toks, A.toks, A.kv, batch=8, stream=A.stream, advance_pos=True)
+    A.stream.synchronize()
+    st = A.ctx.stats()
+    assert st["timed_launches"][2] == 3 * m.num_layers
+    assert st["timed_ms"][2] > 0.0
     A.ctx.destroy()
     Bq.ctx.destroy()
