@@ -41,14 +41,17 @@ struct KParams {
   int stages;
   int m_tiles, n_pairs, tiles;
   int streamk;                  // 1: k-block ranges split evenly over clusters; 0: whole tiles
-  long long total_kb;           // tiles * nkb
+  long long total_kb;           // tiles * nks (work in k-steps)
+  int kps, nks;                 // k-blocks (64 deep) per pipeline stage; k-steps per tile
   int clusters;                 // concurrent CTA pairs (fixed per launch configuration)
+  int prefetch_kb;              // W k-blocks prefetched to L2 ahead of the TMA ring
   void* out; int ldo;
   const bf16* resid; int ldr;
   const bf16* bias;
   float* ws;
   int* counters;
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
+  unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
 };
 
 // ---- cluster / 2-SM helpers ------------------------------------------------------
@@ -75,6 +78,14 @@ SIDP_DEV void tma_load_2d_2sm(const CUtensorMap* m, uint32_t leader_bar, void* s
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+SIDP_DEV void tma_load_3d_2sm(const CUtensorMap* m, uint32_t leader_bar, void* smem_dst, int c0,
+                              int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
       : "memory");
 }
 SIDP_DEV void umma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -134,7 +145,7 @@ struct UnitIter {
     u = cluster;
   }
   SIDP_DEV bool next(const KParams& p, int cluster, Unit& x) {
-    const int nkb = p.K / 64;
+    const int nkb = p.nks;   // k-steps per tile
     int t;
     if (p.streamk) {
       if (g >= end) return false;
@@ -162,6 +173,33 @@ struct UnitIter {
     return true;
   }
 };
+
+// Sequential (unit, k-block) cursor — drives the W L2 prefetch ahead of the TMA ring.
+struct KbCursor {
+  UnitIter ui;
+  Unit x;
+  int kb;
+  bool valid;
+  SIDP_DEV void init(const KParams& p, int cluster) {
+    ui.init(p, cluster);
+    valid = ui.next(p, cluster, x);
+    kb = valid ? x.kb0 : 0;
+  }
+  SIDP_DEV void advance(const KParams& p, int cluster) {
+    if (!valid) return;
+    if (++kb >= x.kb1) {
+      valid = ui.next(p, cluster, x);
+      if (valid) kb = x.kb0;
+    }
+  }
+};
+
+SIDP_DEV void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 
 SIDP_DEV unsigned long long argmax_key(float v, int n) {
   uint32_t u = __float_as_uint(v);
@@ -275,7 +313,7 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
   }
 }
 
-template <int EPI>
+template <int EPI, int KPS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
              const KParams p) {
@@ -283,8 +321,10 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int stages = p.stages, BNT = p.BNT, HALF = p.BNT / 2;
-  const uint32_t a_bytes = WROWS * BK * 2;              // 16 KB
-  const uint32_t b_bytes = (uint32_t)HALF * BK * 2;
+  constexpr int kps = KPS;
+  const uint32_t a_sub = WROWS * BK * 2, b_sub = (uint32_t)HALF * BK * 2;   // one 64-deep k-block
+  const uint32_t a_bytes = kps * a_sub;                 // stage = kps k-blocks
+  const uint32_t b_bytes = kps * b_sub;
   uint8_t* sA = smem;
   uint8_t* sB = sA + (size_t)stages * a_bytes;
   float* stg = reinterpret_cast<float*>(sB + (size_t)stages * b_bytes);   // [32][SROW]
@@ -299,7 +339,6 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  const int nkb = p.K / BK;
   const uint32_t tmem_cols = BNT <= 16 ? 32 : (BNT <= 32 ? 64 : (BNT <= 64 ? 128 : (BNT <= 128 ? 256 : 512)));
 
   if (threadIdx.x == 0) {
@@ -332,11 +371,23 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
       UnitIter ui;
       ui.init(p, cluster);
       Unit x;
+      // W streams from HBM: keep prefetch_kb k-blocks of this CTA's W rows in flight to L2
+      // beyond the shared-memory ring, so a TMA load sees L2 rather than HBM latency.
+      KbCursor pf;
+      pf.init(p, cluster);
+      for (int i = 0; i < p.prefetch_kb && pf.valid; ++i, pf.advance(p, cluster))
+        tma_prefetch_l2_2d(&tm_w, pf.kb * KPS * BK, pf.x.ft * 2 * WROWS + rank * WROWS);
       while (ui.next(p, cluster, x)) {
         for (int kb = x.kb0; kb < x.kb1; ++kb, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
+          if (pf.valid) {
+            tma_prefetch_l2_2d(&tm_w, pf.kb * KPS * BK, pf.x.ft * 2 * WROWS + rank * WROWS);
+            pf.advance(p, cluster);
+          }
+          if (p.trace && cluster == 0 && it < 4096) p.trace[rank * 4096 + it] = globaltimer_ns();
           mbar_wait(&empty[s], ph ^ 1);
+          if (p.trace && cluster == 0 && it < 4096) p.trace[(2 + rank) * 4096 + it] = globaltimer_ns();
           const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
           if (p.debug & 2) {
             if (leader) mbar_arrive(&full[s]);
@@ -345,8 +396,14 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           // Only the leader arrives (expecting both CTAs' bytes); the peer's TMA completes its
           // transaction bytes on the leader's barrier directly — no per-stage remote arrive.
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
-          tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes, kb * BK, x.ft * 2 * WROWS + rank * WROWS);
-          tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes, kb * BK, x.mt * BNT + rank * HALF);
+          // 3-D boxes {64 k, rows, kps k-blocks}: one TMA per operand per stage
+#pragma unroll
+          for (int j = 0; j < KPS; ++j) {
+            const int kk = (kb * KPS + j) * BK;
+            tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes + j * a_sub, kk, x.ft * 2 * WROWS + rank * WROWS);
+            tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes + j * b_sub, kk, x.mt * BNT + rank * HALF);
+          }
+          if (p.trace && cluster == 0 && it < 4096 && rank == 0) p.trace[5 * 4096 + it] = globaltimer_ns();
         }
       }
     }
@@ -369,6 +426,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(&full[s], ph);
+          if (p.trace && cluster == 0 && it < 4096 && lane == 0) p.trace[4 * 4096 + it] = globaltimer_ns();
           tc_fence_after();
           if (lane == 0 && (p.debug & 1)) {
             mbar_arrive(&empty[s]);
@@ -377,9 +435,13 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             const uint32_t a0 = smem_u32(sA + (size_t)s * a_bytes);
             const uint32_t b0 = smem_u32(sB + (size_t)s * b_bytes);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma2_bf16(dcol, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                         (kb > x.kb0 || k > 0) ? 1u : 0u);
+            for (int j = 0; j < KPS; ++j) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                umma2_bf16(dcol, umma_desc_sw128(a0 + j * a_sub + k * 32),
+                           umma_desc_sw128(b0 + j * b_sub + k * 32), idesc,
+                           (kb > x.kb0 || j > 0 || k > 0) ? 1u : 0u);
+            }
             umma2_commit_mc(&empty[s]);
           }
           __syncwarp();
@@ -461,7 +523,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
   pdl_wait();
   // blockIdx.y = cluster boundary c (1..C-1); the tile containing b_c strictly inside is fixed
   // up by the block row of the first boundary that splits it.
-  const long long nkb = p.K / 64;
+  const long long nkb = p.nks;
   const int c = blockIdx.y + 1;
   const long long bc = range_begin(c, p.total_kb, p.clusters);
   const int t = (int)(bc / nkb);
@@ -555,6 +617,22 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+// Row-major [rows x K] bf16 viewed as {64 (k in block), rows, K/64 (k-block)} with strides
+// {ld, 128 B}: a box {64, box_rows, kps} lands as kps canonical SW128 K-major tiles back to back.
+bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, uint64_t ld_elems,
+                  uint32_t box_rows, uint32_t kps) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, rows, K / 64};
+  cuuint64_t strides[2] = {ld_elems * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, kps};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                   uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn fn = get_encode_fn();
@@ -574,8 +652,17 @@ thread_local int g_last_launches = 0;
 
 template <int EPI>
 void set_attr() {
-  cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gemm2_kernel<EPI, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kSmemBudget + 1024);
+  cudaFuncSetAttribute(gemm2_kernel<EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSmemBudget + 1024);
+}
+
+template <int EPI>
+cudaError_t launch_gemm2(int kps, dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& tw,
+                         const CUtensorMap& tx, const KParams& p) {
+  if (kps == 2) return launch_pdl(gemm2_kernel<EPI, 2>, grid, dim3(kThreads), smem, st, tw, tx, p);
+  return launch_pdl(gemm2_kernel<EPI, 1>, grid, dim3(kThreads), smem, st, tw, tx, p);
 }
 
 }  // namespace
@@ -624,12 +711,18 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   BNT = std::max(32, std::min(env_bnt, BNT));
   const int m_tiles = (a.M + BNT - 1) / BNT;
   const int n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
-  const int nkb = a.K / BK;
+  const int nkb_blocks = a.K / BK;
+  static int env_kps = getenv("SIDP_GEMM_KPS") ? atoi(getenv("SIDP_GEMM_KPS")) : 2;
+  const int kps = (env_kps == 2 && nkb_blocks % 2 == 0) ? 2 : 1;
+  const int nkb = nkb_blocks / kps;   // k-steps per tile (the unit of stream-K work)
   const int tiles = n_pairs * m_tiles;
   // stream-K over all pairs unless the epilogue needs whole dot products (fused argmax) or the
   // caller pins whole tiles (k_splits == 1); max segments per tile bounds the workspace
   int clusters = pair_slots;
-  int streamk = (a.epi != EPI_ARGMAX && a.k_splits != 1 && tiles % clusters != 0) ? 1 : 0;
+  // whole tiles balance well once every pair has >= 1 tile (measured: qkv 40 tiles, gate/up
+  // 200 tiles faster whole); stream-K pays off for heavily underfilled shapes (O, down: 20)
+  int streamk = (a.epi != EPI_ARGMAX && a.k_splits != 1 &&
+                 (a.k_splits > 1 || 2 * tiles <= clusters)) ? 1 : 0;
   if (streamk) {
     const long long total = (long long)tiles * nkb;
     const long long per = total / clusters;
@@ -638,7 +731,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     if ((size_t)max_seg * a.M * a.N * 4 > w.ws_bytes) streamk = 0;
   }
   if (!streamk) clusters = std::min(tiles, pair_slots);
-  const size_t stage_bytes = (size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2;
+  const size_t stage_bytes = kps * ((size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2);
   const size_t extra = 32 * SROW * 4 + 512;
   int stages = (int)std::min<size_t>(env_stages, (kSmemBudget - extra) / stage_bytes);
   stages = std::max(2, stages);
@@ -650,23 +743,51 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   KParams p;
   p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
   p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.tiles = tiles; p.streamk = streamk;
-  p.total_kb = (long long)tiles * nkb; p.clusters = clusters;
+  p.total_kb = (long long)tiles * nkb; p.clusters = clusters; p.kps = kps; p.nks = nkb;
+  static int env_pf = getenv("SIDP_GEMM_PF") ? atoi(getenv("SIDP_GEMM_PF")) : 0;
+  p.prefetch_kb = env_pf;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
+  static int env_trace = getenv("SIDP_GEMM_TRACE") ? atoi(getenv("SIDP_GEMM_TRACE")) : 0;
+  static unsigned long long* trace_buf = nullptr;
+  p.trace = nullptr;
+  if (env_trace) {
+    if (!trace_buf) cudaMallocManaged(&trace_buf, 6 * 4096 * 8);
+    cudaMemset(trace_buf, 0, 6 * 4096 * 8);
+    p.trace = trace_buf;
+  }
   const size_t smem = stages * stage_bytes + extra + 1024;
   dim3 grid(2 * clusters);
   cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
   switch (a.epi) {
-    case EPI_F32: e0 = launch_pdl(gemm2_kernel<EPI_F32>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
-    case EPI_BF16: e0 = launch_pdl(gemm2_kernel<EPI_BF16>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
-    case EPI_RESID: e0 = launch_pdl(gemm2_kernel<EPI_RESID>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
-    case EPI_SILU_MUL: e0 = launch_pdl(gemm2_kernel<EPI_SILU_MUL>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
-    case EPI_ARGMAX: e0 = launch_pdl(gemm2_kernel<EPI_ARGMAX>, grid, dim3(kThreads), smem, stream, tw, tx, p); break;
+    case EPI_F32: e0 = launch_gemm2<EPI_F32>(kps, grid, smem, stream, tw, tx, p); break;
+    case EPI_BF16: e0 = launch_gemm2<EPI_BF16>(kps, grid, smem, stream, tw, tx, p); break;
+    case EPI_RESID: e0 = launch_gemm2<EPI_RESID>(kps, grid, smem, stream, tw, tx, p); break;
+    case EPI_SILU_MUL: e0 = launch_gemm2<EPI_SILU_MUL>(kps, grid, smem, stream, tw, tx, p); break;
+    case EPI_ARGMAX: e0 = launch_gemm2<EPI_ARGMAX>(kps, grid, smem, stream, tw, tx, p); break;
     default: return cudaErrorInvalidValue;
   }
   g_last_launches = 1;
+  if (env_trace) {   // perf experiment: dump per-k-block timing of cluster 0
+    cudaStreamSynchronize(stream);
+    int n = 0;
+    while (n < 4096 && trace_buf[4 * 4096 + n]) ++n;
+    double sw = 0, tl = 0, gap = 0, iss = 0, loop = 0;
+    for (int i = 0; i < n; ++i) {
+      iss += (double)(trace_buf[5 * 4096 + i] - trace_buf[2 * 4096 + i]);     // TMA issue cost
+      if (i) loop += (double)(trace_buf[i] - trace_buf[i - 1]);
+      sw += (double)(trace_buf[2 * 4096 + i] - trace_buf[i]);           // producer wait on empty
+      tl += (double)(trace_buf[4 * 4096 + i] - trace_buf[2 * 4096 + i]); // issue -> full (TMA lat)
+      if (i) gap += (double)(trace_buf[4 * 4096 + i] - trace_buf[4 * 4096 + i - 1]);
+    }
+    if (n > 1)
+      fprintf(stderr, "[gemm trace] M=%d N=%d K=%d stages=%d kb=%d: producer empty-wait %.0f ns, "
+              "issue->full %.0f ns, full-to-full %.0f ns per kb, TMA issue %.0f ns, producer loop %.0f ns, span %.1f us\n", a.M, a.N, a.K,
+              stages, n, sw / n, tl / n, gap / (n - 1), iss / n, loop / (n - 1),
+              (trace_buf[4 * 4096 + n - 1] - trace_buf[2 * 4096]) / 1e3);
+  }
   if (e0 != cudaSuccess || !streamk) return e0;
   g_last_launches = 2;
   dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, clusters - 1));
