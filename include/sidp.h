@@ -248,6 +248,9 @@ sidp_status sidp_test_gen_kv(void* cache, int32_t B, int32_t nkv, int32_t smax, 
                              int32_t T, int64_t b0, uint64_t seed, int32_t tensor, int32_t layer,
                              void* stream);
 
+/* Copy this rank's CaS flag words (arrive[world], done, served) to host out[n] (debugging). */
+sidp_status sidp_debug_flags(const sidp_ctx* ctx, uint64_t* out, int32_t n);
+
 /* Pointer to layer `layer`'s pooled blob as resident on this rank (owned arena, else NULL)
  * and the byte offsets of its components. */
 sidp_status sidp_layer_ptr(const sidp_ctx* ctx, int32_t layer, void** pooled, void** local);

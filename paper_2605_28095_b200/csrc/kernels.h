@@ -20,6 +20,18 @@ enum GemmEpilogue : int {
   EPI_SILU_MUL = 3,   // W rows interleaved per 128-row tile: [gate 64 | up 64];
                       // out[m, f] bf16 = silu(gate) * up, f = tile*64 + i
   EPI_ARGMAX = 4,     // fused argmax over n: packed (value, lowest index) into out u64[M]
+  EPI_QKV = 5,        // fused QKV post-processing: (+bias) (qk-norm) RoPE -> q bf16, k/v -> KV cache
+};
+
+// Destination of the fused QKV epilogue (rows of W_qkv = [q heads | k heads | v heads]).
+struct QkvEpi {
+  bf16* q;                       // [M, nq, hd]
+  bf16* kc; bf16* vc;            // this layer's caches [Bmax, nkv, smax, hd]
+  const int32_t* pos;            // [M] position of the new token
+  const float2* rope;            // [max_pos, hd/2] (cos, sin)
+  const bf16* gq; const bf16* gk;   // qk-norm gains (null = off)
+  float eps;
+  int nq, nkv, hd, smax;
 };
 
 struct GemmArgs {
@@ -32,6 +44,7 @@ struct GemmArgs {
   const bf16* bias;            // [N] or null
   int k_splits;                // 0 = auto
   int max_ctas;                // 0 = all SMs
+  const QkvEpi* qkv;           // EPI_QKV only
 };
 
 struct GemmWorkspace {
@@ -110,5 +123,11 @@ cudaError_t wait_launch(const FlagSet& flags, uint64_t value, uint64_t timeout_n
                         cudaStream_t s);
 cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int rows, int row_bytes,
                              cudaStream_t s);
+
+// Eager module loading of every kernel (called once by sidp_alloc).
+cudaError_t gemm_preload();
+cudaError_t attention_preload();
+cudaError_t norm_preload();
+cudaError_t fetch_preload();
 
 }  // namespace sidp

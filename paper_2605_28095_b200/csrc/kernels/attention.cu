@@ -394,4 +394,15 @@ cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
                      : launch_pdl(attn_combine_kernel<64>, dim3(a.B * a.nq), dim3(64), 0, s, wsc, oc, nq, splits);
 }
 
+cudaError_t attention_preload() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  if (cudaFuncGetAttributes(&fa, qkv_post_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, attn_kernel<128>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, attn_kernel<64>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, attn_combine_kernel<128>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, attn_combine_kernel<64>) != cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
 }  // namespace sidp

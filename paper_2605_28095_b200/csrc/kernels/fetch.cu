@@ -125,4 +125,15 @@ cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int r
   return cudaGetLastError();
 }
 
+cudaError_t fetch_preload() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  if (cudaFuncGetAttributes(&fa, fetch_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, delay_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, signal_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, wait_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, copy_rows_kernel) != cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
 }  // namespace sidp

@@ -52,6 +52,7 @@ struct KParams {
   int* counters;
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
+  QkvEpi qkv;                   // EPI_QKV destination
 };
 
 // ---- cluster / 2-SM helpers ------------------------------------------------------
@@ -287,6 +288,88 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
           x[q] = g / (1.0f + __expf(-g)) * u;
         }
         *reinterpret_cast<uint4*>(out + (size_t)m * p.ldo + of) = pack_bf16x8(x);
+      }
+    }
+  } else if constexpr (EPI == EPI_QKV) {
+    // warp w handles tokens w*8 .. w*8+7; lane l holds features 4l..4l+3 of the 128-row tile,
+    // which lies entirely in the q, k or v region (q_dim, kv_dim multiples of 128)
+    const QkvEpi& e = p.qkv;
+    const int w = tid >> 5, lane = tid & 31;
+    const int hd = e.hd, half = hd / 2;
+    const int qd = e.nq * hd, kvd = e.nkv * hd;
+    const int region = n0 < qd ? 0 : (n0 < qd + kvd ? 1 : 2);
+    const int f = lane * 4;                          // feature within tile
+    const int nabs = n0 + f;
+    const int lane_span = hd / 4;                    // lanes per head (32 or 16)
+    float bias4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (p.bias) {
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(p.bias + nabs);
+      const float2 t0 = __bfloat1622float2(b2[0]), t1 = __bfloat1622float2(b2[1]);
+      bias4[0] = t0.x; bias4[1] = t0.y; bias4[2] = t1.x; bias4[3] = t1.y;
+    }
+    const bf16* gain = region == 0 ? e.gq : (region == 1 ? e.gk : nullptr);
+    const int d = (n0 - (region == 0 ? 0 : (region == 1 ? qd : qd + kvd)) + f) % hd;  // dim in head
+    const int head = (n0 - (region == 0 ? 0 : (region == 1 ? qd : qd + kvd)) + f) / hd;
+    float g4[4] = {1.f, 1.f, 1.f, 1.f};
+    if (gain) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) g4[q] = bf16_to_f(gain[d + q]);
+    }
+    // positions of this warp's 8 tokens (one load per lane, broadcast by shuffles) and the
+    // RoPE table entries of 4 tokens at a time issued before use: no dependent global loads
+    // inside the per-token loop
+    int mypos = 0;
+    if (lane < 8 && m0 + w * 8 + lane < p.M) mypos = e.pos[m0 + w * 8 + lane];
+    const bool lo = d < half;
+    const int rd = lo ? d : d - half;
+#pragma unroll
+    for (int grp = 0; grp < 2; ++grp) {
+      float2 cs[4][4];
+      int posv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        posv[t] = __shfl_sync(0xffffffffu, mypos, grp * 4 + t);
+        if (region < 2) {
+          const float2* row = e.rope + (size_t)posv[t] * half + rd;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cs[t][q] = row[q];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = w * 8 + grp * 4 + t, m = m0 + j;
+        const float4 v4 = *reinterpret_cast<const float4*>(sm + j * SROW + f);
+        float x[4] = {v4.x + bias4[0], v4.y + bias4[1], v4.z + bias4[2], v4.w + bias4[3]};
+        if (region < 2) {
+          if (gain) {   // per-head RMSNorm over hd dims (Qwen3 qk_norm)
+            float ss = x[0] * x[0] + x[1] * x[1] + x[2] * x[2] + x[3] * x[3];
+            for (int o = lane_span / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            const float r = rsqrtf(ss / (float)hd + e.eps);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = x[q] * r * g4[q];
+          }
+          // rotate-half RoPE: partner of dim d is d +- hd/2, held by lane ^ (hd/8)
+          float y[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) y[q] = __shfl_xor_sync(0xffffffffu, x[q], hd / 8);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            x[q] = lo ? x[q] * cs[t][q].x - y[q] * cs[t][q].y : x[q] * cs[t][q].x + y[q] * cs[t][q].y;
+        }
+        if (m < p.M) {
+          __nv_bfloat162 o0 = __floats2bfloat162_rn(x[0], x[1]), o1 = __floats2bfloat162_rn(x[2], x[3]);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&o0);
+          pk.y = *reinterpret_cast<uint32_t*>(&o1);
+          bf16* dst;
+          if (region == 0) {
+            dst = e.q + ((size_t)m * e.nq + head) * hd + d;
+          } else {
+            bf16* cache = region == 1 ? e.kc : e.vc;
+            dst = cache + (((size_t)m * e.nkv + head) * e.smax + posv[t]) * hd + d;
+          }
+          *reinterpret_cast<uint2*>(dst) = pk;
+        }
       }
     }
   } else {  // EPI_ARGMAX: warp w reduces tokens w*8 .. w*8+7 over the 128 features
@@ -702,6 +785,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     set_attr<EPI_RESID>();
     set_attr<EPI_SILU_MUL>();
     set_attr<EPI_ARGMAX>();
+    set_attr<EPI_QKV>();
   }
   static int env_bnt = getenv("SIDP_GEMM_BNT") ? atoi(getenv("SIDP_GEMM_BNT")) : 256;
   static int env_stages = getenv("SIDP_GEMM_STAGES") ? atoi(getenv("SIDP_GEMM_STAGES")) : 12;
@@ -721,7 +805,9 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   int clusters = pair_slots;
   // whole tiles balance well once every pair has >= 1 tile (measured: qkv 40 tiles, gate/up
   // 200 tiles faster whole); stream-K pays off for heavily underfilled shapes (O, down: 20)
-  int streamk = (a.epi != EPI_ARGMAX && a.k_splits != 1 &&
+  if (a.epi == EPI_QKV && (!a.qkv || (a.qkv->hd != 64 && a.qkv->hd != 128))) return cudaErrorInvalidValue;
+  // whole-row epilogues (argmax over a tile, per-head qk-norm/RoPE) need whole dot products
+  int streamk = (a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.k_splits != 1 &&
                  (a.k_splits > 1 || 2 * tiles <= clusters)) ? 1 : 0;
   if (streamk) {
     const long long total = (long long)tiles * nkb;
@@ -748,6 +834,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.prefetch_kb = env_pf;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
+  if (a.qkv) p.qkv = *a.qkv;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
   static int env_trace = getenv("SIDP_GEMM_TRACE") ? atoi(getenv("SIDP_GEMM_TRACE")) : 0;
@@ -767,6 +854,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     case EPI_RESID: e0 = launch_gemm2<EPI_RESID>(kps, grid, smem, stream, tw, tx, p); break;
     case EPI_SILU_MUL: e0 = launch_gemm2<EPI_SILU_MUL>(kps, grid, smem, stream, tw, tx, p); break;
     case EPI_ARGMAX: e0 = launch_gemm2<EPI_ARGMAX>(kps, grid, smem, stream, tw, tx, p); break;
+    case EPI_QKV: e0 = launch_gemm2<EPI_QKV>(kps, grid, smem, stream, tw, tx, p); break;
     default: return cudaErrorInvalidValue;
   }
   g_last_launches = 1;
@@ -799,6 +887,25 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     default: return cudaErrorInvalidValue;
   }
   return e1;
+}
+
+// Force-load every kernel of this file (CUDA lazy loading would otherwise load a module on
+// first launch, which waits for the device to idle — a deadlock while another virtual rank's
+// flag-wait kernel spins; see runtime sidp_alloc).
+cudaError_t gemm_preload() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+#define SIDP_PRELOAD(k) if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) e = cudaGetLastError();
+  SIDP_PRELOAD((gemm2_kernel<EPI_F32, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_F32, 2>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 2>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 2>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 2>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2>))
+  SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
+  SIDP_PRELOAD((gemm_reduce_kernel<EPI_RESID>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_SILU_MUL>))
+#undef SIDP_PRELOAD
+  return e;
 }
 
 }  // namespace sidp

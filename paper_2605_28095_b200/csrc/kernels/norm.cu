@@ -106,4 +106,14 @@ cudaError_t argmax_reset_launch(unsigned long long* packed, int rows, cudaStream
   return launch_pdl(argmax_reset_kernel, dim3((rows + 255) / 256), dim3(256), 0, s, packed, rows);
 }
 
+cudaError_t norm_preload() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  if (cudaFuncGetAttributes(&fa, rmsnorm_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, embed_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, argmax_finalize_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, argmax_reset_kernel) != cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
 }  // namespace sidp

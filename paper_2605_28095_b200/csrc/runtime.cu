@@ -307,10 +307,10 @@ sidp::GemmWorkspace gws(sidp_ctx* c) {
 
 cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, int M, int N, int K,
                  int epi, void* out, int ldo, const bf16* resid, int ldr, const bf16* bias,
-                 cudaStream_t s) {
+                 cudaStream_t s, const sidp::QkvEpi* qkv = nullptr) {
   sidp::GemmArgs a{};
   a.x = x; a.ldx = ldx; a.w = w; a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = epi;
-  a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias;
+  a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias; a.qkv = qkv;
   timing_begin(c, cls, s);
   cudaError_t e = sidp::gemm_launch(a, gws(c), s);
   timing_end(c, cls, s);
@@ -324,23 +324,27 @@ cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, in
 sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int layer,
                       const sidp_kv* kv, const float* qkv_in, cudaStream_t s) {
   const auto& m = ctx->m;
-  const float* qkv = qkv_in;
-  if (!qkv) {
-    CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
-    count_launch(ctx);
-    CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_F32, ctx->qkv,
-            ctx->qkvdim, nullptr, 0, W.b_qkv, s));
-    qkv = ctx->qkv;
-  }
   const size_t lstride = (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
   bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
   bf16* vc = reinterpret_cast<bf16*>(kv->v_cache) + (size_t)layer * lstride;
-  sidp::QkvPostArgs qa{};
-  qa.qkv = qkv; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
-  qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;
-  qa.q = ctx->q; qa.kc = kc; qa.vc = vc; qa.smax = ctx->c.max_ctx;
-  CK(sidp::qkv_post_launch(qa, s));
-  count_launch(ctx);
+  if (!qkv_in) {
+    // RMSNorm, then the QKV GEMM whose epilogue applies bias, qk-norm and RoPE and writes q
+    // and the new k/v straight into the KV cache (no fp32 qkv round trip)
+    CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+    count_launch(ctx);
+    sidp::QkvEpi qe{ctx->q, kc, vc, kv->pos, ctx->rope, W.g_q, W.g_k, m.rms_eps,
+                    m.n_q_heads, m.n_kv_heads, m.head_dim, ctx->c.max_ctx};
+    CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_QKV, nullptr,
+            0, nullptr, 0, W.b_qkv, s, &qe));
+  } else {
+    // CaS: the owner returned u W_qkv^T (+b) in fp32; qk-norm / RoPE / KV append stay local
+    sidp::QkvPostArgs qa{};
+    qa.qkv = qkv_in; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
+    qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;
+    qa.q = ctx->q; qa.kc = kc; qa.vc = vc; qa.smax = ctx->c.max_ctx;
+    CK(sidp::qkv_post_launch(qa, s));
+    count_launch(ctx);
+  }
   sidp::AttnArgs aa{};
   aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.pos = kv->pos; aa.o = ctx->o; aa.B = B;
   aa.nq = m.n_q_heads; aa.nkv = m.n_kv_heads; aa.hd = m.head_dim; aa.smax = ctx->c.max_ctx;
@@ -513,6 +517,11 @@ sidp_status cas_round_trip(sidp_ctx* ctx, int layer, const std::vector<SendPart>
   const int Bme = ctx->batches[me];
   const int64_t prev = ctx->last_rt[o][slot];
   ctx->last_rt[o][slot] = rt;
+  static const bool trace = getenv("SIDP_CAS_TRACE") != nullptr;
+  if (trace)
+    fprintf(stderr, "[cas] rank %d layer %d rt %lld owner %d slot %d prev %lld total %d me_off %d own_cas %p owner_cas %p\n",
+            me, layer, (long long)rt, o, slot, (long long)prev, total, off[me], (void*)ctx->cas,
+            (void*)ctx->peer_cas[o]);
   uint8_t* owner_cas = ctx->peer_cas[o];
   if (!owner_cas) return fail(SIDP_ESTATE, "CaS arena of rank %d not imported", o);
   const uint64_t tmo = 20ull * 1000 * 1000 * 1000;   // 20 s
@@ -817,6 +826,13 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
     CK(cudaEventCreateWithFlags(&ctx->ready_ev[s], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->free_ev[s], cudaEventDisableTiming));
   }
+  // CUDA lazy loading would load each kernel's module at its first launch, which blocks until
+  // the device idles: with CaS flag-wait kernels spinning on another (virtual) rank that is a
+  // deadlock.  Load every kernel now.
+  CK(sidp::gemm_preload());
+  CK(sidp::attention_preload());
+  CK(sidp::norm_preload());
+  CK(sidp::fetch_preload());
   ctx->peer_arena.assign(ctx->d, nullptr);
   ctx->peer_arena[ctx->r] = ctx->arena;
   ctx->peer_cas.assign(ctx->d, nullptr);
@@ -1248,6 +1264,14 @@ sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t class_mask) {
     ctx->timed_acc_ms[i] = 0.0;
     ctx->st.timed_launches[i] = 0;
   }
+  return SIDP_OK;
+}
+
+sidp_status sidp_debug_flags(const sidp_ctx* ctx, uint64_t* out, int32_t n) {
+  if (!ctx || !out || !ctx->allocated) return fail(SIDP_EINVAL, "bad argument");
+  const int cnt = std::min<int>(n, ctx->d + 2);
+  if (cudaMemcpy(out, ctx->cas, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SIDP_ECUDA, "flag read");
   return SIDP_OK;
 }
 
