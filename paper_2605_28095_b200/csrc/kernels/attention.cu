@@ -23,13 +23,16 @@ namespace {
 __global__ void qkv_post_kernel(QkvPostArgs a) {
   pdl_trigger();
   pdl_wait();
+  // grid (B, ceil(nh / 8)): one warp per (token, head) so every load is issued up front
   const int b = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hd = a.hd, half = hd / 2;
   const int nh = a.nq + 2 * a.nkv;
+  const int nwarps = (blockDim.x >> 5) * gridDim.y;
+  const int head0 = blockIdx.y * (blockDim.x >> 5) + warp;
   const int pos = a.pos[b];
   const float2* rope = a.rope + (size_t)pos * half;
-  for (int head = warp; head < nh; head += nwarps) {
+  for (int head = head0; head < nh; head += nwarps) {
     const float* src = a.qkv + ((size_t)b * nh + head) * hd;
     const bool is_v = head >= a.nq + a.nkv;
     const bool is_q = head < a.nq;
@@ -345,7 +348,8 @@ thread_local int g_attn_launches = 0;
 cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s) {
   if (a.B <= 0) return cudaSuccess;
   if (a.hd != 64 && a.hd != 128) return cudaErrorInvalidValue;
-  return launch_pdl(qkv_post_kernel, dim3(a.B), dim3(256), 0, s, a);
+  const int nh = a.nq + 2 * a.nkv;
+  return launch_pdl(qkv_post_kernel, dim3(a.B, (nh + 7) / 8), dim3(256), 0, s, a);
 }
 
 int attention_last_launch_count() { return g_attn_launches; }

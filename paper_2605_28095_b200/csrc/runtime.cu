@@ -327,9 +327,19 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   const size_t lstride = (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
   bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
   bf16* vc = reinterpret_cast<bf16*>(kv->v_cache) + (size_t)layer * lstride;
+  static const bool fused_qkv = getenv("SIDP_FUSED_QKV") && atoi(getenv("SIDP_FUSED_QKV")) != 0;
+  if (!qkv_in && !fused_qkv) {
+    // RMSNorm -> QKV GEMM (fp32, + bias) -> qkv_post (qk-norm, RoPE, KV append) on all SMs
+    CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+    count_launch(ctx);
+    CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_F32, ctx->qkv,
+            ctx->qkvdim, nullptr, 0, W.b_qkv, s));
+    qkv_in = ctx->qkv;
+  }
   if (!qkv_in) {
     // RMSNorm, then the QKV GEMM whose epilogue applies bias, qk-norm and RoPE and writes q
-    // and the new k/v straight into the KV cache (no fp32 qkv round trip)
+    // and the new k/v straight into the KV cache (no fp32 qkv round trip; SIDP_FUSED_QKV=1:
+    // on these shapes the per-tile epilogue is not hidden, so it is off by default)
     CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
     count_launch(ctx);
     sidp::QkvEpi qe{ctx->q, kc, vc, kv->pos, ctx->rope, W.g_q, W.g_k, m.rms_eps,
@@ -337,7 +347,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
     CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_QKV, nullptr,
             0, nullptr, 0, W.b_qkv, s, &qe));
   } else {
-    // CaS: the owner returned u W_qkv^T (+b) in fp32; qk-norm / RoPE / KV append stay local
+    // fp32 qkv (local GEMM, or CaS: returned by the owner): qk-norm / RoPE / KV append here
     sidp::QkvPostArgs qa{};
     qa.qkv = qkv_in; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
     qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;

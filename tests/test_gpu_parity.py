@@ -269,3 +269,66 @@ def test_cuda_graph_replay_matches_eager(P):
     assert st["timed_ms"][2] > 0.0
     A.ctx.destroy()
     Bq.ctx.destroy()
+
+
+@pytest.mark.parametrize("name,B,ctx,span", [("tiny", 1, 1500, 0), ("tiny", 3, 700, 900),
+                                              ("tiny-qwen3", 2, 2000, 100)])
+def test_long_context_split_kv(P, name, B, ctx, span):
+    """Small batches with long contexts take the split-KV attention path (partials + combine);
+    ragged positions make some splits empty."""
+    m = MODELS[name]
+    max_ctx = ctx + span + 8
+    R = Rank(P, m, B=B, ctx=ctx, span=span, max_ctx=max_ctx)
+    R.step(); R.finish_step()
+    _, logits, dump = R.history[0]
+    om = OracleModel(m, SEED)
+    bg = np.arange(B)
+    pos = gen.positions(SEED, bg, ctx, span)
+    xs = dump.double().numpy()
+    out = None
+    for l in range(m.num_layers):
+        K = gen.kv(SEED, gen.KCACHE, l, bg, range(max_ctx), m.n_kv_heads, m.head_dim)
+        V = gen.kv(SEED, gen.VCACHE, l, bg, range(max_ctx), m.n_kv_heads, m.head_dim)
+        out, _, _ = oracle_layer(om, l, xs[l], pos, K, V)
+        if l + 1 < m.num_layers:
+            assert rel_err(xs[l + 1], out) <= TOL, (l, rel_err(xs[l + 1], out))
+    assert rel_err(logits.double().numpy(), OM.lm_head(m, om.head, out)) <= TOL
+    R.ctx.destroy()
+
+
+def test_batch_one_and_max_batch(P):
+    """Degenerate batch sizes: B=1 and B = max_batch with a ragged tail (M not a tile multiple)."""
+    m = MODELS["tiny"]
+    for B in (1, 37):
+        R = Rank(P, m, B=B, span=63, max_ctx=80)
+        R.step(); R.finish_step()
+        _, logits, dump = R.history[0]
+        om = OracleModel(m, SEED)
+        _, toks, pos, caches = rank_inputs(m, SEED, 0, B, 0, 63, 80)
+        xs = dump.double().numpy()
+        out = None
+        for l in range(m.num_layers):
+            out, _, _ = oracle_layer(om, l, xs[l], pos, *caches[l])
+        assert rel_err(logits.double().numpy(), OM.lm_head(m, om.head, out)) <= TOL
+        R.ctx.destroy()
+
+
+def test_dummy_step_was_keeps_schedule(P):
+    """A WaS rank with batch 0 (dummy) still walks its ring; the fetch log stays equal to the
+    oracle's FIFO schedule and the next real step is correct."""
+    m = MODELS["tiny"].with_layers(8)
+    ranks = _group(P, m, 2, [3, 4])
+    R = ranks[0]
+    with torch.cuda.stream(R.stream):
+        R.ctx.step(R.toks, R.next, R.kv, batch=0, stream=R.stream)      # dummy step
+    R.stream.synchronize()
+    R.step(); R.finish_step()
+    own = OS.owner_map(8, 2)
+    log = R.ctx.fetch_log()
+    ref = OS.slot_schedule(OS.plan_exec(own, 0), 2, 3)
+    assert log == ref[:len(log)] and len(log) >= 2 * 4
+    rep = _replicated(P, m, 3, 0)
+    rep.step(); rep.finish_step()
+    assert torch.equal(rep.history[0][1], R.history[0][1])
+    for Rk in ranks + [rep]:
+        Rk.ctx.destroy()
