@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--order", default="exec", choices=["exec", "paper"])
     ap.add_argument("--pool", default="layer", choices=["layer", "ffn"])
     ap.add_argument("--fetch", default="sm", choices=["sm", "ce"])
-    ap.add_argument("--fetch-sms", type=int, default=32)
+    ap.add_argument("--fetch-sms", type=int, default=48)
     ap.add_argument("--no-stagger", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -243,6 +243,11 @@ sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uin
                           int32_t tensor, int32_t layer, int32_t kind, int32_t scale_k,
                           int64_t row0, int64_t lcols, int32_t row_map, void* stream);
 
+/* K1 fetch of `bytes` (multiple of 16) from src (local or peer VA) to dst with the SM copy kernel
+ * on `ctas` CTAs (engine 0) or the copy engine (engine 1). */
+sidp_status sidp_test_fetch(void* dst, const void* src, size_t bytes, int32_t ctas, int32_t engine,
+                            void* stream);
+
 /* Synthetic KV cache fill: cache[b][g][t][d] (b < B, t < T) from logical b_global = b0 + b. */
 sidp_status sidp_test_gen_kv(void* cache, int32_t B, int32_t nkv, int32_t smax, int32_t hd,
                              int32_t T, int64_t b0, uint64_t seed, int32_t tensor, int32_t layer,

@@ -84,6 +84,7 @@ SIGNATURES = {
     "sidp_test_gen_kv": [_P, _I32, _I32, _I32, _I32, _I32, _I64, C.c_uint64, _I32, _I32, _P],
     "sidp_layer_ptr": [_P, _I32, C.POINTER(_P), C.POINTER(_P)],
     "sidp_debug_flags": [_P, C.POINTER(C.c_uint64), _I32],
+    "sidp_test_fetch": [_P, _P, C.c_size_t, _I32, _I32, _P],
 }
 
 _lib = None

@@ -65,7 +65,7 @@ class KVCache:
 
 class Context:
     def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
-                 max_batch=8, max_ctx=128, fetch_sms=32, fetch_engine="sm", stagger=True,
+                 max_batch=8, max_ctx=128, fetch_sms=48, fetch_engine="sm", stagger=True,
                  device=0, seed=20261017, layer_owner=None, alloc=True):
         self.m = m
         self.rank, self.world = rank, world

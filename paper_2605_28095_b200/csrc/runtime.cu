@@ -1332,6 +1332,15 @@ sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uin
   return SIDP_OK;
 }
 
+sidp_status sidp_test_fetch(void* dst, const void* src, size_t bytes, int32_t ctas, int32_t engine,
+                            void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = engine == SIDP_FETCH_CE ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s)
+                                          : sidp::fetch_launch(dst, src, bytes, ctas, s);
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "fetch: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
 sidp_status sidp_test_gen_kv(void* cache, int32_t B, int32_t nkv, int32_t smax, int32_t hd,
                              int32_t T, int64_t b0, uint64_t seed, int32_t tensor, int32_t layer,
                              void* stream) {
