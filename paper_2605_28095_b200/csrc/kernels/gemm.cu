@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "../common.cuh"
 #include "../kernels.h"
@@ -396,6 +397,10 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
   }
 }
 
+// perf experiment timeline: per CTA, slot k of TL(k) = globaltimer at a kernel milestone
+#define SIDP_TL(k) \
+  do { if (p.trace && blockIdx.x < 512) p.trace[6 * 4096 + blockIdx.x * 8 + (k)] = globaltimer_ns(); } while (0)
+
 template <int EPI, int KPS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
@@ -425,6 +430,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   const uint32_t tmem_cols = BNT <= 16 ? 32 : (BNT <= 32 ? 64 : (BNT <= 64 ? 128 : (BNT <= 128 ? 256 : 512)));
 
   if (threadIdx.x == 0) {
+    SIDP_TL(0);
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
     for (int s = 0; s < stages; ++s) {
@@ -446,6 +452,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   // prologue done: let the next kernel of the chain launch, then wait for our inputs
   pdl_trigger();
   pdl_wait();
+  if (threadIdx.x == 0) SIDP_TL(1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -509,6 +516,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
           mbar_wait(&full[s], ph);
+          if (lane == 0 && it == 0) SIDP_TL(2);
           if (p.trace && cluster == 0 && it < 4096 && lane == 0) p.trace[4 * 4096 + it] = globaltimer_ns();
           tc_fence_after();
           if (lane == 0 && (p.debug & 1)) {
@@ -532,6 +540,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (lane == 0) umma2_commit_mc(&tfull[acc]);
         __syncwarp();
       }
+      if (lane == 0) SIDP_TL(3);
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
@@ -587,7 +596,9 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
       }
     }
+    if (tid == 0) SIDP_TL(4);
   }
+  if (warp == 2 && lane == 0) SIDP_TL(5);
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();
@@ -595,6 +606,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     tc_fence_after();
     tmem_dealloc2(tmem_base, tmem_cols);
   }
+  if (threadIdx.x == 0) SIDP_TL(6);
 }
 
 // Stream-K fix-up over all SMs: for tiles covered by several k-range segments, each thread sums
@@ -841,8 +853,8 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   static unsigned long long* trace_buf = nullptr;
   p.trace = nullptr;
   if (env_trace) {
-    if (!trace_buf) cudaMallocManaged(&trace_buf, 6 * 4096 * 8);
-    cudaMemset(trace_buf, 0, 6 * 4096 * 8);
+    if (!trace_buf) cudaMallocManaged(&trace_buf, (6 * 4096 + 512 * 8) * 8);
+    cudaMemset(trace_buf, 0, (6 * 4096 + 512 * 8) * 8);
     p.trace = trace_buf;
   }
   const size_t smem = stages * stage_bytes + extra + 1024;
@@ -875,6 +887,22 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
               "issue->full %.0f ns, full-to-full %.0f ns per kb, TMA issue %.0f ns, producer loop %.0f ns, span %.1f us\n", a.M, a.N, a.K,
               stages, n, sw / n, tl / n, gap / (n - 1), iss / n, loop / (n - 1),
               (trace_buf[4 * 4096 + n - 1] - trace_buf[2 * 4096]) / 1e3);
+    // per-CTA milestones relative to the earliest CTA entry: min / median / max (us)
+    const int nb = std::min<int>(grid.x, 512);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < nb; ++b) t0 = std::min(t0, trace_buf[6 * 4096 + b * 8]);
+    const char* names[7] = {"entry", "pdl", "1st-full", "mma-done", "epi-done", "tail-done", "exit"};
+    for (int k = 0; k < 7; ++k) {
+      std::vector<double> v;
+      for (int b = 0; b < nb; ++b) {
+        const unsigned long long t = trace_buf[6 * 4096 + b * 8 + k];
+        if (t) v.push_back((t - t0) / 1e3);
+      }
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "[gemm trace]   %-9s n=%3zu min %6.2f med %6.2f max %6.2f us\n", names[k],
+              v.size(), v.front(), v[v.size() / 2], v.back());
+    }
   }
   if (e0 != cudaSuccess || !streamk) return e0;
   g_last_launches = 2;
