@@ -229,8 +229,9 @@ const char* sidp_last_error(void);
 /* ---- test hooks (parity tests of single kernels; same kernels as the hot path) ---------- */
 
 /* tcgen05 GEMM: out = epilogue(x[M,K] . w[N,K]^T).  epi: 0 fp32, 1 bf16, 2 bf16 + resid,
- * 3 SiLU(gate)*up over 128-row [gate 64 | up 64] tiles, 4 fused argmax (u64 packed; call
- * with out zeroed).  k_splits 0 = auto.  Device pointers; enqueued on stream. */
+ * 3 SiLU(gate)*up over 16-row [gate 8 | up 8] groups, 4 fused argmax (u64 packed; call
+ * with out zeroed).  k_splits 0 = auto, 1 = whole tiles, >1 = forced stream-K, -1 = token-major
+ * orientation (X as the UMMA A operand; not for epilogue 5).  Device pointers; enqueued on stream. */
 sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ldw, int32_t M,
                            int32_t N, int32_t K, int32_t epi, void* out, int32_t ldo,
                            const void* resid, int32_t ldr, const void* bias, int32_t k_splits,

@@ -17,8 +17,8 @@ enum GemmEpilogue : int {
   EPI_F32 = 0,        // out fp32 = acc (+ bias)
   EPI_BF16 = 1,       // out bf16 = acc (+ bias)
   EPI_RESID = 2,      // out bf16 = acc + resid (bf16); out may alias resid
-  EPI_SILU_MUL = 3,   // W rows interleaved per 128-row tile: [gate 64 | up 64];
-                      // out[m, f] bf16 = silu(gate) * up, f = tile*64 + i
+  EPI_SILU_MUL = 3,   // W rows interleaved in 16-row groups g: [gate 8g..8g+7 | up 8g..8g+7];
+                      // out[m, f] bf16 = silu(gate f) * up f, f = 8g + i
   EPI_ARGMAX = 4,     // fused argmax over n: packed (value, lowest index) into out u64[M]
   EPI_QKV = 5,        // fused QKV post-processing: (+bias) (qk-norm) RoPE -> q bf16, k/v -> KV cache
 };
@@ -42,7 +42,7 @@ struct GemmArgs {
   void* out; int ldo;
   const bf16* resid; int ldr;
   const bf16* bias;            // [N] or null
-  int k_splits;                // 0 = auto
+  int k_splits;                // 0 = auto, 1 = whole tiles, >1 stream-K, -1 = token-major (SW)
   int max_ctas;                // 0 = all SMs
   const QkvEpi* qkv;           // EPI_QKV only
 };

@@ -20,60 +20,81 @@ namespace sidp {
 namespace {
 
 // ---------------------------------------------------------------- qkv post
-__global__ void qkv_post_kernel(QkvPostArgs a) {
+// lane l holds dims [E*l, E*l+E) of the first half and the same dims + hd/2 (its RoPE
+// partners), E = hd/64: every load and store is one E-wide vector per lane
+template <int HD>
+__global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
   pdl_trigger();
   pdl_wait();
+  constexpr int half = HD / 2, E = HD / 64;
   // grid (B, ceil(nh / 8)): one warp per (token, head) so every load is issued up front
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hd = a.hd, half = hd / 2;
   const int nh = a.nq + 2 * a.nkv;
   const int nwarps = (blockDim.x >> 5) * gridDim.y;
   const int head0 = blockIdx.y * (blockDim.x >> 5) + warp;
   const int pos = a.pos[b];
-  const float2* rope = a.rope + (size_t)pos * half;
+  const int i0 = E * lane;
+  float cs[E][2];
+  {
+    const float* rp = reinterpret_cast<const float*>(a.rope + (size_t)pos * half + i0);
+    if constexpr (E == 2) {
+      const float4 t = *reinterpret_cast<const float4*>(rp);
+      cs[0][0] = t.x; cs[0][1] = t.y; cs[1][0] = t.z; cs[1][1] = t.w;
+    } else {
+      const float2 t = *reinterpret_cast<const float2*>(rp);
+      cs[0][0] = t.x; cs[0][1] = t.y;
+    }
+  }
   for (int head = head0; head < nh; head += nwarps) {
-    const float* src = a.qkv + ((size_t)b * nh + head) * hd;
+    const float* src = a.qkv + ((size_t)b * nh + head) * HD;
     const bool is_v = head >= a.nq + a.nkv;
     const bool is_q = head < a.nq;
-    float x1[2], x2[2];
-    const int ne = half / 32;   // 1 (hd 64) or 2 (hd 128)
-    for (int e = 0; e < ne; ++e) {
-      x1[e] = src[lane + 32 * e];
-      x2[e] = src[lane + 32 * e + half];
+    float x1[E], x2[E];
+    if constexpr (E == 2) {
+      const float2 u = *reinterpret_cast<const float2*>(src + i0);
+      const float2 w = *reinterpret_cast<const float2*>(src + i0 + half);
+      x1[0] = u.x; x1[1] = u.y; x2[0] = w.x; x2[1] = w.y;
+    } else {
+      x1[0] = src[i0];
+      x2[0] = src[i0 + half];
     }
     if (!is_v) {
       const bf16* gain = is_q ? a.gq : a.gk;
       if (gain) {
         float ss = 0.0f;
-        for (int e = 0; e < ne; ++e) ss += x1[e] * x1[e] + x2[e] * x2[e];
+#pragma unroll
+        for (int e = 0; e < E; ++e) ss += x1[e] * x1[e] + x2[e] * x2[e];
         ss = warp_sum(ss);
-        const float r = rsqrtf(ss / (float)hd + a.eps);
-        for (int e = 0; e < ne; ++e) {
-          const int i = lane + 32 * e;
-          x1[e] = x1[e] * r * bf16_to_f(gain[i]);
-          x2[e] = x2[e] * r * bf16_to_f(gain[i + half]);
+        const float r = rsqrtf(ss / (float)HD + a.eps);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          x1[e] = x1[e] * r * bf16_to_f(gain[i0 + e]);
+          x2[e] = x2[e] * r * bf16_to_f(gain[i0 + e + half]);
         }
       }
-      for (int e = 0; e < ne; ++e) {
-        const float2 cs = rope[lane + 32 * e];
-        const float y1 = x1[e] * cs.x - x2[e] * cs.y;
-        const float y2 = x2[e] * cs.x + x1[e] * cs.y;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const float y1 = x1[e] * cs[e][0] - x2[e] * cs[e][1];
+        const float y2 = x2[e] * cs[e][0] + x1[e] * cs[e][1];
         x1[e] = y1;
         x2[e] = y2;
       }
     }
     bf16* dst;
     if (is_q) {
-      dst = a.q + ((size_t)b * a.nq + head) * hd;
+      dst = a.q + ((size_t)b * a.nq + head) * HD;
     } else {
       const int g = is_v ? head - a.nq - a.nkv : head - a.nq;
       bf16* cache = is_v ? a.vc : a.kc;
-      dst = cache + (((size_t)b * a.nkv + g) * a.smax + pos) * hd;
+      dst = cache + (((size_t)b * a.nkv + g) * a.smax + pos) * HD;
     }
-    for (int e = 0; e < ne; ++e) {
-      dst[lane + 32 * e] = f_to_bf16(x1[e]);
-      dst[lane + 32 * e + half] = f_to_bf16(x2[e]);
+    if constexpr (E == 2) {
+      *reinterpret_cast<__nv_bfloat162*>(dst + i0) = __floats2bfloat162_rn(x1[0], x1[1]);
+      *reinterpret_cast<__nv_bfloat162*>(dst + i0 + half) = __floats2bfloat162_rn(x2[0], x2[1]);
+    } else {
+      dst[i0] = f_to_bf16(x1[0]);
+      dst[i0 + half] = f_to_bf16(x2[0]);
     }
   }
 }
@@ -349,7 +370,8 @@ cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s) {
   if (a.B <= 0) return cudaSuccess;
   if (a.hd != 64 && a.hd != 128) return cudaErrorInvalidValue;
   const int nh = a.nq + 2 * a.nkv;
-  return launch_pdl(qkv_post_kernel, dim3(a.B, (nh + 7) / 8), dim3(256), 0, s, a);
+  if (a.hd == 128) return launch_pdl(qkv_post_kernel<128>, dim3(a.B, (nh + 7) / 8), dim3(256), 0, s, a);
+  return launch_pdl(qkv_post_kernel<64>, dim3(a.B, (nh + 7) / 8), dim3(256), 0, s, a);
 }
 
 int attention_last_launch_count() { return g_attn_launches; }
@@ -401,7 +423,8 @@ cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
 cudaError_t attention_preload() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaSuccess;
-  if (cudaFuncGetAttributes(&fa, qkv_post_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, qkv_post_kernel<128>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, qkv_post_kernel<64>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, attn_kernel<128>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, attn_kernel<64>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, attn_combine_kernel<128>) != cudaSuccess) e = cudaGetLastError();

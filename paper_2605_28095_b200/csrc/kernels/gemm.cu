@@ -274,7 +274,7 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
       }
     }
   } else if constexpr (EPI == EPI_SILU_MUL) {
-    // this CTA's 128 W rows = [gate 64 | up 64] of packed tile pt -> outputs pt*64 .. +64
+    // this CTA's 128 W rows = 8 groups [gate 8 | up 8] of packed tile pt -> outputs pt*64 .. +64
     bf16* out = reinterpret_cast<bf16*>(p.out);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -285,7 +285,7 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
         float x[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float g = sm[j * SROW + f + q], u = sm[j * SROW + 64 + f + q];
+          const float g = sm[j * SROW + 2 * f + q], u = sm[j * SROW + 2 * f + 8 + q];
           x[q] = g / (1.0f + __expf(-g)) * u;
         }
         *reinterpret_cast<uint4*>(out + (size_t)m * p.ldo + of) = pack_bf16x8(x);
@@ -397,11 +397,88 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
   }
 }
 
+// Token-major (SW) epilogue: this thread holds fp32 accumulators of token m, features
+// n0..n0+31 (N is a multiple of 8, so 8-feature groups are all in or all out).
+template <int EPI>
+SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0,
+                        unsigned long long& best) {
+  if constexpr (EPI == EPI_F32) {
+    float* out = reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const int n = n0 + 4 * g;
+      if (n < p.N) {
+        float4 v = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                               __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
+        if (p.bias) {
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(p.bias + n);
+          const float2 b0 = __bfloat1622float2(b2[0]), b1 = __bfloat1622float2(b2[1]);
+          v.x += b0.x; v.y += b0.y; v.z += b1.x; v.w += b1.y;
+        }
+        *reinterpret_cast<float4*>(out + n) = v;
+      }
+    }
+  } else if constexpr (EPI == EPI_BF16 || EPI == EPI_RESID) {
+    bf16* out = reinterpret_cast<bf16*>(p.out) + (size_t)m * p.ldo;
+    uint4 addv[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {   // issue the residual / bias loads first
+      const int n = n0 + 8 * g;
+      addv[g] = make_uint4(0u, 0u, 0u, 0u);
+      if (n < p.N) {
+        if constexpr (EPI == EPI_RESID) addv[g] = *reinterpret_cast<const uint4*>(p.resid + (size_t)m * p.ldr + n);
+        else if (p.bias) addv[g] = *reinterpret_cast<const uint4*>(p.bias + n);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int n = n0 + 8 * g;
+      if (n < p.N) {
+        float y[8], x[8];
+        unpack_bf16x8(addv[g], y);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = __uint_as_float(r[8 * g + q]) + y[q];
+        *reinterpret_cast<uint4*>(out + n) = pack_bf16x8(x);
+      }
+    }
+  } else if constexpr (EPI == EPI_SILU_MUL) {
+    // columns [16h, 16h+16) = one [gate 8 | up 8] group -> outputs (n0 + 16h) / 2 .. +8
+    bf16* out = reinterpret_cast<bf16*>(p.out) + (size_t)m * p.ldo;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = n0 + 16 * h;
+      if (n < p.N) {
+        float x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float g = __uint_as_float(r[16 * h + q]), u = __uint_as_float(r[16 * h + 8 + q]);
+          x[q] = g / (1.0f + __expf(-g)) * u;
+        }
+        *reinterpret_cast<uint4*>(out + n / 2) = pack_bf16x8(x);
+      }
+    }
+  } else if constexpr (EPI == EPI_ARGMAX) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      if (n0 + q < p.N) {
+        const unsigned long long k2 = argmax_key(__uint_as_float(r[q]), n0 + q);
+        best = k2 > best ? k2 : best;
+      }
+    }
+  }
+}
+
 // perf experiment timeline: per CTA, slot k of TL(k) = globaltimer at a kernel milestone
 #define SIDP_TL(k) \
   do { if (p.trace && blockIdx.x < 512) p.trace[6 * 4096 + blockIdx.x * 8 + (k)] = globaltimer_ns(); } while (0)
 
-template <int EPI, int KPS>
+// SW = false: A = W (128 rows per CTA, 256-feature pair tile), B = tokens (BNT per pair).
+// SW = true (token-major, large batches): A = X (128 tokens per CTA, 256-token pair tile),
+//   B = W (BNT features per pair, any multiple of 32), so the feature tile can be sized to give
+//   every CTA pair work without splitting K; TMEM lanes are tokens, columns features, and the
+//   epilogue writes each thread's token row straight from registers.  The mainloop is the same
+//   code: the host passes the X map as tm_w and the W map as tm_x.
+template <int EPI, int KPS, bool SW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
              const KParams p) {
@@ -427,7 +504,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  const uint32_t tmem_cols = BNT <= 16 ? 32 : (BNT <= 32 ? 64 : (BNT <= 64 ? 128 : (BNT <= 128 ? 256 : 512)));
+  const int ACCS = (BNT + 31) / 32 * 32;                 // TMEM columns per accumulator
+  const uint32_t tmem_cols = ACCS <= 16 ? 32 : (ACCS <= 32 ? 64 : (ACCS <= 64 ? 128 : (ACCS <= 128 ? 256 : 512)));
 
   if (threadIdx.x == 0) {
     SIDP_TL(0);
@@ -465,13 +543,13 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
       // beyond the shared-memory ring, so a TMA load sees L2 rather than HBM latency.
       KbCursor pf;
       pf.init(p, cluster);
-      for (int i = 0; i < p.prefetch_kb && pf.valid; ++i, pf.advance(p, cluster))
+      for (int i = 0; !SW && i < p.prefetch_kb && pf.valid; ++i, pf.advance(p, cluster))
         tma_prefetch_l2_2d(&tm_w, pf.kb * KPS * BK, pf.x.ft * 2 * WROWS + rank * WROWS);
       while (ui.next(p, cluster, x)) {
         for (int kb = x.kb0; kb < x.kb1; ++kb, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
-          if (pf.valid) {
+          if (!SW && pf.valid) {
             tma_prefetch_l2_2d(&tm_w, pf.kb * KPS * BK, pf.x.ft * 2 * WROWS + rank * WROWS);
             pf.advance(p, cluster);
           }
@@ -511,7 +589,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         ++un;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
-        const uint32_t dcol = tmem_base + acc * BNT;
+        const uint32_t dcol = tmem_base + acc * ACCS;
         for (int kb = x.kb0; kb < x.kb1; ++kb, ++it) {
           const int s = it % stages;
           const uint32_t ph = (it / stages) & 1;
@@ -545,55 +623,94 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int quarter = warp & 3;                       // TMEM lane quarter of this warp
-    const int row = quarter * 32 + lane;                // W row within this CTA (feature)
+    const int row = quarter * 32 + lane;                // TMEM lane (W row, or token if SW)
     const int tid = (warp - 2) * 32 + lane;             // 0..127
-    int un = 0;
-    UnitIter ui;
-    ui.init(p, cluster);
-    Unit x;
-    while (ui.next(p, cluster, x)) {
-      const int acc = un & 1;
-      const uint32_t aph = (un >> 1) & 1;
-      ++un;
-      const int n0 = x.ft * 2 * WROWS + rank * WROWS;
-      const int pt = x.ft * 2 + rank;
-      const int mbase = x.mt * BNT;
-      const int nchunks = min(BNT, ((p.M - mbase + 31) / 32) * 32) / 32;
-      float* part = p.ws + (size_t)x.seg * p.M * p.N;   // partial slice (nseg > 1 only)
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      const uint32_t tl = tmem_base + acc * BNT + ((uint32_t)(quarter * 32) << 16);
-      for (int c = 0; c < nchunks; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tl + c * 32, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
-        if (c == nchunks - 1) {   // last TMEM read of this accumulator: hand it back early
+    if constexpr (SW) {
+      int un = 0;
+      UnitIter ui;
+      ui.init(p, cluster);
+      Unit x;
+      while (ui.next(p, cluster, x)) {
+        const int acc = un & 1;
+        const uint32_t aph = (un >> 1) & 1;
+        ++un;
+        const int m = x.ft * 2 * WROWS + rank * WROWS + row;   // this thread's token
+        const int fbase = x.mt * BNT;                           // first feature of the tile
+        const int nch = (min(BNT, p.N - fbase) + 31) / 32;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tl = tmem_base + acc * ACCS + ((uint32_t)(quarter * 32) << 16);
+        unsigned long long best = 0ull;
+        for (int c = 0; c < nch; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tl + c * 32, r);
+          tmem_ld_wait();
+          if (c == nch - 1) {   // last TMEM read of this accumulator: hand it back early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          }
+          const int n0 = fbase + c * 32;
+          if (m < p.M) store_row<EPI>(p, r, m, n0, best);
+        }
+        if (nch <= 0) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
-        named_bar_sync(1, 128);
-        if (x.nseg == 1) {
-          store_phase<EPI>(p, stg, mbase + c * 32, n0, pt, tid);
-        } else {
-          // partial of this k-range -> ws[seg][m][n] (token-major, coalesced 16-byte stores)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
-            const int m = mbase + c * 32 + j, n = n0 + f;
-            if (m < p.M && n < p.N)
-              __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N + n),
-                     *reinterpret_cast<const float4*>(stg + j * SROW + f));
-          }
+        if constexpr (EPI == EPI_ARGMAX) {
+          if (m < p.M && best) atomicMax(reinterpret_cast<unsigned long long*>(p.out) + m, best);
         }
-        named_bar_sync(1, 128);
       }
-      if (nchunks == 0) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+    } else {
+      int un = 0;
+      UnitIter ui;
+      ui.init(p, cluster);
+      Unit x;
+      while (ui.next(p, cluster, x)) {
+        const int acc = un & 1;
+        const uint32_t aph = (un >> 1) & 1;
+        ++un;
+        const int n0 = x.ft * 2 * WROWS + rank * WROWS;
+        const int pt = x.ft * 2 + rank;
+        const int mbase = x.mt * BNT;
+        const int nchunks = min(BNT, ((p.M - mbase + 31) / 32) * 32) / 32;
+        float* part = p.ws + (size_t)x.seg * p.M * p.N;   // partial slice (nseg > 1 only)
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tl = tmem_base + acc * ACCS + ((uint32_t)(quarter * 32) << 16);
+        for (int c = 0; c < nchunks; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tl + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
+          if (c == nchunks - 1) {   // last TMEM read of this accumulator: hand it back early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          }
+          named_bar_sync(1, 128);
+          if (x.nseg == 1) {
+            store_phase<EPI>(p, stg, mbase + c * 32, n0, pt, tid);
+          } else {
+            // partial of this k-range -> ws[seg][m][n] (token-major, coalesced 16-byte stores)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
+              const int m = mbase + c * 32 + j, n = n0 + f;
+              if (m < p.M && n < p.N)
+                __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N + n),
+                       *reinterpret_cast<const float4*>(stg + j * SROW + f));
+            }
+          }
+          named_bar_sync(1, 128);
+        }
+        if (nchunks == 0) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        }
       }
     }
     if (tid == 0) SIDP_TL(4);
@@ -643,8 +760,8 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
     for (int q = 0; q < 8; ++q) a[q] = b[q] = 0.0f;
     int na = f, nb = 0;
     if constexpr (EPI == EPI_SILU_MUL) {
-      na = (f / 64) * 128 + (f % 64);   // gate rows of packed tile f/64
-      nb = na + 64;                     // matching up rows
+      na = 2 * f;                       // gate rows of 16-row group f/8 (f multiple of 8)
+      nb = na + 8;                      // matching up rows
     }
     const float* base = p.ws + (size_t)m * p.N;
 #pragma unroll 4
@@ -745,19 +862,36 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
 int g_num_sms = 0;
 thread_local int g_last_launches = 0;
 
+// the token-major variant exists for every epilogue but the fused QKV one
+template <int EPI>
+constexpr bool kHasSw = EPI != EPI_QKV;
+
 template <int EPI>
 void set_attr() {
-  cudaFuncSetAttribute(gemm2_kernel<EPI, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gemm2_kernel<EPI, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kSmemBudget + 1024);
-  cudaFuncSetAttribute(gemm2_kernel<EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(gemm2_kernel<EPI, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kSmemBudget + 1024);
+  if constexpr (kHasSw<EPI>) {
+    cudaFuncSetAttribute(gemm2_kernel<EPI, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBudget + 1024);
+    cudaFuncSetAttribute(gemm2_kernel<EPI, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBudget + 1024);
+  }
 }
 
 template <int EPI>
-cudaError_t launch_gemm2(int kps, dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& tw,
-                         const CUtensorMap& tx, const KParams& p) {
-  if (kps == 2) return launch_pdl(gemm2_kernel<EPI, 2>, grid, dim3(kThreads), smem, st, tw, tx, p);
-  return launch_pdl(gemm2_kernel<EPI, 1>, grid, dim3(kThreads), smem, st, tw, tx, p);
+cudaError_t launch_gemm2(int kps, bool sw, dim3 grid, size_t smem, cudaStream_t st,
+                         const CUtensorMap& tw, const CUtensorMap& tx, const KParams& p) {
+  if constexpr (kHasSw<EPI>) {
+    if (sw) {
+      if (kps == 2) return launch_pdl(gemm2_kernel<EPI, 2, true>, grid, dim3(kThreads), smem, st, tw, tx, p);
+      return launch_pdl(gemm2_kernel<EPI, 1, true>, grid, dim3(kThreads), smem, st, tw, tx, p);
+    }
+  }
+  if (sw) return cudaErrorInvalidValue;
+  if (kps == 2) return launch_pdl(gemm2_kernel<EPI, 2, false>, grid, dim3(kThreads), smem, st, tw, tx, p);
+  return launch_pdl(gemm2_kernel<EPI, 1, false>, grid, dim3(kThreads), smem, st, tw, tx, p);
 }
 
 }  // namespace
@@ -787,7 +921,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   if (a.M <= 0) return cudaSuccess;
   if (a.K % BK != 0 || a.N <= 0 || a.N % 8 != 0 || a.x == nullptr || a.w == nullptr)
     return cudaErrorInvalidValue;
-  if (a.epi == EPI_SILU_MUL && (a.N % WROWS) != 0) return cudaErrorInvalidValue;
+  if (a.epi == EPI_SILU_MUL && (a.N % 16) != 0) return cudaErrorInvalidValue;
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -801,25 +935,61 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   }
   static int env_bnt = getenv("SIDP_GEMM_BNT") ? atoi(getenv("SIDP_GEMM_BNT")) : 256;
   static int env_stages = getenv("SIDP_GEMM_STAGES") ? atoi(getenv("SIDP_GEMM_STAGES")) : 12;
+  // token-major (SW) orientation from this many tokens up (0 = never); X-tile overhead in
+  // equivalent W rows for the feature-tile choice
+  static int env_sw_min = getenv("SIDP_GEMM_SW_MIN_M") ? atoi(getenv("SIDP_GEMM_SW_MIN_M")) : 128;
+  static int env_sw_c0 = getenv("SIDP_GEMM_SW_C0") ? atoi(getenv("SIDP_GEMM_SW_C0")) : 64;
+  static int env_sw_bnf = getenv("SIDP_GEMM_SW_BNF") ? atoi(getenv("SIDP_GEMM_SW_BNF")) : 0;
   const int sms = a.max_ctas > 0 ? std::min(a.max_ctas, g_num_sms) : g_num_sms;
   const int pair_slots = std::max(1, sms / 2);
-  int BNT = ((a.M + 31) / 32) * 32;
-  BNT = std::max(32, std::min(env_bnt, BNT));
-  const int m_tiles = (a.M + BNT - 1) / BNT;
-  const int n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
   const int nkb_blocks = a.K / BK;
   static int env_kps = getenv("SIDP_GEMM_KPS") ? atoi(getenv("SIDP_GEMM_KPS")) : 2;
   const int kps = (env_kps == 2 && nkb_blocks % 2 == 0) ? 2 : 1;
   const int nkb = nkb_blocks / kps;   // k-steps per tile (the unit of stream-K work)
+  if (a.epi == EPI_QKV && (!a.qkv || (a.qkv->hd != 64 && a.qkv->hd != 128))) return cudaErrorInvalidValue;
+  // SW pays where whole 256-feature tiles would leave CTA pairs idle but are too many for
+  // stream-K (e.g. QKV: 40 tiles on 74 pairs): the token tile is re-read per feature tile
+  // (256/BNF x the W traffic from L2), so shapes that already fill the machine stay W-major.
+  // SIDP_GEMM_SW = 0 never, 1 auto (default), 2 whenever M >= SIDP_GEMM_SW_MIN_M.
+  static int env_sw = getenv("SIDP_GEMM_SW") ? atoi(getenv("SIDP_GEMM_SW")) : 1;
+  const int wm_tiles = ((a.N + 2 * WROWS - 1) / (2 * WROWS)) *
+                       ((a.M + std::min(256, env_bnt) - 1) / std::min(256, env_bnt));
+  const bool underfilled = 2 * wm_tiles > pair_slots && wm_tiles < pair_slots;
+  const bool sw = a.k_splits < 0 ? a.epi != EPI_QKV
+                                  : (env_sw > 0 && env_sw_min > 0 && a.M >= env_sw_min &&
+                                     a.epi != EPI_QKV && a.k_splits <= 1 && (env_sw == 2 || underfilled));
+  int BNT, m_tiles, n_pairs;
+  if (sw) {
+    // feature tile BNF (UMMA N, multiple of 16) minimising rounds x (BNF + c0): whole tiles
+    // on every pair without splitting K (cost ~ W rows + the re-read token tile per tile)
+    const int tok_pairs = (a.M + 2 * WROWS - 1) / (2 * WROWS);
+    int best = 256;
+    double best_c = 1e30;
+    // BNF multiple of 32: with cta_group::2 each CTA supplies BNF/2 B rows, which must be a
+    // multiple of 16 (BNF = 16 or 80 gives wrong results on sm_100a, measured)
+    for (int bnf = 256; bnf >= 32; bnf -= 32) {
+      const long long t = (long long)tok_pairs * ((a.N + bnf - 1) / bnf);
+      const double c = (double)((t + pair_slots - 1) / pair_slots) * (bnf + env_sw_c0);
+      if (c < best_c - 1e-9) { best_c = c; best = bnf; }
+    }
+    if (env_sw_bnf >= 32 && env_sw_bnf <= 256 && env_sw_bnf % 32 == 0) best = env_sw_bnf;
+    BNT = best;
+    m_tiles = (a.N + BNT - 1) / BNT;   // feature tiles (fastest)
+    n_pairs = tok_pairs;               // token-pair tiles
+  } else {
+    BNT = ((a.M + 31) / 32) * 32;
+    BNT = std::max(32, std::min(env_bnt, BNT));
+    m_tiles = (a.M + BNT - 1) / BNT;
+    n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
+  }
   const int tiles = n_pairs * m_tiles;
   // stream-K over all pairs unless the epilogue needs whole dot products (fused argmax) or the
   // caller pins whole tiles (k_splits == 1); max segments per tile bounds the workspace
   int clusters = pair_slots;
   // whole tiles balance well once every pair has >= 1 tile (measured: qkv 40 tiles, gate/up
   // 200 tiles faster whole); stream-K pays off for heavily underfilled shapes (O, down: 20)
-  if (a.epi == EPI_QKV && (!a.qkv || (a.qkv->hd != 64 && a.qkv->hd != 128))) return cudaErrorInvalidValue;
   // whole-row epilogues (argmax over a tile, per-head qk-norm/RoPE) need whole dot products
-  int streamk = (a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.k_splits != 1 &&
+  int streamk = (!sw && a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.k_splits != 1 &&
                  (a.k_splits > 1 || 2 * tiles <= clusters)) ? 1 : 0;
   if (streamk) {
     const long long total = (long long)tiles * nkb;
@@ -834,9 +1004,14 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   int stages = (int)std::min<size_t>(env_stages, (kSmemBudget - extra) / stage_bytes);
   stages = std::max(2, stages);
 
-  CUtensorMap tw, tx;
-  if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, WROWS)) return cudaErrorInvalidValue;
-  if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) return cudaErrorInvalidValue;
+  CUtensorMap tw, tx;   // A operand map (128 rows per CTA), B operand map (BNT/2 rows per CTA)
+  if (sw) {
+    if (!make_tmap_2d(&tw, a.x, a.K, a.M, a.ldx, BK, WROWS)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&tx, a.w, a.K, a.N, a.ldw, BK, BNT / 2)) return cudaErrorInvalidValue;
+  } else {
+    if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, WROWS)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) return cudaErrorInvalidValue;
+  }
 
   KParams p;
   p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
@@ -861,12 +1036,12 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   dim3 grid(2 * clusters);
   cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
   switch (a.epi) {
-    case EPI_F32: e0 = launch_gemm2<EPI_F32>(kps, grid, smem, stream, tw, tx, p); break;
-    case EPI_BF16: e0 = launch_gemm2<EPI_BF16>(kps, grid, smem, stream, tw, tx, p); break;
-    case EPI_RESID: e0 = launch_gemm2<EPI_RESID>(kps, grid, smem, stream, tw, tx, p); break;
-    case EPI_SILU_MUL: e0 = launch_gemm2<EPI_SILU_MUL>(kps, grid, smem, stream, tw, tx, p); break;
-    case EPI_ARGMAX: e0 = launch_gemm2<EPI_ARGMAX>(kps, grid, smem, stream, tw, tx, p); break;
-    case EPI_QKV: e0 = launch_gemm2<EPI_QKV>(kps, grid, smem, stream, tw, tx, p); break;
+    case EPI_F32: e0 = launch_gemm2<EPI_F32>(kps, sw, grid, smem, stream, tw, tx, p); break;
+    case EPI_BF16: e0 = launch_gemm2<EPI_BF16>(kps, sw, grid, smem, stream, tw, tx, p); break;
+    case EPI_RESID: e0 = launch_gemm2<EPI_RESID>(kps, sw, grid, smem, stream, tw, tx, p); break;
+    case EPI_SILU_MUL: e0 = launch_gemm2<EPI_SILU_MUL>(kps, sw, grid, smem, stream, tw, tx, p); break;
+    case EPI_ARGMAX: e0 = launch_gemm2<EPI_ARGMAX>(kps, sw, grid, smem, stream, tw, tx, p); break;
+    case EPI_QKV: e0 = launch_gemm2<EPI_QKV>(kps, false, grid, smem, stream, tw, tx, p); break;
     default: return cudaErrorInvalidValue;
   }
   g_last_launches = 1;
@@ -924,12 +1099,17 @@ cudaError_t gemm_preload() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaSuccess;
 #define SIDP_PRELOAD(k) if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) e = cudaGetLastError();
-  SIDP_PRELOAD((gemm2_kernel<EPI_F32, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_F32, 2>))
-  SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 2>))
-  SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 2>))
-  SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 2>))
-  SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2>))
-  SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_F32, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_F32, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_F32, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_F32, 2, true>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_BF16, 2, true>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_RESID, 2, true>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_SILU_MUL, 2, true>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2, true>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2, false>))
   SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
   SIDP_PRELOAD((gemm_reduce_kernel<EPI_RESID>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_SILU_MUL>))
 #undef SIDP_PRELOAD

@@ -42,11 +42,11 @@ __global__ void gen_kernel(GenArgs a, float wscale) {
     const int64_t r = e / a.cols, c = e % a.cols;
     int tensor = a.tensor;
     int64_t lrow = a.row0 + r;
-    if (a.row_map == 1) {            // packed gate/up: 128-row tile t = [gate 64t.. | up 64t..]
+    if (a.row_map == 1) {            // packed gate/up: 16-row group g = [gate 8g.. | up 8g..]
       const int64_t pr = a.row0 + r;
-      const int64_t t = pr / 128, i = pr % 128;
-      tensor = i < 64 ? kTensorWGate : kTensorWUp;
-      lrow = t * 64 + (i & 63);
+      const int64_t g = pr / 16, i = pr % 16;
+      tensor = i < 8 ? kTensorWGate : kTensorWUp;
+      lrow = g * 8 + (i & 7);
     }
     const uint64_t idx = (uint64_t)(lrow * a.lcols + c);
     a.dst[r * a.ld + c] = f_to_bf16(gen_value(a.seed, tensor, a.layer, idx, a.kind, wscale));

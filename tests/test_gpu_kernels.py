@@ -42,8 +42,8 @@ def test_gen_gate_up_interleave_bit_exact(P):
     P.test_gen(dst, SEED, gen.WGATE, 1, 0, scale_k=K, row_map=1)
     g = gen.weight(SEED, gen.WGATE, 1, I, K)
     u = gen.weight(SEED, gen.WUP, 1, I, K)
-    ref = np.concatenate([np.concatenate([g[64 * t:64 * t + 64], u[64 * t:64 * t + 64]])
-                          for t in range(I // 64)])
+    ref = np.concatenate([np.concatenate([g[8 * t:8 * t + 8], u[8 * t:8 * t + 8]])
+                          for t in range(I // 8)])
     assert torch.equal(dst.cpu().double(), torch.from_numpy(ref))
 
 
@@ -73,7 +73,7 @@ SHAPES = [(1, 128, 64), (8, 256, 256), (16, 384, 512), (37, 1000, 320), (100, 64
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
-@pytest.mark.parametrize("splits", [1, 3, 0])
+@pytest.mark.parametrize("splits", [1, 3, 0, -1])
 def test_gemm_f32(P, M, N, K, splits):
     g = torch.Generator().manual_seed(M * 7 + N + K)
     x = _lvl((M, K), g).cuda()
@@ -87,13 +87,14 @@ def test_gemm_f32(P, M, N, K, splits):
 
 
 @pytest.mark.parametrize("M,N,K", [(8, 256, 256), (37, 1000, 320), (256, 512, 2048)])
-def test_gemm_bf16_bias_and_residual(P, M, N, K):
+@pytest.mark.parametrize("orient", [0, -1])
+def test_gemm_bf16_bias_and_residual(P, M, N, K, orient):
     g = torch.Generator().manual_seed(1)
     x = _lvl((M, K), g).cuda()
     w = _lvl((N, K), g, 2.0 ** -5).cuda()
     bias = _lvl((N,), g, 0.125).cuda()
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    P.test_gemm(x, w, out, M, N, K, 1, bias=bias, k_splits=2)
+    P.test_gemm(x, w, out, M, N, K, 1, bias=bias, k_splits=2 if orient == 0 else -1)
     ref = x.cpu().double() @ w.cpu().double().T + bias.cpu().double()
     torch.cuda.synchronize()
     d = (out.cpu().double() - ref).abs()
@@ -101,19 +102,20 @@ def test_gemm_bf16_bias_and_residual(P, M, N, K):
     # residual, in place (out aliases resid)
     r = _lvl((M, N), g).cuda()
     ref2 = x.cpu().double() @ w.cpu().double().T + r.cpu().double()
-    P.test_gemm(x, w, r, M, N, K, 2, resid=r)
+    P.test_gemm(x, w, r, M, N, K, 2, resid=r, k_splits=orient)
     torch.cuda.synchronize()
     d2 = (r.cpu().double() - ref2).abs()
     assert (d2 <= ref2.abs() * 2.0 ** -8 + 1e-6 * ref2.abs().max()).all()
 
 
-@pytest.mark.parametrize("M,F,K,splits", [(8, 64, 256, 1), (33, 192, 512, 0), (256, 640, 1024, 4)])
+@pytest.mark.parametrize("M,F,K,splits", [(8, 64, 256, 1), (33, 192, 512, 0), (256, 640, 1024, 4),
+                                          (200, 328, 512, -1), (300, 1040, 256, -1), (40, 200, 256, -1)])
 def test_gemm_silu_mul(P, M, F, K, splits):
     g = torch.Generator().manual_seed(2)
     x = _lvl((M, K), g).cuda()
     wg = _lvl((F, K), g, 2.0 ** -4)
     wu = _lvl((F, K), g, 2.0 ** -4)
-    packed = torch.cat([torch.cat([wg[64 * t:64 * t + 64], wu[64 * t:64 * t + 64]]) for t in range(F // 64)]).cuda()
+    packed = torch.cat([torch.cat([wg[8 * t:8 * t + 8], wu[8 * t:8 * t + 8]]) for t in range(F // 8)]).cuda()
     out = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
     P.test_gemm(x, packed, out, M, 2 * F, K, 3, k_splits=splits)
     torch.cuda.synchronize()
@@ -125,12 +127,13 @@ def test_gemm_silu_mul(P, M, F, K, splits):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 1024, 256), (8, 151936 // 8, 512), (200, 2000, 256)])
-def test_gemm_fused_argmax(P, M, N, K):
+@pytest.mark.parametrize("orient", [0, -1])
+def test_gemm_fused_argmax(P, M, N, K, orient):
     g = torch.Generator().manual_seed(3)
     x = _lvl((M, K), g).cuda()
     w = _lvl((N, K), g, 2.0 ** -4).cuda()
     packed = torch.zeros(M, dtype=torch.int64, device="cuda")
-    P.test_gemm(x, w, packed, M, N, K, 4, ldo=0)
+    P.test_gemm(x, w, packed, M, N, K, 4, ldo=0, k_splits=orient)
     logits = torch.empty(M, N, dtype=torch.float32, device="cuda")
     P.test_gemm(x, w, logits, M, N, K, 0)
     torch.cuda.synchronize()
