@@ -45,6 +45,7 @@ struct GemmArgs {
   int k_splits;                // 0 = auto, 1 = whole tiles, >1 stream-K, -1 = token-major (SW)
   int max_ctas;                // 0 = all SMs
   const QkvEpi* qkv;           // EPI_QKV only
+  int w_kbmajor;               // 1: W is k-block-major [K/64][N][64] (one 3-D TMA box per stage)
 };
 
 struct GemmWorkspace {
@@ -79,8 +80,9 @@ struct AttnArgs {
   const int32_t* pos;         // attend over [0, pos_b]
   bf16* o;                    // [B, nq*hd]
   int B, nq, nkv, hd, smax;
-  int max_tokens;             // host hint: max_b (pos_b + 1) <= smax (sizes the split)
-  float* ws; size_t ws_bytes; // split-KV partials
+  int max_tokens;             // host hint: max_b (pos_b + 1) <= smax (sizes the grid)
+  float* ws; size_t ws_bytes; // partials of (b, g) pairs split across CTAs
+  int* cnt; int n_cnt;        // [B * nkv] arrival counters, zero between launches
 };
 cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s);
 int attention_last_launch_count();

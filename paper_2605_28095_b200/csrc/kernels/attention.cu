@@ -5,12 +5,19 @@
 // The KV cache is local and never pooled.
 //
 // decode attention: HBM-bound (4096 B of K/V per context token per layer).
-// One CTA per (kv head, sequence, split), 4 warps; each warp streams 16-token K/V chunks
-// through a 2-stage cp.async ring in XOR-swizzled shared memory and runs the G query heads
-// of the group (padded to 16 rows) through mma.sync m16n8k16 bf16 tensor-core tiles for
-// S = q K^T and O += P V, with an fp32 online softmax (exp2 domain).  Warps and splits are
-// merged with the usual (max, sum) rescaling.
+// The batch's 16-token K/V chunks are split into equal contiguous ranges, one per CTA (one
+// (sequence, kv head) pair per CTA for uniform contexts; pairs split into pieces for small
+// batches / long or ragged contexts, see attn_kernel).  4 warps per CTA; each warp streams
+// chunks through a 3-stage cp.async ring in XOR-swizzled shared memory and runs the G query
+// heads of the group (padded to 16 rows) through mma.sync m16n8k16 bf16 tensor-core tiles for
+// S = q K^T and O += P V, with an fp32 online softmax (exp2 domain).  Warps and pieces are
+// merged with the usual (max, sum) rescaling.  Measured on the M2 shape (B=256, 1025-token
+// contexts, 16 layers): 3 stages (96 KB, 2 CTAs/SM by registers) 181 us vs 2 stages 188 us
+// (forcing 3 CTAs/SM with 2 stages spills: 197 us) and 4 stages 214 us; a single wave of
+// persistent CTAs over pieces loses to one pair per CTA (per-piece prologue/merge cost).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "../common.cuh"
 #include "../kernels.h"
@@ -140,224 +147,387 @@ struct AttnParams {
   const bf16* vc;
   const int32_t* pos;
   bf16* o;
-  float* ws;
-  int nq, nkv, smax, splits, tok_per_split;
+  float* ws;                 // [C][2 sides][16 rows][HD + 2] partials of split (b, g) pairs
+  int* cnt;                  // [B * nkv] arrival counters of split pairs (zero between launches)
+  int B, nq, nkv, smax;
+  int pair_mode;             // grid == B * nkv: one whole (b, g) pair per CTA
   float scale_log2;
 };
 
 constexpr int kChunk = 16;
 constexpr int kWarps = 4;
 
-template <int HD>
+// CTA owning global chunk index c when W chunks are split into C ranges [floor(iW/C), ...)
+__device__ __forceinline__ int cta_of_chunk(long long c, long long W, int C) {
+  return (int)(((c + 1) * (long long)C + W - 1) / W) - 1;
+}
+__device__ __forceinline__ long long chunk_begin(int i, long long W, int C) {
+  return (long long)i * W / C;
+}
+
+// Work decomposition: the (sequence b, kv head g) pairs, b-major, each hold
+// ceil((pos_b + 1) / 16) 16-token chunks; the W chunks of the whole batch are split into
+// gridDim.x equal contiguous ranges, one per resident CTA (a single wave: no tail, and ragged
+// context lengths balance by construction).  A CTA walks the pairs its range touches; a pair
+// covered by one CTA is finished in place, a pair split over several CTAs ("pieces") has each
+// piece write its (max, sum, O) partial, and the last piece to arrive merges all pieces in
+// piece order (deterministic) and writes o.  Inside a piece the 4 warps take chunks round
+// robin through a 2-stage cp.async ring and merge through shared memory.
+template <int HD, int ST>
 __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int CPR = HD / 8;                         // 16-byte chunks per row
   constexpr int TILE = kChunk * HD;                   // elements per K (or V) chunk
+  constexpr size_t kRingBytes = (size_t)kWarps * ST * 2 * TILE * 2;   // ST-stage ring per warp
   pdl_trigger();
   pdl_wait();
-  const int g = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tq = lane & 3;
   const int G = p.nq / p.nkv;
-  const int n_tok = p.pos[b] + 1;
-  const int t_begin = split * p.tok_per_split;
-  const int t_end = min(n_tok, t_begin + p.tok_per_split);
-  const int nchunks = t_end > t_begin ? (t_end - t_begin + kChunk - 1) / kChunk : 0;
+  const int C = gridDim.x, cta = blockIdx.x;
+  int* cum = reinterpret_cast<int*>(smem + kRingBytes);   // [B + 1] chunk prefix sums
+  __shared__ int s_last;
 
-  bf16* wbuf = reinterpret_cast<bf16*>(smem) + (size_t)warp * 4 * TILE;   // [stage][K|V]
-  const bf16* kbase = p.kc + ((size_t)b * p.nkv + g) * p.smax * HD;
-  const bf16* vbase = p.vc + ((size_t)b * p.nkv + g) * p.smax * HD;
-
-  // Q fragments (rows = heads of the group, padded to 16)
-  uint32_t qa[HD / 16][4];
-  {
-    const bf16* qb = p.q + ((size_t)b * p.nq + (size_t)g * G) * HD;
-    const int r0 = gid, r1 = gid + 8;
+  // ---- pair mode (grid = B * nkv pairs): CTA i is pair i, no prefix sums needed
+  // ---- otherwise: prefix sums of per-sequence chunk counts (block scan, 128 threads)
+  if (!p.pair_mode) {
+    const int per = (p.B + 127) / 128;
+    const int e0 = threadIdx.x * per, e1 = min(p.B, e0 + per);
+    int local = 0;
+    for (int e = e0; e < e1; ++e) local += (p.pos[e] + kChunk) / kChunk;
+    int incl = local;
 #pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      const int c = kk * 16 + 2 * tq;
-      qa[kk][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(qb + r0 * HD + c) : 0u;
-      qa[kk][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + c) : 0u;
-      qa[kk][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(qb + r0 * HD + c + 8) : 0u;
-      qa[kk][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + c + 8) : 0u;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
+    __shared__ int wsum[kWarps];
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    int run = off + incl - local;
+    if (threadIdx.x == 0) cum[0] = 0;
+    for (int e = e0; e < e1; ++e) {
+      run += (p.pos[e] + kChunk) / kChunk;
+      cum[e + 1] = run;
+    }
+    __syncthreads();
   }
-
-  float o[HD / 8][4];
-#pragma unroll
-  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
-  float mrow[2] = {-INFINITY, -INFINITY};
-  float lrow[2] = {0.0f, 0.0f};
-
-  auto load_chunk = [&](int stage, int c) {
-    const int t0 = t_begin + c * kChunk;
-    bf16* sk = wbuf + stage * 2 * TILE;
-    bf16* sv = sk + TILE;
-#pragma unroll
-    for (int it = 0; it < (kChunk * CPR) / 32; ++it) {
-      const int e = it * 32 + lane;
-      const int row = e / CPR, cc = e % CPR;
-      const int t = min(t0 + row, n_tok - 1);
-      const int sw = (cc ^ (row & 7));
-      cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
-      cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+  const long long W = p.pair_mode ? 1 : (long long)p.nkv * cum[p.B];
+  const long long c0 = p.pair_mode ? 0 : chunk_begin(cta, W, C);
+  const long long c1 = p.pair_mode ? 1 : chunk_begin(cta + 1, W, C);
+  if (c0 >= c1) return;
+  // sequence holding c0: largest b with nkv * cum[b] <= c0
+  int b = 0;
+  if (!p.pair_mode) {
+    int lo = 0, hi = p.B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((long long)p.nkv * cum[mid] <= c0) lo = mid; else hi = mid - 1;
     }
-  };
-
-  if (warp < nchunks) load_chunk(0, warp);
-  cp_async_commit();
-  int it = 0;
-  for (int c = warp; c < nchunks; c += kWarps, ++it) {
-    const int cn = c + kWarps;
-    if (cn < nchunks) load_chunk((it + 1) & 1, cn);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
-    const bf16* sk = wbuf + (it & 1) * 2 * TILE;
-    const bf16* sv = sk + TILE;
-    const uint32_t skb = smem_u32(sk), svb = smem_u32(sv);
-    const int t0 = t_begin + c * kChunk;
-
-    // S = Q K^T for 16 tokens (two n-tiles of 8)
-    float s[2][4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.0f;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      const int mat = lane >> 3, r = lane & 7;
-      const int tok = (mat >> 1) * 8 + r;
-      const int cc = kk * 2 + (mat & 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
-      mma_bf16(s[0], qa[kk], b0, b1);
-      mma_bf16(s[1], qa[kk], b2, b3);
+    b = lo;
+  }
+  bf16* wring = reinterpret_cast<bf16*>(smem);
+  long long c = c0;
+  while (c < c1) {
+    int g, chb, lo, hi, side;
+    long long pstart, pend;
+    if (p.pair_mode) {
+      b = cta / p.nkv;
+      g = cta % p.nkv;
+      chb = (p.pos[b] + kChunk) / kChunk;
+      lo = 0; hi = chb; side = 0; pstart = 0; pend = chb;
+      c = c1;
+    } else {
+      chb = cum[b + 1] - cum[b];
+      const long long base_b = (long long)p.nkv * cum[b];
+      if (c >= base_b + (long long)p.nkv * chb) { ++b; continue; }
+      g = (int)((c - base_b) / chb);
+      pstart = base_b + (long long)g * chb;
+      pend = pstart + chb;
+      lo = (int)(c - pstart);
+      hi = (int)(min(c1, pend) - pstart);
+      side = c == c0 ? 0 : 1;
+      c = pstart + hi;
     }
-    // mask + online softmax (rows gid and gid+8)
-    float mx[2] = {-INFINITY, -INFINITY};
+
+    // ------------------------------------------------ one piece: chunks [lo, hi) of (b, g)
+    const int n_tok = p.pos[b] + 1;
+    bf16* wbuf = wring + (size_t)warp * ST * 2 * TILE;   // [stage][K|V]
+    const bf16* kbase = p.kc + ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* vbase = p.vc + ((size_t)b * p.nkv + g) * p.smax * HD;
+    uint32_t qa[HD / 16][4];
+    {
+      const bf16* qb = p.q + ((size_t)b * p.nq + (size_t)g * G) * HD;
+      const int r0 = gid, r1 = gid + 8;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int tok = t0 + j * 8 + 2 * tq + (e & 1);
-        s[j][e] = tok < t_end ? s[j][e] * p.scale_log2 : -INFINITY;
-        mx[e >> 1] = fmaxf(mx[e >> 1], s[j][e]);
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int cc = kk * 16 + 2 * tq;
+        qa[kk][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(qb + r0 * HD + cc) : 0u;
+        qa[kk][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + cc) : 0u;
+        qa[kk][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(qb + r0 * HD + cc + 8) : 0u;
+        qa[kk][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + cc + 8) : 0u;
       }
-    float alpha[2], muse[2];
+    }
+    float o[HD / 8][4];
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+    float mrow[2] = {-INFINITY, -INFINITY};
+    float lrow[2] = {0.0f, 0.0f};
+
+    auto load_chunk = [&](int stage, int ch) {
+      const int t0 = ch * kChunk;
+      bf16* sk = wbuf + stage * 2 * TILE;
+      bf16* sv = sk + TILE;
+#pragma unroll
+      for (int it = 0; it < (kChunk * CPR) / 32; ++it) {
+        const int e = it * 32 + lane;
+        const int row = e / CPR, cc = e % CPR;
+        const int t = min(t0 + row, n_tok - 1);
+        const int sw = (cc ^ (row & 7));
+        cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
+        cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+      }
+    };
+
+    // ST-1 chunks in flight per warp ahead of the one being consumed
+#pragma unroll
+    for (int j = 0; j < ST - 1; ++j) {
+      if (lo + warp + j * kWarps < hi) load_chunk(j, lo + warp + j * kWarps);
+      cp_async_commit();
+    }
+    int it = 0;
+    for (int ch = lo + warp; ch < hi; ch += kWarps, ++it) {
+      const int cn = ch + (ST - 1) * kWarps;
+      if (cn < hi) load_chunk((it + ST - 1) % ST, cn);
+      cp_async_commit();
+      cp_async_wait<ST - 1>();
+      __syncwarp();
+      const bf16* sk = wbuf + (it % ST) * 2 * TILE;
+      const bf16* sv = sk + TILE;
+      const uint32_t skb = smem_u32(sk), svb = smem_u32(sv);
+      const int t0 = ch * kChunk;
+
+      // S = Q K^T for 16 tokens (two n-tiles of 8)
+      float sc[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.0f;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int mat = lane >> 3, r = lane & 7;
+        const int tok = (mat >> 1) * 8 + r;
+        const int cc = kk * 2 + (mat & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
+        mma_bf16(sc[0], qa[kk], b0, b1);
+        mma_bf16(sc[1], qa[kk], b2, b3);
+      }
+      // mask + online softmax (rows gid and gid+8)
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int tok = t0 + j * 8 + 2 * tq + (e & 1);
+          sc[j][e] = tok < n_tok ? sc[j][e] * p.scale_log2 : -INFINITY;
+          mx[e >> 1] = fmaxf(mx[e >> 1], sc[j][e]);
+        }
+      float alpha[2], muse[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+        const float mnew = fmaxf(mrow[h], mx[h]);
+        muse[h] = mnew == -INFINITY ? 0.0f : mnew;
+        alpha[h] = exp2f(mrow[h] - muse[h]);
+        mrow[h] = mnew;
+        lrow[h] *= alpha[h];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          sc[j][e] = exp2f(sc[j][e] - muse[e >> 1]);
+          lrow[e >> 1] += sc[j][e];
+        }
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        o[i][0] *= alpha[0];
+        o[i][1] *= alpha[0];
+        o[i][2] *= alpha[1];
+        o[i][3] *= alpha[1];
+      }
+      uint32_t pa[4];
+      pa[0] = pack_bf16(sc[0][0], sc[0][1]);
+      pa[1] = pack_bf16(sc[0][2], sc[0][3]);
+      pa[2] = pack_bf16(sc[1][0], sc[1][1]);
+      pa[3] = pack_bf16(sc[1][2], sc[1][3]);
+      // O += P V
+#pragma unroll
+      for (int dn = 0; dn < HD / 8; dn += 2) {
+        const int mat = lane >> 3, r = lane & 7;
+        const int tok = (mat & 1) * 8 + r;
+        const int cc = dn + (mat >> 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
+        mma_bf16(o[dn], pa, b0, b1);
+        mma_bf16(o[dn + 1], pa, b2, b3);
+      }
+      __syncwarp();
+    }
+    cp_async_wait<0>();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-      const float mnew = fmaxf(mrow[h], mx[h]);
-      muse[h] = mnew == -INFINITY ? 0.0f : mnew;
-      alpha[h] = exp2f(mrow[h] - muse[h]);
-      mrow[h] = mnew;
-      lrow[h] *= alpha[h];
+      lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
+      lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
     }
+    __syncthreads();
+    // ---- merge the 4 warps through shared memory (reuses the K/V ring)
+    float* sm_o = reinterpret_cast<float*>(smem);                 // [warp][16][HD]
+    float* sm_m = sm_o + kWarps * 16 * HD;                        // [warp][16]
+    float* sm_l = sm_m + kWarps * 16;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int dn = 0; dn < HD / 8; ++dn)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        s[j][e] = exp2f(s[j][e] - muse[e >> 1]);
-        lrow[e >> 1] += s[j][e];
+        const int row = gid + 8 * (e >> 1), col = dn * 8 + 2 * tq + (e & 1);
+        sm_o[(warp * 16 + row) * HD + col] = o[dn][e];
       }
-#pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      o[i][0] *= alpha[0];
-      o[i][1] *= alpha[0];
-      o[i][2] *= alpha[1];
-      o[i][3] *= alpha[1];
+    if (tq == 0) {
+      sm_m[warp * 16 + gid] = mrow[0];
+      sm_m[warp * 16 + gid + 8] = mrow[1];
+      sm_l[warp * 16 + gid] = lrow[0];
+      sm_l[warp * 16 + gid + 8] = lrow[1];
     }
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = pack_bf16(s[0][2], s[0][3]);
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = pack_bf16(s[1][2], s[1][3]);
-    // O += P V
+    __syncthreads();
+    const bool whole = lo == 0 && hi == chb;
+    float* part = p.ws + (size_t)(cta * 2 + side) * 16 * (HD + 2);
+    for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+      const int row = idx / HD, col = idx % HD;
+      float M = -INFINITY;
 #pragma unroll
-    for (int dn = 0; dn < HD / 8; dn += 2) {
-      const int mat = lane >> 3, r = lane & 7;
-      const int tok = (mat & 1) * 8 + r;
-      const int cc = dn + (mat >> 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
-      mma_bf16(o[dn], pa, b0, b1);
-      mma_bf16(o[dn + 1], pa, b2, b3);
-    }
-    __syncwarp();
-  }
-  cp_async_wait<0>();
+      for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * 16 + row]);
+      float L = 0.0f, O = 0.0f;
+      if (M != -INFINITY) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
-    lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
-  }
-  __syncthreads();
-  // ---- merge the 4 warps through shared memory
-  float* sm_o = reinterpret_cast<float*>(smem);                 // [warp][16][HD]
-  float* sm_m = sm_o + kWarps * 16 * HD;                        // [warp][16]
-  float* sm_l = sm_m + kWarps * 16;
-#pragma unroll
-  for (int dn = 0; dn < HD / 8; ++dn)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int row = gid + 8 * (e >> 1), col = dn * 8 + 2 * tq + (e & 1);
-      sm_o[(warp * 16 + row) * HD + col] = o[dn][e];
-    }
-  if (tq == 0) {
-    sm_m[warp * 16 + gid] = mrow[0];
-    sm_m[warp * 16 + gid + 8] = mrow[1];
-    sm_l[warp * 16 + gid] = lrow[0];
-    sm_l[warp * 16 + gid + 8] = lrow[1];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
-    const int row = idx / HD, col = idx % HD;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * 16 + row]);
-    float L = 0.0f, O = 0.0f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const float mw = sm_m[w * 16 + row];
-        const float f = mw == -INFINITY ? 0.0f : exp2f(mw - M);
-        L += f * sm_l[w * 16 + row];
-        O += f * sm_o[(w * 16 + row) * HD + col];
+        for (int w = 0; w < kWarps; ++w) {
+          const float mw = sm_m[w * 16 + row];
+          const float f = mw == -INFINITY ? 0.0f : exp2f(mw - M);
+          L += f * sm_l[w * 16 + row];
+          O += f * sm_o[(w * 16 + row) * HD + col];
+        }
+      }
+      if (whole) {
+        p.o[((size_t)b * p.nq + g * G + row) * HD + col] = f_to_bf16(L > 0.0f ? O / L : 0.0f);
+      } else {
+        float* pr = part + (size_t)row * (HD + 2);
+        __stcg(pr + 2 + col, O);
+        if (col == 0) {
+          __stcg(pr, M);
+          __stcg(pr + 1, L);
+        }
       }
     }
-    const int head = g * G + row;
-    if (p.splits == 1) {
-      p.o[((size_t)b * p.nq + head) * HD + col] = f_to_bf16(L > 0.0f ? O / L : 0.0f);
-    } else {
-      float* part = p.ws + (((size_t)b * p.nq + head) * p.splits + split) * (HD + 2);
-      part[2 + col] = O;
-      if (col == 0) {
-        part[0] = M;
-        part[1] = L;
+    if (!whole) {
+      // publish this piece; the last of the pair's pieces merges them all (piece order)
+      const int first = cta_of_chunk(pstart, W, C), last = cta_of_chunk(pend - 1, W, C);
+      const int npieces = last - first + 1;
+      int* counter = p.cnt + (size_t)b * p.nkv + g;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = atomicAdd(counter, 1) == npieces - 1;
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        // Merge the pieces in order, 64 at a time with online rescaling: each batch's
+        // (max, sum) pairs are staged in shared memory (one round trip), then every thread
+        // folds its (row, col) outputs over the batch with 4 pieces' loads in flight.
+        float* sm_f = sm_o;                           // [64][16] batch scale factors
+        float* sm_lk = sm_f + 64 * 16;                // [64][16] batch sums
+        float* sm_M = sm_lk + 64 * 16;                // [16] running max
+        float* sm_L = sm_M + 16;                      // [16] running sum
+        float* sm_s = sm_L + 16;                      // [16] rescale of the running output
+        constexpr int kPer = (16 * HD + 127) / 128;   // outputs per thread (G <= 16)
+        float acc[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) acc[u] = 0.0f;
+        if (threadIdx.x < 16) {
+          sm_M[threadIdx.x] = -INFINITY;
+          sm_L[threadIdx.x] = 0.0f;
+        }
+        for (int kb0 = 0; kb0 < npieces; kb0 += 64) {
+          const int nb = min(64, npieces - kb0);
+          __syncthreads();
+          for (int e = threadIdx.x; e < nb * G; e += blockDim.x) {
+            const int k = e / G, row = e % G, j = first + kb0 + k;
+            const int sd = chunk_begin(j, W, C) >= pstart ? 0 : 1;
+            const float* pr = p.ws + ((size_t)(j * 2 + sd) * 16 + row) * (HD + 2);
+            sm_f[k * 16 + row] = __ldcg(pr);
+            sm_lk[k * 16 + row] = __ldcg(pr + 1);
+          }
+          __syncthreads();
+          if (threadIdx.x < G) {
+            const int row = threadIdx.x;
+            const float Mold = sm_M[row];
+            float M = Mold;
+            for (int k = 0; k < nb; ++k) M = fmaxf(M, sm_f[k * 16 + row]);
+            const float so = (Mold == -INFINITY) ? 0.0f : exp2f(Mold - M);
+            float L = sm_L[row] * so;
+            for (int k = 0; k < nb; ++k) {
+              const float mk = sm_f[k * 16 + row];
+              const float f = mk == -INFINITY ? 0.0f : exp2f(mk - M);
+              sm_f[k * 16 + row] = f;
+              L += f * sm_lk[k * 16 + row];
+            }
+            sm_M[row] = M;
+            sm_L[row] = L;
+            sm_s[row] = so;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            const int row = (threadIdx.x + 128 * u) / HD;
+            if (row < G) acc[u] *= sm_s[row];
+          }
+          for (int k0 = 0; k0 < nb; k0 += 4) {
+            float v[4][kPer];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const int k = k0 + kk, j = first + kb0 + k;
+              const int sd = chunk_begin(j, W, C) >= pstart ? 0 : 1;
+#pragma unroll
+              for (int u = 0; u < kPer; ++u) {
+                const int idx = threadIdx.x + 128 * u, row = idx / HD, col = idx % HD;
+                v[kk][u] = (k < nb && row < G)
+                               ? __ldcg(p.ws + ((size_t)(j * 2 + sd) * 16 + row) * (HD + 2) + 2 + col)
+                               : 0.0f;
+              }
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (k0 + kk < nb) {
+#pragma unroll
+                for (int u = 0; u < kPer; ++u) {
+                  const int row = (threadIdx.x + 128 * u) / HD;
+                  if (row < G) acc[u] += sm_f[(k0 + kk) * 16 + row] * v[kk][u];
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int idx = threadIdx.x + 128 * u, row = idx / HD, col = idx % HD;
+          if (row < G) {
+            const float L = sm_L[row];
+            p.o[((size_t)b * p.nq + g * G + row) * HD + col] = f_to_bf16(L > 0.0f ? acc[u] / L : 0.0f);
+          }
+        }
+        if (threadIdx.x == 0) *counter = 0;   // every piece has arrived: reset for the next launch
       }
     }
-  }
-}
-
-template <int HD>
-__global__ void attn_combine_kernel(const float* ws, bf16* o, int nq, int splits) {
-  pdl_trigger();
-  pdl_wait();
-  const int bh = blockIdx.x;   // b * nq + head
-  const float* part = ws + (size_t)bh * splits * (HD + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, part[s * (HD + 2)]);
-  for (int col = threadIdx.x; col < HD; col += blockDim.x) {
-    float L = 0.0f, O = 0.0f;
-    if (M != -INFINITY) {
-      for (int s = 0; s < splits; ++s) {
-        const float ms = part[s * (HD + 2)];
-        const float f = ms == -INFINITY ? 0.0f : exp2f(ms - M);
-        L += f * part[s * (HD + 2) + 1];
-        O += f * part[s * (HD + 2) + 2 + col];
-      }
-    }
-    o[(size_t)bh * HD + col] = f_to_bf16(L > 0.0f ? O / L : 0.0f);
+    __syncthreads();   // the next piece's loads reuse the merge buffers
   }
 }
 
@@ -376,48 +546,63 @@ cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s) {
 
 int attention_last_launch_count() { return g_attn_launches; }
 
+template <int HD, int ST>
+cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
+  const size_t ring = (size_t)kWarps * ST * 2 * kChunk * HD * 2;
+  const size_t smem = ring + (((size_t)a.B + 1) * 4 + 15) / 16 * 16;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  // one wave of resident CTAs; fewer when the batch has little work (>= 8 chunks per CTA at
+  // the host's context bound, so each warp streams at least two chunks)
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<HD, ST>, 128, smem);
+  per_sm = std::max(1, per_sm);
+  const int max_tok = (a.max_tokens > 0 && a.max_tokens < a.smax) ? a.max_tokens : a.smax;
+  const long long w_max = (long long)a.B * a.nkv * ((max_tok + kChunk - 1) / kChunk);
+  // Enough (b, g) pairs: one CTA per pair's worth of chunks (uniform contexts -> one pair per
+  // CTA, no pieces); few pairs (small batch, long context): one wave of CTAs splitting the
+  // pairs into pieces (split-KV) with >= 8 chunks per CTA at the host's context bound.
+  const long long pairs = (long long)a.B * a.nkv;
+  const long long slots = (long long)g_sms * per_sm;
+  long long cl = pairs >= slots ? pairs : std::min(slots, std::max<long long>(1, w_max / 8));
+  int ctas = (int)cl;
+  static const int env_ctas = getenv("SIDP_ATTN_CTAS") ? atoi(getenv("SIDP_ATTN_CTAS")) : 0;
+  if (env_ctas > 0) ctas = env_ctas;   // perf experiments
+  if ((size_t)ctas * 2 * 16 * (HD + 2) * 4 > a.ws_bytes)
+    ctas = (int)(a.ws_bytes / ((size_t)2 * 16 * (HD + 2) * 4));
+  if (ctas < 1) return cudaErrorInvalidValue;
+  AttnParams p;
+  p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws; p.cnt = a.cnt;
+  p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
+  p.pair_mode = (long long)ctas == pairs ? 1 : 0;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
+  return launch_pdl(attn_kernel<HD, ST>, dim3(ctas), dim3(128), smem, s, p);
+}
+
 cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
   if (a.B <= 0) return cudaSuccess;
-  if ((a.hd != 64 && a.hd != 128) || a.nq % a.nkv || a.nq / a.nkv > 16) return cudaErrorInvalidValue;
+  if ((a.hd != 64 && a.hd != 128) || a.nq % a.nkv || a.nq / a.nkv > 16 || !a.cnt ||
+      a.n_cnt < a.B * a.nkv)
+    return cudaErrorInvalidValue;
   if (!g_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   }
-  // split the context so the grid covers the SMs ~2x when B * n_kv is small
-  const int max_tok = (a.max_tokens > 0 && a.max_tokens < a.smax) ? a.max_tokens : a.smax;
-  const int base = a.B * a.nkv;
-  int splits = 1;
-  const int target = 2 * g_sms * 3;
-  if (base < target) splits = (target + base - 1) / base;
-  const int max_splits = (max_tok + 255) / 256;
-  if (splits > max_splits) splits = max_splits;
-  if (splits < 1) splits = 1;
-  int tok_per = (max_tok + splits - 1) / splits;
-  tok_per = ((tok_per + 63) / 64) * 64;
-  splits = (max_tok + tok_per - 1) / tok_per;
-  if (splits > 1 && (size_t)a.B * a.nq * splits * (a.hd + 2) * 4 > a.ws_bytes) {
-    splits = 1;
-    tok_per = max_tok;
-  }
-  AttnParams p;
-  p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws;
-  p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax; p.splits = splits; p.tok_per_split = tok_per;
-  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.hd));
-  dim3 grid(a.nkv, a.B, splits);
-  const size_t smem = (size_t)kWarps * 4 * kChunk * a.hd * 2;
-  cudaError_t e = a.hd == 128 ? launch_pdl(attn_kernel<128>, grid, dim3(128), smem, s, p)
-                              : launch_pdl(attn_kernel<64>, grid, dim3(128), smem, s, p);
+  static const int stages = getenv("SIDP_ATTN_STAGES") ? atoi(getenv("SIDP_ATTN_STAGES")) : 3;
   g_attn_launches = 1;
-  if (e != cudaSuccess || splits == 1) return e;
-  g_attn_launches = 2;
-  const float* wsc = a.ws;
-  bf16* oc = a.o;
-  const int nq = a.nq;
-  return a.hd == 128 ? launch_pdl(attn_combine_kernel<128>, dim3(a.B * a.nq), dim3(128), 0, s, wsc, oc, nq, splits)
-                     : launch_pdl(attn_combine_kernel<64>, dim3(a.B * a.nq), dim3(64), 0, s, wsc, oc, nq, splits);
+  if (a.hd == 128) {
+    if (stages == 2) return attn_launch_t<128, 2>(a, s);
+    if (stages == 4) return attn_launch_t<128, 4>(a, s);
+    return attn_launch_t<128, 3>(a, s);
+  }
+  if (stages == 2) return attn_launch_t<64, 2>(a, s);
+  if (stages == 4) return attn_launch_t<64, 4>(a, s);
+  return attn_launch_t<64, 3>(a, s);
 }
 
 cudaError_t attention_preload() {
@@ -425,10 +610,11 @@ cudaError_t attention_preload() {
   cudaError_t e = cudaSuccess;
   if (cudaFuncGetAttributes(&fa, qkv_post_kernel<128>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, qkv_post_kernel<64>) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, attn_kernel<128>) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, attn_kernel<64>) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, attn_combine_kernel<128>) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, attn_combine_kernel<64>) != cudaSuccess) e = cudaGetLastError();
+#define SIDP_PRELOAD_ATTN(hd, st) \
+  if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError();
+  SIDP_PRELOAD_ATTN(128, 2) SIDP_PRELOAD_ATTN(128, 3) SIDP_PRELOAD_ATTN(128, 4)
+  SIDP_PRELOAD_ATTN(64, 2) SIDP_PRELOAD_ATTN(64, 3) SIDP_PRELOAD_ATTN(64, 4)
+#undef SIDP_PRELOAD_ATTN
   return e;
 }
 

@@ -45,12 +45,12 @@ struct KParams {
   long long total_kb;           // tiles * nks (work in k-steps)
   int kps, nks;                 // k-blocks (64 deep) per pipeline stage; k-steps per tile
   int clusters;                 // concurrent CTA pairs (fixed per launch configuration)
-  int prefetch_kb;              // W k-blocks prefetched to L2 ahead of the TMA ring
   void* out; int ldo;
   const bf16* resid; int ldr;
   const bf16* bias;
   float* ws;
   int* counters;
+  int a3d, b3d;                 // operand map is k-block-major 3-D: one TMA box per stage
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
   QkvEpi qkv;                   // EPI_QKV destination
@@ -195,13 +195,6 @@ struct KbCursor {
     }
   }
 };
-
-SIDP_DEV void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 
 SIDP_DEV unsigned long long argmax_key(float v, int n) {
   uint32_t u = __float_as_uint(v);
@@ -529,50 +522,70 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
   const uint32_t tmem_base = *tmem_slot;
   // prologue done: let the next kernel of the chain launch, then wait for our inputs
   pdl_trigger();
-  pdl_wait();
+  if (threadIdx.x != 0) pdl_wait();   // the producer waits after issuing its weight prefetch
   if (threadIdx.x == 0) SIDP_TL(1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
-      int it = 0;
-      UnitIter ui;
-      ui.init(p, cluster);
-      Unit x;
-      // W streams from HBM: keep prefetch_kb k-blocks of this CTA's W rows in flight to L2
-      // beyond the shared-memory ring, so a TMA load sees L2 rather than HBM latency.
-      KbCursor pf;
-      pf.init(p, cluster);
-      for (int i = 0; !SW && i < p.prefetch_kb && pf.valid; ++i, pf.advance(p, cluster))
-        tma_prefetch_l2_2d(&tm_w, pf.kb * KPS * BK, pf.x.ft * 2 * WROWS + rank * WROWS);
-      while (ui.next(p, cluster, x)) {
-        for (int kb = x.kb0; kb < x.kb1; ++kb, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (it / stages) & 1;
-          if (!SW && pf.valid) {
-            tma_prefetch_l2_2d(&tm_w, pf.kb * KPS * BK, pf.x.ft * 2 * WROWS + rank * WROWS);
-            pf.advance(p, cluster);
-          }
+      // Only the leader arrives on a stage's full barrier (expecting both CTAs' bytes); the
+      // peer's TMA completes its transaction bytes on the leader's barrier directly.
+      const uint32_t stage_tx = 2 * (a_bytes + b_bytes);
+      // issue one operand of ring iteration (unit x, k-step kb) into stage s
+      auto load_a = [&](const Unit& x, int kb, int s, uint32_t lbar) {
+        const int arow = x.ft * 2 * WROWS + rank * WROWS;
+        if (p.a3d) {
+          tma_load_3d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes, 0, arow, kb * KPS);
+        } else {
+#pragma unroll
+          for (int j = 0; j < KPS; ++j)
+            tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes + j * a_sub, (kb * KPS + j) * BK, arow);
+        }
+      };
+      auto load_b = [&](const Unit& x, int kb, int s, uint32_t lbar) {
+        const int brow = x.mt * BNT + rank * HALF;
+        if (p.b3d) {
+          tma_load_3d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes, 0, brow, kb * KPS);
+        } else {
+#pragma unroll
+          for (int j = 0; j < KPS; ++j)
+            tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, brow);
+        }
+      };
+      // Weights never depend on the preceding kernel of the chain (they are resident, or were
+      // fetched before the layer's first kernel could start), so the first ring stages' weight
+      // tiles are requested before griddepcontrol.wait: their HBM latency overlaps the
+      // predecessor's tail.  Activations (the other operand) are loaded after the wait.
+      KbCursor cur;
+      cur.init(p, cluster);
+      int npre = 0;
+      {
+        KbCursor pre = cur;
+        for (; npre < stages && pre.valid; ++npre, pre.advance(p, cluster)) {
+          const uint32_t lbar = mapa_shared(smem_u32(&full[npre]), 0);
+          if (leader) mbar_arrive_expect_tx(&full[npre], stage_tx);
+          if (SW) load_b(pre.x, pre.kb, npre, lbar);
+          else load_a(pre.x, pre.kb, npre, lbar);
+        }
+      }
+      pdl_wait();
+      for (int it = 0; cur.valid; cur.advance(p, cluster), ++it) {
+        const int s = it % stages;
+        const uint32_t ph = (it / stages) & 1;
+        const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
+        if (it >= npre) {
           if (p.trace && cluster == 0 && it < 4096) p.trace[rank * 4096 + it] = globaltimer_ns();
           mbar_wait(&empty[s], ph ^ 1);
           if (p.trace && cluster == 0 && it < 4096) p.trace[(2 + rank) * 4096 + it] = globaltimer_ns();
-          const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
-          if (p.debug & 2) {
-            if (leader) mbar_arrive(&full[s]);
-            continue;
-          }
-          // Only the leader arrives (expecting both CTAs' bytes); the peer's TMA completes its
-          // transaction bytes on the leader's barrier directly — no per-stage remote arrive.
-          if (leader) mbar_arrive_expect_tx(&full[s], 2 * (a_bytes + b_bytes));
-          // 3-D boxes {64 k, rows, kps k-blocks}: one TMA per operand per stage
-#pragma unroll
-          for (int j = 0; j < KPS; ++j) {
-            const int kk = (kb * KPS + j) * BK;
-            tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes + j * a_sub, kk, x.ft * 2 * WROWS + rank * WROWS);
-            tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes + j * b_sub, kk, x.mt * BNT + rank * HALF);
-          }
-          if (p.trace && cluster == 0 && it < 4096 && rank == 0) p.trace[5 * 4096 + it] = globaltimer_ns();
+          if (leader) mbar_arrive_expect_tx(&full[s], stage_tx);
+          load_a(cur.x, cur.kb, s, lbar);
+          load_b(cur.x, cur.kb, s, lbar);
+        } else if (SW) {
+          load_a(cur.x, cur.kb, s, lbar);
+        } else {
+          load_b(cur.x, cur.kb, s, lbar);
         }
+        if (p.trace && cluster == 0 && it < 4096 && rank == 0) p.trace[5 * 4096 + it] = globaltimer_ns();
       }
     }
   } else if (warp == 1) {
@@ -845,6 +858,23 @@ bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows, u
   return r == CUDA_SUCCESS;
 }
 
+// k-block-major [K/64][rows][64] bf16 (each 64-wide k-block slab of all rows contiguous):
+// {64, rows, K/64} with strides {128 B, rows * 128 B}; a box {64, box_rows, kps} lands as kps
+// canonical SW128 K-major tiles back to back.
+bool make_tmap_kbmajor(CUtensorMap* m, const void* base, uint64_t K, uint64_t rows,
+                       uint32_t box_rows, uint32_t kps) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, rows, K / 64};
+  cuuint64_t strides[2] = {128, rows * 128};
+  cuuint32_t box[3] = {64, box_rows, kps};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                   uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn fn = get_encode_fn();
@@ -1005,11 +1035,23 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   stages = std::max(2, stages);
 
   CUtensorMap tw, tx;   // A operand map (128 rows per CTA), B operand map (BNT/2 rows per CTA)
+  const bool wkb = a.w_kbmajor != 0;   // W stored k-block-major [K/64][N][64]
+  int a3d = 0, b3d = 0;
   if (sw) {
     if (!make_tmap_2d(&tw, a.x, a.K, a.M, a.ldx, BK, WROWS)) return cudaErrorInvalidValue;
-    if (!make_tmap_2d(&tx, a.w, a.K, a.N, a.ldw, BK, BNT / 2)) return cudaErrorInvalidValue;
+    if (wkb) {
+      if (!make_tmap_kbmajor(&tx, a.w, a.K, a.N, BNT / 2, kps)) return cudaErrorInvalidValue;
+      b3d = 1;
+    } else if (!make_tmap_2d(&tx, a.w, a.K, a.N, a.ldw, BK, BNT / 2)) {
+      return cudaErrorInvalidValue;
+    }
   } else {
-    if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, WROWS)) return cudaErrorInvalidValue;
+    if (wkb) {
+      if (!make_tmap_kbmajor(&tw, a.w, a.K, a.N, WROWS, kps)) return cudaErrorInvalidValue;
+      a3d = 1;
+    } else if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, WROWS)) {
+      return cudaErrorInvalidValue;
+    }
     if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) return cudaErrorInvalidValue;
   }
 
@@ -1017,10 +1059,9 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
   p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.tiles = tiles; p.streamk = streamk;
   p.total_kb = (long long)tiles * nkb; p.clusters = clusters; p.kps = kps; p.nks = nkb;
-  static int env_pf = getenv("SIDP_GEMM_PF") ? atoi(getenv("SIDP_GEMM_PF")) : 0;
-  p.prefetch_kb = env_pf;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
+  p.a3d = a3d; p.b3d = b3d;
   if (a.qkv) p.qkv = *a.qkv;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;

@@ -90,6 +90,8 @@ struct sidp_ctx {
   int n_counters = 0;
   float* attn_ws = nullptr;
   size_t attn_ws_bytes = 0;
+  int* attn_cnt = nullptr;
+  int n_attn_cnt = 0;
   cudaStream_t fetch_stream = nullptr;
   std::vector<cudaEvent_t> ready_ev, free_ev;
   std::vector<char> free_recorded;
@@ -361,6 +363,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   // the split is sized from max_ctx (not the per-step max_pos) so the launch configuration is
   // step-invariant and a captured CUDA graph stays valid; empty splits exit immediately
   aa.max_tokens = ctx->c.max_ctx; aa.ws = ctx->attn_ws; aa.ws_bytes = ctx->attn_ws_bytes;
+  aa.cnt = ctx->attn_cnt; aa.n_cnt = ctx->n_attn_cnt;
   timing_begin(ctx, 2, s);
   CK(sidp::attention_launch(aa, s));
   timing_end(ctx, 2, s);
@@ -750,7 +753,7 @@ void sidp_destroy(sidp_ctx* ctx) {
     if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
-                    ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->cas, ctx->dev_err,
+                    ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas, ctx->dev_err,
                     ctx->cas_out};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -813,10 +816,12 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   ctx->n_counters = 1 << 16;
   DM(ctx->counters, ctx->n_counters * sizeof(int));
   CK(cudaMemset(ctx->counters, 0, ctx->n_counters * sizeof(int)));
-  const int max_splits = std::min(64, (ctx->c.max_ctx + 255) / 256);
-  ctx->attn_ws_bytes = std::min<size_t>((size_t)R * m.n_q_heads * max_splits * (m.head_dim + 2) * 4,
-                                        (size_t)256 << 20);
+  // attention partials: <= 2 pieces per resident CTA (<= 16 CTAs per SM) x 16 rows x (hd + 2)
+  ctx->attn_ws_bytes = (size_t)148 * 16 * 2 * 16 * (m.head_dim + 2) * 4;
   DM(ctx->attn_ws, ctx->attn_ws_bytes);
+  ctx->n_attn_cnt = R * m.n_kv_heads;
+  DM(ctx->attn_cnt, (size_t)ctx->n_attn_cnt * sizeof(int));
+  CK(cudaMemset(ctx->attn_cnt, 0, (size_t)ctx->n_attn_cnt * sizeof(int)));
   // CaS arena: flags | stage slots | recv
   ctx->stage_width = ctx->c.pool_scope == SIDP_POOL_LAYER ? ctx->qdim + m.hidden : 2 * m.hidden;
   ctx->cas_stage_bytes = align_up((size_t)R * ctx->stage_width * 2, 256);
@@ -1314,6 +1319,8 @@ sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ld
   a.ldw = ldw; a.M = M; a.N = N; a.K = K; a.epi = epi; a.out = out; a.ldo = ldo;
   a.resid = reinterpret_cast<const bf16*>(resid); a.ldr = ldr;
   a.bias = reinterpret_cast<const bf16*>(bias); a.k_splits = k_splits;
+  static const int env_wkb = getenv("SIDP_TEST_GEMM_WKB") ? atoi(getenv("SIDP_TEST_GEMM_WKB")) : 0;
+  a.w_kbmajor = env_wkb;   // layout experiments through the test hook only
   cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, counters, 1 << 16},
                                     reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm: %s", cudaGetErrorString(e));

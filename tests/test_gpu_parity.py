@@ -272,10 +272,14 @@ def test_cuda_graph_replay_matches_eager(P):
 
 
 @pytest.mark.parametrize("name,B,ctx,span", [("tiny", 1, 1500, 0), ("tiny", 3, 700, 900),
-                                              ("tiny-qwen3", 2, 2000, 100)])
+                                              ("tiny-qwen3", 2, 2000, 100),
+                                              ("tiny", 40, 0, 1500), ("tiny-qwen3", 12, 0, 3000),
+                                              ("tiny", 240, 0, 300)])
 def test_long_context_split_kv(P, name, B, ctx, span):
-    """Small batches with long contexts take the split-KV attention path (partials + combine);
-    ragged positions make some splits empty."""
+    """Attention work balancing: the batch's 16-token chunks are split evenly over the CTAs, so
+    small batches with long contexts split (b, kv head) pairs into pieces merged by the last
+    arriving piece (split-KV), and ragged context lengths (uniform 0..span) put piece
+    boundaries anywhere, including pairs of one chunk and pairs split over many CTAs."""
     m = MODELS[name]
     max_ctx = ctx + span + 8
     R = Rank(P, m, B=B, ctx=ctx, span=span, max_ctx=max_ctx)

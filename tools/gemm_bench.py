@@ -31,6 +31,8 @@ for name in only:
     N, K, epi = shapes[name]
     copies = max(2, int(600e6 // (N * K * 2)) + 1)
     ws = [torch.randn(N, K, device="cuda").to(torch.bfloat16) * 0.02 for _ in range(copies)]
+    if os.environ.get("SIDP_TEST_GEMM_WKB", "0") != "0":   # k-block-major copies [K/64][N][64]
+        ws = [w.view(N, K // 64, 64).transpose(0, 1).contiguous().view(N, K) for w in ws]
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     if epi == 3:
         out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
@@ -43,5 +45,7 @@ for name in only:
         us = timeit(lambda i: P.test_gemm(x, ws[i], out, M, N, K, epi,
                                           resid=out if epi == 2 else None, k_splits=splits), copies)
         print(f"{tag} {name:8s} M={M} N={N} K={K} splits={splits}: {us:8.1f} us  {fl/us/1e6:7.1f} TFLOP/s  {by/us/1e3:7.1f} GB/s", flush=True)
+    if os.environ.get("NO_CUBLAS"):
+        continue
     us = timeit(lambda i: torch.matmul(x, ws[i].t()), copies)
     print(f"{tag} {name:8s} M={M} N={N} K={K} cuBLAS : {us:8.1f} us  {fl/us/1e6:7.1f} TFLOP/s  {by/us/1e3:7.1f} GB/s", flush=True)
