@@ -332,6 +332,9 @@ def main():
     shares = ctx.stats()["timed_ms"]
     tot = sum(shares[1:]) or 1.0
     kernel_shares = {CLS_NAMES[c]: shares[c] / tot for c in CLS_NAMES}
+    # absolute per-layer class times of that (event-bracketed, so PDL-serialised) warm-up step
+    kernel_us_per_layer = {CLS_NAMES[c]: round(shares[c] * 1e3 / m.num_layers, 2) for c in CLS_NAMES
+                           if shares[c] > 0}
     dom = max((c for c in CLS_NAMES if c != 3 or world > 1), key=lambda c: shares[c])
 
     # ---------------- timed region (device-side, CUDA events, max over ranks)
@@ -428,6 +431,7 @@ def main():
         "clocks": clocks,
         "per_gpu_tokens_s": value / world,
         "kernel_shares": kernel_shares,
+        "kernel_us_per_layer": kernel_us_per_layer,
         "footprint_bytes_per_gpu": {"owned": st["owned_bytes"], "slots": st["slot_bytes"],
                                     "replicated": st["replicated_bytes"],
                                     "kv": 2 * kv.k.numel() * 2},

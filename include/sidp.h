@@ -237,6 +237,16 @@ sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ld
                            const void* resid, int32_t ldr, const void* bias, int32_t k_splits,
                            void* stream);
 
+/* Test hook for the deferred stream-K fix-up (SURVEY.md a8+a9, a11+a5): the EPI_PARTIAL GEMM
+ * Y = X W^T (X [M,K] row stride ldx, W [N,K] contiguous, bf16) leaves fp32 k-range partials
+ * that resid_norm sums in slice order: xout = bf16(Y + resid) ([M,N], resid row stride ldr,
+ * may alias xout) and u = bf16(xout * rsqrt(mean(xout^2) + eps) * g) ([M,N]).  SIDP_EINVAL
+ * (nothing enqueued) if the shape fills the machine with whole tiles or its slices exceed the
+ * hook's 256 MB workspace.  Device pointers; enqueued on stream. */
+sidp_status sidp_test_gemm_resid_norm(const void* x, int32_t ldx, const void* w, int32_t M,
+                                      int32_t N, int32_t K, const void* resid, int32_t ldr,
+                                      const void* g, float eps, void* xout, void* u, void* stream);
+
 /* K12 on an arbitrary buffer: dst[r*ld + c] = value(seed, tensor, layer, (row0+r)*lcols + c)
  * with kind 0 weight (scale from scale_k), 1 gain, 2 bias, 3 unit; row_map 1 = packed
  * gate/up interleave. */

@@ -211,6 +211,14 @@ def test_gemm(x, w, out, M, N, K, epi, resid=None, bias=None, k_splits=0, ldo=No
                                    k_splits, _stream_ptr(stream)), "sidp_test_gemm")
 
 
+def test_gemm_resid_norm(x, w, resid, g, eps, xout, u, stream=None):
+    M, K = x.shape
+    N = w.shape[0]
+    A.check(A.lib().sidp_test_gemm_resid_norm(_ptr(x), x.stride(0), _ptr(w), M, N, K, _ptr(resid),
+                                              resid.stride(0), _ptr(g), eps, _ptr(xout), _ptr(u),
+                                              _stream_ptr(stream)), "sidp_test_gemm_resid_norm")
+
+
 def test_gen(dst, seed, tensor, layer, kind, scale_k=0, row0=0, lcols=None, row_map=0, stream=None):
     rows, cols = dst.shape
     A.check(A.lib().sidp_test_gen(_ptr(dst), dst.stride(0), rows, cols, seed, tensor, layer, kind,

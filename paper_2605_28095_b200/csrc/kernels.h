@@ -21,7 +21,32 @@ enum GemmEpilogue : int {
                       // out[m, f] bf16 = silu(gate f) * up f, f = 8g + i
   EPI_ARGMAX = 4,     // fused argmax over n: packed (value, lowest index) into out u64[M]
   EPI_QKV = 5,        // fused QKV post-processing: (+bias) (qk-norm) RoPE -> q bf16, k/v -> KV cache
+  EPI_PARTIAL = 6,    // deferred reduction: stream-K over all CTA pairs, EVERY unit writes its fp32
+                      // k-range partial to the workspace slice of its segment; no fix-up kernel —
+                      // the consumer (resid_norm, qkv_post) sums the slices (see PartialSrc)
 };
+
+// Where an EPI_PARTIAL GEMM left Y: Y[m, n] = sum_{s < nseg(tile(m, n))} ws[s][m][n] in slice
+// order (deterministic: depends only on the shapes and the launch's cluster count).  Tiles
+// are (tile_m tokens x tile_f features); tile index t = sw ? (m / tile_m) * f_tiles + n / tile_f
+// : (n / tile_f) * m_tiles + m / tile_m; the t-th tile covers k-steps [t nks, (t+1) nks) of
+// the stream-K range split evenly over `clusters` CTA pairs.
+struct PartialSrc {
+  const float* ws;
+  int M, N;
+  int sw, tile_m, tile_f, m_tiles, f_tiles;
+  int nks, clusters;
+  long long total_kb;
+};
+__host__ __device__ inline int partial_cluster_of(long long g, long long total, int C) {
+  return (int)(((g + 1) * (long long)C + total - 1) / total) - 1;
+}
+__host__ __device__ inline int partial_nseg(const PartialSrc& p, int m, int n) {
+  const long long t = p.sw ? (long long)(m / p.tile_m) * p.f_tiles + n / p.tile_f
+                           : (long long)(n / p.tile_f) * p.m_tiles + m / p.tile_m;
+  return partial_cluster_of((t + 1) * p.nks - 1, p.total_kb, p.clusters) -
+         partial_cluster_of(t * p.nks, p.total_kb, p.clusters) + 1;
+}
 
 // Destination of the fused QKV epilogue (rows of W_qkv = [q heads | k heads | v heads]).
 struct QkvEpi {
@@ -46,6 +71,7 @@ struct GemmArgs {
   int max_ctas;                // 0 = all SMs
   const QkvEpi* qkv;           // EPI_QKV only
   int w_kbmajor;               // 1: W is k-block-major [K/64][N][64] (one 3-D TMA box per stage)
+  PartialSrc* partial_out;     // EPI_PARTIAL: receives the slice geometry for the consumer
 };
 
 struct GemmWorkspace {
@@ -55,11 +81,21 @@ struct GemmWorkspace {
 
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t s);
 int gemm_pick_splits(int tiles, int nkb, int sms);
+// true when an EPI_PARTIAL launch of this shape is both possible (slices fit the workspace)
+// and worthwhile (whole 256x256 tiles would leave CTA pairs idle, so the GEMM is stream-K
+// anyway and the fix-up can move into the consumer)
+bool gemm_partial_ok(int M, int N, int K, size_t ws_bytes);
 int gemm_last_launch_count();   // kernels enqueued by the last gemm_launch on this thread
 
 // ---------------------------------------------------------------- element-wise / small kernels
 cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf16* y, int ldy,
                            int rows, int h, cudaStream_t s);
+// Deferred stream-K fix-up fused with the residual add and the next RMSNorm (SURVEY.md a8 + a9,
+// a11 + next layer's a5): per row m, x_out = bf16(sum of the partial slices + resid) and
+// u = bf16(x_out * rsqrt(mean(x_out^2) + eps) * g).  resid may alias x_out.
+cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, bf16* xout, int ldx,
+                              const bf16* g, float eps, bf16* u, int ldu, int rows, int h,
+                              cudaStream_t s);
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
                          cudaStream_t s);
 // qkv fp32 [B, (nq+2nkv)*hd] -> q bf16 [B, nq, hd]; k, v appended to caches at pos[b]
@@ -71,6 +107,8 @@ struct QkvPostArgs {
   bf16* q;
   bf16* kc; bf16* vc;                           // [Bmax, nkv, Smax, hd]
   int smax;
+  PartialSrc part;                              // part.ws != null: qkv is the sum of these slices
+  const bf16* bias;                             // added in the partial form only (else by the GEMM)
 };
 cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s);
 

@@ -53,18 +53,42 @@ __global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
       cs[0][0] = t.x; cs[0][1] = t.y;
     }
   }
+  const size_t slice = (size_t)a.part.M * a.part.N;
   for (int head = head0; head < nh; head += nwarps) {
-    const float* src = a.qkv + ((size_t)b * nh + head) * HD;
     const bool is_v = head >= a.nq + a.nkv;
     const bool is_q = head < a.nq;
     float x1[E], x2[E];
-    if constexpr (E == 2) {
-      const float2 u = *reinterpret_cast<const float2*>(src + i0);
-      const float2 w = *reinterpret_cast<const float2*>(src + i0 + half);
-      x1[0] = u.x; x1[1] = u.y; x2[0] = w.x; x2[1] = w.y;
+#pragma unroll
+    for (int e = 0; e < E; ++e) x1[e] = x2[e] = 0.0f;
+    auto load = [&](const float* src) {
+      if constexpr (E == 2) {
+        const float2 u = __ldcg(reinterpret_cast<const float2*>(src + i0));
+        const float2 w = __ldcg(reinterpret_cast<const float2*>(src + i0 + half));
+        x1[0] += u.x; x1[1] += u.y; x2[0] += w.x; x2[1] += w.y;
+      } else {
+        x1[0] += __ldcg(src + i0);
+        x2[0] += __ldcg(src + i0 + half);
+      }
+    };
+    if (a.part.ws) {
+      // deferred stream-K fix-up: a head lies inside one 256-feature tile (hd divides 256),
+      // so its partial slices are summed in slice order, then the bias is added
+      const int n = head * HD;
+      const int nseg = partial_nseg(a.part, b, n);
+      const float* src = a.part.ws + (size_t)b * a.part.N + n;
+#pragma unroll
+      for (int sgi = 0; sgi < 4; ++sgi)   // issued together (predicated), summed in order
+        if (sgi < nseg) load(src + sgi * slice);
+      for (int sgi = 4; sgi < nseg; ++sgi) load(src + sgi * slice);
+      if (a.bias) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          x1[e] += bf16_to_f(a.bias[n + i0 + e]);
+          x2[e] += bf16_to_f(a.bias[n + i0 + e + half]);
+        }
+      }
     } else {
-      x1[0] = src[i0];
-      x2[0] = src[i0 + half];
+      load(a.qkv + ((size_t)b * nh + head) * HD);
     }
     if (!is_v) {
       const bf16* gain = is_q ? a.gq : a.gk;

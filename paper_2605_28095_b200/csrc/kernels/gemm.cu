@@ -51,6 +51,7 @@ struct KParams {
   float* ws;
   int* counters;
   int a3d, b3d;                 // operand map is k-block-major 3-D: one TMA box per stage
+  int partial_all;              // EPI_PARTIAL: every unit writes its fp32 partial slice
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
   QkvEpi qkv;                   // EPI_QKV destination
@@ -366,7 +367,7 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
         }
       }
     }
-  } else {  // EPI_ARGMAX: warp w reduces tokens w*8 .. w*8+7 over the 128 features
+  } else if constexpr (EPI == EPI_ARGMAX) {  // warp w reduces tokens w*8 .. w*8+7 over the 128 features
     unsigned long long* out = reinterpret_cast<unsigned long long*>(p.out);
     const int w = tid >> 5, lane = tid & 31;
     for (int jj = 0; jj < 8; ++jj) {
@@ -664,7 +665,23 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
           }
           const int n0 = fbase + c * 32;
-          if (m < p.M) store_row<EPI>(p, r, m, n0, best);
+          if (m < p.M) {
+            if (x.nseg > 1 || p.partial_all) {
+              // k-range partial of this token row -> ws[seg][m][n0 .. n0+31], straight from
+              // registers (TMEM lanes are tokens: 128 contiguous bytes per thread)
+              float* dst = p.ws + (size_t)x.seg * p.M * p.N + (size_t)m * p.N;
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const int n = n0 + 4 * g;
+                if (n < p.N)
+                  __stcg(reinterpret_cast<float4*>(dst + n),
+                         make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                     __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
+              }
+            } else {
+              store_row<EPI>(p, r, m, n0, best);
+            }
+          }
         }
         if (nch <= 0) {
           tc_fence_before();
@@ -704,7 +721,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
           }
           named_bar_sync(1, 128);
-          if (x.nseg == 1) {
+          if (x.nseg == 1 && !p.partial_all) {
             store_phase<EPI>(p, stg, mbase + c * 32, n0, pt, tid);
           } else {
             // partial of this k-range -> ws[seg][m][n] (token-major, coalesced 16-byte stores)
@@ -896,6 +913,46 @@ thread_local int g_last_launches = 0;
 template <int EPI>
 constexpr bool kHasSw = EPI != EPI_QKV;
 
+// EPI_PARTIAL launch geometry (shared by gemm_launch and gemm_partial_ok): W-major, token tile =
+// M rounded up to 32 (<= 256), partials staged through shared memory into coalesced rows.
+// SIDP_GEMM_PART_SW_MIN_M = m > 0 switches to token-major from m tokens up (feature tile 256,
+// each thread stores its token row's partial straight from registers) — measured slower on
+// the M2 O / down shapes (O 48.7 vs 35 us live), so off by default.
+struct PartialPlan {
+  bool sw;
+  int BNT, m_tiles, n_pairs, tiles, clusters, nkb, kps;
+  long long total;
+  int max_seg;
+};
+PartialPlan plan_partial(int M, int N, int K, int pair_slots) {
+  static int env_sw_min = getenv("SIDP_GEMM_PART_SW_MIN_M") ? atoi(getenv("SIDP_GEMM_PART_SW_MIN_M")) : 0;
+  static int env_bnf = getenv("SIDP_GEMM_PART_BNF") ? atoi(getenv("SIDP_GEMM_PART_BNF")) : 256;
+  PartialPlan q{};
+  const int nkb_blocks = K / BK;
+  q.kps = nkb_blocks % 2 == 0 ? 2 : 1;
+  q.nkb = nkb_blocks / q.kps;
+  q.sw = env_sw_min > 0 && M >= env_sw_min;
+  if (q.sw) {
+    q.BNT = (env_bnf >= 32 && env_bnf <= 256 && env_bnf % 32 == 0) ? env_bnf : 256;
+    q.m_tiles = (N + q.BNT - 1) / q.BNT;
+    q.n_pairs = (M + 2 * WROWS - 1) / (2 * WROWS);
+  } else {
+    q.BNT = std::max(32, std::min(256, ((M + 31) / 32) * 32));
+    q.m_tiles = (M + q.BNT - 1) / q.BNT;
+    q.n_pairs = (N + 2 * WROWS - 1) / (2 * WROWS);
+  }
+  q.tiles = q.n_pairs * q.m_tiles;
+  q.clusters = pair_slots;
+  q.total = (long long)q.tiles * q.nkb;
+  long long per = q.total / q.clusters;
+  if (per < 2) {
+    q.clusters = (int)std::max<long long>(1, q.total / 2);
+    per = q.total / q.clusters;
+  }
+  q.max_seg = (int)((q.nkb + per - 1) / std::max<long long>(per, 1)) + 1;
+  return q;
+}
+
 template <int EPI>
 void set_attr() {
   cudaFuncSetAttribute(gemm2_kernel<EPI, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -946,16 +1003,36 @@ int gemm_pick_splits(int tiles, int nkb, int slots) {
 
 int gemm_last_launch_count() { return g_last_launches; }
 
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+bool gemm_partial_ok(int M, int N, int K, size_t ws_bytes) {
+  static int env = getenv("SIDP_GEMM_PARTIAL") ? atoi(getenv("SIDP_GEMM_PARTIAL")) : 1;
+  if (!env || M <= 0 || N <= 0 || K % BK != 0 || N % 8 != 0) return false;
+  const int pair_slots = std::max(1, num_sms() / 2);
+  const long long wm_tiles = (long long)((N + 2 * WROWS - 1) / (2 * WROWS)) * ((M + 255) / 256);
+  if (wm_tiles >= pair_slots) return false;   // whole tiles fill the machine: no split, no fix-up
+  const PartialPlan q = plan_partial(M, N, K, pair_slots);
+  return (size_t)q.max_seg * M * N * 4 <= ws_bytes;
+}
+
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t stream) {
   g_last_launches = 0;
   if (a.M <= 0) return cudaSuccess;
   if (a.K % BK != 0 || a.N <= 0 || a.N % 8 != 0 || a.x == nullptr || a.w == nullptr)
     return cudaErrorInvalidValue;
   if (a.epi == EPI_SILU_MUL && (a.N % 16) != 0) return cudaErrorInvalidValue;
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  static bool attrs = false;
+  if (!attrs) {
+    attrs = true;
+    num_sms();
+    set_attr<EPI_PARTIAL>();
     set_attr<EPI_F32>();
     set_attr<EPI_BF16>();
     set_attr<EPI_RESID>();
@@ -985,7 +1062,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   const int wm_tiles = ((a.N + 2 * WROWS - 1) / (2 * WROWS)) *
                        ((a.M + std::min(256, env_bnt) - 1) / std::min(256, env_bnt));
   const bool underfilled = 2 * wm_tiles > pair_slots && wm_tiles < pair_slots;
-  const bool sw = a.k_splits < 0 ? a.epi != EPI_QKV
+  bool sw = a.k_splits < 0 ? a.epi != EPI_QKV
                                   : (env_sw > 0 && env_sw_min > 0 && a.M >= env_sw_min &&
                                      a.epi != EPI_QKV && a.k_splits <= 1 && (env_sw == 2 || underfilled));
   int BNT, m_tiles, n_pairs;
@@ -1012,7 +1089,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     m_tiles = (a.M + BNT - 1) / BNT;
     n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
   }
-  const int tiles = n_pairs * m_tiles;
+  int tiles = n_pairs * m_tiles;
   // stream-K over all pairs unless the epilogue needs whole dot products (fused argmax) or the
   // caller pins whole tiles (k_splits == 1); max segments per tile bounds the workspace
   int clusters = pair_slots;
@@ -1027,6 +1104,20 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     if (per < 2) clusters = (int)std::max<long long>(1, total / 2);   // tiny problems
     const int max_seg = (int)((nkb + per - 1) / std::max<long long>(per, 1)) + 1;
     if ((size_t)max_seg * a.M * a.N * 4 > w.ws_bytes) streamk = 0;
+  }
+  const bool part = a.epi == EPI_PARTIAL;
+  if (part) {
+    const PartialPlan q = plan_partial(a.M, a.N, a.K, pair_slots);
+    if ((size_t)q.max_seg * a.M * a.N * 4 > w.ws_bytes || q.kps != kps) return cudaErrorInvalidValue;
+    sw = q.sw; BNT = q.BNT; m_tiles = q.m_tiles; n_pairs = q.n_pairs;
+    tiles = q.tiles; clusters = q.clusters; streamk = 1;
+    if (a.partial_out) {
+      PartialSrc& o = *a.partial_out;
+      o.ws = w.ws; o.M = a.M; o.N = a.N; o.sw = sw ? 1 : 0;
+      o.tile_m = sw ? 2 * WROWS : BNT; o.tile_f = sw ? BNT : 2 * WROWS;
+      o.m_tiles = sw ? n_pairs : m_tiles; o.f_tiles = sw ? m_tiles : n_pairs;
+      o.nks = nkb; o.clusters = clusters; o.total_kb = q.total;
+    }
   }
   if (!streamk) clusters = std::min(tiles, pair_slots);
   const size_t stage_bytes = kps * ((size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2);
@@ -1062,6 +1153,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
   p.a3d = a3d; p.b3d = b3d;
+  p.partial_all = part ? 1 : 0;
   if (a.qkv) p.qkv = *a.qkv;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
@@ -1083,6 +1175,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     case EPI_SILU_MUL: e0 = launch_gemm2<EPI_SILU_MUL>(kps, sw, grid, smem, stream, tw, tx, p); break;
     case EPI_ARGMAX: e0 = launch_gemm2<EPI_ARGMAX>(kps, sw, grid, smem, stream, tw, tx, p); break;
     case EPI_QKV: e0 = launch_gemm2<EPI_QKV>(kps, false, grid, smem, stream, tw, tx, p); break;
+    case EPI_PARTIAL: e0 = launch_gemm2<EPI_PARTIAL>(kps, sw, grid, smem, stream, tw, tx, p); break;
     default: return cudaErrorInvalidValue;
   }
   g_last_launches = 1;
@@ -1120,7 +1213,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
               v.size(), v.front(), v[v.size() / 2], v.back());
     }
   }
-  if (e0 != cudaSuccess || !streamk) return e0;
+  if (e0 != cudaSuccess || !streamk || part) return e0;
   g_last_launches = 2;
   dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, clusters - 1));
   switch (a.epi) {
@@ -1151,7 +1244,9 @@ cudaError_t gemm_preload() {
   SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2, false>))
   SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2, true>))
   SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2, false>))
-  SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 2, true>))
+    SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
   SIDP_PRELOAD((gemm_reduce_kernel<EPI_RESID>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_SILU_MUL>))
 #undef SIDP_PRELOAD
   return e;

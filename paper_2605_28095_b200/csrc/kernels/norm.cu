@@ -1,11 +1,25 @@
 // norm.cu — RMSNorm, embedding gather, argmax finalisation.
 // HBM-bound row kernels: 16-byte vector loads, fp32 statistics, one bf16 rounding.
+#include <algorithm>
+
 #include "../common.cuh"
 #include "../kernels.h"
 
 namespace sidp {
 
 namespace {
+
+__device__ __forceinline__ float2 bf16x2_to_f2(uint32_t w) {
+  __nv_bfloat162 h;
+  memcpy(&h, &w, 4);
+  return __bfloat1622float2(h);
+}
+__device__ __forceinline__ uint32_t f2_to_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  uint32_t w;
+  memcpy(&w, &h, 4);
+  return w;
+}
 
 // y = bf16( x * rsqrt(mean(x^2) + eps) * g ), one CTA per row, h % 8 == 0.  The row is read
 // once: up to kVec 16-byte vectors per thread are loaded up front (all in flight together) and
@@ -84,6 +98,90 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const bf16* __res
   }
 }
 
+// Deferred stream-K fix-up + residual + RMSNorm, one CTA per row (see resid_norm_launch), one
+// thread per 8-feature vector (h <= 8 * 640; longer rows loop).  Per vector the fp32 partial
+// slices of its tile are summed in slice order, the bf16 residual added in fp32 and the sum
+// rounded once to bf16 (x_out, the residual stream); the norm statistics use the rounded
+// x_out, exactly as rmsnorm_kernel on a stored x_out.  The slice loads of a vector are issued
+// together (unrolled, predicated): the kernel is bound by their L2 round trips otherwise.
+constexpr int kFixSeg = 4, kMaxFixTiles = 128;
+__global__ void __launch_bounds__(640, 2) resid_norm_kernel(
+    const PartialSrc ps, const bf16* __restrict__ resid, int ldr, bf16* xout, int ldx,
+    const bf16* __restrict__ g, float eps, bf16* __restrict__ u, int ldu, int h) {
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.x;
+  const int nvec = h / 8;
+  const size_t slice = (size_t)ps.M * ps.N;
+  const float* wrow = ps.ws + (size_t)row * ps.N;
+  // segment count of each feature tile of this row, computed once (64-bit divisions)
+  __shared__ int nseg_of[kMaxFixTiles];
+  for (int t = threadIdx.x; t * ps.tile_f < ps.N; t += blockDim.x)
+    nseg_of[t] = partial_nseg(ps, row, t * ps.tile_f);
+  __syncthreads();
+  float ss = 0.0f;
+  for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
+    const int n = k * 8;
+    const int nseg = nseg_of[n / ps.tile_f];
+    const float* src = wrow + n;
+    const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
+    float4 lo[kFixSeg], hi[kFixSeg];
+#pragma unroll
+    for (int q = 0; q < kFixSeg; ++q) {
+      lo[q] = hi[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < nseg) {
+        lo[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
+        hi[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
+      }
+    }
+    float4 al = make_float4(0.f, 0.f, 0.f, 0.f), ah = al;
+#pragma unroll
+    for (int q = 0; q < kFixSeg; ++q) {   // slice order; slices past nseg add +0
+      al.x += lo[q].x; al.y += lo[q].y; al.z += lo[q].z; al.w += lo[q].w;
+      ah.x += hi[q].x; ah.y += hi[q].y; ah.z += hi[q].z; ah.w += hi[q].w;
+    }
+    for (int q = kFixSeg; q < nseg; ++q) {
+      const float4 x0 = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
+      const float4 x1 = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
+      al.x += x0.x; al.y += x0.y; al.z += x0.z; al.w += x0.w;
+      ah.x += x1.x; ah.y += x1.y; ah.z += x1.z; ah.w += x1.w;
+    }
+    const float2 r0 = bf16x2_to_f2(rr.x), r1 = bf16x2_to_f2(rr.y), r2 = bf16x2_to_f2(rr.z),
+                 r3 = bf16x2_to_f2(rr.w);
+    const uint4 out = make_uint4(f2_to_bf16x2(al.x + r0.x, al.y + r0.y), f2_to_bf16x2(al.z + r1.x, al.w + r1.y),
+                                 f2_to_bf16x2(ah.x + r2.x, ah.y + r2.y), f2_to_bf16x2(ah.z + r3.x, ah.w + r3.y));
+    *reinterpret_cast<uint4*>(xout + (size_t)row * ldx + n) = out;
+    const float2 o0 = bf16x2_to_f2(out.x), o1 = bf16x2_to_f2(out.y), o2 = bf16x2_to_f2(out.z),
+                 o3 = bf16x2_to_f2(out.w);
+    ss += o0.x * o0.x + o0.y * o0.y + o1.x * o1.x + o1.y * o1.y + o2.x * o2.x + o2.y * o2.y +
+          o3.x * o3.x + o3.y * o3.y;
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / (float)h + eps);
+  auto scale = [&](const uint4& raw, int k) {
+    const uint4 graw = *reinterpret_cast<const uint4*>(g + k * 8);
+    const bf16* e = reinterpret_cast<const bf16*>(&raw);
+    const bf16* ge = reinterpret_cast<const bf16*>(&graw);
+    uint4 out;
+    bf16* o = reinterpret_cast<bf16*>(&out);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = f_to_bf16(bf16_to_f(e[q]) * r * bf16_to_f(ge[q]));
+    *reinterpret_cast<uint4*>(u + (size_t)row * ldu + k * 8) = out;
+  };
+  // re-read this thread's own x_out vectors (L1/L2 hits)
+  for (int k = threadIdx.x; k < nvec; k += blockDim.x)
+    scale(*reinterpret_cast<const uint4*>(xout + (size_t)row * ldx + k * 8), k);
+}
+
 __global__ void embed_kernel(const bf16* __restrict__ E, int h, const int32_t* __restrict__ tok,
                              bf16* __restrict__ x) {
   pdl_trigger();
@@ -121,6 +219,17 @@ cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf1
   return launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, s, x, ldx, g, eps, y, ldy, h);
 }
 
+cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, bf16* xout, int ldx,
+                              const bf16* g, float eps, bf16* u, int ldu, int rows, int h,
+                              cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  if (h % 8 || ps.ws == nullptr || ps.N != h || rows > ps.M || ps.N > kMaxFixTiles * ps.tile_f)
+    return cudaErrorInvalidValue;
+  const int threads = std::min(640, (h / 8 + 31) / 32 * 32);
+  return launch_pdl(resid_norm_kernel, dim3(rows), dim3(threads), 0, s, ps, resid, ldr, xout, ldx,
+                    g, eps, u, ldu, h);
+}
+
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
                          cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
@@ -144,6 +253,7 @@ cudaError_t norm_preload() {
   cudaError_t e = cudaSuccess;
   if (cudaFuncGetAttributes(&fa, rmsnorm_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, embed_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, resid_norm_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, argmax_finalize_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, argmax_reset_kernel) != cudaSuccess) e = cudaGetLastError();
   return e;

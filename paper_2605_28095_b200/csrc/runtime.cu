@@ -113,6 +113,11 @@ struct sidp_ctx {
   std::vector<int32_t> log_t, log_l, log_s;
   int next_layer = 0;
   int64_t step = 0;
+  // RMSNorm fused into the previous layer's down-projection fix-up (resid_norm): u holds
+  // RMSNorm(x) * g for layer u_for (L = the final norm); chain_g is the gain to use, set by
+  // sidp_step around each WaS layer (a standalone sidp_decode_layer has no successor)
+  int u_for = -1;
+  const bf16* chain_g = nullptr;
   bool stagger_pending = false;
   // mode
   int mode = SIDP_WAS;
@@ -303,16 +308,23 @@ LayerW layer_weights(const sidp_ctx* c, const bf16* pooled, const bf16* local) {
                 P(C_GMLP), P(C_GQ), P(C_GK), P(C_BQKV)};
 }
 
+// a gain that is never pooled (R2): the layer's local blob
+const bf16* local_gain(const sidp_ctx* c, int layer, int comp) {
+  return c->local + (size_t)layer * c->local_elems + c->comp_off[comp];
+}
+
 sidp::GemmWorkspace gws(sidp_ctx* c) {
   return sidp::GemmWorkspace{c->gemm_ws, c->gemm_ws_bytes, c->counters, c->n_counters};
 }
 
 cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, int M, int N, int K,
                  int epi, void* out, int ldo, const bf16* resid, int ldr, const bf16* bias,
-                 cudaStream_t s, const sidp::QkvEpi* qkv = nullptr) {
+                 cudaStream_t s, const sidp::QkvEpi* qkv = nullptr,
+                 sidp::PartialSrc* partial = nullptr) {
   sidp::GemmArgs a{};
   a.x = x; a.ldx = ldx; a.w = w; a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = epi;
   a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias; a.qkv = qkv;
+  a.partial_out = partial;
   timing_begin(c, cls, s);
   cudaError_t e = sidp::gemm_launch(a, gws(c), s);
   timing_end(c, cls, s);
@@ -330,20 +342,36 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
   bf16* vc = reinterpret_cast<bf16*>(kv->v_cache) + (size_t)layer * lstride;
   static const bool fused_qkv = getenv("SIDP_FUSED_QKV") && atoi(getenv("SIDP_FUSED_QKV")) != 0;
+  const bool u_ready = ctx->u_for == layer;
+  ctx->u_for = -1;
+  sidp::PartialSrc part{};
   if (!qkv_in && !fused_qkv) {
-    // RMSNorm -> QKV GEMM (fp32, + bias) -> qkv_post (qk-norm, RoPE, KV append) on all SMs
-    CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
-    count_launch(ctx);
-    CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_F32, ctx->qkv,
-            ctx->qkvdim, nullptr, 0, W.b_qkv, s));
-    qkv_in = ctx->qkv;
+    // RMSNorm (unless the previous layer's fix-up produced u) -> QKV GEMM -> qkv_post
+    // (qk-norm, RoPE, KV append) on all SMs.  SIDP_QKV_PARTIAL=1: the GEMM leaves stream-K
+    // partial slices for qkv_post to sum with the bias (measured: GEMM -6 us, qkv_post +8 us
+    // on M2, so off by default; the token-major no-split GEMM writes fp32 qkv instead).
+    if (!u_ready) {
+      CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+      count_launch(ctx);
+    }
+    static const bool qkv_partial = getenv("SIDP_QKV_PARTIAL") && atoi(getenv("SIDP_QKV_PARTIAL")) != 0;
+    if (qkv_partial && sidp::gemm_partial_ok(B, ctx->qkvdim, m.hidden, ctx->gemm_ws_bytes)) {
+      CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_PARTIAL,
+              nullptr, 0, nullptr, 0, nullptr, s, nullptr, &part));
+    } else {
+      CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_F32, ctx->qkv,
+              ctx->qkvdim, nullptr, 0, W.b_qkv, s));
+      qkv_in = ctx->qkv;
+    }
   }
-  if (!qkv_in) {
+  if (!qkv_in && !part.ws) {
     // RMSNorm, then the QKV GEMM whose epilogue applies bias, qk-norm and RoPE and writes q
     // and the new k/v straight into the KV cache (no fp32 qkv round trip; SIDP_FUSED_QKV=1:
     // on these shapes the per-tile epilogue is not hidden, so it is off by default)
-    CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
-    count_launch(ctx);
+    if (!u_ready) {
+      CK(sidp::rmsnorm_launch(x, m.hidden, W.g_attn, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+      count_launch(ctx);
+    }
     sidp::QkvEpi qe{ctx->q, kc, vc, kv->pos, ctx->rope, W.g_q, W.g_k, m.rms_eps,
                     m.n_q_heads, m.n_kv_heads, m.head_dim, ctx->c.max_ctx};
     CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_QKV, nullptr,
@@ -354,6 +382,10 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
     qa.qkv = qkv_in; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
     qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;
     qa.q = ctx->q; qa.kc = kc; qa.vc = vc; qa.smax = ctx->c.max_ctx;
+    if (part.ws) {
+      qa.part = part;
+      qa.bias = W.b_qkv;
+    }
     CK(sidp::qkv_post_launch(qa, s));
     count_launch(ctx);
   }
@@ -371,19 +403,38 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   return SIDP_OK;
 }
 
-// C-N2 steps 7-10 on rows of (o, x); writes out (may alias x).
+// C-N2 steps 7-10 on rows of (o, x); writes out (may alias x).  With next_g (the next layer's
+// input-norm gain, or the final norm's), the down projection's fix-up also writes
+// u = RMSNorm(out) * next_g for the next layer (ctx->u_for).
 sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf16* x, int ldx,
-                     bf16* out, int B, cudaStream_t s) {
+                     bf16* out, int B, cudaStream_t s, const bf16* next_g = nullptr,
+                     int next_layer = -1) {
   const auto& m = ctx->m;
-  // x2 = x + o W_o^T  (into out)
-  CK(gemm(ctx, 6, o, ldo_, W.wo, B, m.hidden, ctx->qdim, sidp::EPI_RESID, out, m.hidden, x, ldx,
-          nullptr, s));
-  CK(sidp::rmsnorm_launch(out, m.hidden, W.g_mlp, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
-  count_launch(ctx);
-  CK(gemm(ctx, 1, ctx->u, m.hidden, W.wgu, B, 2 * m.intermediate, m.hidden, sidp::EPI_SILU_MUL,
-          ctx->act, m.intermediate, nullptr, 0, nullptr, s));
-  CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, m.hidden, m.intermediate, sidp::EPI_RESID,
-          out, m.hidden, out, m.hidden, nullptr, s));
+  const int h = m.hidden;
+  // x2 = x + o W_o^T  (into out), u2 = RMSNorm(x2) * g_mlp
+  sidp::PartialSrc part{};
+  if (sidp::gemm_partial_ok(B, h, ctx->qdim, ctx->gemm_ws_bytes)) {
+    CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_PARTIAL, nullptr, 0, nullptr, 0,
+            nullptr, s, nullptr, &part));
+    CK(sidp::resid_norm_launch(part, x, ldx, out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
+    count_launch(ctx);
+  } else {
+    CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, out, h, x, ldx, nullptr, s));
+    CK(sidp::rmsnorm_launch(out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
+    count_launch(ctx);
+  }
+  CK(gemm(ctx, 1, ctx->u, h, W.wgu, B, 2 * m.intermediate, h, sidp::EPI_SILU_MUL, ctx->act,
+          m.intermediate, nullptr, 0, nullptr, s));
+  if (next_g && sidp::gemm_partial_ok(B, h, m.intermediate, ctx->gemm_ws_bytes)) {
+    CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_PARTIAL,
+            nullptr, 0, nullptr, 0, nullptr, s, nullptr, &part));
+    CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s));
+    count_launch(ctx);
+    ctx->u_for = next_layer;
+  } else {
+    CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_RESID, out, h,
+            out, h, nullptr, s));
+  }
   return SIDP_OK;
 }
 
@@ -391,7 +442,7 @@ sidp_status full_layer(sidp_ctx* ctx, const LayerW& W, bf16* x, int B, int layer
                        const sidp_kv* kv, cudaStream_t s) {
   sidp_status st = attn_part(ctx, W, x, B, layer, kv, nullptr, s);
   if (st != SIDP_OK) return st;
-  return mlp_part(ctx, W, ctx->o, ctx->qdim, x, ctx->m.hidden, x, B, s);
+  return mlp_part(ctx, W, ctx->o, ctx->qdim, x, ctx->m.hidden, x, B, s, ctx->chain_g, layer + 1);
 }
 
 // ---- WaS fetch pump ----
@@ -1043,17 +1094,26 @@ static sidp_status step_body(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s)
     count_launch(ctx);
   }
   const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
+  ctx->u_for = -1;
   for (int l = 0; l < ctx->L; ++l) {
     if (b->layer_inputs && B > 0) {
       CK(cudaMemcpyAsync(reinterpret_cast<bf16*>(b->layer_inputs) + (size_t)l * B * m.hidden, x,
                          (size_t)B * m.hidden * 2, cudaMemcpyDeviceToDevice, s));
     }
+    // WaS: the next layer's input-norm gain (always local, R2) lets this layer's down-GEMM
+    // fix-up produce the next layer's u
+    ctx->chain_g = mode == SIDP_WAS ? (l + 1 < ctx->L ? local_gain(ctx, l + 1, C_GATTN) : ctx->g_final)
+                                    : nullptr;
     st = sidp_decode_layer(ctx, x, B, l, mode, &b->kv, s);
+    ctx->chain_g = nullptr;
     if (st != SIDP_OK) return st;
   }
   if (B > 0) {
-    CK(sidp::rmsnorm_launch(x, m.hidden, ctx->g_final, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
-    count_launch(ctx);
+    if (ctx->u_for != ctx->L) {
+      CK(sidp::rmsnorm_launch(x, m.hidden, ctx->g_final, m.rms_eps, ctx->u, m.hidden, B, m.hidden, s));
+      count_launch(ctx);
+    }
+    ctx->u_for = -1;
     CK(sidp::argmax_reset_launch(ctx->amax, B, s));
     count_launch(ctx);
     CK(gemm(ctx, 7, ctx->u, m.hidden, ctx->wlm, B, m.vocab, m.hidden, sidp::EPI_ARGMAX, ctx->amax,
@@ -1324,6 +1384,28 @@ sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ld
   cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, counters, 1 << 16},
                                     reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
+sidp_status sidp_test_gemm_resid_norm(const void* x, int32_t ldx, const void* w, int32_t M,
+                                      int32_t N, int32_t K, const void* resid, int32_t ldr,
+                                      const void* g, float eps, void* xout, void* u, void* stream) {
+  static float* ws = nullptr;
+  static const size_t ws_bytes = (size_t)256 << 20;
+  if (!ws && cudaMalloc(&ws, ws_bytes) != cudaSuccess) return fail(SIDP_ENOMEM, "test workspace");
+  if (!sidp::gemm_partial_ok(M, N, K, ws_bytes))
+    return fail(SIDP_EINVAL, "shape %dx%dx%d not eligible for the deferred fix-up", M, N, K);
+  sidp::PartialSrc part{};
+  sidp::GemmArgs a{};
+  a.x = reinterpret_cast<const bf16*>(x); a.ldx = ldx; a.w = reinterpret_cast<const bf16*>(w);
+  a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = sidp::EPI_PARTIAL; a.partial_out = &part;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, nullptr, 0}, s);
+  if (e == cudaSuccess)
+    e = sidp::resid_norm_launch(part, reinterpret_cast<const bf16*>(resid), ldr,
+                                reinterpret_cast<bf16*>(xout), N, reinterpret_cast<const bf16*>(g),
+                                eps, reinterpret_cast<bf16*>(u), N, M, N, s);
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm_resid_norm: %s", cudaGetErrorString(e));
   return SIDP_OK;
 }
 

@@ -108,6 +108,33 @@ def test_gemm_bf16_bias_and_residual(P, M, N, K, orient):
     assert (d2 <= ref2.abs() * 2.0 ** -8 + 1e-6 * ref2.abs().max()).all()
 
 
+@pytest.mark.parametrize("M,N,K", [(8, 256, 256), (100, 640, 1024), (256, 5120, 8192),
+                                   (200, 1000, 2048), (300, 512, 512), (128, 2048, 25600)])
+def test_gemm_deferred_fixup_resid_norm(P, M, N, K):
+    """EPI_PARTIAL stream-K slices summed by resid_norm: x2 = x W^T + resid, u = RMSNorm(x2) g
+    (SURVEY.md a8+a9 / a11+a5), vs the fp64 product of the same bf16 operands."""
+    g = torch.Generator().manual_seed(M + N + K)
+    x = _lvl((M, K), g).cuda()
+    w = _lvl((N, K), g, 2.0 ** -6).cuda()
+    r = _lvl((M, N), g).cuda()
+    gain = (1 + _lvl((N,), g, 2.0 ** -3).float()).to(torch.bfloat16).cuda()
+    xout = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    u = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    eps = 1e-6
+    P.test_gemm_resid_norm(x, w, r, gain, eps, xout, u)
+    torch.cuda.synchronize()
+    ref = x.cpu().double() @ w.cpu().double().T + r.cpu().double()
+    got = xout.cpu().double()
+    assert ((got - ref).abs() <= ref.abs() * 2.0 ** -8 + 1e-6 * ref.abs().max()).all()
+    ur = got * torch.rsqrt((got * got).mean(-1, keepdim=True) + eps) * gain.cpu().double()
+    assert ((u.cpu().double() - ur).abs() <= ur.abs() * 2.0 ** -7 + 1e-6 * ur.abs().max()).all()
+    # in place (resid aliases xout), as the hot path runs it
+    r2 = r.clone()
+    P.test_gemm_resid_norm(x, w, r2, gain, eps, r2, u)
+    torch.cuda.synchronize()
+    assert torch.equal(r2, xout)
+
+
 @pytest.mark.parametrize("M,F,K,splits", [(8, 64, 256, 1), (33, 192, 512, 0), (256, 640, 1024, 4),
                                           (200, 328, 512, -1), (300, 1040, 256, -1), (40, 200, 256, -1)])
 def test_gemm_silu_mul(P, M, F, K, splits):
