@@ -31,15 +31,20 @@ enum GemmEpilogue : int {
 // are (tile_m tokens x tile_f features); tile index t = sw ? (m / tile_m) * f_tiles + n / tile_f
 // : (n / tile_f) * m_tiles + m / tile_m; the t-th tile covers k-steps [t nks, (t+1) nks) of
 // the stream-K range split evenly over `clusters` CTA pairs.
+constexpr int kPartialMaxTiles = 128;
 struct PartialSrc {
   const float* ws;
   int M, N;
   int sw, tile_m, tile_f, m_tiles, f_tiles;
   int nks, clusters;
   long long total_kb;
+  unsigned char nseg[kPartialMaxTiles];   // partial_nseg of every tile (tiles <= 128), host-built
 };
 __host__ __device__ inline int partial_cluster_of(long long g, long long total, int C) {
   return (int)(((g + 1) * (long long)C + total - 1) / total) - 1;
+}
+__host__ __device__ inline int partial_tile(const PartialSrc& p, int m, int n) {
+  return p.sw ? (m / p.tile_m) * p.f_tiles + n / p.tile_f : (n / p.tile_f) * p.m_tiles + m / p.tile_m;
 }
 __host__ __device__ inline int partial_nseg(const PartialSrc& p, int m, int n) {
   const long long t = p.sw ? (long long)(m / p.tile_m) * p.f_tiles + n / p.tile_f

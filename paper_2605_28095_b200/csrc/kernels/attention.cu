@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
       // deferred stream-K fix-up: a head lies inside one 256-feature tile (hd divides 256),
       // so its partial slices are summed in slice order, then the bias is added
       const int n = head * HD;
-      const int nseg = partial_nseg(a.part, b, n);
+      const int nseg = a.part.nseg[partial_tile(a.part, b, n)];
       const float* src = a.part.ws + (size_t)b * a.part.N + n;
 #pragma unroll
       for (int sgi = 0; sgi < 4; ++sgi)   // issued together (predicated), summed in order
@@ -135,6 +135,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
                : "memory");
 }
+// K/V are streamed once per step: evict-first keeps L2 for the small re-read tensors
+__device__ __forceinline__ void cp_async16_ef(void* smem, const void* gmem, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)),
+               "l"(gmem), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -175,6 +181,7 @@ struct AttnParams {
   int* cnt;                  // [B * nkv] arrival counters of split pairs (zero between launches)
   int B, nq, nkv, smax;
   int pair_mode;             // grid == B * nkv: one whole (b, g) pair per CTA
+  int kv_evict;              // K/V loads carry an L2 evict-first policy
   float scale_log2;
 };
 
@@ -300,6 +307,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     float mrow[2] = {-INFINITY, -INFINITY};
     float lrow[2] = {0.0f, 0.0f};
 
+    uint64_t kvpol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kvpol));
     auto load_chunk = [&](int stage, int ch) {
       const int t0 = ch * kChunk;
       bf16* sk = wbuf + stage * 2 * TILE;
@@ -310,8 +319,13 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
         const int row = e / CPR, cc = e % CPR;
         const int t = min(t0 + row, n_tok - 1);
         const int sw = (cc ^ (row & 7));
-        cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
-        cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+        if (p.kv_evict) {
+          cp_async16_ef(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8, kvpol);
+          cp_async16_ef(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8, kvpol);
+        } else {
+          cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
+          cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+        }
       }
     };
 
@@ -602,6 +616,8 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   AttnParams p;
   p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws; p.cnt = a.cnt;
   p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
+  static const int env_evict = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
+  p.kv_evict = env_evict;
   p.pair_mode = (long long)ctas == pairs ? 1 : 0;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
   return launch_pdl(attn_kernel<HD, ST>, dim3(ctas), dim3(128), smem, s, p);

@@ -52,6 +52,7 @@ struct KParams {
   int* counters;
   int a3d, b3d;                 // operand map is k-block-major 3-D: one TMA box per stage
   int partial_all;              // EPI_PARTIAL: every unit writes its fp32 partial slice
+  int w_evict;                  // weight TMA loads carry an L2 evict-first policy
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
   QkvEpi qkv;                   // EPI_QKV destination
@@ -82,6 +83,22 @@ SIDP_DEV void tma_load_2d_2sm(const CUtensorMap* m, uint32_t leader_bar, void* s
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(leader_bar)
       : "memory");
+}
+// same, with an L2 cache policy (createpolicy): weights are streamed exactly once per step,
+// so they are loaded evict-first and the small re-read tensors (activations, partial slices)
+// keep their L2 lines
+SIDP_DEV void tma_load_2d_2sm_hint(const CUtensorMap* m, uint32_t leader_bar, void* smem_dst, int c0,
+                                   int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy)
+      : "memory");
+}
+SIDP_DEV uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 SIDP_DEV void tma_load_3d_2sm(const CUtensorMap* m, uint32_t leader_bar, void* smem_dst, int c0,
                               int c1, int c2) {
@@ -532,6 +549,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
       // Only the leader arrives on a stage's full barrier (expecting both CTAs' bytes); the
       // peer's TMA completes its transaction bytes on the leader's barrier directly.
       const uint32_t stage_tx = 2 * (a_bytes + b_bytes);
+      const uint64_t wpol = policy_evict_first();
       // issue one operand of ring iteration (unit x, k-step kb) into stage s
       auto load_a = [&](const Unit& x, int kb, int s, uint32_t lbar) {
         const int arow = x.ft * 2 * WROWS + rank * WROWS;
@@ -539,8 +557,12 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           tma_load_3d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes, 0, arow, kb * KPS);
         } else {
 #pragma unroll
-          for (int j = 0; j < KPS; ++j)
-            tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes + j * a_sub, (kb * KPS + j) * BK, arow);
+          for (int j = 0; j < KPS; ++j) {
+            if (!SW && p.w_evict)
+              tma_load_2d_2sm_hint(&tm_w, lbar, sA + (size_t)s * a_bytes + j * a_sub, (kb * KPS + j) * BK, arow, wpol);
+            else
+              tma_load_2d_2sm(&tm_w, lbar, sA + (size_t)s * a_bytes + j * a_sub, (kb * KPS + j) * BK, arow);
+          }
         }
       };
       auto load_b = [&](const Unit& x, int kb, int s, uint32_t lbar) {
@@ -549,8 +571,12 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           tma_load_3d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes, 0, brow, kb * KPS);
         } else {
 #pragma unroll
-          for (int j = 0; j < KPS; ++j)
-            tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, brow);
+          for (int j = 0; j < KPS; ++j) {
+            if (SW && p.w_evict)
+              tma_load_2d_2sm_hint(&tm_x, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, brow, wpol);
+            else
+              tma_load_2d_2sm(&tm_x, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, brow);
+          }
         }
       };
       // Weights never depend on the preceding kernel of the chain (they are resident, or were
@@ -1019,7 +1045,7 @@ bool gemm_partial_ok(int M, int N, int K, size_t ws_bytes) {
   const long long wm_tiles = (long long)((N + 2 * WROWS - 1) / (2 * WROWS)) * ((M + 255) / 256);
   if (wm_tiles >= pair_slots) return false;   // whole tiles fill the machine: no split, no fix-up
   const PartialPlan q = plan_partial(M, N, K, pair_slots);
-  return (size_t)q.max_seg * M * N * 4 <= ws_bytes;
+  return q.tiles <= kPartialMaxTiles && q.max_seg <= 255 && (size_t)q.max_seg * M * N * 4 <= ws_bytes;
 }
 
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t stream) {
@@ -1117,6 +1143,10 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
       o.tile_m = sw ? 2 * WROWS : BNT; o.tile_f = sw ? BNT : 2 * WROWS;
       o.m_tiles = sw ? n_pairs : m_tiles; o.f_tiles = sw ? m_tiles : n_pairs;
       o.nks = nkb; o.clusters = clusters; o.total_kb = q.total;
+      if (tiles > kPartialMaxTiles) return cudaErrorInvalidValue;
+      for (int t = 0; t < tiles; ++t)
+        o.nseg[t] = (unsigned char)(partial_cluster_of((long long)(t + 1) * nkb - 1, q.total, clusters) -
+                                    partial_cluster_of((long long)t * nkb, q.total, clusters) + 1);
     }
   }
   if (!streamk) clusters = std::min(tiles, pair_slots);
@@ -1154,6 +1184,8 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.ws = w.ws; p.counters = w.counters;
   p.a3d = a3d; p.b3d = b3d;
   p.partial_all = part ? 1 : 0;
+  static int env_evict = getenv("SIDP_GEMM_W_EVICT") ? atoi(getenv("SIDP_GEMM_W_EVICT")) : 1;
+  p.w_evict = env_evict;
   if (a.qkv) p.qkv = *a.qkv;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;

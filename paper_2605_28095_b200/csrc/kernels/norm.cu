@@ -1,6 +1,7 @@
 // norm.cu — RMSNorm, embedding gather, argmax finalisation.
 // HBM-bound row kernels: 16-byte vector loads, fp32 statistics, one bf16 rounding.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../common.cuh"
 #include "../kernels.h"
@@ -104,25 +105,24 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const bf16* __res
 // rounded once to bf16 (x_out, the residual stream); the norm statistics use the rounded
 // x_out, exactly as rmsnorm_kernel on a stored x_out.  The slice loads of a vector are issued
 // together (unrolled, predicated): the kernel is bound by their L2 round trips otherwise.
-constexpr int kFixSeg = 4, kMaxFixTiles = 128;
+constexpr int kFixSeg = 4;
 __global__ void __launch_bounds__(640, 2) resid_norm_kernel(
     const PartialSrc ps, const bf16* __restrict__ resid, int ldr, bf16* xout, int ldx,
-    const bf16* __restrict__ g, float eps, bf16* __restrict__ u, int ldu, int h) {
-  pdl_trigger();
+    const bf16* __restrict__ g, float eps, bf16* __restrict__ u, int ldu, int h, int rows,
+    int late_trigger) {
+  if (!late_trigger) pdl_trigger();
   pdl_wait();
-  const int row = blockIdx.x;
   const int nvec = h / 8;
   const size_t slice = (size_t)ps.M * ps.N;
+  __shared__ float red[32];
+  // rows are walked by a grid of at most one CTA per SM, so the CTAs fit beside the next
+  // kernel's early-launched (PDL) CTAs instead of queueing behind them
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
   const float* wrow = ps.ws + (size_t)row * ps.N;
-  // segment count of each feature tile of this row, computed once (64-bit divisions)
-  __shared__ int nseg_of[kMaxFixTiles];
-  for (int t = threadIdx.x; t * ps.tile_f < ps.N; t += blockDim.x)
-    nseg_of[t] = partial_nseg(ps, row, t * ps.tile_f);
-  __syncthreads();
   float ss = 0.0f;
   for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
     const int n = k * 8;
-    const int nseg = nseg_of[n / ps.tile_f];
+    const int nseg = ps.nseg[partial_tile(ps, row, n)];
     const float* src = wrow + n;
     const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
     float4 lo[kFixSeg], hi[kFixSeg];
@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(640, 2) resid_norm_kernel(
     ss += o0.x * o0.x + o0.y * o0.y + o1.x * o1.x + o1.y * o1.y + o2.x * o2.x + o2.y * o2.y +
           o3.x * o3.x + o3.y * o3.y;
   }
-  __shared__ float red[32];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
@@ -180,6 +179,9 @@ __global__ void __launch_bounds__(640, 2) resid_norm_kernel(
   // re-read this thread's own x_out vectors (L1/L2 hits)
   for (int k = threadIdx.x; k < nvec; k += blockDim.x)
     scale(*reinterpret_cast<const uint4*>(xout + (size_t)row * ldx + k * 8), k);
+  __syncthreads();   // red is reused by the next row
+  }
+  if (late_trigger) pdl_trigger();
 }
 
 __global__ void embed_kernel(const bf16* __restrict__ E, int h, const int32_t* __restrict__ tok,
@@ -223,11 +225,20 @@ cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, 
                               const bf16* g, float eps, bf16* u, int ldu, int rows, int h,
                               cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  if (h % 8 || ps.ws == nullptr || ps.N != h || rows > ps.M || ps.N > kMaxFixTiles * ps.tile_f)
-    return cudaErrorInvalidValue;
+  if (h % 8 || ps.ws == nullptr || ps.N != h || rows > ps.M) return cudaErrorInvalidValue;
   const int threads = std::min(640, (h / 8 + 31) / 32 * 32);
-  return launch_pdl(resid_norm_kernel, dim3(rows), dim3(threads), 0, s, ps, resid, ldr, xout, ldx,
-                    g, eps, u, ldu, h);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // SIDP_FIX_GRID: 0 = one CTA per row; else at most one CTA per SM (default)
+  static const int grid_mode = getenv("SIDP_FIX_GRID") ? atoi(getenv("SIDP_FIX_GRID")) : 1;
+  static const int late = getenv("SIDP_FIX_LATE_TRIGGER") ? atoi(getenv("SIDP_FIX_LATE_TRIGGER")) : 0;
+  const int grid = grid_mode ? std::min(rows, sms) : rows;
+  return launch_pdl(resid_norm_kernel, dim3(grid), dim3(threads), 0, s, ps, resid, ldr, xout, ldx,
+                    g, eps, u, ldu, h, rows, late);
 }
 
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,

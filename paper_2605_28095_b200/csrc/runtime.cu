@@ -308,6 +308,13 @@ LayerW layer_weights(const sidp_ctx* c, const bf16* pooled, const bf16* local) {
                 P(C_GMLP), P(C_GQ), P(C_GK), P(C_BQKV)};
 }
 
+// perf experiments only (results are wrong): SIDP_DEBUG_SKIP bit 1 = qkv_post, 2 = resid_norm,
+// 4 = attention — the marginal cost of a kernel inside the pipelined step
+int dbg_skip() {
+  static const int v = getenv("SIDP_DEBUG_SKIP") ? atoi(getenv("SIDP_DEBUG_SKIP")) : 0;
+  return v;
+}
+
 // a gain that is never pooled (R2): the layer's local blob
 const bf16* local_gain(const sidp_ctx* c, int layer, int comp) {
   return c->local + (size_t)layer * c->local_elems + c->comp_off[comp];
@@ -386,7 +393,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
       qa.part = part;
       qa.bias = W.b_qkv;
     }
-    CK(sidp::qkv_post_launch(qa, s));
+    if (!(dbg_skip() & 1)) CK(sidp::qkv_post_launch(qa, s));
     count_launch(ctx);
   }
   sidp::AttnArgs aa{};
@@ -397,7 +404,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   aa.max_tokens = ctx->c.max_ctx; aa.ws = ctx->attn_ws; aa.ws_bytes = ctx->attn_ws_bytes;
   aa.cnt = ctx->attn_cnt; aa.n_cnt = ctx->n_attn_cnt;
   timing_begin(ctx, 2, s);
-  CK(sidp::attention_launch(aa, s));
+  if (!(dbg_skip() & 4)) CK(sidp::attention_launch(aa, s));
   timing_end(ctx, 2, s);
   count_launch(ctx, sidp::attention_last_launch_count());
   return SIDP_OK;
@@ -416,7 +423,7 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
   if (sidp::gemm_partial_ok(B, h, ctx->qdim, ctx->gemm_ws_bytes)) {
     CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_PARTIAL, nullptr, 0, nullptr, 0,
             nullptr, s, nullptr, &part));
-    CK(sidp::resid_norm_launch(part, x, ldx, out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
+    if (!(dbg_skip() & 2)) CK(sidp::resid_norm_launch(part, x, ldx, out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
   } else {
     CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, out, h, x, ldx, nullptr, s));
@@ -428,7 +435,7 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
   if (next_g && sidp::gemm_partial_ok(B, h, m.intermediate, ctx->gemm_ws_bytes)) {
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_PARTIAL,
             nullptr, 0, nullptr, 0, nullptr, s, nullptr, &part));
-    CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s));
+    if (!(dbg_skip() & 2)) CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
     ctx->u_for = next_layer;
   } else {
