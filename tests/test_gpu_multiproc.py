@@ -63,8 +63,9 @@ def _run_rank(rank, world, port, mode, pool, batches, steps, q):
             ctx.step(toks, nxt, kv, batch=B, logits=logits)
             torch.cuda.synchronize()
             out.append((nxt[:B].cpu().numpy().copy(), logits[:B].cpu().numpy().copy()))
-            if B:
-                toks = nxt[:B].clone()
+            if B:   # teacher-forced: the next inputs do not depend on this step's argmax, so a
+                # near-tie decided differently by CaS and replicated rounding cannot fork the runs
+                toks = torch.from_numpy(gen.tokens(SEED + s + 1, bg, m.vocab)).to(torch.int32).cuda()
                 kv.advance(1, B)
         st = ctx.stats()
         log = ctx.fetch_log()
@@ -94,7 +95,7 @@ def _replicated(batches, r, steps, pool):
         ctx.step(toks, nxt, kv, batch=B, logits=logits)
         torch.cuda.synchronize()
         out.append((nxt[:B].cpu().numpy().copy(), logits[:B].cpu().numpy().copy()))
-        toks = nxt[:B].clone()
+        toks = torch.from_numpy(gen.tokens(SEED + s + 1, bg, m.vocab)).to(torch.int32).cuda()
         kv.advance(1, B)
     ctx.destroy()
     return out
