@@ -51,6 +51,14 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=8)
+    ap.add_argument("--emulate-world", type=int, default=8,
+                    help="N=1 only: also time rank 0 of a d-rank WaS group on this GPU, the d-1 "
+                         "owners being serve-only contexts in local HBM (0 = off)")
+    ap.add_argument("--emulate-fetch-sms", type=int, default=16,
+                    help="fetch CTAs of the emulated rank: 16 read local HBM at ~NVLink 5 rate")
+    ap.add_argument("--emulate-batch", type=int, default=None)
+    ap.add_argument("--emulate-ctx", type=int, default=None)
+    ap.add_argument("--emulate-steps", type=int, default=4)
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 with a gloo control plane (functional multi-process "
                          "test of the IPC path on a 1-GPU box; not a scaling number)")
@@ -232,6 +240,92 @@ def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms):
             "frac_T3": T3 * 1e3 / step_ms, "nvlink_bytes_per_step": remote,
             "peaks": {"bf16_tflops": peaks["tflops"], "hbm_gbs": peaks["hbm"],
                       "nvlink_gbs": peaks["nvl"]}}
+
+
+# ----------------------------------------------------------------------------- WaS emulation
+def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, peaks):
+    """Rank 0 of a W-rank WaS group on ONE GPU (SURVEY.md §8(a) a2-a4 at full size): the W-1
+    other owners are serve-only contexts (sidp_alloc_serve_only) whose arenas sit in this GPU's
+    HBM, so the fetch kernel reads local HBM instead of a peer over NVLink.  With
+    --emulate-fetch-sms 16 it reads at ~766 GB/s (profiles/r1_fetch_local.json), the NVLink 5
+    reader rate; HBM traffic equals a real rank's (its slot writes + one owner's serve reads
+    under the stagger).  Not a multi-GPU number: NVLink latency and the other ranks' compute
+    are absent."""
+    import numpy as np
+    import torch
+    max_ctx = kv.max_ctx
+    slots = args.slots or wl.slots
+    ctx0 = P.Context(m, rank=0, world=W, slots=slots, order=args.order, pool=args.pool,
+                     max_batch=kv.max_batch, max_ctx=max_ctx, fetch_sms=args.emulate_fetch_sms,
+                     fetch_engine=args.fetch, stagger=not args.no_stagger, device=local, seed=seed)
+    peers = []
+    try:
+        for r in range(1, W):
+            c = P.Context(m, rank=r, world=W, slots=slots, pool=args.pool, max_batch=kv.max_batch,
+                          max_ctx=max_ctx, device=local, seed=seed, alloc=False)
+            c.alloc_serve_only()
+            peers.append(c)
+        with torch.cuda.stream(stream):
+            ctx0.init_weights_synthetic(stream=stream)
+            for c in peers:
+                c.init_weights_synthetic(stream=stream)
+        stream.synchronize()
+        ctx0.import_handles([ctx0.export_handles()] + [c.export_handles() for c in peers])
+        kv.set_pos(np.full(B, ctx_len))
+
+        def step():
+            ctx0.step(tok, tok, kv, batch=B, stream=stream, advance_pos=True)
+
+        all_mask = sum(1 << c for c in CLS_NAMES)
+        warm = max(2, min(args.warmup, 3))
+        for i in range(warm):
+            if i == warm - 1:
+                ctx0.set_timing(all_mask)
+            step()
+        stream.synchronize()
+        st0 = ctx0.stats()
+        shares = st0["timed_ms"]
+        us_layer = {CLS_NAMES[c]: round(shares[c] * 1e3 / m.num_layers, 2) for c in CLS_NAMES
+                    if shares[c] > 0}
+        ctx0.set_timing(1 << 3)
+        pos_before = kv.max_pos
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.emulate_steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / args.emulate_steps
+        st = ctx0.stats()
+        n_f = st["timed_launches"][3] - st0["timed_launches"][3]
+        f_ms = (st["timed_ms"][3] - st0["timed_ms"][3]) / max(1, n_f)
+        lb = st["layer_bytes"]
+        fetch_gbs = lb / (f_ms * 1e-3) / 1e9 if f_ms > 0 else None
+        ctx_avg = pos_before + (args.emulate_steps - 1) / 2.0
+        ns = north_star_roofline(m, B, ctx_avg, W, peaks, ms)
+        remote_layers = m.num_layers - len([l for l in range(m.num_layers) if l % W == 0])
+        return {
+            "what": f"rank 0 of a {W}-rank WaS group on one B200; the {W - 1} other owners are "
+                    "serve-only contexts in local HBM (bench.py was_emulation docstring)",
+            "world_emulated": W, "batch": B, "ctx": ctx_len, "slots": slots,
+            "fetch_sms": args.emulate_fetch_sms, "steps": args.emulate_steps,
+            "ms_per_step": ms, "tokens_s_rank": B / (ms / 1e3),
+            "group_tokens_s_est": W * B / (ms / 1e3),
+            "remote_layers_per_step": remote_layers,
+            "fetch_bytes_per_step": remote_layers * lb,
+            "fetch": {"avg_launch_ms": f_ms, "GBps": fetch_gbs,
+                      "frac_of_nvlink_770": (fetch_gbs / peaks["nvl"]) if fetch_gbs else None,
+                      "fetch_busy_frac": (remote_layers * f_ms / ms) if f_ms else None},
+            "north_star_roofline": ns,
+            "kernel_us_per_layer": us_layer,
+            "footprint_bytes_rank0": {"owned": st["owned_bytes"], "slots": st["slot_bytes"],
+                                      "replicated": st["replicated_bytes"]},
+        }
+    finally:
+        ctx0.destroy()
+        for c in peers:
+            c.destroy()
 
 
 # ----------------------------------------------------------------------------- main arms
@@ -436,8 +530,24 @@ def main():
                                     "replicated": st["replicated_bytes"],
                                     "kv": 2 * kv.k.numel() * 2},
     }
-    print(json.dumps(line), flush=True)
     ctx.destroy()
+    if world == 1 and args.emulate_world > 1:
+        eb = args.emulate_batch or B
+        ec = args.emulate_ctx or ctx_len
+        try:
+            if eb != B or ec + args.warmup + args.emulate_steps + 8 > kv.max_ctx:
+                del kv
+                torch.cuda.empty_cache()
+                kv = P.KVCache(m, eb, ec + args.warmup + args.emulate_steps + 8)
+                with torch.cuda.stream(stream):
+                    kv.fill_synthetic(seed, 0, eb, ec, stream=stream)
+                stream.synchronize()
+                tok = torch.from_numpy(gen.tokens(seed, np.arange(eb), m.vocab)).to(torch.int32).cuda()
+            line["was_emulation"] = was_emulation(args, P, m, wl, seed, local, stream, kv, tok, eb,
+                                                  ec, args.emulate_world, peaks)
+        except Exception as e:   # reported, never fatal for the main line
+            line["was_emulation"] = {"error": str(e)[:300]}
+    print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -152,6 +152,16 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
  * replicated tensors, CaS staging + flags, workspaces, the fetch stream and events. */
 sidp_status sidp_alloc(sidp_ctx* ctx);
 
+/* Alternative to sidp_alloc for a serve-only rank: allocate only the owned-weight arena (and
+ * the small local per-layer blobs and a CaS flag block so the exported blob is well formed).
+ * The rank owns, initialises (sidp_init_weights_synthetic fills only its owned and local
+ * parts) and exports its layers for WaS peers to fetch ("each GPU ... serves its
+ * layers to peers"), but never computes: sidp_step / sidp_decode_layer return SIDP_ESTATE and
+ * it cannot serve CaS.  Used to emulate the d-1 owners of a DP group beside one computing rank
+ * on a single GPU (bench.py --emulate-world).  SIDP_ESTATE if already allocated, SIDP_ENOMEM
+ * on allocation failure (nothing left allocated is leaked: sidp_destroy frees it). */
+sidp_status sidp_alloc_serve_only(sidp_ctx* ctx);
+
 /* K12: fill owned layers, local layer parts and replicated tensors with the counter-hash
  * synthetic values (same function as sidp_inputs/gen.py), on `stream`. */
 sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream);

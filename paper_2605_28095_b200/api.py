@@ -92,6 +92,10 @@ class Context:
     def alloc(self):
         A.check(A.lib().sidp_alloc(self.h), "sidp_alloc")
 
+    def alloc_serve_only(self):
+        """Owner-only rank: allocates and exports its arena, never computes (sidp.h)."""
+        A.check(A.lib().sidp_alloc_serve_only(self.h), "sidp_alloc_serve_only")
+
     def init_weights_synthetic(self, stream=None):
         A.check(A.lib().sidp_init_weights_synthetic(self.h, _stream_ptr(stream)),
                 "sidp_init_weights_synthetic")

@@ -73,6 +73,7 @@ struct sidp_ctx {
   int qdim = 0, kvdim = 0, qkvdim = 0;
   // device state
   bool allocated = false;
+  bool serve_only = false;         // sidp_alloc_serve_only: owns + exports its arena, never computes
   int sticky = 0;
   bf16* arena = nullptr;           // owned pooled blobs
   bf16* local = nullptr;           // L local blobs
@@ -922,6 +923,37 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   return SIDP_OK;
 }
 
+sidp_status sidp_alloc_serve_only(sidp_ctx* ctx) {
+  if (!ctx) return fail(SIDP_EINVAL, "null ctx");
+  if (ctx->allocated) return fail(SIDP_ESTATE, "already allocated");
+  CK(cudaSetDevice(ctx->c.device));
+  const size_t pooled_b = ctx->pooled_elems * 2, local_b = ctx->local_elems * 2;
+  auto dm = [&](void** p, size_t bytes) -> bool {
+    if (cudaMalloc(p, std::max<size_t>(bytes, 256)) == cudaSuccess) return true;
+    cudaGetLastError();
+    fail(SIDP_ENOMEM, "cudaMalloc(%zu)", bytes);
+    return false;
+  };
+  if (!dm(reinterpret_cast<void**>(&ctx->arena), std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b) ||
+      !dm(reinterpret_cast<void**>(&ctx->local), (size_t)ctx->L * local_b))
+    return SIDP_ENOMEM;
+  // a flag block only, so the exported blob is well-formed (a serve-only rank serves no CaS)
+  ctx->cas_bytes = 4096;
+  ctx->cas_stage_off = ctx->cas_recv_off = 4096;
+  if (!dm(reinterpret_cast<void**>(&ctx->cas), ctx->cas_bytes)) return SIDP_ENOMEM;
+  CK(cudaMemset(ctx->cas, 0, ctx->cas_bytes));
+  ctx->peer_arena.assign(ctx->d, nullptr);
+  ctx->peer_arena[ctx->r] = ctx->arena;
+  ctx->peer_cas.assign(ctx->d, nullptr);
+  ctx->peer_cas[ctx->r] = ctx->cas;
+  ctx->serve_only = true;
+  ctx->allocated = true;
+  ctx->st.layer_bytes = pooled_b;
+  ctx->st.local_layer_bytes = local_b;
+  ctx->st.owned_bytes = ctx->owned_layers.size() * pooled_b;
+  return SIDP_OK;
+}
+
 sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream) {
   sidp_status st = check_ready(ctx);
   if (st != SIDP_OK) return st;
@@ -981,6 +1013,7 @@ sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream) {
         return SIDP_ECUDA;
     }
   }
+  if (ctx->serve_only) return SIDP_OK;   // no replicated tensors on a serve-only rank
   if (!gen(ctx->embed, m.vocab, m.hidden, EMBED, 0, sidp::GEN_UNIT, 0, 0, 0)) return SIDP_ECUDA;
   if (!gen(ctx->g_final, 1, m.hidden, G_FINAL, 0, sidp::GEN_GAIN, 0, 0, 0)) return SIDP_ECUDA;
   if (!gen(ctx->wlm, m.vocab, m.hidden, WLM, 0, sidp::GEN_WEIGHT, m.hidden, 0, 0)) return SIDP_ECUDA;
@@ -1054,6 +1087,7 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
   if (!ctx) return fail(SIDP_EINVAL, "null ctx");
   sidp_status st = check_ready(ctx);
   if (st != SIDP_OK) return st;
+  if (ctx->serve_only) return fail(SIDP_ESTATE, "serve-only context does not compute");
   if (layer < 0 || layer >= ctx->L) return fail(SIDP_EINVAL, "layer %d out of range", layer);
   if (batch < 0 || batch > ctx->c.max_batch) return fail(SIDP_EINVAL, "batch %d out of range", batch);
   if (batch > 0 && !x) return fail(SIDP_EINVAL, "null x");
@@ -1165,6 +1199,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
   if (!ctx || !b) return fail(SIDP_EINVAL, "null argument");
   sidp_status st = check_ready(ctx);
   if (st != SIDP_OK) return st;
+  if (ctx->serve_only) return fail(SIDP_ESTATE, "serve-only context does not compute");
   const int B = b->batch;
   if (B < 0 || B > ctx->c.max_batch) return fail(SIDP_EINVAL, "batch %d out of range", B);
   if (B > 0 && (!b->tokens || !b->next)) return fail(SIDP_EINVAL, "null tokens/next");

@@ -118,6 +118,40 @@ def _group(P, m, d, B, **kw):
     return ranks
 
 
+@pytest.mark.parametrize("d,slots", [(4, 2), (8, 1)])
+def test_was_serve_only_peers(P, d, slots):
+    """One computing rank beside d-1 serve-only owners (sidp_alloc_serve_only: arena only, as
+    bench.py --emulate-world uses them): fetch log == oracle FIFO schedule and logits BITWISE
+    equal to the replicated run; the serve-only ranks refuse to compute."""
+    m = MODELS["tiny"].with_layers(8)
+    R = Rank(P, m, rank=0, world=d, B=5, slots=slots)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=5, max_ctx=80, seed=SEED, alloc=False)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    R.ctx.import_handles([R.ctx.export_handles()] + [c.export_handles() for c in peers])
+    steps = 3
+    for s in range(steps):
+        R.step(); R.finish_step()
+    pl = OS.plan(OS.owner_map(m.num_layers, d), d, 0, "exec")
+    log = R.ctx.fetch_log()
+    assert log == OS.slot_schedule(pl, slots, steps + 1)[:len(log)]
+    assert len(log) >= steps * len(pl)
+    rep = _replicated(P, m, 5, 0)
+    for s in range(steps):
+        rep.step(); rep.finish_step()
+        assert torch.equal(rep.history[s][1], R.history[s][1]), s
+    rep.ctx.destroy()
+    with pytest.raises(RuntimeError):
+        peers[0].step(R.toks, R.next, R.kv, batch=5)
+    for c in peers:
+        c.destroy()
+    R.ctx.destroy()
+
+
 def _replicated(P, m, B, b0, **kw):
     kw = {k: v for k, v in kw.items() if k in ("pool",)}
     return Rank(P, m, B=B, b0=b0, **kw)
