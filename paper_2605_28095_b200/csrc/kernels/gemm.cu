@@ -1122,6 +1122,9 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   // whole tiles balance well once every pair has >= 1 tile (measured: qkv 40 tiles, gate/up
   // 200 tiles faster whole); stream-K pays off for heavily underfilled shapes (O, down: 20)
   // whole-row epilogues (argmax over a tile, per-head qk-norm/RoPE) need whole dot products
+  // (Stream-K for badly quantised larger tile counts — e.g. down at M = 1024: 80 tiles on 74
+  // pairs, 2 waves, 282 us vs cuBLAS 192 — measured slower still: 258-295 us at M = 1024 and
+  // 431 vs 301 us at M = 1536, so those shapes keep whole tiles.)
   int streamk = (!sw && a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.k_splits != 1 &&
                  (a.k_splits > 1 || 2 * tiles <= clusters)) ? 1 : 0;
   if (streamk) {
@@ -1185,7 +1188,9 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.a3d = a3d; p.b3d = b3d;
   p.partial_all = part ? 1 : 0;
   static int env_evict = getenv("SIDP_GEMM_W_EVICT") ? atoi(getenv("SIDP_GEMM_W_EVICT")) : 1;
-  p.w_evict = env_evict;
+  // evict-first only when every weight tile is read by one unit (one token tile): with
+  // several token tiles the other units re-read the same W tile from L2
+  p.w_evict = env_evict && (sw ? n_pairs == 1 : m_tiles == 1);
   if (a.qkv) p.qkv = *a.qkv;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
