@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--emulate-batch", type=int, default=None)
     ap.add_argument("--emulate-ctx", type=int, default=None)
     ap.add_argument("--emulate-steps", type=int, default=4)
+    ap.add_argument("--cas-emulate", type=int, default=1,
+                    help="N=1 only: time CaS steps of --emulate-world virtual ranks on this GPU "
+                         "(small-batch tail, SURVEY.md M5 analogue; 0 = off)")
+    ap.add_argument("--cas-ctx", type=int, default=1024)
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 with a gloo control plane (functional multi-process "
                          "test of the IPC path on a 1-GPU box; not a scaling number)")
@@ -320,12 +324,113 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "north_star_roofline": ns,
             "kernel_us_per_layer": us_layer,
             "footprint_bytes_rank0": {"owned": st["owned_bytes"], "slots": st["slot_bytes"],
-                                      "replicated": st["replicated_bytes"]},
+                                      "replicated": st["replicated_bytes"],
+                                      "workspace": st["workspace_bytes"]},
         }
     finally:
         ctx0.destroy()
         for c in peers:
             c.destroy()
+
+
+def cas_emulation(args, P, m, seed, local, W, ctx_len):
+    """CaS tail (SURVEY.md §8(a) a12, M5 analogue) with W virtual ranks on ONE GPU: every rank is
+    a full context with its own arena, KV cache and stream; per layer the owner runs the fused
+    GEMMs over all live rows while the others wait on device flags — as on W GPUs, where the
+    non-owners also idle, so the step time is representative minus NVLink hop latency (the
+    shipped activations are KBs).  Ranks' attention kernels share this GPU (small at B <= 16).
+    Step time = max over ranks of (common start event -> rank's end event)."""
+    import numpy as np
+    import torch
+    from sidp_inputs import gen
+    Bmax = 16
+    steps = max(2, args.emulate_steps)
+    max_ctx = ctx_len + 3 + steps * 8 + 8
+    ranks = []
+    try:
+        for r in range(W):
+            c = P.Context(m, rank=r, world=W, max_batch=Bmax, max_ctx=max_ctx, device=local,
+                          seed=seed, pool=args.pool)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                c.init_weights_synthetic(stream=st)
+                kv = P.KVCache(m, Bmax, max_ctx)
+                kv.fill_synthetic(seed, r * Bmax, Bmax, ctx_len, stream=st)
+            st.synchronize()
+            tok = torch.from_numpy(gen.tokens(seed, np.arange(r * Bmax, (r + 1) * Bmax), m.vocab)).to(torch.int32).cuda()
+            ranks.append((c, st, kv, tok))
+        blobs = [c.export_handles() for c, _, _, _ in ranks]
+        for c, _, _, _ in ranks:
+            c.import_handles(blobs)
+            c.set_mode(1, 0)   # SIDP_CAS from step 0 (collective-consistent: same on all ranks)
+        patterns = [("all live, B=1", [1] * W), ("all live, B=4", [4] * W),
+                    ("all live, B=16", [16] * W), ("half live, B=16", [16] * (W // 2) + [0] * (W - W // 2)),
+                    ("one live, B=16", [16] + [0] * (W - 1))]
+        out = []
+        common = torch.cuda.Stream()
+        xs = [(torch.randn(Bmax, m.hidden, device="cuda") * 0.5).to(torch.bfloat16) for _ in range(W)]
+        for name, bt in patterns:
+            for c, _, kv, _ in ranks:
+                c.set_batches(bt)
+            for r, (c, st, kv, tok) in enumerate(ranks):
+                kv.set_pos(np.full(Bmax, ctx_len))
+            def run(n):
+                # layer by layer across ranks (sidp_decode_layer, the per-layer collective):
+                # enqueuing one rank's whole step first can fill the launch queue while its
+                # stream spins on a flag only a later rank's (not yet enqueued) kernels set
+                evs = []
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(common)
+                for r, (c, st, kv, tok) in enumerate(ranks):
+                    st.wait_event(e0)
+                for _ in range(n):
+                    for layer in range(m.num_layers):
+                        for r, (c, st, kv, tok) in enumerate(ranks):
+                            c.decode_layer(xs[r], layer, 1, kv, batch=bt[r], stream=st)
+                for r, (c, st, kv, tok) in enumerate(ranks):
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(st)
+                    evs.append(e1)
+                torch.cuda.synchronize()
+                return max(e0.elapsed_time(e) for e in evs) / n
+            run(2)   # warm-up
+            ms = run(steps)
+            live = sum(1 for b in bt if b)
+            out.append({"pattern": name, "batches": bt, "ms_per_layer_stack": ms,
+                        "ms_per_layer": ms / m.num_layers,
+                        "group_tokens_s": sum(bt) / (ms / 1e3),
+                        "tokens_s_per_live_rank": (sum(bt) / max(1, live)) / (ms / 1e3)})
+        timeouts = sum(c.stats()["timeouts"] for c, _, _, _ in ranks)
+        return {"what": f"CaS (pool={args.pool}) decode of all {m.num_layers} layers by {W} "
+                        f"virtual ranks on one B200, S_ctx={ctx_len} (bench.py cas_emulation "
+                        "docstring); a full step adds the local embed + LM head; the ranks' "
+                        "per-layer small kernels serialise on this one GPU, so the all-live "
+                        "patterns over-state the W-GPU time",
+                "world_emulated": W, "ctx": ctx_len, "steps": steps, "timeouts": timeouts,
+                "results": out}
+    finally:
+        for c, _, _, _ in ranks:
+            c.destroy()
+
+
+def kv_capacity(m, st_d1, fp_dw, W, util=0.9):
+    """KV tokens per GPU left by the MEASURED per-GPU footprint of this library (owned weights +
+    WaS slots + replicated tensors + workspaces) at a vLLM-style 0.9 memory utilisation: the
+    replicated-DP run (d=1) vs rank 0 of the emulated d=W SiDP group.  PAPER.md:21 reports up
+    to 1.8x (H20/H200/B200, with TP); the arithmetic is SPEC.md:100-103's MemoryBreakdown."""
+    import torch
+    total = torch.cuda.mem_get_info()[1]
+    per_tok = 2 * m.n_kv_heads * m.head_dim * 2 * m.num_layers
+    def tokens(fp):
+        return max(0, int((total * util - fp) // per_tok))
+    fp1 = st_d1["owned_bytes"] + st_d1["slot_bytes"] + st_d1["replicated_bytes"] + st_d1["workspace_bytes"]
+    out = {"gpu_bytes": total, "util": util, "kv_bytes_per_token": per_tok,
+           "replicated_d1": {"footprint_bytes": fp1, "kv_tokens": tokens(fp1)}}
+    if fp_dw:
+        fpw = sum(fp_dw.values())
+        out[f"sidp_d{W}"] = {"footprint_bytes": fpw, "kv_tokens": tokens(fpw)}
+        out["ratio"] = tokens(fpw) / max(1, tokens(fp1))
+    return out
 
 
 # ----------------------------------------------------------------------------- main arms
@@ -547,6 +652,16 @@ def main():
                                                   ec, args.emulate_world, peaks)
         except Exception as e:   # reported, never fatal for the main line
             line["was_emulation"] = {"error": str(e)[:300]}
+        line["kv_capacity"] = kv_capacity(m, st, line["was_emulation"].get("footprint_bytes_rank0"),
+                                          args.emulate_world)
+        if args.cas_emulate:
+            try:
+                del kv
+                torch.cuda.empty_cache()
+                line["cas_emulation"] = cas_emulation(args, P, m, seed, local, args.emulate_world,
+                                                      args.cas_ctx)
+            except Exception as e:
+                line["cas_emulation"] = {"error": str(e)[:300]}
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
