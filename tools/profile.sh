@@ -3,15 +3,19 @@
 # top kernels.  Outputs under gpurun_out/.
 set -x
 mkdir -p gpurun_out
-B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
+B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --emulate-world 0"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 6000 --csv \
    --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
-S="python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e --no-cpu-baseline"
+S="python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e --no-cpu-baseline --emulate-world 0"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 8 -c 1 \
    -o gpurun_out/prof_attn -f $S > gpurun_out/ncu_attn.log 2>&1
 # one decoder layer's GEMMs (qkv, o, gate/up, down) after the warm-up layers, then the LM head
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm2_kernel -s 32 -c 4 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm2_kernel -s 32 -c 5 \
    -o gpurun_out/prof_gemm -f $S > gpurun_out/ncu_gemm.log 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:"qkv_post|rmsnorm|gemm_reduce" -s 24 -c 4 \
+timeout 600 ncu --set full --clock-control none -k regex:"qkv_post|rmsnorm|resid_norm" -s 24 -c 4 \
    -o gpurun_out/prof_small -f $S > gpurun_out/ncu_small.log 2>&1
+# the WaS fetch kernel inside the d=8 single-GPU emulation (2 launches)
+E="python bench.py --steps 1 --warmup 3 --layers 16 --no-e2e --no-cpu-baseline --cas-emulate 0 --emulate-steps 1"
+timeout 600 ncu --set full --clock-control none -k regex:fetch_kernel -s 20 -c 2 \
+   -o gpurun_out/prof_fetch -f $E > gpurun_out/ncu_fetch.log 2>&1
 ls -la gpurun_out
