@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsidp.so")
+# SIDP_LIB: another build of the same library (A/B experiments between builds on one box)
+LIB_PATH = os.environ.get("SIDP_LIB") or os.path.join(HERE, "libsidp.so")
 
 SIDP_OK, SIDP_EINVAL, SIDP_ECUDA, SIDP_ENOMEM, SIDP_ESTATE, SIDP_EPEER, SIDP_ETIMEOUT = 0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "SIDP_OK", -1: "SIDP_EINVAL", -2: "SIDP_ECUDA", -3: "SIDP_ENOMEM",

@@ -106,7 +106,61 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const bf16* __res
 // x_out, exactly as rmsnorm_kernel on a stored x_out.  The slice loads of a vector are issued
 // together (unrolled, predicated): the kernel is bound by their L2 round trips otherwise.
 constexpr int kFixSeg = 4;
-__global__ void __launch_bounds__(640, 2) resid_norm_kernel(
+// one 8-feature vector of the deferred fix-up: fp32 slices summed in slice order (slices past
+// nseg add +0), + the bf16 residual, rounded once; the loads of a vector are issued together
+__device__ __forceinline__ uint4 fix_vector(const PartialSrc& ps, const float* src, size_t slice,
+                                            int nseg, uint4 rr) {
+  float4 lo[kFixSeg], hi[kFixSeg];
+#pragma unroll
+  for (int q = 0; q < kFixSeg; ++q) {
+    lo[q] = hi[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q < nseg) {
+      lo[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
+      hi[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
+    }
+  }
+  float4 al = make_float4(0.f, 0.f, 0.f, 0.f), ah = al;
+#pragma unroll
+  for (int q = 0; q < kFixSeg; ++q) {
+    al.x += lo[q].x; al.y += lo[q].y; al.z += lo[q].z; al.w += lo[q].w;
+    ah.x += hi[q].x; ah.y += hi[q].y; ah.z += hi[q].z; ah.w += hi[q].w;
+  }
+  for (int q = kFixSeg; q < nseg; ++q) {
+    const float4 x0 = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
+    const float4 x1 = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
+    al.x += x0.x; al.y += x0.y; al.z += x0.z; al.w += x0.w;
+    ah.x += x1.x; ah.y += x1.y; ah.z += x1.z; ah.w += x1.w;
+  }
+  const float2 r0 = bf16x2_to_f2(rr.x), r1 = bf16x2_to_f2(rr.y), r2 = bf16x2_to_f2(rr.z),
+               r3 = bf16x2_to_f2(rr.w);
+  return make_uint4(f2_to_bf16x2(al.x + r0.x, al.y + r0.y), f2_to_bf16x2(al.z + r1.x, al.w + r1.y),
+                    f2_to_bf16x2(ah.x + r2.x, ah.y + r2.y), f2_to_bf16x2(ah.z + r3.x, ah.w + r3.y));
+}
+__device__ __forceinline__ float sumsq8(uint4 v) {
+  const float2 o0 = bf16x2_to_f2(v.x), o1 = bf16x2_to_f2(v.y), o2 = bf16x2_to_f2(v.z),
+               o3 = bf16x2_to_f2(v.w);
+  return o0.x * o0.x + o0.y * o0.y + o1.x * o1.x + o1.y * o1.y + o2.x * o2.x + o2.y * o2.y +
+         o3.x * o3.x + o3.y * o3.y;
+}
+__device__ __forceinline__ uint4 scale8(uint4 v, uint4 gw, float r) {
+  uint4 o;
+  uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+  const uint32_t vw[4] = {v.x, v.y, v.z, v.w}, gg[4] = {gw.x, gw.y, gw.z, gw.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 x = bf16x2_to_f2(vw[q]), gf = bf16x2_to_f2(gg[q]);
+    ow[q] = f2_to_bf16x2(x.x * r * gf.x, x.y * r * gf.y);
+  }
+  return o;
+}
+
+// Deferred stream-K fix-up + residual + RMSNorm (see resid_norm_launch): the rows are walked by
+// a grid of at most one CTA per SM (fits beside the next kernel's early-launched PDL CTAs); one
+// thread per 8-feature vector.  When every thread holds one vector (h <= 8 x blockDim) the
+// slices, residual and gain of a row are all loaded in ONE round trip and x stays in registers
+// for the scaling pass; the norm statistics use the rounded x_out, exactly as rmsnorm_kernel
+// would on a stored x_out.  Longer rows take the looped path (re-reads its own x_out).
+__global__ void __launch_bounds__(1024, 1) resid_norm_kernel(
     const PartialSrc ps, const bf16* __restrict__ resid, int ldr, bf16* xout, int ldx,
     const bf16* __restrict__ g, float eps, bf16* __restrict__ u, int ldu, int h, int rows,
     int late_trigger) {
@@ -114,72 +168,52 @@ __global__ void __launch_bounds__(640, 2) resid_norm_kernel(
   pdl_wait();
   const int nvec = h / 8;
   const size_t slice = (size_t)ps.M * ps.N;
+  const bool one = nvec <= (int)blockDim.x;
   __shared__ float red[32];
-  // rows are walked by a grid of at most one CTA per SM, so the CTAs fit beside the next
-  // kernel's early-launched (PDL) CTAs instead of queueing behind them
+  auto block_sum = [&](float v) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float tot = red[0];
+    __syncthreads();   // red is reused by the next row
+    return tot;
+  };
   for (int row = blockIdx.x; row < rows; row += gridDim.x) {
-  const float* wrow = ps.ws + (size_t)row * ps.N;
-  float ss = 0.0f;
-  for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
-    const int n = k * 8;
-    const int nseg = ps.nseg[partial_tile(ps, row, n)];
-    const float* src = wrow + n;
-    const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
-    float4 lo[kFixSeg], hi[kFixSeg];
-#pragma unroll
-    for (int q = 0; q < kFixSeg; ++q) {
-      lo[q] = hi[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (q < nseg) {
-        lo[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
-        hi[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
+    const float* wrow = ps.ws + (size_t)row * ps.N;
+    if (one) {
+      const int k = threadIdx.x, n = k * 8;
+      uint4 x = make_uint4(0u, 0u, 0u, 0u), gw = x;
+      if (k < nvec) {
+        gw = *reinterpret_cast<const uint4*>(g + n);
+        const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
+        x = fix_vector(ps, wrow + n, slice, ps.nseg[partial_tile(ps, row, n)], rr);
+        *reinterpret_cast<uint4*>(xout + (size_t)row * ldx + n) = x;
+      }
+      const float r = rsqrtf(block_sum(k < nvec ? sumsq8(x) : 0.0f) / (float)h + eps);
+      if (k < nvec) *reinterpret_cast<uint4*>(u + (size_t)row * ldu + n) = scale8(x, gw, r);
+    } else {
+      float ss = 0.0f;
+      for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
+        const int n = k * 8;
+        const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
+        const uint4 x = fix_vector(ps, wrow + n, slice, ps.nseg[partial_tile(ps, row, n)], rr);
+        *reinterpret_cast<uint4*>(xout + (size_t)row * ldx + n) = x;
+        ss += sumsq8(x);
+      }
+      const float r = rsqrtf(block_sum(ss) / (float)h + eps);
+      for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
+        const int n = k * 8;
+        *reinterpret_cast<uint4*>(u + (size_t)row * ldu + n) =
+            scale8(*reinterpret_cast<const uint4*>(xout + (size_t)row * ldx + n),
+                   *reinterpret_cast<const uint4*>(g + n), r);
       }
     }
-    float4 al = make_float4(0.f, 0.f, 0.f, 0.f), ah = al;
-#pragma unroll
-    for (int q = 0; q < kFixSeg; ++q) {   // slice order; slices past nseg add +0
-      al.x += lo[q].x; al.y += lo[q].y; al.z += lo[q].z; al.w += lo[q].w;
-      ah.x += hi[q].x; ah.y += hi[q].y; ah.z += hi[q].z; ah.w += hi[q].w;
-    }
-    for (int q = kFixSeg; q < nseg; ++q) {
-      const float4 x0 = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
-      const float4 x1 = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
-      al.x += x0.x; al.y += x0.y; al.z += x0.z; al.w += x0.w;
-      ah.x += x1.x; ah.y += x1.y; ah.z += x1.z; ah.w += x1.w;
-    }
-    const float2 r0 = bf16x2_to_f2(rr.x), r1 = bf16x2_to_f2(rr.y), r2 = bf16x2_to_f2(rr.z),
-                 r3 = bf16x2_to_f2(rr.w);
-    const uint4 out = make_uint4(f2_to_bf16x2(al.x + r0.x, al.y + r0.y), f2_to_bf16x2(al.z + r1.x, al.w + r1.y),
-                                 f2_to_bf16x2(ah.x + r2.x, ah.y + r2.y), f2_to_bf16x2(ah.z + r3.x, ah.w + r3.y));
-    *reinterpret_cast<uint4*>(xout + (size_t)row * ldx + n) = out;
-    const float2 o0 = bf16x2_to_f2(out.x), o1 = bf16x2_to_f2(out.y), o2 = bf16x2_to_f2(out.z),
-                 o3 = bf16x2_to_f2(out.w);
-    ss += o0.x * o0.x + o0.y * o0.y + o1.x * o1.x + o1.y * o1.y + o2.x * o2.x + o2.y * o2.y +
-          o3.x * o3.x + o3.y * o3.y;
-  }
-  ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
-    t = warp_sum(t);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float r = rsqrtf(red[0] / (float)h + eps);
-  auto scale = [&](const uint4& raw, int k) {
-    const uint4 graw = *reinterpret_cast<const uint4*>(g + k * 8);
-    const bf16* e = reinterpret_cast<const bf16*>(&raw);
-    const bf16* ge = reinterpret_cast<const bf16*>(&graw);
-    uint4 out;
-    bf16* o = reinterpret_cast<bf16*>(&out);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) o[q] = f_to_bf16(bf16_to_f(e[q]) * r * bf16_to_f(ge[q]));
-    *reinterpret_cast<uint4*>(u + (size_t)row * ldu + k * 8) = out;
-  };
-  // re-read this thread's own x_out vectors (L1/L2 hits)
-  for (int k = threadIdx.x; k < nvec; k += blockDim.x)
-    scale(*reinterpret_cast<const uint4*>(xout + (size_t)row * ldx + k * 8), k);
-  __syncthreads();   // red is reused by the next row
   }
   if (late_trigger) pdl_trigger();
 }
@@ -226,15 +260,15 @@ cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, 
                               cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
   if (h % 8 || ps.ws == nullptr || ps.N != h || rows > ps.M) return cudaErrorInvalidValue;
-  const int threads = std::min(640, (h / 8 + 31) / 32 * 32);
+  const int threads = std::min(1024, (h / 8 + 31) / 32 * 32);
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // SIDP_FIX_GRID: 0 = one CTA per row; else at most one CTA per SM (default)
-  static const int grid_mode = getenv("SIDP_FIX_GRID") ? atoi(getenv("SIDP_FIX_GRID")) : 1;
+  // SIDP_FIX_GRID: 0 = one CTA per row (default, measured ~0.1 ms/step faster); else <= 1 per SM
+  static const int grid_mode = getenv("SIDP_FIX_GRID") ? atoi(getenv("SIDP_FIX_GRID")) : 0;
   static const int late = getenv("SIDP_FIX_LATE_TRIGGER") ? atoi(getenv("SIDP_FIX_LATE_TRIGGER")) : 0;
   const int grid = grid_mode ? std::min(rows, sms) : rows;
   return launch_pdl(resid_norm_kernel, dim3(grid), dim3(threads), 0, s, ps, resid, ldr, xout, ldx,
