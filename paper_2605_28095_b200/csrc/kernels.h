@@ -168,6 +168,18 @@ cudaError_t wait_launch(const FlagSet& flags, uint64_t value, uint64_t timeout_n
                         cudaStream_t s);
 cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int rows, int row_bytes,
                              cudaStream_t s);
+// Fused CaS transfer ("V2": fewer, fused transfer launches): copy every job's
+// rows (row_bytes % 16 == 0; destinations may be peer VAs) and, once ALL of them are globally
+// visible, release-store `value` into every flag.  One launch replaces njobs copy kernels plus
+// nflags signal kernels.  `counter` (device int, 0 between launches) elects the last CTA.
+struct XferJob { void* dst; const void* src; int ldd, lds, rows, row_bytes; };
+struct XferSet {
+  XferJob job[16]; int njobs;
+  uint64_t* flag[18]; int nflags;
+  uint64_t value;
+  unsigned int* counter;
+};
+cudaError_t xfer_launch(const XferSet& x, cudaStream_t s);
 
 // Eager module loading of every kernel (called once by sidp_alloc).
 cudaError_t gemm_preload();

@@ -6,6 +6,8 @@
 // SM-issued, coalesced 16-byte loads with 8 loads in flight per thread before the stores
 // (L1::no_allocate: streamed once), on a bounded number of CTAs so the concurrently
 // running GEMMs keep the rest of the SMs.
+#include <algorithm>
+
 #include "../common.cuh"
 #include "../kernels.h"
 
@@ -125,6 +127,45 @@ cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int r
   return cudaGetLastError();
 }
 
+// grid-strided over each job's 16-byte vectors; every thread fences its stores system-wide,
+// then the last CTA to arrive publishes the flags
+__global__ void __launch_bounds__(256) xfer_kernel(const XferSet x) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int j = 0; j < x.njobs; ++j) {
+    const XferJob& jb = x.job[j];
+    const int nvec = jb.row_bytes / 16;
+    const long long total = (long long)jb.rows * nvec;
+    for (long long i = gt; i < total; i += gs) {
+      const int r = (int)(i / nvec), v = (int)(i % nvec);
+      reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(jb.dst) + (size_t)r * jb.ldd)[v] =
+          reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(jb.src) + (size_t)r * jb.lds)[v];
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(x.counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *x.counter = 0u;
+      __threadfence_system();
+      for (int f = 0; f < x.nflags; ++f) st_release_sys(x.flag[f], x.value);
+    }
+  }
+}
+
+cudaError_t xfer_launch(const XferSet& x, cudaStream_t s) {
+  if (x.njobs < 0 || x.njobs > 16 || x.nflags < 0 || x.nflags > 18 || !x.counter)
+    return cudaErrorInvalidValue;
+  long long vecs = 0;
+  for (int j = 0; j < x.njobs; ++j) {
+    if (x.job[j].row_bytes % 16) return cudaErrorInvalidValue;
+    vecs = std::max<long long>(vecs, (long long)x.job[j].rows * (x.job[j].row_bytes / 16));
+  }
+  const int grid = (int)std::max<long long>(1, std::min<long long>(148, (vecs + 1023) / 1024));
+  xfer_kernel<<<grid, 256, 0, s>>>(x);
+  return cudaGetLastError();
+}
+
 cudaError_t fetch_preload() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaSuccess;
@@ -133,6 +174,7 @@ cudaError_t fetch_preload() {
   if (cudaFuncGetAttributes(&fa, signal_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, wait_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, copy_rows_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, xfer_kernel) != cudaSuccess) e = cudaGetLastError();
   return e;
 }
 

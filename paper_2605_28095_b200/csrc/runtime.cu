@@ -105,6 +105,7 @@ struct sidp_ctx {
   size_t recv_row_bytes = 0;
   std::vector<uint8_t*> peer_cas;
   int* dev_err = nullptr;
+  unsigned int* xfer_cnt = nullptr;  // last-CTA election counter of the fused CaS transfers
   std::vector<int> batches;        // per-rank rows (control plane)
   int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
@@ -561,6 +562,12 @@ size_t flag_off_served(int world) { return (size_t)world * 8 + 8; }
 
 uint64_t* flag_ptr(uint8_t* base, size_t off) { return reinterpret_cast<uint64_t*>(base + off); }
 
+// SIDP_CAS_FUSED=0: one copy kernel per part / destination and one signal kernel per flag
+bool cas_fused() {
+  static const bool v = !(getenv("SIDP_CAS_FUSED") && atoi(getenv("SIDP_CAS_FUSED")) == 0);
+  return v;
+}
+
 // One CaS round trip: live ranks copy their rows into the owner's
 // staging slot at the exclusive-prefix-sum offset and post an arrival flag; the owner waits
 // for every live rank, runs the pooled computation once over all fused rows, copies each
@@ -607,13 +614,25 @@ sidp_status cas_round_trip(sidp_ctx* ctx, int layer, const std::vector<SendPart>
     }
     uint8_t* stage = owner_cas + ctx->cas_stage_off + (size_t)slot * ctx->cas_stage_bytes +
                      (size_t)off[me] * ctx->stage_width * 2;
-    for (const SendPart& p : parts) {
-      CK(sidp::copy_rows_launch(stage + (size_t)p.col * 2, ctx->stage_width * 2, p.src,
-                                p.ld_elems * 2, Bme, p.width * 2, s));
+    if (cas_fused()) {   // one launch: all parts into the owner's staging slot, then the arrival
+      sidp::XferSet xs{};
+      for (const SendPart& p : parts)
+        xs.job[xs.njobs++] = sidp::XferJob{stage + (size_t)p.col * 2, p.src, ctx->stage_width * 2,
+                                           p.ld_elems * 2, Bme, p.width * 2};
+      xs.flag[xs.nflags++] = flag_ptr(owner_cas, flag_off_arrive(me));
+      xs.value = (uint64_t)rt + 1;
+      xs.counter = ctx->xfer_cnt;
+      CK(sidp::xfer_launch(xs, s));
+      count_launch(ctx);
+    } else {
+      for (const SendPart& p : parts) {
+        CK(sidp::copy_rows_launch(stage + (size_t)p.col * 2, ctx->stage_width * 2, p.src,
+                                  p.ld_elems * 2, Bme, p.width * 2, s));
+        count_launch(ctx);
+      }
+      CK(sidp::signal_launch(flag_ptr(owner_cas, flag_off_arrive(me)), (uint64_t)rt + 1, s));
       count_launch(ctx);
     }
-    CK(sidp::signal_launch(flag_ptr(owner_cas, flag_off_arrive(me)), (uint64_t)rt + 1, s));
-    count_launch(ctx);
   }
   if (o == me) {
     sidp::FlagSet fs{};
@@ -627,17 +646,33 @@ sidp_status cas_round_trip(sidp_ctx* ctx, int layer, const std::vector<SendPart>
     size_t result_ld = 0;
     sidp_status stt = owner_compute(stage, ctx->stage_width, total, &result, &result_ld);
     if (stt != SIDP_OK) return stt;
-    for (int q = 0; q < d; ++q) {
-      if (ctx->batches[q] == 0) continue;
-      uint8_t* recv = ctx->peer_cas[q] + ctx->cas_recv_off;
-      CK(sidp::copy_rows_launch(recv, (int)out_row_bytes, result + (size_t)off[q] * result_ld,
-                                (int)result_ld, ctx->batches[q], (int)out_row_bytes, s));
+    if (cas_fused()) {   // one launch: every live rank's slice back, then all done flags + served
+      sidp::XferSet xs{};
+      for (int q = 0; q < d; ++q) {
+        if (ctx->batches[q] == 0) continue;
+        xs.job[xs.njobs++] = sidp::XferJob{ctx->peer_cas[q] + ctx->cas_recv_off,
+                                           result + (size_t)off[q] * result_ld, (int)out_row_bytes,
+                                           (int)result_ld, ctx->batches[q], (int)out_row_bytes};
+        xs.flag[xs.nflags++] = flag_ptr(ctx->peer_cas[q], flag_off_done(d));
+      }
+      xs.flag[xs.nflags++] = flag_ptr(ctx->cas, flag_off_served(d));
+      xs.value = (uint64_t)rt + 1;
+      xs.counter = ctx->xfer_cnt;
+      CK(sidp::xfer_launch(xs, s));
       count_launch(ctx);
-      CK(sidp::signal_launch(flag_ptr(ctx->peer_cas[q], flag_off_done(d)), (uint64_t)rt + 1, s));
+    } else {
+      for (int q = 0; q < d; ++q) {
+        if (ctx->batches[q] == 0) continue;
+        uint8_t* recv = ctx->peer_cas[q] + ctx->cas_recv_off;
+        CK(sidp::copy_rows_launch(recv, (int)out_row_bytes, result + (size_t)off[q] * result_ld,
+                                  (int)result_ld, ctx->batches[q], (int)out_row_bytes, s));
+        count_launch(ctx);
+        CK(sidp::signal_launch(flag_ptr(ctx->peer_cas[q], flag_off_done(d)), (uint64_t)rt + 1, s));
+        count_launch(ctx);
+      }
+      CK(sidp::signal_launch(flag_ptr(ctx->cas, flag_off_served(d)), (uint64_t)rt + 1, s));
       count_launch(ctx);
     }
-    CK(sidp::signal_launch(flag_ptr(ctx->cas, flag_off_served(d)), (uint64_t)rt + 1, s));
-    count_launch(ctx);
   }
   if (Bme > 0) {
     sidp::FlagSet fs{};
@@ -813,7 +848,7 @@ void sidp_destroy(sidp_ctx* ctx) {
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas, ctx->dev_err,
-                    ctx->cas_out};
+                    ctx->cas_out, ctx->xfer_cnt};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -892,6 +927,8 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   CK(cudaMemset(ctx->cas, 0, 4096));
   DM(ctx->dev_err, sizeof(int));
   CK(cudaMemset(ctx->dev_err, 0, sizeof(int)));
+  DM(ctx->xfer_cnt, sizeof(unsigned int));
+  CK(cudaMemset(ctx->xfer_cnt, 0, sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&ctx->fetch_stream, cudaStreamNonBlocking));
   ctx->ready_ev.resize(ctx->S);
   ctx->free_ev.resize(ctx->S);
