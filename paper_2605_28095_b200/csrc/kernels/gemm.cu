@@ -409,16 +409,17 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
 }
 
 // Token-major (SW) epilogue: this thread holds fp32 accumulators of token m, features
-// n0..n0+31 (N is a multiple of 8, so 8-feature groups are all in or all out).
+// n0..n0+31; nlim = min(N, end of this feature tile) (N and the tile width are multiples of 8,
+// so 8-feature groups are all in or all out — columns past the tile belong to the next tile).
 template <int EPI>
-SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0,
+SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0, int nlim,
                         unsigned long long& best) {
   if constexpr (EPI == EPI_F32) {
     float* out = reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo;
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
       const int n = n0 + 4 * g;
-      if (n < p.N) {
+      if (n < nlim) {
         float4 v = make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
                                __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3]));
         if (p.bias) {
@@ -436,7 +437,7 @@ SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0
     for (int g = 0; g < 4; ++g) {   // issue the residual / bias loads first
       const int n = n0 + 8 * g;
       addv[g] = make_uint4(0u, 0u, 0u, 0u);
-      if (n < p.N) {
+      if (n < nlim) {
         if constexpr (EPI == EPI_RESID) addv[g] = *reinterpret_cast<const uint4*>(p.resid + (size_t)m * p.ldr + n);
         else if (p.bias) addv[g] = *reinterpret_cast<const uint4*>(p.bias + n);
       }
@@ -444,7 +445,7 @@ SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       const int n = n0 + 8 * g;
-      if (n < p.N) {
+      if (n < nlim) {
         float y[8], x[8];
         unpack_bf16x8(addv[g], y);
 #pragma unroll
@@ -458,7 +459,7 @@ SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int n = n0 + 16 * h;
-      if (n < p.N) {
+      if (n < nlim) {
         float x[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -471,7 +472,7 @@ SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0
   } else if constexpr (EPI == EPI_ARGMAX) {
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
-      if (n0 + q < p.N) {
+      if (n0 + q < nlim) {
         const unsigned long long k2 = argmax_key(__uint_as_float(r[q]), n0 + q);
         best = k2 > best ? k2 : best;
       }
@@ -676,7 +677,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         ++un;
         const int m = x.ft * 2 * WROWS + rank * WROWS + row;   // this thread's token
         const int fbase = x.mt * BNT;                           // first feature of the tile
-        const int nch = (min(BNT, p.N - fbase) + 31) / 32;
+        const int nlim = min(p.N, fbase + BNT);
+        const int nch = (nlim - fbase + 31) / 32;
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t tl = tmem_base + acc * ACCS + ((uint32_t)(quarter * 32) << 16);
@@ -699,13 +701,13 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
 #pragma unroll
               for (int g = 0; g < 8; ++g) {
                 const int n = n0 + 4 * g;
-                if (n < p.N)
+                if (n < nlim)
                   __stcg(reinterpret_cast<float4*>(dst + n),
                          make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
                                      __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
               }
             } else {
-              store_row<EPI>(p, r, m, n0, best);
+              store_row<EPI>(p, r, m, n0, nlim, best);
             }
           }
         }
@@ -1098,14 +1100,15 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     const int tok_pairs = (a.M + 2 * WROWS - 1) / (2 * WROWS);
     int best = 256;
     double best_c = 1e30;
-    // BNF multiple of 32: with cta_group::2 each CTA supplies BNF/2 B rows, which must be a
-    // multiple of 16 (BNF = 16 or 80 gives wrong results on sm_100a, measured)
-    for (int bnf = 256; bnf >= 32; bnf -= 32) {
+    // BNF multiple of 16 (UMMA N for M = 256); each CTA supplies BNF/2 B rows, whole 8-row
+    // SW128 core-matrix groups.  (BNF = 80 once gave wrong results: the epilogue's last
+    // 32-column chunk stored past the tile end into the next tile; it now stops at nlim.)
+    for (int bnf = 256; bnf >= 32; bnf -= 16) {
       const long long t = (long long)tok_pairs * ((a.N + bnf - 1) / bnf);
       const double c = (double)((t + pair_slots - 1) / pair_slots) * (bnf + env_sw_c0);
       if (c < best_c - 1e-9) { best_c = c; best = bnf; }
     }
-    if (env_sw_bnf >= 32 && env_sw_bnf <= 256 && env_sw_bnf % 32 == 0) best = env_sw_bnf;
+    if (env_sw_bnf >= 32 && env_sw_bnf <= 256 && env_sw_bnf % 16 == 0) best = env_sw_bnf;
     BNT = best;
     m_tiles = (a.N + BNT - 1) / BNT;   // feature tiles (fastest)
     n_pairs = tok_pairs;               // token-pair tiles

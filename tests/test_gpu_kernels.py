@@ -69,7 +69,8 @@ def test_gen_gain_bias_unit_kv_bit_exact(P):
 
 # ------------------------------------------------------------------ tcgen05 GEMM
 SHAPES = [(1, 128, 64), (8, 256, 256), (16, 384, 512), (37, 1000, 320), (100, 640, 1024),
-          (256, 512, 5120), (300, 256, 512), (513, 128, 128), (64, 10240, 5120)]
+          (256, 512, 5120), (300, 256, 512), (513, 128, 128), (64, 10240, 5120),
+          (256, 10240, 5120), (200, 3440, 512)]   # token-major feature tiles of 144 / odd 16s
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
