@@ -277,6 +277,41 @@ def test_big_shapes_sampled_rows(P, name, B, ctx):
     R.ctx.destroy()
 
 
+def test_was_full_width_d8_serve_only_bitwise(P):
+    """WaS at the bench's full per-layer shapes and launch configuration (Qwen3-32B width,
+    B = 256, S_ctx = 1024; 16 layers to fit beside a replicated run): rank 0 of a d = 8 group
+    whose 7 owners are serve-only contexts (as bench.py --emulate-world) fetches 14 full
+    0.975 GB layers per step into 2 slots.  Logits of 2 steps are BITWISE equal to the
+    replicated run (verbatim fetch, same kernels) and the fetch log equals the oracle's FIFO
+    schedule."""
+    m = MODELS["qwen3-32b"].with_layers(16)
+    B, ctx, d, steps = 256, 1024, 8, 2
+    R = Rank(P, m, rank=0, world=d, B=B, ctx=ctx, span=0, max_ctx=ctx + 8, slots=2, fetch_sms=16)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=ctx + 8, seed=SEED, alloc=False)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    R.ctx.import_handles([R.ctx.export_handles()] + [c.export_handles() for c in peers])
+    for s in range(steps):
+        R.step(); R.finish_step()
+    pl = OS.plan(OS.owner_map(m.num_layers, d), d, 0, "exec")
+    log = R.ctx.fetch_log()
+    assert len(log) >= steps * len(pl) == steps * 14
+    assert log == OS.slot_schedule(pl, 2, steps + 1)[:len(log)]
+    for c in peers:
+        c.destroy()
+    rep = Rank(P, m, B=B, ctx=ctx, span=0, max_ctx=ctx + 8)
+    for s in range(steps):
+        rep.step(); rep.finish_step()
+        assert torch.equal(rep.history[s][1], R.history[s][1]), s
+        assert torch.equal(rep.history[s][0], R.history[s][0]), s
+    rep.ctx.destroy()
+    R.ctx.destroy()
+
+
 def test_cuda_graph_replay_matches_eager(P):
     """An all-local step is captured once and replayed as a CUDA graph; the decoded tokens of
     several replays equal an eager run (logits requested => no graph) bit for bit."""
