@@ -54,11 +54,17 @@ def parse():
     ap.add_argument("--emulate-world", type=int, default=8,
                     help="N=1 only: also time rank 0 of a d-rank WaS group on this GPU, the d-1 "
                          "owners being serve-only contexts in local HBM (0 = off)")
-    ap.add_argument("--emulate-fetch-sms", type=int, default=16,
-                    help="fetch CTAs of the emulated rank: 16 read local HBM at ~NVLink 5 rate")
+    ap.add_argument("--emulate-fetch-sms", type=int, default=48,
+                    help="fetch CTAs of the emulated rank (the real-run default, 48)")
+    ap.add_argument("--emulate-pace-gbps", type=float, default=770.0,
+                    help="the emulated rank's fetch kernel paces itself to this rate: the NVLink 5 "
+                         "reader rate (B200_PROFILING.md measured peer copy); 0 = unpaced")
     ap.add_argument("--emulate-batch", type=int, default=None)
     ap.add_argument("--emulate-ctx", type=int, default=None)
     ap.add_argument("--emulate-steps", type=int, default=4)
+    ap.add_argument("--emulate-only", action="store_true",
+                    help="skip the d=1 run (shapes whose weights do not fit one GPU, e.g. M3 "
+                         "Llama-3.1-70B) and print only the WaS emulation line")
     ap.add_argument("--cas-emulate", type=int, default=1,
                     help="N=1 only: time CaS steps of --emulate-world virtual ranks on this GPU "
                          "(small-batch tail, SURVEY.md M5 analogue; 0 = off)")
@@ -250,18 +256,19 @@ def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms):
 def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, peaks):
     """Rank 0 of a W-rank WaS group on ONE GPU (SURVEY.md §8(a) a2-a4 at full size): the W-1
     other owners are serve-only contexts (sidp_alloc_serve_only) whose arenas sit in this GPU's
-    HBM, so the fetch kernel reads local HBM instead of a peer over NVLink.  With
-    --emulate-fetch-sms 16 it reads at ~766 GB/s (profiles/r1_fetch_local.json), the NVLink 5
-    reader rate; HBM traffic equals a real rank's (its slot writes + one owner's serve reads
-    under the stagger).  Not a multi-GPU number: NVLink latency and the other ranks' compute
-    are absent."""
+    HBM, so the fetch kernel reads local HBM instead of a peer over NVLink.  It runs on the real
+    run's 48 CTAs but paces itself (sidp_config.fetch_pace_gbps) to the NVLink 5 reader rate,
+    770 GB/s, which local HBM would otherwise exceed ~4x; HBM traffic equals a real rank's (its
+    slot writes + one owner's serve reads under the stagger).  Not a multi-GPU number: NVLink
+    latency and the other ranks' compute are absent."""
     import numpy as np
     import torch
     max_ctx = kv.max_ctx
     slots = args.slots or wl.slots
     ctx0 = P.Context(m, rank=0, world=W, slots=slots, order=args.order, pool=args.pool,
                      max_batch=kv.max_batch, max_ctx=max_ctx, fetch_sms=args.emulate_fetch_sms,
-                     fetch_engine=args.fetch, stagger=not args.no_stagger, device=local, seed=seed)
+                     fetch_engine=args.fetch, stagger=not args.no_stagger, device=local, seed=seed,
+                     fetch_pace_gbps=args.emulate_pace_gbps)
     peers = []
     try:
         for r in range(1, W):
@@ -313,10 +320,11 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "what": f"rank 0 of a {W}-rank WaS group on one B200; the {W - 1} other owners are "
                     "serve-only contexts in local HBM (bench.py was_emulation docstring)",
             "world_emulated": W, "batch": B, "ctx": ctx_len, "slots": slots,
-            "fetch_sms": args.emulate_fetch_sms, "steps": args.emulate_steps,
+            "fetch_sms": args.emulate_fetch_sms, "fetch_pace_gbps": args.emulate_pace_gbps,
+            "steps": args.emulate_steps,
             "ms_per_step": ms, "tokens_s_rank": B / (ms / 1e3),
             "group_tokens_s_est": W * B / (ms / 1e3),
-            "remote_layers_per_step": remote_layers,
+            "remote_layers_per_step": remote_layers, "layer_bytes": lb,
             "fetch_bytes_per_step": remote_layers * lb,
             "fetch": {"avg_launch_ms": f_ms, "GBps": fetch_gbs,
                       "frac_of_nvlink_770": (fetch_gbs / peaks["nvl"]) if fetch_gbs else None,
@@ -413,6 +421,39 @@ def cas_emulation(args, P, m, seed, local, W, ctx_len):
             c.destroy()
 
 
+def run_emulation_only(args, P, m, wl, local, world):
+    """--emulate-only: the d=W WaS emulation line alone (the d=1 run would not fit)."""
+    import numpy as np
+    import torch
+    from sidp_inputs import gen
+    if world != 1:
+        raise SystemExit("--emulate-only is a single-GPU mode")
+    W = max(2, args.emulate_world)
+    B = args.emulate_batch or args.batch or wl.batch
+    ctx_len = args.emulate_ctx or args.ctx or wl.ctx
+    seed = wl.seed
+    stream = torch.cuda.Stream()
+    kv = P.KVCache(m, B, ctx_len + args.warmup + args.emulate_steps + 8)
+    with torch.cuda.stream(stream):
+        kv.fill_synthetic(seed, 0, B, ctx_len, stream=stream)
+    stream.synchronize()
+    tok = torch.from_numpy(gen.tokens(seed, np.arange(B), m.vocab)).to(torch.int32).cuda()
+    peaks = load_peaks()
+    emu = was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, peaks)
+    fp = emu["footprint_bytes_rank0"]
+    st_d1 = {"owned_bytes": m.num_layers * emu["layer_bytes"], "slot_bytes": 0,
+             "replicated_bytes": fp["replicated"], "workspace_bytes": fp["workspace"]}
+    line = {"metric": METRIC, "emulate_only": True, "unit": UNIT, "n_gpus": 1,
+            "dtype": "bf16", "data": "synthetic: counter-hash bf16 weights and KV (sidp_inputs.gen), seeded",
+            "config": {"workload": f"{wl.id}: {m.name} WaS d={W} single-GPU emulation, B={B}, S_ctx={ctx_len}",
+                       "layers": m.num_layers, "reduced": args.layers is not None},
+            "was_emulation": emu,
+            "kv_capacity": kv_capacity(m, st_d1, fp, W)}
+    line["kv_capacity"]["replicated_d1"]["note"] = ("footprint = all layers + replicated + "
+                                                    "workspaces (the d=1 run is not executed)")
+    print(json.dumps(line), flush=True)
+
+
 def kv_capacity(m, st_d1, fp_dw, W, util=0.9):
     """KV tokens per GPU left by the MEASURED per-GPU footprint of this library (owned weights +
     WaS slots + replicated tensors + workspaces) at a vLLM-style 0.9 memory utilisation: the
@@ -496,6 +537,9 @@ def main():
     B = args.batch or wl.batch
     ctx_len = args.ctx or wl.ctx
     slots = args.slots or wl.slots
+    if args.emulate_only:
+        run_emulation_only(args, P, m, wl, local, world)
+        return
     e2e_steps = 0 if args.no_e2e else args.steps
     max_ctx = ctx_len + args.warmup + args.steps + e2e_steps + 8
     seed = wl.seed

@@ -91,6 +91,10 @@ typedef struct {
   int32_t stagger;              /* 1 => C-S7 start offsets t_r = (-r) mod (d-1) fetch ticks */
   int32_t device;               /* CUDA device ordinal the context lives on */
   uint64_t seed;                /* seed of the synthetic (counter-hash) weights, K12 */
+  float fetch_pace_gbps;        /* > 0: the SM fetch kernel paces itself to at most this rate
+                                   (GB/s).  Only for emulating NVLink with local-HBM owners on
+                                   one GPU (bench.py --emulate-world); 0 on real NVLink, which
+                                   caps the rate by itself. */
 } sidp_config;
 
 /* Caller-owned KV cache of this rank (never pooled).

@@ -33,7 +33,7 @@ class Config(C.Structure):
                 ("was_slots", C.c_int32), ("cas_slots", C.c_int32), ("order", C.c_int32),
                 ("pool_scope", C.c_int32), ("max_batch", C.c_int32), ("max_ctx", C.c_int32),
                 ("fetch_sms", C.c_int32), ("fetch_engine", C.c_int32), ("stagger", C.c_int32),
-                ("device", C.c_int32), ("seed", C.c_uint64)]
+                ("device", C.c_int32), ("seed", C.c_uint64), ("fetch_pace_gbps", C.c_float)]
 
 
 class KV(C.Structure):

@@ -155,7 +155,8 @@ cudaError_t gen_kv_launch(bf16* cache, int B, int nkv, int smax, int hd, int T, 
 
 // ---------------------------------------------------------------- WaS fetch
 // Verbatim copy of one pooled layer, owner HBM (possibly a peer VA) -> local slot.
-cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s);
+cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s,
+                         float pace_gbps = 0.0f);
 cudaError_t delay_launch(uint64_t ns, cudaStream_t s);
 
 // ---------------------------------------------------------------- CaS signalling

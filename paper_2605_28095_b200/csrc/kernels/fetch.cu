@@ -30,11 +30,18 @@ __device__ __forceinline__ void st_na_v4(uint4* p, const uint4& v) {
 
 constexpr int kUnroll = 8;   // 128 B in flight per thread (NVLink peer latency ~2 us)
 
+// ns_per_iter > 0 paces the copy: iteration `it` (kUnroll x grid x 512 x 16 B) starts no
+// earlier than it x ns_per_iter after the CTA's start (NVLink-rate emulation on one GPU).
 __global__ void __launch_bounds__(512) fetch_kernel(uint4* __restrict__ dst,
-                                                    const uint4* __restrict__ src, size_t nvec) {
+                                                    const uint4* __restrict__ src, size_t nvec,
+                                                    uint64_t ns_per_iter) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride) {
+  const uint64_t t0 = ns_per_iter ? globaltimer_ns() : 0;
+  uint64_t it = 0;
+  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride, ++it) {
+    if (ns_per_iter)
+      while (globaltimer_ns() - t0 < it * ns_per_iter) __nanosleep(200);
     uint4 v[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) v[u] = ld_nc_v4(src + i + u * stride);
@@ -86,14 +93,18 @@ __global__ void copy_rows_kernel(uint8_t* dst, int ldd, const uint8_t* src, int 
 
 }  // namespace
 
-cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s) {
+cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s,
+                         float pace_gbps) {
   if (bytes == 0) return cudaSuccess;
   if ((bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) ||
       (reinterpret_cast<uintptr_t>(src) & 15))
     return cudaErrorInvalidValue;
   if (ctas <= 0) ctas = 32;
+  // bytes per iteration of all CTAs / (GB/s == bytes per ns)
+  const uint64_t ns_per_iter =
+      pace_gbps > 0.0f ? (uint64_t)((double)kUnroll * ctas * 512 * 16 / pace_gbps) : 0;
   fetch_kernel<<<ctas, 512, 0, s>>>(reinterpret_cast<uint4*>(dst),
-                                    reinterpret_cast<const uint4*>(src), bytes / 16);
+                                    reinterpret_cast<const uint4*>(src), bytes / 16, ns_per_iter);
   return cudaGetLastError();
 }
 

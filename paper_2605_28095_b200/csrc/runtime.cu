@@ -481,7 +481,7 @@ sidp_status enqueue_fetch(sidp_ctx* ctx) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
   } else {
     CK(sidp::fetch_launch(dst, src, bytes, ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 16,
-                          ctx->fetch_stream));
+                          ctx->fetch_stream, ctx->c.fetch_pace_gbps));
   }
   timing_end(ctx, 3, ctx->fetch_stream);
   count_launch(ctx);
