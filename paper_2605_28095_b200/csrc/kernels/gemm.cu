@@ -51,6 +51,8 @@ struct KParams {
   float* ws;
   int* counters;
   int a3d, b3d;                 // operand map is k-block-major 3-D: one TMA box per stage
+  int dp_tiles;                 // hybrid: tiles [0, dp_tiles) whole, round-robin; stream-K after
+  int compact;                  // stream-K partials in per-cluster tile buffers (see part_tile)
   int partial_all;              // EPI_PARTIAL: every unit writes its fp32 partial slice
   int w_evict;                  // weight TMA loads carry an L2 evict-first policy
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
@@ -154,30 +156,41 @@ __host__ __device__ inline long long range_begin(int c, long long total, int C) 
 
 struct Unit {
   int ft, mt, kb0, kb1, seg, nseg;
+  int slot;   // 0: the unit starts this cluster's stream-K range, 1: it ends it
 };
 
 struct UnitIter {
-  long long g, end;   // stream-K cursor
-  int u;              // whole-tile cursor
+  long long g, g0, end;   // stream-K cursor (k-steps of tiles >= dp_tiles)
+  int u;                  // whole-tile cursor
   SIDP_DEV void init(const KParams& p, int cluster) {
-    g = range_begin(cluster, p.total_kb, p.clusters);
+    g0 = g = range_begin(cluster, p.total_kb, p.clusters);
     end = range_begin(cluster + 1, p.total_kb, p.clusters);
     u = cluster;
   }
   SIDP_DEV bool next(const KParams& p, int cluster, Unit& x) {
     const int nkb = p.nks;   // k-steps per tile
     int t;
-    if (p.streamk) {
+    x.slot = 0;
+    if (p.streamk && u < p.dp_tiles) {   // hybrid: the whole-tile waves first
+      t = u;
+      u += p.clusters;
+      x.kb0 = 0;
+      x.kb1 = nkb;
+      x.seg = 0;
+      x.nseg = 1;
+    } else if (p.streamk) {
       if (g >= end) return false;
-      t = (int)(g / nkb);
-      const long long tile_end = (long long)(t + 1) * nkb;
+      const int tl = (int)(g / nkb);            // tile within the stream-K region
+      const long long tile_end = (long long)(tl + 1) * nkb;
       const long long seg_end = end < tile_end ? end : tile_end;
-      x.kb0 = (int)(g - (long long)t * nkb);
+      x.kb0 = (int)(g - (long long)tl * nkb);
       x.kb1 = x.kb0 + (int)(seg_end - g);
-      const int first = cluster_of_kb((long long)t * nkb, p.total_kb, p.clusters);
+      const int first = cluster_of_kb((long long)tl * nkb, p.total_kb, p.clusters);
       const int last = cluster_of_kb(tile_end - 1, p.total_kb, p.clusters);
       x.seg = cluster - first;
       x.nseg = last - first + 1;
+      x.slot = g == g0 ? 0 : 1;
+      t = p.dp_tiles + tl;
       g = seg_end;
     } else {
       if (u >= p.tiles) return false;
@@ -733,7 +746,10 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const int pt = x.ft * 2 + rank;
         const int mbase = x.mt * BNT;
         const int nchunks = min(BNT, ((p.M - mbase + 31) / 32) * 32) / 32;
-        float* part = p.ws + (size_t)x.seg * p.M * p.N;   // partial slice (nseg > 1 only)
+        // partial of a split tile: a full [M][N] slice per segment, or (compact) this cluster's
+        // tile buffer [BNT tokens][256 features] of its first / last stream-K unit
+        float* part = p.compact ? p.ws + ((size_t)cluster * 2 + x.slot) * (size_t)(2 * WROWS) * BNT
+                                : p.ws + (size_t)x.seg * p.M * p.N;
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t tl = tmem_base + acc * ACCS + ((uint32_t)(quarter * 32) << 16);
@@ -757,9 +773,11 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             for (int i = 0; i < 8; ++i) {
               const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
               const int m = mbase + c * 32 + j, n = n0 + f;
-              if (m < p.M && n < p.N)
-                __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N + n),
-                       *reinterpret_cast<const float4*>(stg + j * SROW + f));
+              if (m < p.M && n < p.N) {
+                float* dst = p.compact ? part + (size_t)(c * 32 + j) * (2 * WROWS) + rank * WROWS + f
+                                       : part + (size_t)m * p.N + n;
+                __stcg(reinterpret_cast<float4*>(dst), *reinterpret_cast<const float4*>(stg + j * SROW + f));
+              }
             }
           }
           named_bar_sync(1, 128);
@@ -796,11 +814,12 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
   const long long nkb = p.nks;
   const int c = blockIdx.y + 1;
   const long long bc = range_begin(c, p.total_kb, p.clusters);
-  const int t = (int)(bc / nkb);
+  const int tl = (int)(bc / nkb);                             // tile within the stream-K region
   if (bc % nkb == 0) return;                                  // boundary on a tile edge
-  if (c > 1 && range_begin(c - 1, p.total_kb, p.clusters) > (long long)t * nkb) return;
-  const int nseg = cluster_of_kb((long long)(t + 1) * nkb - 1, p.total_kb, p.clusters) -
-                   cluster_of_kb((long long)t * nkb, p.total_kb, p.clusters) + 1;
+  if (c > 1 && range_begin(c - 1, p.total_kb, p.clusters) > (long long)tl * nkb) return;
+  const int first = cluster_of_kb((long long)tl * nkb, p.total_kb, p.clusters);
+  const int nseg = cluster_of_kb((long long)(tl + 1) * nkb - 1, p.total_kb, p.clusters) - first + 1;
+  const int t = p.dp_tiles + tl;
   const int mt = t % p.m_tiles, ft = t / p.m_tiles;
   const int m0 = mt * p.BNT, rows = min(p.BNT, p.M - m0);
   const int tile_out = EPI == EPI_SILU_MUL ? 2 * WROWS / 2 : 2 * WROWS;   // outputs per row
@@ -824,13 +843,22 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
     const float* base = p.ws + (size_t)m * p.N;
 #pragma unroll 4
     for (int s = 0; s < nseg; ++s) {
-      const float4 x0 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + na));
-      const float4 x1 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + na + 4));
+      // segment s = cluster first + s: its full slice, or (compact) its tile buffer — slot 0
+      // when its stream-K range starts inside this tile, else 1 (the range ends here)
+      const float* src = base + s * slice;
+      if (p.compact) {
+        const int cs = first + s;
+        const int slot = range_begin(cs, p.total_kb, p.clusters) >= (long long)tl * nkb ? 0 : 1;
+        src = p.ws + ((size_t)cs * 2 + slot) * (size_t)(2 * WROWS) * p.BNT +
+              (size_t)(m - m0) * (2 * WROWS) - (size_t)ft * 2 * WROWS;
+      }
+      const float4 x0 = __ldcg(reinterpret_cast<const float4*>(src + na));
+      const float4 x1 = __ldcg(reinterpret_cast<const float4*>(src + na + 4));
       a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
       a[4] += x1.x; a[5] += x1.y; a[6] += x1.z; a[7] += x1.w;
       if constexpr (EPI == EPI_SILU_MUL) {
-        const float4 y0 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + nb));
-        const float4 y1 = __ldcg(reinterpret_cast<const float4*>(base + s * slice + nb + 4));
+        const float4 y0 = __ldcg(reinterpret_cast<const float4*>(src + nb));
+        const float4 y1 = __ldcg(reinterpret_cast<const float4*>(src + nb + 4));
         b[0] += y0.x; b[1] += y0.y; b[2] += y0.z; b[3] += y0.w;
         b[4] += y1.x; b[5] += y1.y; b[6] += y1.z; b[7] += y1.w;
       }
@@ -1137,6 +1165,31 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     const int max_seg = (int)((nkb + per - 1) / std::max<long long>(per, 1)) + 1;
     if ((size_t)max_seg * a.M * a.N * 4 > w.ws_bytes) streamk = 0;
   }
+  // Hybrid data-parallel + stream-K tail: when whole tiles leave the last wave mostly idle
+  // (e.g. down at M = 1024: 80 tiles on 74 pairs = 1 full wave + 6 tiles that take a whole
+  // wave's time), the full waves stay whole and only the remaining tiles' k-steps are split
+  // over every pair; their partials go to per-cluster tile buffers (compact: 2 per cluster),
+  // summed by gemm_reduce_kernel in cluster order.
+  int dp_tiles = 0, compact = 0;
+  static int env_hybrid = getenv("SIDP_GEMM_HYBRID") ? atoi(getenv("SIDP_GEMM_HYBRID")) : 1;
+  if (!streamk && env_hybrid && !sw && a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.epi != EPI_PARTIAL &&
+      a.k_splits != 1 && tiles > pair_slots) {
+    const int rem = tiles % pair_slots;
+    const int waves = (tiles + pair_slots - 1) / pair_slots;
+    const double eff = (double)tiles / ((double)waves * pair_slots);
+    const size_t need = (size_t)pair_slots * 2 * (2 * WROWS) * BNT * 4;
+    // measured (tools/gemm_bench.py): pays for down at M = 1024 (80 tiles: 282 -> 200 us, the
+    // tail is 6 tiles of 200 k-steps, ~16 per pair); loses when the tail per pair is a few
+    // k-steps (QKV M = 512: 62 -> 67 us, each pair's 256 KB partial costs more than its work) or
+    // when the last wave is mostly full (gate/up M = 256: 200 tiles, 121 -> 126 us; M = 1536
+    // down 301 -> 319 us: split k-ranges of one feature tile no longer share W lines in L2)
+    if (rem != 0 && eff < 0.6 && need <= w.ws_bytes && (long long)rem * nkb >= 12LL * pair_slots) {
+      dp_tiles = tiles - rem;
+      streamk = 1;
+      compact = 1;
+      clusters = pair_slots;
+    }
+  }
   const bool part = a.epi == EPI_PARTIAL;
   if (part) {
     const PartialPlan q = plan_partial(a.M, a.N, a.K, pair_slots);
@@ -1185,7 +1238,8 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   KParams p;
   p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
   p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.tiles = tiles; p.streamk = streamk;
-  p.total_kb = (long long)tiles * nkb; p.clusters = clusters; p.kps = kps; p.nks = nkb;
+  p.total_kb = (long long)(tiles - dp_tiles) * nkb; p.clusters = clusters; p.kps = kps; p.nks = nkb;
+  p.dp_tiles = dp_tiles; p.compact = compact;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
   p.a3d = a3d; p.b3d = b3d;

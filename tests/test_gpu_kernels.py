@@ -136,6 +136,35 @@ def test_gemm_deferred_fixup_resid_norm(P, M, N, K):
     assert torch.equal(r2, xout)
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 5120, 2048), (600, 9728, 4096)])
+def test_gemm_hybrid_streamk_tail(P, M, N, K):
+    """Tile counts just over one wave of the 74 CTA pairs (80, 76 tiles): a whole-tile wave +
+    a stream-K tail whose partials live in per-cluster buffers (gemm_reduce_kernel), for the
+    fp32 (+bias), residual and SiLU*mul epilogues, vs fp64 of the same operands."""
+    g = torch.Generator().manual_seed(M + N)
+    x = _lvl((M, K), g).cuda()
+    w = _lvl((N, K), g, 2.0 ** -6).cuda()
+    bias = _lvl((N,), g, 0.125).cuda()
+    xd, wd = x.cpu().double(), w.cpu().double()
+    out = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    P.test_gemm(x, w, out, M, N, K, 0, bias=bias)
+    r = _lvl((M, N), g).cuda()
+    ref2 = xd @ wd.T + r.cpu().double()
+    P.test_gemm(x, w, r, M, N, K, 2, resid=r)
+    act = torch.full((M, N // 2), float("nan"), dtype=torch.bfloat16, device="cuda")
+    P.test_gemm(x, w, act, M, N, K, 3)   # rows read as interleaved [gate 8 | up 8] groups
+    torch.cuda.synchronize()
+    ref = xd @ wd.T + bias.cpu().double()
+    assert (out.cpu().double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item() + 1e-6
+    d2 = (r.cpu().double() - ref2).abs()
+    assert (d2 <= ref2.abs() * 2.0 ** -8 + 1e-6 * ref2.abs().max()).all()
+    y = (xd @ wd.T).view(M, N // 16, 2, 8)
+    gate, up = y[:, :, 0, :].reshape(M, N // 2), y[:, :, 1, :].reshape(M, N // 2)
+    refs = gate / (1 + torch.exp(-gate)) * up
+    d3 = (act.cpu().double() - refs).abs()
+    assert (d3 <= refs.abs() * 2.0 ** -7 + 1e-4 * refs.abs().max()).all()
+
+
 @pytest.mark.parametrize("M,F,K,splits", [(8, 64, 256, 1), (33, 192, 512, 0), (256, 640, 1024, 4),
                                           (200, 328, 512, -1), (300, 1040, 256, -1), (40, 200, 256, -1)])
 def test_gemm_silu_mul(P, M, F, K, splits):
