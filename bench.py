@@ -69,6 +69,9 @@ def parse():
                     help="N=1 only: time CaS steps of --emulate-world virtual ranks on this GPU "
                          "(small-batch tail, SURVEY.md M5 analogue; 0 = off)")
     ap.add_argument("--cas-ctx", type=int, default=1024)
+    ap.add_argument("--cas-batches", default="1,4,16",
+                    help="all-live per-rank batches of the CaS emulation (B=16 also runs the "
+                         "half-live and one-live dummy patterns)")
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 with a gloo control plane (functional multi-process "
                          "test of the IPC path on a 1-GPU box; not a scaling number)")
@@ -351,7 +354,8 @@ def cas_emulation(args, P, m, seed, local, W, ctx_len):
     import numpy as np
     import torch
     from sidp_inputs import gen
-    Bmax = 16
+    bl = [int(b) for b in str(getattr(args, "cas_batches", "1,4,16")).split(",") if b]
+    Bmax = max(bl + [16])
     steps = max(2, args.emulate_steps)
     max_ctx = ctx_len + 3 + steps * 8 + 8
     ranks = []
@@ -371,9 +375,9 @@ def cas_emulation(args, P, m, seed, local, W, ctx_len):
         for c, _, _, _ in ranks:
             c.import_handles(blobs)
             c.set_mode(1, 0)   # SIDP_CAS from step 0 (collective-consistent: same on all ranks)
-        patterns = [("all live, B=1", [1] * W), ("all live, B=4", [4] * W),
-                    ("all live, B=16", [16] * W), ("half live, B=16", [16] * (W // 2) + [0] * (W - W // 2)),
-                    ("one live, B=16", [16] + [0] * (W - 1))]
+        patterns = [(f"all live, B={b}", [b] * W) for b in bl]
+        patterns += [("half live, B=16", [16] * (W // 2) + [0] * (W - W // 2)),
+                     ("one live, B=16", [16] + [0] * (W - 1))]
         out = []
         common = torch.cuda.Stream()
         xs = [(torch.randn(Bmax, m.hidden, device="cuda") * 0.5).to(torch.bfloat16) for _ in range(W)]

@@ -13,7 +13,9 @@ wl = WORKLOADS["M2"]
 m = MODELS[model or wl.model].with_layers(L)
 class A: pass
 a = A(); a.emulate_steps = 2; a.pool = "layer"
+a.cas_batches = os.environ.get("CAS_BATCHES", "1,4,16")
+ctx = int(os.environ.get("CAS_CTX", "256"))
 torch.cuda.set_device(0)
 t = time.time()
-r = bench.cas_emulation(a, P, m, wl.seed, 0, W, 256)
+r = bench.cas_emulation(a, P, m, wl.seed, 0, W, ctx)
 print(time.time() - t, "s", r, flush=True)
