@@ -192,7 +192,10 @@ void sidp_destroy(sidp_ctx* ctx);
  *  mode SIDP_CAS: collective per layer — every rank of the group calls it for every layer
  *    in order; batch == 0 (dummy) returns after serving peers if this rank owns the layer.
  *  mode SIDP_REPLICATED: world == 1 only.
- * batch > max_batch, layer out of range, or pos out of range => SIDP_EINVAL. */
+ * batch > max_batch, layer out of range, or pos out of range => SIDP_EINVAL.
+ * A CaS flag wait that exceeds the timeout (20 s; SIDP_CAS_TIMEOUT_MS read at sidp_init) writes
+ * a mapped host word: every later call on this context returns SIDP_ETIMEOUT (sticky) and
+ * sidp_stats reports it in `timeouts`. */
 sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t layer,
                               int32_t mode, const sidp_kv* kv, void* stream);
 

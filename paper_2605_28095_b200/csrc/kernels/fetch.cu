@@ -71,7 +71,8 @@ __global__ void wait_kernel(const FlagSet flags, uint64_t value, uint64_t timeou
     const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_sys(flags.p[i]) < value) {
       if (globaltimer_ns() - t0 > timeout_ns) {
-        atomicExch(err, 1);
+        *reinterpret_cast<volatile int*>(err) = 1;   // mapped host word (read without a sync)
+        __threadfence_system();
         break;
       }
       __nanosleep(64);

@@ -104,7 +104,9 @@ struct sidp_ctx {
   int stage_width = 0;             // bf16 elements per staged row
   size_t recv_row_bytes = 0;
   std::vector<uint8_t*> peer_cas;
-  int* dev_err = nullptr;
+  int* dev_err = nullptr;           // device view of host_err (mapped pinned host memory)
+  volatile int* host_err = nullptr; // set by a timed-out flag wait; read without a sync
+  uint64_t cas_timeout_ns = 20ull * 1000 * 1000 * 1000;   // SIDP_CAS_TIMEOUT_MS at sidp_init
   unsigned int* xfer_cnt = nullptr;  // last-CTA election counter of the fused CaS transfers
   std::vector<int> batches;        // per-rank rows (control plane)
   int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
@@ -507,6 +509,11 @@ sidp_status pump(sidp_ctx* ctx) {
 sidp_status check_ready(sidp_ctx* ctx) {
   if (!ctx->allocated) return fail(SIDP_ESTATE, "sidp_alloc not called");
   if (ctx->sticky) return fail(SIDP_ECUDA, "context has a sticky CUDA error");
+  if (ctx->host_err && *ctx->host_err) {   // sticky: a CaS peer did not arrive in time
+    ctx->st.timeouts = *ctx->host_err;
+    return fail(SIDP_ETIMEOUT, "a device-side CaS flag wait timed out (%llu ms)",
+                (unsigned long long)(ctx->cas_timeout_ns / 1000000));
+  }
   return SIDP_OK;
 }
 
@@ -603,7 +610,7 @@ sidp_status cas_round_trip(sidp_ctx* ctx, int layer, const std::vector<SendPart>
             (void*)ctx->peer_cas[o]);
   uint8_t* owner_cas = ctx->peer_cas[o];
   if (!owner_cas) return fail(SIDP_ESTATE, "CaS arena of rank %d not imported", o);
-  const uint64_t tmo = 20ull * 1000 * 1000 * 1000;   // 20 s
+  const uint64_t tmo = ctx->cas_timeout_ns;
   if (Bme > 0) {
     if (prev >= 0) {   // the owner's staging slot must be free of round trip `prev`
       sidp::FlagSet fs{};
@@ -830,6 +837,7 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
   c->mode = SIDP_WAS;
   c->st.mode = c->mode;
   schedule_reset(c);
+  if (const char* t = getenv("SIDP_CAS_TIMEOUT_MS")) c->cas_timeout_ns = (uint64_t)atoll(t) * 1000000ull;
   *out = c;
   return SIDP_OK;
 }
@@ -847,10 +855,11 @@ void sidp_destroy(sidp_ctx* ctx) {
     if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
-                    ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas, ctx->dev_err,
+                    ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
                     ctx->cas_out, ctx->xfer_cnt};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    if (ctx->host_err) cudaFreeHost(const_cast<int*>(ctx->host_err));
   }
   delete ctx;
 }
@@ -925,8 +934,16 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   ctx->cas_bytes = ctx->cas_recv_off + (size_t)ctx->c.max_batch * ctx->recv_row_bytes;
   DM(ctx->cas, ctx->cas_bytes);
   CK(cudaMemset(ctx->cas, 0, 4096));
-  DM(ctx->dev_err, sizeof(int));
-  CK(cudaMemset(ctx->dev_err, 0, sizeof(int)));
+  {   // the timeout word lives in mapped pinned host memory: the host reads it at the next
+      // call without synchronising (SIDP_ETIMEOUT)
+    void* hp = nullptr;
+    CK(cudaHostAlloc(&hp, sizeof(int), cudaHostAllocMapped));
+    ctx->host_err = reinterpret_cast<volatile int*>(hp);
+    *ctx->host_err = 0;
+    void* dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, hp, 0));
+    ctx->dev_err = reinterpret_cast<int*>(dp);
+  }
   DM(ctx->xfer_cnt, sizeof(unsigned int));
   CK(cudaMemset(ctx->xfer_cnt, 0, sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&ctx->fetch_stream, cudaStreamNonBlocking));
@@ -1392,9 +1409,7 @@ sidp_status sidp_stats(const sidp_ctx* ctx_c, sidp_stats_t* out) {
   if (!ctx_c || !out) return fail(SIDP_EINVAL, "null argument");
   sidp_ctx* ctx = const_cast<sidp_ctx*>(ctx_c);
   if (ctx->allocated) {
-    int err = 0;
-    if (cudaMemcpy(&err, ctx->dev_err, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && err)
-      ctx->st.timeouts = err;
+    if (ctx->host_err && *ctx->host_err) ctx->st.timeouts = *ctx->host_err;
     if (ctx->tev_used > 0) timing_flush(ctx);
   }
   for (int i = 0; i < 8; ++i) ctx->st.timed_ms[i] = ctx->timed_acc_ms[i];

@@ -79,3 +79,25 @@ def test_controller_driven_switch(P):
     for R in ranks:
         assert R.ctx.stats()["timeouts"] == 0
         R.ctx.destroy()
+
+
+def test_cas_peer_timeout_surfaces_etimeout(P, monkeypatch):
+    """A CaS peer that never arrives: the owner's device-side flag wait gives up after
+    SIDP_CAS_TIMEOUT_MS, writes the mapped host error word, and every later call on that
+    context returns SIDP_ETIMEOUT (sidp.h); sidp_stats counts it."""
+    monkeypatch.setenv("SIDP_CAS_TIMEOUT_MS", "200")
+    m = MODELS["tiny"].with_layers(2)
+    ranks = _group(P, m, 2, [2, 2])
+    for R in ranks:
+        R.ctx.set_batches([2, 2])
+        R.ctx.set_mode(1, 0)
+    R = ranks[0]
+    x = torch.zeros(2, m.hidden, dtype=torch.bfloat16, device="cuda")
+    R.ctx.decode_layer(x, 0, 1, R.kv, batch=2, stream=R.stream)   # rank 1 never calls
+    R.stream.synchronize()
+    with pytest.raises(P.SidpError) as e:
+        R.ctx.decode_layer(x, 1, 1, R.kv, batch=2, stream=R.stream)
+    assert e.value.status == -6
+    assert R.ctx.stats()["timeouts"] >= 1
+    for Q in ranks:
+        Q.ctx.destroy()
