@@ -158,6 +158,8 @@ cudaError_t gen_kv_launch(bf16* cache, int B, int nkv, int smax, int hd, int T, 
 cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s,
                          float pace_gbps = 0.0f);
 cudaError_t delay_launch(uint64_t ns, cudaStream_t s);
+// copy-engine fetch pacing: first != 0 stamps *t0; else waits until *t0 + offset_ns
+cudaError_t pace_launch(unsigned long long* t0, int first, uint64_t offset_ns, cudaStream_t s);
 
 // ---------------------------------------------------------------- CaS signalling
 struct FlagSet {

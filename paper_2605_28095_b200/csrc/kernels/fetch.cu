@@ -51,6 +51,17 @@ __global__ void __launch_bounds__(512) fetch_kernel(uint4* __restrict__ dst,
   for (; i < nvec; i += stride) st_na_v4(dst + i, ld_nc_v4(src + i));
 }
 
+// Pacing of a copy-engine fetch (NVLink-rate emulation): chunk 0 stamps the start time,
+// chunk i waits until offset_ns after it.
+__global__ void pace_kernel(unsigned long long* t0, int first, uint64_t offset_ns) {
+  if (first) {
+    *reinterpret_cast<volatile unsigned long long*>(t0) = globaltimer_ns();
+    return;
+  }
+  const unsigned long long start = *reinterpret_cast<volatile unsigned long long*>(t0);
+  while (globaltimer_ns() - start < offset_ns) __nanosleep(500);
+}
+
 __global__ void delay_kernel(uint64_t ns) {
   const uint64_t t0 = globaltimer_ns();
   while (globaltimer_ns() - t0 < ns) {
@@ -106,6 +117,11 @@ cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cud
       pace_gbps > 0.0f ? (uint64_t)((double)kUnroll * ctas * 512 * 16 / pace_gbps) : 0;
   fetch_kernel<<<ctas, 512, 0, s>>>(reinterpret_cast<uint4*>(dst),
                                     reinterpret_cast<const uint4*>(src), bytes / 16, ns_per_iter);
+  return cudaGetLastError();
+}
+
+cudaError_t pace_launch(unsigned long long* t0, int first, uint64_t offset_ns, cudaStream_t s) {
+  pace_kernel<<<1, 32, 0, s>>>(t0, first, offset_ns);
   return cudaGetLastError();
 }
 
@@ -183,6 +199,7 @@ cudaError_t fetch_preload() {
   cudaError_t e = cudaSuccess;
   if (cudaFuncGetAttributes(&fa, fetch_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, delay_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, pace_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, signal_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, wait_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, copy_rows_kernel) != cudaSuccess) e = cudaGetLastError();

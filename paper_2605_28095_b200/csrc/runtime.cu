@@ -108,6 +108,7 @@ struct sidp_ctx {
   volatile int* host_err = nullptr; // set by a timed-out flag wait; read without a sync
   uint64_t cas_timeout_ns = 20ull * 1000 * 1000 * 1000;   // SIDP_CAS_TIMEOUT_MS at sidp_init
   unsigned int* xfer_cnt = nullptr;  // last-CTA election counter of the fused CaS transfers
+  unsigned long long* pace_t0 = nullptr;   // start stamp of a paced copy-engine fetch
   std::vector<int> batches;        // per-rank rows (control plane)
   int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
@@ -479,7 +480,17 @@ sidp_status enqueue_fetch(sidp_ctx* ctx) {
   bf16* dst = ctx->slots + (size_t)s * ctx->pooled_elems;
   const size_t bytes = ctx->pooled_elems * 2;
   timing_begin(ctx, 3, ctx->fetch_stream);
-  if (ctx->c.fetch_engine == SIDP_FETCH_CE) {
+  if (ctx->c.fetch_engine == SIDP_FETCH_CE && ctx->c.fetch_pace_gbps > 0.0f) {
+    // emulation only: 16 MB copy-engine chunks released at the paced rate
+    const size_t chunk = (size_t)16 << 20;
+    for (size_t off = 0, i = 0; off < bytes; off += chunk, ++i) {
+      CK(sidp::pace_launch(ctx->pace_t0, i == 0, (uint64_t)((double)off / ctx->c.fetch_pace_gbps),
+                           ctx->fetch_stream));
+      CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + off,
+                         reinterpret_cast<const uint8_t*>(src) + off, std::min(chunk, bytes - off),
+                         cudaMemcpyDefault, ctx->fetch_stream));
+    }
+  } else if (ctx->c.fetch_engine == SIDP_FETCH_CE) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
   } else {
     CK(sidp::fetch_launch(dst, src, bytes, ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 16,
@@ -856,7 +867,7 @@ void sidp_destroy(sidp_ctx* ctx) {
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
-                    ctx->cas_out, ctx->xfer_cnt};
+                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (ctx->host_err) cudaFreeHost(const_cast<int*>(ctx->host_err));
@@ -944,6 +955,7 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
     CK(cudaHostGetDevicePointer(&dp, hp, 0));
     ctx->dev_err = reinterpret_cast<int*>(dp);
   }
+  DM(ctx->pace_t0, sizeof(unsigned long long));
   DM(ctx->xfer_cnt, sizeof(unsigned int));
   CK(cudaMemset(ctx->xfer_cnt, 0, sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&ctx->fetch_stream, cudaStreamNonBlocking));
