@@ -395,20 +395,24 @@ def cas_emulation(args, P, m, seed, local, W, ctx_len):
                 e0.record(common)
                 for r, (c, st, kv, tok) in enumerate(ranks):
                     st.wait_event(e0)
+                h0 = time.perf_counter()
                 for _ in range(n):
                     for layer in range(m.num_layers):
                         for r, (c, st, kv, tok) in enumerate(ranks):
                             c.decode_layer(xs[r], layer, 1, kv, batch=bt[r], stream=st)
+                host_ms[0] = (time.perf_counter() - h0) * 1e3 / n
                 for r, (c, st, kv, tok) in enumerate(ranks):
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(st)
                     evs.append(e1)
                 torch.cuda.synchronize()
                 return max(e0.elapsed_time(e) for e in evs) / n
+            host_ms = [0.0]
             run(2)   # warm-up
             ms = run(steps)
             live = sum(1 for b in bt if b)
             out.append({"pattern": name, "batches": bt, "ms_per_layer_stack": ms,
+                        "host_enqueue_ms": host_ms[0],
                         "ms_per_layer": ms / m.num_layers,
                         "group_tokens_s": sum(bt) / (ms / 1e3),
                         "tokens_s_per_live_rank": (sum(bt) / max(1, live)) / (ms / 1e3)})
