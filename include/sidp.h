@@ -264,6 +264,15 @@ sidp_status sidp_test_gemm_resid_norm(const void* x, int32_t ldx, const void* w,
                                       int32_t N, int32_t K, const void* resid, int32_t ldr,
                                       const void* g, float eps, void* xout, void* u, void* stream);
 
+/* Test hook for the fused gate/up -> down launch (SURVEY.md a10 + a11 + next a5): act =
+ * SiLU(u Wg^T) * (u Wu^T) (wgu [2I][h], gate/up rows interleaved in 16-row groups), then the down
+ * projection's partial slices summed by resid_norm: xout = bf16(resid + act Wd^T) (wd [h][I]) and
+ * unorm = RMSNorm(xout) * g.  u, resid, xout, unorm [M][h], act [M][I], all contiguous bf16.
+ * SIDP_EINVAL (nothing enqueued) if M > 256, h % 256 or I % 128.  Device pointers. */
+sidp_status sidp_test_mlp_fused(const void* u, const void* wgu, const void* wd, const void* resid,
+                                int32_t M, int32_t h, int32_t I, const void* g, float eps,
+                                void* act, void* xout, void* unorm, void* stream);
+
 /* K12 on an arbitrary buffer: dst[r*ld + c] = value(seed, tensor, layer, (row0+r)*lcols + c)
  * with kind 0 weight (scale from scale_k), 1 gain, 2 bias, 3 unit; row_map 1 = packed
  * gate/up interleave. */

@@ -223,6 +223,14 @@ def test_gemm_resid_norm(x, w, resid, g, eps, xout, u, stream=None):
                                               _stream_ptr(stream)), "sidp_test_gemm_resid_norm")
 
 
+def test_mlp_fused(u, wgu, wd, resid, g, eps, act, xout, unorm, stream=None):
+    M, h = u.shape
+    I = wd.shape[1]
+    A.check(A.lib().sidp_test_mlp_fused(_ptr(u), _ptr(wgu), _ptr(wd), _ptr(resid), M, h, I, _ptr(g),
+                                        eps, _ptr(act), _ptr(xout), _ptr(unorm), _stream_ptr(stream)),
+            "sidp_test_mlp_fused")
+
+
 def test_gen(dst, seed, tensor, layer, kind, scale_k=0, row0=0, lcols=None, row_map=0, stream=None):
     rows, cols = dst.shape
     A.check(A.lib().sidp_test_gen(_ptr(dst), dst.stride(0), rows, cols, seed, tensor, layer, kind,

@@ -92,6 +92,22 @@ int gemm_pick_splits(int tiles, int nkb, int sms);
 bool gemm_partial_ok(int M, int N, int K, size_t ws_bytes);
 int gemm_last_launch_count();   // kernels enqueued by the last gemm_launch on this thread
 
+// Fused gate/up -> down (SURVEY.md a10 + a11) in one persistent tcgen05 launch: gate/up tiles
+// (SiLU*mul -> act) and down k-range units (fp32 partial slices, summed by resid_norm in slice
+// order) in host-scheduled per-pair lists; a down unit's act k-block is loaded once the gate/up
+// tile producing it is stored (device tile counters in GemmWorkspace.counters).
+struct MlpArgs {
+  const bf16* u; int ldu;        // [M][h] gate/up input
+  const bf16* wgu;               // [2I][h], gate/up rows interleaved in 16-row groups
+  const bf16* wd;                // [h][I]
+  bf16* act; int ldact;          // [M][I] SiLU(gate) * up
+  int M, h, I;
+  PartialSrc* partial_out;       // down partial slices for resid_norm
+};
+bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters);
+void mlp_prepare(int h, int I, size_t ws_bytes);   // builds the schedule (call before capture)
+cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t s);
+
 // ---------------------------------------------------------------- element-wise / small kernels
 cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf16* y, int ldy,
                            int rows, int h, cudaStream_t s);

@@ -19,6 +19,8 @@
 //    split of a tile half sums the partials in split order 0..S-1 (deterministic) and runs the
 //    epilogue.
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -896,6 +898,252 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
   }
 }
 
+// ---------------------------------------------------------------- fused MLP (gate/up -> down)
+// One persistent launch runs the layer's gate/up GEMM (whole 256-feature tiles, SiLU*mul epilogue
+// -> act) and its down GEMM (k-range units, fp32 partial slices summed later by resid_norm).
+// Down k-step k reads act features [128k, 128k+128), produced by gate/up tile k: the TMA
+// producer waits on that tile's completion counter (both CTAs of its pair add 1 after their
+// stores) before loading the act k-block, so down work fills the CTA pairs that the last,
+// partial gate/up wave leaves idle (200 tiles on 74 pairs: 22 pairs idle for a whole tile
+// time) instead of waiting for a kernel boundary.  The unit lists are host-built by list
+// scheduling (mlp_schedule).  All co-dependent CTAs are of this grid, which depends on nothing
+// launched after it: the PDL trigger is issued at exit, so no successor can take SM resources
+// from a not-yet-resident CTA of this grid.
+struct MlpParams {
+  int M, N1, K1, N2, K2;         // gate/up [N1 = 2I][K1 = h]; down [N2 = h][K2 = I]
+  int BNT, stages;
+  const int4* units;             // {phase | seg << 8, tile, kb0, kb1}; cluster c: [uoff[c], uoff[c+1])
+  const int* uoff;
+  bf16* act; int ldact;          // [M][I]
+  float* ws;                     // down partials [seg][M][N2]
+  int* flags;                    // [N1 / 256] gate/up tile completion counters (0 between launches)
+  unsigned int* done;            // CTA exit counter (the last CTA resets the flags)
+  int n_flags;
+};
+
+SIDP_DEV int ld_acquire_gpu_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ CUtensorMap tm_x1,
+            const __grid_constant__ CUtensorMap tm_w2, const __grid_constant__ CUtensorMap tm_x2,
+            const MlpParams p) {
+  constexpr int KPS = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int stages = p.stages, BNT = p.BNT, HALF = p.BNT / 2;
+  const uint32_t a_sub = WROWS * BK * 2, b_sub = (uint32_t)HALF * BK * 2;
+  const uint32_t a_bytes = KPS * a_sub, b_bytes = KPS * b_sub;
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + (size_t)stages * a_bytes;
+  float* stg = reinterpret_cast<float*>(sB + (size_t)stages * b_bytes);   // [32][SROW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + 32 * SROW);
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;                      // [2]
+  uint64_t* tempty = tfull + 2;                          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int ACCS = (BNT + 31) / 32 * 32;
+  const uint32_t tmem_cols = ACCS <= 32 ? 64 : (ACCS <= 64 ? 128 : (ACCS <= 128 ? 256 : 512));
+  const int u0 = p.uoff[cluster], u1 = p.uoff[cluster + 1];
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm_w1);
+    tma_prefetch_desc(&tm_x1);
+    tma_prefetch_desc(&tm_w2);
+    tma_prefetch_desc(&tm_x2);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x != 0) pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t stage_tx = 2 * (a_bytes + b_bytes);
+      const uint64_t wpol = policy_evict_first();
+      auto issue = [&](const int4 un, int kb, int s, bool pre) {
+        const int phase = un.x & 0xff;
+        const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
+        const CUtensorMap* tw = phase ? &tm_w2 : &tm_w1;
+        const CUtensorMap* tx = phase ? &tm_x2 : &tm_x1;
+        const int arow = un.y * 2 * WROWS + rank * WROWS;
+#pragma unroll
+        for (int j = 0; j < KPS; ++j)
+          tma_load_2d_2sm_hint(tw, lbar, sA + (size_t)s * a_bytes + j * a_sub, (kb * KPS + j) * BK, arow, wpol);
+        if (pre) return;
+        if (phase) {   // act k-block kb is gate/up tile kb's output: wait until both CTAs stored it
+          while (ld_acquire_gpu_s32(p.flags + kb) < 2) __nanosleep(64);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+#pragma unroll
+        for (int j = 0; j < KPS; ++j)
+          tma_load_2d_2sm(tx, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, rank * HALF);
+      };
+      // the first stages' weight tiles before griddepcontrol.wait (weights are resident)
+      int npre = 0;
+      {
+        int ui = u0, kb = ui < u1 ? p.units[ui].z : 0;
+        for (; npre < stages && ui < u1; ++npre) {
+          if (leader) mbar_arrive_expect_tx(&full[npre], stage_tx);
+          issue(p.units[ui], kb, npre, true);
+          if (++kb >= p.units[ui].w && ++ui < u1) kb = p.units[ui].z;
+        }
+      }
+      pdl_wait();
+      int it = 0;
+      for (int ui = u0; ui < u1; ++ui) {
+        const int4 un = p.units[ui];
+        for (int kb = un.z; kb < un.w; ++kb, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          if (it >= npre) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (leader) mbar_arrive_expect_tx(&full[s], stage_tx);
+            issue(un, kb, s, false);
+          } else {   // weight half already in flight: the activation half now
+            const int phase = un.x & 0xff;
+            const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
+            const CUtensorMap* tx = phase ? &tm_x2 : &tm_x1;
+            if (phase) {
+              while (ld_acquire_gpu_s32(p.flags + kb) < 2) __nanosleep(64);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+#pragma unroll
+            for (int j = 0; j < KPS; ++j)
+              tma_load_2d_2sm(tx, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, rank * HALF);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      const uint32_t idesc = umma_idesc_bf16(2 * WROWS, BNT);
+      int it = 0, un_i = 0;
+      for (int ui = u0; ui < u1; ++ui, ++un_i) {
+        const int4 un = p.units[ui];
+        const int acc = un_i & 1;
+        const uint32_t aph = (un_i >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * ACCS;
+        for (int kb = un.z; kb < un.w; ++kb, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (it / stages) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sA + (size_t)s * a_bytes);
+            const uint32_t b0 = smem_u32(sB + (size_t)s * b_bytes);
+#pragma unroll
+            for (int j = 0; j < KPS; ++j) {
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                umma2_bf16(dcol, umma_desc_sw128(a0 + j * a_sub + k * 32),
+                           umma_desc_sw128(b0 + j * b_sub + k * 32), idesc,
+                           (kb > un.z || j > 0 || k > 0) ? 1u : 0u);
+            }
+            umma2_commit_mc(&empty[s]);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) umma2_commit_mc(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int tid = (warp - 2) * 32 + lane;
+    KParams kp{};   // the SiLU*mul store of store_phase
+    kp.M = p.M; kp.N = p.N1; kp.out = p.act; kp.ldo = p.ldact;
+    const int nchunks = min(BNT, ((p.M + 31) / 32) * 32) / 32;
+    int un_i = 0;
+    for (int ui = u0; ui < u1; ++ui, ++un_i) {
+      const int4 un = p.units[ui];
+      const int phase = un.x & 0xff, seg = un.x >> 8;
+      const int acc = un_i & 1;
+      const uint32_t aph = (un_i >> 1) & 1;
+      const int n0 = un.y * 2 * WROWS + rank * WROWS;
+      const int pt = un.y * 2 + rank;
+      float* part = p.ws + (size_t)seg * p.M * p.N2;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t tl = tmem_base + acc * ACCS + ((uint32_t)(quarter * 32) << 16);
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tl + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg[j * SROW + row] = __uint_as_float(r[j]);
+        if (c == nchunks - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        }
+        named_bar_sync(1, 128);
+        if (phase == 0) {
+          store_phase<EPI_SILU_MUL>(kp, stg, c * 32, n0, pt, tid);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
+            const int m = c * 32 + j, n = n0 + f;
+            if (m < p.M && n < p.N2)
+              __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N2 + n),
+                     *reinterpret_cast<const float4*>(stg + j * SROW + f));
+          }
+        }
+        named_bar_sync(1, 128);
+      }
+      if (phase == 0) {   // this CTA's half of gate/up tile un.y is stored: publish it
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (tid == 0) atomicAdd(p.flags + un.y, 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, tmem_cols);
+  }
+  if (threadIdx.x == 0) {   // the last CTA out resets the tile counters for the next launch
+    __threadfence();
+    if (atomicAdd(p.done, 1u) == gridDim.x - 1) {
+      for (int i = 0; i < p.n_flags; ++i) p.flags[i] = 0;
+      *p.done = 0u;
+      __threadfence();
+    }
+  }
+  pdl_trigger();
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1320,6 +1568,138 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   return e1;
 }
 
+// ---- fused MLP host side ------------------------------------------------------------
+namespace {
+struct MlpSched {
+  int4* d_units = nullptr;
+  int* d_uoff = nullptr;
+  std::vector<int> nseg;   // per down tile
+  int max_seg = 0;
+};
+struct MlpKey {
+  int M, h, I, C;
+  bool operator<(const MlpKey& o) const {
+    return std::tie(M, h, I, C) < std::tie(o.M, o.h, o.I, o.C);
+  }
+};
+
+// List scheduling of the two GEMMs' units over C CTA pairs with unit cost = k-steps: gate/up
+// tiles round-robin (whole tiles, the SiLU epilogue needs complete sums); then the down tiles'
+// k-range chunks in k-major order, each to the earliest-free pair, starting no earlier than the
+// gate/up tile producing its first act k-block (a down k-step k depends on gate/up tile k).
+MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
+  MlpSched sc;
+  std::vector<std::vector<int4>> lists(C);
+  std::vector<double> F(C, 0.0), done(G, 0.0);
+  for (int g = 0; g < G; ++g) {
+    const int c = g % C;
+    lists[c].push_back(make_int4(0, g, 0, nks1));
+    F[c] += nks1;
+    done[g] = F[c];
+  }
+  const int nch = std::max(1, std::min(max_seg, nks2));
+  const int q = (nks2 + nch - 1) / nch;
+  sc.nseg.assign(D, 0);
+  for (int k0 = 0; k0 < nks2; k0 += q) {
+    const int k1 = std::min(nks2, k0 + q);
+    for (int t = 0; t < D; ++t) {
+      int c = 0;
+      for (int i = 1; i < C; ++i)
+        if (F[i] < F[c]) c = i;
+      const double start = std::max(F[c], done[k0]);
+      F[c] = std::max(start + (k1 - k0), done[k1 - 1] + 1.0);
+      lists[c].push_back(make_int4(1 | (sc.nseg[t] << 8), t, k0, k1));
+      sc.nseg[t]++;
+    }
+  }
+  for (int t = 0; t < D; ++t) sc.max_seg = std::max(sc.max_seg, sc.nseg[t]);
+  std::vector<int4> flat;
+  std::vector<int> off(1, 0);
+  for (int c = 0; c < C; ++c) {
+    flat.insert(flat.end(), lists[c].begin(), lists[c].end());
+    off.push_back((int)flat.size());
+  }
+  cudaMalloc(&sc.d_units, flat.size() * sizeof(int4));
+  cudaMalloc(&sc.d_uoff, off.size() * sizeof(int));
+  cudaMemcpy(sc.d_units, flat.data(), flat.size() * sizeof(int4), cudaMemcpyHostToDevice);
+  cudaMemcpy(sc.d_uoff, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice);
+  return sc;
+}
+}  // namespace
+
+// The schedule depends on the shapes, not on M (segments are sized for M <= 256): built once
+// per (h, I) — mlp_prepare runs it at allocation time, outside any CUDA-graph capture.
+const MlpSched* mlp_sched(int h, int I, size_t ws_bytes) {
+  static std::map<MlpKey, MlpSched> cache;
+  const int C = std::max(1, num_sms() / 2);
+  const int max_seg = (int)std::min<size_t>(8, ws_bytes / ((size_t)256 * h * 4));
+  const MlpKey key{max_seg, h, I, C};
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    it = cache.emplace(key, build_mlp_sched(I / 128, h / (BK * 2), (h + 255) / 256, I / (BK * 2), C,
+                                            max_seg)).first;
+  }
+  return &it->second;
+}
+
+void mlp_prepare(int h, int I, size_t ws_bytes) {
+  if (h > 0 && I > 0 && h % 256 == 0 && I % 128 == 0) mlp_sched(h, I, ws_bytes);
+}
+
+bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters) {
+  static int env = getenv("SIDP_MLP_FUSED") ? atoi(getenv("SIDP_MLP_FUSED")) : 1;
+  if (!env || M <= 0 || M > 256 || h % 256 || I % 128 || h % BK || I % BK) return false;
+  const int G = I / 128;                 // gate/up pair tiles = act k-steps of the down GEMM
+  if (n_counters < G + 1) return false;
+  return (size_t)2 * 256 * h * 4 <= ws_bytes;   // at least 2 down segments of M <= 256 rows fit
+}
+
+cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t stream) {
+  g_last_launches = 0;
+  if (!mlp_fused_ok(a.M, a.h, a.I, w.ws_bytes, w.n_counters)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    attr = true;
+    num_sms();
+    cudaFuncSetAttribute(mlp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
+  }
+  const int C = std::max(1, g_num_sms / 2);
+  const int G = a.I / 128, nks1 = a.h / (BK * 2), D = (a.h + 255) / 256, nks2 = a.I / (BK * 2);
+  const int BNT = std::max(32, ((a.M + 31) / 32) * 32);
+  const MlpSched* scp = mlp_sched(a.h, a.I, w.ws_bytes);
+  if (!scp || !scp->d_units) return cudaErrorMemoryAllocation;
+  const MlpSched& sc = *scp;
+  CUtensorMap tw1, tx1, tw2, tx2;
+  if (!make_tmap_2d(&tw1, a.wgu, a.h, 2 * (uint64_t)a.I, a.h, BK, WROWS) ||
+      !make_tmap_2d(&tx1, a.u, a.h, a.M, a.ldu, BK, BNT / 2) ||
+      !make_tmap_2d(&tw2, a.wd, a.I, a.h, a.I, BK, WROWS) ||
+      !make_tmap_2d(&tx2, a.act, a.I, a.M, a.ldact, BK, BNT / 2))
+    return cudaErrorInvalidValue;
+  MlpParams p{};
+  p.M = a.M; p.N1 = 2 * a.I; p.K1 = a.h; p.N2 = a.h; p.K2 = a.I;
+  p.BNT = BNT;
+  const size_t stage_bytes = 2 * ((size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2);
+  const size_t extra = 32 * SROW * 4 + 512;
+  static int env_stages = getenv("SIDP_GEMM_STAGES") ? atoi(getenv("SIDP_GEMM_STAGES")) : 12;
+  p.stages = std::max(2, (int)std::min<size_t>(env_stages, (kSmemBudget - extra) / stage_bytes));
+  p.units = sc.d_units; p.uoff = sc.d_uoff;
+  p.act = a.act; p.ldact = a.ldact; p.ws = w.ws;
+  p.flags = w.counters; p.done = reinterpret_cast<unsigned int*>(w.counters + G); p.n_flags = G;
+  const size_t smem = p.stages * stage_bytes + extra + 1024;
+  cudaError_t e = launch_pdl(mlp2_kernel, dim3(2 * C), dim3(kThreads), smem, stream, tw1, tx1, tw2, tx2, p);
+  if (e != cudaSuccess) return e;
+  g_last_launches = 1;
+  if (a.partial_out) {
+    PartialSrc& o = *a.partial_out;
+    o = PartialSrc{};
+    o.ws = w.ws; o.M = a.M; o.N = a.h; o.sw = 0;
+    o.tile_m = BNT; o.tile_f = 2 * WROWS; o.m_tiles = 1; o.f_tiles = D;
+    if (D > kPartialMaxTiles) return cudaErrorInvalidValue;
+    for (int t = 0; t < D; ++t) o.nseg[t] = (unsigned char)sc.nseg[t];
+  }
+  return cudaSuccess;
+}
+
 // Force-load every kernel of this file (CUDA lazy loading would otherwise load a module on
 // first launch, which waits for the device to idle — a deadlock while another virtual rank's
 // flag-wait kernel spins; see runtime sidp_alloc).
@@ -1340,7 +1720,8 @@ cudaError_t gemm_preload() {
   SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2, false>))
   SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 2, false>))
   SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 2, true>))
-    SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
+    SIDP_PRELOAD((mlp2_kernel))
+  SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
   SIDP_PRELOAD((gemm_reduce_kernel<EPI_RESID>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_SILU_MUL>))
 #undef SIDP_PRELOAD
   return e;

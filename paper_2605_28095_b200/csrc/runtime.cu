@@ -435,6 +435,22 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
     CK(sidp::rmsnorm_launch(out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
   }
+  if (next_g && sidp::mlp_fused_ok(B, h, m.intermediate, ctx->gemm_ws_bytes, ctx->n_counters)) {
+    // gate/up and down in one persistent launch (down units start on the CTA pairs the last
+    // gate/up wave leaves idle), then the deferred fix-up with the next layer's RMSNorm
+    sidp::MlpArgs ma{};
+    ma.u = ctx->u; ma.ldu = h; ma.wgu = W.wgu; ma.wd = W.wd; ma.act = ctx->act;
+    ma.ldact = m.intermediate; ma.M = B; ma.h = h; ma.I = m.intermediate; ma.partial_out = &part;
+    timing_begin(ctx, 1, s);
+    cudaError_t e = sidp::mlp_launch(ma, gws(ctx), s);
+    timing_end(ctx, 1, s);
+    CK(e);
+    count_launch(ctx);
+    CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s));
+    count_launch(ctx);
+    ctx->u_for = next_layer;
+    return SIDP_OK;
+  }
   CK(gemm(ctx, 1, ctx->u, h, W.wgu, B, 2 * m.intermediate, h, sidp::EPI_SILU_MUL, ctx->act,
           m.intermediate, nullptr, 0, nullptr, s));
   if (next_g && sidp::gemm_partial_ok(B, h, m.intermediate, ctx->gemm_ws_bytes)) {
@@ -970,6 +986,7 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   // the device idles: with CaS flag-wait kernels spinning on another (virtual) rank that is a
   // deadlock.  Load every kernel now.
   CK(sidp::gemm_preload());
+  sidp::mlp_prepare(m.hidden, m.intermediate, ctx->gemm_ws_bytes);
   CK(sidp::attention_preload());
   CK(sidp::norm_preload());
   CK(sidp::fetch_preload());
@@ -1512,6 +1529,34 @@ sidp_status sidp_test_gemm_resid_norm(const void* x, int32_t ldx, const void* w,
                                 reinterpret_cast<bf16*>(xout), N, reinterpret_cast<const bf16*>(g),
                                 eps, reinterpret_cast<bf16*>(u), N, M, N, s);
   if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm_resid_norm: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
+sidp_status sidp_test_mlp_fused(const void* u, const void* wgu, const void* wd, const void* resid,
+                                int32_t M, int32_t h, int32_t I, const void* g, float eps,
+                                void* act, void* xout, void* unorm, void* stream) {
+  static float* ws = nullptr;
+  static int* counters = nullptr;
+  static const size_t ws_bytes = (size_t)58 << 20;
+  if (!ws && (cudaMalloc(&ws, ws_bytes) != cudaSuccess ||
+              cudaMalloc(&counters, (1 << 16) * sizeof(int)) != cudaSuccess ||
+              cudaMemset(counters, 0, (1 << 16) * sizeof(int)) != cudaSuccess))
+    return fail(SIDP_ENOMEM, "test workspace");
+  const sidp::GemmWorkspace w{ws, ws_bytes, counters, 1 << 16};
+  if (!sidp::mlp_fused_ok(M, h, I, ws_bytes, 1 << 16))
+    return fail(SIDP_EINVAL, "shape M=%d h=%d I=%d not eligible for the fused MLP", M, h, I);
+  sidp::PartialSrc part{};
+  sidp::MlpArgs a{};
+  a.u = reinterpret_cast<const bf16*>(u); a.ldu = h; a.wgu = reinterpret_cast<const bf16*>(wgu);
+  a.wd = reinterpret_cast<const bf16*>(wd); a.act = reinterpret_cast<bf16*>(act); a.ldact = I;
+  a.M = M; a.h = h; a.I = I; a.partial_out = &part;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = sidp::mlp_launch(a, w, s);
+  if (e == cudaSuccess)
+    e = sidp::resid_norm_launch(part, reinterpret_cast<const bf16*>(resid), h,
+                                reinterpret_cast<bf16*>(xout), h, reinterpret_cast<const bf16*>(g),
+                                eps, reinterpret_cast<bf16*>(unorm), h, M, h, s);
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "mlp_fused: %s", cudaGetErrorString(e));
   return SIDP_OK;
 }
 

@@ -165,6 +165,37 @@ def test_gemm_hybrid_streamk_tail(P, M, N, K):
     assert (d3 <= refs.abs() * 2.0 ** -7 + 1e-4 * refs.abs().max()).all()
 
 
+@pytest.mark.parametrize("M,h,I", [(8, 256, 768), (256, 1024, 3072), (200, 5120, 25600),
+                                   (256, 5120, 25600), (64, 2048, 9472)])
+def test_mlp_fused(P, M, h, I):
+    """Fused gate/up -> down launch (SURVEY.md a10 + a11) + resid_norm, vs fp64 of the same bf16
+    operands: act within bf16 rounding, xout = resid + act Wd^T and u = RMSNorm(xout) g."""
+    g = torch.Generator().manual_seed(M + h + I)
+    u = _lvl((M, h), g).cuda()
+    wg = _lvl((I, h), g, 2.0 ** -5)
+    wu = _lvl((I, h), g, 2.0 ** -5)
+    wgu = torch.cat([torch.cat([wg[8 * t:8 * t + 8], wu[8 * t:8 * t + 8]]) for t in range(I // 8)]).cuda()
+    wd = _lvl((h, I), g, 2.0 ** -7).cuda()
+    r = _lvl((M, h), g).cuda()
+    gain = (1 + _lvl((h,), g, 2.0 ** -3).float()).to(torch.bfloat16).cuda()
+    act = torch.full((M, I), float("nan"), dtype=torch.bfloat16, device="cuda")
+    xout = torch.full((M, h), float("nan"), dtype=torch.bfloat16, device="cuda")
+    un = torch.full((M, h), float("nan"), dtype=torch.bfloat16, device="cuda")
+    for _ in range(2):   # twice: the tile counters must be reset by the previous launch
+        P.test_mlp_fused(u, wgu, wd, r, gain, 1e-6, act, xout, un)
+        torch.cuda.synchronize()
+    ud = u.cpu().double()
+    a_, b_ = ud @ wg.double().T, ud @ wu.double().T
+    aref = a_ / (1 + torch.exp(-a_)) * b_
+    d = (act.cpu().double() - aref).abs()
+    assert (d <= aref.abs() * 2.0 ** -7 + 1e-4 * aref.abs().max()).all()
+    xref = r.cpu().double() + act.cpu().double() @ wd.cpu().double().T   # from the GPU's act
+    got = xout.cpu().double()
+    assert ((got - xref).abs() <= xref.abs() * 2.0 ** -8 + 1e-5 * xref.abs().max()).all()
+    uref = got * torch.rsqrt((got * got).mean(-1, keepdim=True) + 1e-6) * gain.cpu().double()
+    assert ((un.cpu().double() - uref).abs() <= uref.abs() * 2.0 ** -7 + 1e-6 * uref.abs().max()).all()
+
+
 @pytest.mark.parametrize("M,F,K,splits", [(8, 64, 256, 1), (33, 192, 512, 0), (256, 640, 1024, 4),
                                           (200, 328, 512, -1), (300, 1040, 256, -1), (40, 200, 256, -1)])
 def test_gemm_silu_mul(P, M, F, K, splits):
