@@ -1632,7 +1632,8 @@ MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
 const MlpSched* mlp_sched(int h, int I, size_t ws_bytes) {
   static std::map<MlpKey, MlpSched> cache;
   const int C = std::max(1, num_sms() / 2);
-  const int max_seg = (int)std::min<size_t>(8, ws_bytes / ((size_t)256 * h * 4));
+  static int env_seg = getenv("SIDP_MLP_SEGS") ? atoi(getenv("SIDP_MLP_SEGS")) : 8;
+  const int max_seg = (int)std::min<size_t>(std::max(1, env_seg), ws_bytes / ((size_t)256 * h * 4));
   const MlpKey key{max_seg, h, I, C};
   auto it = cache.find(key);
   if (it == cache.end()) {
