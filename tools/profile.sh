@@ -10,7 +10,7 @@ S="python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e --no-cpu-baseline --
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 8 -c 1 \
    -o gpurun_out/prof_attn -f $S > gpurun_out/ncu_attn.log 2>&1
 # one decoder layer's GEMMs (qkv, o, gate/up, down) after the warm-up layers, then the LM head
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm2_kernel -s 32 -c 5 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"gemm2_kernel|mlp2_kernel" -s 24 -c 4 \
    -o gpurun_out/prof_gemm -f $S > gpurun_out/ncu_gemm.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:"qkv_post|rmsnorm|resid_norm" -s 24 -c 4 \
    -o gpurun_out/prof_small -f $S > gpurun_out/ncu_small.log 2>&1
