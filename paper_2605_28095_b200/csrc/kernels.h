@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace sidp {
 
 using bf16 = __nv_bfloat16;
@@ -106,6 +108,10 @@ struct MlpArgs {
 };
 bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters);
 void mlp_prepare(int h, int I, size_t ws_bytes);   // builds the schedule (call before capture)
+// The host list schedule (no CUDA calls): per-pair unit lists {phase | seg << 8, tile, kb0, kb1}
+// (flat, cluster c at [off[c], off[c+1])) and the down segments per tile.
+void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, std::vector<int4>& flat,
+                    std::vector<int>& off, std::vector<int>& nseg);
 cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t s);
 
 // ---------------------------------------------------------------- element-wise / small kernels

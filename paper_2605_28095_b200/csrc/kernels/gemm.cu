@@ -1587,8 +1587,11 @@ struct MlpKey {
 // tiles round-robin (whole tiles, the SiLU epilogue needs complete sums); then the down tiles'
 // k-range chunks in k-major order, each to the earliest-free pair, starting no earlier than the
 // gate/up tile producing its first act k-block (a down k-step k depends on gate/up tile k).
-MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
-  MlpSched sc;
+}  // namespace
+
+// host-only planning half of build_mlp_sched (exposed for the CPU test of the schedule)
+void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, std::vector<int4>& flat,
+                    std::vector<int>& off, std::vector<int>& nseg) {
   std::vector<std::vector<int4>> lists(C);
   std::vector<double> F(C, 0.0), done(G, 0.0);
   for (int g = 0; g < G; ++g) {
@@ -1599,7 +1602,7 @@ MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
   }
   const int nch = std::max(1, std::min(max_seg, nks2));
   const int q = (nks2 + nch - 1) / nch;
-  sc.nseg.assign(D, 0);
+  nseg.assign(D, 0);
   for (int k0 = 0; k0 < nks2; k0 += q) {
     const int k1 = std::min(nks2, k0 + q);
     for (int t = 0; t < D; ++t) {
@@ -1608,17 +1611,25 @@ MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
         if (F[i] < F[c]) c = i;
       const double start = std::max(F[c], done[k0]);
       F[c] = std::max(start + (k1 - k0), done[k1 - 1] + 1.0);
-      lists[c].push_back(make_int4(1 | (sc.nseg[t] << 8), t, k0, k1));
-      sc.nseg[t]++;
+      lists[c].push_back(make_int4(1 | (nseg[t] << 8), t, k0, k1));
+      nseg[t]++;
     }
   }
-  for (int t = 0; t < D; ++t) sc.max_seg = std::max(sc.max_seg, sc.nseg[t]);
-  std::vector<int4> flat;
-  std::vector<int> off(1, 0);
+  flat.clear();
+  off.assign(1, 0);
   for (int c = 0; c < C; ++c) {
     flat.insert(flat.end(), lists[c].begin(), lists[c].end());
     off.push_back((int)flat.size());
   }
+}
+
+namespace {
+MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
+  MlpSched sc;
+  std::vector<int4> flat;
+  std::vector<int> off;
+  plan_mlp_units(G, nks1, D, nks2, C, max_seg, flat, off, sc.nseg);
+  for (int t = 0; t < D; ++t) sc.max_seg = std::max(sc.max_seg, sc.nseg[t]);
   cudaMalloc(&sc.d_units, flat.size() * sizeof(int4));
   cudaMalloc(&sc.d_uoff, off.size() * sizeof(int));
   cudaMemcpy(sc.d_units, flat.data(), flat.size() * sizeof(int4), cudaMemcpyHostToDevice);

@@ -1560,6 +1560,26 @@ sidp_status sidp_test_mlp_fused(const void* u, const void* wgu, const void* wd, 
   return SIDP_OK;
 }
 
+sidp_status sidp_test_mlp_schedule(int32_t G, int32_t nks1, int32_t D, int32_t nks2, int32_t C,
+                                   int32_t max_seg, int32_t* units, int32_t cap, int32_t* off,
+                                   int32_t* nseg, int32_t* n_units) {
+  if (G <= 0 || nks1 <= 0 || D <= 0 || nks2 <= 0 || C <= 0 || max_seg <= 0 || !units || !off ||
+      !nseg || !n_units)
+    return fail(SIDP_EINVAL, "bad schedule arguments");
+  std::vector<int4> flat;
+  std::vector<int> o, ns;
+  sidp::plan_mlp_units(G, nks1, D, nks2, C, max_seg, flat, o, ns);
+  *n_units = (int32_t)flat.size();
+  if ((int)flat.size() > cap) return fail(SIDP_EINVAL, "capacity %d < %zu units", cap, flat.size());
+  for (size_t i = 0; i < flat.size(); ++i) {
+    units[4 * i] = flat[i].x; units[4 * i + 1] = flat[i].y;
+    units[4 * i + 2] = flat[i].z; units[4 * i + 3] = flat[i].w;
+  }
+  for (int c = 0; c <= C; ++c) off[c] = o[c];
+  for (int t = 0; t < D; ++t) nseg[t] = ns[t];
+  return SIDP_OK;
+}
+
 sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
                           int32_t tensor, int32_t layer, int32_t kind, int32_t scale_k,
                           int64_t row0, int64_t lcols, int32_t row_map, void* stream) {
