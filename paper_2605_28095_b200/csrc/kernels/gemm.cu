@@ -1576,10 +1576,10 @@ struct MlpSched {
   std::vector<int> nseg;   // per down tile
   int max_seg = 0;
 };
-struct MlpKey {
-  int M, h, I, C;
+struct MlpKey {   // the unit tables live on the device that was current when they were built
+  int dev, max_seg, h, I, C;
   bool operator<(const MlpKey& o) const {
-    return std::tie(M, h, I, C) < std::tie(o.M, o.h, o.I, o.C);
+    return std::tie(dev, max_seg, h, I, C) < std::tie(o.dev, o.max_seg, o.h, o.I, o.C);
   }
 };
 
@@ -1645,7 +1645,9 @@ const MlpSched* mlp_sched(int h, int I, size_t ws_bytes) {
   const int C = std::max(1, num_sms() / 2);
   static int env_seg = getenv("SIDP_MLP_SEGS") ? atoi(getenv("SIDP_MLP_SEGS")) : 8;
   const int max_seg = (int)std::min<size_t>(std::max(1, env_seg), ws_bytes / ((size_t)256 * h * 4));
-  const MlpKey key{max_seg, h, I, C};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const MlpKey key{dev, max_seg, h, I, C};
   auto it = cache.find(key);
   if (it == cache.end()) {
     it = cache.emplace(key, build_mlp_sched(I / 128, h / (BK * 2), (h + 255) / 256, I / (BK * 2), C,
