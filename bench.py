@@ -235,14 +235,17 @@ def load_traffic(workload, cls):
         return None
 
 
-def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms):
+def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms, remote_bytes=None):
     """Step-level roofline of SURVEY.md §8(d): T2 = max(sum 2PB/P_peak, sum R/BW_nvl) + T_lm;
-    T3 adds HBM weight reads and KV reads per layer."""
+    T3 adds HBM weight reads and KV reads per layer.  remote_bytes: the bytes actually fetched
+    per step (FFN-only pooling fetches less than whole layers)."""
     P = m.hidden * m.qkv_dim + m.q_dim * m.hidden + 3 * m.hidden * m.intermediate   # P_l
     L = m.num_layers
     lm = max(2.0 * B * m.vocab * m.hidden / (peaks["tflops"] * 1e12),
              2.0 * m.vocab * m.hidden / (peaks["hbm"] * 1e9))
     remote = (L - -(-L // d)) * P * 2.0 if d > 1 else 0.0      # (L - L/d) layers x bytes
+    if remote_bytes is not None:
+        remote = float(remote_bytes)
     t_gemm = L * 2.0 * P * B / (peaks["tflops"] * 1e12)
     t_nvl = remote / (peaks["nvl"] * 1e9)
     T2 = max(t_gemm, t_nvl) + lm
@@ -317,7 +320,9 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
         lb = st["layer_bytes"]
         fetch_gbs = lb / (f_ms * 1e-3) / 1e9 if f_ms > 0 else None
         ctx_avg = pos_before + (args.emulate_steps - 1) / 2.0
-        ns = north_star_roofline(m, B, ctx_avg, W, peaks, ms)
+        ns = north_star_roofline(m, B, ctx_avg, W, peaks, ms,
+                                 remote_bytes=(m.num_layers - len([l for l in range(m.num_layers)
+                                                                    if l % W == 0])) * st["layer_bytes"])
         remote_layers = m.num_layers - len([l for l in range(m.num_layers) if l % W == 0])
         return {
             "what": f"rank 0 of a {W}-rank WaS group on one B200; the {W - 1} other owners are "

@@ -156,8 +156,8 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
  * replicated tensors, CaS staging + flags, workspaces, the fetch stream and events. */
 sidp_status sidp_alloc(sidp_ctx* ctx);
 
-/* Alternative to sidp_alloc for a serve-only rank: allocate only the owned-weight arena (and
- * the small local per-layer blobs and a CaS flag block so the exported blob is well formed).
+/* Alternative to sidp_alloc for a serve-only rank: allocate only the owned-weight arena (and a
+ * CaS flag block so the exported blob is well formed; no local per-layer parts).
  * The rank owns, initialises (sidp_init_weights_synthetic fills only its owned and local
  * parts) and exports its layers for WaS peers to fetch ("each GPU ... serves its
  * layers to peers"), but never computes: sidp_step / sidp_decode_layer return SIDP_ESTATE and

@@ -1017,8 +1017,8 @@ sidp_status sidp_alloc_serve_only(sidp_ctx* ctx) {
     fail(SIDP_ENOMEM, "cudaMalloc(%zu)", bytes);
     return false;
   };
-  if (!dm(reinterpret_cast<void**>(&ctx->arena), std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b) ||
-      !dm(reinterpret_cast<void**>(&ctx->local), (size_t)ctx->L * local_b))
+  // the owned pooled blobs only: the local (replicated) per-layer parts are never read by peers
+  if (!dm(reinterpret_cast<void**>(&ctx->arena), std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b))
     return SIDP_ENOMEM;
   // a flag block only, so the exported blob is well-formed (a serve-only rank serves no CaS)
   ctx->cas_bytes = 4096;
@@ -1060,6 +1060,7 @@ sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream) {
       if (ctx->owner[l] != ctx->r) return nullptr;
       return ctx->arena + (size_t)ctx->owned_index[l] * ctx->pooled_elems + ctx->comp_off[comp];
     }
+    if (ctx->serve_only) return nullptr;   // no local parts on a serve-only rank
     return ctx->local + (size_t)l * ctx->local_elems + ctx->comp_off[comp];
   };
   for (int l = 0; l < ctx->L; ++l) {
