@@ -22,11 +22,12 @@ SIDP_DEV uint32_t f2_to_bf16x2(float a, float b) {
 constexpr int kFixSeg = 4;
 // one 8-feature vector of the deferred fix-up: fp32 slices summed in slice order (slices past
 // nseg add +0), + the bf16 residual, rounded once; the loads of a vector are issued together
+template <int NS = kFixSeg>
 SIDP_DEV uint4 fix_vector(const PartialSrc& ps, const float* src, size_t slice,
                                             int nseg, uint4 rr) {
-  float4 lo[kFixSeg], hi[kFixSeg];
+  float4 lo[NS], hi[NS];
 #pragma unroll
-  for (int q = 0; q < kFixSeg; ++q) {
+  for (int q = 0; q < NS; ++q) {
     lo[q] = hi[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (q < nseg) {
       lo[q] = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
@@ -35,11 +36,11 @@ SIDP_DEV uint4 fix_vector(const PartialSrc& ps, const float* src, size_t slice,
   }
   float4 al = make_float4(0.f, 0.f, 0.f, 0.f), ah = al;
 #pragma unroll
-  for (int q = 0; q < kFixSeg; ++q) {
+  for (int q = 0; q < NS; ++q) {
     al.x += lo[q].x; al.y += lo[q].y; al.z += lo[q].z; al.w += lo[q].w;
     ah.x += hi[q].x; ah.y += hi[q].y; ah.z += hi[q].z; ah.w += hi[q].w;
   }
-  for (int q = kFixSeg; q < nseg; ++q) {
+  for (int q = NS; q < nseg; ++q) {
     const float4 x0 = __ldcg(reinterpret_cast<const float4*>(src + q * slice));
     const float4 x1 = __ldcg(reinterpret_cast<const float4*>(src + q * slice + 4));
     al.x += x0.x; al.y += x0.y; al.z += x0.z; al.w += x0.w;

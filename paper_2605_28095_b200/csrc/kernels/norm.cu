@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const bf16* __res
 // slices, residual and gain of a row are all loaded in ONE round trip and x stays in registers
 // for the scaling pass; the norm statistics use the rounded x_out, exactly as rmsnorm_kernel
 // would on a stored x_out.  Longer rows take the looped path (re-reads its own x_out).
-__global__ void __launch_bounds__(1024, 1) resid_norm_kernel(
+template <int NS, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) resid_norm_kernel(
     const PartialSrc ps, const bf16* __restrict__ resid, int ldr, bf16* xout, int ldx,
     const bf16* __restrict__ g, float eps, bf16* __restrict__ u, int ldu, int h, int rows,
     int late_trigger) {
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(1024, 1) resid_norm_kernel(
       if (k < nvec) {
         gw = *reinterpret_cast<const uint4*>(g + n);
         const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
-        x = fix_vector(ps, wrow + n, slice, ps.nseg[partial_tile(ps, row, n)], rr);
+        x = fix_vector<NS>(ps, wrow + n, slice, ps.nseg[partial_tile(ps, row, n)], rr);
         *reinterpret_cast<uint4*>(xout + (size_t)row * ldx + n) = x;
       }
       const float r = rsqrtf(block_sum(k < nvec ? sumsq8(x) : 0.0f) / (float)h + eps);
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(1024, 1) resid_norm_kernel(
       for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
         const int n = k * 8;
         const uint4 rr = *reinterpret_cast<const uint4*>(resid + (size_t)row * ldr + n);
-        const uint4 x = fix_vector(ps, wrow + n, slice, ps.nseg[partial_tile(ps, row, n)], rr);
+        const uint4 x = fix_vector<NS>(ps, wrow + n, slice, ps.nseg[partial_tile(ps, row, n)], rr);
         *reinterpret_cast<uint4*>(xout + (size_t)row * ldx + n) = x;
         ss += sumsq8(x);
       }
@@ -211,8 +212,18 @@ cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, 
   static const int grid_mode = getenv("SIDP_FIX_GRID") ? atoi(getenv("SIDP_FIX_GRID")) : 0;
   static const int late = getenv("SIDP_FIX_LATE_TRIGGER") ? atoi(getenv("SIDP_FIX_LATE_TRIGGER")) : 0;
   const int grid = grid_mode ? std::min(rows, sms) : rows;
-  return launch_pdl(resid_norm_kernel, dim3(grid), dim3(threads), 0, s, ps, resid, ldr, xout, ldx,
-                    g, eps, u, ldu, h, rows, late);
+  // slices loaded in one round trip: up to 8 per vector (640-thread rows, 96 registers) when the
+  // producer split tiles into more than 4 segments (the fused MLP's down units); else 4
+  int max_seg = 0;
+  const int tiles = ps.m_tiles * ps.f_tiles;
+  for (int t = 0; t < tiles && t < kPartialMaxTiles; ++t) max_seg = std::max(max_seg, (int)ps.nseg[t]);
+  static const int env_ns = getenv("SIDP_FIX_NS") ? atoi(getenv("SIDP_FIX_NS")) : 0;
+  const bool wide = env_ns ? env_ns == 8 : max_seg > 4;
+  if (wide && threads <= 640)
+    return launch_pdl(resid_norm_kernel<8, 640>, dim3(grid), dim3(threads), 0, s, ps, resid, ldr,
+                      xout, ldx, g, eps, u, ldu, h, rows, late);
+  return launch_pdl(resid_norm_kernel<kFixSeg, 1024>, dim3(grid), dim3(threads), 0, s, ps, resid,
+                    ldr, xout, ldx, g, eps, u, ldu, h, rows, late);
 }
 
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
@@ -238,7 +249,8 @@ cudaError_t norm_preload() {
   cudaError_t e = cudaSuccess;
   if (cudaFuncGetAttributes(&fa, rmsnorm_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, embed_kernel) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, resid_norm_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, resid_norm_kernel<8, 640>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, resid_norm_kernel<kFixSeg, 1024>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, argmax_finalize_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, argmax_reset_kernel) != cudaSuccess) e = cudaGetLastError();
   return e;
