@@ -274,12 +274,13 @@ sidp_status sidp_test_mlp_fused(const void* u, const void* wgu, const void* wd, 
                                 void* act, void* xout, void* unorm, void* stream);
 
 /* Host-only (no GPU): the fused MLP's list schedule for G gate/up tiles of nks1 k-steps and D
- * down tiles of nks2 k-steps over C CTA pairs, down split into <= max_seg chunks.  units: int32
- * [cap][4] = {phase | seg << 8, tile, kb0, kb1}; off [C + 1] (pair c owns units [off[c],
- * off[c+1])); nseg [D]; *n_units = count.  SIDP_EINVAL on bad arguments or cap too small. */
+ * down tiles of nks2 k-steps, MT token tiles of 256 rows, over C CTA pairs, down split into
+ * <= max_seg chunks per (tile, token tile).  units: int32 [cap][4] = {phase | seg << 8 |
+ * mt << 16, tile, kb0, kb1}; off [C + 1] (pair c owns units [off[c], off[c+1])); nseg [D * MT]
+ * (index tile * MT + mt); *n_units = count.  SIDP_EINVAL on bad arguments or cap too small. */
 sidp_status sidp_test_mlp_schedule(int32_t G, int32_t nks1, int32_t D, int32_t nks2, int32_t C,
-                                   int32_t max_seg, int32_t* units, int32_t cap, int32_t* off,
-                                   int32_t* nseg, int32_t* n_units);
+                                   int32_t max_seg, int32_t MT, int32_t* units, int32_t cap,
+                                   int32_t* off, int32_t* nseg, int32_t* n_units);
 
 /* K12 on an arbitrary buffer: dst[r*ld + c] = value(seed, tensor, layer, (row0+r)*lcols + c)
  * with kind 0 weight (scale from scale_k), 1 gain, 2 bias, 3 unit; row_map 1 = packed

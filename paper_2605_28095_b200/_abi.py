@@ -85,7 +85,8 @@ SIGNATURES = {
     "sidp_test_gemm_resid_norm": [_P, _I32, _P, _I32, _I32, _I32, _P, _I32, _P, C.c_float, _P,
                                   _P, _P],
     "sidp_test_mlp_fused": [_P, _P, _P, _P, _I32, _I32, _I32, _P, C.c_float, _P, _P, _P, _P],
-    "sidp_test_mlp_schedule": [_I32, _I32, _I32, _I32, _I32, _I32, _PI32, _I32, _PI32, _PI32, _PI32],
+    "sidp_test_mlp_schedule": [_I32, _I32, _I32, _I32, _I32, _I32, _I32, _PI32, _I32, _PI32, _PI32,
+                               _PI32],
     "sidp_test_gen": [_P, _I64, _I64, _I64, C.c_uint64, _I32, _I32, _I32, _I32, _I64, _I64, _I32, _P],
     "sidp_test_gen_kv": [_P, _I32, _I32, _I32, _I32, _I32, _I64, C.c_uint64, _I32, _I32, _P],
     "sidp_layer_ptr": [_P, _I32, C.POINTER(_P), C.POINTER(_P)],

@@ -106,12 +106,14 @@ struct MlpArgs {
   int M, h, I;
   PartialSrc* partial_out;       // down partial slices for resid_norm
 };
-bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters);
+// max_tt: most 256-row token tiles allowed (0 = the runtime policy, SIDP_MLP_MAX_TT, default 1;
+// the kernel supports 2).
+bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters, int max_tt = 0);
 void mlp_prepare(int h, int I, size_t ws_bytes);   // builds the schedule (call before capture)
 // The host list schedule (no CUDA calls): per-pair unit lists {phase | seg << 8, tile, kb0, kb1}
 // (flat, cluster c at [off[c], off[c+1])) and the down segments per tile.
-void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, std::vector<int4>& flat,
-                    std::vector<int>& off, std::vector<int>& nseg);
+void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, int MT,
+                    std::vector<int4>& flat, std::vector<int>& off, std::vector<int>& nseg);
 cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t s);
 
 // ---------------------------------------------------------------- element-wise / small kernels

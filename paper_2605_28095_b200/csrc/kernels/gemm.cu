@@ -911,12 +911,12 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
 // from a not-yet-resident CTA of this grid.
 struct MlpParams {
   int M, N1, K1, N2, K2;         // gate/up [N1 = 2I][K1 = h]; down [N2 = h][K2 = I]
-  int BNT, stages;
-  const int4* units;             // {phase | seg << 8, tile, kb0, kb1}; cluster c: [uoff[c], uoff[c+1])
+  int BNT, stages, MT;           // MT token tiles of BNT rows
+  const int4* units;             // {phase | seg << 8 | mt << 16, tile, kb0, kb1}; pair c: [uoff[c], uoff[c+1])
   const int* uoff;
   bf16* act; int ldact;          // [M][I]
   float* ws;                     // down partials [seg][M][N2]
-  int* flags;                    // [N1 / 256] gate/up tile completion counters (0 between launches)
+  int* flags;                    // [N1 / 256][MT] gate/up tile completion counters (0 between launches)
   unsigned int* done;            // CTA exit counter (the last CTA resets the flags)
   int n_flags;
 };
@@ -984,7 +984,7 @@ mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ C
       const uint32_t stage_tx = 2 * (a_bytes + b_bytes);
       const uint64_t wpol = policy_evict_first();
       auto issue = [&](const int4 un, int kb, int s, bool pre) {
-        const int phase = un.x & 0xff;
+        const int phase = un.x & 0xff, mt = (un.x >> 16) & 0xffff;
         const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
         const CUtensorMap* tw = phase ? &tm_w2 : &tm_w1;
         const CUtensorMap* tx = phase ? &tm_x2 : &tm_x1;
@@ -993,13 +993,14 @@ mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ C
         for (int j = 0; j < KPS; ++j)
           tma_load_2d_2sm_hint(tw, lbar, sA + (size_t)s * a_bytes + j * a_sub, (kb * KPS + j) * BK, arow, wpol);
         if (pre) return;
-        if (phase) {   // act k-block kb is gate/up tile kb's output: wait until both CTAs stored it
-          while (ld_acquire_gpu_s32(p.flags + kb) < 2) __nanosleep(64);
+        if (phase) {   // act k-block kb is gate/up tile (kb, mt)'s output: wait until both CTAs stored it
+          while (ld_acquire_gpu_s32(p.flags + kb * p.MT + mt) < 2) __nanosleep(64);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
 #pragma unroll
         for (int j = 0; j < KPS; ++j)
-          tma_load_2d_2sm(tx, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, rank * HALF);
+          tma_load_2d_2sm(tx, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK,
+                          mt * BNT + rank * HALF);
       };
       // the first stages' weight tiles before griddepcontrol.wait (weights are resident)
       int npre = 0;
@@ -1023,16 +1024,17 @@ mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ C
             if (leader) mbar_arrive_expect_tx(&full[s], stage_tx);
             issue(un, kb, s, false);
           } else {   // weight half already in flight: the activation half now
-            const int phase = un.x & 0xff;
+            const int phase = un.x & 0xff, mt = (un.x >> 16) & 0xffff;
             const uint32_t lbar = mapa_shared(smem_u32(&full[s]), 0);
             const CUtensorMap* tx = phase ? &tm_x2 : &tm_x1;
             if (phase) {
-              while (ld_acquire_gpu_s32(p.flags + kb) < 2) __nanosleep(64);
+              while (ld_acquire_gpu_s32(p.flags + kb * p.MT + mt) < 2) __nanosleep(64);
               asm volatile("fence.proxy.async.global;" ::: "memory");
             }
 #pragma unroll
             for (int j = 0; j < KPS; ++j)
-              tma_load_2d_2sm(tx, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK, rank * HALF);
+              tma_load_2d_2sm(tx, lbar, sB + (size_t)s * b_bytes + j * b_sub, (kb * KPS + j) * BK,
+                              mt * BNT + rank * HALF);
           }
         }
       }
@@ -1080,11 +1082,12 @@ mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ C
     const int tid = (warp - 2) * 32 + lane;
     KParams kp{};   // the SiLU*mul store of store_phase
     kp.M = p.M; kp.N = p.N1; kp.out = p.act; kp.ldo = p.ldact;
-    const int nchunks = min(BNT, ((p.M + 31) / 32) * 32) / 32;
     int un_i = 0;
     for (int ui = u0; ui < u1; ++ui, ++un_i) {
       const int4 un = p.units[ui];
-      const int phase = un.x & 0xff, seg = un.x >> 8;
+      const int phase = un.x & 0xff, seg = (un.x >> 8) & 0xff, mt = (un.x >> 16) & 0xffff;
+      const int mbase = mt * BNT;
+      const int nchunks = min(BNT, ((p.M - mbase + 31) / 32) * 32) / 32;
       const int acc = un_i & 1;
       const uint32_t aph = (un_i >> 1) & 1;
       const int n0 = un.y * 2 * WROWS + rank * WROWS;
@@ -1106,12 +1109,12 @@ mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ C
         }
         named_bar_sync(1, 128);
         if (phase == 0) {
-          store_phase<EPI_SILU_MUL>(kp, stg, c * 32, n0, pt, tid);
+          store_phase<EPI_SILU_MUL>(kp, stg, mbase + c * 32, n0, pt, tid);
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
-            const int m = c * 32 + j, n = n0 + f;
+            const int m = mbase + c * 32 + j, n = n0 + f;
             if (m < p.M && n < p.N2)
               __stcg(reinterpret_cast<float4*>(part + (size_t)m * p.N2 + n),
                      *reinterpret_cast<const float4*>(stg + j * SROW + f));
@@ -1122,7 +1125,7 @@ mlp2_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ C
       if (phase == 0) {   // this CTA's half of gate/up tile un.y is stored: publish it
         __threadfence();
         named_bar_sync(1, 128);
-        if (tid == 0) atomicAdd(p.flags + un.y, 1);
+        if (tid == 0) atomicAdd(p.flags + un.y * p.MT + mt, 1);
       }
     }
   }
@@ -1589,32 +1592,38 @@ struct MlpKey {   // the unit tables live on the device that was current when th
 // gate/up tile producing its first act k-block (a down k-step k depends on gate/up tile k).
 }  // namespace
 
-// host-only planning half of build_mlp_sched (exposed for the CPU test of the schedule)
-void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, std::vector<int4>& flat,
-                    std::vector<int>& off, std::vector<int>& nseg) {
+// host-only planning half of build_mlp_sched (exposed for the CPU test of the schedule).
+// MT token tiles of 256 rows: gate/up units (g, mt) round-robin, token tile by token tile; the
+// down chunks (t, mt, k-range) mt-major then k-major; unit = {phase | seg << 8 | mt << 16, tile,
+// kb0, kb1}; nseg is indexed by the W-major tile t * MT + mt.
+void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, int MT,
+                    std::vector<int4>& flat, std::vector<int>& off, std::vector<int>& nseg) {
   std::vector<std::vector<int4>> lists(C);
-  std::vector<double> F(C, 0.0), done(G, 0.0);
-  for (int g = 0; g < G; ++g) {
-    const int c = g % C;
-    lists[c].push_back(make_int4(0, g, 0, nks1));
-    F[c] += nks1;
-    done[g] = F[c];
-  }
+  std::vector<double> F(C, 0.0), done((size_t)G * MT, 0.0);
+  for (int mt = 0; mt < MT; ++mt)
+    for (int g = 0; g < G; ++g) {
+      const int c = (mt * G + g) % C;
+      lists[c].push_back(make_int4(0 | (mt << 16), g, 0, nks1));
+      F[c] += nks1;
+      done[(size_t)g * MT + mt] = F[c];
+    }
   const int nch = std::max(1, std::min(max_seg, nks2));
   const int q = (nks2 + nch - 1) / nch;
-  nseg.assign(D, 0);
-  for (int k0 = 0; k0 < nks2; k0 += q) {
-    const int k1 = std::min(nks2, k0 + q);
-    for (int t = 0; t < D; ++t) {
-      int c = 0;
-      for (int i = 1; i < C; ++i)
-        if (F[i] < F[c]) c = i;
-      const double start = std::max(F[c], done[k0]);
-      F[c] = std::max(start + (k1 - k0), done[k1 - 1] + 1.0);
-      lists[c].push_back(make_int4(1 | (nseg[t] << 8), t, k0, k1));
-      nseg[t]++;
+  nseg.assign((size_t)D * MT, 0);
+  for (int mt = 0; mt < MT; ++mt)
+    for (int k0 = 0; k0 < nks2; k0 += q) {
+      const int k1 = std::min(nks2, k0 + q);
+      for (int t = 0; t < D; ++t) {
+        int c = 0;
+        for (int i = 1; i < C; ++i)
+          if (F[i] < F[c]) c = i;
+        const double start = std::max(F[c], done[(size_t)k0 * MT + mt]);
+        F[c] = std::max(start + (k1 - k0), done[(size_t)(k1 - 1) * MT + mt] + 1.0);
+        int& ns = nseg[(size_t)t * MT + mt];
+        lists[c].push_back(make_int4(1 | (ns << 8) | (mt << 16), t, k0, k1));
+        ns++;
+      }
     }
-  }
   flat.clear();
   off.assign(1, 0);
   for (int c = 0; c < C; ++c) {
@@ -1624,12 +1633,12 @@ void plan_mlp_units(int G, int nks1, int D, int nks2, int C, int max_seg, std::v
 }
 
 namespace {
-MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
+MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg, int MT) {
   MlpSched sc;
   std::vector<int4> flat;
   std::vector<int> off;
-  plan_mlp_units(G, nks1, D, nks2, C, max_seg, flat, off, sc.nseg);
-  for (int t = 0; t < D; ++t) sc.max_seg = std::max(sc.max_seg, sc.nseg[t]);
+  plan_mlp_units(G, nks1, D, nks2, C, max_seg, MT, flat, off, sc.nseg);
+  for (int v : sc.nseg) sc.max_seg = std::max(sc.max_seg, v);
   cudaMalloc(&sc.d_units, flat.size() * sizeof(int4));
   cudaMalloc(&sc.d_uoff, off.size() * sizeof(int));
   cudaMemcpy(sc.d_units, flat.data(), flat.size() * sizeof(int4), cudaMemcpyHostToDevice);
@@ -1638,39 +1647,54 @@ MlpSched build_mlp_sched(int G, int nks1, int D, int nks2, int C, int max_seg) {
 }
 }  // namespace
 
-// The schedule depends on the shapes, not on M (segments are sized for M <= 256): built once
-// per (h, I) — mlp_prepare runs it at allocation time, outside any CUDA-graph capture.
-const MlpSched* mlp_sched(int h, int I, size_t ws_bytes) {
+constexpr int kMlpMaxTokenTiles = 2;   // M <= 512
+
+// The schedule depends on the shapes and the token-tile count, not on M itself (segments are
+// sized for MT x 256 rows): built once per (h, I, MT) — mlp_prepare runs it at allocation
+// time, outside any CUDA-graph capture.
+const MlpSched* mlp_sched(int h, int I, int MT, size_t ws_bytes) {
   static std::map<MlpKey, MlpSched> cache;
   const int C = std::max(1, num_sms() / 2);
   static int env_seg = getenv("SIDP_MLP_SEGS") ? atoi(getenv("SIDP_MLP_SEGS")) : 8;
-  const int max_seg = (int)std::min<size_t>(std::max(1, env_seg), ws_bytes / ((size_t)256 * h * 4));
+  const int max_seg =
+      (int)std::min<size_t>(std::max(1, env_seg), ws_bytes / ((size_t)MT * 256 * h * 4));
   int dev = 0;
   cudaGetDevice(&dev);
-  const MlpKey key{dev, max_seg, h, I, C};
+  const MlpKey key{dev, max_seg * 16 + MT, h, I, C};
   auto it = cache.find(key);
   if (it == cache.end()) {
     it = cache.emplace(key, build_mlp_sched(I / 128, h / (BK * 2), (h + 255) / 256, I / (BK * 2), C,
-                                            max_seg)).first;
+                                            max_seg, MT)).first;
   }
   return &it->second;
 }
 
 void mlp_prepare(int h, int I, size_t ws_bytes) {
-  if (h > 0 && I > 0 && h % 256 == 0 && I % 128 == 0) mlp_sched(h, I, ws_bytes);
+  if (h > 0 && I > 0 && h % 256 == 0 && I % 128 == 0)
+    for (int mt = 1; mt <= kMlpMaxTokenTiles; ++mt) mlp_sched(h, I, mt, ws_bytes);
 }
 
-bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters) {
+bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters, int max_tt) {
   static int env = getenv("SIDP_MLP_FUSED") ? atoi(getenv("SIDP_MLP_FUSED")) : 1;
-  if (!env || M <= 0 || M > 256 || h % 256 || I % 128 || h % BK || I % BK) return false;
+  // Policy default: one token tile.  At M = 512 (2 tiles) the fused launch is ~5% faster than
+  // gate/up + down, but resid_norm then reads up to 8 fp32 slices of 512 rows instead of one
+  // bf16 row block, which cancels it (53.2 vs 53.1 ms/step, B=512).
+  static int env_mt = getenv("SIDP_MLP_MAX_TT") ? atoi(getenv("SIDP_MLP_MAX_TT")) : 1;
+  if (max_tt <= 0) max_tt = env_mt;
+  const int MT = (M + 255) / 256;
+  if (!env || M <= 0 || MT > std::min(max_tt, kMlpMaxTokenTiles) || h % 256 || I % 128 || h % BK ||
+      I % BK)
+    return false;
   const int G = I / 128;                 // gate/up pair tiles = act k-steps of the down GEMM
-  if (n_counters < G + 1) return false;
-  return (size_t)2 * 256 * h * 4 <= ws_bytes;   // at least 2 down segments of M <= 256 rows fit
+  if (n_counters < G * MT + 1) return false;
+  if ((h + 255) / 256 * MT > kPartialMaxTiles) return false;
+  return (size_t)2 * MT * 256 * h * 4 <= ws_bytes;   // at least 2 down segments fit
 }
 
 cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t stream) {
   g_last_launches = 0;
-  if (!mlp_fused_ok(a.M, a.h, a.I, w.ws_bytes, w.n_counters)) return cudaErrorInvalidValue;
+  if (!mlp_fused_ok(a.M, a.h, a.I, w.ws_bytes, w.n_counters, kMlpMaxTokenTiles))
+    return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     attr = true;
@@ -1679,8 +1703,9 @@ cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t st
   }
   const int C = std::max(1, g_num_sms / 2);
   const int G = a.I / 128, nks1 = a.h / (BK * 2), D = (a.h + 255) / 256, nks2 = a.I / (BK * 2);
-  const int BNT = std::max(32, ((a.M + 31) / 32) * 32);
-  const MlpSched* scp = mlp_sched(a.h, a.I, w.ws_bytes);
+  const int MT = (a.M + 255) / 256;
+  const int BNT = MT > 1 ? 256 : std::max(32, ((a.M + 31) / 32) * 32);
+  const MlpSched* scp = mlp_sched(a.h, a.I, MT, w.ws_bytes);
   if (!scp || !scp->d_units) return cudaErrorMemoryAllocation;
   const MlpSched& sc = *scp;
   CUtensorMap tw1, tx1, tw2, tx2;
@@ -1691,14 +1716,15 @@ cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t st
     return cudaErrorInvalidValue;
   MlpParams p{};
   p.M = a.M; p.N1 = 2 * a.I; p.K1 = a.h; p.N2 = a.h; p.K2 = a.I;
-  p.BNT = BNT;
+  p.BNT = BNT; p.MT = MT;
   const size_t stage_bytes = 2 * ((size_t)WROWS * BK * 2 + (size_t)(BNT / 2) * BK * 2);
   const size_t extra = 32 * SROW * 4 + 512;
   static int env_stages = getenv("SIDP_GEMM_STAGES") ? atoi(getenv("SIDP_GEMM_STAGES")) : 12;
   p.stages = std::max(2, (int)std::min<size_t>(env_stages, (kSmemBudget - extra) / stage_bytes));
   p.units = sc.d_units; p.uoff = sc.d_uoff;
   p.act = a.act; p.ldact = a.ldact; p.ws = w.ws;
-  p.flags = w.counters; p.done = reinterpret_cast<unsigned int*>(w.counters + G); p.n_flags = G;
+  p.flags = w.counters; p.done = reinterpret_cast<unsigned int*>(w.counters + G * MT);
+  p.n_flags = G * MT;
   const size_t smem = p.stages * stage_bytes + extra + 1024;
   cudaError_t e = launch_pdl(mlp2_kernel, dim3(2 * C), dim3(kThreads), smem, stream, tw1, tx1, tw2, tx2, p);
   if (e != cudaSuccess) return e;
@@ -1707,9 +1733,9 @@ cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t st
     PartialSrc& o = *a.partial_out;
     o = PartialSrc{};
     o.ws = w.ws; o.M = a.M; o.N = a.h; o.sw = 0;
-    o.tile_m = BNT; o.tile_f = 2 * WROWS; o.m_tiles = 1; o.f_tiles = D;
-    if (D > kPartialMaxTiles) return cudaErrorInvalidValue;
-    for (int t = 0; t < D; ++t) o.nseg[t] = (unsigned char)sc.nseg[t];
+    o.tile_m = BNT; o.tile_f = 2 * WROWS; o.m_tiles = MT; o.f_tiles = D;
+    if (D * MT > kPartialMaxTiles) return cudaErrorInvalidValue;
+    for (int t = 0; t < D * MT; ++t) o.nseg[t] = (unsigned char)sc.nseg[t];
   }
   return cudaSuccess;
 }

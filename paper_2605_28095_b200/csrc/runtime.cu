@@ -942,6 +942,8 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   DM(ctx->qkv, R * ctx->qkvdim * 4);
   DM(ctx->amax, R * 8);
   ctx->gemm_ws_bytes = (size_t)3 * 148 * 128 * 256 * 4;
+  // fused MLP over two token tiles: room for 8 fp32 down k-range slices of 512 rows
+  if (R > 256) ctx->gemm_ws_bytes = std::max(ctx->gemm_ws_bytes, (size_t)8 * 512 * m.hidden * 4);
   DM(ctx->gemm_ws, ctx->gemm_ws_bytes);
   ctx->n_counters = 1 << 16;
   DM(ctx->counters, ctx->n_counters * sizeof(int));
@@ -1544,7 +1546,7 @@ sidp_status sidp_test_mlp_fused(const void* u, const void* wgu, const void* wd, 
               cudaMemset(counters, 0, (1 << 16) * sizeof(int)) != cudaSuccess))
     return fail(SIDP_ENOMEM, "test workspace");
   const sidp::GemmWorkspace w{ws, ws_bytes, counters, 1 << 16};
-  if (!sidp::mlp_fused_ok(M, h, I, ws_bytes, 1 << 16))
+  if (!sidp::mlp_fused_ok(M, h, I, ws_bytes, 1 << 16, 2))
     return fail(SIDP_EINVAL, "shape M=%d h=%d I=%d not eligible for the fused MLP", M, h, I);
   sidp::PartialSrc part{};
   sidp::MlpArgs a{};
@@ -1562,14 +1564,14 @@ sidp_status sidp_test_mlp_fused(const void* u, const void* wgu, const void* wd, 
 }
 
 sidp_status sidp_test_mlp_schedule(int32_t G, int32_t nks1, int32_t D, int32_t nks2, int32_t C,
-                                   int32_t max_seg, int32_t* units, int32_t cap, int32_t* off,
-                                   int32_t* nseg, int32_t* n_units) {
-  if (G <= 0 || nks1 <= 0 || D <= 0 || nks2 <= 0 || C <= 0 || max_seg <= 0 || !units || !off ||
-      !nseg || !n_units)
+                                   int32_t max_seg, int32_t MT, int32_t* units, int32_t cap,
+                                   int32_t* off, int32_t* nseg, int32_t* n_units) {
+  if (G <= 0 || nks1 <= 0 || D <= 0 || nks2 <= 0 || C <= 0 || max_seg <= 0 || MT <= 0 || !units ||
+      !off || !nseg || !n_units)
     return fail(SIDP_EINVAL, "bad schedule arguments");
   std::vector<int4> flat;
   std::vector<int> o, ns;
-  sidp::plan_mlp_units(G, nks1, D, nks2, C, max_seg, flat, o, ns);
+  sidp::plan_mlp_units(G, nks1, D, nks2, C, max_seg, MT, flat, o, ns);
   *n_units = (int32_t)flat.size();
   if ((int)flat.size() > cap) return fail(SIDP_EINVAL, "capacity %d < %zu units", cap, flat.size());
   for (size_t i = 0; i < flat.size(); ++i) {
@@ -1577,7 +1579,7 @@ sidp_status sidp_test_mlp_schedule(int32_t G, int32_t nks1, int32_t D, int32_t n
     units[4 * i + 2] = flat[i].z; units[4 * i + 3] = flat[i].w;
   }
   for (int c = 0; c <= C; ++c) off[c] = o[c];
-  for (int t = 0; t < D; ++t) nseg[t] = ns[t];
+  for (int t = 0; t < D * MT; ++t) nseg[t] = ns[t];
   return SIDP_OK;
 }
 

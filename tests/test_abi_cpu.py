@@ -107,59 +107,63 @@ def test_host_calls_need_alloc(sidp):
     c.destroy()
 
 
-@pytest.mark.parametrize("h,I,C,max_seg", [(5120, 25600, 74, 8), (8192, 28672, 74, 6),
-                                           (256, 768, 74, 8), (5120, 25600, 10, 3)])
-def test_fused_mlp_schedule_invariants(sidp, h, I, C, max_seg):
-    """Host list schedule of the fused gate/up -> down launch (no GPU): every gate/up tile runs
-    once, whole; each down tile's k-range is partitioned exactly by its units, whose segment
-    indices are 0..nseg-1; per pair all gate/up units precede its down units; and the makespan
-    under the scheduler's own cost model (k-steps, down k-step k after gate/up tile k) stays
-    within 10% of the work lower bound (or the dependency bound) for the M2/Llama shapes."""
+@pytest.mark.parametrize("h,I,C,max_seg,MT", [(5120, 25600, 74, 8, 1), (8192, 28672, 74, 6, 1),
+                                              (256, 768, 74, 8, 1), (5120, 25600, 10, 3, 1),
+                                              (5120, 25600, 74, 8, 2), (256, 768, 74, 8, 2)])
+def test_fused_mlp_schedule_invariants(sidp, h, I, C, max_seg, MT):
+    """Host list schedule of the fused gate/up -> down launch (no GPU), MT token tiles: every
+    gate/up (tile, token tile) runs once, whole; each down (tile, token tile)'s k-range is
+    partitioned exactly by its units, whose segment indices are 0..nseg-1; per pair all gate/up
+    units precede its down units; and the makespan under the scheduler's own cost model
+    (k-steps; down k-step k of token tile mt after gate/up tile (k, mt)) stays within 10% of the
+    work lower bound (or the dependency bound) for the full-size shapes."""
     import ctypes
     G, nks1, D, nks2 = I // 128, h // 128, (h + 255) // 256, I // 128
-    cap = G + D * max_seg + 8
+    cap = G * MT + D * MT * max_seg + 8
     units = (ctypes.c_int32 * (4 * cap))()
     off = (ctypes.c_int32 * (C + 1))()
-    nseg = (ctypes.c_int32 * D)()
+    nseg = (ctypes.c_int32 * (D * MT))()
     n = ctypes.c_int32()
-    sidp._abi.check(sidp._abi.lib().sidp_test_mlp_schedule(G, nks1, D, nks2, C, max_seg, units, cap,
-                                                          off, nseg, ctypes.byref(n)), "schedule")
+    sidp._abi.check(sidp._abi.lib().sidp_test_mlp_schedule(G, nks1, D, nks2, C, max_seg, MT, units,
+                                                          cap, off, nseg, ctypes.byref(n)), "schedule")
     U = [tuple(units[4 * i:4 * i + 4]) for i in range(n.value)]
-    gate = sorted(u[1] for u in U if u[0] & 0xff == 0)
-    assert gate == list(range(G)) and all(u[2:] == (0, nks1) for u in U if u[0] & 0xff == 0)
+    ph = lambda u: u[0] & 0xff
+    seg = lambda u: (u[0] >> 8) & 0xff
+    mt_ = lambda u: (u[0] >> 16) & 0xffff
+    gate = sorted((u[1], mt_(u)) for u in U if ph(u) == 0)
+    assert gate == sorted((g, m) for g in range(G) for m in range(MT))
+    assert all(u[2:] == (0, nks1) for u in U if ph(u) == 0)
     per_tile = {}
     for u in U:
-        if u[0] & 0xff == 1:
-            per_tile.setdefault(u[1], []).append((u[2], u[3], u[0] >> 8))
-    assert sorted(per_tile) == list(range(D))
-    for t, parts in per_tile.items():
+        if ph(u) == 1:
+            per_tile.setdefault((u[1], mt_(u)), []).append((u[2], u[3], seg(u)))
+    assert sorted(per_tile) == sorted((t, m) for t in range(D) for m in range(MT))
+    for (t, m), parts in per_tile.items():
         ks = sorted((a, b) for a, b, _ in parts)
         assert ks[0][0] == 0 and ks[-1][1] == nks2
         assert all(ks[i][1] == ks[i + 1][0] for i in range(len(ks) - 1))
-        assert sorted(sg for _, _, sg in parts) == list(range(len(parts))) == list(range(nseg[t]))
-        assert nseg[t] <= max_seg
-    # per pair: gate/up first, then down; simulated makespan
-    done = {}
-    free = []
+        assert sorted(sg for _, _, sg in parts) == list(range(len(parts))) == list(range(nseg[t * MT + m]))
+        assert nseg[t * MT + m] <= max_seg
+    done, free = {}, []
     for c in range(C):
         lst = U[off[c]:off[c + 1]]
-        phases = [u[0] & 0xff for u in lst]
+        phases = [ph(u) for u in lst]
         assert phases == sorted(phases)
         t = 0.0
         for u in lst:
-            if u[0] & 0xff == 0:
+            if ph(u) == 0:
                 t += nks1
-                done[u[1]] = t
+                done[(u[1], mt_(u))] = t
         free.append(t)
     end = list(free)
     for c in range(C):
         t = free[c]
         for u in U[off[c]:off[c + 1]]:
-            if u[0] & 0xff == 1:
+            if ph(u) == 1:
                 for k in range(u[2], u[3]):
-                    t = max(t, done[k]) + 1
+                    t = max(t, done[(k, mt_(u))]) + 1
         end[c] = t
-    work = G * nks1 + D * nks2
+    work = MT * (G * nks1 + D * nks2)
     bound = max(work / C, max(done.values()) + 1)
     if C == 74 and h >= 5120:
         assert max(end) <= 1.10 * bound, (max(end), bound)

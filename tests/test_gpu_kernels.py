@@ -166,7 +166,8 @@ def test_gemm_hybrid_streamk_tail(P, M, N, K):
 
 
 @pytest.mark.parametrize("M,h,I", [(8, 256, 768), (256, 1024, 3072), (200, 5120, 25600),
-                                   (256, 5120, 25600), (64, 2048, 9472)])
+                                   (256, 5120, 25600), (64, 2048, 9472), (300, 1024, 3072),
+                                   (512, 5120, 25600), (448, 2048, 5120)])
 def test_mlp_fused(P, M, h, I):
     """Fused gate/up -> down launch (SURVEY.md a10 + a11) + resid_norm, vs fp64 of the same bf16
     operands: act within bf16 rounding, xout = resid + act Wd^T and u = RMSNorm(xout) g."""
