@@ -78,6 +78,7 @@ struct GemmArgs {
   int max_ctas;                // 0 = all SMs
   const QkvEpi* qkv;           // EPI_QKV only
   int w_kbmajor;               // 1: W is k-block-major [K/64][N][64] (one 3-D TMA box per stage)
+  int x_kbmajor;               // 1: X is k-block-major [K/64][M][64] (layout experiment)
   PartialSrc* partial_out;     // EPI_PARTIAL: receives the slice geometry for the consumer
 };
 

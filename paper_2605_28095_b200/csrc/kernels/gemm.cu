@@ -620,6 +620,10 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
           if (p.trace && cluster == 0 && it < 4096) p.trace[rank * 4096 + it] = globaltimer_ns();
           mbar_wait(&empty[s], ph ^ 1);
           if (p.trace && cluster == 0 && it < 4096) p.trace[(2 + rank) * 4096 + it] = globaltimer_ns();
+          if (p.debug & 2) {   // perf experiment: MMA-only (stale stage data, no loads)
+            if (leader) mbar_arrive(&full[s]);
+            continue;
+          }
           if (leader) mbar_arrive_expect_tx(&full[s], stage_tx);
           load_a(cur.x, cur.kb, s, lbar);
           load_b(cur.x, cur.kb, s, lbar);
@@ -1469,7 +1473,12 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   const bool wkb = a.w_kbmajor != 0;   // W stored k-block-major [K/64][N][64]
   int a3d = 0, b3d = 0;
   if (sw) {
-    if (!make_tmap_2d(&tw, a.x, a.K, a.M, a.ldx, BK, WROWS)) return cudaErrorInvalidValue;
+    if (a.x_kbmajor) {
+      if (!make_tmap_kbmajor(&tw, a.x, a.K, a.M, WROWS, kps)) return cudaErrorInvalidValue;
+      a3d = 1;
+    } else if (!make_tmap_2d(&tw, a.x, a.K, a.M, a.ldx, BK, WROWS)) {
+      return cudaErrorInvalidValue;
+    }
     if (wkb) {
       if (!make_tmap_kbmajor(&tx, a.w, a.K, a.N, BNT / 2, kps)) return cudaErrorInvalidValue;
       b3d = 1;
@@ -1483,7 +1492,12 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     } else if (!make_tmap_2d(&tw, a.w, a.K, a.N, a.ldw, BK, WROWS)) {
       return cudaErrorInvalidValue;
     }
-    if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) return cudaErrorInvalidValue;
+    if (a.x_kbmajor) {
+      if (!make_tmap_kbmajor(&tx, a.x, a.K, a.M, BNT / 2, kps)) return cudaErrorInvalidValue;
+      b3d = 1;
+    } else if (!make_tmap_2d(&tx, a.x, a.K, a.M, a.ldx, BK, BNT / 2)) {
+      return cudaErrorInvalidValue;
+    }
   }
 
   KParams p;

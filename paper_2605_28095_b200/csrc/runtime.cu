@@ -1507,6 +1507,8 @@ sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ld
   a.bias = reinterpret_cast<const bf16*>(bias); a.k_splits = k_splits;
   static const int env_wkb = getenv("SIDP_TEST_GEMM_WKB") ? atoi(getenv("SIDP_TEST_GEMM_WKB")) : 0;
   a.w_kbmajor = env_wkb;   // layout experiments through the test hook only
+  static const int env_xkb = getenv("SIDP_TEST_GEMM_XKB") ? atoi(getenv("SIDP_TEST_GEMM_XKB")) : 0;
+  a.x_kbmajor = env_xkb;
   cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, counters, 1 << 16},
                                     reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm: %s", cudaGetErrorString(e));

@@ -34,6 +34,8 @@ for name in only:
     if os.environ.get("SIDP_TEST_GEMM_WKB", "0") != "0":   # k-block-major copies [K/64][N][64]
         ws = [w.view(N, K // 64, 64).transpose(0, 1).contiguous().view(N, K) for w in ws]
     x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    if os.environ.get("SIDP_TEST_GEMM_XKB", "0") != "0":   # k-block-major X [K/64][M][64]
+        x = x.view(M, K // 64, 64).transpose(0, 1).contiguous().view(M, K)
     if epi == 3:
         out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
     elif epi == 2:
