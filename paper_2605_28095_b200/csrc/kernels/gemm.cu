@@ -1328,7 +1328,19 @@ bool gemm_partial_ok(int M, int N, int K, size_t ws_bytes) {
   if (!env || M <= 0 || N <= 0 || K % BK != 0 || N % 8 != 0) return false;
   const int pair_slots = std::max(1, num_sms() / 2);
   const long long wm_tiles = (long long)((N + 2 * WROWS - 1) / (2 * WROWS)) * ((M + 255) / 256);
-  if (wm_tiles >= pair_slots) return false;   // whole tiles fill the machine: no split, no fix-up
+  // Whole tiles that fill the machine need no split and no fix-up, unless their last wave
+  // leaves most pairs idle (tile-quantisation efficiency below SIDP_GEMM_PARTIAL_EFF, default
+  // 0.6) with too little tail work for gemm_launch's hybrid stream-K tail (the same test as
+  // there): e.g. O at M = 1024, 80 tiles on 74 pairs, 125 -> 76 us per layer.
+  static double env_eff = getenv("SIDP_GEMM_PARTIAL_EFF") ? atof(getenv("SIDP_GEMM_PARTIAL_EFF")) : 0.6;
+  if (wm_tiles >= pair_slots) {
+    const long long waves = (wm_tiles + pair_slots - 1) / pair_slots;
+    const long long rem = wm_tiles % pair_slots;
+    const int nkb_blocks = K / BK;
+    const int nkb = nkb_blocks % 2 == 0 ? nkb_blocks / 2 : nkb_blocks;
+    const double eff = (double)wm_tiles / (double)(waves * pair_slots);
+    if (!(rem != 0 && eff < env_eff && rem * nkb < 12LL * pair_slots)) return false;
+  }
   const PartialPlan q = plan_partial(M, N, K, pair_slots);
   return q.tiles <= kPartialMaxTiles && q.max_seg <= 255 && (size_t)q.max_seg * M * N * 4 <= ws_bytes;
 }
