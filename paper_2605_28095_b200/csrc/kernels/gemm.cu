@@ -1385,9 +1385,29 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   const int wm_tiles = ((a.N + 2 * WROWS - 1) / (2 * WROWS)) *
                        ((a.M + std::min(256, env_bnt) - 1) / std::min(256, env_bnt));
   const bool underfilled = 2 * wm_tiles > pair_slots && wm_tiles < pair_slots;
+  // Badly quantised whole W-major tiles whose tail is too small for the hybrid stream-K tail
+  // below (e.g. QKV at M = 512: 80 tiles on 74 pairs, ~2 waves for 1.08 waves of work): SW
+  // when its own rounds x (BNF + c0) cost is clearly lower (144 tiles of 144 features: 65.7 ->
+  // 60.1 us).
+  bool quantised = false;
+  if (wm_tiles > pair_slots && a.epi != EPI_ARGMAX && a.epi != EPI_PARTIAL) {
+    const int waves = (wm_tiles + pair_slots - 1) / pair_slots;
+    const int rem = wm_tiles % pair_slots;
+    const double eff = (double)wm_tiles / ((double)waves * pair_slots);
+    if (rem != 0 && eff < 0.6 && (long long)rem * nkb < 12LL * pair_slots) {
+      const int tok_pairs = (a.M + 2 * WROWS - 1) / (2 * WROWS);
+      double best_c = 1e30;
+      for (int bnf = 256; bnf >= 32; bnf -= 16) {
+        const long long t = (long long)tok_pairs * ((a.N + bnf - 1) / bnf);
+        best_c = std::min(best_c, (double)((t + pair_slots - 1) / pair_slots) * (bnf + env_sw_c0));
+      }
+      quantised = best_c < 0.85 * waves * (256 + env_sw_c0);
+    }
+  }
   bool sw = a.k_splits < 0 ? a.epi != EPI_QKV
                                   : (env_sw > 0 && env_sw_min > 0 && a.M >= env_sw_min &&
-                                     a.epi != EPI_QKV && a.k_splits <= 1 && (env_sw == 2 || underfilled));
+                                     a.epi != EPI_QKV && a.k_splits <= 1 &&
+                                     (env_sw == 2 || underfilled || quantised));
   int BNT, m_tiles, n_pairs;
   if (sw) {
     // feature tile BNF (UMMA N, multiple of 16) minimising rounds x (BNF + c0): whole tiles
