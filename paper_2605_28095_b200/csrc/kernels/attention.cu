@@ -27,19 +27,21 @@ namespace sidp {
 namespace {
 
 // ---------------------------------------------------------------- qkv post
+// heads per warp: 5 x 8 warps = 40 heads per CTA, two CTAs per token for nq + 2 nkv = 80
+constexpr int kQkvHeadsPerWarp = 5;
 // lane l holds dims [E*l, E*l+E) of the first half and the same dims + hd/2 (its RoPE
 // partners), E = hd/64: every load and store is one E-wide vector per lane
-template <int HD>
-__global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
+template <int HD, int HPW>
+__global__ void __launch_bounds__(256, 2) qkv_post_kernel(QkvPostArgs a) {
   pdl_trigger();
   pdl_wait();
   constexpr int half = HD / 2, E = HD / 64;
-  // grid (B, ceil(nh / 8)): one warp per (token, head) so every load is issued up front
+  // grid (B, ceil(nh / (8 HPW))): each warp owns HPW (token, head) vectors and issues all their
+  // loads before any arithmetic (one warp per head left ~0.5 KB in flight per warp: at B = 1024
+  // the kernel ran at ~0.9 TB/s, latency-bound)
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nh = a.nq + 2 * a.nkv;
-  const int nwarps = (blockDim.x >> 5) * gridDim.y;
-  const int head0 = blockIdx.y * (blockDim.x >> 5) + warp;
   const int pos = a.pos[b];
   const int i0 = E * lane;
   float cs[E][2];
@@ -54,22 +56,27 @@ __global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
     }
   }
   const size_t slice = (size_t)a.part.M * a.part.N;
-  for (int head = head0; head < nh; head += nwarps) {
-    const bool is_v = head >= a.nq + a.nkv;
-    const bool is_q = head < a.nq;
-    float x1[E], x2[E];
+  float x1[HPW][E], x2[HPW][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) x1[e] = x2[e] = 0.0f;
-    auto load = [&](const float* src) {
-      if constexpr (E == 2) {
-        const float2 u = __ldcg(reinterpret_cast<const float2*>(src + i0));
-        const float2 w = __ldcg(reinterpret_cast<const float2*>(src + i0 + half));
-        x1[0] += u.x; x1[1] += u.y; x2[0] += w.x; x2[1] += w.y;
-      } else {
-        x1[0] += __ldcg(src + i0);
-        x2[0] += __ldcg(src + i0 + half);
-      }
-    };
+  for (int hh = 0; hh < HPW; ++hh) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) x1[hh][e] = x2[hh][e] = 0.0f;
+  }
+  auto load = [&](const float* src, float (&y1)[E], float (&y2)[E]) {
+    if constexpr (E == 2) {
+      const float2 u = __ldcg(reinterpret_cast<const float2*>(src + i0));
+      const float2 w = __ldcg(reinterpret_cast<const float2*>(src + i0 + half));
+      y1[0] += u.x; y1[1] += u.y; y2[0] += w.x; y2[1] += w.y;
+    } else {
+      y1[0] += __ldcg(src + i0);
+      y2[0] += __ldcg(src + i0 + half);
+    }
+  };
+  // phase 1: loads (summing partial slices in slice order when QKV left stream-K partials)
+#pragma unroll
+  for (int hh = 0; hh < HPW; ++hh) {
+    const int head = (blockIdx.y * HPW + hh) * 8 + warp;
+    if (head >= nh) continue;
     if (a.part.ws) {
       // deferred stream-K fix-up: a head lies inside one 256-feature tile (hd divides 256),
       // so its partial slices are summed in slice order, then the bias is added
@@ -78,38 +85,46 @@ __global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
       const float* src = a.part.ws + (size_t)b * a.part.N + n;
 #pragma unroll
       for (int sgi = 0; sgi < 4; ++sgi)   // issued together (predicated), summed in order
-        if (sgi < nseg) load(src + sgi * slice);
-      for (int sgi = 4; sgi < nseg; ++sgi) load(src + sgi * slice);
+        if (sgi < nseg) load(src + sgi * slice, x1[hh], x2[hh]);
+      for (int sgi = 4; sgi < nseg; ++sgi) load(src + sgi * slice, x1[hh], x2[hh]);
       if (a.bias) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          x1[e] += bf16_to_f(a.bias[n + i0 + e]);
-          x2[e] += bf16_to_f(a.bias[n + i0 + e + half]);
+          x1[hh][e] += bf16_to_f(a.bias[n + i0 + e]);
+          x2[hh][e] += bf16_to_f(a.bias[n + i0 + e + half]);
         }
       }
     } else {
-      load(a.qkv + ((size_t)b * nh + head) * HD);
+      load(a.qkv + ((size_t)b * nh + head) * HD, x1[hh], x2[hh]);
     }
+  }
+  // phase 2: qk-norm, RoPE, stores
+#pragma unroll
+  for (int hh = 0; hh < HPW; ++hh) {
+    const int head = (blockIdx.y * HPW + hh) * 8 + warp;
+    if (head >= nh) continue;
+    const bool is_v = head >= a.nq + a.nkv;
+    const bool is_q = head < a.nq;
     if (!is_v) {
       const bf16* gain = is_q ? a.gq : a.gk;
       if (gain) {
         float ss = 0.0f;
 #pragma unroll
-        for (int e = 0; e < E; ++e) ss += x1[e] * x1[e] + x2[e] * x2[e];
+        for (int e = 0; e < E; ++e) ss += x1[hh][e] * x1[hh][e] + x2[hh][e] * x2[hh][e];
         ss = warp_sum(ss);
         const float r = rsqrtf(ss / (float)HD + a.eps);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          x1[e] = x1[e] * r * bf16_to_f(gain[i0 + e]);
-          x2[e] = x2[e] * r * bf16_to_f(gain[i0 + e + half]);
+          x1[hh][e] = x1[hh][e] * r * bf16_to_f(gain[i0 + e]);
+          x2[hh][e] = x2[hh][e] * r * bf16_to_f(gain[i0 + e + half]);
         }
       }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const float y1 = x1[e] * cs[e][0] - x2[e] * cs[e][1];
-        const float y2 = x2[e] * cs[e][0] + x1[e] * cs[e][1];
-        x1[e] = y1;
-        x2[e] = y2;
+        const float y1 = x1[hh][e] * cs[e][0] - x2[hh][e] * cs[e][1];
+        const float y2 = x2[hh][e] * cs[e][0] + x1[hh][e] * cs[e][1];
+        x1[hh][e] = y1;
+        x2[hh][e] = y2;
       }
     }
     bf16* dst;
@@ -121,11 +136,11 @@ __global__ void __launch_bounds__(256) qkv_post_kernel(QkvPostArgs a) {
       dst = cache + (((size_t)b * a.nkv + g) * a.smax + pos) * HD;
     }
     if constexpr (E == 2) {
-      *reinterpret_cast<__nv_bfloat162*>(dst + i0) = __floats2bfloat162_rn(x1[0], x1[1]);
-      *reinterpret_cast<__nv_bfloat162*>(dst + i0 + half) = __floats2bfloat162_rn(x2[0], x2[1]);
+      *reinterpret_cast<__nv_bfloat162*>(dst + i0) = __floats2bfloat162_rn(x1[hh][0], x1[hh][1]);
+      *reinterpret_cast<__nv_bfloat162*>(dst + i0 + half) = __floats2bfloat162_rn(x2[hh][0], x2[hh][1]);
     } else {
-      dst[i0] = f_to_bf16(x1[0]);
-      dst[i0 + half] = f_to_bf16(x2[0]);
+      dst[i0] = f_to_bf16(x1[hh][0]);
+      dst[i0 + half] = f_to_bf16(x2[hh][0]);
     }
   }
 }
@@ -578,8 +593,10 @@ cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s) {
   if (a.B <= 0) return cudaSuccess;
   if (a.hd != 64 && a.hd != 128) return cudaErrorInvalidValue;
   const int nh = a.nq + 2 * a.nkv;
-  if (a.hd == 128) return launch_pdl(qkv_post_kernel<128>, dim3(a.B, (nh + 7) / 8), dim3(256), 0, s, a);
-  return launch_pdl(qkv_post_kernel<64>, dim3(a.B, (nh + 7) / 8), dim3(256), 0, s, a);
+  constexpr int HPW = kQkvHeadsPerWarp;
+  const dim3 grid(a.B, (nh + 8 * HPW - 1) / (8 * HPW));
+  if (a.hd == 128) return launch_pdl(qkv_post_kernel<128, HPW>, grid, dim3(256), 0, s, a);
+  return launch_pdl(qkv_post_kernel<64, HPW>, grid, dim3(256), 0, s, a);
 }
 
 int attention_last_launch_count() { return g_attn_launches; }
@@ -653,8 +670,8 @@ cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
 cudaError_t attention_preload() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaSuccess;
-  if (cudaFuncGetAttributes(&fa, qkv_post_kernel<128>) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, qkv_post_kernel<64>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, qkv_post_kernel<128, kQkvHeadsPerWarp>) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, qkv_post_kernel<64, kQkvHeadsPerWarp>) != cudaSuccess) e = cudaGetLastError();
 #define SIDP_PRELOAD_ATTN(hd, st) \
   if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError();
   SIDP_PRELOAD_ATTN(128, 2) SIDP_PRELOAD_ATTN(128, 3) SIDP_PRELOAD_ATTN(128, 4)
