@@ -833,6 +833,9 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
   const int n_out = EPI == EPI_SILU_MUL ? p.N / 2 : p.N;
   const int vec_per_row = tile_out / 8;
   const size_t slice = (size_t)p.M * p.N;
+  // compact slot of segment s: 0 when its cluster's range starts inside this tile — every
+  // s > 0 — else 1 (the first cluster's range began in an earlier tile and ends here)
+  const int slot0 = p.compact && range_begin(first, p.total_kb, p.clusters) < (long long)tl * nkb ? 1 : 0;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < rows * vec_per_row;
        idx += gridDim.x * blockDim.x) {
     const int m = m0 + idx / vec_per_row;
@@ -854,7 +857,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
       const float* src = base + s * slice;
       if (p.compact) {
         const int cs = first + s;
-        const int slot = range_begin(cs, p.total_kb, p.clusters) >= (long long)tl * nkb ? 0 : 1;
+        const int slot = s == 0 ? slot0 : 0;
         src = p.ws + ((size_t)cs * 2 + slot) * (size_t)(2 * WROWS) * p.BNT +
               (size_t)(m - m0) * (2 * WROWS) - (size_t)ft * 2 * WROWS;
       }
