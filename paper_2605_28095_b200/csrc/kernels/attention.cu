@@ -197,6 +197,7 @@ struct AttnParams {
   int B, nq, nkv, smax;
   int pair_mode;             // grid == B * nkv: one whole (b, g) pair per CTA
   int kv_evict;              // K/V loads carry an L2 evict-first policy
+  int pre_wait;              // pair mode: first ring chunks requested before the PDL wait
   float scale_log2;
 };
 
@@ -226,8 +227,46 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
   constexpr int TILE = kChunk * HD;                   // elements per K (or V) chunk
   constexpr size_t kRingBytes = (size_t)kWarps * ST * 2 * TILE * 2;   // ST-stage ring per warp
   pdl_trigger();
-  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Pair mode: the first ST-1 ring chunks of this warp hold only context tokens written by
+  // earlier steps (never by the preceding qkv_post, which appends token pos_b), so they are
+  // requested before griddepcontrol.wait and stream while qkv_post finishes.  pos_b read here
+  // may be one step stale (pos_b - 1): only tokens below it are touched, all complete, and the
+  // chunk ids do not depend on pos_b.  SIDP_ATTN_PRE=0 disables.
+  bool pre = false;
+  if (p.pair_mode && p.pre_wait) {
+    const int b0 = blockIdx.x / p.nkv, g0 = blockIdx.x % p.nkv;
+    const int pos_pre = p.pos[b0];
+    if ((warp + (ST - 2) * kWarps + 1) * kChunk <= pos_pre) {
+      const bf16* kb0 = p.kc + ((size_t)b0 * p.nkv + g0) * p.smax * HD;
+      const bf16* vb0 = p.vc + ((size_t)b0 * p.nkv + g0) * p.smax * HD;
+      bf16* wb = reinterpret_cast<bf16*>(smem) + (size_t)warp * ST * 2 * TILE;
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+      for (int j = 0; j < ST - 1; ++j) {
+        const int t0 = (warp + j * kWarps) * kChunk;
+        bf16* sk = wb + j * 2 * TILE;
+        bf16* sv = sk + TILE;
+#pragma unroll
+        for (int it = 0; it < (kChunk * CPR) / 32; ++it) {
+          const int e = it * 32 + lane;
+          const int row = e / CPR, cc = e % CPR;
+          const int sw = (cc ^ (row & 7));
+          if (p.kv_evict) {
+            cp_async16_ef(sk + row * HD + sw * 8, kb0 + (size_t)(t0 + row) * HD + cc * 8, pol);
+            cp_async16_ef(sv + row * HD + sw * 8, vb0 + (size_t)(t0 + row) * HD + cc * 8, pol);
+          } else {
+            cp_async16(sk + row * HD + sw * 8, kb0 + (size_t)(t0 + row) * HD + cc * 8);
+            cp_async16(sv + row * HD + sw * 8, vb0 + (size_t)(t0 + row) * HD + cc * 8);
+          }
+        }
+        cp_async_commit();
+      }
+      pre = true;
+    }
+  }
+  pdl_wait();
   const int gid = lane >> 2, tq = lane & 3;
   const int G = p.nq / p.nkv;
   const int C = gridDim.x, cta = blockIdx.x;
@@ -344,11 +383,14 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
       }
     };
 
-    // ST-1 chunks in flight per warp ahead of the one being consumed
+    // ST-1 chunks in flight per warp ahead of the one being consumed (already requested
+    // before the PDL wait when pre)
+    if (!pre) {
 #pragma unroll
-    for (int j = 0; j < ST - 1; ++j) {
-      if (lo + warp + j * kWarps < hi) load_chunk(j, lo + warp + j * kWarps);
-      cp_async_commit();
+      for (int j = 0; j < ST - 1; ++j) {
+        if (lo + warp + j * kWarps < hi) load_chunk(j, lo + warp + j * kWarps);
+        cp_async_commit();
+      }
     }
     int it = 0;
     for (int ch = lo + warp; ch < hi; ch += kWarps, ++it) {
@@ -640,6 +682,8 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
   static const int env_evict = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
   p.kv_evict = env_evict;
+  static const int env_pre = getenv("SIDP_ATTN_PRE") ? atoi(getenv("SIDP_ATTN_PRE")) : 1;
+  p.pre_wait = env_pre;
   p.pair_mode = (long long)ctas == pairs ? 1 : 0;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
   return launch_pdl(attn_kernel<HD, ST>, dim3(ctas), dim3(128), smem, s, p);
