@@ -665,11 +665,14 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   // pairs into pieces (split-KV) with >= 8 chunks per CTA at the host's context bound.
   const long long pairs = (long long)a.B * a.nkv;
   const long long slots = (long long)g_sms * per_sm;
-  // Many SHORT pairs (< 16 chunks each at the context bound, e.g. B = 1536 at 32 tokens): one
-  // wave of CTAs walking contiguous chunk ranges instead of one CTA per pair — measured 254-260
-  // vs 326 us per layer at B = 1536, S_ctx = 32 (the per-CTA launch and prologue dominated)
+  // Many pairs of < 64 chunks each at the context bound: one wave of CTAs walking contiguous
+  // chunk ranges instead of one CTA per pair (the per-CTA launch, prologue and warp merge
+  // dominated).  Measured per layer, pair mode vs one wave: B = 1024 / S_ctx = 256 (17 chunks)
+  // 414 vs 307 us; B = 768 / 512 430 vs 323; B = 512 / 768 389 vs 293; B = 256 / 1024
+  // (65 chunks) 194-197 vs 190-191, step equal; B = 128 / 2048 177 vs 190; B = 64 / 4096
+  // 170 vs 185 (long pairs keep pair mode); B = 1536 / 32 326 vs 254-260.
   const long long chunks_per_pair = (max_tok + kChunk - 1) / kChunk;
-  long long cl = pairs >= slots ? (chunks_per_pair >= 16 ? pairs : slots)
+  long long cl = pairs >= slots ? (chunks_per_pair >= 64 ? pairs : slots)
                                 : std::min(slots, std::max<long long>(1, w_max / 8));
   int ctas = (int)cl;
   static const int env_ctas = getenv("SIDP_ATTN_CTAS") ? atoi(getenv("SIDP_ATTN_CTAS")) : 0;
