@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--slots", type=int, default=None)
     ap.add_argument("--order", default="exec", choices=["exec", "paper"])
     ap.add_argument("--pool", default="layer", choices=["layer", "ffn"])
-    ap.add_argument("--fetch", default="sm", choices=["sm", "ce"])
+    ap.add_argument("--fetch", default="ce", choices=["sm", "ce"],
+                    help="WaS fetch engine: copy engine (default; the SM-fetch kernel slows the concurrent compute kernels ~1.5x, DESIGN.md §12) or SM copy kernel")
     ap.add_argument("--fetch-sms", type=int, default=48)
     ap.add_argument("--no-stagger", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -497,8 +497,11 @@ sidp_status enqueue_fetch(sidp_ctx* ctx) {
   const size_t bytes = ctx->pooled_elems * 2;
   timing_begin(ctx, 3, ctx->fetch_stream);
   if (ctx->c.fetch_engine == SIDP_FETCH_CE && ctx->c.fetch_pace_gbps > 0.0f) {
-    // emulation only: 16 MB copy-engine chunks released at the paced rate
-    const size_t chunk = (size_t)16 << 20;
+    // emulation only: copy-engine chunks (SIDP_CE_CHUNK_MB, default 16) released at the paced rate
+    // (SIDP_CE_CHUNK_MB, default 64); a last pace point holds the layer's completion (and so its
+    // ready flag) until bytes / rate after the start, so bursts never beat the emulated link
+    static const size_t chunk_mb = getenv("SIDP_CE_CHUNK_MB") ? std::max(1, atoi(getenv("SIDP_CE_CHUNK_MB"))) : 64;
+    const size_t chunk = chunk_mb << 20;
     for (size_t off = 0, i = 0; off < bytes; off += chunk, ++i) {
       CK(sidp::pace_launch(ctx->pace_t0, i == 0, (uint64_t)((double)off / ctx->c.fetch_pace_gbps),
                            ctx->fetch_stream));
@@ -506,6 +509,8 @@ sidp_status enqueue_fetch(sidp_ctx* ctx) {
                          reinterpret_cast<const uint8_t*>(src) + off, std::min(chunk, bytes - off),
                          cudaMemcpyDefault, ctx->fetch_stream));
     }
+    CK(sidp::pace_launch(ctx->pace_t0, 0, (uint64_t)((double)bytes / ctx->c.fetch_pace_gbps),
+                         ctx->fetch_stream));
   } else if (ctx->c.fetch_engine == SIDP_FETCH_CE) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
   } else {
