@@ -263,9 +263,10 @@ def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms, remote_bytes=None):
 def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, peaks):
     """Rank 0 of a W-rank WaS group on ONE GPU (SURVEY.md §8(a) a2-a4 at full size): the W-1
     other owners are serve-only contexts (sidp_alloc_serve_only) whose arenas sit in this GPU's
-    HBM, so the fetch kernel reads local HBM instead of a peer over NVLink.  It runs on the real
-    run's 48 CTAs but paces itself (sidp_config.fetch_pace_gbps) to the NVLink 5 reader rate,
-    770 GB/s, which local HBM would otherwise exceed ~4x; HBM traffic equals a real rank's (its
+    HBM, so the fetch reads local HBM instead of a peer over NVLink: on the copy engine by
+    default (--fetch ce: 64 MB chunks), or the SM fetch kernel on --emulate-fetch-sms CTAs
+    (--fetch sm), paced (sidp_config.fetch_pace_gbps) to the NVLink 5 reader rate, 770 GB/s,
+    which local HBM would otherwise exceed ~4x; HBM traffic equals a real rank's (its
     slot writes + one owner's serve reads under the stagger).  Not a multi-GPU number: NVLink
     latency and the other ranks' compute are absent."""
     import numpy as np
