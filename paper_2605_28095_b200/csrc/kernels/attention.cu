@@ -204,6 +204,81 @@ struct AttnParams {
 constexpr int kChunk = 16;
 constexpr int kWarps = 4;
 
+// One 16-token K/V chunk of a (sequence, kv head) pair for one warp: S = Q K^T (mma.sync),
+// masked online softmax in the exp2 domain (rows gid and gid + 8), O += P V.
+template <int HD>
+__device__ __forceinline__ void attn_chunk(const uint32_t (&qa)[HD / 16][4], uint32_t skb,
+                                           uint32_t svb, int t0, int n_tok, float scale_log2,
+                                           float (&o)[HD / 8][4], float (&mrow)[2],
+                                           float (&lrow)[2], int lane) {
+  const int tq = lane & 3;
+  // S = Q K^T for 16 tokens (two n-tiles of 8)
+  float sc[2][4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int mat = lane >> 3, r = lane & 7;
+    const int tok = (mat >> 1) * 8 + r;
+    const int cc = kk * 2 + (mat & 1);
+    uint32_t b0, b1, b2, b3;
+    ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
+    mma_bf16(sc[0], qa[kk], b0, b1);
+    mma_bf16(sc[1], qa[kk], b2, b3);
+  }
+  // mask + online softmax (rows gid and gid+8)
+  float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int tok = t0 + j * 8 + 2 * tq + (e & 1);
+      sc[j][e] = tok < n_tok ? sc[j][e] * scale_log2 : -INFINITY;
+      mx[e >> 1] = fmaxf(mx[e >> 1], sc[j][e]);
+    }
+  float alpha[2], muse[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
+    const float mnew = fmaxf(mrow[h], mx[h]);
+    muse[h] = mnew == -INFINITY ? 0.0f : mnew;
+    alpha[h] = exp2f(mrow[h] - muse[h]);
+    mrow[h] = mnew;
+    lrow[h] *= alpha[h];
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      sc[j][e] = exp2f(sc[j][e] - muse[e >> 1]);
+      lrow[e >> 1] += sc[j][e];
+    }
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    o[i][0] *= alpha[0];
+    o[i][1] *= alpha[0];
+    o[i][2] *= alpha[1];
+    o[i][3] *= alpha[1];
+  }
+  uint32_t pa[4];
+  pa[0] = pack_bf16(sc[0][0], sc[0][1]);
+  pa[1] = pack_bf16(sc[0][2], sc[0][3]);
+  pa[2] = pack_bf16(sc[1][0], sc[1][1]);
+  pa[3] = pack_bf16(sc[1][2], sc[1][3]);
+  // O += P V
+#pragma unroll
+  for (int dn = 0; dn < HD / 8; dn += 2) {
+    const int mat = lane >> 3, r = lane & 7;
+    const int tok = (mat & 1) * 8 + r;
+    const int cc = dn + (mat >> 1);
+    uint32_t b0, b1, b2, b3;
+    ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
+    mma_bf16(o[dn], pa, b0, b1);
+    mma_bf16(o[dn + 1], pa, b2, b3);
+  }
+}
+
 // CTA owning global chunk index c when W chunks are split into C ranges [floor(iW/C), ...)
 __device__ __forceinline__ int cta_of_chunk(long long c, long long W, int C) {
   return (int)(((c + 1) * (long long)C + W - 1) / W) - 1;
@@ -404,71 +479,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
       const uint32_t skb = smem_u32(sk), svb = smem_u32(sv);
       const int t0 = ch * kChunk;
 
-      // S = Q K^T for 16 tokens (two n-tiles of 8)
-      float sc[2][4];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.0f;
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const int mat = lane >> 3, r = lane & 7;
-        const int tok = (mat >> 1) * 8 + r;
-        const int cc = kk * 2 + (mat & 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
-        mma_bf16(sc[0], qa[kk], b0, b1);
-        mma_bf16(sc[1], qa[kk], b2, b3);
-      }
-      // mask + online softmax (rows gid and gid+8)
-      float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int tok = t0 + j * 8 + 2 * tq + (e & 1);
-          sc[j][e] = tok < n_tok ? sc[j][e] * p.scale_log2 : -INFINITY;
-          mx[e >> 1] = fmaxf(mx[e >> 1], sc[j][e]);
-        }
-      float alpha[2], muse[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-        const float mnew = fmaxf(mrow[h], mx[h]);
-        muse[h] = mnew == -INFINITY ? 0.0f : mnew;
-        alpha[h] = exp2f(mrow[h] - muse[h]);
-        mrow[h] = mnew;
-        lrow[h] *= alpha[h];
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          sc[j][e] = exp2f(sc[j][e] - muse[e >> 1]);
-          lrow[e >> 1] += sc[j][e];
-        }
-#pragma unroll
-      for (int i = 0; i < HD / 8; ++i) {
-        o[i][0] *= alpha[0];
-        o[i][1] *= alpha[0];
-        o[i][2] *= alpha[1];
-        o[i][3] *= alpha[1];
-      }
-      uint32_t pa[4];
-      pa[0] = pack_bf16(sc[0][0], sc[0][1]);
-      pa[1] = pack_bf16(sc[0][2], sc[0][3]);
-      pa[2] = pack_bf16(sc[1][0], sc[1][1]);
-      pa[3] = pack_bf16(sc[1][2], sc[1][3]);
-      // O += P V
-#pragma unroll
-      for (int dn = 0; dn < HD / 8; dn += 2) {
-        const int mat = lane >> 3, r = lane & 7;
-        const int tok = (mat & 1) * 8 + r;
-        const int cc = dn + (mat >> 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, b0, b1, b2, b3);
-        mma_bf16(o[dn], pa, b0, b1);
-        mma_bf16(o[dn + 1], pa, b2, b3);
-      }
+      attn_chunk<HD>(qa, skb, svb, t0, n_tok, p.scale_log2, o, mrow, lrow, lane);
       __syncwarp();
     }
     cp_async_wait<0>();
@@ -626,6 +637,106 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
   }
 }
 
+// Warp-per-pair decode attention for many SHORT pairs: each warp owns whole (sequence, kv
+// head) pairs (strided over the grid's warps), streams the pair's chunks through its own
+// ST-stage ring and normalises and stores o itself — no cross-warp merge, no CTA barrier, so
+// one warp's per-pair prologue (q load, first chunks) overlaps the other warps' streaming.
+template <int HD, int ST>
+__global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int CPR = HD / 8;
+  constexpr int TILE = kChunk * HD;
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tq = lane & 3;
+  const int G = p.nq / p.nkv;
+  const int pairs = p.B * p.nkv;
+  bf16* wbuf = reinterpret_cast<bf16*>(smem) + (size_t)warp * ST * 2 * TILE;
+  uint64_t kvpol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kvpol));
+  for (int pr = blockIdx.x * kWarps + warp; pr < pairs; pr += gridDim.x * kWarps) {
+    const int b = pr / p.nkv, g = pr % p.nkv;
+    const int n_tok = p.pos[b] + 1;
+    const int chb = (p.pos[b] + kChunk) / kChunk;
+    const bf16* kbase = p.kc + ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* vbase = p.vc + ((size_t)b * p.nkv + g) * p.smax * HD;
+    auto load_chunk = [&](int stage, int ch) {
+      const int t0 = ch * kChunk;
+      bf16* sk = wbuf + stage * 2 * TILE;
+      bf16* sv = sk + TILE;
+#pragma unroll
+      for (int it = 0; it < (kChunk * CPR) / 32; ++it) {
+        const int e = it * 32 + lane;
+        const int row = e / CPR, cc = e % CPR;
+        const int t = min(t0 + row, n_tok - 1);
+        const int sw = (cc ^ (row & 7));
+        if (p.kv_evict) {
+          cp_async16_ef(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8, kvpol);
+          cp_async16_ef(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8, kvpol);
+        } else {
+          cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
+          cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+        }
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < ST - 1; ++j) {
+      if (j < chb) load_chunk(j, j);
+      cp_async_commit();
+    }
+    uint32_t qa[HD / 16][4];
+    {
+      const bf16* qb = p.q + ((size_t)b * p.nq + (size_t)g * G) * HD;
+      const int r0 = gid, r1 = gid + 8;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int cc = kk * 16 + 2 * tq;
+        qa[kk][0] = r0 < G ? *reinterpret_cast<const uint32_t*>(qb + r0 * HD + cc) : 0u;
+        qa[kk][1] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + cc) : 0u;
+        qa[kk][2] = r0 < G ? *reinterpret_cast<const uint32_t*>(qb + r0 * HD + cc + 8) : 0u;
+        qa[kk][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + cc + 8) : 0u;
+      }
+    }
+    float o[HD / 8][4];
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+    float mrow[2] = {-INFINITY, -INFINITY};
+    float lrow[2] = {0.0f, 0.0f};
+    for (int ch = 0; ch < chb; ++ch) {
+      const int cn = ch + ST - 1;
+      if (cn < chb) load_chunk(cn % ST, cn);
+      cp_async_commit();
+      cp_async_wait<ST - 1>();
+      __syncwarp();
+      const bf16* sk = wbuf + (ch % ST) * 2 * TILE;
+      attn_chunk<HD>(qa, smem_u32(sk), smem_u32(sk + TILE), ch * kChunk, n_tok, p.scale_log2, o,
+                     mrow, lrow, lane);
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
+      lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = gid + 8 * h;
+      if (row < G) {
+        const float L = lrow[h];
+        bf16* dst = p.o + ((size_t)b * p.nq + g * G + row) * HD + 2 * tq;
+#pragma unroll
+        for (int dn = 0; dn < HD / 8; ++dn)
+          *reinterpret_cast<__nv_bfloat162*>(dst + dn * 8) =
+              __floats2bfloat162_rn(L > 0.0f ? o[dn][2 * h] / L : 0.0f,
+                                    L > 0.0f ? o[dn][2 * h + 1] / L : 0.0f);
+      }
+    }
+  }
+}
+
 int g_sms = 0;
 thread_local int g_attn_launches = 0;
 
@@ -674,6 +785,29 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   const long long chunks_per_pair = (max_tok + kChunk - 1) / kChunk;
   long long cl = pairs >= slots ? (chunks_per_pair >= 64 ? pairs : slots)
                                 : std::min(slots, std::max<long long>(1, w_max / 8));
+  // Many pairs of < SIDP_ATTN_WARP_CH (default 128) chunks: warp-per-pair kernel, one wave
+  // (B = 1024 / S_ctx = 256: 301 -> 185 us; 768 / 512: 322 -> 277; 512 / 768: 290 -> 259;
+  // M2, 65 chunks: step 29.52-29.63 -> 29.29-29.34 ms; B = 128 / 2048 equal)
+  static const int env_warp_ch = getenv("SIDP_ATTN_WARP_CH") ? atoi(getenv("SIDP_ATTN_WARP_CH")) : 128;
+  if (pairs >= slots && chunks_per_pair < env_warp_ch) {
+    static bool wattr = false;
+    if (!wattr) {
+      cudaFuncSetAttribute(attn_warp_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      wattr = true;
+    }
+    int wper = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, attn_warp_kernel<HD, ST>, 128, ring);
+    const long long wslots = (long long)g_sms * std::max(1, wper);
+    const int wctas = (int)std::min<long long>(wslots, (pairs + kWarps - 1) / kWarps);
+    AttnParams p{};
+    p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws; p.cnt = a.cnt;
+    p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
+    static const int env_evict_w = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
+    p.kv_evict = env_evict_w;
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
+    return launch_pdl(attn_warp_kernel<HD, ST>, dim3(wctas), dim3(128), ring, s, p);
+  }
   int ctas = (int)cl;
   static const int env_ctas = getenv("SIDP_ATTN_CTAS") ? atoi(getenv("SIDP_ATTN_CTAS")) : 0;
   if (env_ctas > 0) ctas = env_ctas;   // perf experiments

@@ -344,14 +344,15 @@ def test_cuda_graph_replay_matches_eager(P):
                                               ("tiny-qwen3", 2, 2000, 100),
                                               ("tiny", 40, 0, 1500), ("tiny-qwen3", 12, 0, 3000),
                                               ("tiny", 240, 0, 300),
-                                              ("tiny", 200, 0, 60), ("tiny-qwen3", 160, 20, 40)])
+                                              ("tiny", 200, 0, 60), ("tiny-qwen3", 160, 20, 40),
+                                              ("tiny", 300, 0, 400), ("tiny-qwen3", 320, 100, 300)])
 def test_long_context_split_kv(P, name, B, ctx, span):
     """Attention work balancing: the batch's 16-token chunks are split evenly over the CTAs, so
     small batches with long contexts split (b, kv head) pairs into pieces merged by the last
     arriving piece (split-KV), and ragged context lengths (uniform 0..span) put piece
     boundaries anywhere, including pairs of one chunk and pairs split over many CTAs.  The last
-    two cases have many short pairs (>= one wave of pairs, < 16 chunks each): one wave of CTAs
-    walks contiguous chunk ranges over many pairs."""
+    cases have many short pairs (>= one wave of pairs, < 32 chunks each at the context bound):
+    the warp-per-pair kernel, each warp finishing whole pairs of ragged lengths."""
     m = MODELS[name]
     max_ctx = ctx + span + 8
     R = Rank(P, m, B=B, ctx=ctx, span=span, max_ctx=max_ctx)
