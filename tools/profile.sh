@@ -7,7 +7,7 @@ B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --emulate-wor
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 6000 --csv \
    --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
 S="python bench.py --steps 1 --warmup 3 --layers 4 --no-e2e --no-cpu-baseline --emulate-world 0"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 8 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"attn_(warp_)?kernel" -s 8 -c 1 \
    -o gpurun_out/prof_attn -f $S > gpurun_out/ncu_attn.log 2>&1
 # one decoder layer's GEMMs (qkv, o, gate/up, down) after the warm-up layers, then the LM head
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"gemm2_kernel|mlp2_kernel" -s 24 -c 4 \
