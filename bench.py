@@ -172,10 +172,15 @@ def oracle_sample(m, seed, rows, ctx_len, timed_iters=1):
 
 
 # ----------------------------------------------------------------------------- roofline
-def kernel_work(cls, m, B, ctx_avg, layer_bytes):
-    """Algorithmic (flops, bytes) per launch of a kernel class."""
+def kernel_work(cls, m, B, ctx_avg, layer_bytes, fused_mlp=False):
+    """Algorithmic (flops, bytes) per launch of a kernel class.  Class 1 with
+    fused_mlp is the fused gate/up -> down launch (mlp2_kernel): gate/up plus down work, the act
+    tile written and read once, the fp32 down output slice written once."""
     h, I, V = m.hidden, m.intermediate, m.vocab
     q, kvd = m.q_dim, m.kv_dim
+    if cls == 1 and fused_mlp:
+        return (2.0 * B * 2 * I * h + 2.0 * B * h * I,
+                2.0 * (3 * I * h + B * h + 2 * B * I) + 4.0 * B * h)
     if cls == 1:
         return 2.0 * B * 2 * I * h, 2.0 * (2 * I * h + B * h + B * I)
     if cls == 4:
@@ -194,8 +199,8 @@ def kernel_work(cls, m, B, ctx_avg, layer_bytes):
     raise ValueError(cls)
 
 
-def roofline_entry(cls, m, B, ctx_avg, layer_bytes, avg_ms, peaks, traffic=None):
-    flops, byts = kernel_work(cls, m, B, ctx_avg, layer_bytes)
+def roofline_entry(cls, m, B, ctx_avg, layer_bytes, avg_ms, peaks, traffic=None, fused_mlp=False):
+    flops, byts = kernel_work(cls, m, B, ctx_avg, layer_bytes, fused_mlp)
     t_tensor = flops / (peaks["tflops"] * 1e12) if flops else 0.0
     t_hbm = byts / (peaks["hbm"] * 1e9)
     if cls == 3:
@@ -666,8 +671,10 @@ def main():
         return
 
     peaks = load_peaks()
+    # the gate/up class is the fused gate/up -> down launch when no separate down GEMM ran
+    fused_mlp = shares[1] > 0 and shares[4] == 0
     roof = roofline_entry(dom, m, B, ctx_avg, st["layer_bytes"], dom_ms, peaks,
-                          load_traffic(wl.id, dom))
+                          load_traffic(wl.id, dom), fused_mlp=fused_mlp)
     roof["avg_launch_ms"] = dom_ms
     roof["launches_timed"] = st["timed_launches"][dom]
     roof["peak_source"] = peaks["source"] + (" (sustained bf16)" if roof["unit"] == "TFLOP/s" else "")

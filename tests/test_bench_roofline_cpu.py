@@ -39,3 +39,16 @@ def test_remote_bytes_override_and_kernel_work():
     fl, by = bench.kernel_work(2, m, 256, 1024, 0)
     assert by == pytest.approx(2.0 * 2 * m.kv_dim * 256 * 1025 + 2.0 * 2 * 256 * m.q_dim)
     assert fl == pytest.approx(4.0 * m.n_q_heads * m.head_dim * 256 * 1025)
+
+
+def test_fused_mlp_kernel_work():
+    """The fused gate/up -> down launch (mlp2_kernel) is charged both GEMMs' work: 2 B (2I) h +
+    2 B h I flops (Qwen3-32B at B = 256: 201.3 GFLOP) and the three weight matrices once."""
+    m = MODELS["qwen3-32b"]
+    B, h, I = 256, m.hidden, m.intermediate
+    fl, by = bench.kernel_work(1, m, B, 0, 0, fused_mlp=True)
+    fl_gu, _ = bench.kernel_work(1, m, B, 0, 0)
+    fl_d, _ = bench.kernel_work(4, m, B, 0, 0)
+    assert fl == pytest.approx(fl_gu + fl_d)
+    assert fl == pytest.approx(201.3e9, rel=1e-3)
+    assert by >= 2.0 * 3 * I * h and by < 2.0 * 3 * I * h * 1.02
