@@ -51,4 +51,5 @@ def test_fused_mlp_kernel_work():
     fl_d, _ = bench.kernel_work(4, m, B, 0, 0)
     assert fl == pytest.approx(fl_gu + fl_d)
     assert fl == pytest.approx(201.3e9, rel=1e-3)
-    assert by >= 2.0 * 3 * I * h and by < 2.0 * 3 * I * h * 1.02
+    # + the act tile written and read once (B I bf16 x 2, 3.3% at B = 256), x in, fp32 slice out
+    assert by >= 2.0 * 3 * I * h and by < 2.0 * 3 * I * h * 1.05
