@@ -45,9 +45,11 @@ def parse():
     ap.add_argument("--slots", type=int, default=None)
     ap.add_argument("--order", default="exec", choices=["exec", "paper"])
     ap.add_argument("--pool", default="layer", choices=["layer", "ffn"])
-    ap.add_argument("--fetch", default="ce", choices=["sm", "ce"],
-                    help="WaS fetch engine: copy engine (default; the SM-fetch kernel slows the concurrent compute kernels ~1.5x, DESIGN.md §12) or SM copy kernel")
-    ap.add_argument("--fetch-sms", type=int, default=48)
+    ap.add_argument("--fetch", default="sm", choices=["sm", "ce"],
+                    help="WaS fetch engine: the SM fetch kernel (default: TMA bulk copies on "
+                         "--fetch-sms dedicated SMs, device epoch flags) or the copy engine + CUDA "
+                         "events (the paper's mechanism, A/B baseline)")
+    ap.add_argument("--fetch-sms", type=int, default=16)
     ap.add_argument("--no-stagger", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -55,8 +57,8 @@ def parse():
     ap.add_argument("--emulate-world", type=int, default=8,
                     help="N=1 only: also time rank 0 of a d-rank WaS group on this GPU, the d-1 "
                          "owners being serve-only contexts in local HBM (0 = off)")
-    ap.add_argument("--emulate-fetch-sms", type=int, default=48,
-                    help="fetch CTAs of the emulated rank (the real-run default, 48)")
+    ap.add_argument("--emulate-fetch-sms", type=int, default=16,
+                    help="SMs the emulated rank's fetch kernel holds (the real-run default, 16)")
     ap.add_argument("--emulate-pace-gbps", type=float, default=770.0,
                     help="the emulated rank's fetch kernel paces itself to this rate: the NVLink 5 "
                          "reader rate (B200_PROFILING.md measured peer copy); 0 = unpaced")
@@ -325,6 +327,11 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
         n_f = st["timed_launches"][3] - st0["timed_launches"][3]
         f_ms = (st["timed_ms"][3] - st0["timed_ms"][3]) / max(1, n_f)
         lb = st["layer_bytes"]
+        trace = ctx0.fetch_trace() if args.fetch == "sm" else []
+        if trace:   # device log: first fetch CTA start -> publish, the timed steps' fetches
+            durs = [(e[6] - e[5]) * 1e-6 for e in trace[-n_f:]] if n_f else []
+            if durs:
+                f_ms = sum(durs) / len(durs)
         fetch_gbs = lb / (f_ms * 1e-3) / 1e9 if f_ms > 0 else None
         ctx_avg = pos_before + (args.emulate_steps - 1) / 2.0
         ns = north_star_roofline(m, B, ctx_avg, W, peaks, ms,
@@ -335,7 +342,9 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "what": f"rank 0 of a {W}-rank WaS group on one B200; the {W - 1} other owners are "
                     "serve-only contexts in local HBM (bench.py was_emulation docstring)",
             "world_emulated": W, "batch": B, "ctx": ctx_len, "slots": slots,
-            "fetch_sms": args.emulate_fetch_sms, "fetch_pace_gbps": args.emulate_pace_gbps,
+            "fetch_engine": args.fetch, "fetch_sms": st["fetch_sms_held"],
+            "compute_sms": st["compute_sms"], "stagger_tick_ms": st["stagger_tick_ns"] * 1e-6,
+            "fetch_pace_gbps": args.emulate_pace_gbps,
             "steps": args.emulate_steps,
             "ms_per_step": ms, "tokens_s_rank": B / (ms / 1e3),
             "group_tokens_s_est": W * B / (ms / 1e3),

@@ -60,8 +60,11 @@ typedef enum {
 } sidp_pool;
 
 typedef enum {
-  SIDP_FETCH_SM = 0,    /* hand-written SM copy kernel over peer memory (K1) */
-  SIDP_FETCH_CE = 1     /* copy-engine cudaMemcpyAsync (the paper's mechanism; baseline) */
+  SIDP_FETCH_SM = 0,    /* hand-written K1 (TMA bulk copies through shared memory, CTA pairs) over
+                           peer memory; device epoch flags per slot; the compute kernels size
+                           their grids for the SMs the fetch does not hold */
+  SIDP_FETCH_CE = 1     /* copy-engine cudaMemcpyAsync + CUDA events (the paper's mechanism,
+                           PAPER.md:236-237; baseline) */
 } sidp_fetch_engine;
 
 /* Decoder model dimensions (HF-Llama block; Qwen3 qk_norm and Qwen2.5 QKV-bias variants).
@@ -86,7 +89,10 @@ typedef struct {
   int32_t pool_scope;           /* sidp_pool */
   int32_t max_batch;            /* max rows per rank per step */
   int32_t max_ctx;              /* KV positions per sequence; a step needs pos + 1 <= max_ctx */
-  int32_t fetch_sms;            /* CTAs used by the SM fetch kernel (0 => 16) */
+  int32_t fetch_sms;            /* SMs (CTAs, rounded to CTA pairs) the SM fetch kernel holds
+                                   (0 => 16: ~50 GB/s of copy per SM, so 16 cover NVLink 5's
+                                   ~770 GB/s reader rate); the WaS compute kernels then use the
+                                   remaining SMs.  Ignored by SIDP_FETCH_CE and when d == 1 */
   int32_t fetch_engine;         /* sidp_fetch_engine */
   int32_t stagger;              /* 1 => C-S7 start offsets t_r = (-r) mod (d-1) fetch ticks */
   int32_t device;               /* CUDA device ordinal the context lives on */
@@ -95,6 +101,10 @@ typedef struct {
                                    (GB/s).  Only for emulating NVLink with local-HBM owners on
                                    one GPU (bench.py --emulate-world); 0 on real NVLink, which
                                    caps the rate by itself. */
+  int32_t compute_sms;          /* SMs the compute grids are sized for: 0 = automatic (all SMs,
+                                   minus fetch_sms while an SM-fetch WaS ring is active); > 0 =
+                                   explicit (e.g. a replicated baseline sized like a WaS rank,
+                                   so both run bitwise-identical kernels) */
 } sidp_config;
 
 /* Caller-owned KV cache of this rank (never pooled).
@@ -140,6 +150,9 @@ typedef struct {
   uint64_t workspace_bytes; /* activations, split-K / split-KV workspaces, staging */
   double timed_ms[8];       /* per kernel class: summed CUDA-event durations (sidp_set_timing) */
   uint64_t timed_launches[8];  /* per kernel class: timed launches */
+  int32_t fetch_sms_held;   /* SMs the SM fetch kernel holds (0: copy engine, or no remote layer) */
+  int32_t compute_sms;      /* SMs the WaS compute grids are sized for (0 = all) */
+  double stagger_tick_ns;   /* measured single-reader layer fetch (C-S7 tick; 0 = not measured) */
 } sidp_stats_t;
 
 /* ---- lifecycle --------------------------------------------------------------------- */
@@ -228,10 +241,25 @@ sidp_status sidp_get_schedule(const sidp_ctx* ctx, int32_t steps, int32_t* fetch
 /* Fetch-tick offset of this rank's fetch stream (C-S7 stagger). */
 sidp_status sidp_stagger_ticks(const sidp_ctx* ctx, int32_t* ticks);
 
-/* Device-side log of fetches actually issued by the runtime (step, layer, slot) since the
- * last reset of the plan (for protocol parity). */
+/* The fetches performed since the last reset of the plan, as (step, layer, slot).
+ * SIDP_FETCH_SM: read back from the device log that the fetch kernel's publishing CTA appends
+ * to (the layer id and slot it actually copied; the last 4096 entries); synchronises the fetch
+ * stream.  SIDP_FETCH_CE: the host's enqueue log (the copy engine writes no log).
+ * fetch_step == NULL: *n = count only; else capacity must be >= the count (SIDP_EINVAL). */
 sidp_status sidp_get_fetch_log(const sidp_ctx* ctx, int32_t* fetch_step, int32_t* fetch_layer,
                                int32_t* fetch_slot, int32_t capacity, int32_t* n);
+
+/* SIDP_FETCH_SM only (else *n = 0): the device fetch log with timing — int64 [n][7] =
+ * {fetch index j, layer, slot, owner rank, fill epoch of the slot, %globaltimer ns of the first
+ * fetch CTA's start, %globaltimer ns of the publish}.  Per-owner reader traces (C-S7) and the
+ * achieved per-fetch GB/s come from it.  Synchronises the fetch stream. */
+sidp_status sidp_get_fetch_trace(const sidp_ctx* ctx, int64_t* out, int32_t capacity, int32_t* n);
+
+/* SIDP_FETCH_SM only (else *n = 0): the compute side's device log of slot consumptions —
+ * int64 [n][5] = {layer expected, slot, layer tag found in the slot, consumption epoch,
+ * %globaltimer ns when the weights were ready}.  A tag != layer also raises the sticky error
+ * word (protocol violation).  Synchronises the device. */
+sidp_status sidp_get_consume_log(const sidp_ctx* ctx, int64_t* out, int32_t capacity, int32_t* n);
 
 sidp_status sidp_stats(const sidp_ctx* ctx, sidp_stats_t* out);
 
@@ -289,8 +317,10 @@ sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uin
                           int32_t tensor, int32_t layer, int32_t kind, int32_t scale_k,
                           int64_t row0, int64_t lcols, int32_t row_map, void* stream);
 
-/* K1 fetch of `bytes` (multiple of 16) from src (local or peer VA) to dst with the SM copy kernel
- * on `ctas` CTAs (engine 0) or the copy engine (engine 1). */
+/* K1 fetch of `bytes` (multiple of 16, 16-byte aligned pointers) from src (local or peer VA) to
+ * dst: engine 0 = the TMA bulk-copy kernel on `ctas` CTAs (rounded to CTA pairs; the WaS
+ * default), 1 = the copy engine (cudaMemcpyAsync), 2 = the vectorised LDG/STG copy kernel
+ * (round-1 design, kept for A/B).  Device pointers; enqueued on stream; no flags posted. */
 sidp_status sidp_test_fetch(void* dst, const void* src, size_t bytes, int32_t ctas, int32_t engine,
                             void* stream);
 

@@ -165,6 +165,54 @@ def cas_offsets(batches: list[int]) -> list[int]:
     return off
 
 
+def cas_layer(m, W: dict, p_loc: dict, xs: dict, pos: dict, caches: dict, pool: str = "layer",
+              on_serve=None) -> dict:
+    """One layer in CaS mode for every live rank (§4.3).  W: the owner's pooled
+    tensors of this layer (only the owner touches them); p_loc: the tensors every rank keeps.
+    xs / pos / caches: per live rank r (ascending order) its layer input [B_r, h], positions
+    [B_r] and this layer's (Kc, Vc), updated in place (the KV cache is local).
+    Returns {r: layer output}.  Dummy ranks are simply absent."""
+    live = sorted(xs)
+    off, acc = {}, 0
+    for r in live:                                 # exclusive prefix sums (C-A10)
+        off[r] = acc
+        acc += xs[r].shape[0]
+
+    def serve(parts, fn):
+        """Owner: fuse rows of all live ranks in rank order, compute once, split."""
+        stage = {k: np.concatenate([parts[r][k] for r in live], axis=0) for k in parts[live[0]]}
+        out = fn(stage)
+        if on_serve is not None:
+            on_serve(live)
+        return {r: out[off[r]:off[r] + xs[r].shape[0]] for r in live}
+
+    if not live:
+        return {}
+    if pool == "layer":
+        P = {**p_loc, **W}
+        # RT1: send u, receive u W_qkv^T (+b)
+        qkv = serve({r: {"u": M.attn_norm(m, P, xs[r])} for r in live},
+                    lambda s: M.qkv_proj(m, P, s["u"]))
+        os_ = {}
+        for r in live:
+            q, k, v = M.qkv_post(m, P, qkv[r], pos[r])
+            M.append_kv(caches[r][0], caches[r][1], k, v, pos[r])
+            os_[r] = {"o": M.attend(m, q, caches[r][0], caches[r][1], pos[r]), "x": xs[r]}
+        # RT2: send (o, x), receive out
+        return serve(os_, lambda s: M.post_attn(m, P, s["x"], s["o"]))
+    # ffn scope: attention local, one round trip for the FFN
+    u2s, x2s = {}, {}
+    for r in live:
+        u = M.attn_norm(m, p_loc, xs[r])
+        q, k, v = M.qkv_post(m, p_loc, M.qkv_proj(m, p_loc, u), pos[r])
+        M.append_kv(caches[r][0], caches[r][1], k, v, pos[r])
+        o_ = M.attend(m, q, caches[r][0], caches[r][1], pos[r])
+        x2s[r] = M.o_proj_residual(m, p_loc, xs[r], o_)
+        u2s[r] = {"u2": M.mlp_norm(m, W, x2s[r])}
+    ys = serve(u2s, lambda s: M.down_proj(m, W, M.mlp_act(m, W, s["u2"])))
+    return {r: x2s[r] + ys[r] for r in live}
+
+
 def run_cas(m, layers, head, embed_fn, ranks: list[RankState], steps: int, d: int,
             owner: list[int], pool: str = "layer", traffic: list | None = None):
     arenas = build_owned_arenas(layers, owner, d, pool)
@@ -172,58 +220,16 @@ def run_cas(m, layers, head, embed_fn, ranks: list[RankState], steps: int, d: in
     toks = [st.tokens for st in ranks]
     for t in range(steps):
         live = [st for st in ranks if st.B > 0]
-        Bs = [st.B for st in ranks]
-        off = cas_offsets(Bs)
         xs = {st.r: embed_fn(toks[st.r]) for st in live}
         coll = {st.r: [] for st in live}
         for l in range(len(layers)):
             o = owner[l]
-            W = arenas[o][l]                      # only the owner touches pooled weights
-
-            def serve(parts, fn):
-                """Owner: fuse rows of all live ranks in rank order, compute once, split."""
-                if not parts:
-                    return {}
-                stage = {k: np.concatenate([parts[st.r][k] for st in live], axis=0)
-                         for k in parts[live[0].r]}
-                out = fn(stage)
-                res = {st.r: out[off[st.r]:off[st.r] + st.B] for st in live}
-                if traffic is not None:
-                    traffic.append((t, l, o, [st.r for st in live]))
-                return res
-
             for st in live:
                 coll[st.r].append(xs[st.r].copy())
-            if pool == "layer":
-                p_loc = local[l]
-                # RT1: send u, receive u W_qkv^T (+b)
-                us = {st.r: {"u": M.attn_norm(m, {**p_loc, **W}, xs[st.r])} for st in live}
-                qkv = serve(us, lambda s: M.qkv_proj(m, {**p_loc, **W}, s["u"]))
-                os_ = {}
-                for st in live:
-                    pos = st.pos + t
-                    q, k, v = M.qkv_post(m, {**p_loc, **W}, qkv[st.r], pos)
-                    M.append_kv(st.caches[l][0], st.caches[l][1], k, v, pos)
-                    os_[st.r] = {"o": M.attend(m, q, st.caches[l][0], st.caches[l][1], pos),
-                                 "x": xs[st.r]}
-                # RT2: send (o, x), receive out
-                outs = serve(os_, lambda s: M.post_attn(m, {**p_loc, **W}, s["x"], s["o"]))
-                for st in live:
-                    xs[st.r] = outs[st.r]
-            else:  # ffn scope: attention local, one round trip for the FFN
-                p_loc = local[l]
-                u2s, x2s = {}, {}
-                for st in live:
-                    pos = st.pos + t
-                    u = M.attn_norm(m, p_loc, xs[st.r])
-                    q, k, v = M.qkv_post(m, p_loc, M.qkv_proj(m, p_loc, u), pos)
-                    M.append_kv(st.caches[l][0], st.caches[l][1], k, v, pos)
-                    o_ = M.attend(m, q, st.caches[l][0], st.caches[l][1], pos)
-                    x2s[st.r] = M.o_proj_residual(m, p_loc, xs[st.r], o_)
-                    u2s[st.r] = {"u2": M.mlp_norm(m, W, x2s[st.r])}
-                ys = serve(u2s, lambda s: M.down_proj(m, W, M.mlp_act(m, W, s["u2"])))
-                for st in live:
-                    xs[st.r] = x2s[st.r] + ys[st.r]
+            xs = cas_layer(m, arenas[o][l], local[l], xs, {st.r: st.pos + t for st in live},
+                           {st.r: st.caches[l] for st in live}, pool,
+                           on_serve=None if traffic is None else
+                           (lambda lv, t=t, l=l, o=o: traffic.append((t, l, o, list(lv)))))
         for st in ranks:
             if st.B == 0:
                 st.history.append(None)

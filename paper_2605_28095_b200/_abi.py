@@ -33,7 +33,8 @@ class Config(C.Structure):
                 ("was_slots", C.c_int32), ("cas_slots", C.c_int32), ("order", C.c_int32),
                 ("pool_scope", C.c_int32), ("max_batch", C.c_int32), ("max_ctx", C.c_int32),
                 ("fetch_sms", C.c_int32), ("fetch_engine", C.c_int32), ("stagger", C.c_int32),
-                ("device", C.c_int32), ("seed", C.c_uint64), ("fetch_pace_gbps", C.c_float)]
+                ("device", C.c_int32), ("seed", C.c_uint64), ("fetch_pace_gbps", C.c_float),
+                ("compute_sms", C.c_int32)]
 
 
 class KV(C.Structure):
@@ -53,7 +54,8 @@ class Stats(C.Structure):
                 ("local_layer_bytes", C.c_uint64), ("owned_bytes", C.c_uint64),
                 ("slot_bytes", C.c_uint64), ("replicated_bytes", C.c_uint64),
                 ("workspace_bytes", C.c_uint64), ("timed_ms", C.c_double * 8),
-                ("timed_launches", C.c_uint64 * 8)]
+                ("timed_launches", C.c_uint64 * 8), ("fetch_sms_held", C.c_int32),
+                ("compute_sms", C.c_int32), ("stagger_tick_ns", C.c_double)]
 
 
 _P = C.c_void_p
@@ -78,6 +80,8 @@ SIGNATURES = {
     "sidp_get_schedule": [_P, _I32, _PI32, _PI32, _PI32, _I32, _PI32],
     "sidp_stagger_ticks": [_P, _PI32],
     "sidp_get_fetch_log": [_P, _PI32, _PI32, _PI32, _I32, _PI32],
+    "sidp_get_fetch_trace": [_P, C.POINTER(_I64), _I32, _PI32],
+    "sidp_get_consume_log": [_P, C.POINTER(_I64), _I32, _PI32],
     "sidp_stats": [_P, C.POINTER(Stats)],
     "sidp_set_timing": [_P, _I32],
     "sidp_last_error": [],

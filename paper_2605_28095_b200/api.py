@@ -65,8 +65,9 @@ class KVCache:
 
 class Context:
     def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
-                 max_batch=8, max_ctx=128, fetch_sms=48, fetch_engine="sm", stagger=True,
-                 device=0, seed=20261017, layer_owner=None, alloc=True, fetch_pace_gbps=0.0):
+                 max_batch=8, max_ctx=128, fetch_sms=16, fetch_engine="sm", stagger=True,
+                 device=0, seed=20261017, layer_owner=None, alloc=True, fetch_pace_gbps=0.0,
+                 compute_sms=0):
         self.m = m
         self.rank, self.world = rank, world
         self._owner_arr = None
@@ -79,7 +80,7 @@ class Context:
                             A.POOL_LAYER if pool == "layer" else A.POOL_FFN,
                             max_batch, max_ctx, fetch_sms,
                             A.FETCH_SM if fetch_engine == "sm" else A.FETCH_CE,
-                            int(bool(stagger)), device, seed, float(fetch_pace_gbps))
+                            int(bool(stagger)), device, seed, float(fetch_pace_gbps), int(compute_sms))
         self.desc = model_desc(m)
         h = C.c_void_p()
         A.check(A.lib().sidp_init(C.byref(self.desc), C.byref(self.cfg), C.byref(h)), "sidp_init")
@@ -181,6 +182,22 @@ class Context:
         t, l, s = (C.c_int32 * k)(), (C.c_int32 * k)(), (C.c_int32 * k)()
         A.check(A.lib().sidp_get_fetch_log(self.h, t, l, s, k, C.byref(n)), "log")
         return list(zip(t[:n.value], l[:n.value], s[:n.value]))
+
+    def fetch_trace(self) -> list[tuple]:
+        """SM fetch: device log rows (j, layer, slot, owner, epoch, t_start_ns, t_end_ns)."""
+        return self._rows(A.lib().sidp_get_fetch_trace, 7)
+
+    def consume_log(self) -> list[tuple]:
+        """SM fetch: compute-side consumptions (layer, slot, tag, epoch, t_ready_ns)."""
+        return self._rows(A.lib().sidp_get_consume_log, 5)
+
+    def _rows(self, fn, w):
+        n = C.c_int32()
+        A.check(fn(self.h, None, 0, C.byref(n)), fn.__name__)
+        k = max(1, n.value)
+        buf = (C.c_int64 * (k * w))()
+        A.check(fn(self.h, buf, k, C.byref(n)), fn.__name__)
+        return [tuple(buf[i * w:(i + 1) * w]) for i in range(n.value)]
 
     def stagger_ticks(self) -> int:
         v = C.c_int32()

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsidp.so")
 SOURCES = ["runtime.cu", "kernels/gemm.cu", "kernels/init.cu", "kernels/norm.cu",
-           "kernels/attention.cu", "kernels/fetch.cu"]
+           "kernels/attention.cu", "kernels/fetch.cu", "kernels/ring.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-cudart", "static", "--expt-relaxed-constexpr",

@@ -183,6 +183,18 @@ SIDP_DEV float warp_max(float v) {
   return v;
 }
 
+// True the first time a call site asks for the current device: kernel attributes (max dynamic
+// shared memory) are per device context, so "once per process" guards would miss a second
+// device.  The preload functions also set every attribute at sidp_alloc (after cudaSetDevice).
+inline bool first_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 inline bool pdl_enabled() {
   static const int v = getenv("SIDP_PDL") ? atoi(getenv("SIDP_PDL")) : 1;
   return v != 0;

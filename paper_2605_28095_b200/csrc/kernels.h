@@ -88,6 +88,13 @@ struct GemmWorkspace {
 };
 
 cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t s);
+// Grid-sizing SM budget of the persistent / one-wave compute kernels (GEMMs, fused MLP,
+// attention) on this host thread: 0 = every SM of the device; n > 0 = the first n (even) — set
+// by the runtime while a WaS fetch kernel holds dedicated SMs, so no compute CTA (pair) ever
+// waits for an SM the fetch occupies.  SIDP_SM_BUDGET overrides the default 0.
+void set_compute_sms(int n);
+int get_compute_sms_budget();
+int compute_sms();
 int gemm_pick_splits(int tiles, int nkb, int sms);
 // true when an EPI_PARTIAL launch of this shape is both possible (slices fit the workspace)
 // and worthwhile (whole 256x256 tiles would leave CTA pairs idle, so the GEMM is stream-K
@@ -122,10 +129,11 @@ cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf1
                            int rows, int h, cudaStream_t s);
 // Deferred stream-K fix-up fused with the residual add and the next RMSNorm (SURVEY.md a8 + a9,
 // a11 + next layer's a5): per row m, x_out = bf16(sum of the partial slices + resid) and
-// u = bf16(x_out * rsqrt(mean(x_out^2) + eps) * g).  resid may alias x_out.
+// u = bf16(x_out * rsqrt(mean(x_out^2) + eps) * g).  resid may alias x_out.  post (optional):
+// a WaS slot's release counter, incremented (release) once the predecessor kernel completed.
 cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, bf16* xout, int ldx,
                               const bf16* g, float eps, bf16* u, int ldu, int rows, int h,
-                              cudaStream_t s);
+                              cudaStream_t s, unsigned long long* post = nullptr);
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
                          cudaStream_t s);
 // qkv fp32 [B, (nq+2nkv)*hd] -> q bf16 [B, nq, hd]; k, v appended to caches at pos[b]
@@ -185,6 +193,65 @@ cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cud
 cudaError_t delay_launch(uint64_t ns, cudaStream_t s);
 // copy-engine fetch pacing: first != 0 stamps *t0; else waits until *t0 + offset_ns
 cudaError_t pace_launch(unsigned long long* t0, int first, uint64_t offset_ns, cudaStream_t s);
+
+// ---------------------------------------------------------------- WaS ring on the device
+// (kernels/ring.cu): epoch flags per slot + device-side logs of what was actually fetched and
+// consumed.  One FetchRing per context, library-owned, zeroed (t_first = ~0) at alloc and at
+// every plan reset.
+constexpr int kRingMaxSlots = 16;
+constexpr int kFetchLogCap = 4096;
+constexpr int kFetchStages = 6;                 // shared-memory ring of the bulk fetch
+constexpr int kFetchChunk = 32 * 1024;          // bytes per bulk copy
+struct FetchLogEnt {
+  unsigned long long j;        // fetch index since the last reset
+  int layer, slot, owner, pad;
+  unsigned long long epoch;    // fill number of the slot (1-based)
+  unsigned long long t_start, t_end;   // %globaltimer ns: first CTA start, publish
+};
+struct ConsLogEnt {
+  int layer, slot, tag, pad;
+  unsigned long long epoch;    // consumption number of the slot (1-based)
+  unsigned long long t;        // %globaltimer ns when the layer's weights were ready
+};
+struct FetchRing {
+  unsigned long long fill[kRingMaxSlots];   // completed fills per slot (fetch side)
+  unsigned long long rel[kRingMaxSlots];    // releases per slot (compute side)
+  unsigned long long cons[kRingMaxSlots];   // consumptions started (compute side)
+  unsigned long long t_first[kRingMaxSlots];   // earliest CTA start of the slot's current fill
+  unsigned int arrive[kRingMaxSlots];       // CTAs done with the slot's current fill
+  int tag[kRingMaxSlots];                   // layer held by the slot (last fill)
+  unsigned long long nfetch, ncons;
+  FetchLogEnt log[kFetchLogCap];
+  ConsLogEnt clog[kFetchLogCap];
+};
+// One fetch of a window: layer `layer` of owner `owner` from src into slot `slot`, fill number
+// `fill` of that slot (0-based; host-counted, so the gate needs no device read of fill[slot]).
+struct FetchEnt {
+  const uint8_t* src;
+  int layer, slot, owner;
+  unsigned int fill;
+};
+constexpr int kFetchWindow = 96;   // fetches one launch can carry (>= remote layers per pass)
+struct FetchArgs {
+  uint8_t* slots; size_t slot_stride; size_t bytes;   // destination slot s = slots + s * stride
+  FetchRing* ring;             // null: plain copy (test hook: src -> slots), no gate / publish
+  int n;                       // entries in this launch
+  int gate;                    // 1: each CTA waits for rel[slot] >= fill in-kernel (windowed)
+  uint64_t ns_per_chunk;       // > 0: emulated link rate (chunk c starts >= c x ns after start)
+  uint64_t delay_ns;           // start offset (C-S7 stagger) before the first entry
+  uint64_t timeout_ns; int* err;   // gate timeout -> *err (mapped host word)
+  int chunk, stages;           // set by fetch_bulk_launch (shared-memory ring geometry)
+  FetchEnt ent[kFetchWindow];
+};
+size_t fetch_bulk_smem();
+cudaError_t fetch_bulk_launch(const FetchArgs& a, int ctas, cudaStream_t s);
+cudaError_t ring_free_wait_launch(FetchRing* r, int slot, unsigned long long fill,
+                                  uint64_t timeout_ns, int* err, cudaStream_t s);
+cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t timeout_ns, int* err,
+                                   cudaStream_t s);
+cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s);
+cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s);
+cudaError_t ring_preload();
 
 // ---------------------------------------------------------------- CaS signalling
 struct FlagSet {

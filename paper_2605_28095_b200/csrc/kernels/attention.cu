@@ -759,11 +759,9 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   const size_t ring = (size_t)kWarps * ST * 2 * kChunk * HD * 2;
   const size_t smem = ring + (((size_t)a.B + 1) * 4 + 15) / 16 * 16;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
     cudaFuncSetAttribute(attn_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
   // one wave of resident CTAs; fewer when the batch has little work (>= 8 chunks per CTA at
   // the host's context bound, so each warp streams at least two chunks)
   int per_sm = 0;
@@ -775,7 +773,7 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   // CTA, no pieces); few pairs (small batch, long context): one wave of CTAs splitting the
   // pairs into pieces (split-KV) with >= 8 chunks per CTA at the host's context bound.
   const long long pairs = (long long)a.B * a.nkv;
-  const long long slots = (long long)g_sms * per_sm;
+  const long long slots = (long long)compute_sms() * per_sm;
   // Many pairs of < 64 chunks each at the context bound: one wave of CTAs walking contiguous
   // chunk ranges instead of one CTA per pair (the per-CTA launch, prologue and warp merge
   // dominated).  Measured per layer, pair mode vs one wave: B = 1024 / S_ctx = 256 (17 chunks)
@@ -790,15 +788,13 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   // M2, 65 chunks: step 29.52-29.63 -> 29.29-29.34 ms; B = 128 / 2048 equal)
   static const int env_warp_ch = getenv("SIDP_ATTN_WARP_CH") ? atoi(getenv("SIDP_ATTN_WARP_CH")) : 128;
   if (pairs >= slots && chunks_per_pair < env_warp_ch) {
-    static bool wattr = false;
-    if (!wattr) {
+    static unsigned long long wattr = 0;
+    if (first_on_device(wattr))
       cudaFuncSetAttribute(attn_warp_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-      wattr = true;
-    }
     int wper = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, attn_warp_kernel<HD, ST>, 128, ring);
-    const long long wslots = (long long)g_sms * std::max(1, wper);
+    const long long wslots = (long long)compute_sms() * std::max(1, wper);
     const int wctas = (int)std::min<long long>(wslots, (pairs + kWarps - 1) / kWarps);
     AttnParams p{};
     p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws; p.cnt = a.cnt;
@@ -853,8 +849,17 @@ cudaError_t attention_preload() {
   cudaError_t e = cudaSuccess;
   if (cudaFuncGetAttributes(&fa, qkv_post_kernel<128, kQkvHeadsPerWarp>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, qkv_post_kernel<64, kQkvHeadsPerWarp>) != cudaSuccess) e = cudaGetLastError();
-#define SIDP_PRELOAD_ATTN(hd, st) \
-  if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError();
+  // every kernel the launcher can pick — including the warp-per-pair kernels, which CaS steps
+  // select from B * n_kv >= one wave of pairs: a module loaded lazily at its first launch waits
+  // for the device to idle, a deadlock while another rank's flag wait spins — and the
+  // >48 KB shared-memory attribute, set here for this device (sidp_alloc calls this)
+#define SIDP_PRELOAD_ATTN(hd, st)                                                                \
+  if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError();    \
+  if (cudaFuncGetAttributes(&fa, attn_warp_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError(); \
+  if (cudaFuncSetAttribute(attn_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                           200 * 1024) != cudaSuccess) e = cudaGetLastError();                     \
+  if (cudaFuncSetAttribute(attn_warp_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           200 * 1024) != cudaSuccess) e = cudaGetLastError();
   SIDP_PRELOAD_ATTN(128, 2) SIDP_PRELOAD_ATTN(128, 3) SIDP_PRELOAD_ATTN(128, 4)
   SIDP_PRELOAD_ATTN(64, 2) SIDP_PRELOAD_ATTN(64, 3) SIDP_PRELOAD_ATTN(64, 4)
 #undef SIDP_PRELOAD_ATTN

@@ -28,25 +28,24 @@ __device__ __forceinline__ void st_na_v4(uint4* p, const uint4& v) {
                : "memory");
 }
 
-constexpr int kUnroll = 8;   // 128 B in flight per thread (NVLink peer latency ~2 us)
-
-// ns_per_iter > 0 paces the copy: iteration `it` (kUnroll x grid x 512 x 16 B) starts no
-// earlier than it x ns_per_iter after the CTA's start (NVLink-rate emulation on one GPU).
-__global__ void __launch_bounds__(512) fetch_kernel(uint4* __restrict__ dst,
-                                                    const uint4* __restrict__ src, size_t nvec,
-                                                    uint64_t ns_per_iter) {
+// ns_per_iter > 0 paces the copy: iteration `it` (U x grid x T x 16 B) starts no earlier than
+// it x ns_per_iter after the CTA's start (NVLink-rate emulation on one GPU).
+template <int T, int U>
+__global__ void __launch_bounds__(T) fetch_kernel(uint4* __restrict__ dst,
+                                                  const uint4* __restrict__ src, size_t nvec,
+                                                  uint64_t ns_per_iter) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t t0 = ns_per_iter ? globaltimer_ns() : 0;
   uint64_t it = 0;
-  for (; i + (kUnroll - 1) * stride < nvec; i += kUnroll * stride, ++it) {
+  for (; i + (U - 1) * stride < nvec; i += U * stride, ++it) {
     if (ns_per_iter)
       while (globaltimer_ns() - t0 < it * ns_per_iter) __nanosleep(200);
-    uint4 v[kUnroll];
+    uint4 v[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_nc_v4(src + i + u * stride);
+    for (int u = 0; u < U; ++u) v[u] = ld_nc_v4(src + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_na_v4(dst + i + u * stride, v[u]);
+    for (int u = 0; u < U; ++u) st_na_v4(dst + i + u * stride, v[u]);
   }
   for (; i < nvec; i += stride) st_na_v4(dst + i, ld_nc_v4(src + i));
 }
@@ -112,11 +111,20 @@ cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cud
       (reinterpret_cast<uintptr_t>(src) & 15))
     return cudaErrorInvalidValue;
   if (ctas <= 0) ctas = 32;
+  // threads x loads in flight per thread (SIDP_LDG_CFG: 0 = 512 x 8, 1 = 1024 x 8, 2 = 256 x 16,
+  // 3 = 1024 x 4) — per-SM copy-rate probes
+  static const int cfg = getenv("SIDP_LDG_CFG") ? atoi(getenv("SIDP_LDG_CFG")) : 0;
+  const int T = cfg == 1 || cfg == 3 ? 1024 : cfg == 2 ? 256 : 512;
+  const int U = cfg == 2 ? 16 : cfg == 3 ? 4 : 8;
   // bytes per iteration of all CTAs / (GB/s == bytes per ns)
   const uint64_t ns_per_iter =
-      pace_gbps > 0.0f ? (uint64_t)((double)kUnroll * ctas * 512 * 16 / pace_gbps) : 0;
-  fetch_kernel<<<ctas, 512, 0, s>>>(reinterpret_cast<uint4*>(dst),
-                                    reinterpret_cast<const uint4*>(src), bytes / 16, ns_per_iter);
+      pace_gbps > 0.0f ? (uint64_t)((double)U * ctas * T * 16 / pace_gbps) : 0;
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const uint4* sp = reinterpret_cast<const uint4*>(src);
+  if (cfg == 1) fetch_kernel<1024, 8><<<ctas, 1024, 0, s>>>(d, sp, bytes / 16, ns_per_iter);
+  else if (cfg == 2) fetch_kernel<256, 16><<<ctas, 256, 0, s>>>(d, sp, bytes / 16, ns_per_iter);
+  else if (cfg == 3) fetch_kernel<1024, 4><<<ctas, 1024, 0, s>>>(d, sp, bytes / 16, ns_per_iter);
+  else fetch_kernel<512, 8><<<ctas, 512, 0, s>>>(d, sp, bytes / 16, ns_per_iter);
   return cudaGetLastError();
 }
 
@@ -197,7 +205,7 @@ cudaError_t xfer_launch(const XferSet& x, cudaStream_t s) {
 cudaError_t fetch_preload() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaSuccess;
-  if (cudaFuncGetAttributes(&fa, fetch_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, fetch_kernel<512, 8>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, delay_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, pace_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, signal_kernel) != cudaSuccess) e = cudaGetLastError();

@@ -1317,7 +1317,7 @@ int gemm_pick_splits(int tiles, int nkb, int slots) {
 
 int gemm_last_launch_count() { return g_last_launches; }
 
-static int num_sms() {
+static int device_sms() {
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1325,6 +1325,20 @@ static int num_sms() {
   }
   return g_num_sms;
 }
+
+// SMs the compute kernels size their grids for (see kernels.h set_compute_sms): the device's
+// count, or fewer while a WaS fetch kernel holds dedicated SMs.  Even, so CTA pairs fill it.
+static thread_local int g_sm_budget = 0;
+void set_compute_sms(int n) { g_sm_budget = n; }
+int get_compute_sms_budget() { return g_sm_budget; }
+int compute_sms() {
+  static const int env = getenv("SIDP_SM_BUDGET") ? atoi(getenv("SIDP_SM_BUDGET")) : 0;
+  int n = device_sms();
+  const int b = g_sm_budget > 0 ? g_sm_budget : env;
+  if (b > 0 && b < n) n = std::max(2, b & ~1);
+  return n;
+}
+static int num_sms() { return compute_sms(); }
 
 bool gemm_partial_ok(int M, int N, int K, size_t ws_bytes) {
   static int env = getenv("SIDP_GEMM_PARTIAL") ? atoi(getenv("SIDP_GEMM_PARTIAL")) : 1;
@@ -1354,9 +1368,8 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   if (a.K % BK != 0 || a.N <= 0 || a.N % 8 != 0 || a.x == nullptr || a.w == nullptr)
     return cudaErrorInvalidValue;
   if (a.epi == EPI_SILU_MUL && (a.N % 16) != 0) return cudaErrorInvalidValue;
-  static bool attrs = false;
-  if (!attrs) {
-    attrs = true;
+  static unsigned long long attrs = 0;
+  if (first_on_device(attrs)) {
     num_sms();
     set_attr<EPI_PARTIAL>();
     set_attr<EPI_F32>();
@@ -1373,7 +1386,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   static int env_sw_min = getenv("SIDP_GEMM_SW_MIN_M") ? atoi(getenv("SIDP_GEMM_SW_MIN_M")) : 128;
   static int env_sw_c0 = getenv("SIDP_GEMM_SW_C0") ? atoi(getenv("SIDP_GEMM_SW_C0")) : 64;
   static int env_sw_bnf = getenv("SIDP_GEMM_SW_BNF") ? atoi(getenv("SIDP_GEMM_SW_BNF")) : 0;
-  const int sms = a.max_ctas > 0 ? std::min(a.max_ctas, g_num_sms) : g_num_sms;
+  const int sms = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
   const int pair_slots = std::max(1, sms / 2);
   const int nkb_blocks = a.K / BK;
   static int env_kps = getenv("SIDP_GEMM_KPS") ? atoi(getenv("SIDP_GEMM_KPS")) : 2;
@@ -1744,13 +1757,10 @@ cudaError_t mlp_launch(const MlpArgs& a, const GemmWorkspace& w, cudaStream_t st
   g_last_launches = 0;
   if (!mlp_fused_ok(a.M, a.h, a.I, w.ws_bytes, w.n_counters, kMlpMaxTokenTiles))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    attr = true;
-    num_sms();
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
     cudaFuncSetAttribute(mlp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024);
-  }
-  const int C = std::max(1, g_num_sms / 2);
+  const int C = std::max(1, num_sms() / 2);
   const int G = a.I / 128, nks1 = a.h / (BK * 2), D = (a.h + 255) / 256, nks2 = a.I / (BK * 2);
   const int MT = (a.M + 255) / 256;
   const int BNT = MT > 1 ? 256 : std::max(32, ((a.M + 31) / 32) * 32);
@@ -1813,6 +1823,17 @@ cudaError_t gemm_preload() {
   SIDP_PRELOAD((gemm_reduce_kernel<EPI_F32>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_BF16>))
   SIDP_PRELOAD((gemm_reduce_kernel<EPI_RESID>)) SIDP_PRELOAD((gemm_reduce_kernel<EPI_SILU_MUL>))
 #undef SIDP_PRELOAD
+  // the >48 KB shared-memory attributes, for the current device (sidp_alloc calls this)
+  set_attr<EPI_PARTIAL>();
+  set_attr<EPI_F32>();
+  set_attr<EPI_BF16>();
+  set_attr<EPI_RESID>();
+  set_attr<EPI_SILU_MUL>();
+  set_attr<EPI_ARGMAX>();
+  set_attr<EPI_QKV>();
+  if (cudaFuncSetAttribute(mlp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemBudget + 1024) != cudaSuccess)
+    e = cudaGetLastError();
   return e;
 }
 

@@ -104,9 +104,15 @@ template <int NS, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) resid_norm_kernel(
     const PartialSrc ps, const bf16* __restrict__ resid, int ldr, bf16* xout, int ldx,
     const bf16* __restrict__ g, float eps, bf16* __restrict__ u, int ldu, int h, int rows,
-    int late_trigger) {
+    int late_trigger, unsigned long long* post) {
   if (!late_trigger) pdl_trigger();
   pdl_wait();
+  if (post && blockIdx.x == 0 && threadIdx.x == 0) {
+    // WaS slot release (kernels/ring.cu): the predecessor — the last reader of the slot's
+    // weights — has completed, so the fetch stream may refill the slot
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(post) : "memory");
+  }
   const int nvec = h / 8;
   const size_t slice = (size_t)ps.M * ps.N;
   const bool one = nvec <= (int)blockDim.x;
@@ -198,7 +204,7 @@ cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf1
 
 cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, bf16* xout, int ldx,
                               const bf16* g, float eps, bf16* u, int ldu, int rows, int h,
-                              cudaStream_t s) {
+                              cudaStream_t s, unsigned long long* post) {
   if (rows <= 0) return cudaSuccess;
   if (h % 8 || ps.ws == nullptr || ps.N != h || rows > ps.M) return cudaErrorInvalidValue;
   const int threads = std::min(1024, (h / 8 + 31) / 32 * 32);
@@ -221,9 +227,9 @@ cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, 
   const bool wide = env_ns ? env_ns == 8 : max_seg > 4;
   if (wide && threads <= 640)
     return launch_pdl(resid_norm_kernel<8, 640>, dim3(grid), dim3(threads), 0, s, ps, resid, ldr,
-                      xout, ldx, g, eps, u, ldu, h, rows, late);
+                      xout, ldx, g, eps, u, ldu, h, rows, late, post);
   return launch_pdl(resid_norm_kernel<kFixSeg, 1024>, dim3(grid), dim3(threads), 0, s, ps, resid,
-                    ldr, xout, ldx, g, eps, u, ldu, h, rows, late);
+                    ldr, xout, ldx, g, eps, u, ldu, h, rows, late, post);
 }
 
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,

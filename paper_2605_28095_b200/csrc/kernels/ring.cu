@@ -1,0 +1,370 @@
+// ring.cu — the WaS cache ring on the device (SURVEY.md §8(a) a3 + a4): the remote-weight fetch
+// kernel (K1) and the epoch-flag protocol that replaces host-side CUDA events.
+//
+// "the non-owner issues non-blocking device-to-device copies from r(l)'s HBM
+// into its local cache"; a slot is reserved before the fill, marked ready
+// after it and released after its last reader.  Here every transition is a device flag:
+//
+//   fill[s]  completed fills of slot s     written by the fetch kernel's last CTA (release)
+//   rel[s]   releases of slot s            added by the compute stream after the down GEMM
+//   cons[s]  consumptions started          advanced by the compute stream's ready wait
+//
+// Fill number n of slot s (n = fill[s] when it starts; fills of one slot are ordered on the
+// fetch stream) may start once rel[s] >= n; consumer number c of slot s (c = ++cons[s]) may
+// read once fill[s] >= c and then checks that the slot holds the layer it expects (tag[s]).
+// None of the kernel parameters depends on the step, so a step's kernels replay as a CUDA graph.
+//
+// The fetch itself (fetch_bulk_kernel): TMA bulk copies (cp.async.bulk) staged through a shared-
+// memory ring, issued by one thread per CTA — owner HBM (a peer VA over NVLink, or local in the
+// single-GPU emulation) -> smem -> local slot.  It is launched as clusters of 2 CTAs with ~200 KB
+// of shared memory each, so its CTAs hold whole TPCs that the compute kernels (grids sized to the
+// remaining SMs, kernels.h set_compute_sms) never wait for, and no compute CTA shares their SMs.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../common.cuh"
+#include "../kernels.h"
+
+namespace sidp {
+
+namespace {
+
+SIDP_DEV unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+SIDP_DEV void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+SIDP_DEV void red_release_gpu_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+SIDP_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+SIDP_DEV void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<uint64_t>(gdst)),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+SIDP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// all but the most recent `N` committed store groups have finished READING shared memory
+template <int N>
+SIDP_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+SIDP_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Spin until *p >= v (acquire); bounded by timeout_ns, after which *err |= code.
+SIDP_DEV bool spin_ge(const unsigned long long* p, unsigned long long v, uint64_t timeout_ns,
+                      int* err, int code) {
+  if (ld_acquire_gpu(p) >= v) return true;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_gpu(p) < v) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      if (err) {   // mapped host word, read by the host without a sync (SIDP_ETIMEOUT)
+        *reinterpret_cast<volatile int*>(err) = code;
+        __threadfence_system();
+      }
+      return false;
+    }
+    __nanosleep(128);
+  }
+  return true;
+}
+
+// Run by one thread of every fetch CTA once that CTA's stores of entry `e` are performed: the
+// last CTA to arrive publishes fill e.fill + 1 of the slot (tag, device log entry, then the epoch
+// with release semantics).  Fills of one slot are strictly ordered (the next one is gated on a
+// release that needs this one's consumer), so per-slot counters cannot mix two fills.
+SIDP_DEV void fetch_publish(const FetchArgs& a, const FetchEnt& e, int F) {
+  if (!a.ring) return;
+  FetchRing* r = a.ring;
+  const unsigned prev = atomicAdd(&r->arrive[e.slot], 1u);
+  if (prev != (unsigned)F - 1) return;
+  __threadfence();
+  r->arrive[e.slot] = 0u;
+  r->tag[e.slot] = e.layer;
+  const unsigned long long j = r->nfetch;
+  FetchLogEnt& g = r->log[j % kFetchLogCap];
+  g.j = j;
+  g.layer = e.layer;
+  g.slot = e.slot;
+  g.owner = e.owner;
+  g.epoch = (unsigned long long)e.fill + 1;
+  g.t_start = r->t_first[e.slot];
+  g.t_end = globaltimer_ns();
+  r->t_first[e.slot] = ~0ull;
+  r->nfetch = j + 1;
+  __threadfence();
+  st_release_gpu(&r->fill[e.slot], (unsigned long long)e.fill + 1);
+}
+
+// Windowed gate (one thread per CTA): the slot's previous fill is published and its reader has
+// released it — rel[slot] >= fill.  Waiting here holds this CTA's SM, which the compute grids
+// never count on (their SM budget excludes the fetch's).
+SIDP_DEV void fetch_gate(const FetchArgs& a, const FetchEnt& e) {
+  if (!a.ring || !a.gate) return;
+  spin_ge(&a.ring->fill[e.slot], e.fill, a.timeout_ns, a.err, 4);
+  spin_ge(&a.ring->rel[e.slot], e.fill, a.timeout_ns, a.err, 4);
+}
+
+// K1: a window of pooled layers, each owner arena -> slot, in plan order.  CTA b copies chunks
+// b, b + F, b + 2F, ... of every entry (a layer streams front to back across all CTAs); one
+// thread keeps stages - 1 TMA bulk loads and one bulk store in flight through the shared-memory
+// ring; the last CTA to finish an entry publishes its fill.  One launch per step (or per layer
+// when several computing contexts share the device) keeps the fetch's SMs held between layers,
+// so no compute CTA can slip onto them and delay the next fetch.
+__global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant__ FetchArgs a) {
+  extern __shared__ __align__(128) uint8_t fsm[];
+  const int NST = a.stages;
+  const size_t CH = a.chunk;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(fsm + (size_t)NST * CH);
+  const int F = gridDim.x;
+  const int b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+  fence_barrier_init();
+  if (a.delay_ns) {
+    const uint64_t t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < a.delay_ns) __nanosleep(1000);
+  }
+  const size_t nchunks = (a.bytes + CH - 1) / CH;
+  const size_t mine = nchunks > (size_t)b ? (nchunks - b + F - 1) / F : 0;
+  uint32_t use = 0;   // ring uses so far (stage = use % NST, parity = (use / NST) & 1)
+  for (int k = 0; k < a.n; ++k) {
+    const FetchEnt& e = a.ent[k];
+    fetch_gate(a, e);
+    const uint64_t t_start = globaltimer_ns();
+    if (a.ring) atomicMin(&a.ring->t_first[e.slot], (unsigned long long)t_start);
+    const uint8_t* src = e.src;
+    uint8_t* dst = a.slots + (size_t)e.slot * a.slot_stride;
+    auto chunk_of = [&](size_t i) { return (size_t)b + i * F; };
+    auto len_of = [&](size_t c) { return (uint32_t)std::min<size_t>(CH, a.bytes - c * CH); };
+    auto issue = [&](size_t i) {
+      const size_t c = chunk_of(i);
+      if (a.ns_per_chunk) {   // NVLink-rate emulation: chunk c starts >= c x ns after the start
+        const uint64_t due = t_start + (uint64_t)c * a.ns_per_chunk;
+        while (globaltimer_ns() < due) __nanosleep(256);
+      }
+      const int s = (int)((use + i) % NST);
+      mbar_arrive_expect_tx(&bars[s], len_of(c));
+      bulk_load(fsm + (size_t)s * CH, src + c * CH, len_of(c), &bars[s]);
+    };
+    const size_t pre = std::min<size_t>(mine, NST - 1);
+    for (size_t i = 0; i < pre; ++i) issue(i);
+    for (size_t i = 0; i < mine; ++i) {
+      const uint32_t u = use + (uint32_t)i;
+      const int s = (int)(u % NST);
+      mbar_wait(&bars[s], (u / NST) & 1);
+      const size_t c = chunk_of(i);
+      bulk_store(dst + c * CH, fsm + (size_t)s * CH, len_of(c));
+      bulk_commit();
+      const size_t nxt = i + NST - 1;
+      if (nxt < mine) {
+        bulk_wait_read<1>();   // the stage of load `nxt` was last read by store i - 1
+        issue(nxt);
+      }
+    }
+    use += (uint32_t)mine;
+    bulk_wait_all();           // every store of this CTA performed (and smem free again)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    fetch_publish(a, e, F);
+  }
+}
+
+// Vectorised LDG/STG variant of the same copy (SIDP_FETCH_KIND=ldg; A/B against the bulk copy):
+// 512 threads, 8 x 16-byte loads in flight per thread, CTA b takes vectors b*512 + t + k*F*512.
+__global__ void __launch_bounds__(512, 1) fetch_ldg_kernel(const __grid_constant__ FetchArgs a) {
+  const int F = gridDim.x;
+  if (threadIdx.x == 0 && a.delay_ns) {
+    const uint64_t t0 = globaltimer_ns();
+    while (globaltimer_ns() - t0 < a.delay_ns) __nanosleep(1000);
+  }
+  for (int k = 0; k < a.n; ++k) {
+    const FetchEnt& e = a.ent[k];
+    if (threadIdx.x == 0) fetch_gate(a, e);
+    __syncthreads();
+    const uint64_t t_start = globaltimer_ns();
+    if (threadIdx.x == 0 && a.ring) atomicMin(&a.ring->t_first[e.slot], (unsigned long long)t_start);
+    const uint4* src = reinterpret_cast<const uint4*>(e.src);
+    uint4* dst = reinterpret_cast<uint4*>(a.slots + (size_t)e.slot * a.slot_stride);
+    const size_t nvec = a.bytes / 16, stride = (size_t)F * 512;
+    size_t i = (size_t)blockIdx.x * 512 + threadIdx.x;
+    constexpr int U = 8;
+    const uint64_t ns_iter = a.ns_per_chunk ? a.ns_per_chunk * U * stride * 16 / a.chunk : 0;
+    uint64_t it = 0;
+    for (; i + (U - 1) * stride < nvec; i += U * stride, ++it) {
+      if (ns_iter)
+        while (globaltimer_ns() - t_start < it * ns_iter) __nanosleep(200);
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(src + i + u * stride));
+#pragma unroll
+      for (int u = 0; u < U; ++u) dst[i + u * stride] = v[u];
+    }
+    for (; i < nvec; i += stride) dst[i] = src[i];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) fetch_publish(a, e, F);
+  }
+}
+
+// Fetch-stream gate before fill number `fill` of a slot (per-layer windows): rel[slot] >= fill.
+// One thread; it holds no SM a compute kernel needs.
+__global__ void ring_free_wait_kernel(FetchRing* r, int slot, unsigned long long fill,
+                                      uint64_t timeout_ns, int* err) {
+  spin_ge(&r->rel[slot], fill, timeout_ns, err, 4);
+}
+
+// Compute-stream gate before a remote layer: consumption c = ++cons[s] waits for fill[s] >= c
+// and checks the slot holds `layer` (C-S6: consumed with the tag it was filled with).
+__global__ void ring_ready_wait_kernel(FetchRing* r, int slot, int layer, uint64_t timeout_ns,
+                                       int* err) {
+  pdl_wait();
+  const unsigned long long c = r->cons[slot] + 1;
+  r->cons[slot] = c;
+  if (spin_ge(&r->fill[slot], c, timeout_ns, err, 8)) {
+    const int tag = *reinterpret_cast<volatile int*>(&r->tag[slot]);
+    if (tag != layer && err) {   // protocol violation: the slot holds another layer
+      *reinterpret_cast<volatile int*>(err) = 16;
+      __threadfence_system();
+    }
+    const unsigned long long k = r->ncons;
+    ConsLogEnt& e = r->clog[k % kFetchLogCap];
+    e.layer = layer;
+    e.slot = slot;
+    e.tag = tag;
+    e.epoch = c;
+    e.t = globaltimer_ns();
+    r->ncons = k + 1;
+  }
+}
+
+// Release after the last reader of the slot (stream order: everything before this kernel).
+__global__ void ring_release_kernel(unsigned long long* rel) {
+  pdl_wait();
+  __threadfence();
+  red_release_gpu_add(rel, 1ull);
+}
+
+__global__ void ring_delay_kernel(uint64_t ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+
+}  // namespace
+
+// shared-memory ring geometry: SIDP_BULK_CFG = "<chunk KB>x<stages>" (default 32 x 6)
+static void bulk_geometry(int* chunk, int* stages) {
+  static int c = 0, n = 0;
+  if (!c) {
+    c = kFetchChunk;
+    n = kFetchStages;
+    if (const char* e = getenv("SIDP_BULK_CFG")) {
+      int kb = 0, st = 0;
+      if (sscanf(e, "%dx%d", &kb, &st) == 2 && kb >= 4 && st >= 2 && st <= 16 &&
+          (size_t)kb * 1024 * st <= 200 * 1024) {
+        c = kb * 1024;
+        n = st;
+      }
+    }
+  }
+  *chunk = c;
+  *stages = n;
+}
+
+size_t fetch_bulk_smem() {
+  int c, n;
+  bulk_geometry(&c, &n);
+  return (size_t)std::max(n * c, kFetchStages * kFetchChunk) + 16 * 8;
+}
+
+cudaError_t fetch_bulk_launch(const FetchArgs& a, int ctas, cudaStream_t s) {
+  if (a.bytes == 0 || a.n == 0) return cudaSuccess;
+  if ((a.bytes & 15) || (reinterpret_cast<uintptr_t>(a.slots) & 15) || (a.slot_stride & 15) ||
+      a.n < 0 || a.n > kFetchWindow)
+    return cudaErrorInvalidValue;
+  for (int k = 0; k < a.n; ++k)
+    if ((reinterpret_cast<uintptr_t>(a.ent[k].src) & 15) ||
+        (a.ring && (a.ent[k].slot < 0 || a.ent[k].slot >= kRingMaxSlots)))
+      return cudaErrorInvalidValue;
+  ctas = std::max(2, ctas & ~1);
+  FetchArgs b = a;
+  bulk_geometry(&b.chunk, &b.stages);
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
+    cudaFuncSetAttribute(fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fetch_bulk_smem());
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = fetch_bulk_smem();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;   // CTA pairs: whole TPCs
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  static const bool ldg = getenv("SIDP_FETCH_KIND") && !strcmp(getenv("SIDP_FETCH_KIND"), "ldg");
+  if (ldg) {
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&cfg, fetch_ldg_kernel, b);
+  }
+  return cudaLaunchKernelEx(&cfg, fetch_bulk_kernel, b);
+}
+
+cudaError_t ring_free_wait_launch(FetchRing* r, int slot, unsigned long long fill,
+                                  uint64_t timeout_ns, int* err, cudaStream_t s) {
+  ring_free_wait_kernel<<<1, 1, 0, s>>>(r, slot, fill, timeout_ns, err);
+  return cudaGetLastError();
+}
+
+cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t timeout_ns, int* err,
+                                   cudaStream_t s) {
+  return launch_pdl(ring_ready_wait_kernel, dim3(1), dim3(1), 0, s, r, slot, layer, timeout_ns, err);
+}
+
+cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s) {
+  return launch_pdl(ring_release_kernel, dim3(1), dim3(1), 0, s, rel);
+}
+
+cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s) {
+  if (ns == 0) return cudaSuccess;
+  ring_delay_kernel<<<1, 1, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
+cudaError_t ring_preload() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  if (cudaFuncGetAttributes(&fa, fetch_bulk_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, fetch_ldg_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, ring_free_wait_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, ring_ready_wait_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, ring_release_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, ring_delay_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncSetAttribute(fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fetch_bulk_smem()) != cudaSuccess)
+    e = cudaGetLastError();
+  return e;
+}
+
+}  // namespace sidp

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -94,6 +95,18 @@ struct sidp_ctx {
   int* attn_cnt = nullptr;
   int n_attn_cnt = 0;
   cudaStream_t fetch_stream = nullptr;
+  // SIDP_FETCH_SM: the ring lives on the device (kernels/ring.cu epoch flags + logs); the fetch
+  // kernel holds fetch_ctas SMs (whole TPCs) and the compute kernels size their grids for the
+  // remaining compute_sms.  SIDP_FETCH_CE: the copy engine + CUDA events (the paper's mechanism).
+  sidp::FetchRing* ring = nullptr;
+  bool ring_mode = false;
+  int fetch_ctas = 16;
+  int compute_sms = 0;
+  double tick_ns = 0.0;                  // stagger tick: a measured single-reader layer fetch
+  unsigned long long* release_ptr = nullptr;   // set around a remote layer's compute
+  std::vector<int> gslots;               // slots of the captured graph's remote layers
+  cudaStream_t last_stream = nullptr;    // compute stream of the last step (mode-switch drain)
+  bool graph_fresh = false;              // the graph was just captured (host state advanced)
   std::vector<cudaEvent_t> ready_ev, free_ev;
   std::vector<char> free_recorded;
   std::vector<const bf16*> peer_arena;
@@ -114,7 +127,8 @@ struct sidp_ctx {
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
   // WaS schedule state
   int64_t fetch_j = 0, compute_k = 0;
-  std::vector<int> push, slot_of_fetch;
+  std::vector<int> slot_of_fetch;        // FIFO recurrence, extended lazily (slot_for_fetch)
+  std::vector<unsigned> fills;           // fills enqueued per slot
   std::vector<int32_t> log_t, log_l, log_s;
   int next_layer = 0;
   int64_t step = 0;
@@ -147,6 +161,13 @@ struct sidp_ctx {
 };
 
 namespace {
+
+// Compute-grid SM budget for the duration of one public call (kernels.h set_compute_sms).
+struct BudgetGuard {
+  int prev;
+  explicit BudgetGuard(int n) : prev(sidp::get_compute_sms_budget()) { sidp::set_compute_sms(n); }
+  ~BudgetGuard() { sidp::set_compute_sms(prev); }
+};
 
 bool ck(sidp_ctx* c, cudaError_t e, const char* what) {
   if (e == cudaSuccess) return true;
@@ -230,9 +251,8 @@ int64_t fetch_index_of_compute(const sidp_ctx* c, int64_t k) {
 
 void schedule_reset(sidp_ctx* c) {
   c->fetch_j = c->compute_k = 0;
-  c->push.clear();
-  for (int s = 0; s < c->S; ++s) c->push.push_back(s);
   c->slot_of_fetch.clear();
+  c->fills.assign(c->S, 0u);
   c->log_t.clear();
   c->log_l.clear();
   c->log_s.clear();
@@ -446,7 +466,11 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
     timing_end(ctx, 1, s);
     CK(e);
     count_launch(ctx);
-    CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s));
+    // the fix-up is the fused launch's successor: it releases the WaS slot (if any) once the
+    // fused launch — the last reader of the layer's weights — has completed
+    CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s,
+                               ctx->release_ptr));
+    ctx->release_ptr = nullptr;
     count_launch(ctx);
     ctx->u_for = next_layer;
     return SIDP_OK;
@@ -456,7 +480,11 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
   if (next_g && sidp::gemm_partial_ok(B, h, m.intermediate, ctx->gemm_ws_bytes)) {
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_PARTIAL,
             nullptr, 0, nullptr, 0, nullptr, s, nullptr, &part));
-    if (!(dbg_skip() & 2)) CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s));
+    if (!(dbg_skip() & 2)) {
+      CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s,
+                                 ctx->release_ptr));   // successor of the down GEMM
+      ctx->release_ptr = nullptr;
+    }
     count_launch(ctx);
     ctx->u_for = next_layer;
   } else {
@@ -474,68 +502,152 @@ sidp_status full_layer(sidp_ctx* ctx, const LayerW& W, bf16* x, int B, int layer
 }
 
 // ---- WaS fetch pump ----
-sidp_status enqueue_fetch(sidp_ctx* ctx) {
-  const int64_t j = ctx->fetch_j;
-  const int s = ctx->push[j];
-  const int64_t t = j / ctx->R;
-  const int l = ctx->plan[j % ctx->R];
-  if (ctx->stagger_pending) {
-    ctx->stagger_pending = false;
-    const int ticks = stagger_ticks_of(ctx);
-    if (ticks > 0) {
-      // one tick = one single-reader layer fetch at the NVLink peer-copy rate (~770 GB/s)
-      const double tick_ns = (double)ctx->pooled_elems * 2.0 / 770.0;
-      CK(sidp::delay_launch((uint64_t)(ticks * tick_ns), ctx->fetch_stream));
-      count_launch(ctx);
-    }
-  }
-  if (ctx->free_recorded[s]) CK(cudaStreamWaitEvent(ctx->fetch_stream, ctx->free_ev[s], 0));
-  const bf16* src = ctx->peer_arena[ctx->owner[l]];
-  if (!src) return fail(SIDP_ESTATE, "peer arena of rank %d not imported", ctx->owner[l]);
-  src += (size_t)ctx->owned_index[l] * ctx->pooled_elems;
-  bf16* dst = ctx->slots + (size_t)s * ctx->pooled_elems;
-  const size_t bytes = ctx->pooled_elems * 2;
-  timing_begin(ctx, 3, ctx->fetch_stream);
-  if (ctx->c.fetch_engine == SIDP_FETCH_CE && ctx->c.fetch_pace_gbps > 0.0f) {
-    // emulation only: copy-engine chunks (SIDP_CE_CHUNK_MB, default 16) released at the paced rate
-    // (SIDP_CE_CHUNK_MB, default 64); a last pace point holds the layer's completion (and so its
-    // ready flag) until bytes / rate after the start, so bursts never beat the emulated link
-    static const size_t chunk_mb = getenv("SIDP_CE_CHUNK_MB") ? std::max(1, atoi(getenv("SIDP_CE_CHUNK_MB"))) : 64;
-    const size_t chunk = chunk_mb << 20;
-    for (size_t off = 0, i = 0; off < bytes; off += chunk, ++i) {
-      CK(sidp::pace_launch(ctx->pace_t0, i == 0, (uint64_t)((double)off / ctx->c.fetch_pace_gbps),
-                           ctx->fetch_stream));
-      CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + off,
-                         reinterpret_cast<const uint8_t*>(src) + off, std::min(chunk, bytes - off),
-                         cudaMemcpyDefault, ctx->fetch_stream));
-    }
-    CK(sidp::pace_launch(ctx->pace_t0, 0, (uint64_t)((double)bytes / ctx->c.fetch_pace_gbps),
-                         ctx->fetch_stream));
-  } else if (ctx->c.fetch_engine == SIDP_FETCH_CE) {
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
-  } else {
-    CK(sidp::fetch_launch(dst, src, bytes, ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 16,
-                          ctx->fetch_stream, ctx->c.fetch_pace_gbps));
-  }
-  timing_end(ctx, 3, ctx->fetch_stream);
-  count_launch(ctx);
-  CK(cudaEventRecord(ctx->ready_ev[s], ctx->fetch_stream));
-  ctx->slot_of_fetch.push_back(s);
-  ctx->log_t.push_back((int32_t)t);
-  ctx->log_l.push_back(l);
-  ctx->log_s.push_back(s);
-  ctx->st.fetches++;
-  ctx->st.bytes_fetched += bytes;
-  ctx->fetch_j++;
-  return SIDP_OK;
+// Zero the device ring (epochs, counters, logs' indices) — at allocation and whenever the host
+// schedule restarts (mode switch; nothing of the ring is in flight then).
+cudaError_t ring_reset_device(sidp_ctx* ctx) {
+  if (!ctx->ring) return cudaSuccess;
+  cudaError_t e = cudaMemset(ctx->ring, 0, offsetof(sidp::FetchRing, log));
+  if (e != cudaSuccess) return e;
+  std::vector<unsigned long long> inf(sidp::kRingMaxSlots, ~0ull);
+  return cudaMemcpy(ctx->ring->t_first, inf.data(), inf.size() * sizeof(inf[0]),
+                    cudaMemcpyHostToDevice);
 }
 
-sidp_status pump(sidp_ctx* ctx) {
-  while (ctx->R > 0 && ctx->fetch_j < (int64_t)ctx->push.size()) {
-    sidp_status st = enqueue_fetch(ctx);
-    if (st != SIDP_OK) return st;
+// FIFO free-list recurrence, extended lazily: slot(fetch j) = j for j < S, else
+// the slot freed by remote compute entry k = j - S, i.e. slot(fetch p(k)).  Timing-independent,
+// so the host knows every fetch's slot ahead of the device.
+int slot_for_fetch(sidp_ctx* c, int64_t j) {
+  while ((int64_t)c->slot_of_fetch.size() <= j) {
+    const int64_t jj = (int64_t)c->slot_of_fetch.size();
+    c->slot_of_fetch.push_back(jj < c->S ? (int)jj
+                                         : c->slot_of_fetch[fetch_index_of_compute(c, jj - c->S)]);
   }
-  return SIDP_OK;
+  return c->slot_of_fetch[j];
+}
+
+// Computing SM-fetch contexts per device (process-wide).  With one, the fetch of a whole step is
+// ONE launch whose CTAs gate themselves on the release flags (its SMs stay held between layers);
+// with several (virtual ranks on one GPU) each fetch is its own launch behind a one-thread gate
+// kernel, so no fetch CTA ever waits while holding an SM another context's compute needs.
+std::vector<int>& ring_ctx_count() {
+  static std::vector<int> v(64, 0);
+  return v;
+}
+bool fetch_windowed(const sidp_ctx* ctx) {
+  static const int env = getenv("SIDP_FETCH_WINDOW") ? atoi(getenv("SIDP_FETCH_WINDOW")) : -1;
+  if (env >= 0) return env != 0;
+  return ring_ctx_count()[ctx->c.device & 63] <= 1;
+}
+
+// Enqueue fetches [fetch_j, upto) on the fetch stream: the device ring takes them
+// as one windowed launch (or one launch per fetch); the copy engine one copy per fetch.
+sidp_status enqueue_fetches(sidp_ctx* ctx, int64_t upto) {
+  if (ctx->R == 0 || upto <= ctx->fetch_j) return SIDP_OK;
+  const size_t bytes = ctx->pooled_elems * 2;
+  uint64_t delay_ns = 0;
+  if (ctx->stagger_pending) {
+    ctx->stagger_pending = false;
+    // one tick = one single-reader layer fetch: measured at sidp_import_handles (tick_ns),
+    // else the layer's bytes at the NVLink 5 peer-copy rate (~770 GB/s)
+    const double tick = ctx->tick_ns > 0.0 ? ctx->tick_ns : (double)bytes / 770.0;
+    delay_ns = (uint64_t)(stagger_ticks_of(ctx) * tick);
+  }
+  const bool tm = !ctx->capturing;   // fetch-class timing (the fetch stream is never captured)
+  const bool windowed = ctx->ring_mode && fetch_windowed(ctx);
+  sidp::FetchArgs fa{};
+  fa.slots = reinterpret_cast<uint8_t*>(ctx->slots);
+  fa.slot_stride = bytes;
+  fa.bytes = bytes;
+  fa.ring = ctx->ring;
+  fa.gate = windowed ? 1 : 0;
+  fa.timeout_ns = ctx->cas_timeout_ns;
+  fa.err = ctx->dev_err;
+  // emulated link rate: chunk c (kFetchChunk bytes) no earlier than c x chunk / rate
+  fa.ns_per_chunk = ctx->c.fetch_pace_gbps > 0.0f
+                        ? (uint64_t)((double)sidp::kFetchChunk / ctx->c.fetch_pace_gbps) : 0;
+  auto launch_window = [&]() -> sidp_status {
+    if (fa.n == 0) return SIDP_OK;
+    if (tm) timing_begin(ctx, 3, ctx->fetch_stream);
+    CK(sidp::fetch_bulk_launch(fa, ctx->fetch_ctas, ctx->fetch_stream));
+    if (tm) timing_end(ctx, 3, ctx->fetch_stream);
+    count_launch(ctx);
+    fa.n = 0;
+    fa.delay_ns = 0;
+    return SIDP_OK;
+  };
+  if (delay_ns && !windowed) {
+    CK(sidp::delay_launch(delay_ns, ctx->fetch_stream));
+    count_launch(ctx);
+    delay_ns = 0;
+  }
+  fa.delay_ns = delay_ns;
+  for (; ctx->fetch_j < upto; ctx->fetch_j++) {
+    const int64_t j = ctx->fetch_j;
+    const int s = slot_for_fetch(ctx, j);
+    const int l = ctx->plan[j % ctx->R];
+    const bf16* src = ctx->peer_arena[ctx->owner[l]];
+    if (!src) return fail(SIDP_ESTATE, "peer arena of rank %d not imported", ctx->owner[l]);
+    src += (size_t)ctx->owned_index[l] * ctx->pooled_elems;
+    bf16* dst = ctx->slots + (size_t)s * ctx->pooled_elems;
+    ctx->log_t.push_back((int32_t)(j / ctx->R));
+    ctx->log_l.push_back(l);
+    ctx->log_s.push_back(s);
+    ctx->st.fetches++;
+    ctx->st.bytes_fetched += bytes;
+    const unsigned fill = ctx->fills[s]++;
+    if (ctx->ring_mode) {
+      // device ring: the window's CTAs (or a one-thread gate kernel) wait for the slot's release
+      // epoch; the last CTA done with a fetch publishes its fill epoch + the device log entry
+      if (!windowed) {
+        CK(sidp::ring_free_wait_launch(ctx->ring, s, fill, ctx->cas_timeout_ns, ctx->dev_err,
+                                       ctx->fetch_stream));
+        count_launch(ctx);
+      }
+      fa.ent[fa.n++] = sidp::FetchEnt{reinterpret_cast<const uint8_t*>(src), l, s, ctx->owner[l], fill};
+      if (!windowed || fa.n == sidp::kFetchWindow) {
+        sidp_status st = launch_window();
+        if (st != SIDP_OK) return st;
+      }
+      continue;
+    }
+    // copy engine + CUDA events (the paper's mechanism)
+    if (ctx->free_recorded[s]) CK(cudaStreamWaitEvent(ctx->fetch_stream, ctx->free_ev[s], 0));
+    if (tm) timing_begin(ctx, 3, ctx->fetch_stream);
+    if (ctx->c.fetch_pace_gbps > 0.0f) {
+      // emulation only: copy-engine chunks (SIDP_CE_CHUNK_MB, default 64) released at the paced
+      // rate; a last pace point holds the layer's completion (and so its ready flag) until
+      // bytes / rate after the start, so bursts never beat the emulated link
+      static const size_t chunk_mb = getenv("SIDP_CE_CHUNK_MB") ? std::max(1, atoi(getenv("SIDP_CE_CHUNK_MB"))) : 64;
+      const size_t chunk = chunk_mb << 20;
+      for (size_t off = 0, i = 0; off < bytes; off += chunk, ++i) {
+        CK(sidp::pace_launch(ctx->pace_t0, i == 0, (uint64_t)((double)off / ctx->c.fetch_pace_gbps),
+                             ctx->fetch_stream));
+        CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(dst) + off,
+                           reinterpret_cast<const uint8_t*>(src) + off, std::min(chunk, bytes - off),
+                           cudaMemcpyDefault, ctx->fetch_stream));
+      }
+      CK(sidp::pace_launch(ctx->pace_t0, 0, (uint64_t)((double)bytes / ctx->c.fetch_pace_gbps),
+                           ctx->fetch_stream));
+    } else {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
+    }
+    if (tm) timing_end(ctx, 3, ctx->fetch_stream);
+    count_launch(ctx);
+    CK(cudaEventRecord(ctx->ready_ev[s], ctx->fetch_stream));
+  }
+  return launch_window();
+}
+
+// Keep the fetch stream S fetches ahead of the remote compute entries enqueued so far (the FIFO
+// free-list: fetch j needs the slot freed by compute entry j - S).  With the windowed device
+// ring, sidp_step enqueues the whole step's window up front instead (pump_step).
+sidp_status pump(sidp_ctx* ctx) { return enqueue_fetches(ctx, ctx->compute_k + ctx->S); }
+
+// sidp_step, device ring with one computing context: the step's remaining fetches plus the next
+// step's first S (the lookahead that overlaps this step's tail) as one launch.
+sidp_status pump_step(sidp_ctx* ctx) {
+  if (!ctx->ring_mode || !fetch_windowed(ctx)) return pump(ctx);
+  return enqueue_fetches(ctx, ctx->compute_k + ctx->R + ctx->S);
 }
 
 sidp_status check_ready(sidp_ctx* ctx) {
@@ -574,14 +686,28 @@ sidp_status was_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* k
     st = pump(ctx);
     if (st != SIDP_OK) return st;
     if (p >= ctx->fetch_j) return fail(SIDP_ESTATE, "slot ring deadlock (plan lag >= slots)");
-    const int slot = ctx->slot_of_fetch[p];
-    CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
+    const int slot = slot_for_fetch(ctx, p);
     const bf16* pooled = ctx->slots + (size_t)slot * ctx->pooled_elems;
-    st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
-    if (st != SIDP_OK) return st;
-    CK(cudaEventRecord(ctx->free_ev[slot], s));   // housekeeper: release after last reader
-    ctx->free_recorded[slot] = 1;
-    ctx->push.push_back(slot);
+    if (ctx->ring_mode) {
+      // device flags: wait for this consumption's fill epoch (and check the slot's layer tag);
+      // the release rides on the kernel after the layer's last weight reader
+      CK(sidp::ring_ready_wait_launch(ctx->ring, slot, layer, ctx->cas_timeout_ns, ctx->dev_err, s));
+      count_launch(ctx);
+      ctx->release_ptr = &ctx->ring->rel[slot];
+      st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
+      if (st != SIDP_OK) return st;
+      if (ctx->release_ptr) {   // no fused carrier kernel took it: a release kernel
+        CK(sidp::ring_release_launch(ctx->release_ptr, s));
+        count_launch(ctx);
+        ctx->release_ptr = nullptr;
+      }
+    } else {
+      CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
+      st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
+      if (st != SIDP_OK) return st;
+      CK(cudaEventRecord(ctx->free_ev[slot], s));   // housekeeper: release after last reader
+      ctx->free_recorded[slot] = 1;
+    }
     ctx->compute_k++;
     st = pump(ctx);
   }
@@ -831,6 +957,7 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
   if (cfg->pool_scope != SIDP_POOL_LAYER && cfg->pool_scope != SIDP_POOL_FFN)
     return fail(SIDP_EINVAL, "bad pool_scope");
   if (cfg->max_batch < 1 || cfg->max_ctx < 1) return fail(SIDP_EINVAL, "max_batch/max_ctx >= 1");
+  if (cfg->compute_sms < 0 || cfg->fetch_sms < 0) return fail(SIDP_EINVAL, "negative SM count");
   std::vector<int> owner(m.num_layers);
   for (int l = 0; l < m.num_layers; ++l) {
     owner[l] = cfg->layer_owner ? cfg->layer_owner[l] : l % cfg->world;
@@ -876,6 +1003,7 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
 
 void sidp_destroy(sidp_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->ring_mode) ring_ctx_count()[ctx->c.device & 63]--;
   if (ctx->allocated) {
     cudaSetDevice(ctx->c.device);
     cudaDeviceSynchronize();
@@ -888,7 +1016,7 @@ void sidp_destroy(sidp_ctx* ctx) {
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
-                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0};
+                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0, ctx->ring};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (ctx->host_err) cudaFreeHost(const_cast<int*>(ctx->host_err));
@@ -982,6 +1110,23 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   DM(ctx->xfer_cnt, sizeof(unsigned int));
   CK(cudaMemset(ctx->xfer_cnt, 0, sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&ctx->fetch_stream, cudaStreamNonBlocking));
+  // WaS ring on the device (SIDP_FETCH_SM): epoch flags + logs; the fetch kernel's CTA pairs
+  // hold fetch_ctas SMs, the compute kernels size their grids for the rest
+  ctx->ring_mode = ctx->R > 0 && ctx->c.fetch_engine == SIDP_FETCH_SM;
+  if (ctx->ring_mode) {
+    ring_ctx_count()[ctx->c.device & 63]++;
+    if (ctx->S > sidp::kRingMaxSlots)
+      return fail(SIDP_EINVAL, "was_slots %d > %d with the SM fetch", ctx->S, sidp::kRingMaxSlots);
+    DM(ctx->ring, sizeof(sidp::FetchRing));
+    CK(ring_reset_device(ctx));
+    int dev_sms = 0;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->c.device));
+    ctx->fetch_ctas = std::max(2, (ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 16) & ~1);
+    ctx->fetch_ctas = std::min(ctx->fetch_ctas, std::max(2, (dev_sms / 2) & ~1));
+    ctx->compute_sms = std::max(2, (dev_sms - ctx->fetch_ctas) & ~1);
+    CK(sidp::ring_preload());
+  }
+  if (ctx->c.compute_sms > 0) ctx->compute_sms = std::max(2, ctx->c.compute_sms & ~1);
   ctx->ready_ev.resize(ctx->S);
   ctx->free_ev.resize(ctx->S);
   ctx->free_recorded.assign(ctx->S, 0);
@@ -994,6 +1139,10 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   // deadlock.  Load every kernel now.
   CK(sidp::gemm_preload());
   sidp::mlp_prepare(m.hidden, m.intermediate, ctx->gemm_ws_bytes);
+  if (ctx->compute_sms > 0) {   // the fused MLP's schedule for the WaS compute budget too
+    BudgetGuard budget(ctx->compute_sms);
+    sidp::mlp_prepare(m.hidden, m.intermediate, ctx->gemm_ws_bytes);
+  }
   CK(sidp::attention_preload());
   CK(sidp::norm_preload());
   CK(sidp::fetch_preload());
@@ -1170,6 +1319,43 @@ sidp_status sidp_import_handles(sidp_ctx* ctx, const void* const* blobs, const s
     ctx->ipc_opened.push_back(p);
     ctx->peer_cas[q] = reinterpret_cast<uint8_t*>(p);
   }
+  // Stagger tick (C-S7): one single-reader fetch of the first planned layer from its owner into
+  // slot 0, timed on the fetch stream with the engine the run uses (no step has started, so
+  // the slot is free).  Replaces an assumed link rate.
+  if (ctx->R > 0 && !ctx->serve_only && ctx->slots) {
+    const int l = ctx->plan[0];
+    const bf16* src = ctx->peer_arena[ctx->owner[l]];
+    if (src) {
+      src += (size_t)ctx->owned_index[l] * ctx->pooled_elems;
+      const size_t bytes = ctx->pooled_elems * 2;
+      cudaEvent_t e0, e1;
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, ctx->fetch_stream));
+      if (ctx->ring_mode) {
+        sidp::FetchArgs fa{};
+        fa.slots = reinterpret_cast<uint8_t*>(ctx->slots);
+        fa.slot_stride = bytes;
+        fa.bytes = bytes;
+        fa.n = 1;
+        fa.ent[0] = sidp::FetchEnt{reinterpret_cast<const uint8_t*>(src), l, 0, ctx->owner[l], 0};
+        fa.ns_per_chunk = ctx->c.fetch_pace_gbps > 0.0f
+                              ? (uint64_t)((double)sidp::kFetchChunk / ctx->c.fetch_pace_gbps) : 0;
+        CK(sidp::fetch_bulk_launch(fa, ctx->fetch_ctas, ctx->fetch_stream));
+      } else {
+        CK(cudaMemcpyAsync(ctx->slots, src, bytes, cudaMemcpyDefault, ctx->fetch_stream));
+      }
+      CK(cudaEventRecord(e1, ctx->fetch_stream));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.0f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      ctx->tick_ns = (double)ms * 1e6;
+      if (ctx->c.fetch_engine == SIDP_FETCH_CE && ctx->c.fetch_pace_gbps > 0.0f)
+        ctx->tick_ns = std::max(ctx->tick_ns, (double)bytes / ctx->c.fetch_pace_gbps);
+    }
+  }
   return SIDP_OK;
 }
 
@@ -1186,6 +1372,7 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
   if (st != SIDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   bf16* xb = reinterpret_cast<bf16*>(x);
+  BudgetGuard budget(mode == SIDP_CAS ? 0 : ctx->compute_sms);
   if (mode == SIDP_REPLICATED) {
     if (ctx->d != 1) return fail(SIDP_EINVAL, "SIDP_REPLICATED needs world == 1");
     mode = SIDP_WAS;
@@ -1197,11 +1384,16 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
         const int64_t p = fetch_index_of_compute(ctx, ctx->compute_k);
         st = pump(ctx);
         if (st != SIDP_OK) return st;
-        const int slot = ctx->slot_of_fetch[p];
-        CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
-        CK(cudaEventRecord(ctx->free_ev[slot], s));
-        ctx->free_recorded[slot] = 1;
-        ctx->push.push_back(slot);
+        const int slot = slot_for_fetch(ctx, p);
+        if (ctx->ring_mode) {
+          CK(sidp::ring_ready_wait_launch(ctx->ring, slot, layer, ctx->cas_timeout_ns, ctx->dev_err, s));
+          CK(sidp::ring_release_launch(&ctx->ring->rel[slot], s));
+          count_launch(ctx, 2);
+        } else {
+          CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
+          CK(cudaEventRecord(ctx->free_ev[slot], s));
+          ctx->free_recorded[slot] = 1;
+        }
         ctx->compute_k++;
         st = pump(ctx);
         if (st != SIDP_OK) return st;
@@ -1260,14 +1452,39 @@ static sidp_status step_body(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s)
   return SIDP_OK;
 }
 
-// CUDA graphs (launch-bound inner loop: ~700 kernels per step).  A step is replayable when it
-// touches no WaS ring (every layer local) and its pointers / batch / timing mask are unchanged;
-// kernel parameters never depend on the step index (positions live on the device).
+// CUDA graphs (launch-bound inner loop: ~700 kernels per step).  A step is replayable when its
+// pointers / batch / timing mask are unchanged and, with a WaS ring, when it is on the device
+// (SIDP_FETCH_SM: ready waits and releases are device epoch flags whose parameters name only
+// the slot) and the remote layers consume the same slots as in the captured step; kernel
+// parameters never depend on the step index (positions live on the device).  The fetch stream
+// is never captured: its fetches are enqueued by the host pump around each replay.
 static bool graph_eligible(const sidp_ctx* ctx, const sidp_batch* b) {
   static const bool enabled = !(getenv("SIDP_GRAPH") && atoi(getenv("SIDP_GRAPH")) == 0);
   const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
-  return enabled && mode == SIDP_WAS && ctx->R == 0 && b->batch > 0 && !b->logits &&
-         !b->layer_inputs;
+  return enabled && mode == SIDP_WAS && (ctx->R == 0 || (ctx->ring_mode && !ctx->stagger_pending)) &&
+         b->batch > 0 && !b->logits && !b->layer_inputs;
+}
+
+// Slots the remote layers of pass `ahead` (0 = the coming step) consume (FIFO recurrence).
+static std::vector<int> coming_slots(sidp_ctx* ctx, int ahead) {
+  std::vector<int> out;
+  const int64_t k0 = ctx->compute_k + (int64_t)ahead * ctx->R;
+  for (int64_t k = k0; k < k0 + ctx->R; ++k)
+    out.push_back(slot_for_fetch(ctx, fetch_index_of_compute(ctx, k)));
+  return out;
+}
+
+// Host bookkeeping of one replayed step's remote layers (what was_layer does while enqueuing).
+static sidp_status replay_bookkeeping(sidp_ctx* ctx) {
+  for (int l = 0; l < ctx->L; ++l) {
+    if (ctx->owner[l] == ctx->r) continue;
+    const int64_t p = fetch_index_of_compute(ctx, ctx->compute_k);
+    sidp_status st = pump(ctx);
+    if (st != SIDP_OK) return st;
+    if (p >= ctx->fetch_j) return fail(SIDP_ESTATE, "slot ring deadlock (plan lag >= slots)");
+    ctx->compute_k++;
+  }
+  return pump(ctx);
 }
 
 static void graph_drop(sidp_ctx* ctx) {
@@ -1300,17 +1517,38 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
   if (ctx->pending_mode >= 0 && ctx->step >= ctx->pending_step) {
     if (ctx->pending_mode != ctx->mode) {
       ctx->mode = ctx->pending_mode;
-      // drain: wait for in-flight fetches, then restart the plan (reading C-A7)
+      // drain: wait for in-flight fetches (and, for the device ring, the compute stream's last
+      // waits / releases), then restart the plan (reading C-A7)
+      CK(cudaStreamSynchronize(ctx->fetch_stream));
+      if (ctx->ring_mode && ctx->last_stream) CK(cudaStreamSynchronize(ctx->last_stream));
       CK(cudaStreamSynchronize(ctx->fetch_stream));
       std::fill(ctx->free_recorded.begin(), ctx->free_recorded.end(), 0);
       schedule_reset(ctx);
+      graph_drop(ctx);
+      if (ctx->ring_mode) CK(ring_reset_device(ctx));
     }
     ctx->pending_mode = -1;
     ctx->st.mode = ctx->mode;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (s != nullptr && graph_eligible(ctx, b)) {   // capture needs a non-default stream
-    if (!graph_key_matches(ctx, b)) {
+  ctx->last_stream = s;
+  BudgetGuard budget(ctx->mode == SIDP_CAS ? 0 : ctx->compute_sms);
+  if (ctx->mode != SIDP_CAS && ctx->R > 0) {
+    // the step's fetches (+ the next step's first S) up front: one launch with the windowed
+    // device ring, else the first S (the layers' pumps add the rest as slots free up)
+    st = pump_step(ctx);
+    if (st != SIDP_OK) return st;
+  }
+  std::vector<int> slots_now;
+  bool replayable = s != nullptr && graph_eligible(ctx, b);   // capture needs a non-default stream
+  if (replayable && ctx->R > 0) {
+    slots_now = coming_slots(ctx, 0);
+    // capture only a step whose successor consumes the same slots (else eager every step)
+    if (!(ctx->gexec && ctx->gslots == slots_now) && slots_now != coming_slots(ctx, 1))
+      replayable = false;
+  }
+  if (replayable) {
+    if (!graph_key_matches(ctx, b) || ctx->gslots != slots_now) {
       graph_drop(ctx);
       if (ctx->tev_used > 0) timing_flush(ctx);
       const uint64_t l0 = ctx->st.launches;
@@ -1332,7 +1570,9 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
       ctx->graph_launches = ctx->st.launches - l0;
       ctx->st.launches = l0;
       ctx->gkey = GraphKey{B, b->tokens, b->next, b->kv.k_cache, b->kv.v_cache, b->kv.pos, b->pos_out};
+      ctx->gslots = slots_now;
       ctx->gmask = ctx->timed_mask;
+      ctx->graph_fresh = true;   // capture enqueued this step's fetches and bookkeeping
       ctx->graph_tev_pairs = ctx->tev_used / 2;
       ctx->graph_timed_pending = false;
       for (int i = 0; i < 8; ++i) {
@@ -1342,7 +1582,13 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
     }
     // harvest the previous replay's kernel timings before the events are re-recorded
     if (ctx->graph_timed_pending) graph_harvest(ctx);
+    const bool fresh = ctx->graph_fresh;
+    ctx->graph_fresh = false;
     CK(cudaGraphLaunch(ctx->gexec, s));
+    if (!fresh && ctx->R > 0) {
+      st = replay_bookkeeping(ctx);
+      if (st != SIDP_OK) return st;
+    }
     ctx->st.launches += ctx->graph_launches;
     ctx->graph_timed_pending = ctx->graph_tev_pairs > 0;
     ctx->step++;
@@ -1428,9 +1674,42 @@ sidp_status sidp_stagger_ticks(const sidp_ctx* ctx, int32_t* ticks) {
   return SIDP_OK;
 }
 
+// SIDP_FETCH_SM: the device log the fetch kernels wrote (what was actually copied, in fetch
+// order since the last plan reset; synchronises the fetch stream).  SIDP_FETCH_CE: the host's
+// enqueue log (the copy engine writes no log of its own).
+static sidp_status read_device_log(const sidp_ctx* ctx, std::vector<sidp::FetchLogEnt>& out) {
+  out.clear();
+  if (!ctx->ring_mode || !ctx->allocated) return SIDP_OK;
+  if (cudaStreamSynchronize(ctx->fetch_stream) != cudaSuccess) return fail(SIDP_ECUDA, "fetch stream");
+  unsigned long long n = 0;
+  if (cudaMemcpy(&n, &ctx->ring->nfetch, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SIDP_ECUDA, "fetch log count");
+  const unsigned long long first = n > (unsigned long long)sidp::kFetchLogCap ? n - sidp::kFetchLogCap : 0;
+  std::vector<sidp::FetchLogEnt> all(sidp::kFetchLogCap);
+  if (cudaMemcpy(all.data(), ctx->ring->log, sizeof(sidp::FetchLogEnt) * all.size(),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SIDP_ECUDA, "fetch log");
+  for (unsigned long long j = first; j < n; ++j) out.push_back(all[j % sidp::kFetchLogCap]);
+  return SIDP_OK;
+}
+
 sidp_status sidp_get_fetch_log(const sidp_ctx* ctx, int32_t* fetch_step, int32_t* fetch_layer,
                                int32_t* fetch_slot, int32_t capacity, int32_t* n) {
   if (!ctx || !n) return fail(SIDP_EINVAL, "null argument");
+  if (ctx->ring_mode && ctx->allocated) {
+    std::vector<sidp::FetchLogEnt> lg;
+    sidp_status st = read_device_log(ctx, lg);
+    if (st != SIDP_OK) return st;
+    *n = (int32_t)lg.size();
+    if (!fetch_step) return SIDP_OK;
+    if (capacity < *n) return fail(SIDP_EINVAL, "capacity too small");
+    for (int32_t i = 0; i < *n; ++i) {
+      fetch_step[i] = (int32_t)(lg[i].j / std::max(1, ctx->R));
+      fetch_layer[i] = lg[i].layer;
+      fetch_slot[i] = lg[i].slot;
+    }
+    return SIDP_OK;
+  }
   *n = (int32_t)ctx->log_t.size();
   if (!fetch_step) return SIDP_OK;
   if (capacity < *n) return fail(SIDP_EINVAL, "capacity too small");
@@ -1438,6 +1717,50 @@ sidp_status sidp_get_fetch_log(const sidp_ctx* ctx, int32_t* fetch_step, int32_t
     fetch_step[i] = ctx->log_t[i];
     fetch_layer[i] = ctx->log_l[i];
     fetch_slot[i] = ctx->log_s[i];
+  }
+  return SIDP_OK;
+}
+
+sidp_status sidp_get_fetch_trace(const sidp_ctx* ctx, int64_t* out, int32_t capacity, int32_t* n) {
+  if (!ctx || !n) return fail(SIDP_EINVAL, "null argument");
+  if (!ctx->ring_mode) {
+    *n = 0;
+    return SIDP_OK;
+  }
+  std::vector<sidp::FetchLogEnt> lg;
+  sidp_status st = read_device_log(ctx, lg);
+  if (st != SIDP_OK) return st;
+  *n = (int32_t)lg.size();
+  if (!out) return SIDP_OK;
+  if (capacity < *n) return fail(SIDP_EINVAL, "capacity too small");
+  for (int32_t i = 0; i < *n; ++i) {
+    int64_t* e = out + (size_t)i * 7;
+    e[0] = (int64_t)lg[i].j; e[1] = lg[i].layer; e[2] = lg[i].slot; e[3] = lg[i].owner;
+    e[4] = (int64_t)lg[i].epoch; e[5] = (int64_t)lg[i].t_start; e[6] = (int64_t)lg[i].t_end;
+  }
+  return SIDP_OK;
+}
+
+sidp_status sidp_get_consume_log(const sidp_ctx* ctx, int64_t* out, int32_t capacity, int32_t* n) {
+  if (!ctx || !n) return fail(SIDP_EINVAL, "null argument");
+  *n = 0;
+  if (!ctx->ring_mode || !ctx->allocated) return SIDP_OK;
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(SIDP_ECUDA, "sync");
+  unsigned long long cnt = 0;
+  if (cudaMemcpy(&cnt, &ctx->ring->ncons, sizeof(cnt), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SIDP_ECUDA, "consume log count");
+  std::vector<sidp::ConsLogEnt> all(sidp::kFetchLogCap);
+  if (cudaMemcpy(all.data(), ctx->ring->clog, sizeof(sidp::ConsLogEnt) * all.size(),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SIDP_ECUDA, "consume log");
+  const unsigned long long first = cnt > (unsigned long long)sidp::kFetchLogCap ? cnt - sidp::kFetchLogCap : 0;
+  *n = (int32_t)(cnt - first);
+  if (!out) return SIDP_OK;
+  if (capacity < *n) return fail(SIDP_EINVAL, "capacity too small");
+  for (unsigned long long k = first; k < cnt; ++k) {
+    const sidp::ConsLogEnt& c = all[k % sidp::kFetchLogCap];
+    int64_t* e = out + (size_t)(k - first) * 5;
+    e[0] = c.layer; e[1] = c.slot; e[2] = c.tag; e[3] = (int64_t)c.epoch; e[4] = (int64_t)c.t;
   }
   return SIDP_OK;
 }
@@ -1450,6 +1773,9 @@ sidp_status sidp_stats(const sidp_ctx* ctx_c, sidp_stats_t* out) {
     if (ctx->tev_used > 0) timing_flush(ctx);
   }
   for (int i = 0; i < 8; ++i) ctx->st.timed_ms[i] = ctx->timed_acc_ms[i];
+  ctx->st.fetch_sms_held = ctx->ring_mode ? ctx->fetch_ctas : 0;
+  ctx->st.compute_sms = ctx->compute_sms;
+  ctx->st.stagger_tick_ns = ctx->tick_ns;
   *out = ctx->st;
   return SIDP_OK;
 }
@@ -1605,8 +1931,20 @@ sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uin
 sidp_status sidp_test_fetch(void* dst, const void* src, size_t bytes, int32_t ctas, int32_t engine,
                             void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t e = engine == SIDP_FETCH_CE ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s)
-                                          : sidp::fetch_launch(dst, src, bytes, ctas, s);
+  cudaError_t e;
+  if (engine == SIDP_FETCH_CE) {
+    e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
+  } else if (engine == 2) {   // the vectorised LDG/STG copy kernel (round-1 K1, kept for A/B)
+    e = sidp::fetch_launch(dst, src, bytes, ctas, s);
+  } else {                    // K1: TMA bulk copies through shared memory, CTA pairs
+    sidp::FetchArgs a{};
+    a.slots = reinterpret_cast<uint8_t*>(dst);
+    a.slot_stride = 0;
+    a.bytes = bytes;
+    a.n = 1;
+    a.ent[0] = sidp::FetchEnt{reinterpret_cast<const uint8_t*>(src), 0, 0, 0, 0};
+    e = sidp::fetch_bulk_launch(a, ctas, s);
+  }
   if (e != cudaSuccess) return fail(SIDP_ECUDA, "fetch: %s", cudaGetErrorString(e));
   return SIDP_OK;
 }

@@ -75,4 +75,41 @@ def oracle_steps(m, seed, om, toks, pos, caches, steps):
     return out
 
 
-__all__ = ["OracleModel", "rank_inputs", "oracle_layer", "rel_err", "oracle_steps", "OS", "OSD"]
+def cas_oracle_check(m, om: OracleModel, d, pool, dumps, logits, caches, pos, tol):
+    """Teacher-forced CaS parity against the ORACLE's CaS layer (oracle/sidp.py cas_layer: the
+    owner fuses the live ranks' rows in ascending rank order; dummy ranks are
+    absent).  Per live rank r (keys of `dumps`): dumps[r] [L, B_r, h] the GPU's
+    bf16 layer inputs, logits[r] [B_r, V], caches[r] = (K, V) [L, B_r, T, n_kv, hd] the GPU's KV
+    state after the step, pos[r] the step's positions.  Each layer's oracle output must match the
+    next dump, the GPU's newly written k/v, and (last layer) the logits, within tol * max|oracle|.
+    Returns the largest relative error seen."""
+    from oracle import sidp as OSD
+    L = m.num_layers
+    owner = OS.owner_map(L, d)
+    layers = [om.layer(l) for l in range(L)]
+    arenas = OSD.build_owned_arenas(layers, owner, d, pool)
+    local = OSD.local_tensors(layers, pool)
+    live = sorted(dumps)
+    worst = 0.0
+    out = None
+    for l in range(L):
+        xs = {r: dumps[r][l] for r in live}
+        cs = {r: (caches[r][0][l].copy(), caches[r][1][l].copy()) for r in live}
+        gk = {r: caches[r][0][l][np.arange(len(pos[r])), pos[r]] for r in live}
+        gv = {r: caches[r][1][l][np.arange(len(pos[r])), pos[r]] for r in live}
+        out = OSD.cas_layer(m, arenas[owner[l]][l], local[l], xs, pos, cs, pool)
+        for r in live:
+            b = np.arange(len(pos[r]))
+            errs = [rel_err(gk[r], cs[r][0][b, pos[r]]), rel_err(gv[r], cs[r][1][b, pos[r]])]
+            if l + 1 < L:
+                errs.append(rel_err(dumps[r][l + 1], out[r]))
+            worst = max(worst, *errs)
+            assert max(errs) <= tol, (r, l, errs)
+    for r in live:
+        e = rel_err(logits[r], OM.lm_head(m, om.head, out[r]))
+        worst = max(worst, e)
+        assert e <= tol, (r, e)
+    return worst
+
+
+__all__ = ["cas_oracle_check", "OracleModel", "rank_inputs", "oracle_layer", "rel_err", "oracle_steps", "OS", "OSD"]

@@ -10,7 +10,7 @@ import torch
 from oracle import schedule as OS
 from sidp_inputs import MODELS
 
-from .test_gpu_parity import SEED, TOL, Rank, _group, _replicated, P  # noqa: F401  (fixture)
+from .test_gpu_parity import SEED, TOL, Rank, _budget, _group, _replicated, P  # noqa: F401  (fixture)
 from .helpers import rel_err
 
 pytestmark = pytest.mark.gpu
@@ -36,7 +36,7 @@ def test_was_cas_was_switch(P, pool):
             assert R.ctx.stats()["mode"] == (1 if 2 <= s < 4 else 0)
     for r, R in enumerate(ranks):
         assert R.ctx.stats()["timeouts"] == 0
-        rep = _replicated(P, m, B[r], sum(B[:r]), pool=pool)
+        rep = _replicated(P, m, B[r], sum(B[:r]), pool=pool, compute_sms=_budget(R))
         for s in range(6):
             rep.toks = R.history[s - 1][0].cuda() if s else rep.toks   # follow the same tokens
             rep.step(); rep.finish_step()

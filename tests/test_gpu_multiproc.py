@@ -2,7 +2,9 @@
 handles, run WaS (peer arena fetches across processes) and CaS (cross-process staging + flags).
 This exercises the exact N>1 data path except NVLink bandwidth (both ranks share cuda:0).
 
-WaS logits must be BITWISE equal to a single-process replicated run; CaS within tolerance.
+WaS logits must be BITWISE equal to a single-process replicated run (same compute-grid SM
+budget); CaS is checked against the ORACLE's CaS (oracle/sidp.py cas_layer), teacher-forced per
+layer from the layer inputs and KV state each process dumps.
 """
 import os
 import socket
@@ -52,6 +54,7 @@ def _run_rank(rank, world, port, mode, pool, batches, steps, q):
         toks = torch.from_numpy(gen.tokens(SEED, bg, m.vocab)).to(torch.int32).cuda()
         nxt = torch.zeros(mb, dtype=torch.int32, device="cuda")
         logits = torch.zeros(mb, m.vocab, dtype=torch.float32, device="cuda")
+        dump = torch.zeros(m.num_layers, max(B, 1), m.hidden, dtype=torch.bfloat16, device="cuda")
         torch.cuda.synchronize()
         exchange_handles(ctx, dist)
         if mode == "cas":
@@ -60,9 +63,16 @@ def _run_rank(rank, world, port, mode, pool, batches, steps, q):
         dist.barrier()
         out = []
         for s in range(steps):
-            ctx.step(toks, nxt, kv, batch=B, logits=logits)
+            ctx.step(toks, nxt, kv, batch=B, logits=logits,
+                     layer_inputs=dump if mode == "cas" else None)
             torch.cuda.synchronize()
-            out.append((nxt[:B].cpu().numpy().copy(), logits[:B].cpu().numpy().copy()))
+            extra = None
+            if mode == "cas" and B:   # teacher-forcing dumps: layer inputs + KV state (oracle layout)
+                extra = (dump[:, :B].double().cpu().numpy(),
+                         kv.k[:, :B].permute(0, 1, 3, 2, 4).double().cpu().numpy(),
+                         kv.v[:, :B].permute(0, 1, 3, 2, 4).double().cpu().numpy(),
+                         pos + s)
+            out.append((nxt[:B].cpu().numpy().copy(), logits[:B].cpu().numpy().copy(), extra))
             if B:   # teacher-forced: the next inputs do not depend on this step's argmax, so a
                 # near-tie decided differently by CaS and replicated rounding cannot fork the runs
                 toks = torch.from_numpy(gen.tokens(SEED + s + 1, bg, m.vocab)).to(torch.int32).cuda()
@@ -71,17 +81,18 @@ def _run_rank(rank, world, port, mode, pool, batches, steps, q):
         log = ctx.fetch_log()
         dist.barrier()
         ctx.destroy()
-        q.put((rank, out, st["timeouts"], log))
+        q.put((rank, out, st["timeouts"], log, st["compute_sms"]))
     finally:
         dist.destroy_process_group()
 
 
-def _replicated(batches, r, steps, pool):
+def _replicated(batches, r, steps, pool, compute_sms=0):
     import paper_2605_28095_b200 as P
     from sidp_inputs import MODELS, gen
     m = MODELS["tiny"].with_layers(8)
     B, mb, b0 = batches[r], max(batches), sum(batches[:r])
-    ctx = P.Context(m, rank=0, world=1, max_batch=mb, max_ctx=80, seed=SEED, pool=pool)
+    ctx = P.Context(m, rank=0, world=1, max_batch=mb, max_ctx=80, seed=SEED, pool=pool,
+                    compute_sms=compute_sms)
     ctx.init_weights_synthetic()
     kv = P.KVCache(m, mb, 80)
     kv.fill_synthetic(SEED, b0, mb, 80)
@@ -112,8 +123,8 @@ def _launch(mode, pool, batches, steps):
         p.start()
     res = {}
     for _ in range(world):
-        r, out, timeouts, log = q.get(timeout=300)
-        res[r] = (out, timeouts, log)
+        r, out, timeouts, log, budget = q.get(timeout=300)
+        res[r] = (out, timeouts, log, budget)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -127,8 +138,8 @@ def test_was_two_processes_ipc(pool):
     res = _launch("was", pool, batches, 3)
     own = OS.owner_map(8, 2)
     for r in range(2):
-        out, timeouts, log = res[r]
-        ref = _replicated(batches, r, 3, pool)
+        out, timeouts, log, budget = res[r]
+        ref = _replicated(batches, r, 3, pool, budget)
         for s in range(3):
             assert np.array_equal(out[s][1], ref[s][1]), (r, s)      # bitwise: verbatim fetch
             assert np.array_equal(out[s][0], ref[s][0])
@@ -139,14 +150,22 @@ def test_was_two_processes_ipc(pool):
 @pytest.mark.parametrize("pool", ["layer", "ffn"])
 @pytest.mark.parametrize("batches", [[3, 5], [4, 0]])
 def test_cas_two_processes_ipc(pool, batches):
+    """CaS across two processes (cross-process staging + flags over CUDA IPC) against the
+    oracle's CaS, both steps teacher-forced per layer (the second step's KV state holds the
+    first step's appended entries, as dumped)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from sidp_inputs import MODELS
+    from .helpers import OracleModel, cas_oracle_check
     res = _launch("cas", pool, batches, 2)
+    m = MODELS["tiny"].with_layers(8)
+    om = OracleModel(m, SEED)
+    live = [r for r in range(2) if batches[r]]
     for r in range(2):
-        out, timeouts, _ = res[r]
-        assert timeouts == 0
-        if batches[r] == 0:
-            continue
-        ref = _replicated(batches, r, 2, pool)
-        for s in range(2):
-            got, exp = out[s][1], ref[s][1]
-            err = np.abs(got - exp).max() / np.abs(exp).max()
-            assert err <= 1e-2, (r, s, err)
+        assert res[r][1] == 0     # no flag-wait timeout
+    for s in range(2):
+        dumps = {r: res[r][0][s][2][0] for r in live}
+        caches = {r: (res[r][0][s][2][1], res[r][0][s][2][2]) for r in live}
+        pos = {r: res[r][0][s][2][3] for r in live}
+        logits = {r: res[r][0][s][1].astype(np.float64) for r in live}
+        cas_oracle_check(m, om, 2, pool, dumps, logits, caches, pos, 1e-2)

@@ -13,7 +13,7 @@ from oracle import model as OM
 from oracle import schedule as OS
 from sidp_inputs import MODELS, gen
 
-from .helpers import OracleModel, oracle_layer, rank_inputs, rel_err
+from .helpers import OracleModel, cas_oracle_check, oracle_layer, rank_inputs, rel_err
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-2
@@ -140,7 +140,7 @@ def test_was_serve_only_peers(P, d, slots):
     log = R.ctx.fetch_log()
     assert log == OS.slot_schedule(pl, slots, steps + 1)[:len(log)]
     assert len(log) >= steps * len(pl)
-    rep = _replicated(P, m, 5, 0)
+    rep = _replicated(P, m, 5, 0, compute_sms=_budget(R))
     for s in range(steps):
         rep.step(); rep.finish_step()
         assert torch.equal(rep.history[s][1], R.history[s][1]), s
@@ -153,8 +153,15 @@ def test_was_serve_only_peers(P, d, slots):
 
 
 def _replicated(P, m, B, b0, **kw):
-    kw = {k: v for k, v in kw.items() if k in ("pool",)}
+    """Replicated (d = 1) run of the same rows; compute_sms = the WaS rank's compute-grid SM
+    budget (the SM fetch holds the rest), so both run the same kernel configurations and the
+    comparison can be bitwise."""
+    kw = {k: v for k, v in kw.items() if k in ("pool", "compute_sms")}
     return Rank(P, m, B=B, b0=b0, **kw)
+
+
+def _budget(R):
+    return R.ctx.stats()["compute_sms"]
 
 
 @pytest.mark.parametrize("name,d,slots,order,pool", [
@@ -183,7 +190,7 @@ def test_was_virtual_ranks(P, name, d, slots, order, pool):
         assert log == ref[:len(log)]
         st = R.ctx.stats()
         assert st["slot_bytes"] == slots * st["layer_bytes"]
-        rep = _replicated(P, m, B[r], sum(B[:r]), pool=pool)
+        rep = _replicated(P, m, B[r], sum(B[:r]), pool=pool, compute_sms=_budget(R))
         for s in range(steps):
             rep.step(); rep.finish_step()
             assert torch.equal(rep.history[s][1], R.history[s][1]), (r, s)
@@ -196,41 +203,6 @@ def test_was_virtual_ranks(P, name, d, slots, order, pool):
         xs = R.history[0][2].double().numpy()
         out, _, _ = oracle_layer(om, m.num_layers - 1, xs[-1], pos, *caches[-1])
         assert rel_err(R.history[0][1].double().numpy(), OM.lm_head(m, om.head, out)) <= TOL
-    for R in ranks:
-        R.ctx.destroy()
-
-
-@pytest.mark.parametrize("pool", ["layer", "ffn"])
-@pytest.mark.parametrize("B", [[3, 5], [4, 0, 2, 0], [0, 0, 0, 6], [2, 2, 2, 2]])
-def test_cas_virtual_ranks(P, pool, B):
-    """CaS on virtual ranks: fused owner GEMMs over the concatenated rows; dummy ranks
-    (B=0) move nothing.  Per-rank results equal the replicated run within tolerance."""
-    name = "tiny"
-    m = MODELS[name].with_layers(4)
-    d = len(B)
-    ranks = _group(P, m, d, B, pool=pool)
-    for R in ranks:
-        R.ctx.set_batches(B)
-        R.ctx.set_mode(1, 0)                      # SIDP_CAS from step 0 on every rank
-    for s in range(2):
-        for R in ranks:
-            R.step()
-        for R in ranks:
-            R.finish_step()
-    for R in ranks:
-        st = R.ctx.stats()
-        assert st["timeouts"] == 0
-        assert st["mode"] == 1
-    for r, R in enumerate(ranks):
-        if B[r] == 0:
-            continue
-        rep = _replicated(P, m, B[r], sum(B[:r]), pool=pool)
-        for s in range(2):
-            rep.toks = R.history[s - 1][0].cuda() if s else rep.toks
-            rep.step(); rep.finish_step()
-            err = rel_err(R.history[s][1].double().numpy(), rep.history[s][1].double().numpy())
-            assert err <= TOL, (r, s, err)
-        rep.ctx.destroy()
     for R in ranks:
         R.ctx.destroy()
 
@@ -250,16 +222,37 @@ def test_was_layer_order_enforced(P):
         R.ctx.destroy()
 
 
-@pytest.mark.parametrize("name,B,ctx", [("qwen3-32b", 256, 1024), ("llama-3.1-70b", 64, 512)])
-def test_big_shapes_sampled_rows(P, name, B, ctx):
-    """Full-size per-layer shapes (the bench's launch configuration) on 2 layers; the oracle
-    recomputes sampled rows of every layer (teacher-forced) and the new k/v entries."""
+_OM_CACHE = {}
+
+
+def _oracle_model(m):
+    """fp64 parameters of the 2-layer full-width models, kept for the next case of the same
+    model only (a Llama-width layer is 6.8 GB in fp64)."""
+    key = (m.name, m.num_layers)
+    if key not in _OM_CACHE:
+        _OM_CACHE.clear()
+        _OM_CACHE[key] = OracleModel(m, SEED)
+    return _OM_CACHE[key]
+
+
+# (model, B, S_ctx, compute_sms): the M2 point in the d = 1 launch configuration (all SMs) and in
+# the WaS one (132 SMs: 16 held by the SM fetch); the B_e-regime points the WaS emulation reports
+# (Qwen3 B = 512-1536, Llama B = 1024 / 1536 at their max-KV contexts, SURVEY.md §8(d) M3) in the
+# WaS configuration; Qwen2.5-72B (QKV bias at h = 8192) at its M4 point
+@pytest.mark.parametrize("name,B,ctx,sms", [
+    ("qwen3-32b", 256, 1024, 0), ("qwen3-32b", 256, 1024, 132), ("qwen3-32b", 512, 768, 132),
+    ("qwen3-32b", 1024, 384, 132), ("qwen3-32b", 1536, 256, 132),
+    ("llama-3.1-70b", 64, 512, 0), ("llama-3.1-70b", 1024, 432, 132),
+    ("llama-3.1-70b", 1536, 288, 132), ("qwen2.5-72b", 256, 1024, 132)])
+def test_big_shapes_sampled_rows(P, name, B, ctx, sms):
+    """Full-size per-layer shapes in the launch configurations the bench times, on 2 layers;
+    the oracle recomputes sampled rows of every layer (teacher-forced) and the new k/v entries."""
     m = MODELS[name].with_layers(2)
     max_ctx = ctx + 8
-    R = Rank(P, m, B=B, ctx=ctx, span=0, max_ctx=max_ctx)
+    R = Rank(P, m, B=B, ctx=ctx, span=0, max_ctx=max_ctx, compute_sms=sms)
     R.step(); R.finish_step()
     _, logits, dump = R.history[0]
-    om = OracleModel(m, SEED)
+    om = _oracle_model(m)
     rows = np.array([0, 1, B // 3, B // 2, B - 2, B - 1])
     pos = np.full(len(rows), ctx)
     xs = dump[:, rows].double().numpy()
@@ -267,11 +260,12 @@ def test_big_shapes_sampled_rows(P, name, B, ctx):
     for l in range(m.num_layers):
         K = gen.kv(SEED, gen.KCACHE, l, rows, range(max_ctx), m.n_kv_heads, m.head_dim)
         V = gen.kv(SEED, gen.VCACHE, l, rows, range(max_ctx), m.n_kv_heads, m.head_dim)
-        out, kn, _ = oracle_layer(om, l, xs[l], pos, K, V)
+        out, kn, vn = oracle_layer(om, l, xs[l], pos, K, V)
         if l + 1 < m.num_layers:
             assert rel_err(xs[l + 1], out) <= TOL, (l, rel_err(xs[l + 1], out))
         kg = R.kv.k[l, torch.from_numpy(rows).cuda(), :, ctx].cpu().double().numpy()
-        assert rel_err(kg, kn) <= TOL
+        vg = R.kv.v[l, torch.from_numpy(rows).cuda(), :, ctx].cpu().double().numpy()
+        assert rel_err(kg, kn) <= TOL and rel_err(vg, vn) <= TOL
     ref = OM.lm_head(m, om.head, out)
     assert rel_err(logits[rows].double().numpy(), ref) <= TOL
     R.ctx.destroy()
@@ -303,7 +297,7 @@ def test_was_full_width_d8_serve_only_bitwise(P):
     assert log == OS.slot_schedule(pl, 2, steps + 1)[:len(log)]
     for c in peers:
         c.destroy()
-    rep = Rank(P, m, B=B, ctx=ctx, span=0, max_ctx=ctx + 8)
+    rep = Rank(P, m, B=B, ctx=ctx, span=0, max_ctx=ctx + 8, compute_sms=_budget(R))
     for s in range(steps):
         rep.step(); rep.finish_step()
         assert torch.equal(rep.history[s][1], R.history[s][1]), s
@@ -404,8 +398,133 @@ def test_dummy_step_was_keeps_schedule(P):
     log = R.ctx.fetch_log()
     ref = OS.slot_schedule(OS.plan_exec(own, 0), 2, 3)
     assert log == ref[:len(log)] and len(log) >= 2 * 4
-    rep = _replicated(P, m, 3, 0)
+    rep = _replicated(P, m, 3, 0, compute_sms=_budget(R))
     rep.step(); rep.finish_step()
     assert torch.equal(rep.history[0][1], R.history[0][1])
     for Rk in ranks + [rep]:
         Rk.ctx.destroy()
+
+
+def _gpu_caches(R, B):
+    """The rank's KV state in the oracle's layout: (K, V) [L, B, T, n_kv, hd] float64."""
+    K = R.kv.k[:, :B].permute(0, 1, 3, 2, 4).double().cpu().numpy()
+    V = R.kv.v[:, :B].permute(0, 1, 3, 2, 4).double().cpu().numpy()
+    return K, V
+
+
+@pytest.mark.parametrize("pool", ["layer", "ffn"])
+@pytest.mark.parametrize("B", [[3, 5], [4, 0, 2, 0], [0, 0, 0, 6], [2, 2, 2, 2]])
+def test_cas_vs_oracle(P, pool, B):
+    """CaS on virtual ranks against the ORACLE's CaS (oracle/sidp.py cas_layer / run_cas), not
+    against another GPU run: teacher-forced per layer and, untethered, the
+    oracle's whole CaS step from the same tokens (run_cas) — logits within the north_star
+    tolerance, tokens where the oracle's top-2 margin is clear.  Dummy ranks (B = 0) move
+    nothing and the owner serves even when it is dummy itself."""
+    from oracle import sidp as OSD
+    m = MODELS["tiny"].with_layers(4)
+    d = len(B)
+    ranks = _group(P, m, d, B, pool=pool)
+    for R in ranks:
+        R.ctx.set_batches(B)
+        R.ctx.set_mode(1, 0)
+    for R in ranks:
+        R.step()
+    for R in ranks:
+        R.finish_step()
+    for R in ranks:
+        assert R.ctx.stats()["timeouts"] == 0
+    hist = {r: R.history[0] for r, R in enumerate(ranks)}
+    live = [r for r in range(d) if B[r]]
+    om = OracleModel(m, SEED)
+    owner = OS.owner_map(m.num_layers, d)
+    cas_oracle_check(m, om, d, pool, {r: hist[r][2].double().numpy() for r in live},
+                     {r: hist[r][1].double().numpy() for r in live},
+                     {r: _gpu_caches(ranks[r], B[r]) for r in live},
+                     {r: gen.positions(SEED, np.arange(sum(B[:r]), sum(B[:r]) + B[r]), 0, 63)
+                      for r in live}, TOL)
+    # untethered: the oracle's CaS step from the same tokens and caches
+    states = []
+    for r in range(d):
+        _, toks, pos, caches = rank_inputs(m, SEED, sum(B[:r]), B[r], 0, 63, 80)
+        states.append(OSD.RankState(r, toks, pos, caches))
+    OSD.run_cas(m, [om.layer(l) for l in range(m.num_layers)], om.head, om.embed, states, 1, d,
+                owner, pool)
+    for r, st in enumerate(states):
+        if B[r] == 0:
+            assert st.history[0] is None
+            continue
+        ref = st.history[0]["logits"]
+        got = hist[r][1].double().numpy()
+        err = rel_err(got, ref)
+        assert err <= TOL, (r, err)
+        top2 = np.sort(ref, axis=1)[:, -2:]
+        sure = (top2[:, 1] - top2[:, 0]) > 2 * err * np.abs(ref).max()
+        assert (hist[r][0].numpy()[sure] == st.history[0]["next"][sure]).all()
+    for R in ranks:
+        R.ctx.destroy()
+
+
+@pytest.mark.parametrize("case", ["tiny-qwen3-160-20-40", "tiny-200-0-60", "tiny-300-0-400"])
+def test_attention_range_walk_mode(P, case):
+    """The one-wave range-walking attention partition (many short pairs split into contiguous
+    chunk ranges, pieces merged by the last arriver) is only reached when the warp-per-pair
+    kernel is disabled (SIDP_ATTN_WARP_CH=1, read once per process): re-run the ragged short-pair
+    parity cases in a subprocess with it off, against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SIDP_ATTN_WARP_CH="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"tests/test_gpu_parity.py::test_long_context_split_kv[{case}]"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "1 passed" in r.stdout
+
+
+@pytest.mark.parametrize("d,slots", [(4, 2), (8, 1)])
+def test_was_cuda_graph_replay(P, d, slots):
+    """WaS steps replay as a CUDA graph (device epoch flags: the ready waits and releases name
+    only the slot; the fetch stream is enqueued by the host around each replay): decoded tokens
+    of 5 replayed steps equal an eager WaS run's bit for bit, the device fetch log equals the
+    oracle's FIFO schedule, and every consumption found the layer it expected in its slot."""
+    m = MODELS["tiny"].with_layers(8)
+    B = 5
+
+    def group():
+        R = Rank(P, m, rank=0, world=d, B=B, slots=slots)
+        peers = []
+        for r in range(1, d):
+            c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=80, seed=SEED, alloc=False)
+            c.alloc_serve_only()
+            c.init_weights_synthetic()
+            peers.append(c)
+        torch.cuda.synchronize()
+        R.ctx.import_handles([R.ctx.export_handles()] + [c.export_handles() for c in peers])
+        return R, peers
+
+    G, gp = group()     # graph path: no logits / dumps requested
+    E, ep = group()     # eager path (logits requested)
+    steps = 5
+    for s in range(steps):
+        with torch.cuda.stream(G.stream):
+            G.ctx.step(G.toks, G.toks, G.kv, batch=B, stream=G.stream, advance_pos=True)
+        G.stream.synchronize()
+        G.history.append(G.toks.clone().cpu())
+        E.step(); E.finish_step()
+        assert torch.equal(G.history[-1], E.history[-1][0]), s
+    st = G.ctx.stats()
+    assert st["timeouts"] == 0 and st["fetch_sms_held"] > 0
+    pl = OS.plan(OS.owner_map(m.num_layers, d), d, 0, "exec")
+    log = G.ctx.fetch_log()
+    assert len(log) >= steps * len(pl)
+    assert log == OS.slot_schedule(pl, slots, steps + 2)[:len(log)]
+    cons = G.ctx.consume_log()
+    assert len(cons) == steps * len(pl)
+    assert all(c[0] == c[2] for c in cons)                  # slot held the expected layer
+    sched = OS.slot_schedule(pl, slots, steps)
+    assert [(c[0], c[1]) for c in cons] == [(l, s) for (_, l, s) in sorted(sched, key=lambda e: (e[0], e[1]))]
+    for c in gp + ep:
+        c.destroy()
+    G.ctx.destroy()
+    E.ctx.destroy()

@@ -9,6 +9,7 @@ import json
 import math
 import os
 
+import numpy as np
 import pytest
 
 from oracle import accounting as A
@@ -264,3 +265,38 @@ def test_remote_bytes_per_step():
     got = A.remote_bytes_per_step(m, 8)
     assert abs(got - 70 * 1.711e9) / (70 * 1.711e9) < 0.001    # 119.8 GB
     assert A.remote_bytes_per_step(m, 1) == 0
+
+
+def test_kv_bytes_per_token_layer():
+    """Pinned by SPEC.md:64's printed Llama-3.1-70B KV bytes per token (all 80 layers) and by
+    the bytes of one cached token in the oracle's own cache layout (Kc and Vc rows of a layer)."""
+    g = GOLD["model_stats"]["llama-3.1-70b"]
+    m = MODELS["llama-3.1-70b"]
+    assert A.kv_bytes_per_token_layer(m) * m.num_layers == g["kv_bytes_per_token"]
+    t = MODELS["tiny"]
+    from sidp_inputs import gen as G
+    K = G.kv(1, G.KCACHE, 0, np.arange(1), range(1), t.n_kv_heads, t.head_dim)   # [1, 1, nkv, hd]
+    assert A.kv_bytes_per_token_layer(t) == 2 * K[0, 0].size * 2                # K + V, bf16
+
+
+def test_layer_flops_per_token_brute_force():
+    """2 x (multiply-adds) of one decoded token through the oracle layer, counted on the actual
+    parameter arrays (every linear's weight matrix) and by walking the attention loops of
+    oracle.model.attend (scores q.K and values p.V over pos + 1 tokens per query head) — not
+    the closed form under test.  Also the SURVEY.md §8(d) figures: 32,768 (S_ctx + 1) attention
+    FLOPs for 64 x 128 heads and 2 P_l = 1.711 GFLOP for Llama-3.1-70B."""
+    from sidp_inputs import gen as G
+    for name in ("tiny", "tiny-qwen3", "tiny-qwen25"):
+        m = MODELS[name]
+        p = G.layer_params(3, m, 0)
+        linear = sum(p[k].size for k in ("wq", "wk", "wv", "wo", "wgate", "wup", "wdown"))
+        for ctx in (0, 5, 63):
+            macs = linear
+            for _ in range(m.n_q_heads):          # attend(): per head, scores then values
+                macs += (ctx + 1) * m.head_dim    # s_t = q . K[t]
+                macs += (ctx + 1) * m.head_dim    # o += p_t V[t]
+            assert A.layer_flops_per_token(m, ctx) == 2 * macs, (name, ctx)
+    ll = MODELS["llama-3.1-70b"]
+    attn = A.layer_flops_per_token(ll, 100) - A.layer_flops_per_token(ll, 99)
+    assert attn == 32768
+    assert abs((A.layer_flops_per_token(ll, 0) - 32768) / 1.711e9 - 1) < 1e-3
