@@ -75,6 +75,10 @@ def parse():
     ap.add_argument("--cas-batches", default="1,4,16",
                     help="all-live per-rank batches of the CaS emulation (B=16 also runs the "
                          "half-live and one-live dummy patterns)")
+    ap.add_argument("--cas-only", action="store_true",
+                    help="print only the CaS emulation (run as a child of the default bench)")
+    ap.add_argument("--extra-timeout", type=int, default=240,
+                    help="seconds each child measurement (WaS / CaS emulation) may take")
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 with a gloo control plane (functional multi-process "
                          "test of the IPC path on a 1-GPU box; not a scaling number)")
@@ -503,6 +507,24 @@ def kv_capacity(m, st_d1, fp_dw, W, util=0.9):
     return out
 
 
+def _child_json(extra, timeout_s):
+    """Run this script again with the parent's flags plus `extra`; return its last JSON line, or
+    {"error": ...} (non-zero exit, no JSON, or killed after timeout_s)."""
+    argv = [a for a in sys.argv[1:] if a not in ("--emulate-only", "--cas-only")]
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__)] + argv + extra,
+                           capture_output=True, text=True, timeout=timeout_s)
+    except subprocess.TimeoutExpired:
+        return {"error": f"{' '.join(extra)}: killed after {timeout_s} s"}
+    for ln in reversed(r.stdout.strip().splitlines()):
+        if ln.startswith("{"):
+            try:
+                return json.loads(ln)
+            except ValueError:
+                break
+    return {"error": f"{' '.join(extra)}: rc {r.returncode}: {(r.stderr or '')[-300:]}"}
+
+
 # ----------------------------------------------------------------------------- main arms
 def run_reference(args, wl, m, rank, world):
     if rank != 0:
@@ -568,6 +590,11 @@ def main():
     slots = args.slots or wl.slots
     if args.emulate_only:
         run_emulation_only(args, P, m, wl, local, world)
+        return
+    if args.cas_only:
+        print(json.dumps({"cas_emulation": cas_emulation(args, P, m, wl.seed, local,
+                                                         max(2, args.emulate_world), args.cas_ctx)}),
+              flush=True)
         return
     e2e_steps = 0 if args.no_e2e else args.steps
     max_ctx = ctx_len + args.warmup + args.steps + e2e_steps + 8
@@ -711,32 +738,21 @@ def main():
                                     "kv": 2 * kv.k.numel() * 2},
     }
     ctx.destroy()
-    if world == 1 and args.emulate_world > 1:
-        eb = args.emulate_batch or B
-        ec = args.emulate_ctx or ctx_len
-        try:
-            if eb != B or ec + args.warmup + args.emulate_steps + 8 > kv.max_ctx:
-                del kv
-                torch.cuda.empty_cache()
-                kv = P.KVCache(m, eb, ec + args.warmup + args.emulate_steps + 8)
-                with torch.cuda.stream(stream):
-                    kv.fill_synthetic(seed, 0, eb, ec, stream=stream)
-                stream.synchronize()
-                tok = torch.from_numpy(gen.tokens(seed, np.arange(eb), m.vocab)).to(torch.int32).cuda()
-            line["was_emulation"] = was_emulation(args, P, m, wl, seed, local, stream, kv, tok, eb,
-                                                  ec, args.emulate_world, peaks)
-        except Exception as e:   # reported, never fatal for the main line
-            line["was_emulation"] = {"error": str(e)[:300]}
-        line["kv_capacity"] = kv_capacity(m, st, line["was_emulation"].get("footprint_bytes_rank0"),
-                                          args.emulate_world)
-        if args.cas_emulate:
-            try:
-                del kv
-                torch.cuda.empty_cache()
-                line["cas_emulation"] = cas_emulation(args, P, m, seed, local, args.emulate_world,
-                                                      args.cas_ctx)
-            except Exception as e:
-                line["cas_emulation"] = {"error": str(e)[:300]}
+    if world == 1 and (args.emulate_world > 1 or args.cas_emulate):
+        # the extra single-GPU measurements run in child processes with a time limit, so a
+        # failure or hang there can never cost the main line; this process frees the GPU first
+        del kv, tok
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        if args.emulate_world > 1:
+            child = _child_json(["--emulate-only"], args.extra_timeout)
+            line["was_emulation"] = child.get("was_emulation", child)
+            if "was_emulation" in child:
+                line["kv_capacity"] = kv_capacity(m, st, child["was_emulation"].get("footprint_bytes_rank0"),
+                                                  args.emulate_world)
+        if args.cas_emulate and args.emulate_world > 1:
+            child = _child_json(["--cas-only"], args.extra_timeout)
+            line["cas_emulation"] = child.get("cas_emulation", child)
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -157,6 +157,9 @@ struct sidp_ctx {
   std::vector<cudaEvent_t> tev;
   std::vector<int> tev_cls;
   int tev_used = 0;
+  // timed pairs not yet complete at a non-blocking flush (their events left the pool)
+  struct PendingPair { cudaEvent_t a, b; int cls; };
+  std::vector<PendingPair> tev_pending;
   double timed_acc_ms[8]{};
 };
 
@@ -269,7 +272,7 @@ void count_launch(sidp_ctx* c, int n = 1) { c->st.launches += n; }
 void graph_harvest(sidp_ctx* c);
 
 // ---- optional per-class kernel timing ----
-void timing_flush(sidp_ctx* c);
+void timing_flush(sidp_ctx* c, bool block);
 // Inside stream capture a plain cudaEventRecord only expresses a dependency; an "external"
 // record becomes an event-record node that every graph replay re-records.
 void record_timing_event(sidp_ctx* c, cudaEvent_t e, cudaStream_t s) {
@@ -280,7 +283,7 @@ void record_timing_event(sidp_ctx* c, cudaEvent_t e, cudaStream_t s) {
 }
 void timing_begin(sidp_ctx* c, int cls, cudaStream_t s) {
   if (!((c->timed_mask >> cls) & 1)) return;
-  if (c->tev_used + 2 > (int)c->tev.size()) timing_flush(c);
+  if (c->tev_used + 2 > (int)c->tev.size()) timing_flush(c, false);
   record_timing_event(c, c->tev[c->tev_used], s);
 }
 void timing_end(sidp_ctx* c, int cls, cudaStream_t s) {
@@ -306,18 +309,53 @@ void graph_harvest(sidp_ctx* c) {
 
 // Accumulate recorded pairs (synchronises on them) and recycle the pool.  Pairs owned by a
 // live graph (the first graph_tev_pairs) are harvested per replay instead.
-void timing_flush(sidp_ctx* c) {
+// Harvest the timed pairs outside the graph's region.  block = false (while enqueueing): a pair
+// whose end has not completed is moved out of the pool (fresh events replace it) and harvested
+// later — a fetch-stream pair can depend on compute the host has not enqueued yet (the device
+// ring's window gates on releases of coming layers), so waiting on it here would deadlock.
+// block = true only where every dependency is enqueued (sidp_stats).
+void timing_flush(sidp_ctx* c, bool block) {
   const int first = c->gexec ? 2 * c->graph_tev_pairs : 0;
   if (c->gexec && c->graph_timed_pending) graph_harvest(c);
-  for (int i = first; i + 1 < c->tev_used; i += 2) {
+  auto harvest = [&](cudaEvent_t a, cudaEvent_t b, int cls) {
     float ms = 0.0f;
-    cudaEventSynchronize(c->tev[i + 1]);
-    if (cudaEventElapsedTime(&ms, c->tev[i], c->tev[i + 1]) == cudaSuccess)
-      c->timed_acc_ms[c->tev_cls[i / 2]] += ms;
+    if (block) cudaEventSynchronize(b);
+    if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess)
+      c->timed_acc_ms[cls] += ms;
     else
       cudaGetLastError();
+  };
+  for (int i = first; i + 1 < c->tev_used; i += 2) {
+    const int cls = c->tev_cls[i / 2];
+    if (block || cudaEventQuery(c->tev[i + 1]) == cudaSuccess) {
+      harvest(c->tev[i], c->tev[i + 1], cls);
+      continue;
+    }
+    cudaGetLastError();
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+      cudaGetLastError();
+      if (a) cudaEventDestroy(a);
+      harvest(c->tev[i], c->tev[i + 1], cls);   // no spare events: fall back to waiting
+      continue;
+    }
+    c->tev_pending.push_back({c->tev[i], c->tev[i + 1], cls});
+    c->tev[i] = a;
+    c->tev[i + 1] = b;
   }
   c->tev_used = first;
+  std::vector<sidp_ctx::PendingPair> keep;
+  for (const auto& p : c->tev_pending) {
+    if (block || cudaEventQuery(p.b) == cudaSuccess) {
+      harvest(p.a, p.b, p.cls);
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    } else {
+      cudaGetLastError();
+      keep.push_back(p);
+    }
+  }
+  c->tev_pending.swap(keep);
 }
 
 struct LayerW {
@@ -1012,6 +1050,10 @@ void sidp_destroy(sidp_ctx* ctx) {
     for (auto e : ctx->ready_ev) cudaEventDestroy(e);
     for (auto e : ctx->free_ev) cudaEventDestroy(e);
     for (auto e : ctx->tev) cudaEventDestroy(e);
+    for (auto& p : ctx->tev_pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
     if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
@@ -1550,7 +1592,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
   if (replayable) {
     if (!graph_key_matches(ctx, b) || ctx->gslots != slots_now) {
       graph_drop(ctx);
-      if (ctx->tev_used > 0) timing_flush(ctx);
+      if (ctx->tev_used > 0) timing_flush(ctx, false);
       const uint64_t l0 = ctx->st.launches;
       uint64_t t0[8];
       for (int i = 0; i < 8; ++i) t0[i] = ctx->st.timed_launches[i];
@@ -1770,7 +1812,7 @@ sidp_status sidp_stats(const sidp_ctx* ctx_c, sidp_stats_t* out) {
   sidp_ctx* ctx = const_cast<sidp_ctx*>(ctx_c);
   if (ctx->allocated) {
     if (ctx->host_err && *ctx->host_err) ctx->st.timeouts = *ctx->host_err;
-    if (ctx->tev_used > 0) timing_flush(ctx);
+    if (ctx->tev_used > 0 || !ctx->tev_pending.empty()) timing_flush(ctx, true);
   }
   for (int i = 0; i < 8; ++i) ctx->st.timed_ms[i] = ctx->timed_acc_ms[i];
   ctx->st.fetch_sms_held = ctx->ring_mode ? ctx->fetch_ctas : 0;
@@ -1790,6 +1832,11 @@ sidp_status sidp_set_timing(sidp_ctx* ctx, int32_t class_mask) {
     for (auto& e : ctx->tev) CK(cudaEventCreate(&e));
   }
   graph_drop(ctx);
+  for (auto& p : ctx->tev_pending) {   // a previous mask's unharvested pairs: dropped
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  ctx->tev_pending.clear();
   ctx->timed_mask = class_mask;
   ctx->tev_used = 0;
   for (int i = 0; i < 8; ++i) {

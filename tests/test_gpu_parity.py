@@ -528,3 +528,50 @@ def test_was_cuda_graph_replay(P, d, slots):
         c.destroy()
     G.ctx.destroy()
     E.ctx.destroy()
+
+
+def test_was_windowed_graph_with_timing(P, monkeypatch):
+    """The bench's WaS emulation path: ONE computing context (so the fetch of a whole step is one
+    windowed launch gated on device release flags) replaying CUDA graphs while per-class kernel
+    timing is on.  Regression: a blocking harvest of the fetch stream's timing events before a
+    capture waited on a window whose gates need compute not yet enqueued (deadlock until the
+    flag-wait timeout).  Tokens equal a replicated run's bit for bit; no timeouts."""
+    monkeypatch.setenv("SIDP_CAS_TIMEOUT_MS", "4000")
+    m = MODELS["tiny"].with_layers(8)
+    B, d = 5, 4
+    G = Rank(P, m, rank=0, world=d, B=B, slots=2)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=80, seed=SEED, alloc=False)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    G.ctx.import_handles([G.ctx.export_handles()] + [c.export_handles() for c in peers])
+    toks = []
+    for s in range(6):
+        if s == 2:
+            G.ctx.set_timing(sum(1 << c for c in range(1, 8)))   # every class, as the bench
+        if s == 4:
+            G.ctx.set_timing(1 << 3)                             # the fetch class only
+        with torch.cuda.stream(G.stream):
+            G.ctx.step(G.toks, G.toks, G.kv, batch=B, stream=G.stream, advance_pos=True)
+        if s % 2:
+            G.stream.synchronize()
+            toks.append(G.toks.clone().cpu())
+    G.stream.synchronize()
+    st = G.ctx.stats()
+    assert st["timeouts"] == 0 and st["fetch_sms_held"] > 0
+    assert st["timed_launches"][3] > 0 and st["timed_ms"][3] > 0
+    budget = st["compute_sms"]
+    for c in peers:
+        c.destroy()
+    G.ctx.destroy()
+    rep = Rank(P, m, B=B, compute_sms=budget)
+    for s in range(6):
+        with torch.cuda.stream(rep.stream):
+            rep.ctx.step(rep.toks, rep.toks, rep.kv, batch=B, stream=rep.stream, advance_pos=True)
+        if s % 2:
+            rep.stream.synchronize()
+            assert torch.equal(rep.toks.cpu(), toks[s // 2]), s
+    rep.ctx.destroy()
