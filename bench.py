@@ -49,7 +49,7 @@ def parse():
                     help="WaS fetch engine: the SM fetch kernel (default: TMA bulk copies on "
                          "--fetch-sms dedicated SMs, device epoch flags) or the copy engine + CUDA "
                          "events (the paper's mechanism, A/B baseline)")
-    ap.add_argument("--fetch-sms", type=int, default=16)
+    ap.add_argument("--fetch-sms", type=int, default=24)
     ap.add_argument("--no-stagger", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--emulate-world", type=int, default=8,
                     help="N=1 only: also time rank 0 of a d-rank WaS group on this GPU, the d-1 "
                          "owners being serve-only contexts in local HBM (0 = off)")
-    ap.add_argument("--emulate-fetch-sms", type=int, default=16,
+    ap.add_argument("--emulate-fetch-sms", type=int, default=24,
                     help="SMs the emulated rank's fetch kernel holds (the real-run default, 16)")
     ap.add_argument("--emulate-pace-gbps", type=float, default=770.0,
                     help="the emulated rank's fetch kernel paces itself to this rate: the NVLink 5 "

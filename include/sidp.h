@@ -90,9 +90,10 @@ typedef struct {
   int32_t max_batch;            /* max rows per rank per step */
   int32_t max_ctx;              /* KV positions per sequence; a step needs pos + 1 <= max_ctx */
   int32_t fetch_sms;            /* SMs (CTAs, rounded to CTA pairs) the SM fetch kernel holds
-                                   (0 => 16: ~50 GB/s of copy per SM, so 16 cover NVLink 5's
-                                   ~770 GB/s reader rate); the WaS compute kernels then use the
-                                   remaining SMs.  Ignored by SIDP_FETCH_CE and when d == 1 */
+                                   (0 => 24: one bulk-copy CTA moves ~50 GB/s (its SM's TMA unit
+                                   carries both the load and the store of every chunk), so 24 keep
+                                   NVLink 5's ~770 GB/s reader rate with headroom under a loaded
+                                   HBM); the WaS compute kernels then use the remaining SMs.  Ignored by SIDP_FETCH_CE and when d == 1 */
   int32_t fetch_engine;         /* sidp_fetch_engine */
   int32_t stagger;              /* 1 => C-S7 start offsets t_r = (-r) mod (d-1) fetch ticks */
   int32_t device;               /* CUDA device ordinal the context lives on */

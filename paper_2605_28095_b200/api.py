@@ -65,7 +65,7 @@ class KVCache:
 
 class Context:
     def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
-                 max_batch=8, max_ctx=128, fetch_sms=16, fetch_engine="sm", stagger=True,
+                 max_batch=8, max_ctx=128, fetch_sms=24, fetch_engine="sm", stagger=True,
                  device=0, seed=20261017, layer_owner=None, alloc=True, fetch_pace_gbps=0.0,
                  compute_sms=0):
         self.m = m

@@ -159,6 +159,25 @@ SIDP_DEV uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Spin until every *p[i] >= value (system-scope acquire), bounded by timeout_ns per flag; on a
+// timeout *err (a mapped host word) is set and the wait gives up (SIDP_ETIMEOUT at the host).
+SIDP_DEV void flags_wait(const uint64_t* const* p, int n, uint64_t value, uint64_t timeout_ns,
+                         int* err) {
+  for (int i = 0; i < n; ++i) {
+    if (ld_acquire_sys(p[i]) >= value) continue;
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(p[i]) < value) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        if (err) {
+          *reinterpret_cast<volatile int*>(err) = 1;
+          __threadfence_system();
+        }
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+}
 
 // ---------------------------------------------------------------- programmatic dependent launch
 // Kernels of the decode chain are launched with programmatic stream serialization: a kernel

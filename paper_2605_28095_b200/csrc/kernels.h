@@ -66,6 +66,17 @@ struct QkvEpi {
   int nq, nkv, hd, smax;
 };
 
+// A CaS flag wait folded into a consumer kernel's prologue (no standalone wait launch): the
+// kernel's loads of the guarded data start once every *p[i] >= value (system-scope acquire);
+// n == 0: no wait.  Timeout -> *err (mapped host word), surfaced as SIDP_ETIMEOUT.
+struct FlagWait {
+  const uint64_t* p[16];
+  int n;
+  uint64_t value;
+  uint64_t timeout_ns;
+  int* err;
+};
+
 struct GemmArgs {
   const bf16* x; int ldx;      // [M, K]
   const bf16* w; int ldw;      // [N, K]
@@ -80,6 +91,7 @@ struct GemmArgs {
   int w_kbmajor;               // 1: W is k-block-major [K/64][N][64] (one 3-D TMA box per stage)
   int x_kbmajor;               // 1: X is k-block-major [K/64][M][64] (layout experiment)
   PartialSrc* partial_out;     // EPI_PARTIAL: receives the slice geometry for the consumer
+  const FlagWait* wait;        // optional: the activation loads wait for these flags (CaS owner)
 };
 
 struct GemmWorkspace {
@@ -136,6 +148,21 @@ cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, 
                               cudaStream_t s, unsigned long long* post = nullptr);
 cudaError_t embed_launch(const bf16* E, int h, const int32_t* tokens, bf16* x, int rows,
                          cudaStream_t s);
+// CaS requester, round trip 1 (the send fused into the producing kernel):
+// waits for the owner's previous round trip to be served (its staging slot is free), computes
+// u = RMSNorm(x) g and stores [u | x] straight into the owner's staging rows (peer VA), then the
+// last CTA posts the arrival flag (release, system scope).  One launch replaces rmsnorm + wait +
+// transfer.
+struct CasSendArgs {
+  const bf16* x; int ldx;
+  const bf16* g; float eps;
+  int rows, h;
+  bf16* dst; int ldd;          // owner staging rows, u -> cols [0, h), x -> cols [h, 2h)
+  FlagWait wait;               // owner's previous round trip served
+  uint64_t* arrive; uint64_t value;
+  unsigned int* counter;       // last-CTA election (0 between launches)
+};
+cudaError_t cas_send_norm_launch(const CasSendArgs& a, cudaStream_t s);
 // qkv fp32 [B, (nq+2nkv)*hd] -> q bf16 [B, nq, hd]; k, v appended to caches at pos[b]
 struct QkvPostArgs {
   const float* qkv; int B, nq, nkv, hd;
@@ -147,6 +174,8 @@ struct QkvPostArgs {
   int smax;
   PartialSrc part;                              // part.ws != null: qkv is the sum of these slices
   const bf16* bias;                             // added in the partial form only (else by the GEMM)
+  int ldqkv;                                    // qkv row stride in floats (0 = (nq + 2 nkv) hd)
+  FlagWait wait;                                // optional: qkv is read once these flags are set
 };
 cudaError_t qkv_post_launch(const QkvPostArgs& a, cudaStream_t s);
 
@@ -154,7 +183,8 @@ struct AttnArgs {
   const bf16* q;              // [B, nq, hd]
   const bf16* kc; const bf16* vc;   // [Bmax, nkv, Smax, hd]
   const int32_t* pos;         // attend over [0, pos_b]
-  bf16* o;                    // [B, nq*hd]
+  bf16* o;                    // [B, nq*hd], row stride ldo (0 = nq*hd; may be a peer VA)
+  int ldo;
   int B, nq, nkv, hd, smax;
   int max_tokens;             // host hint: max_b (pos_b + 1) <= smax (sizes the grid)
   float* ws; size_t ws_bytes; // partials of (b, g) pairs split across CTAs
@@ -202,6 +232,7 @@ constexpr int kRingMaxSlots = 16;
 constexpr int kFetchLogCap = 4096;
 constexpr int kFetchStages = 6;                 // shared-memory ring of the bulk fetch
 constexpr int kFetchChunk = 32 * 1024;          // bytes per bulk copy
+constexpr int kFetchClaim = 8;                  // chunks per atomic claim (SIDP_FETCH_CLAIM)
 struct FetchLogEnt {
   unsigned long long j;        // fetch index since the last reset
   int layer, slot, owner, pad;
@@ -218,8 +249,16 @@ struct FetchRing {
   unsigned long long rel[kRingMaxSlots];    // releases per slot (compute side)
   unsigned long long cons[kRingMaxSlots];   // consumptions started (compute side)
   unsigned long long t_first[kRingMaxSlots];   // earliest CTA start of the slot's current fill
-  unsigned int arrive[kRingMaxSlots];       // CTAs done with the slot's current fill
+  unsigned int arrive[kRingMaxSlots];       // CTAs done with the slot's current fill (static split)
   int tag[kRingMaxSlots];                   // layer held by the slot (last fill)
+  // dynamic chunk claiming (fetch_bulk_kernel): fill n of slot s owns claim indices
+  // [n (nch + F), (n + 1)(nch + F)) — each CTA over-claims at most once per fill — and is complete
+  // when done[s] reaches (n + 1) nch; t0[s] = paced start of fill t0_fill[s] - 1
+  unsigned long long claim[kRingMaxSlots];
+  unsigned long long done[kRingMaxSlots];
+  unsigned long long t0[kRingMaxSlots];
+  unsigned long long t0_fill[kRingMaxSlots];
+  unsigned long long link_t;                // emulated link: due end of the last started fill
   unsigned long long nfetch, ncons;
   FetchLogEnt log[kFetchLogCap];
   ConsLogEnt clog[kFetchLogCap];
@@ -241,6 +280,7 @@ struct FetchArgs {
   uint64_t delay_ns;           // start offset (C-S7 stagger) before the first entry
   uint64_t timeout_ns; int* err;   // gate timeout -> *err (mapped host word)
   int chunk, stages;           // set by fetch_bulk_launch (shared-memory ring geometry)
+  int claim_group;             // set by fetch_bulk_launch: chunks per atomic claim
   FetchEnt ent[kFetchWindow];
 };
 size_t fetch_bulk_smem();
@@ -275,6 +315,9 @@ struct XferSet {
   unsigned int* counter;
 };
 cudaError_t xfer_launch(const XferSet& x, cudaStream_t s);
+// Wait for the flags, then copy rows (CaS requester: the owner's returned slice -> x).
+cudaError_t wait_copy_launch(const FlagWait& w, void* dst, int ldd, const void* src, int lds,
+                             int rows, int row_bytes, cudaStream_t s);
 
 // Eager module loading of every kernel (called once by sidp_alloc).
 cudaError_t gemm_preload();

@@ -42,6 +42,11 @@ __global__ void __launch_bounds__(256, 2) qkv_post_kernel(QkvPostArgs a) {
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nh = a.nq + 2 * a.nkv;
+  if (a.wait.n) {   // CaS: the owner's returned qkv rows have landed (done flag)
+    if (threadIdx.x == 0) flags_wait(a.wait.p, a.wait.n, a.wait.value, a.wait.timeout_ns, a.wait.err);
+    __syncthreads();
+  }
+  const size_t ldqkv = a.ldqkv > 0 ? (size_t)a.ldqkv : (size_t)nh * HD;
   const int pos = a.pos[b];
   const int i0 = E * lane;
   float cs[E][2];
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(256, 2) qkv_post_kernel(QkvPostArgs a) {
         }
       }
     } else {
-      load(a.qkv + ((size_t)b * nh + head) * HD, x1[hh], x2[hh]);
+      load(a.qkv + (size_t)b * ldqkv + (size_t)head * HD, x1[hh], x2[hh]);
     }
   }
   // phase 2: qk-norm, RoPE, stores
@@ -192,6 +197,7 @@ struct AttnParams {
   const bf16* vc;
   const int32_t* pos;
   bf16* o;
+  size_t ldo;                // row stride of o per sequence (elements)
   float* ws;                 // [C][2 sides][16 rows][HD + 2] partials of split (b, g) pairs
   int* cnt;                  // [B * nkv] arrival counters of split pairs (zero between launches)
   int B, nq, nkv, smax;
@@ -525,7 +531,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
         }
       }
       if (whole) {
-        p.o[((size_t)b * p.nq + g * G + row) * HD + col] = f_to_bf16(L > 0.0f ? O / L : 0.0f);
+        p.o[(size_t)b * p.ldo + (size_t)(g * G + row) * HD + col] = f_to_bf16(L > 0.0f ? O / L : 0.0f);
       } else {
         float* pr = part + (size_t)row * (HD + 2);
         __stcg(pr + 2 + col, O);
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
           const int idx = threadIdx.x + 128 * u, row = idx / HD, col = idx % HD;
           if (row < G) {
             const float L = sm_L[row];
-            p.o[((size_t)b * p.nq + g * G + row) * HD + col] = f_to_bf16(L > 0.0f ? acc[u] / L : 0.0f);
+            p.o[(size_t)b * p.ldo + (size_t)(g * G + row) * HD + col] = f_to_bf16(L > 0.0f ? acc[u] / L : 0.0f);
           }
         }
         if (threadIdx.x == 0) *counter = 0;   // every piece has arrived: reset for the next launch
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
       const int row = gid + 8 * h;
       if (row < G) {
         const float L = lrow[h];
-        bf16* dst = p.o + ((size_t)b * p.nq + g * G + row) * HD + 2 * tq;
+        bf16* dst = p.o + (size_t)b * p.ldo + (size_t)(g * G + row) * HD + 2 * tq;
 #pragma unroll
         for (int dn = 0; dn < HD / 8; ++dn)
           *reinterpret_cast<__nv_bfloat162*>(dst + dn * 8) =
@@ -797,7 +803,7 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
     const long long wslots = (long long)compute_sms() * std::max(1, wper);
     const int wctas = (int)std::min<long long>(wslots, (pairs + kWarps - 1) / kWarps);
     AttnParams p{};
-    p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws; p.cnt = a.cnt;
+    p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ldo = a.ldo > 0 ? (size_t)a.ldo : (size_t)a.nq * a.hd; p.ws = a.ws; p.cnt = a.cnt;
     p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
     static const int env_evict_w = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
     p.kv_evict = env_evict_w;
@@ -811,7 +817,7 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
     ctas = (int)(a.ws_bytes / ((size_t)2 * 16 * (HD + 2) * 4));
   if (ctas < 1) return cudaErrorInvalidValue;
   AttnParams p;
-  p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ws = a.ws; p.cnt = a.cnt;
+  p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ldo = a.ldo > 0 ? (size_t)a.ldo : (size_t)a.nq * a.hd; p.ws = a.ws; p.cnt = a.cnt;
   p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
   static const int env_evict = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
   p.kv_evict = env_evict;

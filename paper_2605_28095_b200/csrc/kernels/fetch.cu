@@ -102,7 +102,31 @@ __global__ void copy_rows_kernel(uint8_t* dst, int ldd, const uint8_t* src, int 
   }
 }
 
+// every CTA waits for the flags (thread 0, acquire), then copies its rows
+__global__ void wait_copy_kernel(const FlagWait w, uint8_t* dst, int ldd, const uint8_t* src,
+                                 int lds, int rows, int row_bytes) {
+  if (threadIdx.x == 0) flags_wait(w.p, w.n, w.value, w.timeout_ns, w.err);
+  __syncthreads();
+  const int nvec = row_bytes / 16;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)r * lds);
+    uint4* d = reinterpret_cast<uint4*>(dst + (size_t)r * ldd);
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x)
+      d[v] = __ldcg(s + v);
+  }
+}
+
 }  // namespace
+
+cudaError_t wait_copy_launch(const FlagWait& w, void* dst, int ldd, const void* src, int lds,
+                             int rows, int row_bytes, cudaStream_t s) {
+  if (rows <= 0 || row_bytes <= 0) return cudaSuccess;
+  if (row_bytes % 16 || w.n > 16) return cudaErrorInvalidValue;
+  dim3 grid((row_bytes / 16 + 255) / 256, rows < 1024 ? rows : 1024);
+  wait_copy_kernel<<<grid, 256, 0, s>>>(w, reinterpret_cast<uint8_t*>(dst), ldd,
+                                        reinterpret_cast<const uint8_t*>(src), lds, rows, row_bytes);
+  return cudaGetLastError();
+}
 
 cudaError_t fetch_launch(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s,
                          float pace_gbps) {
@@ -212,6 +236,7 @@ cudaError_t fetch_preload() {
   if (cudaFuncGetAttributes(&fa, wait_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, copy_rows_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, xfer_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, wait_copy_kernel) != cudaSuccess) e = cudaGetLastError();
   return e;
 }
 

@@ -60,6 +60,7 @@ struct KParams {
   int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
   QkvEpi qkv;                   // EPI_QKV destination
+  FlagWait wait;                // CaS owner: activation loads wait for the arrival flags
 };
 
 // ---- cluster / 2-SM helpers ------------------------------------------------------
@@ -612,6 +613,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
       }
       pdl_wait();
+      if (p.wait.n) flags_wait(p.wait.p, p.wait.n, p.wait.value, p.wait.timeout_ns, p.wait.err);
       for (int it = 0; cur.valid; cur.advance(p, cluster), ++it) {
         const int s = it % stages;
         const uint32_t ph = (it / stages) & 1;
@@ -1548,7 +1550,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     }
   }
 
-  KParams p;
+  KParams p{};
   p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
   p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.tiles = tiles; p.streamk = streamk;
   p.total_kb = (long long)(tiles - dp_tiles) * nkb; p.clusters = clusters; p.kps = kps; p.nks = nkb;
@@ -1562,6 +1564,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   // several token tiles the other units re-read the same W tile from L2
   p.w_evict = env_evict && (sw ? n_pairs == 1 : m_tiles == 1);
   if (a.qkv) p.qkv = *a.qkv;
+  if (a.wait) p.wait = *a.wait;
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
   static int env_trace = getenv("SIDP_GEMM_TRACE") ? atoi(getenv("SIDP_GEMM_TRACE")) : 0;

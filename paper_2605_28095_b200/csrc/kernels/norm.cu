@@ -88,6 +88,68 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(const bf16* __res
   }
 }
 
+// CaS requester, round trip 1 (see cas_send_norm_launch): the rmsnorm_kernel arithmetic with the
+// row's u and x stored into the owner's staging row [u | x] (a peer VA), then the last CTA to
+// finish posts the arrival flag with release semantics at system scope.
+__global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSendArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  if (a.wait.n) {   // the owner served its previous round trip: its staging slots are free
+    if (threadIdx.x == 0) flags_wait(a.wait.p, a.wait.n, a.wait.value, a.wait.timeout_ns, a.wait.err);
+    __syncthreads();
+  }
+  const int h = a.h, nvec = h / 8;
+  for (int row = blockIdx.x; row < a.rows; row += gridDim.x) {
+    const bf16* xr = a.x + (size_t)row * a.ldx;
+    bf16* ur = a.dst + (size_t)row * a.ldd;
+    bf16* xd = ur + h;
+    float ss = 0.0f;
+    for (int k = threadIdx.x; k < nvec; k += kNormThreads) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(xr + k * 8);
+      *reinterpret_cast<uint4*>(xd + k * 8) = raw;
+      const bf16* e = reinterpret_cast<const bf16*>(&raw);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float f = bf16_to_f(e[q]);
+        ss += f * f;
+      }
+    }
+    __shared__ float red[32];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float t = threadIdx.x < (kNormThreads >> 5) ? red[threadIdx.x] : 0.0f;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float r = rsqrtf(red[0] / (float)h + a.eps);
+    for (int k = threadIdx.x; k < nvec; k += kNormThreads) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(xr + k * 8);
+      const uint4 graw = *reinterpret_cast<const uint4*>(a.g + k * 8);
+      const bf16* e = reinterpret_cast<const bf16*>(&raw);
+      const bf16* ge = reinterpret_cast<const bf16*>(&graw);
+      uint4 out;
+      bf16* o = reinterpret_cast<bf16*>(&out);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = f_to_bf16(bf16_to_f(e[q]) * r * bf16_to_f(ge[q]));
+      *reinterpret_cast<uint4*>(ur + k * 8) = out;
+    }
+    __syncthreads();   // red[] reused by the next row
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(a.counter, 1u);
+    if (prev == gridDim.x - 1) {
+      *a.counter = 0u;
+      __threadfence_system();
+      st_release_sys(a.arrive, a.value);
+    }
+  }
+}
+
 // Deferred stream-K fix-up + residual + RMSNorm, one CTA per row (see resid_norm_launch), one
 // thread per 8-feature vector (h <= 8 * 640; longer rows loop).  Per vector the fp32 partial
 // slices of its tile are summed in slice order, the bf16 residual added in fp32 and the sum
@@ -202,6 +264,12 @@ cudaError_t rmsnorm_launch(const bf16* x, int ldx, const bf16* g, float eps, bf1
   return launch_pdl(rmsnorm_kernel, dim3(rows), dim3(kNormThreads), 0, s, x, ldx, g, eps, y, ldy, h);
 }
 
+cudaError_t cas_send_norm_launch(const CasSendArgs& a, cudaStream_t s) {
+  if (a.rows <= 0) return cudaSuccess;
+  if ((a.h & 7) || !a.counter || !a.arrive || a.wait.n > 16) return cudaErrorInvalidValue;
+  return launch_pdl(cas_send_norm_kernel, dim3(std::min(a.rows, 148)), dim3(kNormThreads), 0, s, a);
+}
+
 cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, bf16* xout, int ldx,
                               const bf16* g, float eps, bf16* u, int ldu, int rows, int h,
                               cudaStream_t s, unsigned long long* post) {
@@ -254,6 +322,7 @@ cudaError_t norm_preload() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaSuccess;
   if (cudaFuncGetAttributes(&fa, rmsnorm_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, cas_send_norm_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, embed_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, resid_norm_kernel<8, 640>) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, resid_norm_kernel<kFixSeg, 1024>) != cudaSuccess) e = cudaGetLastError();

@@ -109,6 +109,24 @@ SIDP_DEV void fetch_publish(const FetchArgs& a, const FetchEnt& e, int F) {
   st_release_gpu(&r->fill[e.slot], (unsigned long long)e.fill + 1);
 }
 
+// Dynamic-claim publish (the CTA whose stored-chunk count completes fill e.fill + 1).
+SIDP_DEV void fetch_publish_dyn(const FetchArgs& a, const FetchEnt& e, unsigned long long t_start) {
+  FetchRing* r = a.ring;
+  r->tag[e.slot] = e.layer;
+  const unsigned long long j = r->nfetch;
+  FetchLogEnt& g = r->log[j % kFetchLogCap];
+  g.j = j;
+  g.layer = e.layer;
+  g.slot = e.slot;
+  g.owner = e.owner;
+  g.epoch = (unsigned long long)e.fill + 1;
+  g.t_start = t_start;
+  g.t_end = globaltimer_ns();
+  r->nfetch = j + 1;
+  __threadfence();
+  st_release_gpu(&r->fill[e.slot], (unsigned long long)e.fill + 1);
+}
+
 // Windowed gate (one thread per CTA): the slot's previous fill is published and its reader has
 // released it — rel[slot] >= fill.  Waiting here holds this CTA's SM, which the compute grids
 // never count on (their SM budget excludes the fetch's).
@@ -139,17 +157,112 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
     while (globaltimer_ns() - t0 < a.delay_ns) __nanosleep(1000);
   }
   const size_t nchunks = (a.bytes + CH - 1) / CH;
-  const size_t mine = nchunks > (size_t)b ? (nchunks - b + F - 1) / F : 0;
+  auto len_of = [&](size_t c) { return (uint32_t)std::min<size_t>(CH, a.bytes - c * CH); };
   uint32_t use = 0;   // ring uses so far (stage = use % NST, parity = (use / NST) & 1)
+  if (a.ring) {
+    // Device ring: chunks are CLAIMED (atomic per-slot counter), so a layer streams front to
+    // back across whichever CTAs are fastest and no CTA's lag delays the publish; with the
+    // emulated link rate, chunk v of a fill is due at t0 + v x ns, t0 = max(first claim, due
+    // end of the previous fill) — one continuously busy link, as a real reader's.
+    FetchRing* r = a.ring;
+    for (int k = 0; k < a.n; ++k) {
+      const FetchEnt& e = a.ent[k];
+      fetch_gate(a, e);
+      const int sl = e.slot;
+      // claims are groups of G chunks (one atomic per G x chunk bytes: the claim's latency sits
+      // in the single issuing thread's path); fill n owns group claims [n (ng + F), ...)
+      const unsigned long long G = (unsigned long long)a.claim_group;
+      const unsigned long long ngroups = (nchunks + G - 1) / G;
+      const unsigned long long base = (unsigned long long)e.fill * (ngroups + F);
+      const uint8_t* src = e.src;
+      uint8_t* dst = a.slots + (size_t)sl * a.slot_stride;
+      unsigned long long t0 = 0;
+      bool have_t0 = false;
+      auto get_t0 = [&](unsigned long long v) {
+        if (have_t0) return;
+        if (v == 0) {
+          unsigned long long now = globaltimer_ns();
+          if (a.ns_per_chunk && k > 0) {   // the previous fill's start (and link_t) is published
+            const FetchEnt& pe = a.ent[k - 1];
+            spin_ge(&r->t0_fill[pe.slot], (unsigned long long)pe.fill + 1, a.timeout_ns, a.err, 4);
+          }
+          if (a.ns_per_chunk) {
+            const unsigned long long lt = *reinterpret_cast<volatile unsigned long long*>(&r->link_t);
+            t0 = now > lt ? now : lt;
+            r->link_t = t0 + (unsigned long long)nchunks * a.ns_per_chunk;
+          } else {
+            t0 = now;
+          }
+          r->t0[sl] = t0;
+          __threadfence();
+          st_release_gpu(&r->t0_fill[sl], (unsigned long long)e.fill + 1);
+        } else {
+          spin_ge(&r->t0_fill[sl], (unsigned long long)e.fill + 1, a.timeout_ns, a.err, 4);
+          t0 = *reinterpret_cast<volatile unsigned long long*>(&r->t0[sl]);
+        }
+        have_t0 = true;
+      };
+      unsigned long long cid[16];
+      unsigned long long gnext = 0, gend = 0;   // claimed chunks [gnext, gend) not yet issued
+      uint32_t iss = 0, cmp = 0;
+      bool exhausted = false;
+      auto issue = [&]() {   // the next claimed chunk of this fill (claiming a group if needed)
+        if (gnext >= gend) {
+          const unsigned long long g = atomicAdd(&r->claim[sl], 1ull) - base;
+          if (g >= ngroups) {
+            exhausted = true;
+            return;
+          }
+          gnext = g * G;
+          gend = gnext + G < nchunks ? gnext + G : nchunks;
+          get_t0(g);
+        }
+        const unsigned long long v = gnext++;
+        if (a.ns_per_chunk) {
+          const uint64_t due = t0 + v * a.ns_per_chunk;
+          while (globaltimer_ns() < due) __nanosleep(256);
+        }
+        const uint32_t u = use + iss;
+        const int st = (int)(u % NST);
+        cid[u % 16] = v;
+        mbar_arrive_expect_tx(&bars[st], len_of(v));
+        bulk_load(fsm + (size_t)st * CH, src + v * CH, len_of(v), &bars[st]);
+        ++iss;
+      };
+      while (!exhausted && iss < (uint32_t)(NST - 1)) issue();
+      while (cmp < iss) {
+        const uint32_t u = use + cmp;
+        const int st = (int)(u % NST);
+        mbar_wait(&bars[st], (u / NST) & 1);
+        const unsigned long long v = cid[u % 16];
+        bulk_store(dst + v * CH, fsm + (size_t)st * CH, len_of(v));
+        bulk_commit();
+        ++cmp;
+        if (!exhausted) {
+          bulk_wait_read<1>();   // the stage of the next load was last read by store cmp - 2
+          issue();
+        }
+      }
+      use += iss;
+      bulk_wait_all();           // every store of this CTA performed (and smem free again)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      if (cmp > 0) {
+        const unsigned long long target = (unsigned long long)(e.fill + 1) * nchunks;
+        const unsigned long long prev = atomicAdd(&r->done[sl], (unsigned long long)cmp);
+        if (prev + cmp == target) fetch_publish_dyn(a, e, t0);
+      }
+    }
+    return;
+  }
+  // plain copy (test hook, no ring): CTA b copies chunks b, b + F, b + 2F, ... of every entry
+  const size_t mine = nchunks > (size_t)b ? (nchunks - b + F - 1) / F : 0;
   for (int k = 0; k < a.n; ++k) {
     const FetchEnt& e = a.ent[k];
-    fetch_gate(a, e);
     const uint64_t t_start = globaltimer_ns();
-    if (a.ring) atomicMin(&a.ring->t_first[e.slot], (unsigned long long)t_start);
     const uint8_t* src = e.src;
     uint8_t* dst = a.slots + (size_t)e.slot * a.slot_stride;
     auto chunk_of = [&](size_t i) { return (size_t)b + i * F; };
-    auto len_of = [&](size_t c) { return (uint32_t)std::min<size_t>(CH, a.bytes - c * CH); };
     auto issue = [&](size_t i) {
       const size_t c = chunk_of(i);
       if (a.ns_per_chunk) {   // NVLink-rate emulation: chunk c starts >= c x ns after the start
@@ -176,10 +289,7 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
       }
     }
     use += (uint32_t)mine;
-    bulk_wait_all();           // every store of this CTA performed (and smem free again)
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __threadfence();
-    fetch_publish(a, e, F);
+    bulk_wait_all();
   }
 }
 
@@ -305,6 +415,8 @@ cudaError_t fetch_bulk_launch(const FetchArgs& a, int ctas, cudaStream_t s) {
   ctas = std::max(2, ctas & ~1);
   FetchArgs b = a;
   bulk_geometry(&b.chunk, &b.stages);
+  static const int grp = getenv("SIDP_FETCH_CLAIM") ? std::max(1, atoi(getenv("SIDP_FETCH_CLAIM"))) : kFetchClaim;
+  b.claim_group = grp;
   static unsigned long long attr = 0;
   if (first_on_device(attr)) {
     cudaFuncSetAttribute(fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

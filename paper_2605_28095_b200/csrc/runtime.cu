@@ -57,7 +57,19 @@ struct HandleBlob {
   uint64_t arena_bytes, cas_bytes;
   cudaIpcMemHandle_t arena_h, cas_h;
   int32_t has_arena, has_cas;
+  unsigned char uuid[16];   // the GPU (cudaDeviceProp::uuid): peers on the same GPU share it
 };
+
+bool device_uuid(int device, unsigned char (&out)[16]) {
+  cudaDeviceProp p{};
+  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) {
+    cudaGetLastError();
+    std::memset(out, 0, 16);
+    return false;
+  }
+  std::memcpy(out, p.uuid.bytes, 16);
+  return true;
+}
 
 }  // namespace
 
@@ -125,6 +137,8 @@ struct sidp_ctx {
   std::vector<int> batches;        // per-rank rows (control plane)
   int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
+  std::vector<int64_t> last_rt_any;             // [owner] last round trip with that owner (V3)
+  bool same_device_peer = false;                // a peer shares this GPU (virtual ranks / 1-GPU IPC)
   // WaS schedule state
   int64_t fetch_j = 0, compute_k = 0;
   std::vector<int> slot_of_fetch;        // FIFO recurrence, extended lazily (slot_for_fetch)
@@ -390,8 +404,9 @@ sidp::GemmWorkspace gws(sidp_ctx* c) {
 cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, int M, int N, int K,
                  int epi, void* out, int ldo, const bf16* resid, int ldr, const bf16* bias,
                  cudaStream_t s, const sidp::QkvEpi* qkv = nullptr,
-                 sidp::PartialSrc* partial = nullptr) {
+                 sidp::PartialSrc* partial = nullptr, const sidp::FlagWait* wait = nullptr) {
   sidp::GemmArgs a{};
+  a.wait = wait;
   a.x = x; a.ldx = ldx; a.w = w; a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = epi;
   a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias; a.qkv = qkv;
   a.partial_out = partial;
@@ -405,8 +420,17 @@ cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, in
 // ---- the layer's kernels ----------------------------------------------------------
 // Attention half up to o (C-N2 steps 1-6).  When `qkv_in` is given (CaS RT1 returned it),
 // the RMSNorm + QKV GEMM are skipped.
+// CaS hooks of attn_part: qkv_in's rows are read once `qkv_wait` holds (the owner's done flag),
+// and o goes straight to `o_dst` (the owner's staging rows, row stride ldo_dst) — V3.
+struct AttnHooks {
+  const sidp::FlagWait* qkv_wait = nullptr;
+  bf16* o_dst = nullptr;
+  int ldo_dst = 0;
+};
+
 sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int layer,
-                      const sidp_kv* kv, const float* qkv_in, cudaStream_t s) {
+                      const sidp_kv* kv, const float* qkv_in, cudaStream_t s,
+                      const AttnHooks* hk = nullptr) {
   const auto& m = ctx->m;
   const size_t lstride = (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
   bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
@@ -452,6 +476,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
     qa.qkv = qkv_in; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
     qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;
     qa.q = ctx->q; qa.kc = kc; qa.vc = vc; qa.smax = ctx->c.max_ctx;
+    if (hk && hk->qkv_wait) qa.wait = *hk->qkv_wait;
     if (part.ws) {
       qa.part = part;
       qa.bias = W.b_qkv;
@@ -461,6 +486,10 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   }
   sidp::AttnArgs aa{};
   aa.q = ctx->q; aa.kc = kc; aa.vc = vc; aa.pos = kv->pos; aa.o = ctx->o; aa.B = B;
+  if (hk && hk->o_dst) {
+    aa.o = hk->o_dst;
+    aa.ldo = hk->ldo_dst;
+  }
   aa.nq = m.n_q_heads; aa.nkv = m.n_kv_heads; aa.hd = m.head_dim; aa.smax = ctx->c.max_ctx;
   // the split is sized from max_ctx (not the per-step max_pos) so the launch configuration is
   // step-invariant and a captured CUDA graph stays valid; empty splits exit immediately
@@ -478,18 +507,19 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
 // u = RMSNorm(out) * next_g for the next layer (ctx->u_for).
 sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf16* x, int ldx,
                      bf16* out, int B, cudaStream_t s, const bf16* next_g = nullptr,
-                     int next_layer = -1) {
+                     int next_layer = -1, const sidp::FlagWait* wait = nullptr) {
   const auto& m = ctx->m;
   const int h = m.hidden;
   // x2 = x + o W_o^T  (into out), u2 = RMSNorm(x2) * g_mlp
   sidp::PartialSrc part{};
   if (sidp::gemm_partial_ok(B, h, ctx->qdim, ctx->gemm_ws_bytes)) {
     CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_PARTIAL, nullptr, 0, nullptr, 0,
-            nullptr, s, nullptr, &part));
+            nullptr, s, nullptr, &part, wait));
     if (!(dbg_skip() & 2)) CK(sidp::resid_norm_launch(part, x, ldx, out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
   } else {
-    CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, out, h, x, ldx, nullptr, s));
+    CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, out, h, x, ldx, nullptr, s,
+            nullptr, nullptr, wait));
     CK(sidp::rmsnorm_launch(out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
   }
@@ -765,10 +795,37 @@ size_t flag_off_served(int world) { return (size_t)world * 8 + 8; }
 
 uint64_t* flag_ptr(uint8_t* base, size_t off) { return reinterpret_cast<uint64_t*>(base + off); }
 
-// SIDP_CAS_FUSED=0: one copy kernel per part / destination and one signal kernel per flag
-bool cas_fused() {
-  static const bool v = !(getenv("SIDP_CAS_FUSED") && atoi(getenv("SIDP_CAS_FUSED")) == 0);
+// CaS ladder: SIDP_CAS_FUSED=0 (V1) one copy kernel per part / destination
+// and one signal kernel per flag; 1 (V2) one fused transfer launch per direction; 2 (V3, the
+// default) sends fused into the producing kernels (RMSNorm -> peer staging rows; attention
+// writes o straight into the owner's staging rows), flag waits folded into the consumers'
+// prologues, the return copy fused with its wait.
+int cas_level() {
+  static const int v = getenv("SIDP_CAS_FUSED") ? atoi(getenv("SIDP_CAS_FUSED")) : 2;
   return v;
+}
+bool cas_fused() { return cas_level() >= 1; }
+
+// Prologue waits spin inside the consumer grid's CTAs.  On one GPU shared with the peers
+// (virtual ranks, the 1-GPU IPC test) spinning CTAs could hold the SMs a peer needs to make the
+// progress they wait for, so there a standalone 1-CTA wait kernel gates the consumer instead
+// (SIDP_CAS_PROLOGUE_WAIT=1/0 forces either).
+bool prologue_waits(const sidp_ctx* c) {
+  static const int env = getenv("SIDP_CAS_PROLOGUE_WAIT") ? atoi(getenv("SIDP_CAS_PROLOGUE_WAIT")) : -1;
+  return env >= 0 ? env != 0 : !c->same_device_peer;
+}
+
+// A FlagWait for a consumer kernel, or (no prologue waits) a standalone wait kernel now and an
+// empty FlagWait.
+sidp_status consumer_wait(sidp_ctx* ctx, sidp::FlagWait& w, cudaStream_t s) {
+  if (w.n == 0 || prologue_waits(ctx)) return SIDP_OK;
+  sidp::FlagSet fs{};
+  for (int i = 0; i < w.n; ++i) fs.p[i] = const_cast<uint64_t*>(w.p[i]);
+  fs.n = w.n;
+  CK(sidp::wait_launch(fs, w.value, w.timeout_ns, w.err, s));
+  count_launch(ctx);
+  w.n = 0;
+  return SIDP_OK;
 }
 
 // One CaS round trip: live ranks copy their rows into the owner's
@@ -888,12 +945,221 @@ sidp_status cas_round_trip(sidp_ctx* ctx, int layer, const std::vector<SendPart>
   return SIDP_OK;
 }
 
+// ---- CaS V3 (SIDP_CAS_FUSED=2) -------------------------------------------------------
+// One layer (pool scope LAYER: 2 round trips, FFN: 1), per rank, in stream order:
+//   requester:  cas_send_norm (waits the owner's previous round trip served; u = RMSNorm(x) g
+//               and x -> the owner's staging rows; arrival)             [RT1 / the FFN trip]
+//   owner:      QKV GEMM (prologue waits the live ranks' arrivals) -> xfer back + done + served
+//   requester:  qkv_post (prologue waits done; reads the returned qkv) -> attention (o -> the
+//               owner's staging rows of RT2) -> arrival signal                        [RT2]
+//   owner:      O GEMM (prologue waits arrivals; x from RT1's rows) -> ... -> down -> xfer back
+//   requester:  wait + copy of the returned rows into x
+// Round trip rt uses staging slot rt % cas_slots; RT2's owner compute reads x from RT1's slot,
+// which stays intact because the next send to this owner waits until RT2 was served.
+struct CasTrip {
+  int64_t rt;
+  int slot, total, o;
+  std::vector<int> off;
+};
+
+CasTrip cas_trip(sidp_ctx* ctx, int layer) {
+  CasTrip t;
+  t.rt = ctx->rt++;
+  t.slot = (int)(t.rt % ctx->c.cas_slots);
+  t.o = ctx->owner[layer];
+  t.off.assign(ctx->d, 0);
+  t.total = 0;
+  for (int q = 0; q < ctx->d; ++q) {
+    t.off[q] = t.total;
+    t.total += ctx->batches[q];
+  }
+  return t;
+}
+
+uint8_t* cas_stage_ptr(const sidp_ctx* ctx, uint8_t* cas_base, int slot, int row) {
+  return cas_base + ctx->cas_stage_off + (size_t)slot * ctx->cas_stage_bytes +
+         (size_t)row * ctx->stage_width * 2;
+}
+
+// arrivals of every live rank for round trip rt (owner side)
+sidp::FlagWait arrivals_wait(sidp_ctx* ctx, int64_t rt) {
+  sidp::FlagWait w{};
+  for (int q = 0; q < ctx->d; ++q)
+    if (ctx->batches[q] > 0) w.p[w.n++] = flag_ptr(ctx->cas, flag_off_arrive(q));
+  w.value = (uint64_t)rt + 1;
+  w.timeout_ns = ctx->cas_timeout_ns;
+  w.err = ctx->dev_err;
+  return w;
+}
+
+sidp::FlagWait single_wait(sidp_ctx* ctx, const uint64_t* flag, uint64_t value) {
+  sidp::FlagWait w{};
+  w.p[0] = flag;
+  w.n = 1;
+  w.value = value;
+  w.timeout_ns = ctx->cas_timeout_ns;
+  w.err = ctx->dev_err;
+  return w;
+}
+
+// requester: u = RMSNorm(x) g and x into the owner's staging rows + arrival (one launch)
+sidp_status cas_send(sidp_ctx* ctx, const CasTrip& t, const bf16* x, const bf16* g, int B,
+                     cudaStream_t s) {
+  const int me = ctx->r;
+  uint8_t* owner_cas = ctx->peer_cas[t.o];
+  sidp::CasSendArgs a{};
+  a.x = x; a.ldx = ctx->m.hidden; a.g = g; a.eps = ctx->m.rms_eps; a.rows = B; a.h = ctx->m.hidden;
+  a.dst = reinterpret_cast<bf16*>(cas_stage_ptr(ctx, owner_cas, t.slot, t.off[me]));
+  a.ldd = ctx->stage_width;
+  if (ctx->last_rt_any[t.o] >= 0)
+    a.wait = single_wait(ctx, flag_ptr(owner_cas, flag_off_served(ctx->d)),
+                         (uint64_t)ctx->last_rt_any[t.o] + 1);
+  sidp_status st = consumer_wait(ctx, a.wait, s);
+  if (st != SIDP_OK) return st;
+  a.arrive = flag_ptr(owner_cas, flag_off_arrive(me));
+  a.value = (uint64_t)t.rt + 1;
+  a.counter = ctx->xfer_cnt;
+  CK(sidp::cas_send_norm_launch(a, s));
+  count_launch(ctx);
+  return SIDP_OK;
+}
+
+// owner: every live rank's slice of `result` back to its receive buffer, then done + served
+sidp_status cas_return(sidp_ctx* ctx, const CasTrip& t, const uint8_t* result, size_t result_ld,
+                       size_t row_bytes, cudaStream_t s) {
+  sidp::XferSet xs{};
+  for (int q = 0; q < ctx->d; ++q) {
+    if (ctx->batches[q] == 0) continue;
+    xs.job[xs.njobs++] = sidp::XferJob{ctx->peer_cas[q] + ctx->cas_recv_off,
+                                       result + (size_t)t.off[q] * result_ld, (int)row_bytes,
+                                       (int)result_ld, ctx->batches[q], (int)row_bytes};
+    xs.flag[xs.nflags++] = flag_ptr(ctx->peer_cas[q], flag_off_done(ctx->d));
+  }
+  xs.flag[xs.nflags++] = flag_ptr(ctx->cas, flag_off_served(ctx->d));
+  xs.value = (uint64_t)t.rt + 1;
+  xs.counter = ctx->xfer_cnt;
+  CK(sidp::xfer_launch(xs, s));
+  count_launch(ctx);
+  return SIDP_OK;
+}
+
+sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* kv,
+                         cudaStream_t s) {
+  const auto& m = ctx->m;
+  const int me = ctx->r, h = m.hidden;
+  const int o = ctx->owner[layer];
+  const bf16* local = ctx->local + (size_t)layer * ctx->local_elems;
+  const bf16* own_pooled =
+      o == me ? ctx->arena + (size_t)ctx->owned_index[layer] * ctx->pooled_elems : nullptr;
+  const LayerW W = layer_weights(ctx, own_pooled, local);   // pooled parts valid on the owner only
+  uint8_t* recv = ctx->cas + ctx->cas_recv_off;
+  uint8_t* owner_cas = ctx->peer_cas[o];
+  if (!owner_cas) return fail(SIDP_ESTATE, "CaS arena of rank %d not imported", o);
+  const uint64_t* done = flag_ptr(ctx->cas, flag_off_done(ctx->d));
+  sidp_status st;
+  if (ctx->c.pool_scope == SIDP_POOL_LAYER) {
+    CasTrip t1 = cas_trip(ctx, layer);
+    if (t1.total == 0) {   // every rank dummy: nothing moves (RT2 keeps the rt numbering)
+      cas_trip(ctx, layer);
+      return SIDP_OK;
+    }
+    if (B > 0) {
+      st = cas_send(ctx, t1, x, W.g_attn, B, s);
+      if (st != SIDP_OK) return st;
+    }
+    if (o == me) {   // RT1: u W_qkv^T (+b) in fp32 over all fused rows
+      sidp::FlagWait w = arrivals_wait(ctx, t1.rt);
+      st = consumer_wait(ctx, w, s);
+      if (st != SIDP_OK) return st;
+      const bf16* stage = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t1.slot, 0));
+      CK(gemm(ctx, 5, stage, ctx->stage_width, W.wqkv, t1.total, ctx->qkvdim, h, sidp::EPI_F32,
+              ctx->qkv, ctx->qkvdim, nullptr, 0, W.b_qkv, s, nullptr, nullptr, w.n ? &w : nullptr));
+      st = cas_return(ctx, t1, reinterpret_cast<const uint8_t*>(ctx->qkv), (size_t)ctx->qkvdim * 4,
+                      (size_t)ctx->qkvdim * 4, s);
+      if (st != SIDP_OK) return st;
+    }
+    CasTrip t2 = cas_trip(ctx, layer);
+    if (B > 0) {   // RoPE, KV append and attention stay local (the KV cache is local)
+      sidp::FlagWait dw = single_wait(ctx, done, (uint64_t)t1.rt + 1);
+      st = consumer_wait(ctx, dw, s);
+      if (st != SIDP_OK) return st;
+      AttnHooks hk;
+      hk.qkv_wait = dw.n ? &dw : nullptr;
+      hk.o_dst = reinterpret_cast<bf16*>(cas_stage_ptr(ctx, owner_cas, t2.slot, t2.off[me]));
+      hk.ldo_dst = ctx->stage_width;
+      st = attn_part(ctx, W, x, B, layer, kv, reinterpret_cast<const float*>(recv), s, &hk);
+      if (st != SIDP_OK) return st;
+      CK(sidp::signal_launch(flag_ptr(owner_cas, flag_off_arrive(me)), (uint64_t)t2.rt + 1, s));
+      count_launch(ctx);
+    }
+    if (o == me) {   // RT2: out = x2 + MLP(x2), x2 = x + o W_o^T, x from RT1's staging rows
+      sidp::FlagWait w = arrivals_wait(ctx, t2.rt);
+      st = consumer_wait(ctx, w, s);
+      if (st != SIDP_OK) return st;
+      const bf16* st_o = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t2.slot, 0));
+      bf16* st_x = reinterpret_cast<bf16*>(cas_stage_ptr(ctx, ctx->cas, t1.slot, 0)) + h;
+      st = mlp_part(ctx, W, st_o, ctx->stage_width, st_x, ctx->stage_width, ctx->cas_out, t2.total,
+                    s, nullptr, -1, w.n ? &w : nullptr);
+      if (st != SIDP_OK) return st;
+      st = cas_return(ctx, t2, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
+                      (size_t)h * 2, s);
+      if (st != SIDP_OK) return st;
+    }
+    ctx->last_rt_any[o] = t2.rt;
+    ctx->st.cas_round_trips += 2;
+    if (B > 0) {
+      CK(sidp::wait_copy_launch(single_wait(ctx, done, (uint64_t)t2.rt + 1), x, h * 2, recv, h * 2,
+                                B, h * 2, s));
+      count_launch(ctx);
+    }
+    return SIDP_OK;
+  }
+  // FFN scope (the paper's design): attention, O and the residual stay local; one round trip
+  // ships [u2 | x2] (the send fused with the post-attention RMSNorm) and returns
+  // out = x2 + SiLU(u2 W_g^T) * (u2 W_u^T) W_d^T.
+  CasTrip t = cas_trip(ctx, layer);
+  if (B > 0) {
+    st = attn_part(ctx, W, x, B, layer, kv, nullptr, s);
+    if (st != SIDP_OK) return st;
+    CK(gemm(ctx, 6, ctx->o, ctx->qdim, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, x, h, x, h,
+            nullptr, s));
+  }
+  if (t.total == 0) return SIDP_OK;
+  if (B > 0) {
+    st = cas_send(ctx, t, x, W.g_mlp, B, s);
+    if (st != SIDP_OK) return st;
+  }
+  if (o == me) {
+    sidp::FlagWait w = arrivals_wait(ctx, t.rt);
+    st = consumer_wait(ctx, w, s);
+    if (st != SIDP_OK) return st;
+    const bf16* stage = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t.slot, 0));
+    CK(gemm(ctx, 1, stage, ctx->stage_width, W.wgu, t.total, 2 * m.intermediate, h,
+            sidp::EPI_SILU_MUL, ctx->act, m.intermediate, nullptr, 0, nullptr, s, nullptr, nullptr,
+            w.n ? &w : nullptr));
+    CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, t.total, h, m.intermediate, sidp::EPI_RESID,
+            ctx->cas_out, h, stage + h, ctx->stage_width, nullptr, s));
+    st = cas_return(ctx, t, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
+                    (size_t)h * 2, s);
+    if (st != SIDP_OK) return st;
+  }
+  ctx->last_rt_any[o] = t.rt;
+  ctx->st.cas_round_trips++;
+  if (B > 0) {
+    CK(sidp::wait_copy_launch(single_wait(ctx, done, (uint64_t)t.rt + 1), x, h * 2, recv, h * 2, B,
+                              h * 2, s));
+    count_launch(ctx);
+  }
+  return SIDP_OK;
+}
+
 sidp_status cas_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* kv,
                       cudaStream_t s) {
   const auto& m = ctx->m;
   if ((int)ctx->batches.size() != ctx->d) return fail(SIDP_ESTATE, "sidp_set_batches not called");
   if (B != ctx->batches[ctx->r])
     return fail(SIDP_EINVAL, "batch %d != sidp_set_batches value %d", B, ctx->batches[ctx->r]);
+  if (cas_level() >= 2) return cas_layer_v3(ctx, x, B, layer, kv, s);
   const int o = ctx->owner[layer];
   const bf16* local = ctx->local + (size_t)layer * ctx->local_elems;
   const bf16* own_pooled =
@@ -1031,6 +1297,7 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
   }
   build_layout(c);
   c->last_rt.assign(c->d, std::vector<int64_t>(cfg->cas_slots, -1));
+  c->last_rt_any.assign(c->d, -1);
   c->mode = SIDP_WAS;
   c->st.mode = c->mode;
   schedule_reset(c);
@@ -1130,7 +1397,8 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   DM(ctx->attn_cnt, (size_t)ctx->n_attn_cnt * sizeof(int));
   CK(cudaMemset(ctx->attn_cnt, 0, (size_t)ctx->n_attn_cnt * sizeof(int)));
   // CaS arena: flags | stage slots | recv
-  ctx->stage_width = ctx->c.pool_scope == SIDP_POOL_LAYER ? ctx->qdim + m.hidden : 2 * m.hidden;
+  ctx->stage_width = ctx->c.pool_scope == SIDP_POOL_LAYER ? std::max(ctx->qdim + m.hidden, 2 * m.hidden)
+                                                         : 2 * m.hidden;
   ctx->cas_stage_bytes = align_up((size_t)R * ctx->stage_width * 2, 256);
   ctx->recv_row_bytes = align_up(std::max<size_t>((size_t)ctx->qkvdim * 4, (size_t)m.hidden * 2), 16);
   ctx->cas_stage_off = 4096;
@@ -1163,7 +1431,7 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
     CK(ring_reset_device(ctx));
     int dev_sms = 0;
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->c.device));
-    ctx->fetch_ctas = std::max(2, (ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 16) & ~1);
+    ctx->fetch_ctas = std::max(2, (ctx->c.fetch_sms > 0 ? ctx->c.fetch_sms : 24) & ~1);
     ctx->fetch_ctas = std::min(ctx->fetch_ctas, std::max(2, (dev_sms / 2) & ~1));
     ctx->compute_sms = std::max(2, (dev_sms - ctx->fetch_ctas) & ~1);
     CK(sidp::ring_preload());
@@ -1323,6 +1591,7 @@ sidp_status sidp_export_handles(sidp_ctx* ctx, void* blob, size_t* len) {
   h.has_arena = cudaIpcGetMemHandle(&h.arena_h, ctx->arena) == cudaSuccess;
   h.has_cas = cudaIpcGetMemHandle(&h.cas_h, ctx->cas) == cudaSuccess;
   cudaGetLastError();
+  device_uuid(ctx->c.device, h.uuid);
   std::memcpy(blob, &h, sizeof(h));
   *len = sizeof(h);
   return SIDP_OK;
@@ -1339,6 +1608,11 @@ sidp_status sidp_import_handles(sidp_ctx* ctx, const void* const* blobs, const s
     HandleBlob h;
     std::memcpy(&h, blobs[q], sizeof(h));
     if (h.magic != kMagic || h.rank != q) return fail(SIDP_EINVAL, "blob %d malformed", q);
+    {
+      unsigned char mine[16];
+      if (device_uuid(ctx->c.device, mine) && std::memcmp(mine, h.uuid, 16) == 0)
+        ctx->same_device_peer = true;
+    }
     if (h.pid == (int32_t)getpid()) {   // virtual ranks: same process, plain device pointers
       ctx->peer_arena[q] = reinterpret_cast<const bf16*>(h.arena_ptr);
       ctx->peer_cas[q] = reinterpret_cast<uint8_t*>(h.cas_ptr);

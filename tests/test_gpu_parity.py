@@ -575,3 +575,24 @@ def test_was_windowed_graph_with_timing(P, monkeypatch):
             rep.stream.synchronize()
             assert torch.equal(rep.toks.cpu(), toks[s // 2]), s
     rep.ctx.destroy()
+
+
+@pytest.mark.parametrize("env,case", [
+    ({"SIDP_CAS_PROLOGUE_WAIT": "1"}, "B0-layer"), ({"SIDP_CAS_PROLOGUE_WAIT": "1"}, "B1-ffn"),
+    ({"SIDP_CAS_PROLOGUE_WAIT": "1"}, "B2-layer"),
+    ({"SIDP_CAS_FUSED": "1"}, "B1-layer"), ({"SIDP_CAS_FUSED": "0"}, "B0-ffn")])
+def test_cas_variants_vs_oracle(P, env, case):
+    """The CaS ladder rungs and the flag waits folded into the consumer kernels' prologues (the
+    multi-GPU default; on one shared GPU the library gates consumers with standalone wait kernels
+    instead) re-run the oracle CaS test in a subprocess (the switches are read once per
+    process): V3 with prologue waits forced on, V2 (fused transfer launches), V1."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"tests/test_gpu_parity.py::test_cas_vs_oracle[{case}]"],
+                       cwd=root, env=dict(os.environ, SIDP_CAS_TIMEOUT_MS="20000", **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "1 passed" in r.stdout
