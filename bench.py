@@ -50,6 +50,8 @@ def parse():
                          "--fetch-sms dedicated SMs, device epoch flags) or the copy engine + CUDA "
                          "events (the paper's mechanism, A/B baseline)")
     ap.add_argument("--fetch-sms", type=int, default=24)
+    ap.add_argument("--slot-parts", type=int, default=0, choices=[0, 1, 2],
+                    help="WaS cache granularity: 1 whole layers, 2 tiles (per-component flags); 0 = 1")
     ap.add_argument("--no-stagger", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -287,7 +289,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
     ctx0 = P.Context(m, rank=0, world=W, slots=slots, order=args.order, pool=args.pool,
                      max_batch=kv.max_batch, max_ctx=max_ctx, fetch_sms=args.emulate_fetch_sms,
                      fetch_engine=args.fetch, stagger=not args.no_stagger, device=local, seed=seed,
-                     fetch_pace_gbps=args.emulate_pace_gbps)
+                     fetch_pace_gbps=args.emulate_pace_gbps, slot_parts=args.slot_parts)
     peers = []
     try:
         for r in range(1, W):
@@ -332,8 +334,9 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
         f_ms = (st["timed_ms"][3] - st0["timed_ms"][3]) / max(1, n_f)
         lb = st["layer_bytes"]
         trace = ctx0.fetch_trace() if args.fetch == "sm" else []
-        if trace:   # device log: first fetch CTA start -> publish, the timed steps' fetches
-            durs = [(e[6] - e[5]) * 1e-6 for e in trace[-n_f:]] if n_f else []
+        remote = m.num_layers - len([l for l in range(m.num_layers) if l % W == 0])
+        if trace:   # device log: first claim -> publish of each layer of the timed steps
+            durs = [(e[6] - e[5]) * 1e-6 for e in trace[-remote * args.emulate_steps:]]
             if durs:
                 f_ms = sum(durs) / len(durs)
         fetch_gbs = lb / (f_ms * 1e-3) / 1e9 if f_ms > 0 else None
@@ -346,6 +349,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "what": f"rank 0 of a {W}-rank WaS group on one B200; the {W - 1} other owners are "
                     "serve-only contexts in local HBM (bench.py was_emulation docstring)",
             "world_emulated": W, "batch": B, "ctx": ctx_len, "slots": slots,
+            "slot_parts": args.slot_parts or 1,
             "fetch_engine": args.fetch, "fetch_sms": st["fetch_sms_held"],
             "compute_sms": st["compute_sms"], "stagger_tick_ms": st["stagger_tick_ns"] * 1e-6,
             "fetch_pace_gbps": args.emulate_pace_gbps,
@@ -441,6 +445,24 @@ def cas_emulation(args, P, m, seed, local, W, ctx_len):
                         "ms_per_layer": ms / m.num_layers,
                         "group_tokens_s": sum(bt) / (ms / 1e3),
                         "tokens_s_per_live_rank": (sum(bt) / max(1, live)) / (ms / 1e3)})
+        # per-class kernel time of the one-live pattern (every rank times its kernel classes;
+        # summed over ranks: the owners' GEMMs + the live rank's attention), per layer
+        bt = patterns[-1][1]
+        for c, _, kv, _ in ranks:
+            c.set_batches(bt)
+            kv.set_pos(np.full(Bmax, ctx_len))
+        host_ms = [0.0]
+        run(1)
+        for c, _, _, _ in ranks:
+            c.set_timing(sum(1 << k for k in CLS_NAMES))
+        run(1)
+        cls_us = {}
+        for c, _, _, _ in ranks:
+            st = c.stats()
+            for k, nm in CLS_NAMES.items():
+                if st["timed_ms"][k] > 0:
+                    cls_us[nm] = cls_us.get(nm, 0.0) + st["timed_ms"][k] * 1e3 / m.num_layers
+            c.set_timing(0)
         timeouts = sum(c.stats()["timeouts"] for c, _, _, _ in ranks)
         return {"what": f"CaS (pool={args.pool}) decode of all {m.num_layers} layers by {W} "
                         f"virtual ranks on one B200, S_ctx={ctx_len} (bench.py cas_emulation "
@@ -448,6 +470,8 @@ def cas_emulation(args, P, m, seed, local, W, ctx_len):
                         "per-layer small kernels serialise on this one GPU, so the all-live "
                         "patterns over-state the W-GPU time",
                 "world_emulated": W, "ctx": ctx_len, "steps": steps, "timeouts": timeouts,
+                "cas_level": int(os.environ.get("SIDP_CAS_FUSED", "2")),
+                "one_live_kernel_us_per_layer": {k: round(v, 2) for k, v in cls_us.items()},
                 "results": out}
     finally:
         for c, _, _, _ in ranks:
@@ -602,7 +626,7 @@ def main():
     ctx = P.Context(m, rank=rank, world=world, slots=slots, order=args.order, pool=args.pool,
                     max_batch=B, max_ctx=max_ctx, fetch_sms=args.fetch_sms,
                     fetch_engine=args.fetch, stagger=not args.no_stagger, device=local,
-                    seed=seed)
+                    seed=seed, slot_parts=args.slot_parts)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         ctx.init_weights_synthetic(stream=stream)

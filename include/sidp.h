@@ -106,6 +106,19 @@ typedef struct {
                                    minus fetch_sms while an SM-fetch WaS ring is active); > 0 =
                                    explicit (e.g. a replicated baseline sized like a WaS rank,
                                    so both run bitwise-identical kernels) */
+  int32_t slot_parts;           /* WaS cache granularity ("tensor
+                                   tiles"): 1 = whole layers (a slot is filled, made ready and
+                                   released as one unit); 2 = tiles: each pooled component (W_qkv,
+                                   W_o, W_gate/up, W_down; FFN scope W_gate/up, W_down) of a slot has
+                                   its own fill / ready / release flags, so a GEMM starts once its
+                                   own weights have landed and the next layer's component refills
+                                   as soon as this layer's GEMM released it — which makes a single
+                                   slot (was_slots = 1, about one layer of memory) pipeline;
+                                   0 = 1.  Tiles need the SM fetch (SIDP_FETCH_SM) and
+                                   was_slots x parts <= 16 (else SIDP_EINVAL at sidp_alloc), and one
+                                   computing context per GPU (its fetch is one windowed launch
+                                   whose CTAs gate each part in-kernel; else SIDP_ESTATE at the
+                                   step). */
 } sidp_config;
 
 /* Caller-owned KV cache of this rank (never pooled).

@@ -281,6 +281,8 @@ struct FetchArgs {
   uint64_t timeout_ns; int* err;   // gate timeout -> *err (mapped host word)
   int chunk, stages;           // set by fetch_bulk_launch (shared-memory ring geometry)
   int claim_group;             // set by fetch_bulk_launch: chunks per atomic claim
+  int nparts;                  // tile-granular slots: parts per blob (0/1 = whole layers)
+  size_t part_off[4], part_bytes[4];   // byte range of each part within the blob
   FetchEnt ent[kFetchWindow];
 };
 size_t fetch_bulk_smem();
@@ -289,7 +291,8 @@ cudaError_t ring_free_wait_launch(FetchRing* r, int slot, unsigned long long fil
                                   uint64_t timeout_ns, int* err, cudaStream_t s);
 cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t timeout_ns, int* err,
                                    cudaStream_t s);
-cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s);
+cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s,
+                                unsigned long long* b = nullptr);
 cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s);
 cudaError_t ring_preload();
 

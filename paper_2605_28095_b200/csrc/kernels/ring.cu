@@ -109,31 +109,35 @@ SIDP_DEV void fetch_publish(const FetchArgs& a, const FetchEnt& e, int F) {
   st_release_gpu(&r->fill[e.slot], (unsigned long long)e.fill + 1);
 }
 
-// Dynamic-claim publish (the CTA whose stored-chunk count completes fill e.fill + 1).
-SIDP_DEV void fetch_publish_dyn(const FetchArgs& a, const FetchEnt& e, unsigned long long t_start) {
+// Dynamic-claim publish (the CTA whose stored-chunk count completes fill e.fill + 1 of virtual
+// slot vs); the device fetch log gets one entry per layer, when its last part lands.
+SIDP_DEV void fetch_publish_dyn(const FetchArgs& a, const FetchEnt& e, int vs, bool last_part,
+                                unsigned long long t_start) {
   FetchRing* r = a.ring;
-  r->tag[e.slot] = e.layer;
-  const unsigned long long j = r->nfetch;
-  FetchLogEnt& g = r->log[j % kFetchLogCap];
-  g.j = j;
-  g.layer = e.layer;
-  g.slot = e.slot;
-  g.owner = e.owner;
-  g.epoch = (unsigned long long)e.fill + 1;
-  g.t_start = t_start;
-  g.t_end = globaltimer_ns();
-  r->nfetch = j + 1;
+  r->tag[vs] = e.layer;
+  if (last_part) {
+    const unsigned long long j = r->nfetch;
+    FetchLogEnt& g = r->log[j % kFetchLogCap];
+    g.j = j;
+    g.layer = e.layer;
+    g.slot = e.slot;
+    g.owner = e.owner;
+    g.epoch = (unsigned long long)e.fill + 1;
+    g.t_start = t_start;
+    g.t_end = globaltimer_ns();
+    r->nfetch = j + 1;
+  }
   __threadfence();
-  st_release_gpu(&r->fill[e.slot], (unsigned long long)e.fill + 1);
+  st_release_gpu(&r->fill[vs], (unsigned long long)e.fill + 1);
 }
 
 // Windowed gate (one thread per CTA): the slot's previous fill is published and its reader has
 // released it — rel[slot] >= fill.  Waiting here holds this CTA's SM, which the compute grids
 // never count on (their SM budget excludes the fetch's).
-SIDP_DEV void fetch_gate(const FetchArgs& a, const FetchEnt& e) {
+SIDP_DEV void fetch_gate(const FetchArgs& a, int vs, unsigned int fill) {
   if (!a.ring || !a.gate) return;
-  spin_ge(&a.ring->fill[e.slot], e.fill, a.timeout_ns, a.err, 4);
-  spin_ge(&a.ring->rel[e.slot], e.fill, a.timeout_ns, a.err, 4);
+  spin_ge(&a.ring->fill[vs], fill, a.timeout_ns, a.err, 4);
+  spin_ge(&a.ring->rel[vs], fill, a.timeout_ns, a.err, 4);
 }
 
 // K1: a window of pooled layers, each owner arena -> slot, in plan order.  CTA b copies chunks
@@ -164,41 +168,55 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
     // back across whichever CTAs are fastest and no CTA's lag delays the publish; with the
     // emulated link rate, chunk v of a fill is due at t0 + v x ns, t0 = max(first claim, due
     // end of the previous fill) — one continuously busy link, as a real reader's.
+    // Tile-granular slots (a.nparts > 1): every layer's blob is filled as nparts parts (the
+    // pooled components), each with its own flags — virtual slot vs = slot x nparts + part —
+    // so part c of the next fill is gated only on the release of part c, and published (ready
+    // for its GEMM) as soon as its own bytes have landed.
     FetchRing* r = a.ring;
-    for (int k = 0; k < a.n; ++k) {
+    const int P = a.nparts > 0 ? a.nparts : 1;
+    for (int un = 0; un < a.n * P; ++un) {
+      const int k = un / P, c = un % P;
       const FetchEnt& e = a.ent[k];
-      fetch_gate(a, e);
-      const int sl = e.slot;
+      const int vs = e.slot * P + c;
+      fetch_gate(a, vs, e.fill);
+      const size_t pb = P > 1 ? a.part_bytes[c] : a.bytes;
+      const size_t po = P > 1 ? a.part_off[c] : 0;
+      const unsigned long long nch = (pb + CH - 1) / CH;
+      auto plen = [&](unsigned long long v) { return (uint32_t)std::min<size_t>(CH, pb - v * CH); };
       // claims are groups of G chunks (one atomic per G x chunk bytes: the claim's latency sits
       // in the single issuing thread's path); fill n owns group claims [n (ng + F), ...)
       const unsigned long long G = (unsigned long long)a.claim_group;
-      const unsigned long long ngroups = (nchunks + G - 1) / G;
+      const unsigned long long ngroups = (nch + G - 1) / G;
       const unsigned long long base = (unsigned long long)e.fill * (ngroups + F);
-      const uint8_t* src = e.src;
-      uint8_t* dst = a.slots + (size_t)sl * a.slot_stride;
+      const uint8_t* src = e.src + po;
+      uint8_t* dst = a.slots + (size_t)e.slot * a.slot_stride + po;
       unsigned long long t0 = 0;
       bool have_t0 = false;
       auto get_t0 = [&](unsigned long long v) {
         if (have_t0) return;
         if (v == 0) {
           unsigned long long now = globaltimer_ns();
-          if (a.ns_per_chunk && k > 0) {   // the previous fill's start (and link_t) is published
-            const FetchEnt& pe = a.ent[k - 1];
-            spin_ge(&r->t0_fill[pe.slot], (unsigned long long)pe.fill + 1, a.timeout_ns, a.err, 4);
+          if (a.ns_per_chunk && un > 0) {   // the previous fill's start (and link_t) is published
+            const FetchEnt& pe = a.ent[(un - 1) / P];
+            spin_ge(&r->t0_fill[pe.slot * P + (un - 1) % P], (unsigned long long)pe.fill + 1,
+                    a.timeout_ns, a.err, 4);
           }
           if (a.ns_per_chunk) {
             const unsigned long long lt = *reinterpret_cast<volatile unsigned long long*>(&r->link_t);
             t0 = now > lt ? now : lt;
-            r->link_t = t0 + (unsigned long long)nchunks * a.ns_per_chunk;
+            r->link_t = t0 + nch * a.ns_per_chunk;
           } else {
             t0 = now;
           }
-          r->t0[sl] = t0;
+          r->t0[vs] = t0;
+          // the layer's start for its log entry (part 0; the next fill of part 0 may begin
+          // before this fill's last part lands, so two fills of a slot keep separate stamps)
+          if (c == 0) r->t_first[(e.slot * 2 + (e.fill & 1)) % kRingMaxSlots] = t0;
           __threadfence();
-          st_release_gpu(&r->t0_fill[sl], (unsigned long long)e.fill + 1);
+          st_release_gpu(&r->t0_fill[vs], (unsigned long long)e.fill + 1);
         } else {
-          spin_ge(&r->t0_fill[sl], (unsigned long long)e.fill + 1, a.timeout_ns, a.err, 4);
-          t0 = *reinterpret_cast<volatile unsigned long long*>(&r->t0[sl]);
+          spin_ge(&r->t0_fill[vs], (unsigned long long)e.fill + 1, a.timeout_ns, a.err, 4);
+          t0 = *reinterpret_cast<volatile unsigned long long*>(&r->t0[vs]);
         }
         have_t0 = true;
       };
@@ -208,13 +226,13 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
       bool exhausted = false;
       auto issue = [&]() {   // the next claimed chunk of this fill (claiming a group if needed)
         if (gnext >= gend) {
-          const unsigned long long g = atomicAdd(&r->claim[sl], 1ull) - base;
+          const unsigned long long g = atomicAdd(&r->claim[vs], 1ull) - base;
           if (g >= ngroups) {
             exhausted = true;
             return;
           }
           gnext = g * G;
-          gend = gnext + G < nchunks ? gnext + G : nchunks;
+          gend = gnext + G < nch ? gnext + G : nch;
           get_t0(g);
         }
         const unsigned long long v = gnext++;
@@ -225,8 +243,8 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
         const uint32_t u = use + iss;
         const int st = (int)(u % NST);
         cid[u % 16] = v;
-        mbar_arrive_expect_tx(&bars[st], len_of(v));
-        bulk_load(fsm + (size_t)st * CH, src + v * CH, len_of(v), &bars[st]);
+        mbar_arrive_expect_tx(&bars[st], plen(v));
+        bulk_load(fsm + (size_t)st * CH, src + v * CH, plen(v), &bars[st]);
         ++iss;
       };
       while (!exhausted && iss < (uint32_t)(NST - 1)) issue();
@@ -235,7 +253,7 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
         const int st = (int)(u % NST);
         mbar_wait(&bars[st], (u / NST) & 1);
         const unsigned long long v = cid[u % 16];
-        bulk_store(dst + v * CH, fsm + (size_t)st * CH, len_of(v));
+        bulk_store(dst + v * CH, fsm + (size_t)st * CH, plen(v));
         bulk_commit();
         ++cmp;
         if (!exhausted) {
@@ -248,9 +266,11 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence();
       if (cmp > 0) {
-        const unsigned long long target = (unsigned long long)(e.fill + 1) * nchunks;
-        const unsigned long long prev = atomicAdd(&r->done[sl], (unsigned long long)cmp);
-        if (prev + cmp == target) fetch_publish_dyn(a, e, t0);
+        const unsigned long long target = (unsigned long long)(e.fill + 1) * nch;
+        const unsigned long long prev = atomicAdd(&r->done[vs], (unsigned long long)cmp);
+        if (prev + cmp == target)
+          fetch_publish_dyn(a, e, vs, c == P - 1,
+                            P > 1 ? r->t_first[(e.slot * 2 + (e.fill & 1)) % kRingMaxSlots] : t0);
       }
     }
     return;
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(512, 1) fetch_ldg_kernel(const __grid_constant
   }
   for (int k = 0; k < a.n; ++k) {
     const FetchEnt& e = a.ent[k];
-    if (threadIdx.x == 0) fetch_gate(a, e);
+    if (threadIdx.x == 0) fetch_gate(a, e.slot, e.fill);
     __syncthreads();
     const uint64_t t_start = globaltimer_ns();
     if (threadIdx.x == 0 && a.ring) atomicMin(&a.ring->t_first[e.slot], (unsigned long long)t_start);
@@ -364,11 +384,13 @@ __global__ void ring_ready_wait_kernel(FetchRing* r, int slot, int layer, uint64
   }
 }
 
-// Release after the last reader of the slot (stream order: everything before this kernel).
-__global__ void ring_release_kernel(unsigned long long* rel) {
+// Release after the last reader of the slot (stream order: everything before this kernel);
+// b: optionally a second counter (tile slots: gate/up and down released by one kernel).
+__global__ void ring_release_kernel(unsigned long long* rel, unsigned long long* b) {
   pdl_wait();
   __threadfence();
   red_release_gpu_add(rel, 1ull);
+  if (b) red_release_gpu_add(b, 1ull);
 }
 
 __global__ void ring_delay_kernel(uint64_t ns) {
@@ -454,8 +476,8 @@ cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t t
   return launch_pdl(ring_ready_wait_kernel, dim3(1), dim3(1), 0, s, r, slot, layer, timeout_ns, err);
 }
 
-cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s) {
-  return launch_pdl(ring_release_kernel, dim3(1), dim3(1), 0, s, rel);
+cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s, unsigned long long* b) {
+  return launch_pdl(ring_release_kernel, dim3(1), dim3(1), 0, s, rel, b);
 }
 
 cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s) {

@@ -116,6 +116,12 @@ struct sidp_ctx {
   int compute_sms = 0;
   double tick_ns = 0.0;                  // stagger tick: a measured single-reader layer fetch
   unsigned long long* release_ptr = nullptr;   // set around a remote layer's compute
+  // tile-granular slots (sidp_config.slot_parts): the pooled components of a slot are filled,
+  // made ready and released separately — virtual ring slot = slot x parts + part
+  int parts = 1;
+  size_t part_off[4]{}, part_bytes[4]{};
+  int part_of_comp[C_N]{};
+  int cur_slot = -1, cur_layer = -1;           // remote layer being enqueued (tile mode)
   std::vector<int> gslots;               // slots of the captured graph's remote layers
   cudaStream_t last_stream = nullptr;    // compute stream of the last step (mode-switch drain)
   bool graph_fresh = false;              // the graph was just captured (host state advanced)
@@ -417,6 +423,28 @@ cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, in
   return e;
 }
 
+// Tile-granular slots: before the first kernel reading component `comp` of the remote layer
+// being enqueued, wait for that part's fill (device epoch; checks the part holds the layer);
+// after its last reader, release the part so the next fill of it may start.
+cudaError_t ring_acquire(sidp_ctx* c, int comp, cudaStream_t s) {
+  if (c->parts <= 1 || c->cur_slot < 0 || !c->comp_pooled[comp]) return cudaSuccess;
+  const int vs = c->cur_slot * c->parts + c->part_of_comp[comp];
+  cudaError_t e = sidp::ring_ready_wait_launch(c->ring, vs, c->cur_layer, c->cas_timeout_ns,
+                                               c->dev_err, s);
+  count_launch(c);
+  return e;
+}
+cudaError_t ring_release(sidp_ctx* c, int comp, cudaStream_t s, int comp2 = -1) {
+  if (c->parts <= 1 || c->cur_slot < 0 || !c->comp_pooled[comp]) return cudaSuccess;
+  unsigned long long* a = &c->ring->rel[c->cur_slot * c->parts + c->part_of_comp[comp]];
+  unsigned long long* b = comp2 >= 0 && c->comp_pooled[comp2]
+                              ? &c->ring->rel[c->cur_slot * c->parts + c->part_of_comp[comp2]]
+                              : nullptr;
+  cudaError_t e = sidp::ring_release_launch(a, s, b);
+  count_launch(c);
+  return e;
+}
+
 // ---- the layer's kernels ----------------------------------------------------------
 // Attention half up to o (C-N2 steps 1-6).  When `qkv_in` is given (CaS RT1 returned it),
 // the RMSNorm + QKV GEMM are skipped.
@@ -449,6 +477,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
       count_launch(ctx);
     }
     static const bool qkv_partial = getenv("SIDP_QKV_PARTIAL") && atoi(getenv("SIDP_QKV_PARTIAL")) != 0;
+    CK(ring_acquire(ctx, C_WQKV, s));
     if (qkv_partial && sidp::gemm_partial_ok(B, ctx->qkvdim, m.hidden, ctx->gemm_ws_bytes)) {
       CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_PARTIAL,
               nullptr, 0, nullptr, 0, nullptr, s, nullptr, &part));
@@ -457,6 +486,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
               ctx->qkvdim, nullptr, 0, W.b_qkv, s));
       qkv_in = ctx->qkv;
     }
+    CK(ring_release(ctx, C_WQKV, s));
   }
   if (!qkv_in && !part.ws) {
     // RMSNorm, then the QKV GEMM whose epilogue applies bias, qk-norm and RoPE and writes q
@@ -468,8 +498,10 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
     }
     sidp::QkvEpi qe{ctx->q, kc, vc, kv->pos, ctx->rope, W.g_q, W.g_k, m.rms_eps,
                     m.n_q_heads, m.n_kv_heads, m.head_dim, ctx->c.max_ctx};
+    CK(ring_acquire(ctx, C_WQKV, s));
     CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_QKV, nullptr,
             0, nullptr, 0, W.b_qkv, s, &qe));
+    CK(ring_release(ctx, C_WQKV, s));
   } else {
     // fp32 qkv (local GEMM, or CaS: returned by the owner): qk-norm / RoPE / KV append here
     sidp::QkvPostArgs qa{};
@@ -512,14 +544,17 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
   const int h = m.hidden;
   // x2 = x + o W_o^T  (into out), u2 = RMSNorm(x2) * g_mlp
   sidp::PartialSrc part{};
+  CK(ring_acquire(ctx, C_WO, s));
   if (sidp::gemm_partial_ok(B, h, ctx->qdim, ctx->gemm_ws_bytes)) {
     CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_PARTIAL, nullptr, 0, nullptr, 0,
             nullptr, s, nullptr, &part, wait));
+    CK(ring_release(ctx, C_WO, s));
     if (!(dbg_skip() & 2)) CK(sidp::resid_norm_launch(part, x, ldx, out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
   } else {
     CK(gemm(ctx, 6, o, ldo_, W.wo, B, h, ctx->qdim, sidp::EPI_RESID, out, h, x, ldx, nullptr, s,
             nullptr, nullptr, wait));
+    CK(ring_release(ctx, C_WO, s));
     CK(sidp::rmsnorm_launch(out, h, W.g_mlp, m.rms_eps, ctx->u, h, B, h, s));
     count_launch(ctx);
   }
@@ -529,11 +564,14 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
     sidp::MlpArgs ma{};
     ma.u = ctx->u; ma.ldu = h; ma.wgu = W.wgu; ma.wd = W.wd; ma.act = ctx->act;
     ma.ldact = m.intermediate; ma.M = B; ma.h = h; ma.I = m.intermediate; ma.partial_out = &part;
+    CK(ring_acquire(ctx, C_WGU, s));
+    CK(ring_acquire(ctx, C_WD, s));
     timing_begin(ctx, 1, s);
     cudaError_t e = sidp::mlp_launch(ma, gws(ctx), s);
     timing_end(ctx, 1, s);
     CK(e);
     count_launch(ctx);
+    CK(ring_release(ctx, C_WGU, s, C_WD));
     // the fix-up is the fused launch's successor: it releases the WaS slot (if any) once the
     // fused launch — the last reader of the layer's weights — has completed
     CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s,
@@ -543,11 +581,15 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
     ctx->u_for = next_layer;
     return SIDP_OK;
   }
+  CK(ring_acquire(ctx, C_WGU, s));
   CK(gemm(ctx, 1, ctx->u, h, W.wgu, B, 2 * m.intermediate, h, sidp::EPI_SILU_MUL, ctx->act,
           m.intermediate, nullptr, 0, nullptr, s));
+  CK(ring_release(ctx, C_WGU, s));
+  CK(ring_acquire(ctx, C_WD, s));
   if (next_g && sidp::gemm_partial_ok(B, h, m.intermediate, ctx->gemm_ws_bytes)) {
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_PARTIAL,
             nullptr, 0, nullptr, 0, nullptr, s, nullptr, &part));
+    CK(ring_release(ctx, C_WD, s));
     if (!(dbg_skip() & 2)) {
       CK(sidp::resid_norm_launch(part, out, h, out, h, next_g, m.rms_eps, ctx->u, h, B, h, s,
                                  ctx->release_ptr));   // successor of the down GEMM
@@ -558,6 +600,7 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
   } else {
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_RESID, out, h,
             out, h, nullptr, s));
+    CK(ring_release(ctx, C_WD, s));
   }
   return SIDP_OK;
 }
@@ -633,6 +676,15 @@ sidp_status enqueue_fetches(sidp_ctx* ctx, int64_t upto) {
   // emulated link rate: chunk c (kFetchChunk bytes) no earlier than c x chunk / rate
   fa.ns_per_chunk = ctx->c.fetch_pace_gbps > 0.0f
                         ? (uint64_t)((double)sidp::kFetchChunk / ctx->c.fetch_pace_gbps) : 0;
+  if (ctx->parts > 1) {
+    if (!windowed)
+      return fail(SIDP_ESTATE, "tile slots need one computing context on the GPU (windowed fetch)");
+    fa.nparts = ctx->parts;
+    for (int i = 0; i < ctx->parts; ++i) {
+      fa.part_off[i] = ctx->part_off[i];
+      fa.part_bytes[i] = ctx->part_bytes[i];
+    }
+  }
   auto launch_window = [&]() -> sidp_status {
     if (fa.n == 0) return SIDP_OK;
     if (tm) timing_begin(ctx, 3, ctx->fetch_stream);
@@ -756,7 +808,14 @@ sidp_status was_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* k
     if (p >= ctx->fetch_j) return fail(SIDP_ESTATE, "slot ring deadlock (plan lag >= slots)");
     const int slot = slot_for_fetch(ctx, p);
     const bf16* pooled = ctx->slots + (size_t)slot * ctx->pooled_elems;
-    if (ctx->ring_mode) {
+    if (ctx->ring_mode && ctx->parts > 1) {
+      // tile-granular slot: every GEMM waits for its own component's part and releases it
+      ctx->cur_slot = slot;
+      ctx->cur_layer = layer;
+      st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
+      ctx->cur_slot = ctx->cur_layer = -1;
+      if (st != SIDP_OK) return st;
+    } else if (ctx->ring_mode) {
       // device flags: wait for this consumption's fill epoch (and check the slot's layer tag);
       // the release rides on the kernel after the layer's last weight reader
       CK(sidp::ring_ready_wait_launch(ctx->ring, slot, layer, ctx->cas_timeout_ns, ctx->dev_err, s));
@@ -1043,6 +1102,18 @@ sidp_status cas_return(sidp_ctx* ctx, const CasTrip& t, const uint8_t* result, s
   return SIDP_OK;
 }
 
+// requester: the owner's returned rows -> x once done >= value (one launch with prologue waits)
+sidp_status cas_copy_back(sidp_ctx* ctx, const uint64_t* done, uint64_t value, bf16* x,
+                          const uint8_t* recv, int B, cudaStream_t s) {
+  const int h = ctx->m.hidden;
+  sidp::FlagWait w = single_wait(ctx, done, value);
+  sidp_status st = consumer_wait(ctx, w, s);
+  if (st != SIDP_OK) return st;
+  CK(sidp::wait_copy_launch(w, x, h * 2, recv, h * 2, B, h * 2, s));
+  count_launch(ctx);
+  return SIDP_OK;
+}
+
 sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* kv,
                          cudaStream_t s) {
   const auto& m = ctx->m;
@@ -1108,9 +1179,8 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
     ctx->last_rt_any[o] = t2.rt;
     ctx->st.cas_round_trips += 2;
     if (B > 0) {
-      CK(sidp::wait_copy_launch(single_wait(ctx, done, (uint64_t)t2.rt + 1), x, h * 2, recv, h * 2,
-                                B, h * 2, s));
-      count_launch(ctx);
+      st = cas_copy_back(ctx, done, (uint64_t)t2.rt + 1, x, recv, B, s);
+      if (st != SIDP_OK) return st;
     }
     return SIDP_OK;
   }
@@ -1146,9 +1216,8 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
   ctx->last_rt_any[o] = t.rt;
   ctx->st.cas_round_trips++;
   if (B > 0) {
-    CK(sidp::wait_copy_launch(single_wait(ctx, done, (uint64_t)t.rt + 1), x, h * 2, recv, h * 2, B,
-                              h * 2, s));
-    count_launch(ctx);
+    st = cas_copy_back(ctx, done, (uint64_t)t.rt + 1, x, recv, B, s);
+    if (st != SIDP_OK) return st;
   }
   return SIDP_OK;
 }
@@ -1435,6 +1504,21 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
     ctx->fetch_ctas = std::min(ctx->fetch_ctas, std::max(2, (dev_sms / 2) & ~1));
     ctx->compute_sms = std::max(2, (dev_sms - ctx->fetch_ctas) & ~1);
     CK(sidp::ring_preload());
+    if (ctx->c.slot_parts == 2) {   // one part per pooled component, in blob order
+      int n = 0;
+      for (int i = 0; i < C_N; ++i) {
+        if (!ctx->comp_pooled[i] || ctx->comp_elems[i] == 0) continue;
+        ctx->part_of_comp[i] = n;
+        ctx->part_off[n] = ctx->comp_off[i] * 2;
+        ctx->part_bytes[n] = ctx->comp_elems[i] * 2;
+        ++n;
+      }
+      if (n > 4 || ctx->S * n > sidp::kRingMaxSlots)
+        return fail(SIDP_EINVAL, "tile slots: was_slots %d x %d parts > %d", ctx->S, n, sidp::kRingMaxSlots);
+      ctx->parts = n;
+    }
+  } else if (ctx->c.slot_parts == 2 && ctx->R > 0) {
+    return fail(SIDP_EINVAL, "tile slots (slot_parts = 2) need the SM fetch (SIDP_FETCH_SM)");
   }
   if (ctx->c.compute_sms > 0) ctx->compute_sms = std::max(2, ctx->c.compute_sms & ~1);
   ctx->ready_ev.resize(ctx->S);
@@ -1702,9 +1786,12 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
         if (st != SIDP_OK) return st;
         const int slot = slot_for_fetch(ctx, p);
         if (ctx->ring_mode) {
-          CK(sidp::ring_ready_wait_launch(ctx->ring, slot, layer, ctx->cas_timeout_ns, ctx->dev_err, s));
-          CK(sidp::ring_release_launch(&ctx->ring->rel[slot], s));
-          count_launch(ctx, 2);
+          for (int pt = 0; pt < ctx->parts; ++pt) {
+            const int vs = slot * ctx->parts + pt;
+            CK(sidp::ring_ready_wait_launch(ctx->ring, vs, layer, ctx->cas_timeout_ns, ctx->dev_err, s));
+            CK(sidp::ring_release_launch(&ctx->ring->rel[vs], s));
+            count_launch(ctx, 2);
+          }
         } else {
           CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
           CK(cudaEventRecord(ctx->free_ev[slot], s));

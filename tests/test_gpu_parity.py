@@ -596,3 +596,88 @@ def test_cas_variants_vs_oracle(P, env, case):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "1 passed" in r.stdout
+
+
+@pytest.mark.parametrize("name,d,slots,pool", [("tiny", 4, 1, "layer"), ("tiny", 4, 2, "layer"),
+                                               ("tiny-qwen3", 2, 1, "ffn"), ("tiny-qwen25", 8, 1, "layer")])
+def test_was_tile_slots(P, name, d, slots, pool):
+    """Tile-granular slots (sidp_config.slot_parts = 2): every pooled component
+    of a slot is filled, made ready and released on its own flags, so one slot pipelines.  One
+    computing rank beside d-1 serve-only owners; CUDA-graph steps and an eager step with logits
+    are BITWISE equal to the replicated run; the device fetch log (one entry per layer, when its
+    last part landed) equals the oracle FIFO schedule; every consumption is per part and found
+    the layer it expected in that part."""
+    m = MODELS[name].with_layers(8)
+    B = 5
+    G = Rank(P, m, rank=0, world=d, B=B, slots=slots, pool=pool, slot_parts=2)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=80, seed=SEED, alloc=False, pool=pool)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    G.ctx.import_handles([G.ctx.export_handles()] + [c.export_handles() for c in peers])
+    steps = 4
+    toks = []
+    for s in range(steps):       # graph replays (no logits requested)
+        with torch.cuda.stream(G.stream):
+            G.ctx.step(G.toks, G.toks, G.kv, batch=B, stream=G.stream, advance_pos=True)
+        G.stream.synchronize()
+        toks.append(G.toks.clone().cpu())
+    G.step(); G.finish_step()    # eager, logits
+    st = G.ctx.stats()
+    assert st["timeouts"] == 0
+    pl = OS.plan(OS.owner_map(m.num_layers, d), d, 0, "exec")
+    log = G.ctx.fetch_log()
+    assert len(log) >= (steps + 1) * len(pl)
+    assert log == OS.slot_schedule(pl, slots, steps + 3)[:len(log)]
+    parts = 4 if pool == "layer" else 2
+    cons = G.ctx.consume_log()
+    assert len(cons) == (steps + 1) * len(pl) * parts
+    assert all(c[0] == c[2] for c in cons)
+    budget = st["compute_sms"]
+    for c in peers:
+        c.destroy()
+    G.ctx.destroy()
+    rep = Rank(P, m, B=B, pool=pool, compute_sms=budget)
+    for s in range(steps):
+        with torch.cuda.stream(rep.stream):
+            rep.ctx.step(rep.toks, rep.toks, rep.kv, batch=B, stream=rep.stream, advance_pos=True)
+        rep.stream.synchronize()
+        assert torch.equal(rep.toks.cpu(), toks[s]), s
+    rep.step(); rep.finish_step()
+    assert torch.equal(rep.history[0][1], G.history[0][1])
+    rep.ctx.destroy()
+
+
+def test_was_tile_slots_full_width_one_slot(P):
+    """One tile-granular slot at the bench's full Qwen3-32B width (B = 256, S_ctx = 1024, 12
+    layers; d = 8 with serve-only owners): about one layer of cache memory, logits bitwise equal
+    to the replicated run, fetch log == oracle schedule."""
+    m = MODELS["qwen3-32b"].with_layers(12)
+    B, ctx, d, steps = 256, 1024, 8, 2
+    R = Rank(P, m, rank=0, world=d, B=B, ctx=ctx, span=0, max_ctx=ctx + 8, slots=1, slot_parts=2)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=ctx + 8, seed=SEED, alloc=False)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    R.ctx.import_handles([R.ctx.export_handles()] + [c.export_handles() for c in peers])
+    for s in range(steps):
+        R.step(); R.finish_step()
+    st = R.ctx.stats()
+    assert st["timeouts"] == 0 and st["slot_bytes"] == st["layer_bytes"]
+    pl = OS.plan(OS.owner_map(m.num_layers, d), d, 0, "exec")
+    log = R.ctx.fetch_log()
+    assert log == OS.slot_schedule(pl, 1, steps + 1)[:len(log)] and len(log) >= steps * len(pl)
+    for c in peers:
+        c.destroy()
+    rep = Rank(P, m, B=B, ctx=ctx, span=0, max_ctx=ctx + 8, compute_sms=st["compute_sms"])
+    for s in range(steps):
+        rep.step(); rep.finish_step()
+        assert torch.equal(rep.history[s][1], R.history[s][1]), s
+    rep.ctx.destroy()
+    R.ctx.destroy()
