@@ -332,9 +332,11 @@ sidp_status sidp_test_gen(void* dst, int64_t ld, int64_t rows, int64_t cols, uin
                           int64_t row0, int64_t lcols, int32_t row_map, void* stream);
 
 /* K1 fetch of `bytes` (multiple of 16, 16-byte aligned pointers) from src (local or peer VA) to
- * dst: engine 0 = the TMA bulk-copy kernel on `ctas` CTAs (rounded to CTA pairs; the WaS
- * default), 1 = the copy engine (cudaMemcpyAsync), 2 = the vectorised LDG/STG copy kernel
- * (round-1 design, kept for A/B).  Device pointers; enqueued on stream; no flags posted. */
+ * dst: engine 0 = the TMA bulk-copy kernel on `ctas` CTAs (rounded to CTA pairs) with a static
+ * chunk split, 1 = the copy engine (cudaMemcpyAsync), 2 = the vectorised LDG/STG copy kernel
+ * (round-1 design, kept for A/B), 3 = the same kernel exactly as the WaS ring runs it (chunks
+ * claimed in groups, completion published to a scratch ring; no gates) — for ncu.  Device
+ * pointers; enqueued on stream; no flag of any context is posted. */
 sidp_status sidp_test_fetch(void* dst, const void* src, size_t bytes, int32_t ctas, int32_t engine,
                             void* stream);
 

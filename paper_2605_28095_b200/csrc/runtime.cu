@@ -2344,7 +2344,24 @@ sidp_status sidp_test_fetch(void* dst, const void* src, size_t bytes, int32_t ct
     e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
   } else if (engine == 2) {   // the vectorised LDG/STG copy kernel (round-1 K1, kept for A/B)
     e = sidp::fetch_launch(dst, src, bytes, ctas, s);
-  } else {                    // K1: TMA bulk copies through shared memory, CTA pairs
+  } else if (engine == 3) {   // K1 exactly as the WaS ring runs it (claimed chunks, publish),
+                              // on a scratch ring zeroed per call, no gates (profiling hook)
+    static sidp::FetchRing* scratch = nullptr;
+    if (!scratch && cudaMalloc(&scratch, sizeof(sidp::FetchRing)) != cudaSuccess)
+      return fail(SIDP_ENOMEM, "fetch scratch ring");
+    e = cudaMemsetAsync(scratch, 0, offsetof(sidp::FetchRing, log), s);
+    if (e == cudaSuccess) {
+      sidp::FetchArgs a{};
+      a.slots = reinterpret_cast<uint8_t*>(dst);
+      a.slot_stride = 0;
+      a.bytes = bytes;
+      a.ring = scratch;
+      a.n = 1;
+      a.timeout_ns = 1000000000ull;
+      a.ent[0] = sidp::FetchEnt{reinterpret_cast<const uint8_t*>(src), 0, 0, 0, 0};
+      e = sidp::fetch_bulk_launch(a, ctas, s);
+    }
+  } else {                    // K1's plain copy form: TMA bulk copies through shared memory
     sidp::FetchArgs a{};
     a.slots = reinterpret_cast<uint8_t*>(dst);
     a.slot_stride = 0;

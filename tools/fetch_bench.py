@@ -1,6 +1,7 @@
 """K1 fetch-kernel bandwidth on one GPU (local HBM -> HBM copy of one pooled layer) for several
 CTA counts, beside the copy engine (cudaMemcpyAsync).  NVLink peer bandwidth cannot be measured
-on the 1-GPU pool; this bounds the kernel's own issue capability.  Prints one JSON line."""
+on the 1-GPU pool; this bounds the kernel's own issue capability.  engine 3 = the kernel exactly as
+the WaS ring runs it (claimed chunk groups, completion published).  Prints one JSON line."""
 import ctypes as C, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -12,8 +13,10 @@ dst = torch.empty_like(src)
 res = {"bytes": nbytes}
 L = P._abi.lib()
 L.sidp_test_fetch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p]
-for ctas in [8, 16, 32, 64, 148, 296, 0]:
-    engine = 1 if ctas == 0 else 0
+runs = [(c, 0) for c in [8, 16, 32, 64]] + [(c, 3) for c in [16, 24, 32, 48]] + [(0, 1)]
+if os.environ.get("ONLY_RING"):
+    runs = [(int(os.environ.get("ONLY_RING")), 3)]
+for ctas, engine in runs:
     for _ in range(2):
         P._abi.check(L.sidp_test_fetch(dst.data_ptr(), src.data_ptr(), nbytes, ctas, engine, None), "fetch")
     torch.cuda.synchronize()
@@ -23,7 +26,7 @@ for ctas in [8, 16, 32, 64, 148, 296, 0]:
         P._abi.check(L.sidp_test_fetch(dst.data_ptr(), src.data_ptr(), nbytes, ctas, engine, None), "fetch")
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    key = "copy_engine" if engine else f"sm_fetch_{ctas}ctas"
+    key = "copy_engine" if engine == 1 else (f"ring_fetch_{ctas}ctas" if engine == 3 else f"sm_fetch_{ctas}ctas")
     res[key] = {"ms": ms, "GBps_read": nbytes / ms / 1e6}
 assert torch.equal(dst, src)
 print(json.dumps(res))
