@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _run_rank(rank, world, port, mode, pool, batches, steps, q):
+def _run_rank(rank, world, port, mode, pool, batches, steps, q, per_device=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -38,13 +38,14 @@ def _run_rank(rank, world, port, mode, pool, batches, steps, q):
         import paper_2605_28095_b200 as P
         from paper_2605_28095_b200.orchestrator import exchange_handles
         from sidp_inputs import MODELS, gen
-        torch.cuda.set_device(0)
+        dev = rank % torch.cuda.device_count() if per_device else 0
+        torch.cuda.set_device(dev)
         m = MODELS["tiny"].with_layers(8)
         B = batches[rank]
         mb, max_ctx = max(batches), 80
         b0 = sum(batches[:rank])
         ctx = P.Context(m, rank=rank, world=world, max_batch=mb, max_ctx=max_ctx, seed=SEED,
-                        pool=pool, slots=2)
+                        pool=pool, slots=2, device=dev)
         ctx.init_weights_synthetic()
         kv = P.KVCache(m, mb, max_ctx)
         kv.fill_synthetic(SEED, b0, mb, max_ctx)
@@ -112,12 +113,13 @@ def _replicated(batches, r, steps, pool, compute_sms=0):
     return out
 
 
-def _launch(mode, pool, batches, steps):
+def _launch(mode, pool, batches, steps, per_device=False):
     world = len(batches)
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_run_rank, args=(r, world, port, mode, pool, batches, steps, q))
+    procs = [ctx.Process(target=_run_rank, args=(r, world, port, mode, pool, batches, steps, q,
+                                                 per_device))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -169,3 +171,48 @@ def test_cas_two_processes_ipc(pool, batches):
         pos = {r: res[r][0][s][2][3] for r in live}
         logits = {r: res[r][0][s][1].astype(np.float64) for r in live}
         cas_oracle_check(m, om, 2, pool, dumps, logits, caches, pos, 1e-2)
+
+
+# ---- one process per GPU (the production layout): skipped on a 1-GPU box.  WaS fetches cross
+# real peer mappings (cudaIpcOpenMemHandle + lazy peer access, NVLink on HGX); CaS consumers
+# use the prologue flag waits (peers on other GPUs).
+two_gpus = pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                              reason="needs 2 GPUs")
+
+
+@two_gpus
+@pytest.mark.parametrize("pool", ["layer", "ffn"])
+def test_was_two_gpus(pool):
+    from oracle import schedule as OS
+    batches = [3, 5]
+    res = _launch("was", pool, batches, 3, per_device=True)
+    own = OS.owner_map(8, 2)
+    for r in range(2):
+        out, timeouts, log, budget = res[r]
+        assert timeouts == 0
+        ref = _replicated(batches, r, 3, pool, budget)
+        for s in range(3):
+            assert np.array_equal(out[s][1], ref[s][1]), (r, s)
+        full = OS.slot_schedule(OS.plan_exec(own, r), 2, 4)
+        assert [tuple(x) for x in log] == full[:len(log)]
+
+
+@two_gpus
+@pytest.mark.parametrize("pool", ["layer", "ffn"])
+@pytest.mark.parametrize("batches", [[3, 5], [0, 4]])
+def test_cas_two_gpus(pool, batches):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from sidp_inputs import MODELS
+    from .helpers import OracleModel, cas_oracle_check
+    res = _launch("cas", pool, batches, 2, per_device=True)
+    m = MODELS["tiny"].with_layers(8)
+    om = OracleModel(m, SEED)
+    live = [r for r in range(2) if batches[r]]
+    for r in range(2):
+        assert res[r][1] == 0
+    for s in range(2):
+        cas_oracle_check(m, om, 2, pool, {r: res[r][0][s][2][0] for r in live},
+                         {r: res[r][0][s][1].astype(np.float64) for r in live},
+                         {r: (res[r][0][s][2][1], res[r][0][s][2][2]) for r in live},
+                         {r: res[r][0][s][2][3] for r in live}, 1e-2)
