@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--emulate-batch", type=int, default=None)
     ap.add_argument("--emulate-ctx", type=int, default=None)
     ap.add_argument("--emulate-steps", type=int, default=4)
+    ap.add_argument("--alias-owners", action="store_true",
+                    help="timing only: the d-1 serve-only owners share ONE arena "
+                         "(sidp_alloc_serve_only_alias), so the KV cache of big points fits")
     ap.add_argument("--emulate-only", action="store_true",
                     help="skip the d=1 run (shapes whose weights do not fit one GPU, e.g. M3 "
                          "Llama-3.1-70B) and print only the WaS emulation line")
@@ -295,7 +298,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
         for r in range(1, W):
             c = P.Context(m, rank=r, world=W, slots=slots, pool=args.pool, max_batch=kv.max_batch,
                           max_ctx=max_ctx, device=local, seed=seed, alloc=False)
-            c.alloc_serve_only()
+            c.alloc_serve_only(alias_of=peers[0] if (args.alias_owners and peers) else None)
             peers.append(c)
         with torch.cuda.stream(stream):
             ctx0.init_weights_synthetic(stream=stream)
@@ -353,6 +356,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "fetch_engine": args.fetch, "fetch_sms": st["fetch_sms_held"],
             "compute_sms": st["compute_sms"], "stagger_tick_ms": st["stagger_tick_ns"] * 1e-6,
             "fetch_pace_gbps": args.emulate_pace_gbps,
+            "owners_aliased": bool(args.alias_owners),
             "steps": args.emulate_steps,
             "ms_per_step": ms, "tokens_s_rank": B / (ms / 1e3),
             "group_tokens_s_est": W * B / (ms / 1e3),
@@ -369,7 +373,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
         }
     finally:
         ctx0.destroy()
-        for c in peers:
+        for c in reversed(peers):   # aliases before their donor
             c.destroy()
 
 

@@ -193,6 +193,16 @@ sidp_status sidp_alloc(sidp_ctx* ctx);
  * on allocation failure (nothing left allocated is leaked: sidp_destroy frees it). */
 sidp_status sidp_alloc_serve_only(sidp_ctx* ctx);
 
+/* TIMING EMULATION ONLY.  A serve-only context whose owned arena IS `donor`'s (same device, same
+ * pooled layout, donor owns at least as many layers): d-1 emulated owners of a big model then
+ * cost one arena of HBM, which frees the memory for the KV cache of the configured point (M3:
+ * Llama-3.1-70B at B_e ~ 1536 with max KV).  The fetched bytes, their sizes and the schedule are
+ * a real rank's, but a slot then holds the donor's layer values, so the results are NOT the
+ * model's: never used by a parity test.  sidp_init_weights_synthetic is a no-op on it; destroy
+ * leaves the donor's arena alone (destroy the donor last).  SIDP_EINVAL: null donor or a
+ * mismatching layout. */
+sidp_status sidp_alloc_serve_only_alias(sidp_ctx* ctx, const sidp_ctx* donor);
+
 /* K12: fill owned layers, local layer parts and replicated tensors with the counter-hash
  * synthetic values (same function as sidp_inputs/gen.py), on `stream`. */
 sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream);

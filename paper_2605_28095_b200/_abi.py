@@ -67,6 +67,7 @@ SIGNATURES = {
     "sidp_init": [C.POINTER(ModelDesc), C.POINTER(Config), C.POINTER(_P)],
     "sidp_alloc": [_P],
     "sidp_alloc_serve_only": [_P],
+    "sidp_alloc_serve_only_alias": [_P, _P],
     "sidp_init_weights_synthetic": [_P, _P],
     "sidp_export_handles": [_P, _P, C.POINTER(C.c_size_t)],
     "sidp_import_handles": [_P, C.POINTER(_P), C.POINTER(C.c_size_t)],

@@ -94,9 +94,14 @@ class Context:
     def alloc(self):
         A.check(A.lib().sidp_alloc(self.h), "sidp_alloc")
 
-    def alloc_serve_only(self):
-        """Owner-only rank: allocates and exports its arena, never computes (sidp.h)."""
-        A.check(A.lib().sidp_alloc_serve_only(self.h), "sidp_alloc_serve_only")
+    def alloc_serve_only(self, alias_of=None):
+        """Owner-only rank: allocates and exports its arena, never computes (sidp.h).  alias_of
+        (timing emulation only): share that serve-only context's arena instead of allocating."""
+        if alias_of is None:
+            A.check(A.lib().sidp_alloc_serve_only(self.h), "sidp_alloc_serve_only")
+        else:
+            A.check(A.lib().sidp_alloc_serve_only_alias(self.h, alias_of.h),
+                    "sidp_alloc_serve_only_alias")
 
     def init_weights_synthetic(self, stream=None):
         A.check(A.lib().sidp_init_weights_synthetic(self.h, _stream_ptr(stream)),

@@ -145,6 +145,7 @@ struct sidp_ctx {
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
   std::vector<int64_t> last_rt_any;             // [owner] last round trip with that owner (V3)
   bool same_device_peer = false;                // a peer shares this GPU (virtual ranks / 1-GPU IPC)
+  bool arena_borrowed = false;                  // serve-only alias: the arena is another ctx's
   // WaS schedule state
   int64_t fetch_j = 0, compute_k = 0;
   std::vector<int> slot_of_fetch;        // FIFO recurrence, extended lazily (slot_for_fetch)
@@ -1391,6 +1392,7 @@ void sidp_destroy(sidp_ctx* ctx) {
       cudaEventDestroy(p.b);
     }
     if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
+    if (ctx->arena_borrowed) ctx->arena = nullptr;
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
@@ -1556,9 +1558,22 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   return SIDP_OK;
 }
 
-sidp_status sidp_alloc_serve_only(sidp_ctx* ctx) {
+static sidp_status serve_only_impl(sidp_ctx* ctx, const sidp_ctx* donor);
+
+sidp_status sidp_alloc_serve_only(sidp_ctx* ctx) { return serve_only_impl(ctx, nullptr); }
+
+sidp_status sidp_alloc_serve_only_alias(sidp_ctx* ctx, const sidp_ctx* donor) {
+  if (!donor) return fail(SIDP_EINVAL, "null donor");
+  return serve_only_impl(ctx, donor);
+}
+
+static sidp_status serve_only_impl(sidp_ctx* ctx, const sidp_ctx* donor) {
   if (!ctx) return fail(SIDP_EINVAL, "null ctx");
   if (ctx->allocated) return fail(SIDP_ESTATE, "already allocated");
+  if (donor && (!donor->allocated || !donor->arena || donor->c.device != ctx->c.device ||
+                donor->pooled_elems != ctx->pooled_elems ||
+                donor->owned_layers.size() < ctx->owned_layers.size()))
+    return fail(SIDP_EINVAL, "alias donor: same device and layout, at least as many owned layers");
   CK(cudaSetDevice(ctx->c.device));
   const size_t pooled_b = ctx->pooled_elems * 2, local_b = ctx->local_elems * 2;
   auto dm = [&](void** p, size_t bytes) -> bool {
@@ -1568,8 +1583,13 @@ sidp_status sidp_alloc_serve_only(sidp_ctx* ctx) {
     return false;
   };
   // the owned pooled blobs only: the local (replicated) per-layer parts are never read by peers
-  if (!dm(reinterpret_cast<void**>(&ctx->arena), std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b))
+  if (donor) {   // timing emulation: the donor's arena stands in for this rank's
+    ctx->arena = donor->arena;
+    ctx->arena_borrowed = true;
+  } else if (!dm(reinterpret_cast<void**>(&ctx->arena),
+                 std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b)) {
     return SIDP_ENOMEM;
+  }
   // a flag block only, so the exported blob is well-formed (a serve-only rank serves no CaS)
   ctx->cas_bytes = 4096;
   ctx->cas_stage_off = ctx->cas_recv_off = 4096;
@@ -1583,13 +1603,14 @@ sidp_status sidp_alloc_serve_only(sidp_ctx* ctx) {
   ctx->allocated = true;
   ctx->st.layer_bytes = pooled_b;
   ctx->st.local_layer_bytes = local_b;
-  ctx->st.owned_bytes = ctx->owned_layers.size() * pooled_b;
+  ctx->st.owned_bytes = donor ? 0 : ctx->owned_layers.size() * pooled_b;
   return SIDP_OK;
 }
 
 sidp_status sidp_init_weights_synthetic(sidp_ctx* ctx, void* stream) {
   sidp_status st = check_ready(ctx);
   if (st != SIDP_OK) return st;
+  if (ctx->arena_borrowed) return SIDP_OK;   // the donor initialised (and owns) the arena
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const auto& m = ctx->m;
   const uint64_t seed = ctx->c.seed;
