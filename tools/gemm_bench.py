@@ -14,6 +14,10 @@ splits_list = [int(s) for s in sys.argv[3].split(",")] if len(sys.argv) > 3 else
 tag = os.environ.get("TAG", "")
 
 
+SERIAL = os.environ.get("SERIAL", "0") != "0"   # an event between launches: no PDL overlap
+gap = torch.cuda.Event()
+
+
 def timeit(fn, copies, reps=20):
     for i in range(2):
         fn(i % copies)
@@ -21,6 +25,8 @@ def timeit(fn, copies, reps=20):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(reps):
+        if SERIAL:
+            gap.record()
         fn(i % copies)
     e1.record()
     torch.cuda.synchronize()
