@@ -318,10 +318,7 @@ struct XferSet {
   unsigned int* counter;
 };
 cudaError_t xfer_launch(const XferSet& x, cudaStream_t s);
-// L2 prefetch of [p, p + bytes) (cp.async.bulk.prefetch.L2, no completion): a CaS owner warms
-// the weights of its coming small-M GEMMs (QKV, O) in L2 while it waits for the arrivals, so the
-// weight stream of the latency-bound GEMM comes from L2 instead of HBM.
-cudaError_t l2_prefetch_launch(const void* p, size_t bytes, cudaStream_t s);
+
 // Wait for the flags, then copy rows (CaS requester: the owner's returned slice -> x).
 cudaError_t wait_copy_launch(const FlagWait& w, void* dst, int ldd, const void* src, int lds,
                              int rows, int row_bytes, cudaStream_t s);

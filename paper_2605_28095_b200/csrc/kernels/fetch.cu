@@ -116,28 +116,7 @@ __global__ void wait_copy_kernel(const FlagWait w, uint8_t* dst, int ldd, const 
   }
 }
 
-// one 64 KB bulk L2 prefetch per thread-iteration, grid-strided
-__global__ void l2_prefetch_kernel(const uint8_t* p, size_t bytes) {
-  constexpr size_t kBlk = 64 * 1024;
-  const size_t nblk = (bytes + kBlk - 1) / kBlk;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nblk;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t off = i * kBlk;
-    const uint32_t len = (uint32_t)(bytes - off < kBlk ? bytes - off : kBlk);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p + off)),
-                 "r"(len & ~15u)
-                 : "memory");
-  }
-}
-
 }  // namespace
-
-cudaError_t l2_prefetch_launch(const void* p, size_t bytes, cudaStream_t s) {
-  if (!p || bytes < 16) return cudaSuccess;
-  if (reinterpret_cast<uintptr_t>(p) & 15) return cudaErrorInvalidValue;
-  l2_prefetch_kernel<<<16, 128, 0, s>>>(reinterpret_cast<const uint8_t*>(p), bytes);
-  return cudaGetLastError();
-}
 
 cudaError_t wait_copy_launch(const FlagWait& w, void* dst, int ldd, const void* src, int lds,
                              int rows, int row_bytes, cudaStream_t s) {
@@ -258,7 +237,6 @@ cudaError_t fetch_preload() {
   if (cudaFuncGetAttributes(&fa, copy_rows_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, xfer_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, wait_copy_kernel) != cudaSuccess) e = cudaGetLastError();
-  if (cudaFuncGetAttributes(&fa, l2_prefetch_kernel) != cudaSuccess) e = cudaGetLastError();
   return e;
 }
 

@@ -865,11 +865,6 @@ int cas_level() {
   return v;
 }
 bool cas_fused() { return cas_level() >= 1; }
-// CaS owner L2 warm-up of the latency-bound small-M GEMMs' weights (SIDP_CAS_L2_PREFETCH=0 off)
-bool cas_l2_prefetch() {
-  static const bool v = !(getenv("SIDP_CAS_L2_PREFETCH") && atoi(getenv("SIDP_CAS_L2_PREFETCH")) == 0);
-  return v;
-}
 
 // Prologue waits spin inside the consumer grid's CTAs.  On one GPU shared with the peers
 // (virtual ranks, the 1-GPU IPC test) spinning CTAs could hold the SMs a peer needs to make the
@@ -1154,8 +1149,6 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       st = cas_return(ctx, t1, reinterpret_cast<const uint8_t*>(ctx->qkv), (size_t)ctx->qkvdim * 4,
                       (size_t)ctx->qkvdim * 4, s);
       if (st != SIDP_OK) return st;
-      // W_o into L2 while the requesters run attention (round trip 2's arrivals come after it)
-      if (cas_l2_prefetch()) CK(sidp::l2_prefetch_launch(W.wo, ctx->comp_elems[C_WO] * 2, s));
     }
     CasTrip t2 = cas_trip(ctx, layer);
     if (B > 0) {   // RoPE, KV append and attention stay local (the KV cache is local)
@@ -1183,12 +1176,6 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       st = cas_return(ctx, t2, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
                       (size_t)h * 2, s);
       if (st != SIDP_OK) return st;
-      // W_qkv of this owner's next layer into L2 (its GPU serves nothing until then)
-      const int nl = (layer + ctx->d) % ctx->L;   // wraps to the next step's first owned layer
-      if (cas_l2_prefetch() && ctx->owner[nl] == me) {
-        const bf16* np = ctx->arena + (size_t)ctx->owned_index[nl] * ctx->pooled_elems;
-        CK(sidp::l2_prefetch_launch(np + ctx->comp_off[C_WQKV], ctx->comp_elems[C_WQKV] * 2, s));
-      }
     }
     ctx->last_rt_any[o] = t2.rt;
     ctx->st.cas_round_trips += 2;
