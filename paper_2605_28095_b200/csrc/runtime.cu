@@ -1332,6 +1332,15 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
     return fail(SIDP_EINVAL, "bad pool_scope");
   if (cfg->max_batch < 1 || cfg->max_ctx < 1) return fail(SIDP_EINVAL, "max_batch/max_ctx >= 1");
   if (cfg->compute_sms < 0 || cfg->fetch_sms < 0) return fail(SIDP_EINVAL, "negative SM count");
+  if (cfg->slot_parts < 0 || cfg->slot_parts > 2) return fail(SIDP_EINVAL, "slot_parts must be 0, 1 or 2");
+  if (cfg->slot_parts == 2) {   // tiles: the SM fetch's device ring, was_slots x parts ring entries
+    const int parts = cfg->pool_scope == SIDP_POOL_LAYER ? 4 : 2;
+    if (cfg->world > 1 && cfg->fetch_engine != SIDP_FETCH_SM)
+      return fail(SIDP_EINVAL, "tile slots (slot_parts = 2) need the SM fetch (SIDP_FETCH_SM)");
+    if (cfg->was_slots * parts > sidp::kRingMaxSlots)
+      return fail(SIDP_EINVAL, "tile slots: was_slots %d x %d parts > %d", cfg->was_slots, parts,
+                  sidp::kRingMaxSlots);
+  }
   std::vector<int> owner(m.num_layers);
   for (int l = 0; l < m.num_layers; ++l) {
     owner[l] = cfg->layer_owner ? cfg->layer_owner[l] : l % cfg->world;

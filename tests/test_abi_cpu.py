@@ -88,12 +88,17 @@ def test_custom_owner_map_and_rejections(sidp):
     assert [c.owner_of(l) for l in range(4)] == [1, 1, 0, 0]
     assert c.plan() == [0, 1]
     c.destroy()
-    bad = [dict(layer_owner=[0, 1, 2, 0]), dict(slots=0), dict(rank=2), dict(max_batch=0)]
+    bad = [dict(layer_owner=[0, 1, 2, 0]), dict(slots=0), dict(rank=2), dict(max_batch=0),
+           dict(slot_parts=3),                              # granularity: 0, 1 or 2
+           dict(slot_parts=2, fetch_engine="ce"),           # tiles live in the SM fetch's device ring
+           dict(slot_parts=2, slots=5)]                     # 5 slots x 4 parts > 16 ring entries
     for kw in bad:
         kw = {"rank": 0, "world": 2, **kw}
         with pytest.raises(sidp.SidpError) as e:
             sidp.Context(m, alloc=False, **kw)
         assert e.value.status == -1     # SIDP_EINVAL
+    for kw in (dict(slot_parts=2, slots=4), dict(slot_parts=2, slots=8, pool="ffn")):
+        sidp.Context(m, rank=0, world=2, alloc=False, **kw).destroy()   # 16 ring entries: fine
     with pytest.raises(sidp.SidpError):  # PAPER order with S < d-1 deadlocks (C-S4)
         sidp.Context(m.with_layers(8), rank=1, world=4, slots=2, order="paper", alloc=False)
 
