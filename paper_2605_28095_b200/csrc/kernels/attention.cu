@@ -787,8 +787,19 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   // (65 chunks) 194-197 vs 190-191, step equal; B = 128 / 2048 177 vs 190; B = 64 / 4096
   // 170 vs 185 (long pairs keep pair mode); B = 1536 / 32 326 vs 254-260.
   const long long chunks_per_pair = (max_tok + kChunk - 1) / kChunk;
-  long long cl = pairs >= slots ? (chunks_per_pair >= 64 ? pairs : slots)
-                                : std::min(slots, std::max<long long>(1, w_max / 8));
+  // Fewer pairs than CTA slots (the CaS tail, small batches): each pair split into k equal pieces,
+  // k = 128 / pairs but >= 32 chunks per piece, so a CTA never straddles two pairs and the
+  // last-arriver merge folds at most k pieces.  Measured (bench, 8 layers; was one wave of
+  // w_max / 8 CTAs): B = 1 / S_ctx 4096 48.9 -> 25.1 us (k = 8), B = 4 / 4096 39.4 -> 28.7
+  // (k = 4), B = 16 / 1024 33.0 -> 20.6 and B = 16 / 4096 62.3 -> 49.4 (k = 1: no pieces).
+  long long cl;
+  if (pairs >= slots) {
+    cl = chunks_per_pair >= 64 ? pairs : slots;
+  } else {
+    const long long k = std::max<long long>(1, std::min<long long>(std::max<long long>(1, 128 / pairs),
+                                                                   chunks_per_pair / 32));
+    cl = std::min(slots, pairs * k);
+  }
   // Many pairs of < SIDP_ATTN_WARP_CH (default 128) chunks: warp-per-pair kernel, one wave
   // (B = 1024 / S_ctx = 256: 301 -> 185 us; 768 / 512: 322 -> 277; 512 / 768: 290 -> 259;
   // M2, 65 chunks: step 29.52-29.63 -> 29.29-29.34 ms; B = 128 / 2048 equal)
