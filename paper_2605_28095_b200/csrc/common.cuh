@@ -149,6 +149,14 @@ SIDP_DEV uint32_t elect_one() {
 SIDP_DEV void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// last-arriver election at system scope: acq_rel orders this CTA's prior (barrier-ordered) stores
+// before the count and the winner's later flag stores after every earlier arriver's — no
+// fence.sc.sys (measured ~5 us per use) needed
+SIDP_DEV unsigned atom_add_acq_rel_sys(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 SIDP_DEV uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

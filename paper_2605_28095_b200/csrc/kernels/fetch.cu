@@ -69,8 +69,7 @@ __global__ void delay_kernel(uint64_t ns) {
 
 // Post a flag after all prior work of this stream (kernel boundary orders the data).
 __global__ void signal_kernel(uint64_t* flag, uint64_t value) {
-  __threadfence_system();
-  st_release_sys(flag, value);
+  st_release_sys(flag, value);   // the stream's earlier kernels completed: their stores performed
 }
 
 // Wait until every flag >= value (system-scope acquire); bounded by timeout_ns, after
@@ -187,27 +186,38 @@ cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int r
   return cudaGetLastError();
 }
 
-// grid-strided over each job's 16-byte vectors; every thread fences its stores system-wide,
-// then the last CTA to arrive publishes the flags
+// grid-strided over each job's 16-byte vectors, 4 loads in flight per thread; then each CTA's
+// thread 0 counts the CTA in with an acq_rel system-scope atomic (after the CTA barrier) and the
+// last CTA to arrive publishes the flags with release stores (no fence.sc.sys: ~5 us each)
 __global__ void __launch_bounds__(256) xfer_kernel(const XferSet x) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   for (int j = 0; j < x.njobs; ++j) {
     const XferJob& jb = x.job[j];
     const int nvec = jb.row_bytes / 16;
     const long long total = (long long)jb.rows * nvec;
-    for (long long i = gt; i < total; i += gs) {
+    auto src_of = [&](long long i) {
       const int r = (int)(i / nvec), v = (int)(i % nvec);
-      reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(jb.dst) + (size_t)r * jb.ldd)[v] =
-          reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(jb.src) + (size_t)r * jb.lds)[v];
+      return reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(jb.src) + (size_t)r * jb.lds) + v;
+    };
+    auto dst_of = [&](long long i) {
+      const int r = (int)(i / nvec), v = (int)(i % nvec);
+      return reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(jb.dst) + (size_t)r * jb.ldd) + v;
+    };
+    long long i = gt;
+    for (; i + 3LL * gs < total; i += 4LL * gs) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(src_of(i + u * (long long)gs));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) *dst_of(i + u * (long long)gs) = v[u];
     }
+    for (; i < total; i += gs) *dst_of(i) = __ldcg(src_of(i));
   }
-  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(x.counter, 1u);
+    const unsigned prev = atom_add_acq_rel_sys(x.counter, 1u);
     if (prev == gridDim.x - 1) {
       *x.counter = 0u;
-      __threadfence_system();
       for (int f = 0; f < x.nflags; ++f) st_release_sys(x.flag[f], x.value);
     }
   }

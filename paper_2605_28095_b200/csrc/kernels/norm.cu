@@ -138,13 +138,11 @@ __global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSe
     }
     __syncthreads();   // red[] reused by the next row
   }
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(a.counter, 1u);
+  if (threadIdx.x == 0) {   // the CTA counted in with an acq_rel system-scope atomic
+    const unsigned prev = atom_add_acq_rel_sys(a.counter, 1u);
     if (prev == gridDim.x - 1) {
       *a.counter = 0u;
-      __threadfence_system();
       st_release_sys(a.arrive, a.value);
     }
   }
