@@ -77,6 +77,15 @@ struct FlagWait {
   int* err;
 };
 
+// CaS owner: the GEMM's output rows scattered straight into the requesters'
+// receive buffers — rows [row0[q], row0[q+1]) of the fused staging batch go to base[q] (a peer
+// VA; row stride = the GEMM's ldo).  n == 0: plain output.
+struct RowScatter {
+  int n;
+  int row0[17];
+  void* base[16];
+};
+
 struct GemmArgs {
   const bf16* x; int ldx;      // [M, K]
   const bf16* w; int ldw;      // [N, K]
@@ -92,6 +101,7 @@ struct GemmArgs {
   int x_kbmajor;               // 1: X is k-block-major [K/64][M][64] (layout experiment)
   PartialSrc* partial_out;     // EPI_PARTIAL: receives the slice geometry for the consumer
   const FlagWait* wait;        // optional: the activation loads wait for these flags (CaS owner)
+  const RowScatter* scatter;   // optional (EPI_F32 / EPI_BF16 / EPI_RESID): output rows -> peers
 };
 
 struct GemmWorkspace {

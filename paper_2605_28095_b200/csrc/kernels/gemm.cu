@@ -61,7 +61,18 @@ struct KParams {
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
   QkvEpi qkv;                   // EPI_QKV destination
   FlagWait wait;                // CaS owner: activation loads wait for the arrival flags
+  RowScatter scatter;           // CaS owner: output rows straight into the requesters' buffers
 };
+
+// Base of output row m (elements of size ES): out + m * ldo, or the requester's receive buffer
+// holding fused row m (CaS scatter; rows of one requester are contiguous in both).
+template <typename T>
+SIDP_DEV T* out_row(const KParams& p, int m) {
+  if (p.scatter.n == 0) return reinterpret_cast<T*>(p.out) + (size_t)m * p.ldo;
+  int q = 0;
+  while (q + 1 < p.scatter.n && m >= p.scatter.row0[q + 1]) ++q;
+  return reinterpret_cast<T*>(p.scatter.base[q]) + (size_t)(m - p.scatter.row0[q]) * p.ldo;
+}
 
 // ---- cluster / 2-SM helpers ------------------------------------------------------
 SIDP_DEV uint32_t cluster_ctarank() {
@@ -258,7 +269,6 @@ SIDP_DEV uint4 pack_bf16x8(const float (&f)[8]) {
 template <int EPI>
 SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int pt, int tid) {
   if constexpr (EPI == EPI_F32) {
-    float* out = reinterpret_cast<float*>(p.out);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int v = tid + 128 * i, j = v >> 5, f = (v & 31) * 4;
@@ -270,11 +280,10 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
           const float2 b0 = __bfloat1622float2(b2[0]), b1 = __bfloat1622float2(b2[1]);
           x.x += b0.x; x.y += b0.y; x.z += b1.x; x.w += b1.y;
         }
-        *reinterpret_cast<float4*>(out + (size_t)m * p.ldo + n) = x;
+        *reinterpret_cast<float4*>(out_row<float>(p, m) + n) = x;
       }
     }
   } else if constexpr (EPI == EPI_BF16 || EPI == EPI_RESID) {
-    bf16* out = reinterpret_cast<bf16*>(p.out);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int v = tid + 128 * i, j = v >> 4, f = (v & 15) * 8;
@@ -297,7 +306,7 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) x[q] += y[q];
-        *reinterpret_cast<uint4*>(out + (size_t)m * p.ldo + n) = pack_bf16x8(x);
+        *reinterpret_cast<uint4*>(out_row<bf16>(p, m) + n) = pack_bf16x8(x);
       }
     }
   } else if constexpr (EPI == EPI_SILU_MUL) {
@@ -431,7 +440,7 @@ template <int EPI>
 SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0, int nlim,
                         unsigned long long& best) {
   if constexpr (EPI == EPI_F32) {
-    float* out = reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo;
+    float* out = out_row<float>(p, m);
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
       const int n = n0 + 4 * g;
@@ -447,7 +456,7 @@ SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0
       }
     }
   } else if constexpr (EPI == EPI_BF16 || EPI == EPI_RESID) {
-    bf16* out = reinterpret_cast<bf16*>(p.out) + (size_t)m * p.ldo;
+    bf16* out = out_row<bf16>(p, m);
     uint4 addv[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {   // issue the residual / bias loads first
@@ -881,7 +890,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) a[q] += y[q];
       }
-      float* out = reinterpret_cast<float*>(p.out) + (size_t)m * p.ldo + f;
+      float* out = out_row<float>(p, m) + f;
       *reinterpret_cast<float4*>(out) = make_float4(a[0], a[1], a[2], a[3]);
       *reinterpret_cast<float4*>(out + 4) = make_float4(a[4], a[5], a[6], a[7]);
     } else if constexpr (EPI == EPI_BF16 || EPI == EPI_RESID) {
@@ -896,8 +905,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) a[q] += y[q];
-      *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(p.out) + (size_t)m * p.ldo + f) =
-          pack_bf16x8(a);
+      *reinterpret_cast<uint4*>(out_row<bf16>(p, m) + f) = pack_bf16x8(a);
     } else if constexpr (EPI == EPI_SILU_MUL) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) a[q] = a[q] / (1.0f + __expf(-a[q])) * b[q];
@@ -1565,6 +1573,10 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.w_evict = env_evict && (sw ? n_pairs == 1 : m_tiles == 1);
   if (a.qkv) p.qkv = *a.qkv;
   if (a.wait) p.wait = *a.wait;
+  if (a.scatter) {
+    if (a.epi != EPI_F32 && a.epi != EPI_BF16 && a.epi != EPI_RESID) return cudaErrorInvalidValue;
+    p.scatter = *a.scatter;
+  }
   static int env_debug = getenv("SIDP_GEMM_DEBUG") ? atoi(getenv("SIDP_GEMM_DEBUG")) : 0;
   p.debug = env_debug;
   static int env_trace = getenv("SIDP_GEMM_TRACE") ? atoi(getenv("SIDP_GEMM_TRACE")) : 0;

@@ -411,9 +411,11 @@ sidp::GemmWorkspace gws(sidp_ctx* c) {
 cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, int M, int N, int K,
                  int epi, void* out, int ldo, const bf16* resid, int ldr, const bf16* bias,
                  cudaStream_t s, const sidp::QkvEpi* qkv = nullptr,
-                 sidp::PartialSrc* partial = nullptr, const sidp::FlagWait* wait = nullptr) {
+                 sidp::PartialSrc* partial = nullptr, const sidp::FlagWait* wait = nullptr,
+                 const sidp::RowScatter* scatter = nullptr) {
   sidp::GemmArgs a{};
   a.wait = wait;
+  a.scatter = scatter;
   a.x = x; a.ldx = ldx; a.w = w; a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = epi;
   a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias; a.qkv = qkv;
   a.partial_out = partial;
@@ -540,7 +542,8 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
 // u = RMSNorm(out) * next_g for the next layer (ctx->u_for).
 sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf16* x, int ldx,
                      bf16* out, int B, cudaStream_t s, const bf16* next_g = nullptr,
-                     int next_layer = -1, const sidp::FlagWait* wait = nullptr) {
+                     int next_layer = -1, const sidp::FlagWait* wait = nullptr,
+                     const sidp::RowScatter* scatter = nullptr) {
   const auto& m = ctx->m;
   const int h = m.hidden;
   // x2 = x + o W_o^T  (into out), u2 = RMSNorm(x2) * g_mlp
@@ -600,7 +603,7 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
     ctx->u_for = next_layer;
   } else {
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_RESID, out, h,
-            out, h, nullptr, s));
+            out, h, nullptr, s, nullptr, nullptr, nullptr, scatter));
     CK(ring_release(ctx, C_WD, s));
   }
   return SIDP_OK;
@@ -1084,6 +1087,38 @@ sidp_status cas_send(sidp_ctx* ctx, const CasTrip& t, const bf16* x, const bf16*
   return SIDP_OK;
 }
 
+// SIDP_CAS_SCATTER=0: the owner GEMM writes a local result that one transfer launch returns
+bool cas_scatter() {
+  static const bool v = !(getenv("SIDP_CAS_SCATTER") && atoi(getenv("SIDP_CAS_SCATTER")) == 0);
+  return v;
+}
+
+// owner (K9): the output rows of every live rank go straight into its receive buffer
+sidp::RowScatter cas_row_scatter(sidp_ctx* ctx, const CasTrip& t) {
+  sidp::RowScatter sc{};
+  for (int q = 0; q < ctx->d; ++q) {
+    if (ctx->batches[q] == 0) continue;
+    sc.row0[sc.n] = t.off[q];
+    sc.base[sc.n] = ctx->peer_cas[q] + ctx->cas_recv_off;
+    ++sc.n;
+  }
+  sc.row0[sc.n] = t.total;
+  return sc;
+}
+
+// owner, after a scattering GEMM: done for every live rank + served (one tiny launch)
+sidp_status cas_post(sidp_ctx* ctx, const CasTrip& t, cudaStream_t s) {
+  sidp::XferSet xs{};
+  for (int q = 0; q < ctx->d; ++q)
+    if (ctx->batches[q] > 0) xs.flag[xs.nflags++] = flag_ptr(ctx->peer_cas[q], flag_off_done(ctx->d));
+  xs.flag[xs.nflags++] = flag_ptr(ctx->cas, flag_off_served(ctx->d));
+  xs.value = (uint64_t)t.rt + 1;
+  xs.counter = ctx->xfer_cnt;
+  CK(sidp::xfer_launch(xs, s));
+  count_launch(ctx);
+  return SIDP_OK;
+}
+
 // owner: every live rank's slice of `result` back to its receive buffer, then done + served
 sidp_status cas_return(sidp_ctx* ctx, const CasTrip& t, const uint8_t* result, size_t result_ld,
                        size_t row_bytes, cudaStream_t s) {
@@ -1144,10 +1179,13 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       st = consumer_wait(ctx, w, s);
       if (st != SIDP_OK) return st;
       const bf16* stage = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t1.slot, 0));
+      const sidp::RowScatter sc = cas_row_scatter(ctx, t1);
       CK(gemm(ctx, 5, stage, ctx->stage_width, W.wqkv, t1.total, ctx->qkvdim, h, sidp::EPI_F32,
-              ctx->qkv, ctx->qkvdim, nullptr, 0, W.b_qkv, s, nullptr, nullptr, w.n ? &w : nullptr));
-      st = cas_return(ctx, t1, reinterpret_cast<const uint8_t*>(ctx->qkv), (size_t)ctx->qkvdim * 4,
-                      (size_t)ctx->qkvdim * 4, s);
+              ctx->qkv, ctx->qkvdim, nullptr, 0, W.b_qkv, s, nullptr, nullptr, w.n ? &w : nullptr,
+              cas_scatter() ? &sc : nullptr));
+      st = cas_scatter() ? cas_post(ctx, t1, s)
+                         : cas_return(ctx, t1, reinterpret_cast<const uint8_t*>(ctx->qkv),
+                                      (size_t)ctx->qkvdim * 4, (size_t)ctx->qkvdim * 4, s);
       if (st != SIDP_OK) return st;
     }
     CasTrip t2 = cas_trip(ctx, layer);
@@ -1170,11 +1208,13 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       if (st != SIDP_OK) return st;
       const bf16* st_o = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t2.slot, 0));
       bf16* st_x = reinterpret_cast<bf16*>(cas_stage_ptr(ctx, ctx->cas, t1.slot, 0)) + h;
+      const sidp::RowScatter sc = cas_row_scatter(ctx, t2);
       st = mlp_part(ctx, W, st_o, ctx->stage_width, st_x, ctx->stage_width, ctx->cas_out, t2.total,
-                    s, nullptr, -1, w.n ? &w : nullptr);
+                    s, nullptr, -1, w.n ? &w : nullptr, cas_scatter() ? &sc : nullptr);
       if (st != SIDP_OK) return st;
-      st = cas_return(ctx, t2, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
-                      (size_t)h * 2, s);
+      st = cas_scatter() ? cas_post(ctx, t2, s)
+                         : cas_return(ctx, t2, reinterpret_cast<const uint8_t*>(ctx->cas_out),
+                                      (size_t)h * 2, (size_t)h * 2, s);
       if (st != SIDP_OK) return st;
     }
     ctx->last_rt_any[o] = t2.rt;
@@ -1208,10 +1248,13 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
     CK(gemm(ctx, 1, stage, ctx->stage_width, W.wgu, t.total, 2 * m.intermediate, h,
             sidp::EPI_SILU_MUL, ctx->act, m.intermediate, nullptr, 0, nullptr, s, nullptr, nullptr,
             w.n ? &w : nullptr));
+    const sidp::RowScatter sc = cas_row_scatter(ctx, t);
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, t.total, h, m.intermediate, sidp::EPI_RESID,
-            ctx->cas_out, h, stage + h, ctx->stage_width, nullptr, s));
-    st = cas_return(ctx, t, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
-                    (size_t)h * 2, s);
+            ctx->cas_out, h, stage + h, ctx->stage_width, nullptr, s, nullptr, nullptr, nullptr,
+            cas_scatter() ? &sc : nullptr));
+    st = cas_scatter() ? cas_post(ctx, t, s)
+                       : cas_return(ctx, t, reinterpret_cast<const uint8_t*>(ctx->cas_out),
+                                    (size_t)h * 2, (size_t)h * 2, s);
     if (st != SIDP_OK) return st;
   }
   ctx->last_rt_any[o] = t.rt;
