@@ -14,8 +14,10 @@ res = {"bytes": nbytes}
 L = P._abi.lib()
 L.sidp_test_fetch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p]
 runs = [(c, 0) for c in [8, 16, 32, 64]] + [(c, 3) for c in [16, 24, 32, 48]] + [(0, 1)]
-if os.environ.get("ONLY_RING"):
-    runs = [(int(os.environ.get("ONLY_RING")), 3)]
+if os.environ.get("ONLY_LDG"):
+    runs = [(int(c), 2) for c in os.environ.get("ONLY_LDG").split(",")]
+elif os.environ.get("ONLY_RING"):
+    runs = [(int(c), 3) for c in os.environ.get("ONLY_RING").split(",")]
 for ctas, engine in runs:
     for _ in range(2):
         P._abi.check(L.sidp_test_fetch(dst.data_ptr(), src.data_ptr(), nbytes, ctas, engine, None), "fetch")
@@ -26,7 +28,7 @@ for ctas, engine in runs:
         P._abi.check(L.sidp_test_fetch(dst.data_ptr(), src.data_ptr(), nbytes, ctas, engine, None), "fetch")
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    key = "copy_engine" if engine == 1 else (f"ring_fetch_{ctas}ctas" if engine == 3 else f"sm_fetch_{ctas}ctas")
+    key = {1: "copy_engine", 2: f"ldg_fetch_{ctas}ctas", 3: f"ring_fetch_{ctas}ctas"}.get(engine, f"sm_fetch_{ctas}ctas")
     res[key] = {"ms": ms, "GBps_read": nbytes / ms / 1e6}
 assert torch.equal(dst, src)
 print(json.dumps(res))
