@@ -533,6 +533,14 @@ def kv_capacity(m, st_d1, fp_dw, W, util=0.9):
         fpw = sum(fp_dw.values())
         out[f"sidp_d{W}"] = {"footprint_bytes": fpw, "kv_tokens": tokens(fpw)}
         out["ratio"] = tokens(fpw) / max(1, tokens(fp1))
+        # tensor parallelism over the same W GPUs (PAPER.md:314's other comparison), ANALYTIC:
+        # every weight (layers, embedding, LM head) sharded W ways, KV heads sharded W ways
+        # (so a GPU stores 1/W of each token's KV), the same workspaces; group tokens per GPU
+        # are then free / (per_tok / W) / W = free / per_tok, directly comparable with SiDP's
+        fp_tp = (st_d1["owned_bytes"] + st_d1["replicated_bytes"]) / W + st_d1["workspace_bytes"]
+        out[f"tp{W}_analytic"] = {"footprint_bytes": int(fp_tp), "kv_tokens": tokens(fp_tp),
+                                  "note": "weights and KV heads sharded; tokens per GPU of the group"}
+        out["ratio_vs_tp"] = tokens(fpw) / max(1, tokens(fp_tp))
     return out
 
 
