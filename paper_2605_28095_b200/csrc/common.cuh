@@ -149,12 +149,13 @@ SIDP_DEV uint32_t elect_one() {
 SIDP_DEV void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// last-arriver election at system scope: acq_rel orders this CTA's prior (barrier-ordered) stores
-// before the count and the winner's later flag stores after every earlier arriver's — no
-// fence.sc.sys (measured ~5 us per use) needed
-SIDP_DEV unsigned atom_add_acq_rel_sys(unsigned* p, unsigned v) {
+// Last-arriver election among the CTAs of ONE grid: a gpu-scope acq_rel atomic (all electors
+// are on this GPU).  The winner's later st.release.sys of the flag is cumulative over this
+// causality chain, so every CTA's earlier (barrier-ordered) stores — peer stores included — are
+// visible to whoever acquires the flag; no fence.sc.sys (~5 us) and no sys-scope atomic needed.
+SIDP_DEV unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
   unsigned old;
-  asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
 SIDP_DEV uint64_t ld_acquire_sys(const uint64_t* p) {

@@ -187,7 +187,7 @@ cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int r
 }
 
 // grid-strided over each job's 16-byte vectors, 4 loads in flight per thread; then each CTA's
-// thread 0 counts the CTA in with an acq_rel system-scope atomic (after the CTA barrier) and the
+// thread 0 counts the CTA in with an acq_rel gpu-scope atomic (after the CTA barrier) and the
 // last CTA to arrive publishes the flags with release stores (no fence.sc.sys: ~5 us each)
 __global__ void __launch_bounds__(256) xfer_kernel(const XferSet x) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(256) xfer_kernel(const XferSet x) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned prev = atom_add_acq_rel_sys(x.counter, 1u);
+    const unsigned prev = atom_add_acq_rel_gpu(x.counter, 1u);
     if (prev == gridDim.x - 1) {
       *x.counter = 0u;
       for (int f = 0; f < x.nflags; ++f) st_release_sys(x.flag[f], x.value);

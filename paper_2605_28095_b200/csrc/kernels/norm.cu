@@ -99,19 +99,40 @@ __global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSe
     __syncthreads();
   }
   const int h = a.h, nvec = h / 8;
+  const bool cached = nvec <= kNormThreads * kVec;
   for (int row = blockIdx.x; row < a.rows; row += gridDim.x) {
     const bf16* xr = a.x + (size_t)row * a.ldx;
     bf16* ur = a.dst + (size_t)row * a.ldd;
     bf16* xd = ur + h;
+    // the row read once (kept in registers, as rmsnorm_kernel; same summation order, so u is
+    // bitwise the replicated path's) and forwarded to the owner while the statistics reduce
+    uint4 v[kVec];
     float ss = 0.0f;
-    for (int k = threadIdx.x; k < nvec; k += kNormThreads) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(xr + k * 8);
-      *reinterpret_cast<uint4*>(xd + k * 8) = raw;
+    auto acc = [&](const uint4& raw) {
       const bf16* e = reinterpret_cast<const bf16*>(&raw);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float f = bf16_to_f(e[q]);
         ss += f * f;
+      }
+    };
+    if (cached) {
+#pragma unroll
+      for (int i = 0; i < kVec; ++i) {
+        const int k = threadIdx.x + i * kNormThreads;
+        v[i] = k < nvec ? *reinterpret_cast<const uint4*>(xr + k * 8) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int i = 0; i < kVec; ++i) {
+        const int k = threadIdx.x + i * kNormThreads;
+        if (k < nvec) *reinterpret_cast<uint4*>(xd + k * 8) = v[i];
+        acc(v[i]);
+      }
+    } else {
+      for (int k = threadIdx.x; k < nvec; k += kNormThreads) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(xr + k * 8);
+        *reinterpret_cast<uint4*>(xd + k * 8) = raw;
+        acc(raw);
       }
     }
     __shared__ float red[32];
@@ -125,8 +146,7 @@ __global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSe
     }
     __syncthreads();
     const float r = rsqrtf(red[0] / (float)h + a.eps);
-    for (int k = threadIdx.x; k < nvec; k += kNormThreads) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(xr + k * 8);
+    auto scale = [&](const uint4& raw, int k) {
       const uint4 graw = *reinterpret_cast<const uint4*>(a.g + k * 8);
       const bf16* e = reinterpret_cast<const bf16*>(&raw);
       const bf16* ge = reinterpret_cast<const bf16*>(&graw);
@@ -135,12 +155,22 @@ __global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSe
 #pragma unroll
       for (int q = 0; q < 8; ++q) o[q] = f_to_bf16(bf16_to_f(e[q]) * r * bf16_to_f(ge[q]));
       *reinterpret_cast<uint4*>(ur + k * 8) = out;
+    };
+    if (cached) {
+#pragma unroll
+      for (int i = 0; i < kVec; ++i) {
+        const int k = threadIdx.x + i * kNormThreads;
+        if (k < nvec) scale(v[i], k);
+      }
+    } else {
+      for (int k = threadIdx.x; k < nvec; k += kNormThreads)
+        scale(*reinterpret_cast<const uint4*>(xr + k * 8), k);
     }
     __syncthreads();   // red[] reused by the next row
   }
   __syncthreads();
-  if (threadIdx.x == 0) {   // the CTA counted in with an acq_rel system-scope atomic
-    const unsigned prev = atom_add_acq_rel_sys(a.counter, 1u);
+  if (threadIdx.x == 0) {   // the CTA counted in with an acq_rel gpu-scope atomic
+    const unsigned prev = atom_add_acq_rel_gpu(a.counter, 1u);
     if (prev == gridDim.x - 1) {
       *a.counter = 0u;
       st_release_sys(a.arrive, a.value);
