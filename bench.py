@@ -81,6 +81,10 @@ def parse():
     ap.add_argument("--cas-batches", default="1,4,16",
                     help="all-live per-rank batches of the CaS emulation (B=16 also runs the "
                          "half-live and one-live dummy patterns)")
+    ap.add_argument("--m3-emulate", type=int, default=1,
+                    help="N=1 only: also time the north-star point — M3, Llama-3.1-70B WaS d=8 at "
+                         "B=1024 / S_ctx=384 (the measured B_e, max KV with aliased owners) — in a "
+                         "child process (0 = off)")
     ap.add_argument("--cas-only", action="store_true",
                     help="print only the CaS emulation (run as a child of the default bench)")
     ap.add_argument("--extra-timeout", type=int, default=240,
@@ -800,6 +804,15 @@ def main():
         if args.cas_emulate and args.emulate_world > 1:
             child = _child_json(["--cas-only"], args.extra_timeout)
             line["cas_emulation"] = child.get("cas_emulation", child)
+        if args.m3_emulate and args.emulate_world > 1 and args.layers is None:
+            child = _child_json(["--emulate-only", "--workload", "M3", "--emulate-batch", "1024",
+                                 "--emulate-ctx", "384", "--alias-owners", "--emulate-steps", "3"],
+                                args.extra_timeout)
+            m3 = child.get("was_emulation", child)
+            if isinstance(m3, dict) and "error" not in m3:
+                m3["note"] = ("north-star target shape (SURVEY.md M3) at the measured B_e; owners "
+                              "aliased (timing only), so this GPU keeps a real rank's KV memory")
+            line["m3_emulation"] = m3
     print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
