@@ -62,6 +62,9 @@ def parse():
                          "owners being serve-only contexts in local HBM (0 = off)")
     ap.add_argument("--emulate-fetch-sms", type=int, default=24,
                     help="SMs the emulated rank's fetch kernel holds (the real-run default, 16)")
+    ap.add_argument("--emulate-ce-share", type=float, default=0.0,
+                    help="hybrid fetch of the emulated rank: share of each layer copied by the "
+                         "copy engine (sidp_config.fetch_ce_share)")
     ap.add_argument("--emulate-pace-gbps", type=float, default=770.0,
                     help="the emulated rank's fetch kernel paces itself to this rate: the NVLink 5 "
                          "reader rate (B200_PROFILING.md measured peer copy); 0 = unpaced")
@@ -297,7 +300,8 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
     ctx0 = P.Context(m, rank=0, world=W, slots=slots, order=args.order, pool=args.pool,
                      max_batch=kv.max_batch, max_ctx=max_ctx, fetch_sms=args.emulate_fetch_sms,
                      fetch_engine=args.fetch, stagger=not args.no_stagger, device=local, seed=seed,
-                     fetch_pace_gbps=args.emulate_pace_gbps, slot_parts=args.slot_parts)
+                     fetch_pace_gbps=args.emulate_pace_gbps, slot_parts=args.slot_parts,
+                     fetch_ce_share=args.emulate_ce_share)
     peers = []
     try:
         for r in range(1, W):
@@ -362,6 +366,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "compute_sms": st["compute_sms"], "stagger_tick_ms": st["stagger_tick_ns"] * 1e-6,
             "fetch_pace_gbps": args.emulate_pace_gbps,
             "owners_aliased": bool(args.alias_owners),
+            "fetch_ce_share": args.emulate_ce_share,
             "steps": args.emulate_steps,
             "ms_per_step": ms, "tokens_s_rank": B / (ms / 1e3),
             "group_tokens_s_est": W * B / (ms / 1e3),

@@ -119,6 +119,13 @@ typedef struct {
                                    computing context per GPU (its fetch is one windowed launch
                                    whose CTAs gate each part in-kernel; else SIDP_ESTATE at the
                                    step). */
+  float fetch_ce_share;         /* hybrid WaS fetch (SIDP_FETCH_SM, whole-layer slots): this share of
+                                   each layer (a prefix, in 32 KB chunks) is copied by the copy
+                                   engine on its own stream, the rest by the SM fetch kernel; both
+                                   count into the same fill epoch and whichever completes it
+                                   publishes.  An SM reads ~50 GB/s, so moving part of
+                                   the layer to the copy engine lets fewer fetch SMs hold the link
+                                   rate at compute-bound batches.  [0, 1); 0 = SM fetch only. */
 } sidp_config;
 
 /* Caller-owned KV cache of this rank (never pooled).

@@ -34,7 +34,8 @@ class Config(C.Structure):
                 ("pool_scope", C.c_int32), ("max_batch", C.c_int32), ("max_ctx", C.c_int32),
                 ("fetch_sms", C.c_int32), ("fetch_engine", C.c_int32), ("stagger", C.c_int32),
                 ("device", C.c_int32), ("seed", C.c_uint64), ("fetch_pace_gbps", C.c_float),
-                ("compute_sms", C.c_int32), ("slot_parts", C.c_int32)]
+                ("compute_sms", C.c_int32), ("slot_parts", C.c_int32),
+                ("fetch_ce_share", C.c_float)]
 
 
 class KV(C.Structure):

@@ -67,7 +67,7 @@ class Context:
     def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
                  max_batch=8, max_ctx=128, fetch_sms=24, fetch_engine="sm", stagger=True,
                  device=0, seed=20261017, layer_owner=None, alloc=True, fetch_pace_gbps=0.0,
-                 compute_sms=0, slot_parts=0):
+                 compute_sms=0, slot_parts=0, fetch_ce_share=0.0):
         self.m = m
         self.rank, self.world = rank, world
         self._owner_arr = None
@@ -81,7 +81,7 @@ class Context:
                             max_batch, max_ctx, fetch_sms,
                             A.FETCH_SM if fetch_engine == "sm" else A.FETCH_CE,
                             int(bool(stagger)), device, seed, float(fetch_pace_gbps), int(compute_sms),
-                            int(slot_parts))
+                            int(slot_parts), float(fetch_ce_share))
         self.desc = model_desc(m)
         h = C.c_void_p()
         A.check(A.lib().sidp_init(C.byref(self.desc), C.byref(self.cfg), C.byref(h)), "sidp_init")

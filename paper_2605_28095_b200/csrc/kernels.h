@@ -292,6 +292,8 @@ struct FetchArgs {
   int chunk, stages;           // set by fetch_bulk_launch (shared-memory ring geometry)
   int claim_group;             // set by fetch_bulk_launch: chunks per atomic claim
   int nparts;                  // tile-granular slots: parts per blob (0/1 = whole layers)
+  int ce_chunks;               // hybrid fetch (whole layers): chunks [0, ce_chunks) of every fill
+                               // come from the copy engine (ring_ce_done adds them to `done`)
   size_t part_off[4], part_bytes[4];   // byte range of each part within the blob
   FetchEnt ent[kFetchWindow];
 };
@@ -304,6 +306,10 @@ cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t t
 cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s,
                                 unsigned long long* b = nullptr);
 cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s);
+// Hybrid fetch: after the copy engine wrote chunks [0, ce_chunks) of fill e.fill of e.slot, count
+// them into the fill (the SM kernel counts the rest); whichever side completes it publishes.
+cudaError_t ring_ce_done_launch(FetchRing* r, const FetchEnt& e, unsigned long long nchunks,
+                                unsigned ce_chunks, cudaStream_t s);
 cudaError_t ring_preload();
 
 // ---------------------------------------------------------------- CaS signalling

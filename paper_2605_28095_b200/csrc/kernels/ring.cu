@@ -109,11 +109,10 @@ SIDP_DEV void fetch_publish(const FetchArgs& a, const FetchEnt& e, int F) {
   st_release_gpu(&r->fill[e.slot], (unsigned long long)e.fill + 1);
 }
 
-// Dynamic-claim publish (the CTA whose stored-chunk count completes fill e.fill + 1 of virtual
-// slot vs); the device fetch log gets one entry per layer, when its last part lands.
-SIDP_DEV void fetch_publish_dyn(const FetchArgs& a, const FetchEnt& e, int vs, bool last_part,
-                                unsigned long long t_start) {
-  FetchRing* r = a.ring;
+// Dynamic-claim publish (the side whose count completes fill e.fill + 1 of virtual slot vs); the
+// device fetch log gets one entry per layer, when its last part lands.
+SIDP_DEV void ring_publish(FetchRing* r, const FetchEnt& e, int vs, bool last_part,
+                           unsigned long long t_start) {
   r->tag[vs] = e.layer;
   if (last_part) {
     const unsigned long long j = r->nfetch;
@@ -129,6 +128,10 @@ SIDP_DEV void fetch_publish_dyn(const FetchArgs& a, const FetchEnt& e, int vs, b
   }
   __threadfence();
   st_release_gpu(&r->fill[vs], (unsigned long long)e.fill + 1);
+}
+SIDP_DEV void fetch_publish_dyn(const FetchArgs& a, const FetchEnt& e, int vs, bool last_part,
+                                unsigned long long t_start) {
+  ring_publish(a.ring, e, vs, last_part, t_start);
 }
 
 // Windowed gate (one thread per CTA): the slot's previous fill is published and its reader has
@@ -183,10 +186,13 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
       const size_t po = P > 1 ? a.part_off[c] : 0;
       const unsigned long long nch = (pb + CH - 1) / CH;
       auto plen = [&](unsigned long long v) { return (uint32_t)std::min<size_t>(CH, pb - v * CH); };
+      // hybrid fetch: the copy engine writes chunks [0, cbase), the SMs claim [cbase, nch)
+      const unsigned long long cbase = P == 1 ? (unsigned long long)a.ce_chunks : 0ull;
+      const unsigned long long nsm = nch - cbase;
       // claims are groups of G chunks (one atomic per G x chunk bytes: the claim's latency sits
       // in the single issuing thread's path); fill n owns group claims [n (ng + F), ...)
       const unsigned long long G = (unsigned long long)a.claim_group;
-      const unsigned long long ngroups = (nch + G - 1) / G;
+      const unsigned long long ngroups = (nsm + G - 1) / G;
       const unsigned long long base = (unsigned long long)e.fill * (ngroups + F);
       const uint8_t* src = e.src + po;
       uint8_t* dst = a.slots + (size_t)e.slot * a.slot_stride + po;
@@ -204,7 +210,7 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
           if (a.ns_per_chunk) {
             const unsigned long long lt = *reinterpret_cast<volatile unsigned long long*>(&r->link_t);
             t0 = now > lt ? now : lt;
-            r->link_t = t0 + nch * a.ns_per_chunk;
+            r->link_t = t0 + nsm * a.ns_per_chunk;
           } else {
             t0 = now;
           }
@@ -231,13 +237,13 @@ __global__ void __launch_bounds__(32, 1) fetch_bulk_kernel(const __grid_constant
             exhausted = true;
             return;
           }
-          gnext = g * G;
+          gnext = cbase + g * G;
           gend = gnext + G < nch ? gnext + G : nch;
           get_t0(g);
         }
         const unsigned long long v = gnext++;
         if (a.ns_per_chunk) {
-          const uint64_t due = t0 + v * a.ns_per_chunk;
+          const uint64_t due = t0 + (v - cbase) * a.ns_per_chunk;
           while (globaltimer_ns() < due) __nanosleep(256);
         }
         const uint32_t u = use + iss;
@@ -393,6 +399,16 @@ __global__ void ring_release_kernel(unsigned long long* rel, unsigned long long*
   if (b) red_release_gpu_add(b, 1ull);
 }
 
+// Hybrid fetch: the copy engine's chunks of a fill counted in (stream order: after its copy).
+__global__ void ring_ce_done_kernel(FetchRing* r, FetchEnt e, unsigned long long nchunks,
+                                    unsigned ce_chunks) {
+  __threadfence();
+  const unsigned long long target = (unsigned long long)(e.fill + 1) * nchunks;
+  const unsigned long long prev = atomicAdd(&r->done[e.slot], (unsigned long long)ce_chunks);
+  if (prev + ce_chunks == target)
+    ring_publish(r, e, e.slot, true, r->t_first[(e.slot * 2 + (e.fill & 1)) % kRingMaxSlots]);
+}
+
 __global__ void ring_delay_kernel(uint64_t ns) {
   const uint64_t t0 = globaltimer_ns();
   while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
@@ -480,6 +496,12 @@ cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s, unsigne
   return launch_pdl(ring_release_kernel, dim3(1), dim3(1), 0, s, rel, b);
 }
 
+cudaError_t ring_ce_done_launch(FetchRing* r, const FetchEnt& e, unsigned long long nchunks,
+                                unsigned ce_chunks, cudaStream_t s) {
+  ring_ce_done_kernel<<<1, 1, 0, s>>>(r, e, nchunks, ce_chunks);
+  return cudaGetLastError();
+}
+
 cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s) {
   if (ns == 0) return cudaSuccess;
   ring_delay_kernel<<<1, 1, 0, s>>>(ns);
@@ -495,6 +517,7 @@ cudaError_t ring_preload() {
   if (cudaFuncGetAttributes(&fa, ring_ready_wait_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, ring_release_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, ring_delay_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, ring_ce_done_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncSetAttribute(fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)fetch_bulk_smem()) != cudaSuccess)
     e = cudaGetLastError();

@@ -140,6 +140,11 @@ struct sidp_ctx {
   uint64_t cas_timeout_ns = 20ull * 1000 * 1000 * 1000;   // SIDP_CAS_TIMEOUT_MS at sidp_init
   unsigned int* xfer_cnt = nullptr;  // last-CTA election counter of the fused CaS transfers
   unsigned long long* pace_t0 = nullptr;   // start stamp of a paced copy-engine fetch
+  // hybrid fetch (sidp_config.fetch_ce_share): the copy engine writes each layer's first
+  // ce_chunks chunks on ce_stream, the SM fetch kernel the rest
+  int ce_chunks = 0;
+  cudaStream_t ce_stream = nullptr;
+  unsigned long long* ce_pace_t0 = nullptr;
   std::vector<int> batches;        // per-rank rows (control plane)
   int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
@@ -148,6 +153,10 @@ struct sidp_ctx {
   bool arena_borrowed = false;                  // serve-only alias: the arena is another ctx's
   // WaS schedule state
   int64_t fetch_j = 0, compute_k = 0;
+  // hybrid fetch: copy-engine parts enqueued so far, and what they need (fetch index order)
+  int64_t ce_j = 0;
+  struct CePart { const uint8_t* src; uint8_t* dst; sidp::FetchEnt ent; };
+  std::vector<CePart> ce_pending;
   std::vector<int> slot_of_fetch;        // FIFO recurrence, extended lazily (slot_for_fetch)
   std::vector<unsigned> fills;           // fills enqueued per slot
   std::vector<int32_t> log_t, log_l, log_s;
@@ -275,6 +284,8 @@ int64_t fetch_index_of_compute(const sidp_ctx* c, int64_t k) {
 
 void schedule_reset(sidp_ctx* c) {
   c->fetch_j = c->compute_k = 0;
+  c->ce_j = 0;
+  c->ce_pending.clear();
   c->slot_of_fetch.clear();
   c->fills.assign(c->S, 0u);
   c->log_t.clear();
@@ -654,6 +665,41 @@ bool fetch_windowed(const sidp_ctx* ctx) {
   return ring_ctx_count()[ctx->c.device & 63] <= 1;
 }
 
+// Hybrid fetch: the copy-engine part of fetch j is enqueued only once the remote compute entry
+// that releases its slot (j - S, the FIFO free-list) has been enqueued.  Its first op is a flag
+// gate on that release, and a host blocked on a full stream queue while enqueueing a gate whose
+// releasing compute is not enqueued yet would deadlock (Llama, 70 layers x ~11 ops per step).
+// Per part: gate, the copy in 128 MB pieces (paced to its share of the emulated link, with a last
+// pace point so the fill is never published early), then the chunk count into the fill.
+sidp_status pump_ce(sidp_ctx* ctx) {
+  if (ctx->ce_chunks <= 0) return SIDP_OK;
+  const size_t bytes = ctx->pooled_elems * 2;
+  const size_t ce_bytes = std::min(bytes, (size_t)ctx->ce_chunks * sidp::kFetchChunk);
+  const size_t nch = (bytes + sidp::kFetchChunk - 1) / sidp::kFetchChunk;
+  const double rate = ctx->c.fetch_pace_gbps * (double)ce_bytes / (double)bytes;
+  size_t done = 0;
+  for (; done < ctx->ce_pending.size() && ctx->ce_j - ctx->S < ctx->compute_k; ++done, ++ctx->ce_j) {
+    const auto& p = ctx->ce_pending[done];
+    CK(sidp::ring_free_wait_launch(ctx->ring, p.ent.slot, p.ent.fill, ctx->cas_timeout_ns,
+                                   ctx->dev_err, ctx->ce_stream));
+    if (ctx->c.fetch_pace_gbps > 0.0f) {
+      const size_t piece = (size_t)128 << 20;
+      for (size_t off = 0, i = 0; off < ce_bytes; off += piece, ++i) {
+        CK(sidp::pace_launch(ctx->ce_pace_t0, i == 0, (uint64_t)((double)off / rate), ctx->ce_stream));
+        CK(cudaMemcpyAsync(p.dst + off, p.src + off, std::min(piece, ce_bytes - off),
+                           cudaMemcpyDefault, ctx->ce_stream));
+      }
+      CK(sidp::pace_launch(ctx->ce_pace_t0, 0, (uint64_t)((double)ce_bytes / rate), ctx->ce_stream));
+    } else {
+      CK(cudaMemcpyAsync(p.dst, p.src, ce_bytes, cudaMemcpyDefault, ctx->ce_stream));
+    }
+    CK(sidp::ring_ce_done_launch(ctx->ring, p.ent, nch, (unsigned)ctx->ce_chunks, ctx->ce_stream));
+    count_launch(ctx, 3);
+  }
+  ctx->ce_pending.erase(ctx->ce_pending.begin(), ctx->ce_pending.begin() + done);
+  return SIDP_OK;
+}
+
 // Enqueue fetches [fetch_j, upto) on the fetch stream: the device ring takes them
 // as one windowed launch (or one launch per fetch); the copy engine one copy per fetch.
 sidp_status enqueue_fetches(sidp_ctx* ctx, int64_t upto) {
@@ -677,9 +723,13 @@ sidp_status enqueue_fetches(sidp_ctx* ctx, int64_t upto) {
   fa.gate = windowed ? 1 : 0;
   fa.timeout_ns = ctx->cas_timeout_ns;
   fa.err = ctx->dev_err;
-  // emulated link rate: chunk c (kFetchChunk bytes) no earlier than c x chunk / rate
+  // emulated link rate: chunk c (kFetchChunk bytes) no earlier than c x chunk / rate (the SM
+  // side's share of the link with the hybrid fetch)
+  const double sm_share = ctx->ce_chunks > 0
+      ? 1.0 - (double)ctx->ce_chunks * sidp::kFetchChunk / (double)bytes : 1.0;
   fa.ns_per_chunk = ctx->c.fetch_pace_gbps > 0.0f
-                        ? (uint64_t)((double)sidp::kFetchChunk / ctx->c.fetch_pace_gbps) : 0;
+                        ? (uint64_t)((double)sidp::kFetchChunk / (ctx->c.fetch_pace_gbps * sm_share)) : 0;
+  fa.ce_chunks = ctx->ce_chunks;
   if (ctx->parts > 1) {
     if (!windowed)
       return fail(SIDP_ESTATE, "tile slots need one computing context on the GPU (windowed fetch)");
@@ -727,7 +777,10 @@ sidp_status enqueue_fetches(sidp_ctx* ctx, int64_t upto) {
                                        ctx->fetch_stream));
         count_launch(ctx);
       }
-      fa.ent[fa.n++] = sidp::FetchEnt{reinterpret_cast<const uint8_t*>(src), l, s, ctx->owner[l], fill};
+      const sidp::FetchEnt ent{reinterpret_cast<const uint8_t*>(src), l, s, ctx->owner[l], fill};
+      if (ctx->ce_chunks > 0)   // its copy-engine prefix: enqueued by pump_ce (see there)
+        ctx->ce_pending.push_back({reinterpret_cast<const uint8_t*>(src), reinterpret_cast<uint8_t*>(dst), ent});
+      fa.ent[fa.n++] = ent;
       if (!windowed || fa.n == sidp::kFetchWindow) {
         sidp_status st = launch_window();
         if (st != SIDP_OK) return st;
@@ -759,7 +812,9 @@ sidp_status enqueue_fetches(sidp_ctx* ctx, int64_t upto) {
     count_launch(ctx);
     CK(cudaEventRecord(ctx->ready_ev[s], ctx->fetch_stream));
   }
-  return launch_window();
+  sidp_status st = launch_window();
+  if (st != SIDP_OK) return st;
+  return pump_ce(ctx);
 }
 
 // Keep the fetch stream S fetches ahead of the remote compute entries enqueued so far (the FIFO
@@ -841,6 +896,7 @@ sidp_status was_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* k
     }
     ctx->compute_k++;
     st = pump(ctx);
+    if (st == SIDP_OK) st = pump_ce(ctx);
   }
   if (st != SIDP_OK) return st;
   ctx->next_layer = (layer + 1) % ctx->L;
@@ -1376,6 +1432,10 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
   if (cfg->max_batch < 1 || cfg->max_ctx < 1) return fail(SIDP_EINVAL, "max_batch/max_ctx >= 1");
   if (cfg->compute_sms < 0 || cfg->fetch_sms < 0) return fail(SIDP_EINVAL, "negative SM count");
   if (cfg->slot_parts < 0 || cfg->slot_parts > 2) return fail(SIDP_EINVAL, "slot_parts must be 0, 1 or 2");
+  if (!(cfg->fetch_ce_share >= 0.0f && cfg->fetch_ce_share < 1.0f))
+    return fail(SIDP_EINVAL, "fetch_ce_share must be in [0, 1)");
+  if (cfg->fetch_ce_share > 0.0f && cfg->slot_parts == 2)
+    return fail(SIDP_EINVAL, "the hybrid fetch (fetch_ce_share) needs whole-layer slots");
   if (cfg->slot_parts == 2) {   // tiles: the SM fetch's device ring, was_slots x parts ring entries
     const int parts = cfg->pool_scope == SIDP_POOL_LAYER ? 4 : 2;
     if (cfg->world > 1 && cfg->fetch_engine != SIDP_FETCH_SM)
@@ -1444,11 +1504,12 @@ void sidp_destroy(sidp_ctx* ctx) {
       cudaEventDestroy(p.b);
     }
     if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
+    if (ctx->ce_stream) cudaStreamDestroy(ctx->ce_stream);
     if (ctx->arena_borrowed) ctx->arena = nullptr;
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
-                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0, ctx->ring};
+                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0, ctx->ring, ctx->ce_pace_t0};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (ctx->host_err) cudaFreeHost(const_cast<int*>(ctx->host_err));
@@ -1558,6 +1619,14 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
     ctx->fetch_ctas = std::min(ctx->fetch_ctas, std::max(2, (dev_sms / 2) & ~1));
     ctx->compute_sms = std::max(2, (dev_sms - ctx->fetch_ctas) & ~1);
     CK(sidp::ring_preload());
+    if (ctx->c.fetch_ce_share > 0.0f) {   // hybrid fetch: a copy-engine prefix of every layer
+      const size_t nch = (ctx->pooled_elems * 2 + sidp::kFetchChunk - 1) / sidp::kFetchChunk;
+      ctx->ce_chunks = (int)std::min<double>((double)nch - 1, std::floor(nch * ctx->c.fetch_ce_share));
+      if (ctx->ce_chunks > 0) {
+        CK(cudaStreamCreateWithFlags(&ctx->ce_stream, cudaStreamNonBlocking));
+        DM(ctx->ce_pace_t0, sizeof(unsigned long long));
+      }
+    }
     if (ctx->c.slot_parts == 2) {   // one part per pooled component, in blob order
       int n = 0;
       for (int i = 0; i < C_N; ++i) {
@@ -1570,6 +1639,8 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
       if (n > 4 || ctx->S * n > sidp::kRingMaxSlots)
         return fail(SIDP_EINVAL, "tile slots: was_slots %d x %d parts > %d", ctx->S, n, sidp::kRingMaxSlots);
       ctx->parts = n;
+      if (ctx->ce_chunks > 0)
+        return fail(SIDP_EINVAL, "the hybrid fetch (fetch_ce_share) needs whole-layer slots");
     }
   } else if (ctx->c.slot_parts == 2 && ctx->R > 0) {
     return fail(SIDP_EINVAL, "tile slots (slot_parts = 2) need the SM fetch (SIDP_FETCH_SM)");
@@ -1872,6 +1943,7 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
         }
         ctx->compute_k++;
         st = pump(ctx);
+        if (st == SIDP_OK) st = pump_ce(ctx);
         if (st != SIDP_OK) return st;
       }
       ctx->next_layer = (layer + 1) % ctx->L;
@@ -1959,6 +2031,8 @@ static sidp_status replay_bookkeeping(sidp_ctx* ctx) {
     if (st != SIDP_OK) return st;
     if (p >= ctx->fetch_j) return fail(SIDP_ESTATE, "slot ring deadlock (plan lag >= slots)");
     ctx->compute_k++;
+    st = pump_ce(ctx);
+    if (st != SIDP_OK) return st;
   }
   return pump(ctx);
 }
@@ -1996,6 +2070,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
       // drain: wait for in-flight fetches (and, for the device ring, the compute stream's last
       // waits / releases), then restart the plan (reading C-A7)
       CK(cudaStreamSynchronize(ctx->fetch_stream));
+      if (ctx->ce_stream) CK(cudaStreamSynchronize(ctx->ce_stream));
       if (ctx->ring_mode && ctx->last_stream) CK(cudaStreamSynchronize(ctx->last_stream));
       CK(cudaStreamSynchronize(ctx->fetch_stream));
       std::fill(ctx->free_recorded.begin(), ctx->free_recorded.end(), 0);
@@ -2157,6 +2232,8 @@ static sidp_status read_device_log(const sidp_ctx* ctx, std::vector<sidp::FetchL
   out.clear();
   if (!ctx->ring_mode || !ctx->allocated) return SIDP_OK;
   if (cudaStreamSynchronize(ctx->fetch_stream) != cudaSuccess) return fail(SIDP_ECUDA, "fetch stream");
+  if (ctx->ce_stream && cudaStreamSynchronize(ctx->ce_stream) != cudaSuccess)
+    return fail(SIDP_ECUDA, "copy-engine fetch stream");
   unsigned long long n = 0;
   if (cudaMemcpy(&n, &ctx->ring->nfetch, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
     return fail(SIDP_ECUDA, "fetch log count");

@@ -683,3 +683,48 @@ def test_was_tile_slots_full_width_one_slot(P):
         assert torch.equal(rep.history[s][1], R.history[s][1]), s
     rep.ctx.destroy()
     R.ctx.destroy()
+
+
+@pytest.mark.parametrize("d,slots,share", [(4, 2, 0.5), (8, 1, 0.25), (2, 2, 0.9)])
+def test_was_hybrid_fetch(P, d, slots, share):
+    """Hybrid fetch (sidp_config.fetch_ce_share): the copy engine writes a prefix of every layer,
+    the SM kernel the rest, both counted into the same fill epoch.  One computing rank beside
+    serve-only owners, CUDA-graph steps and an eager step with logits: BITWISE equal to the
+    replicated run; the device fetch log equals the oracle FIFO schedule."""
+    m = MODELS["tiny"].with_layers(8)
+    B = 5
+    G = Rank(P, m, rank=0, world=d, B=B, slots=slots, fetch_ce_share=share)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=80, seed=SEED, alloc=False)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    G.ctx.import_handles([G.ctx.export_handles()] + [c.export_handles() for c in peers])
+    toks = []
+    for s in range(4):
+        with torch.cuda.stream(G.stream):
+            G.ctx.step(G.toks, G.toks, G.kv, batch=B, stream=G.stream, advance_pos=True)
+        G.stream.synchronize()
+        toks.append(G.toks.clone().cpu())
+    G.step(); G.finish_step()
+    st = G.ctx.stats()
+    assert st["timeouts"] == 0
+    pl = OS.plan(OS.owner_map(m.num_layers, d), d, 0, "exec")
+    log = G.ctx.fetch_log()
+    assert len(log) >= 5 * len(pl)
+    assert log == OS.slot_schedule(pl, slots, 8)[:len(log)]
+    budget = st["compute_sms"]
+    for c in peers:
+        c.destroy()
+    G.ctx.destroy()
+    rep = Rank(P, m, B=B, compute_sms=budget)
+    for s in range(4):
+        with torch.cuda.stream(rep.stream):
+            rep.ctx.step(rep.toks, rep.toks, rep.kv, batch=B, stream=rep.stream, advance_pos=True)
+        rep.stream.synchronize()
+        assert torch.equal(rep.toks.cpu(), toks[s]), s
+    rep.step(); rep.finish_step()
+    assert torch.equal(rep.history[0][1], G.history[0][1])
+    rep.ctx.destroy()

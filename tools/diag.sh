@@ -1,4 +1,3 @@
-export SIDP_CAS_TIMEOUT_MS=3000
-timeout 120 python tools/ring_diag.py --layers 16 --steps 6 > gpurun_out/rd_graph.log 2>&1; echo "graph rc=$?"; tail -50 gpurun_out/rd_graph.log
-SIDP_GRAPH=0 timeout 120 python tools/ring_diag.py --layers 16 --steps 6 > gpurun_out/rd_eager.log 2>&1; echo "eager rc=$?"; tail -12 gpurun_out/rd_eager.log
-timeout 120 python tools/ring_diag.py --layers 16 --steps 6 --sync-each > gpurun_out/rd_graph_sync.log 2>&1; echo "graph_sync rc=$?"; tail -30 gpurun_out/rd_graph_sync.log
+export SIDP_CAS_TIMEOUT_MS=5000
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "hybrid or serve_only or windowed" 2>&1 | tail -2
+timeout 240 python bench.py --emulate-only --workload M3 --alias-owners --emulate-batch 1024 --emulate-ctx 384 --emulate-ce-share 0.3 --emulate-fetch-sms 12 --emulate-steps 2 > gpurun_out/hy_m3.log 2>&1; echo "m3 rc=$?"; grep -o '"ms_per_step": [0-9.]*\|"frac_T2": [0-9.]*\|"GBps": [0-9.]*\|Error.*' gpurun_out/hy_m3.log | head -5

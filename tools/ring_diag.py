@@ -26,13 +26,14 @@ ap.add_argument("--steps", type=int, default=6)
 ap.add_argument("--world", type=int, default=8)
 ap.add_argument("--pace", type=float, default=770.0)
 ap.add_argument("--sync-each", action="store_true")
+ap.add_argument("--ce-share", type=float, default=0.0)
 a = ap.parse_args()
 
 m = MODELS[a.model].with_layers(a.layers)
 seed, B, W = 20261017, a.batch, a.world
 max_ctx = a.ctx + a.steps + 8
 ctx0 = P.Context(m, rank=0, world=W, slots=2, max_batch=B, max_ctx=max_ctx, fetch_sms=16,
-                 fetch_engine="sm", seed=seed, fetch_pace_gbps=a.pace)
+                 fetch_engine="sm", seed=seed, fetch_pace_gbps=a.pace, fetch_ce_share=a.ce_share)
 peers = []
 for r in range(1, W):
     c = P.Context(m, rank=r, world=W, max_batch=B, max_ctx=max_ctx, seed=seed, alloc=False)
