@@ -91,7 +91,9 @@ def test_custom_owner_map_and_rejections(sidp):
     bad = [dict(layer_owner=[0, 1, 2, 0]), dict(slots=0), dict(rank=2), dict(max_batch=0),
            dict(slot_parts=3),                              # granularity: 0, 1 or 2
            dict(slot_parts=2, fetch_engine="ce"),           # tiles live in the SM fetch's device ring
-           dict(slot_parts=2, slots=5)]                     # 5 slots x 4 parts > 16 ring entries
+           dict(slot_parts=2, slots=5),                     # 5 slots x 4 parts > 16 ring entries
+           dict(fetch_ce_share=1.0), dict(fetch_ce_share=-0.1),   # copy-engine share in [0, 1)
+           dict(fetch_ce_share=0.3, slot_parts=2)]          # the hybrid fetch needs whole layers
     for kw in bad:
         kw = {"rank": 0, "world": 2, **kw}
         with pytest.raises(sidp.SidpError) as e:
