@@ -336,8 +336,10 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.emulate_steps):
             step()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.emulate_steps
         ev1.record(stream)
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1) / args.emulate_steps
@@ -369,6 +371,8 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
             "fetch_ce_share": args.emulate_ce_share,
             "steps": args.emulate_steps,
             "ms_per_step": ms, "tokens_s_rank": B / (ms / 1e3),
+            "host_enqueue_ms_per_step": host_ms,
+            "graph_replays_in_timed_steps": st["graph_replays"] - st0["graph_replays"],
             "group_tokens_s_est": W * B / (ms / 1e3),
             "remote_layers_per_step": remote_layers, "layer_bytes": lb,
             "fetch_bytes_per_step": remote_layers * lb,
@@ -694,7 +698,8 @@ def main():
 
     # ---------------- timed region (device-side, CUDA events, max over ranks)
     ctx.set_timing(1 << dom)
-    launches0 = ctx.stats()["launches"]
+    st_pre = ctx.stats()
+    launches0, replays0 = st_pre["launches"], st_pre["graph_replays"]
     pos_before = kv.max_pos
     if dist:
         dist.barrier()
@@ -785,6 +790,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "graph_replays_in_timed_steps": st["graph_replays"] - replays0,
         "clocks": clocks,
         "per_gpu_tokens_s": value / world,
         "kernel_shares": kernel_shares,

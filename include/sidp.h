@@ -174,6 +174,7 @@ typedef struct {
   int32_t fetch_sms_held;   /* SMs the SM fetch kernel holds (0: copy engine, or no remote layer) */
   int32_t compute_sms;      /* SMs the WaS compute grids are sized for (0 = all) */
   double stagger_tick_ns;   /* measured single-reader layer fetch (C-S7 tick; 0 = not measured) */
+  uint64_t graph_replays;   /* sidp_step calls that replayed a captured CUDA graph */
 } sidp_stats_t;
 
 /* ---- lifecycle --------------------------------------------------------------------- */

@@ -56,7 +56,8 @@ class Stats(C.Structure):
                 ("slot_bytes", C.c_uint64), ("replicated_bytes", C.c_uint64),
                 ("workspace_bytes", C.c_uint64), ("timed_ms", C.c_double * 8),
                 ("timed_launches", C.c_uint64 * 8), ("fetch_sms_held", C.c_int32),
-                ("compute_sms", C.c_int32), ("stagger_tick_ns", C.c_double)]
+                ("compute_sms", C.c_int32), ("stagger_tick_ns", C.c_double),
+                ("graph_replays", C.c_uint64)]
 
 
 _P = C.c_void_p

@@ -2136,6 +2136,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
     const bool fresh = ctx->graph_fresh;
     ctx->graph_fresh = false;
     CK(cudaGraphLaunch(ctx->gexec, s));
+    ctx->st.graph_replays++;
     if (!fresh && ctx->R > 0) {
       st = replay_bookkeeping(ctx);
       if (st != SIDP_OK) return st;
