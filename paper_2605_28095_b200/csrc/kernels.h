@@ -86,6 +86,15 @@ struct RowScatter {
   void* base[16];
 };
 
+// Flags a grid posts once ALL its CTAs' stores are done (the last CTA to finish releases them at
+// system scope): the CaS owner's done + served flags ride on its last GEMM instead of a launch.
+struct PostFlags {
+  uint64_t* flag[17];
+  int n;
+  uint64_t value;
+  unsigned int* counter;       // last-CTA election (0 between launches)
+};
+
 struct GemmArgs {
   const bf16* x; int ldx;      // [M, K]
   const bf16* w; int ldw;      // [N, K]
@@ -102,6 +111,7 @@ struct GemmArgs {
   PartialSrc* partial_out;     // EPI_PARTIAL: receives the slice geometry for the consumer
   const FlagWait* wait;        // optional: the activation loads wait for these flags (CaS owner)
   const RowScatter* scatter;   // optional (EPI_F32 / EPI_BF16 / EPI_RESID): output rows -> peers
+  const PostFlags* post;       // optional: posted by the last CTA of the GEMM's last launch
 };
 
 struct GemmWorkspace {

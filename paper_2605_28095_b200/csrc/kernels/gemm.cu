@@ -62,7 +62,22 @@ struct KParams {
   QkvEpi qkv;                   // EPI_QKV destination
   FlagWait wait;                // CaS owner: activation loads wait for the arrival flags
   RowScatter scatter;           // CaS owner: output rows straight into the requesters' buffers
+  PostFlags post;               // CaS owner: done + served, posted by this launch's last CTA
 };
+
+// After every thread of this CTA finished its stores: the last CTA of the grid posts the flags
+// (gpu-scope election, cumulative sys-scope releases; see atom_add_acq_rel_gpu).
+SIDP_DEV void post_after_grid(const PostFlags& f) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned prev = atom_add_acq_rel_gpu(f.counter, 1u);
+    if (prev == total - 1) {
+      *f.counter = 0u;
+      for (int i = 0; i < f.n; ++i) st_release_sys(f.flag[i], f.value);
+    }
+  }
+}
 
 // Base of output row m (elements of size ES): out + m * ldo, or the requester's receive buffer
 // holding fused row m (CaS scatter; rows of one requester are contiguous in both).
@@ -817,15 +832,14 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     tmem_dealloc2(tmem_base, tmem_cols);
   }
   if (threadIdx.x == 0) SIDP_TL(6);
+  if (p.post.n) post_after_grid(p.post);
 }
 
 // Stream-K fix-up over all SMs: for tiles covered by several k-range segments, each thread sums
 // 8 consecutive outputs of one token row across the segment slices in order 0..nseg-1
 // (deterministic), then applies EPI.  Tiles finished inside the GEMM are skipped.
 template <int EPI>
-__global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
-  pdl_trigger();
-  pdl_wait();
+SIDP_DEV void reduce_body(const KParams& p) {
   // blockIdx.y = cluster boundary c (1..C-1); the tile containing b_c strictly inside is fixed
   // up by the block row of the first boundary that splits it.
   const long long nkb = p.nks;
@@ -913,6 +927,14 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
           pack_bf16x8(a);
     }
   }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_reduce_kernel(const KParams p) {
+  pdl_trigger();
+  pdl_wait();
+  reduce_body<EPI>(p);
+  if (p.post.n) post_after_grid(p.post);
 }
 
 // ---------------------------------------------------------------- fused MLP (gate/up -> down)
@@ -1573,6 +1595,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.w_evict = env_evict && (sw ? n_pairs == 1 : m_tiles == 1);
   if (a.qkv) p.qkv = *a.qkv;
   if (a.wait) p.wait = *a.wait;
+  const PostFlags* post = a.post && a.post->n > 0 ? a.post : nullptr;
   if (a.scatter) {
     if (a.epi != EPI_F32 && a.epi != EPI_BF16 && a.epi != EPI_RESID) return cudaErrorInvalidValue;
     p.scatter = *a.scatter;
@@ -1589,6 +1612,8 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   }
   const size_t smem = stages * stage_bytes + extra + 1024;
   dim3 grid(2 * clusters);
+  const bool reduce_follows = streamk && !part;
+  if (post && !reduce_follows) p.post = *post;   // this launch is the last: it posts
   cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
   switch (a.epi) {
     case EPI_F32: e0 = launch_gemm2<EPI_F32>(kps, sw, grid, smem, stream, tw, tx, p); break;
@@ -1637,6 +1662,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   }
   if (e0 != cudaSuccess || !streamk || part) return e0;
   g_last_launches = 2;
+  if (post) p.post = *post;   // the fix-up is the last launch: it posts
   dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, clusters - 1));
   switch (a.epi) {
     case EPI_F32: e1 = launch_pdl(gemm_reduce_kernel<EPI_F32>, rgrid, dim3(256), 0, stream, p); break;

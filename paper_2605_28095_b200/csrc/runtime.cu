@@ -423,10 +423,11 @@ cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, in
                  int epi, void* out, int ldo, const bf16* resid, int ldr, const bf16* bias,
                  cudaStream_t s, const sidp::QkvEpi* qkv = nullptr,
                  sidp::PartialSrc* partial = nullptr, const sidp::FlagWait* wait = nullptr,
-                 const sidp::RowScatter* scatter = nullptr) {
+                 const sidp::RowScatter* scatter = nullptr, const sidp::PostFlags* post = nullptr) {
   sidp::GemmArgs a{};
   a.wait = wait;
   a.scatter = scatter;
+  a.post = post;
   a.x = x; a.ldx = ldx; a.w = w; a.ldw = K; a.M = M; a.N = N; a.K = K; a.epi = epi;
   a.out = out; a.ldo = ldo; a.resid = resid; a.ldr = ldr; a.bias = bias; a.qkv = qkv;
   a.partial_out = partial;
@@ -554,7 +555,8 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
 sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf16* x, int ldx,
                      bf16* out, int B, cudaStream_t s, const bf16* next_g = nullptr,
                      int next_layer = -1, const sidp::FlagWait* wait = nullptr,
-                     const sidp::RowScatter* scatter = nullptr) {
+                     const sidp::RowScatter* scatter = nullptr,
+                     const sidp::PostFlags* post = nullptr) {
   const auto& m = ctx->m;
   const int h = m.hidden;
   // x2 = x + o W_o^T  (into out), u2 = RMSNorm(x2) * g_mlp
@@ -614,7 +616,7 @@ sidp_status mlp_part(sidp_ctx* ctx, const LayerW& W, const bf16* o, int ldo_, bf
     ctx->u_for = next_layer;
   } else {
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, B, h, m.intermediate, sidp::EPI_RESID, out, h,
-            out, h, nullptr, s, nullptr, nullptr, nullptr, scatter));
+            out, h, nullptr, s, nullptr, nullptr, nullptr, scatter, post));
     CK(ring_release(ctx, C_WD, s));
   }
   return SIDP_OK;
@@ -1162,17 +1164,16 @@ sidp::RowScatter cas_row_scatter(sidp_ctx* ctx, const CasTrip& t) {
   return sc;
 }
 
-// owner, after a scattering GEMM: done for every live rank + served (one tiny launch)
-sidp_status cas_post(sidp_ctx* ctx, const CasTrip& t, cudaStream_t s) {
-  sidp::XferSet xs{};
+// owner: done for every live rank + served, posted by the last CTA of the scattering GEMM's last
+// launch (no flag launch)
+sidp::PostFlags cas_post_flags(sidp_ctx* ctx, const CasTrip& t) {
+  sidp::PostFlags pf{};
   for (int q = 0; q < ctx->d; ++q)
-    if (ctx->batches[q] > 0) xs.flag[xs.nflags++] = flag_ptr(ctx->peer_cas[q], flag_off_done(ctx->d));
-  xs.flag[xs.nflags++] = flag_ptr(ctx->cas, flag_off_served(ctx->d));
-  xs.value = (uint64_t)t.rt + 1;
-  xs.counter = ctx->xfer_cnt;
-  CK(sidp::xfer_launch(xs, s));
-  count_launch(ctx);
-  return SIDP_OK;
+    if (ctx->batches[q] > 0) pf.flag[pf.n++] = flag_ptr(ctx->peer_cas[q], flag_off_done(ctx->d));
+  pf.flag[pf.n++] = flag_ptr(ctx->cas, flag_off_served(ctx->d));
+  pf.value = (uint64_t)t.rt + 1;
+  pf.counter = ctx->xfer_cnt;
+  return pf;
 }
 
 // owner: every live rank's slice of `result` back to its receive buffer, then done + served
@@ -1236,13 +1237,15 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       if (st != SIDP_OK) return st;
       const bf16* stage = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t1.slot, 0));
       const sidp::RowScatter sc = cas_row_scatter(ctx, t1);
+      const sidp::PostFlags pf = cas_post_flags(ctx, t1);
       CK(gemm(ctx, 5, stage, ctx->stage_width, W.wqkv, t1.total, ctx->qkvdim, h, sidp::EPI_F32,
               ctx->qkv, ctx->qkvdim, nullptr, 0, W.b_qkv, s, nullptr, nullptr, w.n ? &w : nullptr,
-              cas_scatter() ? &sc : nullptr));
-      st = cas_scatter() ? cas_post(ctx, t1, s)
-                         : cas_return(ctx, t1, reinterpret_cast<const uint8_t*>(ctx->qkv),
-                                      (size_t)ctx->qkvdim * 4, (size_t)ctx->qkvdim * 4, s);
-      if (st != SIDP_OK) return st;
+              cas_scatter() ? &sc : nullptr, cas_scatter() ? &pf : nullptr));
+      if (!cas_scatter()) {
+        st = cas_return(ctx, t1, reinterpret_cast<const uint8_t*>(ctx->qkv), (size_t)ctx->qkvdim * 4,
+                        (size_t)ctx->qkvdim * 4, s);
+        if (st != SIDP_OK) return st;
+      }
     }
     CasTrip t2 = cas_trip(ctx, layer);
     if (B > 0) {   // RoPE, KV append and attention stay local (the KV cache is local)
@@ -1265,13 +1268,16 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       const bf16* st_o = reinterpret_cast<const bf16*>(cas_stage_ptr(ctx, ctx->cas, t2.slot, 0));
       bf16* st_x = reinterpret_cast<bf16*>(cas_stage_ptr(ctx, ctx->cas, t1.slot, 0)) + h;
       const sidp::RowScatter sc = cas_row_scatter(ctx, t2);
+      const sidp::PostFlags pf = cas_post_flags(ctx, t2);
       st = mlp_part(ctx, W, st_o, ctx->stage_width, st_x, ctx->stage_width, ctx->cas_out, t2.total,
-                    s, nullptr, -1, w.n ? &w : nullptr, cas_scatter() ? &sc : nullptr);
+                    s, nullptr, -1, w.n ? &w : nullptr, cas_scatter() ? &sc : nullptr,
+                    cas_scatter() ? &pf : nullptr);
       if (st != SIDP_OK) return st;
-      st = cas_scatter() ? cas_post(ctx, t2, s)
-                         : cas_return(ctx, t2, reinterpret_cast<const uint8_t*>(ctx->cas_out),
-                                      (size_t)h * 2, (size_t)h * 2, s);
-      if (st != SIDP_OK) return st;
+      if (!cas_scatter()) {
+        st = cas_return(ctx, t2, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
+                        (size_t)h * 2, s);
+        if (st != SIDP_OK) return st;
+      }
     }
     ctx->last_rt_any[o] = t2.rt;
     ctx->st.cas_round_trips += 2;
@@ -1305,13 +1311,15 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
             sidp::EPI_SILU_MUL, ctx->act, m.intermediate, nullptr, 0, nullptr, s, nullptr, nullptr,
             w.n ? &w : nullptr));
     const sidp::RowScatter sc = cas_row_scatter(ctx, t);
+    const sidp::PostFlags pf = cas_post_flags(ctx, t);
     CK(gemm(ctx, 4, ctx->act, m.intermediate, W.wd, t.total, h, m.intermediate, sidp::EPI_RESID,
             ctx->cas_out, h, stage + h, ctx->stage_width, nullptr, s, nullptr, nullptr, nullptr,
-            cas_scatter() ? &sc : nullptr));
-    st = cas_scatter() ? cas_post(ctx, t, s)
-                       : cas_return(ctx, t, reinterpret_cast<const uint8_t*>(ctx->cas_out),
-                                    (size_t)h * 2, (size_t)h * 2, s);
-    if (st != SIDP_OK) return st;
+            cas_scatter() ? &sc : nullptr, cas_scatter() ? &pf : nullptr));
+    if (!cas_scatter()) {
+      st = cas_return(ctx, t, reinterpret_cast<const uint8_t*>(ctx->cas_out), (size_t)h * 2,
+                      (size_t)h * 2, s);
+      if (st != SIDP_OK) return st;
+    }
   }
   ctx->last_rt_any[o] = t.rt;
   ctx->st.cas_round_trips++;
