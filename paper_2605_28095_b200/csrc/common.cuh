@@ -170,8 +170,14 @@ SIDP_DEV uint64_t globaltimer_ns() {
 }
 // Spin until every *p[i] >= value (system-scope acquire), bounded by timeout_ns per flag; on a
 // timeout *err (a mapped host word) is set and the wait gives up (SIDP_ETIMEOUT at the host).
+// base (optional): the flag values are relative to *base (a device round-trip counter advanced
+// per CaS step), so a captured CUDA graph replays with step-invariant parameters.
+SIDP_DEV uint64_t flag_value(uint64_t value, const uint64_t* base) {
+  return base ? value + *reinterpret_cast<const volatile uint64_t*>(base) : value;
+}
 SIDP_DEV void flags_wait(const uint64_t* const* p, int n, uint64_t value, uint64_t timeout_ns,
-                         int* err) {
+                         int* err, const uint64_t* base = nullptr) {
+  value = flag_value(value, base);
   for (int i = 0; i < n; ++i) {
     if (ld_acquire_sys(p[i]) >= value) continue;
     const uint64_t t0 = globaltimer_ns();

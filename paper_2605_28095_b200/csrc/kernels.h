@@ -75,6 +75,7 @@ struct FlagWait {
   uint64_t value;
   uint64_t timeout_ns;
   int* err;
+  const uint64_t* base;        // optional: value is relative to *base (CaS graph replay)
 };
 
 // CaS owner: the GEMM's output rows scattered straight into the requesters'
@@ -93,6 +94,7 @@ struct PostFlags {
   int n;
   uint64_t value;
   unsigned int* counter;       // last-CTA election (0 between launches)
+  const uint64_t* base;        // optional: value is relative to *base
 };
 
 struct GemmArgs {
@@ -181,6 +183,7 @@ struct CasSendArgs {
   FlagWait wait;               // owner's previous round trip served
   uint64_t* arrive; uint64_t value;
   unsigned int* counter;       // last-CTA election (0 between launches)
+  const uint64_t* base;        // optional: value (and wait.value via wait.base) relative to *base
 };
 cudaError_t cas_send_norm_launch(const CasSendArgs& a, cudaStream_t s);
 // qkv fp32 [B, (nq+2nkv)*hd] -> q bf16 [B, nq, hd]; k, v appended to caches at pos[b]
@@ -327,9 +330,12 @@ struct FlagSet {
   uint64_t* p[16];
   int n;
 };
-cudaError_t signal_launch(uint64_t* flag, uint64_t value, cudaStream_t s);
+cudaError_t signal_launch(uint64_t* flag, uint64_t value, cudaStream_t s,
+                          const uint64_t* base = nullptr);
 cudaError_t wait_launch(const FlagSet& flags, uint64_t value, uint64_t timeout_ns, int* err,
-                        cudaStream_t s);
+                        cudaStream_t s, const uint64_t* base = nullptr);
+// *base += delta (the CaS round-trip counter of a step; first kernel of a CaS step)
+cudaError_t base_add_launch(uint64_t* base, uint64_t delta, cudaStream_t s);
 cudaError_t copy_rows_launch(void* dst, int ldd, const void* src, int lds, int rows, int row_bytes,
                              cudaStream_t s);
 // Fused CaS transfer ("V2": fewer, fused transfer launches): copy every job's

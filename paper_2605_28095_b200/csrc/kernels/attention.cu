@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256, 2) qkv_post_kernel(QkvPostArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nh = a.nq + 2 * a.nkv;
   if (a.wait.n) {   // CaS: the owner's returned qkv rows have landed (done flag)
-    if (threadIdx.x == 0) flags_wait(a.wait.p, a.wait.n, a.wait.value, a.wait.timeout_ns, a.wait.err);
+    if (threadIdx.x == 0) flags_wait(a.wait.p, a.wait.n, a.wait.value, a.wait.timeout_ns, a.wait.err, a.wait.base);
     __syncthreads();
   }
   const size_t ldqkv = a.ldqkv > 0 ? (size_t)a.ldqkv : (size_t)nh * HD;

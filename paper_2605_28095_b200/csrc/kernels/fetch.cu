@@ -68,13 +68,18 @@ __global__ void delay_kernel(uint64_t ns) {
 }
 
 // Post a flag after all prior work of this stream (kernel boundary orders the data).
-__global__ void signal_kernel(uint64_t* flag, uint64_t value) {
-  st_release_sys(flag, value);   // the stream's earlier kernels completed: their stores performed
+__global__ void signal_kernel(uint64_t* flag, uint64_t value, const uint64_t* base) {
+  // the stream's earlier kernels completed: their stores performed
+  st_release_sys(flag, flag_value(value, base));
 }
+
+__global__ void base_add_kernel(uint64_t* base, uint64_t delta) { *base += delta; }
 
 // Wait until every flag >= value (system-scope acquire); bounded by timeout_ns, after
 // which *err is set and the kernel returns (surfaced as SIDP_ETIMEOUT by the host).
-__global__ void wait_kernel(const FlagSet flags, uint64_t value, uint64_t timeout_ns, int* err) {
+__global__ void wait_kernel(const FlagSet flags, uint64_t value, uint64_t timeout_ns, int* err,
+                            const uint64_t* base) {
+  value = flag_value(value, base);
   const int i = threadIdx.x;
   if (i < flags.n) {
     const uint64_t t0 = globaltimer_ns();
@@ -104,7 +109,7 @@ __global__ void copy_rows_kernel(uint8_t* dst, int ldd, const uint8_t* src, int 
 // every CTA waits for the flags (thread 0, acquire), then copies its rows
 __global__ void wait_copy_kernel(const FlagWait w, uint8_t* dst, int ldd, const uint8_t* src,
                                  int lds, int rows, int row_bytes) {
-  if (threadIdx.x == 0) flags_wait(w.p, w.n, w.value, w.timeout_ns, w.err);
+  if (threadIdx.x == 0) flags_wait(w.p, w.n, w.value, w.timeout_ns, w.err, w.base);
   __syncthreads();
   const int nvec = row_bytes / 16;
   for (int r = blockIdx.y; r < rows; r += gridDim.y) {
@@ -162,16 +167,21 @@ cudaError_t delay_launch(uint64_t ns, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t signal_launch(uint64_t* flag, uint64_t value, cudaStream_t s) {
-  signal_kernel<<<1, 1, 0, s>>>(flag, value);
+cudaError_t signal_launch(uint64_t* flag, uint64_t value, cudaStream_t s, const uint64_t* base) {
+  signal_kernel<<<1, 1, 0, s>>>(flag, value, base);
+  return cudaGetLastError();
+}
+
+cudaError_t base_add_launch(uint64_t* base, uint64_t delta, cudaStream_t s) {
+  base_add_kernel<<<1, 1, 0, s>>>(base, delta);
   return cudaGetLastError();
 }
 
 cudaError_t wait_launch(const FlagSet& flags, uint64_t value, uint64_t timeout_ns, int* err,
-                        cudaStream_t s) {
+                        cudaStream_t s, const uint64_t* base) {
   if (flags.n <= 0) return cudaSuccess;
   if (flags.n > 16) return cudaErrorInvalidValue;
-  wait_kernel<<<1, 32, 0, s>>>(flags, value, timeout_ns, err);
+  wait_kernel<<<1, 32, 0, s>>>(flags, value, timeout_ns, err, base);
   return cudaGetLastError();
 }
 
@@ -244,6 +254,7 @@ cudaError_t fetch_preload() {
   if (cudaFuncGetAttributes(&fa, pace_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, signal_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, wait_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, base_add_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, copy_rows_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, xfer_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, wait_copy_kernel) != cudaSuccess) e = cudaGetLastError();

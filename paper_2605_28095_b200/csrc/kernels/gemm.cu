@@ -74,7 +74,8 @@ SIDP_DEV void post_after_grid(const PostFlags& f) {
     const unsigned prev = atom_add_acq_rel_gpu(f.counter, 1u);
     if (prev == total - 1) {
       *f.counter = 0u;
-      for (int i = 0; i < f.n; ++i) st_release_sys(f.flag[i], f.value);
+      const uint64_t v = flag_value(f.value, f.base);
+      for (int i = 0; i < f.n; ++i) st_release_sys(f.flag[i], v);
     }
   }
 }
@@ -637,7 +638,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
       }
       pdl_wait();
-      if (p.wait.n) flags_wait(p.wait.p, p.wait.n, p.wait.value, p.wait.timeout_ns, p.wait.err);
+      if (p.wait.n) flags_wait(p.wait.p, p.wait.n, p.wait.value, p.wait.timeout_ns, p.wait.err, p.wait.base);
       for (int it = 0; cur.valid; cur.advance(p, cluster), ++it) {
         const int s = it % stages;
         const uint32_t ph = (it / stages) & 1;

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSe
   pdl_trigger();
   pdl_wait();
   if (a.wait.n) {   // the owner served its previous round trip: its staging slots are free
-    if (threadIdx.x == 0) flags_wait(a.wait.p, a.wait.n, a.wait.value, a.wait.timeout_ns, a.wait.err);
+    if (threadIdx.x == 0) flags_wait(a.wait.p, a.wait.n, a.wait.value, a.wait.timeout_ns, a.wait.err, a.wait.base);
     __syncthreads();
   }
   const int h = a.h, nvec = h / 8;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kNormThreads) cas_send_norm_kernel(const CasSe
     const unsigned prev = atom_add_acq_rel_gpu(a.counter, 1u);
     if (prev == gridDim.x - 1) {
       *a.counter = 0u;
-      st_release_sys(a.arrive, a.value);
+      st_release_sys(a.arrive, flag_value(a.value, a.base));
     }
   }
 }

@@ -149,6 +149,15 @@ struct sidp_ctx {
   int64_t rt = 0;                  // CaS round-trip counter (identical on all ranks)
   std::vector<std::vector<int64_t>> last_rt;   // [owner][slot] last served round trip
   std::vector<int64_t> last_rt_any;             // [owner] last round trip with that owner (V3)
+  // CaS flag values relative to a device round-trip counter (sidp_step, V3): rel while a step's
+  // kernels are enqueued, rt0 = the host round-trip count at the step's start, which the step's
+  // first kernel makes the device counter (rt_base_host tracks what it holds after enqueued work)
+  uint64_t* rt_base_dev = nullptr;
+  int64_t rt_base_host = 0;
+  bool rel = false;
+  int64_t rt0 = 0;
+  std::vector<int> gbatches;                    // CaS graph key: the batches and base delta captured
+  int64_t gdelta = -1;
   bool same_device_peer = false;                // a peer shares this GPU (virtual ranks / 1-GPU IPC)
   bool arena_borrowed = false;                  // serve-only alias: the arena is another ctx's
   // WaS schedule state
@@ -943,7 +952,7 @@ sidp_status consumer_wait(sidp_ctx* ctx, sidp::FlagWait& w, cudaStream_t s) {
   sidp::FlagSet fs{};
   for (int i = 0; i < w.n; ++i) fs.p[i] = const_cast<uint64_t*>(w.p[i]);
   fs.n = w.n;
-  CK(sidp::wait_launch(fs, w.value, w.timeout_ns, w.err, s));
+  CK(sidp::wait_launch(fs, w.value, w.timeout_ns, w.err, s, w.base));
   count_launch(ctx);
   w.n = 0;
   return SIDP_OK;
@@ -1097,6 +1106,12 @@ CasTrip cas_trip(sidp_ctx* ctx, int layer) {
   return t;
 }
 
+// a flag value for round trip `abs` + 1 etc.: absolute, or relative to the step's device base
+uint64_t fv(const sidp_ctx* ctx, int64_t abs_value) {
+  return ctx->rel ? (uint64_t)(abs_value - ctx->rt0) : (uint64_t)abs_value;
+}
+const uint64_t* fb(const sidp_ctx* ctx) { return ctx->rel ? ctx->rt_base_dev : nullptr; }
+
 uint8_t* cas_stage_ptr(const sidp_ctx* ctx, uint8_t* cas_base, int slot, int row) {
   return cas_base + ctx->cas_stage_off + (size_t)slot * ctx->cas_stage_bytes +
          (size_t)row * ctx->stage_width * 2;
@@ -1107,17 +1122,19 @@ sidp::FlagWait arrivals_wait(sidp_ctx* ctx, int64_t rt) {
   sidp::FlagWait w{};
   for (int q = 0; q < ctx->d; ++q)
     if (ctx->batches[q] > 0) w.p[w.n++] = flag_ptr(ctx->cas, flag_off_arrive(q));
-  w.value = (uint64_t)rt + 1;
+  w.value = fv(ctx, rt + 1);
+  w.base = fb(ctx);
   w.timeout_ns = ctx->cas_timeout_ns;
   w.err = ctx->dev_err;
   return w;
 }
 
-sidp::FlagWait single_wait(sidp_ctx* ctx, const uint64_t* flag, uint64_t value) {
+sidp::FlagWait single_wait(sidp_ctx* ctx, const uint64_t* flag, int64_t abs_value) {
   sidp::FlagWait w{};
   w.p[0] = flag;
   w.n = 1;
-  w.value = value;
+  w.value = fv(ctx, abs_value);
+  w.base = fb(ctx);
   w.timeout_ns = ctx->cas_timeout_ns;
   w.err = ctx->dev_err;
   return w;
@@ -1134,11 +1151,12 @@ sidp_status cas_send(sidp_ctx* ctx, const CasTrip& t, const bf16* x, const bf16*
   a.ldd = ctx->stage_width;
   if (ctx->last_rt_any[t.o] >= 0)
     a.wait = single_wait(ctx, flag_ptr(owner_cas, flag_off_served(ctx->d)),
-                         (uint64_t)ctx->last_rt_any[t.o] + 1);
+                         ctx->last_rt_any[t.o] + 1);
   sidp_status st = consumer_wait(ctx, a.wait, s);
   if (st != SIDP_OK) return st;
   a.arrive = flag_ptr(owner_cas, flag_off_arrive(me));
-  a.value = (uint64_t)t.rt + 1;
+  a.value = fv(ctx, t.rt + 1);
+  a.base = fb(ctx);
   a.counter = ctx->xfer_cnt;
   CK(sidp::cas_send_norm_launch(a, s));
   count_launch(ctx);
@@ -1171,7 +1189,8 @@ sidp::PostFlags cas_post_flags(sidp_ctx* ctx, const CasTrip& t) {
   for (int q = 0; q < ctx->d; ++q)
     if (ctx->batches[q] > 0) pf.flag[pf.n++] = flag_ptr(ctx->peer_cas[q], flag_off_done(ctx->d));
   pf.flag[pf.n++] = flag_ptr(ctx->cas, flag_off_served(ctx->d));
-  pf.value = (uint64_t)t.rt + 1;
+  pf.value = fv(ctx, t.rt + 1);
+  pf.base = fb(ctx);
   pf.counter = ctx->xfer_cnt;
   return pf;
 }
@@ -1196,7 +1215,7 @@ sidp_status cas_return(sidp_ctx* ctx, const CasTrip& t, const uint8_t* result, s
 }
 
 // requester: the owner's returned rows -> x once done >= value (one launch with prologue waits)
-sidp_status cas_copy_back(sidp_ctx* ctx, const uint64_t* done, uint64_t value, bf16* x,
+sidp_status cas_copy_back(sidp_ctx* ctx, const uint64_t* done, int64_t value, bf16* x,
                           const uint8_t* recv, int B, cudaStream_t s) {
   const int h = ctx->m.hidden;
   sidp::FlagWait w = single_wait(ctx, done, value);
@@ -1249,7 +1268,7 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
     }
     CasTrip t2 = cas_trip(ctx, layer);
     if (B > 0) {   // RoPE, KV append and attention stay local (the KV cache is local)
-      sidp::FlagWait dw = single_wait(ctx, done, (uint64_t)t1.rt + 1);
+      sidp::FlagWait dw = single_wait(ctx, done, t1.rt + 1);
       st = consumer_wait(ctx, dw, s);
       if (st != SIDP_OK) return st;
       AttnHooks hk;
@@ -1258,7 +1277,7 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
       hk.ldo_dst = ctx->stage_width;
       st = attn_part(ctx, W, x, B, layer, kv, reinterpret_cast<const float*>(recv), s, &hk);
       if (st != SIDP_OK) return st;
-      CK(sidp::signal_launch(flag_ptr(owner_cas, flag_off_arrive(me)), (uint64_t)t2.rt + 1, s));
+      CK(sidp::signal_launch(flag_ptr(owner_cas, flag_off_arrive(me)), fv(ctx, t2.rt + 1), s, fb(ctx)));
       count_launch(ctx);
     }
     if (o == me) {   // RT2: out = x2 + MLP(x2), x2 = x + o W_o^T, x from RT1's staging rows
@@ -1282,7 +1301,7 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
     ctx->last_rt_any[o] = t2.rt;
     ctx->st.cas_round_trips += 2;
     if (B > 0) {
-      st = cas_copy_back(ctx, done, (uint64_t)t2.rt + 1, x, recv, B, s);
+      st = cas_copy_back(ctx, done, t2.rt + 1, x, recv, B, s);
       if (st != SIDP_OK) return st;
     }
     return SIDP_OK;
@@ -1324,7 +1343,7 @@ sidp_status cas_layer_v3(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv
   ctx->last_rt_any[o] = t.rt;
   ctx->st.cas_round_trips++;
   if (B > 0) {
-    st = cas_copy_back(ctx, done, (uint64_t)t.rt + 1, x, recv, B, s);
+    st = cas_copy_back(ctx, done, t.rt + 1, x, recv, B, s);
     if (st != SIDP_OK) return st;
   }
   return SIDP_OK;
@@ -1517,7 +1536,8 @@ void sidp_destroy(sidp_ctx* ctx) {
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
-                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0, ctx->ring, ctx->ce_pace_t0};
+                    ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0, ctx->ring, ctx->ce_pace_t0,
+                    ctx->rt_base_dev};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (ctx->host_err) cudaFreeHost(const_cast<int*>(ctx->host_err));
@@ -1610,6 +1630,8 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
   }
   DM(ctx->pace_t0, sizeof(unsigned long long));
   DM(ctx->xfer_cnt, sizeof(unsigned int));
+  DM(ctx->rt_base_dev, sizeof(uint64_t));
+  CK(cudaMemset(ctx->rt_base_dev, 0, sizeof(uint64_t)));
   CK(cudaMemset(ctx->xfer_cnt, 0, sizeof(unsigned int)));
   CK(cudaStreamCreateWithFlags(&ctx->fetch_stream, cudaStreamNonBlocking));
   // WaS ring on the device (SIDP_FETCH_SM): epoch flags + logs; the fetch kernel's CTA pairs
@@ -1964,7 +1986,28 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
 }
 
 // Body of one decode step (enqueue only).
+static bool cas_relative(const sidp_ctx* ctx) {
+  return ctx->mode == SIDP_CAS && cas_level() >= 2 && cas_scatter();
+}
+
+static sidp_status step_body_inner(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s);
+
+// One decode step.  CaS (V3): the step's flag values are relative to the device round-trip
+// counter, which the step's first kernel advances to the host's count at the step start — so
+// the kernels' parameters repeat from step to step and the step replays as a CUDA graph.
 static sidp_status step_body(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s) {
+  if (!cas_relative(ctx)) return step_body_inner(ctx, b, s);
+  ctx->rt0 = ctx->rt;
+  CK(sidp::base_add_launch(ctx->rt_base_dev, (uint64_t)(ctx->rt0 - ctx->rt_base_host), s));
+  count_launch(ctx);
+  ctx->rt_base_host = ctx->rt0;
+  ctx->rel = true;
+  sidp_status st = step_body_inner(ctx, b, s);
+  ctx->rel = false;
+  return st;
+}
+
+static sidp_status step_body_inner(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s) {
   const int B = b->batch;
   const auto& m = ctx->m;
   sidp_status st;
@@ -2014,11 +2057,36 @@ static sidp_status step_body(sidp_ctx* ctx, const sidp_batch* b, cudaStream_t s)
 // the slot) and the remote layers consume the same slots as in the captured step; kernel
 // parameters never depend on the step index (positions live on the device).  The fetch stream
 // is never captured: its fetches are enqueued by the host pump around each replay.
+static int cas_rounds_per_step(const sidp_ctx* ctx) {
+  return ctx->c.pool_scope == SIDP_POOL_LAYER ? 2 * ctx->L : ctx->L;
+}
+
 static bool graph_eligible(const sidp_ctx* ctx, const sidp_batch* b) {
   static const bool enabled = !(getenv("SIDP_GRAPH") && atoi(getenv("SIDP_GRAPH")) == 0);
   const int mode = ctx->mode == SIDP_REPLICATED ? SIDP_WAS : ctx->mode;
-  return enabled && mode == SIDP_WAS && (ctx->R == 0 || (ctx->ring_mode && !ctx->stagger_pending)) &&
-         b->batch > 0 && !b->logits && !b->layer_inputs;
+  if (!enabled || b->batch <= 0 || b->logits || b->layer_inputs) return false;
+  if (mode == SIDP_CAS)   // step-relative flags; the staging slots repeat from step to step
+    return cas_relative(ctx) && cas_rounds_per_step(ctx) % ctx->c.cas_slots == 0;
+  return mode == SIDP_WAS && (ctx->R == 0 || (ctx->ring_mode && !ctx->stagger_pending));
+}
+
+// Host state a replayed CaS step advances (what cas_layer_v3 does while enqueueing).
+static void cas_replay_bookkeeping(sidp_ctx* ctx) {
+  int total = 0;
+  for (int q = 0; q < ctx->d; ++q) total += ctx->batches[q];
+  for (int l = 0; l < ctx->L; ++l) {
+    if (ctx->c.pool_scope == SIDP_POOL_LAYER) {
+      ctx->rt += 2;
+      if (total == 0) continue;
+      ctx->last_rt_any[ctx->owner[l]] = ctx->rt - 1;
+      ctx->st.cas_round_trips += 2;
+    } else {
+      ctx->rt += 1;
+      if (total == 0) continue;
+      ctx->last_rt_any[ctx->owner[l]] = ctx->rt - 1;
+      ctx->st.cas_round_trips += 1;
+    }
+  }
 }
 
 // Slots the remote layers of pass `ahead` (0 = the coming step) consume (FIFO recurrence).
@@ -2056,9 +2124,11 @@ static void graph_drop(sidp_ctx* ctx) {
 
 static bool graph_key_matches(const sidp_ctx* ctx, const sidp_batch* b) {
   const auto& k = ctx->gkey;
+  const bool cas_ok = ctx->mode != SIDP_CAS ||
+                      (ctx->gbatches == ctx->batches && ctx->gdelta == ctx->rt - ctx->rt_base_host);
   return ctx->gexec && k.batch == b->batch && k.tokens == b->tokens && k.next == b->next &&
          k.k_cache == b->kv.k_cache && k.v_cache == b->kv.v_cache && k.pos == b->kv.pos &&
-         k.pos_out == b->pos_out && ctx->gmask == ctx->timed_mask;
+         k.pos_out == b->pos_out && ctx->gmask == ctx->timed_mask && cas_ok;
 }
 
 sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
@@ -2100,7 +2170,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
   }
   std::vector<int> slots_now;
   bool replayable = s != nullptr && graph_eligible(ctx, b);   // capture needs a non-default stream
-  if (replayable && ctx->R > 0) {
+  if (replayable && ctx->R > 0 && ctx->mode != SIDP_CAS) {
     slots_now = coming_slots(ctx, 0);
     // capture only a step whose successor consumes the same slots (else eager every step)
     if (!(ctx->gexec && ctx->gslots == slots_now) && slots_now != coming_slots(ctx, 1))
@@ -2113,6 +2183,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
       const uint64_t l0 = ctx->st.launches;
       uint64_t t0[8];
       for (int i = 0; i < 8; ++i) t0[i] = ctx->st.timed_launches[i];
+      const int64_t cas_delta = ctx->rt - ctx->rt_base_host;
       CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       ctx->capturing = true;
       st = step_body(ctx, b, s);
@@ -2131,6 +2202,8 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
       ctx->gkey = GraphKey{B, b->tokens, b->next, b->kv.k_cache, b->kv.v_cache, b->kv.pos, b->pos_out};
       ctx->gslots = slots_now;
       ctx->gmask = ctx->timed_mask;
+      ctx->gbatches = ctx->batches;
+      ctx->gdelta = cas_delta;
       ctx->graph_fresh = true;   // capture enqueued this step's fetches and bookkeeping
       ctx->graph_tev_pairs = ctx->tev_used / 2;
       ctx->graph_timed_pending = false;
@@ -2145,7 +2218,11 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
     ctx->graph_fresh = false;
     CK(cudaGraphLaunch(ctx->gexec, s));
     ctx->st.graph_replays++;
-    if (!fresh && ctx->R > 0) {
+    if (!fresh && ctx->mode == SIDP_CAS) {
+      // the replayed base kernel advanced the device counter by the captured delta
+      ctx->rt_base_host = ctx->rt;
+      cas_replay_bookkeeping(ctx);
+    } else if (!fresh && ctx->R > 0) {
       st = replay_bookkeeping(ctx);
       if (st != SIDP_OK) return st;
     }

@@ -728,3 +728,44 @@ def test_was_hybrid_fetch(P, d, slots, share):
     rep.step(); rep.finish_step()
     assert torch.equal(rep.history[0][1], G.history[0][1])
     rep.ctx.destroy()
+
+
+@pytest.mark.parametrize("pool,B", [("layer", [3, 5]), ("layer", [4, 0, 2, 0]), ("ffn", [2, 2, 2, 2])])
+def test_cas_graph_replay(P, pool, B):
+    """CaS steps replay as CUDA graphs (flag values relative to a device round-trip counter that
+    each step's first kernel advances): the tokens of 5 graph-replayed CaS steps on virtual ranks
+    equal an eager CaS run's bit for bit (eager = logits requested, so never captured), and the
+    live ranks replayed graphs."""
+    m = MODELS["tiny"].with_layers(4)
+    d = len(B)
+    steps = 5
+
+    def group():
+        ranks = _group(P, m, d, B, pool=pool)
+        for R in ranks:
+            R.ctx.set_batches(B)
+            R.ctx.set_mode(1, 0)
+        return ranks
+
+    G = group()
+    E = group()
+    for s in range(steps):
+        for R in G:
+            with torch.cuda.stream(R.stream):
+                R.ctx.step(R.toks, R.toks, R.kv, batch=R.B, stream=R.stream, advance_pos=R.B > 0)
+        for R in E:
+            R.step()
+        for R in G:
+            R.stream.synchronize()
+        for R in E:
+            R.finish_step()
+        for r in range(d):
+            if B[r]:
+                assert torch.equal(G[r].toks[:B[r]].cpu(), E[r].history[-1][0]), (s, r)
+    for r, R in enumerate(G):
+        st = R.ctx.stats()
+        assert st["timeouts"] == 0
+        if B[r]:
+            assert st["graph_replays"] >= steps - 1, st["graph_replays"]
+    for R in G + E:
+        R.ctx.destroy()
