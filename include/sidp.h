@@ -314,6 +314,20 @@ sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ld
                            const void* resid, int32_t ldr, const void* bias, int32_t k_splits,
                            void* stream);
 
+/* Test hook for the fused QKV GEMM (PAPER.md:163 — the KV cache is local):
+ * Y = X W^T (+ bias) with X [M,K] (row stride ldx) and W [N = (nq + 2 nkv) hd, K] bf16
+ * row-major; per token m and head: q/k heads get the per-head RMSNorm (gains gq / gk, null =
+ * off; Qwen3 qk_norm) and rotate-half RoPE with rope[pos[m]] ((cos, sin) fp32 pairs [.][hd/2]),
+ * then q -> q[m][head][hd] bf16, k / v -> kc / vc[(m nkv + g) smax + pos[m]][hd] bf16.
+ * k_splits 0 = the runtime's choice (token-major head tiles with an in-kernel stream-K fix-up
+ * from M >= 128, else W-major whole tiles), 1 = W-major whole tiles.  hd 64 or 128.  SIDP_EINVAL
+ * on bad shapes.  Device pointers; enqueued on stream. */
+sidp_status sidp_test_gemm_qkv(const void* x, int32_t ldx, const void* w, int32_t M, int32_t K,
+                               const void* bias, int32_t nq, int32_t nkv, int32_t hd,
+                               const void* gq, const void* gk, float eps, const void* rope,
+                               const int32_t* pos, void* q, void* kc, void* vc, int32_t smax,
+                               int32_t k_splits, void* stream);
+
 /* Test hook for the deferred stream-K fix-up (SURVEY.md a8+a9, a11+a5): the EPI_PARTIAL GEMM
  * Y = X W^T (X [M,K] row stride ldx, W [N,K] contiguous, bf16) leaves fp32 k-range partials
  * that resid_norm sums in slice order: xout = bf16(Y + resid) ([M,N], resid row stride ldr,

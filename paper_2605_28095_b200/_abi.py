@@ -89,6 +89,8 @@ SIGNATURES = {
     "sidp_set_timing": [_P, _I32],
     "sidp_last_error": [],
     "sidp_test_gemm": [_P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _I32, _P, _I32, _P],
+    "sidp_test_gemm_qkv": [_P, _I32, _P, _I32, _I32, _P, _I32, _I32, _I32, _P, _P, C.c_float, _P,
+                           _P, _P, _P, _P, _I32, _I32, _P],
     "sidp_test_gemm_resid_norm": [_P, _I32, _P, _I32, _I32, _I32, _P, _I32, _P, C.c_float, _P,
                                   _P, _P],
     "sidp_test_mlp_fused": [_P, _P, _P, _P, _I32, _I32, _I32, _P, C.c_float, _P, _P, _P, _P],

@@ -238,6 +238,15 @@ def test_gemm(x, w, out, M, N, K, epi, resid=None, bias=None, k_splits=0, ldo=No
                                    k_splits, _stream_ptr(stream)), "sidp_test_gemm")
 
 
+def test_gemm_qkv(x, w, bias, nq, nkv, hd, gq, gk, eps, rope, pos, q, kc, vc, smax, k_splits=0,
+                  stream=None):
+    M, K = x.shape
+    A.check(A.lib().sidp_test_gemm_qkv(_ptr(x), x.stride(0), _ptr(w), M, K, _ptr(bias), nq, nkv, hd,
+                                       _ptr(gq), _ptr(gk), eps, _ptr(rope), _ptr(pos), _ptr(q),
+                                       _ptr(kc), _ptr(vc), smax, k_splits, _stream_ptr(stream)),
+            "sidp_test_gemm_qkv")
+
+
 def test_gemm_resid_norm(x, w, resid, g, eps, xout, u, stream=None):
     M, K = x.shape
     N = w.shape[0]

@@ -151,6 +151,9 @@ struct MlpArgs {
 // max_tt: most 256-row token tiles allowed (0 = the runtime policy, SIDP_MLP_MAX_TT, default 1;
 // the kernel supports 2).
 bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters, int max_tt = 0);
+// true when an EPI_QKV launch of this shape takes the token-major head-tile path (qk-norm, RoPE
+// and the KV append in the GEMM epilogue; stream-K with an in-kernel fix-up of split tiles)
+bool gemm_qkv_sw_ok(int M, int N, int K, int hd, size_t ws_bytes, int n_counters);
 void mlp_prepare(int h, int I, size_t ws_bytes);   // builds the schedule (call before capture)
 // The host list schedule (no CUDA calls): per-pair unit lists {phase | seg << 8, tile, kb0, kb1}
 // (flat, cluster c at [off[c], off[c+1])) and the down segments per tile.

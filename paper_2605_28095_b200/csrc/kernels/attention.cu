@@ -32,7 +32,7 @@ constexpr int kQkvHeadsPerWarp = 5;
 // lane l holds dims [E*l, E*l+E) of the first half and the same dims + hd/2 (its RoPE
 // partners), E = hd/64: every load and store is one E-wide vector per lane
 template <int HD, int HPW>
-__global__ void __launch_bounds__(256, 2) qkv_post_kernel(QkvPostArgs a) {
+__global__ void __launch_bounds__(256, 4) qkv_post_kernel(QkvPostArgs a) {
   pdl_trigger();
   pdl_wait();
   constexpr int half = HD / 2, E = HD / 64;

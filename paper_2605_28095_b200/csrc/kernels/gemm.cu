@@ -57,9 +57,11 @@ struct KParams {
   int compact;                  // stream-K partials in per-cluster tile buffers (see part_tile)
   int partial_all;              // EPI_PARTIAL: every unit writes its fp32 partial slice
   int w_evict;                  // weight TMA loads carry an L2 evict-first policy
-  int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA
+  int debug;                    // perf experiments only: 1 = skip MMA, 2 = skip TMA; SW EPI_QKV:
+                                // 4 = no stores, 8 = no RoPE loads, 16 = no slice loads, 32 = no gains
   unsigned long long* trace;    // perf experiments only: per-k-block timestamps of cluster 0
   QkvEpi qkv;                   // EPI_QKV destination
+  int qkv_cnt_off;              // SW EPI_QKV: first of this launch's split-tile arrival counters
   FlagWait wait;                // CaS owner: activation loads wait for the arrival flags
   RowScatter scatter;           // CaS owner: output rows straight into the requesters' buffers
   PostFlags post;               // CaS owner: done + served, posted by this launch's last CTA
@@ -521,6 +523,120 @@ SIDP_DEV void store_row(const KParams& p, const uint32_t (&r)[32], int m, int n0
   }
 }
 
+// 32 fp32 values -> 32 bf16 at dst (64 contiguous bytes, 16-byte stores)
+SIDP_DEV void store_bf16x32(bf16* dst, const float (&v)[32]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    float t[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = v[8 * g + q];
+    reinterpret_cast<uint4*>(dst)[g] = pack_bf16x8(t);
+  }
+}
+SIDP_DEV void add_bias32(const bf16* bias, int n, float (&v)[32]) {
+  if (!bias) return;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    float t[8];
+    unpack_bf16x8(*reinterpret_cast<const uint4*>(bias + n + 8 * g), t);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[8 * g + q] += t[q];
+  }
+}
+
+// Token-major fused QKV epilogue (SW EPI_QKV): this thread's token m, the
+// tile's features [fbase, nlim) are whole heads whose fp32 accumulators sit in this thread's
+// TMEM lane at columns tl + (f - fbase).  Per head, the arithmetic of qkv_post_kernel: + bias,
+// per-head RMSNorm (Qwen3 qk_norm: x * r * g), rotate-half RoPE from the fp32 (cos, sin) table
+// at pos, bf16 -> q [m][head] or the KV cache row pos (the KV cache is local).
+// The whole head lies in this thread: the norm needs no reduction and the RoPE partner d + hd/2
+// is the same thread's chunk c + hd/64.  TMEM reads are warp-collective: every lane runs every
+// read; only global loads / stores are predicated on `valid`.  sg = the qk-norm gains staged in
+// shared memory ([0, hd) q, [hd, 2 hd) k) — global gain loads inside the per-head chain cost
+// ~12 us per launch (measured, tools/qkv_bench.py), the RoPE rows are issued ahead of the TMEM
+// reads they are combined with.
+SIDP_DEV void qkv_sw_row(const KParams& p, int m, bool valid, int pos, int fbase, int nlim,
+                         uint32_t tl, const float* sg) {
+  const QkvEpi& e = p.qkv;
+  const int hd = e.hd, hc = hd / 64;                 // chunk pairs (x1 chunk c, x2 chunk c + hc)
+  auto get = [&](int c, float (&v)[32]) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tl + c * 32, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
+  };
+  for (int f0 = fbase; f0 < nlim; f0 += hd) {
+    const int head = f0 / hd;
+    const int region = head < e.nq ? 0 : (head < e.nq + e.nkv ? 1 : 2);
+    const int c0 = (f0 - fbase) / 32;
+    bf16* dst;
+    if (region == 0) {
+      dst = e.q + ((size_t)m * e.nq + head) * hd;
+    } else {
+      const int g = head - e.nq - (region == 2 ? e.nkv : 0);
+      dst = (region == 1 ? e.kc : e.vc) + (((size_t)m * e.nkv + g) * e.smax + pos) * hd;
+    }
+    const bool st = valid && !(p.debug & 4);
+    if (region == 2) {
+      for (int c = 0; c < 2 * hc; ++c) {
+        float v[32];
+        get(c0 + c, v);
+        add_bias32(p.bias, f0 + 32 * c, v);
+        if (st) store_bf16x32(dst + 32 * c, v);
+      }
+      continue;
+    }
+    const bool has_gain = !(p.debug & 32) && (region == 0 ? e.gq : e.gk) != nullptr;
+    const float* gs = sg + (region == 0 ? 0 : hd);
+    for (int c = 0; c < hc; ++c) {
+      // (cos, sin) of dims 32c .. 32c + 31: requested before the norm pass / TMEM reads
+      float4 cs[16];
+      const float4* rp = reinterpret_cast<const float4*>(e.rope + (size_t)pos * (hd / 2) + 32 * c);
+#pragma unroll
+      for (int q2 = 0; q2 < 16; ++q2)
+        cs[q2] = (valid && !(p.debug & 8)) ? __ldg(rp + q2) : make_float4(1.f, 0.f, 1.f, 0.f);
+      float r = 1.0f;
+      if (has_gain) {   // RMSNorm statistic over the whole head (recomputed per chunk pair: TMEM is cheap)
+        float ss = 0.0f;
+        for (int cc = 0; cc < 2 * hc; ++cc) {
+          float v[32];
+          get(c0 + cc, v);
+          add_bias32(p.bias, f0 + 32 * cc, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) ss += v[q] * v[q];
+        }
+        r = rsqrtf(ss / (float)hd + e.eps);
+      }
+      float a[32], b[32];
+      get(c0 + c, a);
+      get(c0 + c + hc, b);
+      add_bias32(p.bias, f0 + 32 * c, a);
+      add_bias32(p.bias, f0 + hd / 2 + 32 * c, b);
+      if (has_gain) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          a[q] = a[q] * r * gs[32 * c + q];
+          b[q] = b[q] * r * gs[hd / 2 + 32 * c + q];
+        }
+      }
+#pragma unroll
+      for (int q2 = 0; q2 < 16; ++q2) {   // (cos, sin) of dims 2 q2, 2 q2 + 1
+        const float4 t = cs[q2];
+        const float a0 = a[2 * q2], b0 = b[2 * q2], a1 = a[2 * q2 + 1], b1 = b[2 * q2 + 1];
+        a[2 * q2] = a0 * t.x - b0 * t.y;
+        b[2 * q2] = b0 * t.x + a0 * t.y;
+        a[2 * q2 + 1] = a1 * t.z - b1 * t.w;
+        b[2 * q2 + 1] = b1 * t.z + a1 * t.w;
+      }
+      if (st) {
+        store_bf16x32(dst + 32 * c, a);
+        store_bf16x32(dst + hd / 2 + 32 * c, b);
+      }
+    }
+  }
+}
+
 // perf experiment timeline: per CTA, slot k of TL(k) = globaltimer at a kernel milestone
 #define SIDP_TL(k) \
   do { if (p.trace && blockIdx.x < 512) p.trace[6 * 4096 + blockIdx.x * 8 + (k)] = globaltimer_ns(); } while (0)
@@ -713,6 +829,14 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int row = quarter * 32 + lane;                // TMEM lane (W row, or token if SW)
     const int tid = (warp - 2) * 32 + lane;             // 0..127
     if constexpr (SW) {
+      if constexpr (EPI == EPI_QKV) {   // qk-norm gains -> shared memory (stg is unused when SW)
+        const int hd = p.qkv.hd;
+        for (int i = tid; i < 2 * hd; i += 128) {
+          const bf16* g = i < hd ? p.qkv.gq : p.qkv.gk;
+          stg[i] = g ? bf16_to_f(g[i < hd ? i : i - hd]) : 1.0f;
+        }
+        named_bar_sync(1, 128);
+      }
       int un = 0;
       UnitIter ui;
       ui.init(p, cluster);
@@ -725,9 +849,96 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const int fbase = x.mt * BNT;                           // first feature of the tile
         const int nlim = min(p.N, fbase + BNT);
         const int nch = (nlim - fbase + 31) / 32;
+        int pos_m = 0;   // EPI_QKV: the new token's position, loaded before the accumulator wait
+        if constexpr (EPI == EPI_QKV) pos_m = m < p.M ? p.qkv.pos[m] : 0;
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t tl = tmem_base + acc * ACCS + ((uint32_t)(quarter * 32) << 16);
+        if constexpr (EPI == EPI_QKV) {
+          const bool valid = m < p.M;
+          const float* sg = stg;   // qk-norm gains, staged at the epilogue's start
+          if (x.nseg == 1) {   // whole dot products in TMEM: the fused epilogue reads them there
+            qkv_sw_row(p, m, valid, pos_m, fbase, nlim, tl, sg);
+          } else {
+            // stream-K segment of a split tile: fp32 partial -> ws[seg][m][features]; the last
+            // of the tile half's nseg segments to arrive folds the other slices into its TMEM
+            // accumulator in slice order (deterministic: its own slice equals its TMEM values)
+            // and runs the fused epilogue from TMEM
+            float* dst = p.ws + (size_t)x.seg * p.M * p.N + (size_t)m * p.N;
+            for (int c = 0; c < nch; ++c) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(tl + c * 32, r);
+              tmem_ld_wait();
+              if (valid) {
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                  __stcg(reinterpret_cast<float4*>(dst + fbase + c * 32 + 4 * g),
+                         make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]),
+                                     __uint_as_float(r[4 * g + 2]), __uint_as_float(r[4 * g + 3])));
+              }
+            }
+            // arrival: the CTA's slice stores, then one thread's gpu-scope fence + counter add
+            // (the cooperative-groups grid-barrier pattern: bar.sync orders the other threads'
+            // stores before thread 0's cumulative fence)
+            named_bar_sync(1, 128);
+            if (tid == 0) {
+              int* cnt = p.counters + p.qkv_cnt_off + 2 * (x.ft * p.m_tiles + x.mt) + rank;
+              __threadfence();
+              const int prev = atomicAdd(cnt, 1);
+              __threadfence();
+              *last_flag = prev == x.nseg - 1;
+              if (prev == x.nseg - 1) *cnt = 0;   // zero between launches
+            }
+            named_bar_sync(1, 128);
+            const bool last = *last_flag;
+            named_bar_sync(1, 128);   // last_flag is rewritten by the next split unit
+            if (last) {
+              const float* src = p.ws + (size_t)m * p.N + fbase;
+              const size_t slice = (size_t)p.M * p.N;
+              for (int c = 0; c < nch; c += 2) {   // two 32-column chunks per slice round trip
+                float v[64];
+#pragma unroll
+                for (int q = 0; q < 64; ++q) v[q] = 0.0f;
+                for (int s = 0; s < x.nseg; ++s) {
+                  if (s == x.seg) {
+                    uint32_t r0[32], r1[32];
+                    tmem_ld_32x32b_x32(tl + c * 32, r0);
+                    tmem_ld_32x32b_x32(tl + c * 32 + 32, r1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                      v[q] += __uint_as_float(r0[q]);
+                      v[32 + q] += __uint_as_float(r1[q]);
+                    }
+                  } else if (valid && !(p.debug & 16)) {
+                    const float4* s4 = reinterpret_cast<const float4*>(src + s * slice + 32 * c);
+                    float4 t[16];
+#pragma unroll
+                    for (int g = 0; g < 16; ++g) t[g] = __ldcg(s4 + g);
+#pragma unroll
+                    for (int g = 0; g < 16; ++g) {
+                      v[4 * g] += t[g].x; v[4 * g + 1] += t[g].y; v[4 * g + 2] += t[g].z; v[4 * g + 3] += t[g].w;
+                    }
+                  }
+                }
+                uint32_t w0[32], w1[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                  w0[q] = __float_as_uint(v[q]);
+                  w1[q] = __float_as_uint(v[32 + q]);
+                }
+                tmem_st_32x32b_x32(tl + c * 32, w0);
+                tmem_st_32x32b_x32(tl + c * 32 + 32, w1);
+              }
+              tmem_st_wait();
+              qkv_sw_row(p, m, valid, pos_m, fbase, nlim, tl, sg);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          continue;
+        }
         unsigned long long best = 0ull;
         for (int c = 0; c < nch; ++c) {
           uint32_t r[32];
@@ -1256,9 +1467,9 @@ bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t out
 int g_num_sms = 0;
 thread_local int g_last_launches = 0;
 
-// the token-major variant exists for every epilogue but the fused QKV one
+// the token-major variant exists for every epilogue
 template <int EPI>
-constexpr bool kHasSw = EPI != EPI_QKV;
+constexpr bool kHasSw = true;
 
 // EPI_PARTIAL launch geometry (shared by gemm_launch and gemm_partial_ok): W-major, token tile =
 // M rounded up to 32 (<= 256), partials staged through shared memory into coalesced rows.
@@ -1297,6 +1508,40 @@ PartialPlan plan_partial(int M, int N, int K, int pair_slots) {
     per = q.total / q.clusters;
   }
   q.max_seg = (int)((q.nkb + per - 1) / std::max<long long>(per, 1)) + 1;
+  return q;
+}
+
+// Token-major fused-QKV geometry (SW EPI_QKV): feature tiles of whole heads (BNF = hd, or
+// SIDP_QKV_BNF), 256-token pair tiles, stream-K over every CTA pair (the head-aligned tile
+// count rarely divides the pair count: 80 heads of Qwen3 / Llama on 74 pairs); split tiles go
+// through fp32 slices [seg][M][N] and an in-kernel last-arriver fix-up.
+struct QkvSwPlan {
+  bool ok;
+  int BNT, m_tiles, n_pairs, tiles, clusters, nkb, max_seg;
+  long long total;
+};
+constexpr int kQkvCntOff = 1 << 15;   // counters [kQkvCntOff, +2 tiles): split-tile arrivals
+QkvSwPlan plan_qkv_sw(int M, int N, int K, int hd, int pair_slots, size_t ws_bytes, int n_counters) {
+  static int env_min = getenv("SIDP_QKV_SW_MIN_M") ? atoi(getenv("SIDP_QKV_SW_MIN_M")) : 128;
+  static int env_bnf = getenv("SIDP_QKV_BNF") ? atoi(getenv("SIDP_QKV_BNF")) : 0;
+  QkvSwPlan q{};
+  if (env_min <= 0 || M < env_min || (hd != 64 && hd != 128) || N % hd || K % BK) return q;
+  const int nkb_blocks = K / BK;
+  const int kps = nkb_blocks % 2 == 0 ? 2 : 1;
+  q.nkb = nkb_blocks / kps;
+  q.BNT = (env_bnf > 0 && env_bnf % hd == 0 && env_bnf <= 256) ? env_bnf : hd;
+  q.m_tiles = N / q.BNT;
+  q.n_pairs = (M + 2 * WROWS - 1) / (2 * WROWS);
+  q.tiles = q.m_tiles * q.n_pairs;
+  q.clusters = pair_slots;
+  q.total = (long long)q.tiles * q.nkb;
+  long long per = q.total / q.clusters;
+  if (per < 2) {
+    q.clusters = (int)std::max<long long>(1, q.total / 2);
+    per = q.total / q.clusters;
+  }
+  q.max_seg = (int)((q.nkb + per - 1) / std::max<long long>(per, 1)) + 1;
+  q.ok = (size_t)q.max_seg * M * N * 4 <= ws_bytes && kQkvCntOff + 2 * q.tiles <= n_counters;
   return q;
 }
 
@@ -1482,6 +1727,14 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     m_tiles = (a.M + BNT - 1) / BNT;
     n_pairs = (a.N + 2 * WROWS - 1) / (2 * WROWS);
   }
+  QkvSwPlan qs{};
+  if (a.epi == EPI_QKV && a.k_splits != 1 && a.k_splits >= 0 && !a.wait && !a.scatter) {
+    qs = plan_qkv_sw(a.M, a.N, a.K, a.qkv->hd, pair_slots, w.ws_bytes, w.n_counters);
+    if (qs.ok) {
+      sw = true;
+      BNT = qs.BNT; m_tiles = qs.m_tiles; n_pairs = qs.n_pairs;
+    }
+  }
   int tiles = n_pairs * m_tiles;
   // stream-K over all pairs unless the epilogue needs whole dot products (fused argmax) or the
   // caller pins whole tiles (k_splits == 1); max segments per tile bounds the workspace
@@ -1525,6 +1778,10 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
       compact = 1;
       clusters = pair_slots;
     }
+  }
+  if (qs.ok) {
+    streamk = 1; dp_tiles = 0; compact = 0;
+    clusters = qs.clusters;
   }
   const bool part = a.epi == EPI_PARTIAL;
   if (part) {
@@ -1595,6 +1852,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   // several token tiles the other units re-read the same W tile from L2
   p.w_evict = env_evict && (sw ? n_pairs == 1 : m_tiles == 1);
   if (a.qkv) p.qkv = *a.qkv;
+  p.qkv_cnt_off = kQkvCntOff;
   if (a.wait) p.wait = *a.wait;
   const PostFlags* post = a.post && a.post->n > 0 ? a.post : nullptr;
   if (a.scatter) {
@@ -1613,7 +1871,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   }
   const size_t smem = stages * stage_bytes + extra + 1024;
   dim3 grid(2 * clusters);
-  const bool reduce_follows = streamk && !part;
+  const bool reduce_follows = streamk && !part && a.epi != EPI_QKV;
   if (post && !reduce_follows) p.post = *post;   // this launch is the last: it posts
   cudaError_t e0 = cudaSuccess, e1 = cudaSuccess;
   switch (a.epi) {
@@ -1622,7 +1880,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     case EPI_RESID: e0 = launch_gemm2<EPI_RESID>(kps, sw, grid, smem, stream, tw, tx, p); break;
     case EPI_SILU_MUL: e0 = launch_gemm2<EPI_SILU_MUL>(kps, sw, grid, smem, stream, tw, tx, p); break;
     case EPI_ARGMAX: e0 = launch_gemm2<EPI_ARGMAX>(kps, sw, grid, smem, stream, tw, tx, p); break;
-    case EPI_QKV: e0 = launch_gemm2<EPI_QKV>(kps, false, grid, smem, stream, tw, tx, p); break;
+    case EPI_QKV: e0 = launch_gemm2<EPI_QKV>(kps, sw, grid, smem, stream, tw, tx, p); break;
     case EPI_PARTIAL: e0 = launch_gemm2<EPI_PARTIAL>(kps, sw, grid, smem, stream, tw, tx, p); break;
     default: return cudaErrorInvalidValue;
   }
@@ -1661,7 +1919,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
               v.size(), v.front(), v[v.size() / 2], v.back());
     }
   }
-  if (e0 != cudaSuccess || !streamk || part) return e0;
+  if (e0 != cudaSuccess || !streamk || part || a.epi == EPI_QKV) return e0;
   g_last_launches = 2;
   if (post) p.post = *post;   // the fix-up is the last launch: it posts
   dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, clusters - 1));
@@ -1778,6 +2036,10 @@ void mlp_prepare(int h, int I, size_t ws_bytes) {
     for (int mt = 1; mt <= kMlpMaxTokenTiles; ++mt) mlp_sched(h, I, mt, ws_bytes);
 }
 
+bool gemm_qkv_sw_ok(int M, int N, int K, int hd, size_t ws_bytes, int n_counters) {
+  return plan_qkv_sw(M, N, K, hd, std::max(1, compute_sms() / 2), ws_bytes, n_counters).ok;
+}
+
 bool mlp_fused_ok(int M, int h, int I, size_t ws_bytes, int n_counters, int max_tt) {
   static int env = getenv("SIDP_MLP_FUSED") ? atoi(getenv("SIDP_MLP_FUSED")) : 1;
   // Policy default: one token tile.  At M = 512 (2 tiles) the fused launch is ~5% faster than
@@ -1859,6 +2121,7 @@ cudaError_t gemm_preload() {
   SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2, false>))
   SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_ARGMAX, 2, true>))
   SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2, false>))
+  SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_QKV, 2, true>))
   SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 1, false>)) SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 2, false>))
   SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 1, true>)) SIDP_PRELOAD((gemm2_kernel<EPI_PARTIAL, 2, true>))
     SIDP_PRELOAD((mlp2_kernel))

@@ -487,7 +487,15 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
   const size_t lstride = (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
   bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
   bf16* vc = reinterpret_cast<bf16*>(kv->v_cache) + (size_t)layer * lstride;
-  static const bool fused_qkv = getenv("SIDP_FUSED_QKV") && atoi(getenv("SIDP_FUSED_QKV")) != 0;
+  // SIDP_FUSED_QKV: 1 = EPI_QKV (one launch: GEMM + qk-norm + RoPE + KV append; token-major
+  // head tiles with an in-kernel stream-K fix-up where gemm_qkv_sw_ok), -1 = EPI_QKV only where
+  // gemm_qkv_sw_ok, 0 / unset = fp32 GEMM + qkv_post.  Default off: measured the
+  // fused launch at 53 us vs 35 + 13 us at M = 256 (head-aligned 128-feature tiles re-read the
+  // token tile 80x and the split tiles' fix-up tail is exposed)
+  static const int fused_env = getenv("SIDP_FUSED_QKV") ? atoi(getenv("SIDP_FUSED_QKV")) : 0;
+  const bool fused_qkv = fused_env > 0 ||
+      (fused_env < 0 && sidp::gemm_qkv_sw_ok(B, ctx->qkvdim, m.hidden, m.head_dim, ctx->gemm_ws_bytes,
+                                             ctx->n_counters));
   const bool u_ready = ctx->u_for == layer;
   ctx->u_for = -1;
   sidp::PartialSrc part{};
@@ -2487,6 +2495,34 @@ sidp_status sidp_test_gemm(const void* x, int32_t ldx, const void* w, int32_t ld
   cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, counters, 1 << 16},
                                     reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm: %s", cudaGetErrorString(e));
+  return SIDP_OK;
+}
+
+sidp_status sidp_test_gemm_qkv(const void* x, int32_t ldx, const void* w, int32_t M, int32_t K,
+                               const void* bias, int32_t nq, int32_t nkv, int32_t hd,
+                               const void* gq, const void* gk, float eps, const void* rope,
+                               const int32_t* pos, void* q, void* kc, void* vc, int32_t smax,
+                               int32_t k_splits, void* stream) {
+  static float* ws = nullptr;
+  static int* counters = nullptr;
+  static const size_t ws_bytes = (size_t)256 << 20;
+  if (!ws) {
+    if (cudaMalloc(&ws, ws_bytes) != cudaSuccess || cudaMalloc(&counters, (1 << 16) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(counters, 0, (1 << 16) * sizeof(int)) != cudaSuccess)
+      return fail(SIDP_ENOMEM, "test gemm workspace");
+  }
+  if (M <= 0 || nq <= 0 || nkv <= 0 || (hd != 64 && hd != 128) || !pos || !rope || !q || !kc || !vc)
+    return fail(SIDP_EINVAL, "test_gemm_qkv: bad arguments");
+  sidp::QkvEpi qe{reinterpret_cast<bf16*>(q), reinterpret_cast<bf16*>(kc), reinterpret_cast<bf16*>(vc),
+                  pos, reinterpret_cast<const float2*>(rope), reinterpret_cast<const bf16*>(gq),
+                  reinterpret_cast<const bf16*>(gk), eps, nq, nkv, hd, smax};
+  sidp::GemmArgs a{};
+  a.x = reinterpret_cast<const bf16*>(x); a.ldx = ldx; a.w = reinterpret_cast<const bf16*>(w);
+  a.ldw = K; a.M = M; a.N = (nq + 2 * nkv) * hd; a.K = K; a.epi = sidp::EPI_QKV;
+  a.bias = reinterpret_cast<const bf16*>(bias); a.k_splits = k_splits; a.qkv = &qe;
+  cudaError_t e = sidp::gemm_launch(a, sidp::GemmWorkspace{ws, ws_bytes, counters, 1 << 16},
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(SIDP_ECUDA, "gemm qkv: %s", cudaGetErrorString(e));
   return SIDP_OK;
 }
 

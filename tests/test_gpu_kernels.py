@@ -234,3 +234,71 @@ def test_gemm_fused_argmax(P, M, N, K, orient):
     top2 = np.sort(ref, axis=1)[:, -2:]
     sure = (top2[:, 1] - top2[:, 0]) > 1e-4
     assert (idx[sure] == np.argmax(ref, axis=1)[sure]).all()
+
+
+# fused QKV GEMM (a6): GEMM + bias + per-head RMSNorm + RoPE + q / KV-cache stores in one launch
+def _qkv_reference(x, w, bias, nq, nkv, hd, gq, gk, eps, rope, pos):
+    """fp64 torch reference of the fused epilogue on the same bf16 operands."""
+    y = x.double() @ w.double().T
+    if bias is not None:
+        y = y + bias.double()
+    M = x.shape[0]
+    y = y.view(M, nq + 2 * nkv, hd)
+    q, k, v = y[:, :nq], y[:, nq:nq + nkv], y[:, nq + nkv:]
+
+    def norm(t, g):
+        if g is None:
+            return t
+        return t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + eps) * g.double()
+
+    cs = rope.double()[pos.long()]                      # [M, hd/2, 2]
+    c, s = cs[..., 0][:, None, :], cs[..., 1][:, None, :]
+
+    def rot(t):
+        a, b = t[..., :hd // 2], t[..., hd // 2:]
+        return torch.cat([a * c - b * s, b * c + a * s], -1)
+
+    return rot(norm(q, gq)), rot(norm(k, gk)), v
+
+
+@pytest.mark.parametrize("M,K,nq,nkv,hd,qk_norm,bias,splits", [
+    (256, 5120, 64, 8, 128, True, False, 0),      # Qwen3-32B shape, token-major head tiles
+    (300, 1024, 16, 4, 128, True, True, 0),       # ragged token tail, QKV bias (Qwen2.5)
+    (1024, 2048, 32, 8, 128, False, False, 0),    # Llama-like, several token pairs
+    (200, 512, 8, 2, 64, True, True, 0),          # hd 64
+    (64, 1024, 16, 4, 128, True, True, 0),        # below the token-major threshold (W-major)
+    (256, 1024, 16, 4, 128, True, False, 1),      # W-major whole tiles forced
+])
+def test_gemm_qkv_fused(P, M, K, nq, nkv, hd, qk_norm, bias, splits):
+    g = torch.Generator().manual_seed(M + K + nq)
+    N = (nq + 2 * nkv) * hd
+    x = _lvl((M, K), g).cuda()
+    w = _lvl((N, K), g, 2.0 ** -5).cuda()
+    b = _lvl((N,), g, 0.125).cuda() if bias else None
+    gq = (1 + _lvl((hd,), g, 0.25).float()).to(torch.bfloat16).cuda() if qk_norm else None
+    gk = (1 + _lvl((hd,), g, 0.25).float()).to(torch.bfloat16).cuda() if qk_norm else None
+    smax = 64
+    pos = torch.randint(0, smax, (M,), generator=g, dtype=torch.int32).cuda()
+    ang = torch.arange(smax, dtype=torch.float64)[:, None] * 10000.0 ** (
+        -torch.arange(0, hd, 2, dtype=torch.float64) / hd)[None, :]
+    rope = torch.stack([ang.cos(), ang.sin()], -1).float().cuda()      # [smax, hd/2, 2]
+    q = torch.full((M, nq, hd), float("nan"), dtype=torch.bfloat16, device="cuda")
+    kc = torch.zeros(M, nkv, smax, hd, dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    eps = 1e-6
+    for _ in range(2):   # twice: the split-tile arrival counters must be back at zero
+        P.test_gemm_qkv(x, w, b, nq, nkv, hd, gq, gk, eps, rope, pos, q, kc, vc, smax, k_splits=splits)
+    torch.cuda.synchronize()
+    rq, rk, rv = _qkv_reference(x.cpu(), w.cpu(), None if b is None else b.cpu(), nq, nkv, hd,
+                                None if gq is None else gq.cpu(), None if gk is None else gk.cpu(),
+                                eps, rope.cpu(), pos.cpu())
+    ar = torch.arange(M)
+    pk = kc.cpu()[ar, :, pos.cpu().long()].double()                     # [M, nkv, hd]
+    pv = vc.cpu()[ar, :, pos.cpu().long()].double()
+    for got, ref in ((q.cpu().double(), rq), (pk, rk), (pv, rv)):
+        err = (got - ref).abs().max().item()
+        assert err <= 2.0 ** -7 * ref.abs().max().item(), err
+    # nothing written outside the new tokens' cache rows
+    mask = torch.ones(M, smax, dtype=torch.bool)
+    mask[ar, pos.cpu().long()] = False
+    assert kc.cpu().permute(0, 2, 1, 3)[mask].abs().max().item() == 0
