@@ -310,8 +310,9 @@ cudaError_t resid_norm_launch(const PartialSrc& ps, const bf16* resid, int ldr, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // SIDP_FIX_GRID: 0 = one CTA per row (default, measured ~0.1 ms/step faster); else <= 1 per SM
-  static const int grid_mode = getenv("SIDP_FIX_GRID") ? atoi(getenv("SIDP_FIX_GRID")) : 0;
+  // SIDP_FIX_GRID: 0 = one CTA per row; else <= 1 per SM walking rows (default: measured M2
+  // 29.22 vs 29.36 ms/step over 3 A/B pairs once qkv_post ran in one wave; r1 had it 0.1 ms slower)
+  static const int grid_mode = getenv("SIDP_FIX_GRID") ? atoi(getenv("SIDP_FIX_GRID")) : 1;
   static const int late = getenv("SIDP_FIX_LATE_TRIGGER") ? atoi(getenv("SIDP_FIX_LATE_TRIGGER")) : 0;
   const int grid = grid_mode ? std::min(rows, sms) : rows;
   // slices loaded in one round trip: up to 8 per vector (640-thread rows, 96 registers) when the

@@ -1,17 +1,19 @@
 """WaS <-> CaS mode switching on virtual ranks: the directive is issued with
 identical arguments on every rank, takes effect at a step boundary, drains and resets the WaS
 ring, and the decoded sequence equals a replicated run throughout (WaS steps bitwise, CaS steps
-within tolerance).  Also the controller-driven switch: per-step batches gathered on the host feed
-the orchestrator policy, whose directive every rank applies."""
+within tolerance) and the fp64 oracle's decode of the same tokens (north_star tolerance).  Also
+the controller-driven switch: per-step batches gathered on the host feed the orchestrator
+policy, whose directive every rank applies."""
 import numpy as np
 import pytest
 import torch
 
+from oracle import model as OM
 from oracle import schedule as OS
 from sidp_inputs import MODELS
 
-from .test_gpu_parity import SEED, TOL, Rank, _budget, _group, _replicated, P  # noqa: F401  (fixture)
-from .helpers import rel_err
+from .test_gpu_parity import SEED, TOL, Rank, _budget, _gpu_caches, _group, _replicated, P  # noqa: F401  (fixture)
+from .helpers import OracleModel, oracle_layer, rank_inputs, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -46,6 +48,27 @@ def test_was_cas_was_switch(P, pool):
             else:
                 assert rel_err(got.double().numpy(), exp.double().numpy()) <= TOL, (r, s)
         rep.ctx.destroy()
+        # and against the fp64 ORACLE through the whole WaS -> CaS -> WaS run (not only against
+        # another GPU run), per layer as the north_star states its tolerance: every step's every
+        # layer recomputed by the oracle from the GPU's bf16 layer input and KV state (teacher
+        # forcing; the oracle's CaS layer equals its replicated layer to 1e-12,
+        # tests/test_oracle_model.py), against the next layer's input, the new k/v entries at
+        # pos + s and the logits
+        om = OracleModel(m, SEED)
+        _, _, pos, _ = rank_inputs(m, SEED, sum(B[:r]), B[r], 0, 63, 80)
+        Kg, Vg = _gpu_caches(R, B[r])
+        b = np.arange(B[r])
+        for s in range(6):
+            _, logits, dump = R.history[s]
+            xs = dump.double().numpy()
+            for l in range(m.num_layers):
+                out, kn, vn = oracle_layer(om, l, xs[l], pos + s, Kg[l], Vg[l])
+                errs = [rel_err(Kg[l][b, pos + s], kn), rel_err(Vg[l][b, pos + s], vn)]
+                if l + 1 < m.num_layers:
+                    errs.append(rel_err(xs[l + 1], out))
+                else:
+                    errs.append(rel_err(logits.double().numpy(), OM.lm_head(m, om.head, out)))
+                assert max(errs) <= TOL, (r, s, l, errs)
         # after the switch back the ring restarted: the log tail is a fresh FIFO schedule
         own = OS.owner_map(8, 2)
         log = R.ctx.fetch_log()
