@@ -191,6 +191,22 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
  * replicated tensors, CaS staging + flags, workspaces, the fetch stream and events. */
 sidp_status sidp_alloc(sidp_ctx* ctx);
 
+/* Bytes of the owned-weight arena this context lays out (its owned layers' pooled blobs,
+ * contiguous; "each GPU holds only its own layers"): what sidp_alloc_owned needs.
+ * Host-only; valid after sidp_init. */
+sidp_status sidp_owned_bytes(const sidp_ctx* ctx, uint64_t* bytes);
+
+/* sidp_alloc with a CALLER-OWNED owned-weight arena (SURVEY.md §8(b) sidp_alloc_owned; e.g. a
+ * torch allocation): arena is device memory on the context's device, >= sidp_owned_bytes bytes,
+ * 256-byte aligned.  The library lays the owned layers out in it (sidp_init_weights_synthetic
+ * fills them), never frees it, and exports it to peers as its allocation's IPC handle plus the
+ * arena's offset inside that allocation, so an arena carved from a larger (caching-allocator)
+ * segment works.  The caller keeps it alive and unmodified until sidp_destroy.  Everything else
+ * (local layers, slots, workspaces, CaS staging) is allocated as by sidp_alloc.  SIDP_EINVAL
+ * (nothing allocated) if the arena is too small, misaligned or not device memory of the
+ * context's device; otherwise as sidp_alloc. */
+sidp_status sidp_alloc_owned(sidp_ctx* ctx, void* arena, uint64_t bytes);
+
 /* Alternative to sidp_alloc for a serve-only rank: allocate only the owned-weight arena (and a
  * CaS flag block so the exported blob is well formed; no local per-layer parts).
  * The rank owns, initialises (sidp_init_weights_synthetic fills only its owned and local

@@ -68,6 +68,8 @@ _PI32 = C.POINTER(C.c_int32)
 SIGNATURES = {
     "sidp_init": [C.POINTER(ModelDesc), C.POINTER(Config), C.POINTER(_P)],
     "sidp_alloc": [_P],
+    "sidp_owned_bytes": [_P, C.POINTER(C.c_uint64)],
+    "sidp_alloc_owned": [_P, _P, C.c_uint64],
     "sidp_alloc_serve_only": [_P],
     "sidp_alloc_serve_only_alias": [_P, _P],
     "sidp_init_weights_synthetic": [_P, _P],

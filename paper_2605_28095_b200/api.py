@@ -91,8 +91,20 @@ class Context:
             self.alloc()
 
     # ---- lifecycle
-    def alloc(self):
-        A.check(A.lib().sidp_alloc(self.h), "sidp_alloc")
+    def alloc(self, arena=None):
+        """arena: optional caller-owned device buffer (e.g. a torch uint8 tensor of at least
+        owned_bytes()) that holds this rank's owned layers (sidp_alloc_owned); kept referenced."""
+        if arena is None:
+            A.check(A.lib().sidp_alloc(self.h), "sidp_alloc")
+            return
+        self._arena = arena
+        A.check(A.lib().sidp_alloc_owned(self.h, _ptr(arena), arena.numel() * arena.element_size()),
+                "sidp_alloc_owned")
+
+    def owned_bytes(self) -> int:
+        n = C.c_uint64()
+        A.check(A.lib().sidp_owned_bytes(self.h, C.byref(n)), "sidp_owned_bytes")
+        return n.value
 
     def alloc_serve_only(self, alias_of=None):
         """Owner-only rank: allocates and exports its arena, never computes (sidp.h).  alias_of

@@ -57,8 +57,33 @@ struct HandleBlob {
   uint64_t arena_bytes, cas_bytes;
   cudaIpcMemHandle_t arena_h, cas_h;
   int32_t has_arena, has_cas;
+  uint64_t arena_off;       // arena - base of its allocation (a caller-owned arena, e.g. torch's)
   unsigned char uuid[16];   // the GPU (cudaDeviceProp::uuid): peers on the same GPU share it
 };
+
+// Offset of p inside its device allocation (cuMemGetAddressRange through the runtime's driver
+// entry point, like cuTensorMapEncodeTiled: the library links no libcuda).  A CUDA IPC handle
+// names the whole allocation, so a caller-owned arena inside a larger (e.g. torch caching
+// allocator) segment is exported as handle + offset.  0 when p is an allocation base.
+uint64_t arena_alloc_offset(const void* p) {
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<RangeFn>(f);
+    cudaGetLastError();
+  }
+  if (!fn || !p) return 0;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return 0;
+  return (uint64_t)(reinterpret_cast<uintptr_t>(p) - (uintptr_t)base);
+}
 
 bool device_uuid(int device, unsigned char (&out)[16]) {
   cudaDeviceProp p{};
@@ -160,6 +185,7 @@ struct sidp_ctx {
   int64_t gdelta = -1;
   bool same_device_peer = false;                // a peer shares this GPU (virtual ranks / 1-GPU IPC)
   bool arena_borrowed = false;                  // serve-only alias: the arena is another ctx's
+  bool arena_external = false;                  // sidp_alloc_owned: the caller owns the arena
   // WaS schedule state
   int64_t fetch_j = 0, compute_k = 0;
   // hybrid fetch: copy-engine parts enqueued so far, and what they need (fetch index order)
@@ -1540,7 +1566,7 @@ void sidp_destroy(sidp_ctx* ctx) {
     }
     if (ctx->fetch_stream) cudaStreamDestroy(ctx->fetch_stream);
     if (ctx->ce_stream) cudaStreamDestroy(ctx->ce_stream);
-    if (ctx->arena_borrowed) ctx->arena = nullptr;
+    if (ctx->arena_borrowed || ctx->arena_external) ctx->arena = nullptr;
     void* ptrs[] = {ctx->arena, ctx->local, ctx->slots, ctx->embed, ctx->g_final, ctx->wlm,
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
@@ -1553,7 +1579,22 @@ void sidp_destroy(sidp_ctx* ctx) {
   delete ctx;
 }
 
-sidp_status sidp_alloc(sidp_ctx* ctx) {
+static sidp_status alloc_impl(sidp_ctx* ctx, void* external_arena, uint64_t external_bytes);
+
+sidp_status sidp_owned_bytes(const sidp_ctx* ctx, uint64_t* bytes) {
+  if (!ctx || !bytes) return fail(SIDP_EINVAL, "null argument");
+  *bytes = (uint64_t)std::max<size_t>(1, ctx->owned_layers.size()) * ctx->pooled_elems * 2;
+  return SIDP_OK;
+}
+
+sidp_status sidp_alloc(sidp_ctx* ctx) { return alloc_impl(ctx, nullptr, 0); }
+
+sidp_status sidp_alloc_owned(sidp_ctx* ctx, void* arena, uint64_t bytes) {
+  if (!ctx || !arena) return fail(SIDP_EINVAL, "null argument");
+  return alloc_impl(ctx, arena, bytes);
+}
+
+static sidp_status alloc_impl(sidp_ctx* ctx, void* external_arena, uint64_t external_bytes) {
   if (!ctx) return fail(SIDP_EINVAL, "null ctx");
   if (ctx->allocated) return fail(SIDP_ESTATE, "already allocated");
   CK(cudaSetDevice(ctx->c.device));
@@ -1575,7 +1616,26 @@ sidp_status sidp_alloc(sidp_ctx* ctx) {
     }                                                              \
   } while (0)
   const size_t pooled_b = ctx->pooled_elems * 2, local_b = ctx->local_elems * 2;
-  DM(ctx->arena, std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b);
+  if (external_arena) {
+    // caller-owned (SURVEY.md §8(b) sidp_alloc_owned): on this device, large enough, aligned for
+    // the 16-byte vector / TMA accesses of every owned layer
+    const size_t need = std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b;
+    if (external_bytes < need)
+      return fail(SIDP_EINVAL, "owned arena of %llu bytes < %zu needed (sidp_owned_bytes)",
+                  (unsigned long long)external_bytes, need);
+    if (reinterpret_cast<uintptr_t>(external_arena) % 256)
+      return fail(SIDP_EINVAL, "owned arena not 256-byte aligned");
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, external_arena) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+        pa.device != ctx->c.device) {
+      cudaGetLastError();
+      return fail(SIDP_EINVAL, "owned arena is not device memory of device %d", ctx->c.device);
+    }
+    ctx->arena = reinterpret_cast<bf16*>(external_arena);
+    ctx->arena_external = true;
+  } else {
+    DM(ctx->arena, std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b);
+  }
   DM(ctx->local, (size_t)ctx->L * local_b);
   if (ctx->R > 0) DM(ctx->slots, (size_t)ctx->S * pooled_b);
   DM(ctx->embed, (size_t)m.vocab * m.hidden * 2);
@@ -1855,6 +1915,7 @@ sidp_status sidp_export_handles(sidp_ctx* ctx, void* blob, size_t* len) {
   h.arena_bytes = std::max<size_t>(1, ctx->owned_layers.size()) * ctx->pooled_elems * 2;
   h.cas_bytes = ctx->cas_bytes;
   h.has_arena = cudaIpcGetMemHandle(&h.arena_h, ctx->arena) == cudaSuccess;
+  h.arena_off = arena_alloc_offset(ctx->arena);
   h.has_cas = cudaIpcGetMemHandle(&h.cas_h, ctx->cas) == cudaSuccess;
   cudaGetLastError();
   device_uuid(ctx->c.device, h.uuid);
@@ -1895,7 +1956,8 @@ sidp_status sidp_import_handles(sidp_ctx* ctx, const void* const* blobs, const s
     cudaError_t e = cudaIpcOpenMemHandle(&p, h.arena_h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return fail(SIDP_EPEER, "IPC open arena of rank %d: %s", q, cudaGetErrorString(e));
     ctx->ipc_opened.push_back(p);
-    ctx->peer_arena[q] = reinterpret_cast<const bf16*>(p);
+    // the handle maps the whole allocation holding the peer's arena: add the arena's offset
+    ctx->peer_arena[q] = reinterpret_cast<const bf16*>(reinterpret_cast<const uint8_t*>(p) + h.arena_off);
     e = cudaIpcOpenMemHandle(&p, h.cas_h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return fail(SIDP_EPEER, "IPC open CaS arena of rank %d: %s", q, cudaGetErrorString(e));
     ctx->ipc_opened.push_back(p);

@@ -26,7 +26,8 @@ def _free_port():
     return p
 
 
-def _run_rank(rank, world, port, mode, pool, batches, steps, q, per_device=False):
+def _run_rank(rank, world, port, mode, pool, batches, steps, q, per_device=False,
+              torch_arena=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -45,7 +46,15 @@ def _run_rank(rank, world, port, mode, pool, batches, steps, q, per_device=False
         mb, max_ctx = max(batches), 80
         b0 = sum(batches[:rank])
         ctx = P.Context(m, rank=rank, world=world, max_batch=mb, max_ctx=max_ctx, seed=SEED,
-                        pool=pool, slots=2, device=dev)
+                        pool=pool, slots=2, device=dev, alloc=False)
+        if torch_arena:
+            # the owned layers in a caller-owned torch buffer, at a nonzero offset inside its
+            # allocation: the peer maps the allocation's IPC handle and adds the offset
+            nb = ctx.owned_bytes()
+            seg = torch.empty(nb + 4096, dtype=torch.uint8, device=f"cuda:{dev}")
+            ctx.alloc(seg[1024:1024 + nb])
+        else:
+            ctx.alloc()
         ctx.init_weights_synthetic()
         kv = P.KVCache(m, mb, max_ctx)
         kv.fill_synthetic(SEED, b0, mb, max_ctx)
@@ -113,13 +122,13 @@ def _replicated(batches, r, steps, pool, compute_sms=0):
     return out
 
 
-def _launch(mode, pool, batches, steps, per_device=False):
+def _launch(mode, pool, batches, steps, per_device=False, torch_arena=False):
     world = len(batches)
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_run_rank, args=(r, world, port, mode, pool, batches, steps, q,
-                                                 per_device))
+                                                 per_device, torch_arena))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -133,11 +142,13 @@ def _launch(mode, pool, batches, steps, per_device=False):
     return res
 
 
-@pytest.mark.parametrize("pool", ["layer", "ffn"])
-def test_was_two_processes_ipc(pool):
+@pytest.mark.parametrize("pool,torch_arena", [("layer", False), ("ffn", False), ("layer", True)])
+def test_was_two_processes_ipc(pool, torch_arena):
+    """torch_arena: each rank's owned layers live in a caller-owned torch buffer
+    (sidp_alloc_owned) inside a larger allocation — exported as handle + offset."""
     from oracle import schedule as OS
     batches = [3, 5]
-    res = _launch("was", pool, batches, 3)
+    res = _launch("was", pool, batches, 3, torch_arena=torch_arena)
     own = OS.owner_map(8, 2)
     for r in range(2):
         out, timeouts, log, budget = res[r]

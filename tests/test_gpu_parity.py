@@ -769,3 +769,52 @@ def test_cas_graph_replay(P, pool, B):
             assert st["graph_replays"] >= steps - 1, st["graph_replays"]
     for R in G + E:
         R.ctx.destroy()
+
+
+def test_alloc_owned_torch_arena(P):
+    """sidp_alloc_owned: the owned layers in a caller-owned torch buffer give
+    bit-identical WaS results to the library-allocated arena (virtual ranks, d = 2), and bad
+    arenas are rejected with SIDP_EINVAL before anything is allocated."""
+    m = MODELS["tiny"].with_layers(4)
+    B = [3, 5]
+
+    outs = []
+    for torch_arena in (False, True):
+        ranks = []
+        for r in range(2):
+            ctx = P.Context(m, rank=r, world=2, max_batch=max(B), max_ctx=80, seed=SEED, alloc=False)
+            nb = ctx.owned_bytes()
+            assert nb > 0
+            if torch_arena:
+                seg = torch.empty(nb + 8192, dtype=torch.uint8, device="cuda")
+                with pytest.raises(P.SidpError):            # too small
+                    ctx.alloc(seg[:nb - 256])
+                with pytest.raises(P.SidpError):            # misaligned
+                    ctx.alloc(seg[8:8 + nb])
+                ctx.alloc(seg[2048:2048 + nb])
+            else:
+                ctx.alloc()
+            ranks.append(ctx)
+        for ctx in ranks:
+            ctx.init_weights_synthetic()
+        blobs = [c.export_handles() for c in ranks]
+        for c in ranks:
+            c.import_handles(blobs)
+        res = []
+        for r, ctx in enumerate(ranks):
+            mb = max(B)
+            kv = P.KVCache(m, mb, 80)
+            kv.fill_synthetic(SEED, sum(B[:r]), mb, 80)
+            bg = np.arange(sum(B[:r]), sum(B[:r]) + B[r])
+            kv.set_pos(gen.positions(SEED, bg, 0, 63))
+            toks = torch.from_numpy(gen.tokens(SEED, bg, m.vocab)).to(torch.int32).cuda()
+            nxt = torch.zeros(mb, dtype=torch.int32, device="cuda")
+            logits = torch.zeros(mb, m.vocab, dtype=torch.float32, device="cuda")
+            ctx.step(toks, nxt, kv, batch=B[r], logits=logits)
+            torch.cuda.synchronize()
+            res.append(logits[:B[r]].cpu().clone())
+        outs.append(res)
+        for c in ranks:
+            c.destroy()
+    for r in range(2):
+        assert torch.equal(outs[0][r], outs[1][r]), r
