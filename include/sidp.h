@@ -175,6 +175,10 @@ typedef struct {
   int32_t compute_sms;      /* SMs the WaS compute grids are sized for (0 = all) */
   double stagger_tick_ns;   /* measured single-reader layer fetch (C-S7 tick; 0 = not measured) */
   uint64_t graph_replays;   /* sidp_step calls that replayed a captured CUDA graph */
+  uint64_t slot_checks;     /* debug SIDP_SLOT_VERIFY=1 (read at sidp_init): landed slots (or slot
+                               parts) compared word for word with the owner's blob before the
+                               layer's first reader */
+  uint64_t slot_mismatches; /* differing 16-byte words found by those checks (0 = verbatim) */
 } sidp_stats_t;
 
 /* ---- lifecycle --------------------------------------------------------------------- */

@@ -57,7 +57,8 @@ class Stats(C.Structure):
                 ("workspace_bytes", C.c_uint64), ("timed_ms", C.c_double * 8),
                 ("timed_launches", C.c_uint64 * 8), ("fetch_sms_held", C.c_int32),
                 ("compute_sms", C.c_int32), ("stagger_tick_ns", C.c_double),
-                ("graph_replays", C.c_uint64)]
+                ("graph_replays", C.c_uint64), ("slot_checks", C.c_uint64),
+                ("slot_mismatches", C.c_uint64)]
 
 
 _P = C.c_void_p

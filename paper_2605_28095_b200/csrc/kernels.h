@@ -319,6 +319,10 @@ cudaError_t ring_free_wait_launch(FetchRing* r, int slot, unsigned long long fil
                                   uint64_t timeout_ns, int* err, cudaStream_t s);
 cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t timeout_ns, int* err,
                                    cudaStream_t s);
+// Debug: compare `bytes` of a landed slot with its owner's source; cnt[0] += 1, cnt[1] +=
+// differing 16-byte words (SIDP_SLOT_VERIFY=1, sidp_stats slot_checks / slot_mismatches).
+cudaError_t slot_verify_launch(const void* slot, const void* src, size_t bytes,
+                               unsigned long long* cnt, cudaStream_t s);
 cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s,
                                 unsigned long long* b = nullptr);
 cudaError_t ring_delay_launch(uint64_t ns, cudaStream_t s);

@@ -492,6 +492,41 @@ cudaError_t ring_ready_wait_launch(FetchRing* r, int slot, int layer, uint64_t t
   return launch_pdl(ring_ready_wait_kernel, dim3(1), dim3(1), 0, s, r, slot, layer, timeout_ns, err);
 }
 
+// Debug (SIDP_SLOT_VERIFY=1): a landed slot (or slot part) compared word for word with the
+// owner's blob it was fetched from, after the ready wait and before the layer's first weight
+// reader — PAPER.md:186 moves the weights verbatim, so any differing 16-byte word is a torn or
+// misplaced fill.  cnt[0] += 1 per check, cnt[1] += differing words, cnt[2] = min differing word.
+static __global__ void slot_verify_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                                          size_t n16, unsigned long long* cnt) {
+  pdl_wait();
+  unsigned long long bad = 0, first = ~0ull;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldcg(a + i), y = __ldcg(b + i);
+    if ((x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w)) {
+      ++bad;
+      first = first < i ? first : i;
+    }
+  }
+  if (first != ~0ull) atomicMin(cnt + 2, first);
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(cnt + 1, bad);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(cnt, 1ull);
+}
+
+cudaError_t slot_verify_launch(const void* slot, const void* src, size_t bytes,
+                               unsigned long long* cnt, cudaStream_t s) {
+  if (bytes % 16 || (reinterpret_cast<uintptr_t>(slot) | reinterpret_cast<uintptr_t>(src)) % 16)
+    return cudaErrorInvalidValue;
+  // a grid within the compute SM budget (the SMs the windowed fetch holds stay its own); the
+  // kernel is force-loaded by ring_preload: a module loaded lazily at its first launch waits
+  // for the device to idle, which never happens while the windowed fetch spins on a release
+  // that this stream posts later (measured: the gate then timed out and later fills tore)
+  return launch_pdl(slot_verify_kernel, dim3(compute_sms()), dim3(512), 0, s,
+                    reinterpret_cast<const uint4*>(slot), reinterpret_cast<const uint4*>(src),
+                    bytes / 16, cnt);
+}
+
 cudaError_t ring_release_launch(unsigned long long* rel, cudaStream_t s, unsigned long long* b) {
   return launch_pdl(ring_release_kernel, dim3(1), dim3(1), 0, s, rel, b);
 }
@@ -518,6 +553,7 @@ cudaError_t ring_preload() {
   if (cudaFuncGetAttributes(&fa, ring_release_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, ring_delay_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncGetAttributes(&fa, ring_ce_done_kernel) != cudaSuccess) e = cudaGetLastError();
+  if (cudaFuncGetAttributes(&fa, slot_verify_kernel) != cudaSuccess) e = cudaGetLastError();
   if (cudaFuncSetAttribute(fetch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)fetch_bulk_smem()) != cudaSuccess)
     e = cudaGetLastError();

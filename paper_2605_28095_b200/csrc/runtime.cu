@@ -186,6 +186,8 @@ struct sidp_ctx {
   bool same_device_peer = false;                // a peer shares this GPU (virtual ranks / 1-GPU IPC)
   bool arena_borrowed = false;                  // serve-only alias: the arena is another ctx's
   bool arena_external = false;                  // sidp_alloc_owned: the caller owns the arena
+  bool slot_verify = false;                     // SIDP_SLOT_VERIFY=1 at sidp_init (debug)
+  unsigned long long* verify_cnt = nullptr;     // device [3]: checks, differing words, lowest
   // WaS schedule state
   int64_t fetch_j = 0, compute_k = 0;
   // hybrid fetch: copy-engine parts enqueued so far, and what they need (fetch index order)
@@ -473,6 +475,20 @@ cudaError_t gemm(sidp_ctx* c, int cls, const bf16* x, int ldx, const bf16* w, in
   return e;
 }
 
+// Debug slot check (SIDP_SLOT_VERIFY=1): the landed copy of component range [off, off + elems)
+// of `layer` (in the slot) against the owner's arena, on the compute stream after the ready
+// wait — i.e. exactly the bytes the layer's GEMMs are about to read.
+cudaError_t slot_verify(sidp_ctx* c, const bf16* slot_blob, int layer, size_t off, size_t elems,
+                        cudaStream_t s) {
+  if (!c->slot_verify || !c->verify_cnt || elems == 0) return cudaSuccess;
+  const bf16* src = c->peer_arena[c->owner[layer]];
+  if (!src) return cudaSuccess;
+  src += (size_t)c->owned_index[layer] * c->pooled_elems;
+  cudaError_t e = sidp::slot_verify_launch(slot_blob + off, src + off, elems * 2, c->verify_cnt, s);
+  count_launch(c);
+  return e;
+}
+
 // Tile-granular slots: before the first kernel reading component `comp` of the remote layer
 // being enqueued, wait for that part's fill (device epoch; checks the part holds the layer);
 // after its last reader, release the part so the next fill of it may start.
@@ -482,6 +498,9 @@ cudaError_t ring_acquire(sidp_ctx* c, int comp, cudaStream_t s) {
   cudaError_t e = sidp::ring_ready_wait_launch(c->ring, vs, c->cur_layer, c->cas_timeout_ns,
                                                c->dev_err, s);
   count_launch(c);
+  if (e == cudaSuccess)
+    e = slot_verify(c, c->slots + (size_t)c->cur_slot * c->pooled_elems, c->cur_layer,
+                    c->comp_off[comp], c->comp_elems[comp], s);
   return e;
 }
 cudaError_t ring_release(sidp_ctx* c, int comp, cudaStream_t s, int comp2 = -1) {
@@ -924,6 +943,7 @@ sidp_status was_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* k
       // the release rides on the kernel after the layer's last weight reader
       CK(sidp::ring_ready_wait_launch(ctx->ring, slot, layer, ctx->cas_timeout_ns, ctx->dev_err, s));
       count_launch(ctx);
+      CK(slot_verify(ctx, pooled, layer, 0, ctx->pooled_elems, s));
       ctx->release_ptr = &ctx->ring->rel[slot];
       st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
       if (st != SIDP_OK) return st;
@@ -934,6 +954,7 @@ sidp_status was_layer(sidp_ctx* ctx, bf16* x, int B, int layer, const sidp_kv* k
       }
     } else {
       CK(cudaStreamWaitEvent(s, ctx->ready_ev[slot], 0));
+      CK(slot_verify(ctx, pooled, layer, 0, ctx->pooled_elems, s));
       st = full_layer(ctx, layer_weights(ctx, pooled, local), x, B, layer, kv, s);
       if (st != SIDP_OK) return st;
       CK(cudaEventRecord(ctx->free_ev[slot], s));   // housekeeper: release after last reader
@@ -1545,6 +1566,7 @@ sidp_status sidp_init(const sidp_model_desc* model, const sidp_config* cfg, sidp
   c->st.mode = c->mode;
   schedule_reset(c);
   if (const char* t = getenv("SIDP_CAS_TIMEOUT_MS")) c->cas_timeout_ns = (uint64_t)atoll(t) * 1000000ull;
+  if (const char* t = getenv("SIDP_SLOT_VERIFY")) c->slot_verify = atoi(t) != 0;
   *out = c;
   return SIDP_OK;
 }
@@ -1571,7 +1593,7 @@ void sidp_destroy(sidp_ctx* ctx) {
                     ctx->rope, ctx->xbuf, ctx->u, ctx->q, ctx->o, ctx->act, ctx->qkv, ctx->amax,
                     ctx->gemm_ws, ctx->counters, ctx->attn_ws, ctx->attn_cnt, ctx->cas,
                     ctx->cas_out, ctx->xfer_cnt, ctx->pace_t0, ctx->ring, ctx->ce_pace_t0,
-                    ctx->rt_base_dev};
+                    ctx->rt_base_dev, ctx->verify_cnt};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (ctx->host_err) cudaFreeHost(const_cast<int*>(ctx->host_err));
@@ -1637,6 +1659,12 @@ static sidp_status alloc_impl(sidp_ctx* ctx, void* external_arena, uint64_t exte
     DM(ctx->arena, std::max<size_t>(1, ctx->owned_layers.size()) * pooled_b);
   }
   DM(ctx->local, (size_t)ctx->L * local_b);
+  if (ctx->slot_verify) {
+    DM(ctx->verify_cnt, 3 * sizeof(unsigned long long));
+    CK(cudaMemset(ctx->verify_cnt, 0, 2 * sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->verify_cnt + 2, 0xff, sizeof(unsigned long long)));
+    CK(sidp::ring_preload());   // loads the verify kernel now, never lazily mid-step
+  }
   if (ctx->R > 0) DM(ctx->slots, (size_t)ctx->S * pooled_b);
   DM(ctx->embed, (size_t)m.vocab * m.hidden * 2);
   DM(ctx->g_final, (size_t)m.hidden * 2);
@@ -2485,6 +2513,14 @@ sidp_status sidp_stats(const sidp_ctx* ctx_c, sidp_stats_t* out) {
   ctx->st.fetch_sms_held = ctx->ring_mode ? ctx->fetch_ctas : 0;
   ctx->st.compute_sms = ctx->compute_sms;
   ctx->st.stagger_tick_ns = ctx->tick_ns;
+  if (ctx->verify_cnt) {
+    unsigned long long v[3] = {0, 0, 0};
+    CK(cudaMemcpy(v, ctx->verify_cnt, sizeof(v), cudaMemcpyDeviceToHost));
+    ctx->st.slot_checks = v[0];
+    ctx->st.slot_mismatches = v[1];
+    if (v[1])
+      fprintf(stderr, "[sidp slot verify] %llu differing 16-byte words, lowest index %llu\n", v[1], v[2]);
+  }
   *out = ctx->st;
   return SIDP_OK;
 }

@@ -818,3 +818,47 @@ def test_alloc_owned_torch_arena(P):
             c.destroy()
     for r in range(2):
         assert torch.equal(outs[0][r], outs[1][r]), r
+
+
+@pytest.mark.parametrize("parts,fetch", [(1, "sm"), (2, "sm"), (1, "ce")])
+def test_was_slot_verify(P, monkeypatch, parts, fetch):
+    """Debug slot check (SIDP_SLOT_VERIFY=1, SURVEY.md §5 slot-checksum mode): every landed slot
+    (whole, or each tile part) is compared word for word with the owner's blob right after its
+    ready wait, before the layer's first reader; over graph-replayed and eager WaS steps every
+    consumption is checked and no word differs (the fetch is verbatim), and the
+    check itself leaves the logits bit-identical."""
+    monkeypatch.setenv("SIDP_SLOT_VERIFY", "1")
+    m = MODELS["tiny"].with_layers(8)
+    d, B, pool = 4, 5, "layer"
+    G = Rank(P, m, rank=0, world=d, B=B, slots=2, pool=pool, slot_parts=parts, fetch_engine=fetch)
+    peers = []
+    for r in range(1, d):
+        c = P.Context(m, rank=r, world=d, max_batch=B, max_ctx=80, seed=SEED, alloc=False, pool=pool)
+        c.alloc_serve_only()
+        c.init_weights_synthetic()
+        peers.append(c)
+    torch.cuda.synchronize()
+    G.ctx.import_handles([G.ctx.export_handles()] + [c.export_handles() for c in peers])
+    steps = 3
+    for s in range(steps):
+        with torch.cuda.stream(G.stream):
+            G.ctx.step(G.toks, G.toks, G.kv, batch=B, stream=G.stream, advance_pos=True)
+        G.stream.synchronize()
+    G.step(); G.finish_step()
+    st = G.ctx.stats()
+    remote = sum(1 for l in range(m.num_layers) if OS.owner_map(m.num_layers, d)[l] != 0)
+    assert st["timeouts"] == 0
+    assert st["slot_checks"] == (steps + 1) * remote * (4 if parts > 1 else 1), st["slot_checks"]
+    assert st["slot_mismatches"] == 0
+    for c in peers:
+        c.destroy()
+    G.ctx.destroy()
+    monkeypatch.delenv("SIDP_SLOT_VERIFY")
+    rep = Rank(P, m, B=B, pool=pool, compute_sms=st["compute_sms"])
+    for s in range(steps):
+        with torch.cuda.stream(rep.stream):
+            rep.ctx.step(rep.toks, rep.toks, rep.kv, batch=B, stream=rep.stream, advance_pos=True)
+        rep.stream.synchronize()
+    rep.step(); rep.finish_step()
+    assert torch.equal(rep.history[0][1], G.history[0][1])
+    rep.ctx.destroy()
