@@ -283,6 +283,33 @@ def north_star_roofline(m, B, ctx_avg, d, peaks, step_ms, remote_bytes=None):
                       "nvlink_gbs": peaks["nvl"]}}
 
 
+def per_remote_layer(ctx0, m, B, W, peaks, layer_bytes, steps):
+    """per remote layer in steady state, T_roof(l) / t_meas(l), T_roof(l) =
+    max(2 P_l B / P_peak, R_l / BW_nvl) and t_meas(l) from the device's %globaltimer stamps: the
+    ring's consume log stamps each remote layer when its ready wait passes (its slot landed and
+    the compute stream reached it), so for two consecutive remote layers l, l+1 of one step
+    t_meas(l) = t(l+1) - t(l) — the period at which the pipeline retires layer l."""
+    cons = ctx0.consume_log()
+    if not cons:
+        return None
+    P = m.hidden * m.qkv_dim + m.q_dim * m.hidden + 3 * m.hidden * m.intermediate
+    t_roof = max(2.0 * P * B / (peaks["tflops"] * 1e12), layer_bytes / (peaks["nvl"] * 1e9))
+    rows = cons[-(m.num_layers - -(-m.num_layers // W)) * steps:]     # the timed steps
+    fr, tm = [], []
+    for a, b in zip(rows, rows[1:]):
+        if b[0] == a[0] + 1 and b[4] > a[4]:           # consecutive remote layers of one step
+            t = (b[4] - a[4]) * 1e-9
+            tm.append(t)
+            fr.append(t_roof / t)
+    if not fr:
+        return None
+    fr.sort()
+    return {"layers": len(fr), "t_roof_us": t_roof * 1e6,
+            "t_meas_us_median": sorted(tm)[len(tm) // 2] * 1e6,
+            "frac_median": fr[len(fr) // 2], "frac_min": fr[0], "frac_max": fr[-1],
+            "how": "t_meas = %globaltimer consume stamps of consecutive remote layers (device ring log)"}
+
+
 # ----------------------------------------------------------------------------- WaS emulation
 def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, peaks):
     """Rank 0 of a W-rank WaS group on ONE GPU (SURVEY.md §8(a) a2-a4 at full size): the W-1
@@ -359,6 +386,8 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
                                  remote_bytes=(m.num_layers - len([l for l in range(m.num_layers)
                                                                     if l % W == 0])) * st["layer_bytes"])
         remote_layers = m.num_layers - len([l for l in range(m.num_layers) if l % W == 0])
+        per_layer = per_remote_layer(ctx0, m, B, W, peaks, st["layer_bytes"], args.emulate_steps) \
+            if args.fetch == "sm" else None
         return {
             "what": f"rank 0 of a {W}-rank WaS group on one B200; the {W - 1} other owners are "
                     "serve-only contexts in local HBM (bench.py was_emulation docstring)",
@@ -380,6 +409,7 @@ def was_emulation(args, P, m, wl, seed, local, stream, kv, tok, B, ctx_len, W, p
                       "frac_of_nvlink_770": (fetch_gbs / peaks["nvl"]) if fetch_gbs else None,
                       "fetch_busy_frac": (remote_layers * f_ms / ms) if f_ms else None},
             "north_star_roofline": ns,
+            "per_remote_layer": per_layer,
             "kernel_us_per_layer": us_layer,
             "footprint_bytes_rank0": {"owned": st["owned_bytes"], "slots": st["slot_bytes"],
                                       "replicated": st["replicated_bytes"],
