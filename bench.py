@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--fetch-sms", type=int, default=24)
     ap.add_argument("--slot-parts", type=int, default=0, choices=[0, 1, 2],
                     help="WaS cache granularity: 1 whole layers, 2 tiles (per-component flags); 0 = 1")
+    ap.add_argument("--paged", action="store_true",
+                    help="paged KV cache (16-token blocks in a shuffled pool, sidp_kv.block_table)")
     ap.add_argument("--no-stagger", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -644,6 +646,7 @@ def _config(args, wl, m, world):
             "reduced": args.layers is not None, "world": world, "slots": args.slots or wl.slots,
             "order": args.order, "pool": args.pool, "fetch": args.fetch,
             "stagger": not args.no_stagger,
+            "kv_layout": "paged, 16-token blocks (shuffled pool)" if args.paged else "contiguous",
             "l2": "no flush needed: per-step working set (weights + KV) >> 126 MB L2",
             "parallelism": f"sidp-dp{world}"}
 
@@ -696,8 +699,13 @@ def main():
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         ctx.init_weights_synthetic(stream=stream)
-        kv = P.KVCache(m, B, max_ctx)
-        kv.fill_synthetic(seed, rank * B, B, ctx_len, stream=stream)
+        if args.paged:
+            nb = -(-max_ctx // P.PagedKVCache.BLOCK)
+            kv = P.PagedKVCache(m, B, max_ctx, B * nb)
+            kv.fill_synthetic(seed, rank * B, B, ctx_len, stream=stream, perm_seed=seed)
+        else:
+            kv = P.KVCache(m, B, max_ctx)
+            kv.fill_synthetic(seed, rank * B, B, ctx_len, stream=stream)
     stream.synchronize()
     if world > 1:
         from paper_2605_28095_b200.orchestrator import exchange_handles

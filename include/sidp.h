@@ -129,7 +129,15 @@ typedef struct {
 } sidp_config;
 
 /* Caller-owned KV cache of this rank (never pooled).
- * k_cache / v_cache: device bf16 [num_layers][max_batch][n_kv_heads][max_ctx][head_dim].
+ * Contiguous (block_table == NULL): k_cache / v_cache device bf16
+ *   [num_layers][max_batch][n_kv_heads][max_ctx][head_dim].
+ * Paged (block_table != NULL; the serving engines' block layout): k_cache /
+ *   v_cache are block pools, device bf16 [num_layers][num_blocks][n_kv_heads][16][head_dim], and
+ *   block_table is device int32 [max_batch][max_blocks]: token t of row b lives in pool block
+ *   block_table[b][t / 16] at slot t % 16.  block_tokens must be 16 (the attention chunk);
+ *   max_blocks * 16 >= max_ctx; every entry the step reads (t <= pos[b]) must be a valid block
+ *   < num_blocks, owned by that row alone.  The table may change between steps (graph replays
+ *   read it on the device); SIDP_EINVAL on bad sizes.
  * pos: device int32[batch], tokens already cached per row; the step writes the new k/v at
  * position pos[b] and attends over [0, pos[b]].  max_pos: host hint >= max_b pos[b]. */
 typedef struct {
@@ -137,6 +145,10 @@ typedef struct {
   void* v_cache;
   const int32_t* pos;
   int32_t max_pos;
+  const int32_t* block_table;   /* NULL: contiguous layout */
+  int32_t block_tokens;         /* 16 when paged */
+  int32_t max_blocks;           /* block_table row stride */
+  int32_t num_blocks;           /* pool blocks per layer */
 } sidp_kv;
 
 /* One decode step of this rank. tokens/next: device int32[batch].  batch == 0 marks a

@@ -40,7 +40,8 @@ class Config(C.Structure):
 
 class KV(C.Structure):
     _fields_ = [("k_cache", C.c_void_p), ("v_cache", C.c_void_p), ("pos", C.c_void_p),
-                ("max_pos", C.c_int32)]
+                ("max_pos", C.c_int32), ("block_table", C.c_void_p), ("block_tokens", C.c_int32),
+                ("max_blocks", C.c_int32), ("num_blocks", C.c_int32)]
 
 
 class Batch(C.Structure):

@@ -63,6 +63,78 @@ class KVCache:
                                                  t_id, l, _stream_ptr(stream)), "gen_kv")
 
 
+class PagedKVCache:
+    """Caller-owned PAGED KV cache (sidp_kv.block_table): per layer a pool of 16-token blocks,
+    bf16 [L][num_blocks][n_kv][16][head_dim] x 2, and a device block table int32
+    [max_batch][max_blocks] (token t of row b in block table[b][t // 16], slot t % 16)."""
+    BLOCK = 16
+
+    def __init__(self, m, max_batch: int, max_ctx: int, num_blocks: int, device="cuda"):
+        import torch
+        self.max_blocks = (max_ctx + self.BLOCK - 1) // self.BLOCK
+        self.num_blocks = num_blocks
+        shape = (m.num_layers, num_blocks, m.n_kv_heads, self.BLOCK, m.head_dim)
+        self.k = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.v = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.table = torch.zeros(max_batch, self.max_blocks, dtype=torch.int32, device=device)
+        self.pos = torch.zeros(max_batch, dtype=torch.int32, device=device)
+        self.max_pos = 0
+        self.max_batch, self.max_ctx = max_batch, max_ctx
+
+    @classmethod
+    def from_contiguous(cls, kv: "KVCache", m, seed: int = 0, spare: int = 0):
+        """The same cache contents in shuffled blocks: row b's c-th block goes to pool block
+        perm[b * max_blocks + c] (a seeded permutation of num_blocks = B * max_blocks + spare)."""
+        import torch
+        B, T = kv.max_batch, kv.max_ctx
+        pk = cls(m, B, T, B * ((T + cls.BLOCK - 1) // cls.BLOCK) + spare, device=kv.k.device)
+        nb = pk.max_blocks
+        g = torch.Generator().manual_seed(seed)
+        perm = torch.randperm(pk.num_blocks, generator=g)[:B * nb]
+        pk.table.copy_(perm.view(B, nb).to(torch.int32))
+        for src, dst in ((kv.k, pk.k), (kv.v, pk.v)):
+            L, _, nkv, _, hd = src.shape
+            pad = torch.zeros(L, B, nkv, nb * cls.BLOCK, hd, dtype=src.dtype, device=src.device)
+            pad[:, :, :, :T] = src
+            blocks = pad.view(L, B, nkv, nb, cls.BLOCK, hd).permute(0, 1, 3, 2, 4, 5)
+            dst[:, perm.to(src.device)] = blocks.reshape(L, B * nb, nkv, cls.BLOCK, hd)
+        pk.pos.copy_(kv.pos)
+        pk.max_pos = kv.max_pos
+        return pk
+
+    def fill_synthetic(self, seed: int, b0: int, batch: int, T: int, stream=None, perm_seed: int = 0):
+        """K12 fill of positions [0, T) of rows [0, batch) (logical rows b0 + b), one layer at a
+        time through a contiguous staging buffer, into a seeded shuffle of the pool's blocks."""
+        import torch
+        L, nb, B = self.k.shape[0], self.max_blocks, self.max_batch
+        nkv, hd = self.k.shape[2], self.k.shape[4]
+        g = torch.Generator().manual_seed(perm_seed)
+        perm = torch.randperm(self.num_blocks, generator=g)[:B * nb]
+        self.table.copy_(perm.view(B, nb).to(torch.int32))
+        perm = perm.to(self.k.device)
+        stage = torch.zeros(B, nkv, nb * self.BLOCK, hd, dtype=torch.bfloat16, device=self.k.device)
+        for l in range(L):
+            for t_id, pool in ((18, self.k), (19, self.v)):   # gen.KCACHE / gen.VCACHE
+                A.check(A.lib().sidp_test_gen_kv(_ptr(stage), batch, nkv, nb * self.BLOCK, hd, T, b0,
+                                                 seed, t_id, l, _stream_ptr(stream)), "gen_kv")
+                blocks = stage.view(B, nkv, nb, self.BLOCK, hd).permute(0, 2, 1, 3, 4)
+                pool[l][perm] = blocks.reshape(B * nb, nkv, self.BLOCK, hd)
+
+    def to_contiguous(self, layer, which="k"):
+        """Layer `layer`'s cache gathered back into [max_batch][n_kv][max_blocks*16][hd]."""
+        pool = (self.k if which == "k" else self.v)[layer]
+        x = pool[self.table.long()]                      # [B][nb][nkv][16][hd]
+        B, nb, nkv, bt, hd = x.shape
+        return x.permute(0, 2, 1, 3, 4).reshape(B, nkv, nb * bt, hd)
+
+    set_pos = KVCache.set_pos
+    advance = KVCache.advance
+
+    def c(self) -> A.KV:
+        return A.KV(self.k.data_ptr(), self.v.data_ptr(), self.pos.data_ptr(), self.max_pos,
+                    self.table.data_ptr(), self.BLOCK, self.max_blocks, self.num_blocks)
+
+
 class Context:
     def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
                  max_batch=8, max_ctx=128, fetch_sms=24, fetch_engine="sm", stagger=True,

@@ -55,6 +55,16 @@ __host__ __device__ inline int partial_nseg(const PartialSrc& p, int m, int n) {
          partial_cluster_of(t * p.nks, p.total_kb, p.clusters) + 1;
 }
 
+// Paged KV (16-token blocks, sidp_kv.block_table): element offset of (row b, kv head g, token t)
+// in a layer's cache — contiguous [B][nkv][smax][hd], or the block pool [nblk][nkv][16][hd].
+constexpr int kKvBlock = 16;
+__host__ __device__ inline size_t kv_off(const int32_t* bt, int bt_stride, int nkv, int smax,
+                                         int hd, int b, int g, int t) {
+  if (!bt) return (((size_t)b * nkv + g) * smax + t) * hd;
+  const size_t blk = (size_t)bt[(size_t)b * bt_stride + t / kKvBlock];
+  return ((blk * nkv + g) * kKvBlock + (t % kKvBlock)) * hd;
+}
+
 // Destination of the fused QKV epilogue (rows of W_qkv = [q heads | k heads | v heads]).
 struct QkvEpi {
   bf16* q;                       // [M, nq, hd]
@@ -64,6 +74,7 @@ struct QkvEpi {
   const bf16* gq; const bf16* gk;   // qk-norm gains (null = off)
   float eps;
   int nq, nkv, hd, smax;
+  const int32_t* bt; int bt_stride;   // paged KV (null: contiguous)
 };
 
 // A CaS flag wait folded into a consumer kernel's prologue (no standalone wait launch): the
@@ -196,8 +207,9 @@ struct QkvPostArgs {
   const float2* rope;                           // [max_pos, hd/2] (cos, sin)
   const int32_t* pos;
   bf16* q;
-  bf16* kc; bf16* vc;                           // [Bmax, nkv, Smax, hd]
+  bf16* kc; bf16* vc;                           // [Bmax, nkv, Smax, hd] (or block pools)
   int smax;
+  const int32_t* bt; int bt_stride;             // paged KV: block table [B][bt_stride] (null: contiguous)
   PartialSrc part;                              // part.ws != null: qkv is the sum of these slices
   const bf16* bias;                             // added in the partial form only (else by the GEMM)
   int ldqkv;                                    // qkv row stride in floats (0 = (nq + 2 nkv) hd)
@@ -212,6 +224,7 @@ struct AttnArgs {
   bf16* o;                    // [B, nq*hd], row stride ldo (0 = nq*hd; may be a peer VA)
   int ldo;
   int B, nq, nkv, hd, smax;
+  const int32_t* bt; int bt_stride;   // paged KV: block table [B][bt_stride], 16-token blocks
   int max_tokens;             // host hint: max_b (pos_b + 1) <= smax (sizes the grid)
   float* ws; size_t ws_bytes; // partials of (b, g) pairs split across CTAs
   int* cnt; int n_cnt;        // [B * nkv] arrival counters, zero between launches

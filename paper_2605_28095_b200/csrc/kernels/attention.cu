@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256, 4) qkv_post_kernel(QkvPostArgs a) {
     } else {
       const int g = is_v ? head - a.nq - a.nkv : head - a.nq;
       bf16* cache = is_v ? a.vc : a.kc;
-      dst = cache + (((size_t)b * a.nkv + g) * a.smax + pos) * HD;
+      dst = cache + kv_off(a.bt, a.bt_stride, a.nkv, a.smax, HD, b, g, pos);
     }
     if constexpr (E == 2) {
       *reinterpret_cast<__nv_bfloat162*>(dst + i0) = __floats2bfloat162_rn(x1[hh][0], x1[hh][1]);
@@ -201,6 +201,7 @@ struct AttnParams {
   float* ws;                 // [C][2 sides][16 rows][HD + 2] partials of split (b, g) pairs
   int* cnt;                  // [B * nkv] arrival counters of split pairs (zero between launches)
   int B, nq, nkv, smax;
+  const int32_t* bt; int bt_stride;   // paged KV (16-token blocks == kChunk), null: contiguous
   int pair_mode;             // grid == B * nkv: one whole (b, g) pair per CTA
   int kv_evict;              // K/V loads carry an L2 evict-first policy
   int pre_wait;              // pair mode: first ring chunks requested before the PDL wait
@@ -319,14 +320,15 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     const int b0 = blockIdx.x / p.nkv, g0 = blockIdx.x % p.nkv;
     const int pos_pre = p.pos[b0];
     if ((warp + (ST - 2) * kWarps + 1) * kChunk <= pos_pre) {
-      const bf16* kb0 = p.kc + ((size_t)b0 * p.nkv + g0) * p.smax * HD;
-      const bf16* vb0 = p.vc + ((size_t)b0 * p.nkv + g0) * p.smax * HD;
+      const bf16* kb0 = p.kc;   // + the chunk's first token below (contiguous or paged)
+      const bf16* vb0 = p.vc;
       bf16* wb = reinterpret_cast<bf16*>(smem) + (size_t)warp * ST * 2 * TILE;
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
       for (int j = 0; j < ST - 1; ++j) {
         const int t0 = (warp + j * kWarps) * kChunk;
+        const size_t co = kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b0, g0, t0);
         bf16* sk = wb + j * 2 * TILE;
         bf16* sv = sk + TILE;
 #pragma unroll
@@ -335,11 +337,11 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
           const int row = e / CPR, cc = e % CPR;
           const int sw = (cc ^ (row & 7));
           if (p.kv_evict) {
-            cp_async16_ef(sk + row * HD + sw * 8, kb0 + (size_t)(t0 + row) * HD + cc * 8, pol);
-            cp_async16_ef(sv + row * HD + sw * 8, vb0 + (size_t)(t0 + row) * HD + cc * 8, pol);
+            cp_async16_ef(sk + row * HD + sw * 8, kb0 + co + (size_t)row * HD + cc * 8, pol);
+            cp_async16_ef(sv + row * HD + sw * 8, vb0 + co + (size_t)row * HD + cc * 8, pol);
           } else {
-            cp_async16(sk + row * HD + sw * 8, kb0 + (size_t)(t0 + row) * HD + cc * 8);
-            cp_async16(sv + row * HD + sw * 8, vb0 + (size_t)(t0 + row) * HD + cc * 8);
+            cp_async16(sk + row * HD + sw * 8, kb0 + co + (size_t)row * HD + cc * 8);
+            cp_async16(sv + row * HD + sw * 8, vb0 + co + (size_t)row * HD + cc * 8);
           }
         }
         cp_async_commit();
@@ -421,8 +423,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     // ------------------------------------------------ one piece: chunks [lo, hi) of (b, g)
     const int n_tok = p.pos[b] + 1;
     bf16* wbuf = wring + (size_t)warp * ST * 2 * TILE;   // [stage][K|V]
-    const bf16* kbase = p.kc + ((size_t)b * p.nkv + g) * p.smax * HD;
-    const bf16* vbase = p.vc + ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* kbase = p.kc;   // + the chunk's first token (kv_off: contiguous or paged)
+    const bf16* vbase = p.vc;
     uint32_t qa[HD / 16][4];
     {
       const bf16* qb = p.q + ((size_t)b * p.nq + (size_t)g * G) * HD;
@@ -446,6 +448,8 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kvpol));
     auto load_chunk = [&](int stage, int ch) {
       const int t0 = ch * kChunk;
+      // the chunk's 16 tokens are contiguous in both layouts (a paged block is one chunk)
+      const size_t co = kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0);
       bf16* sk = wbuf + stage * 2 * TILE;
       bf16* sv = sk + TILE;
 #pragma unroll
@@ -455,11 +459,11 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
         const int t = min(t0 + row, n_tok - 1);
         const int sw = (cc ^ (row & 7));
         if (p.kv_evict) {
-          cp_async16_ef(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8, kvpol);
-          cp_async16_ef(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8, kvpol);
+          cp_async16_ef(sk + row * HD + sw * 8, kbase + co + (size_t)(t - t0) * HD + cc * 8, kvpol);
+          cp_async16_ef(sv + row * HD + sw * 8, vbase + co + (size_t)(t - t0) * HD + cc * 8, kvpol);
         } else {
-          cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
-          cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+          cp_async16(sk + row * HD + sw * 8, kbase + co + (size_t)(t - t0) * HD + cc * 8);
+          cp_async16(sv + row * HD + sw * 8, vbase + co + (size_t)(t - t0) * HD + cc * 8);
         }
       }
     };
@@ -665,10 +669,12 @@ __global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
     const int b = pr / p.nkv, g = pr % p.nkv;
     const int n_tok = p.pos[b] + 1;
     const int chb = (p.pos[b] + kChunk) / kChunk;
-    const bf16* kbase = p.kc + ((size_t)b * p.nkv + g) * p.smax * HD;
-    const bf16* vbase = p.vc + ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* kbase = p.kc;   // + the chunk's first token (kv_off: contiguous or paged)
+    const bf16* vbase = p.vc;
     auto load_chunk = [&](int stage, int ch) {
       const int t0 = ch * kChunk;
+      // the chunk's 16 tokens are contiguous in both layouts (a paged block is one chunk)
+      const size_t co = kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0);
       bf16* sk = wbuf + stage * 2 * TILE;
       bf16* sv = sk + TILE;
 #pragma unroll
@@ -678,11 +684,11 @@ __global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
         const int t = min(t0 + row, n_tok - 1);
         const int sw = (cc ^ (row & 7));
         if (p.kv_evict) {
-          cp_async16_ef(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8, kvpol);
-          cp_async16_ef(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8, kvpol);
+          cp_async16_ef(sk + row * HD + sw * 8, kbase + co + (size_t)(t - t0) * HD + cc * 8, kvpol);
+          cp_async16_ef(sv + row * HD + sw * 8, vbase + co + (size_t)(t - t0) * HD + cc * 8, kvpol);
         } else {
-          cp_async16(sk + row * HD + sw * 8, kbase + (size_t)t * HD + cc * 8);
-          cp_async16(sv + row * HD + sw * 8, vbase + (size_t)t * HD + cc * 8);
+          cp_async16(sk + row * HD + sw * 8, kbase + co + (size_t)(t - t0) * HD + cc * 8);
+          cp_async16(sv + row * HD + sw * 8, vbase + co + (size_t)(t - t0) * HD + cc * 8);
         }
       }
     };
@@ -815,7 +821,7 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
     const int wctas = (int)std::min<long long>(wslots, (pairs + kWarps - 1) / kWarps);
     AttnParams p{};
     p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ldo = a.ldo > 0 ? (size_t)a.ldo : (size_t)a.nq * a.hd; p.ws = a.ws; p.cnt = a.cnt;
-    p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
+    p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax; p.bt = a.bt; p.bt_stride = a.bt_stride;
     static const int env_evict_w = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
     p.kv_evict = env_evict_w;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
@@ -829,7 +835,7 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   if (ctas < 1) return cudaErrorInvalidValue;
   AttnParams p;
   p.q = a.q; p.kc = a.kc; p.vc = a.vc; p.pos = a.pos; p.o = a.o; p.ldo = a.ldo > 0 ? (size_t)a.ldo : (size_t)a.nq * a.hd; p.ws = a.ws; p.cnt = a.cnt;
-  p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax;
+  p.B = a.B; p.nq = a.nq; p.nkv = a.nkv; p.smax = a.smax; p.bt = a.bt; p.bt_stride = a.bt_stride;
   static const int env_evict = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
   p.kv_evict = env_evict;
   static const int env_pre = getenv("SIDP_ATTN_PRE") ? atoi(getenv("SIDP_ATTN_PRE")) : 1;

@@ -421,7 +421,7 @@ SIDP_DEV void store_phase(const KParams& p, const float* sm, int m0, int n0, int
             dst = e.q + ((size_t)m * e.nq + head) * hd + d;
           } else {
             bf16* cache = region == 1 ? e.kc : e.vc;
-            dst = cache + (((size_t)m * e.nkv + head) * e.smax + posv[t]) * hd + d;
+            dst = cache + kv_off(e.bt, e.bt_stride, e.nkv, e.smax, hd, m, head, posv[t]) + d;
           }
           *reinterpret_cast<uint2*>(dst) = pk;
         }
@@ -575,7 +575,7 @@ SIDP_DEV void qkv_sw_row(const KParams& p, int m, bool valid, int pos, int fbase
       dst = e.q + ((size_t)m * e.nq + head) * hd;
     } else {
       const int g = head - e.nq - (region == 2 ? e.nkv : 0);
-      dst = (region == 1 ? e.kc : e.vc) + (((size_t)m * e.nkv + g) * e.smax + pos) * hd;
+      dst = (region == 1 ? e.kc : e.vc) + (valid ? kv_off(e.bt, e.bt_stride, e.nkv, e.smax, hd, m, g, pos) : 0);
     }
     const bool st = valid && !(p.debug & 4);
     if (region == 2) {

@@ -45,7 +45,7 @@ constexpr int kTimingPool = 8192;
 
 struct GraphKey {
   int batch;
-  const void *tokens, *next, *k_cache, *v_cache, *pos, *pos_out;
+  const void *tokens, *next, *k_cache, *v_cache, *pos, *pos_out, *block_table;
 };
 
 struct HandleBlob {
@@ -529,7 +529,11 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
                       const sidp_kv* kv, const float* qkv_in, cudaStream_t s,
                       const AttnHooks* hk = nullptr) {
   const auto& m = ctx->m;
-  const size_t lstride = (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
+  // per-layer stride: contiguous [max_batch][nkv][max_ctx][hd], or the block pool
+  // [num_blocks][nkv][16][hd] (paged, sidp_kv.block_table)
+  const size_t lstride = kv->block_table
+      ? (size_t)kv->num_blocks * m.n_kv_heads * sidp::kKvBlock * m.head_dim
+      : (size_t)ctx->c.max_batch * m.n_kv_heads * ctx->c.max_ctx * m.head_dim;
   bf16* kc = reinterpret_cast<bf16*>(kv->k_cache) + (size_t)layer * lstride;
   bf16* vc = reinterpret_cast<bf16*>(kv->v_cache) + (size_t)layer * lstride;
   // SIDP_FUSED_QKV: 1 = EPI_QKV (one launch: GEMM + qk-norm + RoPE + KV append; token-major
@@ -574,7 +578,8 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
       count_launch(ctx);
     }
     sidp::QkvEpi qe{ctx->q, kc, vc, kv->pos, ctx->rope, W.g_q, W.g_k, m.rms_eps,
-                    m.n_q_heads, m.n_kv_heads, m.head_dim, ctx->c.max_ctx};
+                    m.n_q_heads, m.n_kv_heads, m.head_dim, ctx->c.max_ctx, kv->block_table,
+                    kv->max_blocks};
     CK(ring_acquire(ctx, C_WQKV, s));
     CK(gemm(ctx, 5, ctx->u, m.hidden, W.wqkv, B, ctx->qkvdim, m.hidden, sidp::EPI_QKV, nullptr,
             0, nullptr, 0, W.b_qkv, s, &qe));
@@ -585,6 +590,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
     qa.qkv = qkv_in; qa.B = B; qa.nq = m.n_q_heads; qa.nkv = m.n_kv_heads; qa.hd = m.head_dim;
     qa.gq = W.g_q; qa.gk = W.g_k; qa.eps = m.rms_eps; qa.rope = ctx->rope; qa.pos = kv->pos;
     qa.q = ctx->q; qa.kc = kc; qa.vc = vc; qa.smax = ctx->c.max_ctx;
+    qa.bt = kv->block_table; qa.bt_stride = kv->max_blocks;
     if (hk && hk->qkv_wait) qa.wait = *hk->qkv_wait;
     if (part.ws) {
       qa.part = part;
@@ -600,6 +606,7 @@ sidp_status attn_part(sidp_ctx* ctx, const LayerW& W, const bf16* x, int B, int 
     aa.ldo = hk->ldo_dst;
   }
   aa.nq = m.n_q_heads; aa.nkv = m.n_kv_heads; aa.hd = m.head_dim; aa.smax = ctx->c.max_ctx;
+  aa.bt = kv->block_table; aa.bt_stride = kv->max_blocks;
   // the split is sized from max_ctx (not the per-step max_pos) so the launch configuration is
   // step-invariant and a captured CUDA graph stays valid; empty splits exit immediately
   aa.max_tokens = ctx->c.max_ctx; aa.ws = ctx->attn_ws; aa.ws_bytes = ctx->attn_ws_bytes;
@@ -906,6 +913,12 @@ sidp_status check_ready(sidp_ctx* ctx) {
 
 sidp_status validate_kv(sidp_ctx* ctx, const sidp_kv* kv, int B) {
   if (!kv || !kv->k_cache || !kv->v_cache || !kv->pos) return fail(SIDP_EINVAL, "kv pointers");
+  if (kv->block_table &&
+      (kv->block_tokens != sidp::kKvBlock || kv->num_blocks <= 0 ||
+       (int64_t)kv->max_blocks * sidp::kKvBlock < ctx->c.max_ctx))
+    return fail(SIDP_EINVAL, "paged KV: block_tokens %d (must be %d), num_blocks %d, max_blocks %d "
+                "x %d < max_ctx %d", kv->block_tokens, sidp::kKvBlock, kv->num_blocks,
+                kv->max_blocks, sidp::kKvBlock, ctx->c.max_ctx);
   if (B > 0 && (kv->max_pos < 0 || kv->max_pos + 1 > ctx->c.max_ctx))
     return fail(SIDP_EINVAL, "max_pos %d out of range (max_ctx %d)", kv->max_pos, ctx->c.max_ctx);
   return SIDP_OK;
@@ -2226,6 +2239,7 @@ static bool graph_key_matches(const sidp_ctx* ctx, const sidp_batch* b) {
                       (ctx->gbatches == ctx->batches && ctx->gdelta == ctx->rt - ctx->rt_base_host);
   return ctx->gexec && k.batch == b->batch && k.tokens == b->tokens && k.next == b->next &&
          k.k_cache == b->kv.k_cache && k.v_cache == b->kv.v_cache && k.pos == b->kv.pos &&
+         k.block_table == b->kv.block_table &&
          k.pos_out == b->pos_out && ctx->gmask == ctx->timed_mask && cas_ok;
 }
 
@@ -2297,7 +2311,8 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
       cudaGraphDestroy(g);
       ctx->graph_launches = ctx->st.launches - l0;
       ctx->st.launches = l0;
-      ctx->gkey = GraphKey{B, b->tokens, b->next, b->kv.k_cache, b->kv.v_cache, b->kv.pos, b->pos_out};
+      ctx->gkey = GraphKey{B, b->tokens, b->next, b->kv.k_cache, b->kv.v_cache, b->kv.pos, b->pos_out,
+                           b->kv.block_table};
       ctx->gslots = slots_now;
       ctx->gmask = ctx->timed_mask;
       ctx->gbatches = ctx->batches;

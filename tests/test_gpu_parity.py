@@ -862,3 +862,67 @@ def test_was_slot_verify(P, monkeypatch, parts, fetch):
     rep.step(); rep.finish_step()
     assert torch.equal(rep.history[0][1], G.history[0][1])
     rep.ctx.destroy()
+
+
+@pytest.mark.parametrize("name,B,ctx,span,layers", [
+    ("tiny", 8, 0, 63, 4), ("tiny-qwen3", 6, 20, 40, 4),
+    ("qwen3-32b", 256, 1000, 24, 2),          # pair-mode / warp-per-pair attention
+    ("llama-3.1-70b", 4, 4000, 90, 2),        # few pairs: split-KV pieces
+    ("qwen3-32b", 1024, 200, 56, 2)])         # many short pairs
+def test_paged_kv_bitwise(P, name, B, ctx, span, layers):
+    """Paged KV (sidp_kv.block_table, 16-token blocks): the same cache contents
+    scattered over a shuffled block pool give BIT-IDENTICAL logits to the contiguous layout over
+    several decode steps (CUDA-graph replays and eager steps; appends crossing block boundaries),
+    and every appended k/v lands in the right block."""
+    m = MODELS[name].with_layers(layers)
+    max_ctx = ctx + span + 8
+    ctxt = P.Context(m, max_batch=B, max_ctx=max_ctx, seed=SEED)
+    ctxt.init_weights_synthetic()
+    kv = P.KVCache(m, B, max_ctx)
+    kv.fill_synthetic(SEED, 0, B, max_ctx)
+    bg = np.arange(B)
+    kv.set_pos(gen.positions(SEED, bg, ctx, span))
+    torch.cuda.synchronize()
+    pk = P.PagedKVCache.from_contiguous(kv, m, seed=7, spare=5)
+    toks = torch.from_numpy(gen.tokens(SEED, bg, m.vocab)).to(torch.int32).cuda()
+    outs = []
+    for cache in (kv, pk):
+        t = toks.clone()
+        nxt = torch.zeros(B, dtype=torch.int32, device="cuda")
+        logits = torch.zeros(B, m.vocab, dtype=torch.float32, device="cuda")
+        res = []
+        for s in range(4):
+            if s < 2:      # graph-replayed steps (no logits), tokens fed back
+                ctxt.step(t, t, cache, batch=B, advance_pos=True)
+                torch.cuda.synchronize()
+                res.append(t.cpu().clone())
+            else:
+                ctxt.step(t, nxt, cache, batch=B, logits=logits, advance_pos=True)
+                torch.cuda.synchronize()
+                res.append(logits.cpu().clone())
+                t = nxt.clone()
+        outs.append(res)
+    for s in range(4):
+        assert torch.equal(outs[0][s], outs[1][s]), s
+    # the appended entries of every layer, gathered back through the block table
+    p0 = torch.from_numpy(gen.positions(SEED, bg, ctx, span)).long()
+    ar = torch.arange(B)
+    for l in range(layers):
+        for which, ref in (("k", kv.k[l]), ("v", kv.v[l])):
+            got = pk.to_contiguous(l, which)
+            for s in range(4):
+                assert torch.equal(got[ar, :, p0 + s].cpu(), ref[ar, :, p0 + s].cpu()), (l, which, s)
+    ctxt.destroy()
+
+
+def test_paged_kv_fused_qkv_epilogue():
+    """The paged KV append also from the fused token-major QKV epilogue (SIDP_FUSED_QKV=1, read
+    once per process): the paged tests re-run in a subprocess with it on."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SIDP_FUSED_QKV="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        __file__, "-k", "paged_kv_bitwise"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
