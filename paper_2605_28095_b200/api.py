@@ -135,6 +135,49 @@ class PagedKVCache:
                     self.table.data_ptr(), self.BLOCK, self.max_blocks, self.num_blocks)
 
 
+class _RowsKV:
+    """A paged cache seen through one block-table row per query row (prefill rows of one
+    sequence share that sequence's blocks)."""
+
+    def __init__(self, kv: "PagedKVCache", table, pos):
+        self.k, self.v, self.table, self.pos = kv.k, kv.v, table, pos
+        self.max_pos = int(pos.max().item()) if pos.numel() else 0
+        self.max_blocks, self.num_blocks = kv.max_blocks, kv.num_blocks
+
+    def c(self) -> A.KV:
+        return A.KV(self.k.data_ptr(), self.v.data_ptr(), self.pos.data_ptr(), self.max_pos,
+                    self.table.data_ptr(), PagedKVCache.BLOCK, self.max_blocks, self.num_blocks)
+
+
+def prefill(ctx: "Context", kv: "PagedKVCache", prompts, stream=None, logits=None,
+            layer_inputs=None):
+    """Prefill as ONE ragged decode step: every prompt token of every
+    sequence is a row whose position is its place in the sequence, whose block-table row is its
+    sequence's, so the step's KV append writes all prompt tokens into the sequence's blocks and
+    each row's attention reads exactly the causal prefix [0, pos] — the library's decode kernels
+    unchanged (attention re-reads the prefix per row: O(T^2) KV bytes, no flash-prefill kernel).
+    prompts: per sequence b (rows 0.. of kv) an int sequence of tokens appended at kv.pos[b].
+    Returns (next token per sequence, the row index of each sequence's last prompt token);
+    kv.pos advances by each prompt's length.  logits / layer_inputs: optional per-row outputs."""
+    import numpy as np
+    import torch
+    dev = kv.k.device
+    lens = [len(p) for p in prompts]
+    pos0 = kv.pos[:len(prompts)].cpu().numpy()
+    seq = np.concatenate([np.full(n, b) for b, n in enumerate(lens)]).astype(np.int64)
+    pos = np.concatenate([pos0[b] + np.arange(n) for b, n in enumerate(lens)]).astype(np.int32)
+    toks = torch.from_numpy(np.concatenate([np.asarray(p, dtype=np.int32) for p in prompts])).to(dev)
+    rows = len(seq)
+    view = _RowsKV(kv, kv.table[torch.from_numpy(seq).to(dev)].contiguous(),
+                   torch.from_numpy(pos).to(dev))
+    nxt = torch.zeros(rows, dtype=torch.int32, device=dev)
+    ctx.step(toks, nxt, view, batch=rows, logits=logits, layer_inputs=layer_inputs, stream=stream)
+    last = np.cumsum(lens) - 1
+    kv.pos[:len(prompts)] += torch.as_tensor(lens, dtype=torch.int32, device=dev)
+    kv.max_pos = int(kv.pos[:len(prompts)].max().item())
+    return nxt[torch.from_numpy(last).to(dev)], last
+
+
 class Context:
     def __init__(self, m, *, rank=0, world=1, slots=2, cas_slots=2, order="exec", pool="layer",
                  max_batch=8, max_ctx=128, fetch_sms=24, fetch_engine="sm", stagger=True,

@@ -926,3 +926,43 @@ def test_paged_kv_fused_qkv_epilogue():
                         __file__, "-k", "paged_kv_bitwise"], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny-qwen3", "tiny-qwen25"])
+def test_prefill_vs_oracle(P, name):
+    """Prefill as one ragged step over a paged cache: prompts of 5, 17 and 33
+    tokens (crossing 16-token blocks) appended to three sequences with existing contexts.  Per
+    layer, teacher-forced (C-N8): every prompt row's layer output and new k/v against the fp64
+    oracle from the GPU's layer input and the sequence's KV state (the oracle attends over the
+    row's causal prefix, the earlier prompt rows' entries included), and the logits."""
+    m = MODELS[name].with_layers(4)
+    S, lens, pos0 = 3, [5, 17, 33], [10, 0, 20]
+    rows, max_ctx = sum(lens), 80
+    ctxt = P.Context(m, max_batch=rows, max_ctx=max_ctx, seed=SEED)
+    ctxt.init_weights_synthetic()
+    pk = P.PagedKVCache(m, S, max_ctx, S * (max_ctx // 16) + 3)
+    pk.fill_synthetic(SEED, 0, S, max_ctx, perm_seed=3)
+    pk.set_pos(pos0)
+    g = np.random.default_rng(5)
+    prompts = [g.integers(0, m.vocab, n) for n in lens]
+    logits = torch.zeros(rows, m.vocab, dtype=torch.float32, device="cuda")
+    dump = torch.zeros(m.num_layers, rows, m.hidden, dtype=torch.bfloat16, device="cuda")
+    nxt, last = P.prefill(ctxt, pk, prompts, logits=logits, layer_inputs=dump)
+    torch.cuda.synchronize()
+    assert pk.pos[:S].cpu().tolist() == [p + n for p, n in zip(pos0, lens)]
+    om = OracleModel(m, SEED)
+    seq = np.concatenate([np.full(n, b) for b, n in enumerate(lens)])
+    pos = np.concatenate([pos0[b] + np.arange(n) for b, n in enumerate(lens)])
+    xs = dump.double().cpu().numpy()
+    lg = logits.double().cpu().numpy()
+    for l in range(m.num_layers):
+        K = pk.to_contiguous(l, "k").permute(0, 2, 1, 3).double().cpu().numpy()[seq]   # [rows][T][nkv][hd]
+        V = pk.to_contiguous(l, "v").permute(0, 2, 1, 3).double().cpu().numpy()[seq]
+        out, kn, vn = oracle_layer(om, l, xs[l], pos, K, V)
+        b = np.arange(rows)
+        errs = [rel_err(K[b, pos], kn), rel_err(V[b, pos], vn)]
+        errs.append(rel_err(xs[l + 1], out) if l + 1 < m.num_layers
+                    else rel_err(lg, OM.lm_head(m, om.head, out)))
+        assert max(errs) <= TOL, (l, errs)
+    assert (nxt.cpu().numpy() == np.argmax(lg[last], axis=1)).all()
+    ctxt.destroy()
