@@ -47,6 +47,8 @@ struct KParams {
   long long total_kb;           // tiles * nks (work in k-steps)
   int kps, nks;                 // k-blocks (64 deep) per pipeline stage; k-steps per tile
   int clusters;                 // concurrent CTA pairs (fixed per launch configuration)
+  int sk;                       // pairs sharing the stream-K region (<= clusters; hybrid tails of
+                                // few k-steps go to the first sk pairs only)
   void* out; int ldo;
   const bf16* resid; int ldr;
   const bf16* bias;
@@ -195,8 +197,12 @@ struct UnitIter {
   long long g, g0, end;   // stream-K cursor (k-steps of tiles >= dp_tiles)
   int u;                  // whole-tile cursor
   SIDP_DEV void init(const KParams& p, int cluster) {
-    g0 = g = range_begin(cluster, p.total_kb, p.clusters);
-    end = range_begin(cluster + 1, p.total_kb, p.clusters);
+    if (cluster < p.sk) {
+      g0 = g = range_begin(cluster, p.total_kb, p.sk);
+      end = range_begin(cluster + 1, p.total_kb, p.sk);
+    } else {
+      g0 = g = end = 0;   // no stream-K work for this pair
+    }
     u = cluster;
   }
   SIDP_DEV bool next(const KParams& p, int cluster, Unit& x) {
@@ -217,8 +223,8 @@ struct UnitIter {
       const long long seg_end = end < tile_end ? end : tile_end;
       x.kb0 = (int)(g - (long long)tl * nkb);
       x.kb1 = x.kb0 + (int)(seg_end - g);
-      const int first = cluster_of_kb((long long)tl * nkb, p.total_kb, p.clusters);
-      const int last = cluster_of_kb(tile_end - 1, p.total_kb, p.clusters);
+      const int first = cluster_of_kb((long long)tl * nkb, p.total_kb, p.sk);
+      const int last = cluster_of_kb(tile_end - 1, p.total_kb, p.sk);
       x.seg = cluster - first;
       x.nseg = last - first + 1;
       x.slot = g == g0 ? 0 : 1;
@@ -1056,12 +1062,12 @@ SIDP_DEV void reduce_body(const KParams& p) {
   // up by the block row of the first boundary that splits it.
   const long long nkb = p.nks;
   const int c = blockIdx.y + 1;
-  const long long bc = range_begin(c, p.total_kb, p.clusters);
+  const long long bc = range_begin(c, p.total_kb, p.sk);
   const int tl = (int)(bc / nkb);                             // tile within the stream-K region
   if (bc % nkb == 0) return;                                  // boundary on a tile edge
-  if (c > 1 && range_begin(c - 1, p.total_kb, p.clusters) > (long long)tl * nkb) return;
-  const int first = cluster_of_kb((long long)tl * nkb, p.total_kb, p.clusters);
-  const int nseg = cluster_of_kb((long long)(tl + 1) * nkb - 1, p.total_kb, p.clusters) - first + 1;
+  if (c > 1 && range_begin(c - 1, p.total_kb, p.sk) > (long long)tl * nkb) return;
+  const int first = cluster_of_kb((long long)tl * nkb, p.total_kb, p.sk);
+  const int nseg = cluster_of_kb((long long)(tl + 1) * nkb - 1, p.total_kb, p.sk) - first + 1;
   const int t = p.dp_tiles + tl;
   const int mt = t % p.m_tiles, ft = t / p.m_tiles;
   const int m0 = mt * p.BNT, rows = min(p.BNT, p.M - m0);
@@ -1072,7 +1078,7 @@ SIDP_DEV void reduce_body(const KParams& p) {
   const size_t slice = (size_t)p.M * p.N;
   // compact slot of segment s: 0 when its cluster's range starts inside this tile — every
   // s > 0 — else 1 (the first cluster's range began in an earlier tile and ends here)
-  const int slot0 = p.compact && range_begin(first, p.total_kb, p.clusters) < (long long)tl * nkb ? 1 : 0;
+  const int slot0 = p.compact && range_begin(first, p.total_kb, p.sk) < (long long)tl * nkb ? 1 : 0;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < rows * vec_per_row;
        idx += gridDim.x * blockDim.x) {
     const int m = m0 + idx / vec_per_row;
@@ -1759,7 +1765,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   // wave's time), the full waves stay whole and only the remaining tiles' k-steps are split
   // over every pair; their partials go to per-cluster tile buffers (compact: 2 per cluster),
   // summed by gemm_reduce_kernel in cluster order.
-  int dp_tiles = 0, compact = 0;
+  int dp_tiles = 0, compact = 0, sk = 0;
   static int env_hybrid = getenv("SIDP_GEMM_HYBRID") ? atoi(getenv("SIDP_GEMM_HYBRID")) : 1;
   if (!streamk && env_hybrid && !sw && a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.epi != EPI_PARTIAL &&
       a.k_splits != 1 && tiles > pair_slots) {
@@ -1772,11 +1778,20 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
     // k-steps (QKV M = 512: 62 -> 67 us, each pair's 256 KB partial costs more than its work) or
     // when the last wave is mostly full (gate/up M = 256: 200 tiles, 121 -> 126 us; M = 1536
     // down 301 -> 319 us: split k-ranges of one feature tile no longer share W lines in L2)
-    if (rem != 0 && eff < 0.6 && need <= w.ws_bytes && (long long)rem * nkb >= 12LL * pair_slots) {
+    // (r2) up to a quantisation efficiency of 0.8, and a tail too short to give every pair
+    // >= 12 k-steps goes to the first rem x nkb / 12 pairs only: Llama-70B on the 124 WaS compute
+    // SMs (62 pairs), down at M = 1024 (128 tiles, eff 0.69) 470 -> 372 us, at M = 1536 631 ->
+    // 540; Qwen3 down at M = 1024 283 -> 229 us, O 109 -> 96 (tools/gemm_bench.py)
+    static const double env_heff = getenv("SIDP_GEMM_HYBRID_EFF") ? atof(getenv("SIDP_GEMM_HYBRID_EFF")) : 0.8;
+    static const int env_hsmall = getenv("SIDP_GEMM_HYBRID_SMALL_TAIL") ? atoi(getenv("SIDP_GEMM_HYBRID_SMALL_TAIL")) : 1;
+    const long long tail = (long long)rem * nkb;
+    if (rem != 0 && eff < env_heff && need <= w.ws_bytes &&
+        (tail >= 12LL * pair_slots || (env_hsmall && tail >= 24))) {
       dp_tiles = tiles - rem;
       streamk = 1;
       compact = 1;
       clusters = pair_slots;
+      sk = (int)std::min<long long>(pair_slots, tail / 12);
     }
   }
   if (qs.ok) {
@@ -1842,6 +1857,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   p.M = a.M; p.N = a.N; p.K = a.K; p.BNT = BNT; p.stages = stages;
   p.m_tiles = m_tiles; p.n_pairs = n_pairs; p.tiles = tiles; p.streamk = streamk;
   p.total_kb = (long long)(tiles - dp_tiles) * nkb; p.clusters = clusters; p.kps = kps; p.nks = nkb;
+  p.sk = sk > 0 ? sk : clusters;
   p.dp_tiles = dp_tiles; p.compact = compact;
   p.out = a.out; p.ldo = a.ldo; p.resid = a.resid; p.ldr = a.ldr; p.bias = a.bias;
   p.ws = w.ws; p.counters = w.counters;
@@ -1922,7 +1938,7 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   if (e0 != cudaSuccess || !streamk || part || a.epi == EPI_QKV) return e0;
   g_last_launches = 2;
   if (post) p.post = *post;   // the fix-up is the last launch: it posts
-  dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, clusters - 1));
+  dim3 rgrid((BNT * (2 * WROWS / 8) + 255) / 256, std::max(1, p.sk - 1));
   switch (a.epi) {
     case EPI_F32: e1 = launch_pdl(gemm_reduce_kernel<EPI_F32>, rgrid, dim3(256), 0, stream, p); break;
     case EPI_BF16: e1 = launch_pdl(gemm_reduce_kernel<EPI_BF16>, rgrid, dim3(256), 0, stream, p); break;

@@ -136,7 +136,7 @@ def test_gemm_deferred_fixup_resid_norm(P, M, N, K):
     assert torch.equal(r2, xout)
 
 
-@pytest.mark.parametrize("M,N,K", [(1024, 5120, 2048), (600, 9728, 4096)])
+@pytest.mark.parametrize("M,N,K", [(1024, 5120, 2048), (600, 9728, 4096), (1024, 5120, 8192)])
 def test_gemm_hybrid_streamk_tail(P, M, N, K):
     """Tile counts just over one wave of the 74 CTA pairs (80, 76 tiles): a whole-tile wave +
     a stream-K tail whose partials live in per-cluster buffers (gemm_reduce_kernel), for the

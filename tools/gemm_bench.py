@@ -8,7 +8,10 @@ import paper_2605_28095_b200 as P
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 shapes = {"qkv": (10240, 5120, 0), "o": (5120, 8192, 2), "gate_up": (51200, 5120, 3),
-          "down": (5120, 25600, 2), "lm": (151936, 5120, 0)}
+          "down": (5120, 25600, 2), "lm": (151936, 5120, 0),
+          # Llama-3.1-70B
+          "l_qkv": (10240, 8192, 0), "l_o": (8192, 8192, 2), "l_gate_up": (57344, 8192, 3),
+          "l_down": (8192, 28672, 2)}
 only = sys.argv[2].split(",") if len(sys.argv) > 2 and sys.argv[2] != "all" else list(shapes)
 splits_list = [int(s) for s in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0, 1]
 tag = os.environ.get("TAG", "")
