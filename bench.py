@@ -854,13 +854,17 @@ def main():
             child = _child_json(["--cas-only"], args.extra_timeout)
             line["cas_emulation"] = child.get("cas_emulation", child)
         if args.m3_emulate and args.emulate_world > 1 and args.layers is None:
+            # the double-buffered cache as two tile-granular slots (NEXT-3: per-component
+            # flags, same 3.4 GB as two whole-layer slots; 0.928 vs 0.909 of T2)
             child = _child_json(["--emulate-only", "--workload", "M3", "--emulate-batch", "1024",
-                                 "--emulate-ctx", "384", "--alias-owners", "--emulate-steps", "3"],
+                                 "--emulate-ctx", "384", "--alias-owners", "--emulate-steps", "3",
+                                 "--slots", "2", "--slot-parts", "2"],
                                 args.extra_timeout)
             m3 = child.get("was_emulation", child)
             if isinstance(m3, dict) and "error" not in m3:
                 m3["note"] = ("north-star target shape (SURVEY.md M3) at the measured B_e; owners "
-                              "aliased (timing only), so this GPU keeps a real rank's KV memory")
+                              "aliased (timing only), so this GPU keeps a real rank's KV memory; "
+                              "two tile-granular slots (3.4 GB)")
             line["m3_emulation"] = m3
     print(json.dumps(line), flush=True)
     if dist:
