@@ -296,7 +296,9 @@ def per_remote_layer(ctx0, m, B, W, peaks, layer_bytes, steps):
         return None
     P = m.hidden * m.qkv_dim + m.q_dim * m.hidden + 3 * m.hidden * m.intermediate
     t_roof = max(2.0 * P * B / (peaks["tflops"] * 1e12), layer_bytes / (peaks["nvl"] * 1e9))
-    rows = cons[-(m.num_layers - -(-m.num_layers // W)) * steps:]     # the timed steps
+    # tile slots log one consumption per part: keep each layer's first (its QKV part)
+    firsts = [c for i, c in enumerate(cons) if i == 0 or c[0] != cons[i - 1][0]]
+    rows = firsts[-(m.num_layers - -(-m.num_layers // W)) * steps:]     # the timed steps
     fr, tm = [], []
     for a, b in zip(rows, rows[1:]):
         if b[0] == a[0] + 1 and b[4] > a[4]:           # consecutive remote layers of one step

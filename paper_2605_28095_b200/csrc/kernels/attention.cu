@@ -320,15 +320,16 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     const int b0 = blockIdx.x / p.nkv, g0 = blockIdx.x % p.nkv;
     const int pos_pre = p.pos[b0];
     if ((warp + (ST - 2) * kWarps + 1) * kChunk <= pos_pre) {
-      const bf16* kb0 = p.kc;   // + the chunk's first token below (contiguous or paged)
-      const bf16* vb0 = p.vc;
+      const size_t pair_off0 = p.bt ? 0 : ((size_t)b0 * p.nkv + g0) * p.smax * HD;
+      const bf16* kb0 = p.kc + pair_off0;   // + the chunk's first token below
+      const bf16* vb0 = p.vc + pair_off0;
       bf16* wb = reinterpret_cast<bf16*>(smem) + (size_t)warp * ST * 2 * TILE;
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
       for (int j = 0; j < ST - 1; ++j) {
         const int t0 = (warp + j * kWarps) * kChunk;
-        const size_t co = kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b0, g0, t0);
+        const size_t co = p.bt ? kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b0, g0, t0) : (size_t)t0 * HD;
         bf16* sk = wb + j * 2 * TILE;
         bf16* sv = sk + TILE;
 #pragma unroll
@@ -423,8 +424,10 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     // ------------------------------------------------ one piece: chunks [lo, hi) of (b, g)
     const int n_tok = p.pos[b] + 1;
     bf16* wbuf = wring + (size_t)warp * ST * 2 * TILE;   // [stage][K|V]
-    const bf16* kbase = p.kc;   // + the chunk's first token (kv_off: contiguous or paged)
-    const bf16* vbase = p.vc;
+    // contiguous: the pair's base once, chunk offsets t0 * HD; paged: per-chunk block lookups
+    const size_t pair_off = p.bt ? 0 : ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* kbase = p.kc + pair_off;
+    const bf16* vbase = p.vc + pair_off;
     uint32_t qa[HD / 16][4];
     {
       const bf16* qb = p.q + ((size_t)b * p.nq + (size_t)g * G) * HD;
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     auto load_chunk = [&](int stage, int ch) {
       const int t0 = ch * kChunk;
       // the chunk's 16 tokens are contiguous in both layouts (a paged block is one chunk)
-      const size_t co = kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0);
+      const size_t co = p.bt ? kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0) : (size_t)t0 * HD;
       bf16* sk = wbuf + stage * 2 * TILE;
       bf16* sv = sk + TILE;
 #pragma unroll
@@ -669,12 +672,14 @@ __global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
     const int b = pr / p.nkv, g = pr % p.nkv;
     const int n_tok = p.pos[b] + 1;
     const int chb = (p.pos[b] + kChunk) / kChunk;
-    const bf16* kbase = p.kc;   // + the chunk's first token (kv_off: contiguous or paged)
-    const bf16* vbase = p.vc;
+    // contiguous: the pair's base once, chunk offsets t0 * HD; paged: per-chunk block lookups
+    const size_t pair_off = p.bt ? 0 : ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* kbase = p.kc + pair_off;
+    const bf16* vbase = p.vc + pair_off;
     auto load_chunk = [&](int stage, int ch) {
       const int t0 = ch * kChunk;
       // the chunk's 16 tokens are contiguous in both layouts (a paged block is one chunk)
-      const size_t co = kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0);
+      const size_t co = p.bt ? kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0) : (size_t)t0 * HD;
       bf16* sk = wbuf + stage * 2 * TILE;
       bf16* sv = sk + TILE;
 #pragma unroll
