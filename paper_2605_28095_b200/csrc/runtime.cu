@@ -2039,6 +2039,22 @@ sidp_status sidp_import_handles(sidp_ctx* ctx, const void* const* blobs, const s
       ctx->tick_ns = (double)ms * 1e6;
       if (ctx->c.fetch_engine == SIDP_FETCH_CE && ctx->c.fetch_pace_gbps > 0.0f)
         ctx->tick_ns = std::max(ctx->tick_ns, (double)bytes / ctx->c.fetch_pace_gbps);
+      // First-contact check: that timed fetch is also compared word for word with its source
+      // (the owner's arena — a peer VA over NVLink on a real group), so a transport that
+      // silently mis-copied peer memory fails here, loudly, instead of corrupting weights.
+      unsigned long long* vc = nullptr;
+      CK(cudaMalloc(&vc, 3 * sizeof(unsigned long long)));
+      CK(cudaMemset(vc, 0, 3 * sizeof(unsigned long long)));
+      CK(sidp::ring_preload());
+      CK(sidp::slot_verify_launch(ctx->slots, src, bytes, vc, ctx->fetch_stream));
+      unsigned long long v[3] = {0, 0, 0};
+      CK(cudaMemcpyAsync(v, vc, sizeof(v), cudaMemcpyDeviceToHost, ctx->fetch_stream));
+      CK(cudaStreamSynchronize(ctx->fetch_stream));
+      cudaFree(vc);
+      if (v[1])
+        return fail(SIDP_EPEER, "the first fetch of layer %d from rank %d differs from its source in "
+                    "%llu 16-byte words (SIDP_FETCH_KIND=ldg or fetch_engine=CE select another "
+                    "transport)", l, ctx->owner[l], v[1]);
     }
   }
   return SIDP_OK;
