@@ -966,3 +966,28 @@ def test_prefill_vs_oracle(P, name):
         assert max(errs) <= TOL, (l, errs)
     assert (nxt.cpu().numpy() == np.argmax(lg[last], axis=1)).all()
     ctxt.destroy()
+
+
+def test_paged_kv_cas_bitwise(P):
+    """Paged KV under CaS (the requester's qkv_post appends and attention reads through the block
+    table while the owners compute the linears): bit-identical to the contiguous layout."""
+    m = MODELS["tiny"].with_layers(4)
+    B = [3, 5]
+    outs = []
+    for paged in (False, True):
+        ranks = _group(P, m, 2, B)
+        for r, R in enumerate(ranks):
+            if paged:
+                R.kv = P.PagedKVCache.from_contiguous(R.kv, m, seed=11 + r, spare=2)
+            R.ctx.set_batches(B)
+            R.ctx.set_mode(1, 0)
+        for s in range(2):
+            for R in ranks:
+                R.step()
+            for R in ranks:
+                R.finish_step()
+        outs.append([[h[1] for h in R.history] for R in ranks])
+        for R in ranks:
+            assert R.ctx.stats()["timeouts"] == 0
+            R.ctx.destroy()
+    assert all(torch.equal(a, b) for ra, rb in zip(outs[0], outs[1]) for a, b in zip(ra, rb))
