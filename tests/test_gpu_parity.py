@@ -991,3 +991,33 @@ def test_paged_kv_cas_bitwise(P):
             assert R.ctx.stats()["timeouts"] == 0
             R.ctx.destroy()
     assert all(torch.equal(a, b) for ra, rb in zip(outs[0], outs[1]) for a, b in zip(ra, rb))
+
+
+def test_paged_kv_rejects_bad_geometry(P):
+    """sidp_kv validation (sidp.h): a block size other than 16 or a table shorter than max_ctx
+    is SIDP_EINVAL before anything is enqueued."""
+    m = MODELS["tiny"].with_layers(2)
+    ctxt = P.Context(m, max_batch=2, max_ctx=64, seed=SEED)
+    ctxt.init_weights_synthetic()
+    pk = P.PagedKVCache(m, 2, 64, 8)
+    pk.set_pos([3, 5])
+    toks = torch.zeros(2, dtype=torch.int32, device="cuda")
+    import paper_2605_28095_b200._abi as A
+
+    class Bad:
+        def __init__(self, **over):
+            self.pos, self.max_pos, self.over = pk.pos, pk.max_pos, over
+
+        def c(self):
+            f = dict(block_tokens=16, max_blocks=pk.max_blocks, num_blocks=pk.num_blocks)
+            f.update(self.over)
+            return A.KV(pk.k.data_ptr(), pk.v.data_ptr(), pk.pos.data_ptr(), pk.max_pos,
+                        pk.table.data_ptr(), f["block_tokens"], f["max_blocks"], f["num_blocks"])
+
+    for over in (dict(block_tokens=32), dict(max_blocks=2), dict(num_blocks=0)):
+        with pytest.raises(P.SidpError) as e:
+            ctxt.step(toks, toks, Bad(**over), batch=2)
+        assert e.value.status == -1, over
+    ctxt.step(toks, toks, pk, batch=2)     # the valid geometry runs
+    torch.cuda.synchronize()
+    ctxt.destroy()
