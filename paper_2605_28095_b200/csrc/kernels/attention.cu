@@ -754,6 +754,172 @@ __global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
   }
 }
 
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// One 16-token chunk for a group of exactly 8 query heads, transposed: S^T = K Q^T (m16n8k16 with
+// the 16 tokens as rows, K as the A operand, the 8 heads as the n = 8 columns) and O^T += V^T P^T
+// (V^T as A through ldmatrix.trans, P^T as B through movmatrix.trans of S^T's fragments).  The
+// padded form (Q as A, 16 rows of which 8 are real heads) spends half its MMAs and exp2s on
+// padding; here every MMA row and every exp2 is a real (token, head).  Per thread: heads 2tq,
+// 2tq+1 (their running max / sum), tokens gid and gid + 8 of the chunk.
+template <int HD>
+__device__ __forceinline__ void attn_chunk8(const uint32_t (&qb)[HD / 16][2], uint32_t skb,
+                                            uint32_t svb, int t0, int n_tok, float scale_log2,
+                                            float (&ot)[HD / 16][4], float (&mh)[2],
+                                            float (&lh)[2], int lane) {
+  const int gid = lane >> 2;
+  const int mat = lane >> 3, r = lane & 7;
+  float sc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int tok = (mat & 1) * 8 + r, cc = kk * 2 + (mat >> 1);
+    uint32_t a[4];
+    ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, a[0], a[1], a[2], a[3]);
+    mma_bf16(sc, a, qb[kk][0], qb[kk][1]);
+  }
+  // mask, per-head online softmax (exp2 domain); a head's 16 tokens live in the 8 lanes of
+  // its tq column x 2 rows
+  float mx[2];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int tok = t0 + gid + (e >> 1) * 8;
+    sc[e] = tok < n_tok ? sc[e] * scale_log2 : -INFINITY;
+  }
+  mx[0] = fmaxf(sc[0], sc[2]);
+  mx[1] = fmaxf(sc[1], sc[3]);
+  float alpha[2], muse[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
+    const float mnew = fmaxf(mh[h], mx[h]);
+    muse[h] = mnew == -INFINITY ? 0.0f : mnew;
+    alpha[h] = exp2f(mh[h] - muse[h]);
+    mh[h] = mnew;
+    lh[h] *= alpha[h];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    sc[e] = exp2f(sc[e] - muse[e & 1]);
+    lh[e & 1] += sc[e];
+  }
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    ot[mt][0] *= alpha[0];
+    ot[mt][1] *= alpha[1];
+    ot[mt][2] *= alpha[0];
+    ot[mt][3] *= alpha[1];
+  }
+  const uint32_t b0 = movmatrix_trans(pack_bf16(sc[0], sc[1]));   // P^T, tokens 0-7
+  const uint32_t b1 = movmatrix_trans(pack_bf16(sc[2], sc[3]));   // P^T, tokens 8-15
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    const int tok = (mat >> 1) * 8 + r, cc = mt * 2 + (mat & 1);
+    uint32_t a[4];
+    ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, a[0], a[1], a[2], a[3]);
+    mma_bf16(ot[mt], a, b0, b1);
+  }
+}
+
+// attn_warp_kernel for G = 8 (Qwen3-32B, Llama-3.1-70B, Qwen2.5-72B: 64 / 8 heads) with the
+// transposed chunk math above; same partition, ring and loads.
+template <int HD, int ST>
+__global__ void __launch_bounds__(128) attn_warp8_kernel(const AttnParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int CPR = HD / 8;
+  constexpr int TILE = kChunk * HD;
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tq = lane & 3;
+  const int pairs = p.B * p.nkv;
+  bf16* wbuf = reinterpret_cast<bf16*>(smem) + (size_t)warp * ST * 2 * TILE;
+  uint64_t kvpol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kvpol));
+  for (int pr = blockIdx.x * kWarps + warp; pr < pairs; pr += gridDim.x * kWarps) {
+    const int b = pr / p.nkv, g = pr % p.nkv;
+    const int n_tok = p.pos[b] + 1;
+    const int chb = (p.pos[b] + kChunk) / kChunk;
+    const size_t pair_off = p.bt ? 0 : ((size_t)b * p.nkv + g) * p.smax * HD;
+    const bf16* kbase = p.kc + pair_off;
+    const bf16* vbase = p.vc + pair_off;
+    auto load_chunk = [&](int stage, int ch) {
+      const int t0 = ch * kChunk;
+      const size_t co = p.bt ? kv_off(p.bt, p.bt_stride, p.nkv, p.smax, HD, b, g, t0) : (size_t)t0 * HD;
+      bf16* sk = wbuf + stage * 2 * TILE;
+      bf16* sv = sk + TILE;
+#pragma unroll
+      for (int it = 0; it < (kChunk * CPR) / 32; ++it) {
+        const int e = it * 32 + lane;
+        const int row = e / CPR, cc = e % CPR;
+        const int t = min(t0 + row, n_tok - 1);
+        const int sw = (cc ^ (row & 7));
+        if (p.kv_evict) {
+          cp_async16_ef(sk + row * HD + sw * 8, kbase + co + (size_t)(t - t0) * HD + cc * 8, kvpol);
+          cp_async16_ef(sv + row * HD + sw * 8, vbase + co + (size_t)(t - t0) * HD + cc * 8, kvpol);
+        } else {
+          cp_async16(sk + row * HD + sw * 8, kbase + co + (size_t)(t - t0) * HD + cc * 8);
+          cp_async16(sv + row * HD + sw * 8, vbase + co + (size_t)(t - t0) * HD + cc * 8);
+        }
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < ST - 1; ++j) {
+      if (j < chb) load_chunk(j, j);
+      cp_async_commit();
+    }
+    uint32_t qb[HD / 16][2];   // B = Q^T: (dims 2tq.., head gid) and (dims 2tq + 8.., head gid)
+    {
+      const bf16* qr = p.q + ((size_t)b * p.nq + (size_t)g * 8 + gid) * HD + 2 * tq;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        qb[kk][0] = *reinterpret_cast<const uint32_t*>(qr + kk * 16);
+        qb[kk][1] = *reinterpret_cast<const uint32_t*>(qr + kk * 16 + 8);
+      }
+    }
+    float ot[HD / 16][4];
+#pragma unroll
+    for (int i = 0; i < HD / 16; ++i) ot[i][0] = ot[i][1] = ot[i][2] = ot[i][3] = 0.0f;
+    float mh[2] = {-INFINITY, -INFINITY};
+    float lh[2] = {0.0f, 0.0f};
+    for (int ch = 0; ch < chb; ++ch) {
+      const int cn = ch + ST - 1;
+      if (cn < chb) load_chunk(cn % ST, cn);
+      cp_async_commit();
+      cp_async_wait<ST - 1>();
+      __syncwarp();
+      const bf16* sk = wbuf + (ch % ST) * 2 * TILE;
+      attn_chunk8<HD>(qb, smem_u32(sk), smem_u32(sk + TILE), ch * kChunk, n_tok, p.scale_log2,
+                      ot, mh, lh, lane);
+      __syncwarp();
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      lh[h] += __shfl_xor_sync(0xffffffffu, lh[h], 4);
+      lh[h] += __shfl_xor_sync(0xffffffffu, lh[h], 8);
+      lh[h] += __shfl_xor_sync(0xffffffffu, lh[h], 16);
+    }
+    // o[b][g * 8 + head][dim] = O^T[dim][head] / L[head]
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float L = lh[h];
+      bf16* dst = p.o + (size_t)b * p.ldo + (size_t)(g * 8 + 2 * tq + h) * HD + gid;
+#pragma unroll
+      for (int mt = 0; mt < HD / 16; ++mt) {
+        dst[mt * 16] = f_to_bf16(L > 0.0f ? ot[mt][h] / L : 0.0f);
+        dst[mt * 16 + 8] = f_to_bf16(L > 0.0f ? ot[mt][2 + h] / L : 0.0f);
+      }
+    }
+  }
+}
+
 int g_sms = 0;
 thread_local int g_attn_launches = 0;
 
@@ -820,8 +986,13 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
     if (first_on_device(wattr))
       cudaFuncSetAttribute(attn_warp_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
+    static const int env_swap = getenv("SIDP_ATTN_SWAP") ? atoi(getenv("SIDP_ATTN_SWAP")) : 1;
+    const bool swap8 = env_swap && a.nq == 8 * a.nkv;
     int wper = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, attn_warp_kernel<HD, ST>, 128, ring);
+    if (swap8)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, attn_warp8_kernel<HD, ST>, 128, ring);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, attn_warp_kernel<HD, ST>, 128, ring);
     const long long wslots = (long long)compute_sms() * std::max(1, wper);
     const int wctas = (int)std::min<long long>(wslots, (pairs + kWarps - 1) / kWarps);
     AttnParams p{};
@@ -830,6 +1001,8 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
     static const int env_evict_w = getenv("SIDP_ATTN_EVICT") ? atoi(getenv("SIDP_ATTN_EVICT")) : 1;
     p.kv_evict = env_evict_w;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
+    if (swap8)
+      return launch_pdl(attn_warp8_kernel<HD, ST>, dim3(wctas), dim3(128), ring, s, p);
     return launch_pdl(attn_warp_kernel<HD, ST>, dim3(wctas), dim3(128), ring, s, p);
   }
   int ctas = (int)cl;
@@ -884,6 +1057,9 @@ cudaError_t attention_preload() {
 #define SIDP_PRELOAD_ATTN(hd, st)                                                                \
   if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError();    \
   if (cudaFuncGetAttributes(&fa, attn_warp_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError(); \
+  if (cudaFuncGetAttributes(&fa, attn_warp8_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError(); \
+  if (cudaFuncSetAttribute(attn_warp8_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           200 * 1024) != cudaSuccess) e = cudaGetLastError();                     \
   if (cudaFuncSetAttribute(attn_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                            200 * 1024) != cudaSuccess) e = cudaGetLastError();                     \
   if (cudaFuncSetAttribute(attn_warp_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
