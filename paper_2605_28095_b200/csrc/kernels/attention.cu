@@ -286,6 +286,78 @@ __device__ __forceinline__ void attn_chunk(const uint32_t (&qa)[HD / 16][4], uin
   }
 }
 
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// One 16-token chunk for a group of exactly 8 query heads, transposed: S^T = K Q^T (m16n8k16 with
+// the 16 tokens as rows, K as the A operand, the 8 heads as the n = 8 columns) and O^T += V^T P^T
+// (V^T as A through ldmatrix.trans, P^T as B through movmatrix.trans of S^T's fragments).  The
+// padded form (Q as A, 16 rows of which 8 are real heads) spends half its MMAs and exp2s on
+// padding; here every MMA row and every exp2 is a real (token, head).  Per thread: heads 2tq,
+// 2tq+1 (their running max / sum), tokens gid and gid + 8 of the chunk.
+template <int HD>
+__device__ __forceinline__ void attn_chunk8(const uint32_t (&qb)[HD / 16][2], uint32_t skb,
+                                            uint32_t svb, int t0, int n_tok, float scale_log2,
+                                            float (&ot)[HD / 16][4], float (&mh)[2],
+                                            float (&lh)[2], int lane) {
+  const int gid = lane >> 2;
+  const int mat = lane >> 3, r = lane & 7;
+  float sc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int tok = (mat & 1) * 8 + r, cc = kk * 2 + (mat >> 1);
+    uint32_t a[4];
+    ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, a[0], a[1], a[2], a[3]);
+    mma_bf16(sc, a, qb[kk][0], qb[kk][1]);
+  }
+  // mask, per-head online softmax (exp2 domain); a head's 16 tokens live in the 8 lanes of
+  // its tq column x 2 rows
+  float mx[2];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int tok = t0 + gid + (e >> 1) * 8;
+    sc[e] = tok < n_tok ? sc[e] * scale_log2 : -INFINITY;
+  }
+  mx[0] = fmaxf(sc[0], sc[2]);
+  mx[1] = fmaxf(sc[1], sc[3]);
+  float alpha[2], muse[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
+    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
+    const float mnew = fmaxf(mh[h], mx[h]);
+    muse[h] = mnew == -INFINITY ? 0.0f : mnew;
+    alpha[h] = exp2f(mh[h] - muse[h]);
+    mh[h] = mnew;
+    lh[h] *= alpha[h];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    sc[e] = exp2f(sc[e] - muse[e & 1]);
+    lh[e & 1] += sc[e];
+  }
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    ot[mt][0] *= alpha[0];
+    ot[mt][1] *= alpha[1];
+    ot[mt][2] *= alpha[0];
+    ot[mt][3] *= alpha[1];
+  }
+  const uint32_t b0 = movmatrix_trans(pack_bf16(sc[0], sc[1]));   // P^T, tokens 0-7
+  const uint32_t b1 = movmatrix_trans(pack_bf16(sc[2], sc[3]));   // P^T, tokens 8-15
+#pragma unroll
+  for (int mt = 0; mt < HD / 16; ++mt) {
+    const int tok = (mat >> 1) * 8 + r, cc = mt * 2 + (mat & 1);
+    uint32_t a[4];
+    ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, a[0], a[1], a[2], a[3]);
+    mma_bf16(ot[mt], a, b0, b1);
+  }
+}
+
 // CTA owning global chunk index c when W chunks are split into C ranges [floor(iW/C), ...)
 __device__ __forceinline__ int cta_of_chunk(long long c, long long W, int C) {
   return (int)(((c + 1) * (long long)C + W - 1) / W) - 1;
@@ -302,7 +374,9 @@ __device__ __forceinline__ long long chunk_begin(int i, long long W, int C) {
 // piece write its (max, sum, O) partial, and the last piece to arrive merges all pieces in
 // piece order (deterministic) and writes o.  Inside a piece the 4 warps take chunks round
 // robin through a 2-stage cp.async ring and merge through shared memory.
-template <int HD, int ST>
+// T8: a group of exactly 8 query heads in the transposed form (attn_chunk8); the per-warp
+// state is stored to the same [warp][head][HD] merge layout, so the merges are shared.
+template <int HD, int ST, bool T8 = false>
 __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int CPR = HD / 8;                         // 16-byte chunks per row
@@ -428,8 +502,16 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
     const size_t pair_off = p.bt ? 0 : ((size_t)b * p.nkv + g) * p.smax * HD;
     const bf16* kbase = p.kc + pair_off;
     const bf16* vbase = p.vc + pair_off;
-    uint32_t qa[HD / 16][4];
-    {
+    uint32_t qa[T8 ? 1 : HD / 16][4];
+    uint32_t qb8[T8 ? HD / 16 : 1][2];
+    if constexpr (T8) {   // B = Q^T: (dims 2tq.., head gid), (dims 2tq + 8.., head gid)
+      const bf16* qr = p.q + ((size_t)b * p.nq + (size_t)g * 8 + gid) * HD + 2 * tq;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        qb8[kk][0] = *reinterpret_cast<const uint32_t*>(qr + kk * 16);
+        qb8[kk][1] = *reinterpret_cast<const uint32_t*>(qr + kk * 16 + 8);
+      }
+    } else {
       const bf16* qb = p.q + ((size_t)b * p.nq + (size_t)g * G) * HD;
       const int r0 = gid, r1 = gid + 8;
 #pragma unroll
@@ -441,9 +523,11 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
         qa[kk][3] = r1 < G ? *reinterpret_cast<const uint32_t*>(qb + r1 * HD + cc + 8) : 0u;
       }
     }
-    float o[HD / 8][4];
+    // padded form: o = O[16 rows][HD] fragments; transposed form: O^T[HD][8 heads] fragments
+    constexpr int NO = T8 ? HD / 16 : HD / 8;
+    float o[NO][4];
 #pragma unroll
-    for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
+    for (int i = 0; i < NO; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.0f;
     float mrow[2] = {-INFINITY, -INFINITY};
     float lrow[2] = {0.0f, 0.0f};
 
@@ -492,32 +576,58 @@ __global__ void __launch_bounds__(128) attn_kernel(const AttnParams p) {
       const uint32_t skb = smem_u32(sk), svb = smem_u32(sv);
       const int t0 = ch * kChunk;
 
-      attn_chunk<HD>(qa, skb, svb, t0, n_tok, p.scale_log2, o, mrow, lrow, lane);
+      if constexpr (T8)
+        attn_chunk8<HD>(qb8, skb, svb, t0, n_tok, p.scale_log2, o, mrow, lrow, lane);
+      else
+        attn_chunk<HD>(qa, skb, svb, t0, n_tok, p.scale_log2, o, mrow, lrow, lane);
       __syncwarp();
     }
     cp_async_wait<0>();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
-      lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
+      if constexpr (T8) {   // a head's sum is spread over the 8 gid lanes of its tq column
+        lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 4);
+        lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 8);
+        lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 16);
+      } else {
+        lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
+        lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
+      }
     }
     __syncthreads();
     // ---- merge the 4 warps through shared memory (reuses the K/V ring)
     float* sm_o = reinterpret_cast<float*>(smem);                 // [warp][16][HD]
     float* sm_m = sm_o + kWarps * 16 * HD;                        // [warp][16]
     float* sm_l = sm_m + kWarps * 16;
+    if constexpr (T8) {
+      // O^T fragment: dim = mt * 16 + gid (+ 8), head = 2 tq (+ 1); heads 8-15 are never read
 #pragma unroll
-    for (int dn = 0; dn < HD / 8; ++dn)
+      for (int mt = 0; mt < HD / 16; ++mt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int row = gid + 8 * (e >> 1), col = dn * 8 + 2 * tq + (e & 1);
-        sm_o[(warp * 16 + row) * HD + col] = o[dn][e];
+        for (int e = 0; e < 4; ++e) {
+          const int head = 2 * tq + (e & 1), dim = mt * 16 + gid + 8 * (e >> 1);
+          sm_o[(warp * 16 + head) * HD + dim] = o[mt][e];
+        }
+      if (gid == 0) {
+        sm_m[warp * 16 + 2 * tq] = mrow[0];
+        sm_m[warp * 16 + 2 * tq + 1] = mrow[1];
+        sm_l[warp * 16 + 2 * tq] = lrow[0];
+        sm_l[warp * 16 + 2 * tq + 1] = lrow[1];
       }
-    if (tq == 0) {
-      sm_m[warp * 16 + gid] = mrow[0];
-      sm_m[warp * 16 + gid + 8] = mrow[1];
-      sm_l[warp * 16 + gid] = lrow[0];
-      sm_l[warp * 16 + gid + 8] = lrow[1];
+    } else {
+#pragma unroll
+      for (int dn = 0; dn < HD / 8; ++dn)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = gid + 8 * (e >> 1), col = dn * 8 + 2 * tq + (e & 1);
+          sm_o[(warp * 16 + row) * HD + col] = o[dn][e];
+        }
+      if (tq == 0) {
+        sm_m[warp * 16 + gid] = mrow[0];
+        sm_m[warp * 16 + gid + 8] = mrow[1];
+        sm_l[warp * 16 + gid] = lrow[0];
+        sm_l[warp * 16 + gid + 8] = lrow[1];
+      }
     }
     __syncthreads();
     const bool whole = lo == 0 && hi == chb;
@@ -754,78 +864,6 @@ __global__ void __launch_bounds__(128) attn_warp_kernel(const AttnParams p) {
   }
 }
 
-__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
-  uint32_t y;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-
-// One 16-token chunk for a group of exactly 8 query heads, transposed: S^T = K Q^T (m16n8k16 with
-// the 16 tokens as rows, K as the A operand, the 8 heads as the n = 8 columns) and O^T += V^T P^T
-// (V^T as A through ldmatrix.trans, P^T as B through movmatrix.trans of S^T's fragments).  The
-// padded form (Q as A, 16 rows of which 8 are real heads) spends half its MMAs and exp2s on
-// padding; here every MMA row and every exp2 is a real (token, head).  Per thread: heads 2tq,
-// 2tq+1 (their running max / sum), tokens gid and gid + 8 of the chunk.
-template <int HD>
-__device__ __forceinline__ void attn_chunk8(const uint32_t (&qb)[HD / 16][2], uint32_t skb,
-                                            uint32_t svb, int t0, int n_tok, float scale_log2,
-                                            float (&ot)[HD / 16][4], float (&mh)[2],
-                                            float (&lh)[2], int lane) {
-  const int gid = lane >> 2;
-  const int mat = lane >> 3, r = lane & 7;
-  float sc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-  for (int kk = 0; kk < HD / 16; ++kk) {
-    const int tok = (mat & 1) * 8 + r, cc = kk * 2 + (mat >> 1);
-    uint32_t a[4];
-    ldsm_x4(skb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, a[0], a[1], a[2], a[3]);
-    mma_bf16(sc, a, qb[kk][0], qb[kk][1]);
-  }
-  // mask, per-head online softmax (exp2 domain); a head's 16 tokens live in the 8 lanes of
-  // its tq column x 2 rows
-  float mx[2];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int tok = t0 + gid + (e >> 1) * 8;
-    sc[e] = tok < n_tok ? sc[e] * scale_log2 : -INFINITY;
-  }
-  mx[0] = fmaxf(sc[0], sc[2]);
-  mx[1] = fmaxf(sc[1], sc[3]);
-  float alpha[2], muse[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
-    mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
-    const float mnew = fmaxf(mh[h], mx[h]);
-    muse[h] = mnew == -INFINITY ? 0.0f : mnew;
-    alpha[h] = exp2f(mh[h] - muse[h]);
-    mh[h] = mnew;
-    lh[h] *= alpha[h];
-  }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    sc[e] = exp2f(sc[e] - muse[e & 1]);
-    lh[e & 1] += sc[e];
-  }
-#pragma unroll
-  for (int mt = 0; mt < HD / 16; ++mt) {
-    ot[mt][0] *= alpha[0];
-    ot[mt][1] *= alpha[1];
-    ot[mt][2] *= alpha[0];
-    ot[mt][3] *= alpha[1];
-  }
-  const uint32_t b0 = movmatrix_trans(pack_bf16(sc[0], sc[1]));   // P^T, tokens 0-7
-  const uint32_t b1 = movmatrix_trans(pack_bf16(sc[2], sc[3]));   // P^T, tokens 8-15
-#pragma unroll
-  for (int mt = 0; mt < HD / 16; ++mt) {
-    const int tok = (mat >> 1) * 8 + r, cc = mt * 2 + (mat & 1);
-    uint32_t a[4];
-    ldsm_x4_t(svb + (tok * HD + ((cc ^ (tok & 7)) * 8)) * 2, a[0], a[1], a[2], a[3]);
-    mma_bf16(ot[mt], a, b0, b1);
-  }
-}
-
 // attn_warp_kernel for G = 8 (Qwen3-32B, Llama-3.1-70B, Qwen2.5-72B: 64 / 8 heads) with the
 // transposed chunk math above; same partition, ring and loads.
 template <int HD, int ST>
@@ -942,13 +980,21 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   const size_t ring = (size_t)kWarps * ST * 2 * kChunk * HD * 2;
   const size_t smem = ring + (((size_t)a.B + 1) * 4 + 15) / 16 * 16;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static unsigned long long attr = 0;
+  static unsigned long long attr = 0, attr8 = 0;
   if (first_on_device(attr))
     cudaFuncSetAttribute(attn_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (first_on_device(attr8))
+    cudaFuncSetAttribute(attn_kernel<HD, ST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  // groups of 8 query heads: the transposed chunk math (SIDP_ATTN_SWAP=0: the padded form)
+  static const int env_swap = getenv("SIDP_ATTN_SWAP") ? atoi(getenv("SIDP_ATTN_SWAP")) : 1;
+  const bool swap8 = env_swap && a.nq == 8 * a.nkv;
   // one wave of resident CTAs; fewer when the batch has little work (>= 8 chunks per CTA at
   // the host's context bound, so each warp streams at least two chunks)
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<HD, ST>, 128, smem);
+  if (swap8)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<HD, ST, true>, 128, smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_kernel<HD, ST>, 128, smem);
   per_sm = std::max(1, per_sm);
   const int max_tok = (a.max_tokens > 0 && a.max_tokens < a.smax) ? a.max_tokens : a.smax;
   const long long w_max = (long long)a.B * a.nkv * ((max_tok + kChunk - 1) / kChunk);
@@ -986,8 +1032,6 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
     if (first_on_device(wattr))
       cudaFuncSetAttribute(attn_warp_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-    static const int env_swap = getenv("SIDP_ATTN_SWAP") ? atoi(getenv("SIDP_ATTN_SWAP")) : 1;
-    const bool swap8 = env_swap && a.nq == 8 * a.nkv;
     int wper = 0;
     if (swap8)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, attn_warp8_kernel<HD, ST>, 128, ring);
@@ -1020,6 +1064,7 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   p.pre_wait = env_pre;
   p.pair_mode = (long long)ctas == pairs ? 1 : 0;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)HD));
+  if (swap8) return launch_pdl(attn_kernel<HD, ST, true>, dim3(ctas), dim3(128), smem, s, p);
   return launch_pdl(attn_kernel<HD, ST>, dim3(ctas), dim3(128), smem, s, p);
 }
 
@@ -1056,6 +1101,9 @@ cudaError_t attention_preload() {
   // >48 KB shared-memory attribute, set here for this device (sidp_alloc calls this)
 #define SIDP_PRELOAD_ATTN(hd, st)                                                                \
   if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError();    \
+  if (cudaFuncGetAttributes(&fa, attn_kernel<hd, st, true>) != cudaSuccess) e = cudaGetLastError(); \
+  if (cudaFuncSetAttribute(attn_kernel<hd, st, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           200 * 1024) != cudaSuccess) e = cudaGetLastError();                     \
   if (cudaFuncGetAttributes(&fa, attn_warp_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError(); \
   if (cudaFuncGetAttributes(&fa, attn_warp8_kernel<hd, st>) != cudaSuccess) e = cudaGetLastError(); \
   if (cudaFuncSetAttribute(attn_warp8_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
