@@ -1019,8 +1019,10 @@ cudaError_t attn_launch_t(const AttnArgs& a, cudaStream_t s) {
   if (pairs >= slots) {
     cl = chunks_per_pair >= 64 ? pairs : slots;
   } else {
-    const long long k = std::max<long long>(1, std::min<long long>(std::max<long long>(1, 128 / pairs),
-                                                                   chunks_per_pair / 32));
+    static const long long env_tgt = getenv("SIDP_ATTN_SPLIT_TARGET") ? atoll(getenv("SIDP_ATTN_SPLIT_TARGET")) : 128;
+    static const long long env_minch = getenv("SIDP_ATTN_SPLIT_MINCH") ? atoll(getenv("SIDP_ATTN_SPLIT_MINCH")) : 32;
+    const long long k = std::max<long long>(1, std::min<long long>(std::max<long long>(1, env_tgt / pairs),
+                                                                   chunks_per_pair / env_minch));
     cl = std::min(slots, pairs * k);
   }
   // Many pairs of < SIDP_ATTN_WARP_CH (default 128) chunks: warp-per-pair kernel, one wave
