@@ -217,7 +217,10 @@ sidp_status sidp_owned_bytes(const sidp_ctx* ctx, uint64_t* bytes);
  * 256-byte aligned.  The library lays the owned layers out in it (sidp_init_weights_synthetic
  * fills them), never frees it, and exports it to peers as its allocation's IPC handle plus the
  * arena's offset inside that allocation, so an arena carved from a larger (caching-allocator)
- * segment works.  The caller keeps it alive and unmodified until sidp_destroy.  Everything else
+ * segment works — so it must be cudaMalloc-backed (torch's default caching allocator; not a
+ * cuMemCreate / expandable-segments allocation, which has no legacy IPC handle: peers then fail
+ * sidp_import_handles with SIDP_EPEER).  The caller keeps it alive and unmodified until
+ * sidp_destroy.  Everything else
  * (local layers, slots, workspaces, CaS staging) is allocated as by sidp_alloc.  SIDP_EINVAL
  * (nothing allocated) if the arena is too small, misaligned or not device memory of the
  * context's device; otherwise as sidp_alloc. */
