@@ -130,7 +130,7 @@ void run(const char* name, int commit_every) {
 
 // Ring mode: the GEMM mainloop's MMA side without loads — S stages, each 8 MMAs (two 64-deep
 // k-blocks) then a commit to that stage's barrier; stage i waits for the commit of stage i - S.
-template <int N, int S>
+template <int N, int S, bool MOVE = false>
 __global__ void __launch_bounds__(128, 1) ring_probe(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
@@ -154,9 +154,11 @@ __global__ void __launch_bounds__(128, 1) ring_probe(int iters, unsigned long lo
   const bool leader = ctarank() == 0;
   unsigned long long t0 = clock64();
   if (warp == 1 && leader && threadIdx.x == 32) {
-    const uint32_t a0 = smem_u32(smem), b0 = smem_u32(smem + 32768);
     for (int i = 0; i < iters; ++i) {
       const int st = i % S;
+      // MOVE: every stage reads its own 50 KB operand buffers (as the GEMM's ring does)
+      const uint32_t a0 = smem_u32(smem) + (MOVE ? (uint32_t)(st % 4) * 51200u : 0u);
+      const uint32_t b0 = a0 + 32768;
       if (i >= S) mbar_wait(&bars[st], ((i / S) - 1) & 1);
       tc_fence_after();
       for (int j = 0; j < 2; ++j)
@@ -178,16 +180,16 @@ __global__ void __launch_bounds__(128, 1) ring_probe(int iters, unsigned long lo
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
-template <int N, int S>
+template <int N, int S, bool MOVE = false>
 void run_ring(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
-  auto k = ring_probe<N, S>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  auto k = ring_probe<N, S, MOVE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(148);
   cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = 100 * 1024;
+  cfg.dynamicSmemBytes = 210 * 1024;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -230,6 +232,7 @@ int main() {
   run_ring<144, 2>("ring N=144 S=2");
   run_ring<144, 8>("ring N=144 S=8");
   run_ring<256, 4>("ring N=256 S=4");
+  run_ring<144, 4, true>("ring N=144 S=4 moving buffers");
   run<1, 128>("1-CTA M=128 N=128", 0);
   return 0;
 }
