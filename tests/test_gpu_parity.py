@@ -928,14 +928,15 @@ def test_paged_kv_fused_qkv_epilogue():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("name", ["tiny", "tiny-qwen3", "tiny-qwen25"])
-def test_prefill_vs_oracle(P, name):
+@pytest.mark.parametrize("name,layers", [("tiny", 4), ("tiny-qwen3", 4), ("tiny-qwen25", 4),
+                                         ("qwen3-32b", 2)])   # 8-head groups: transposed attention
+def test_prefill_vs_oracle(P, name, layers):
     """Prefill as one ragged step over a paged cache: prompts of 5, 17 and 33
     tokens (crossing 16-token blocks) appended to three sequences with existing contexts.  Per
     layer, teacher-forced (C-N8): every prompt row's layer output and new k/v against the fp64
     oracle from the GPU's layer input and the sequence's KV state (the oracle attends over the
     row's causal prefix, the earlier prompt rows' entries included), and the logits."""
-    m = MODELS[name].with_layers(4)
+    m = MODELS[name].with_layers(layers)
     S, lens, pos0 = 3, [5, 17, 33], [10, 0, 20]
     rows, max_ctx = sum(lens), 80
     ctxt = P.Context(m, max_batch=rows, max_ctx=max_ctx, seed=SEED)
@@ -961,8 +962,10 @@ def test_prefill_vs_oracle(P, name):
         out, kn, vn = oracle_layer(om, l, xs[l], pos, K, V)
         b = np.arange(rows)
         errs = [rel_err(K[b, pos], kn), rel_err(V[b, pos], vn)]
-        errs.append(rel_err(xs[l + 1], out) if l + 1 < m.num_layers
-                    else rel_err(lg, OM.lm_head(m, om.head, out)))
+        if l + 1 < m.num_layers:
+            errs.append(rel_err(xs[l + 1], out))
+        elif m.vocab <= 10000:   # full-width heads (6 GB in fp64) are checked by the step tests
+            errs.append(rel_err(lg, OM.lm_head(m, om.head, out)))
         assert max(errs) <= TOL, (l, errs)
     assert (nxt.cpu().numpy() == np.argmax(lg[last], axis=1)).all()
     ctxt.destroy()
