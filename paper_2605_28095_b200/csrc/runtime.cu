@@ -233,6 +233,13 @@ struct sidp_ctx {
 namespace {
 
 // Compute-grid SM budget for the duration of one public call (kernels.h set_compute_sms).
+// CaS grids use every SM — except on a GPU shared with the peers (virtual ranks, the 1-GPU IPC
+// test), where the other ranks' one-CTA flag-wait kernels hold a few SMs: a persistent grid
+// sized to all of them would leave some CTA pairs waiting for those SMs (SIDP_CAS_SM_RESERVE
+// SMs are left out there; default 16: one live rank 303 -> 253 us per Qwen3 layer, all live
+// B = 16 480 -> 396; 8: 253 / 457, 24: 260 / 409)
+int cas_compute_sms(const sidp_ctx* c);
+
 struct BudgetGuard {
   int prev;
   explicit BudgetGuard(int n) : prev(sidp::get_compute_sms_budget()) { sidp::set_compute_sms(n); }
@@ -1011,6 +1018,14 @@ bool cas_fused() { return cas_level() >= 1; }
 bool prologue_waits(const sidp_ctx* c) {
   static const int env = getenv("SIDP_CAS_PROLOGUE_WAIT") ? atoi(getenv("SIDP_CAS_PROLOGUE_WAIT")) : -1;
   return env >= 0 ? env != 0 : !c->same_device_peer;
+}
+
+int cas_compute_sms(const sidp_ctx* c) {
+  static const int env = getenv("SIDP_CAS_SM_RESERVE") ? atoi(getenv("SIDP_CAS_SM_RESERVE")) : 16;
+  if (!c->same_device_peer || env <= 0) return 0;
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->c.device);
+  return std::max(2, (dev_sms - env) & ~1);
 }
 
 // A FlagWait for a consumer kernel, or (no prologue waits) a standalone wait kernel now and an
@@ -2073,7 +2088,7 @@ sidp_status sidp_decode_layer(sidp_ctx* ctx, void* x, int32_t batch, int32_t lay
   if (st != SIDP_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   bf16* xb = reinterpret_cast<bf16*>(x);
-  BudgetGuard budget(mode == SIDP_CAS ? 0 : ctx->compute_sms);
+  BudgetGuard budget(mode == SIDP_CAS ? cas_compute_sms(ctx) : ctx->compute_sms);
   if (mode == SIDP_REPLICATED) {
     if (ctx->d != 1) return fail(SIDP_EINVAL, "SIDP_REPLICATED needs world == 1");
     mode = SIDP_WAS;
@@ -2289,7 +2304,7 @@ sidp_status sidp_step(sidp_ctx* ctx, const sidp_batch* b, void* stream) {
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   ctx->last_stream = s;
-  BudgetGuard budget(ctx->mode == SIDP_CAS ? 0 : ctx->compute_sms);
+  BudgetGuard budget(ctx->mode == SIDP_CAS ? cas_compute_sms(ctx) : ctx->compute_sms);
   if (ctx->mode != SIDP_CAS && ctx->R > 0) {
     // the step's fetches (+ the next step's first S) up front: one launch with the windowed
     // device ring, else the first S (the layers' pumps add the rest as slots free up)
