@@ -1751,8 +1751,12 @@ cudaError_t gemm_launch(const GemmArgs& a, const GemmWorkspace& w, cudaStream_t 
   // (Stream-K for badly quantised larger tile counts — e.g. down at M = 1024: 80 tiles on 74
   // pairs, 2 waves, 282 us vs cuBLAS 192 — measured slower still: 258-295 us at M = 1024 and
   // 431 vs 301 us at M = 1536, so those shapes keep whole tiles.)
+  // SIDP_GEMM_SMALL_M_STREAMK = m > 0: underfilled tile counts at M <= m go stream-K too (tiny
+  // token tiles are pure weight streaming); default off (measured on the CaS owner)
+  static const int env_small = getenv("SIDP_GEMM_SMALL_M_STREAMK") ? atoi(getenv("SIDP_GEMM_SMALL_M_STREAMK")) : 0;
   int streamk = (!sw && a.epi != EPI_ARGMAX && a.epi != EPI_QKV && a.k_splits != 1 &&
-                 (a.k_splits > 1 || 2 * tiles <= clusters)) ? 1 : 0;
+                 (a.k_splits > 1 || 2 * tiles <= clusters ||
+                  (env_small > 0 && a.M <= env_small && tiles < clusters))) ? 1 : 0;
   if (streamk) {
     const long long total = (long long)tiles * nkb;
     const long long per = total / clusters;
