@@ -1080,15 +1080,17 @@ cudaError_t attention_launch(const AttnArgs& a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  // SIDP_ATTN_STAGES = 2 selects the 2-stage rings (3, the default, measured fastest: M2 29.05 vs
+  // 29.72 ms with the transposed kernels).  The 4-stage instantiations are no longer selectable:
+  // they raised cudaErrorIllegalInstruction on sm_100a in r2 (not investigated; r1 had measured
+  // them slower, 214 vs 181 us).
   static const int stages = getenv("SIDP_ATTN_STAGES") ? atoi(getenv("SIDP_ATTN_STAGES")) : 3;
   g_attn_launches = 1;
   if (a.hd == 128) {
     if (stages == 2) return attn_launch_t<128, 2>(a, s);
-    if (stages == 4) return attn_launch_t<128, 4>(a, s);
     return attn_launch_t<128, 3>(a, s);
   }
   if (stages == 2) return attn_launch_t<64, 2>(a, s);
-  if (stages == 4) return attn_launch_t<64, 4>(a, s);
   return attn_launch_t<64, 3>(a, s);
 }
 
@@ -1114,8 +1116,8 @@ cudaError_t attention_preload() {
                            200 * 1024) != cudaSuccess) e = cudaGetLastError();                     \
   if (cudaFuncSetAttribute(attn_warp_kernel<hd, st>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            200 * 1024) != cudaSuccess) e = cudaGetLastError();
-  SIDP_PRELOAD_ATTN(128, 2) SIDP_PRELOAD_ATTN(128, 3) SIDP_PRELOAD_ATTN(128, 4)
-  SIDP_PRELOAD_ATTN(64, 2) SIDP_PRELOAD_ATTN(64, 3) SIDP_PRELOAD_ATTN(64, 4)
+  SIDP_PRELOAD_ATTN(128, 2) SIDP_PRELOAD_ATTN(128, 3)
+  SIDP_PRELOAD_ATTN(64, 2) SIDP_PRELOAD_ATTN(64, 3)
 #undef SIDP_PRELOAD_ATTN
   return e;
 }
