@@ -174,3 +174,27 @@ def test_fused_mlp_schedule_invariants(sidp, h, I, C, max_seg, MT):
     bound = max(work / C, max(done.values()) + 1)
     if C == 74 and h >= 5120:
         assert max(end) <= 1.10 * bound, (max(end), bound)
+
+
+def test_paged_kv_binding_layout(sidp):
+    """PagedKVCache (host side of sidp_kv.block_table): from_contiguous scatters each row's
+    16-token blocks to a seeded permutation of the pool and to_contiguous gathers them back
+    exactly; the ctypes struct carries the table, block size, row stride and pool size."""
+    import torch
+    m = MODELS["tiny"].with_layers(2)
+    kv = sidp.KVCache(m, 3, 40, device="cpu")
+    g = torch.Generator().manual_seed(3)
+    kv.k.copy_(torch.randn(kv.k.shape, generator=g).to(torch.bfloat16))
+    kv.v.copy_(torch.randn(kv.v.shape, generator=g).to(torch.bfloat16))
+    kv.set_pos([5, 17, 33])
+    pk = sidp.PagedKVCache.from_contiguous(kv, m, seed=9, spare=4)
+    assert pk.max_blocks == 3 and pk.num_blocks == 3 * 3 + 4
+    assert sorted(pk.table.flatten().tolist()) == sorted(set(pk.table.flatten().tolist()))
+    for l in range(2):
+        for which, ref in (("k", kv.k[l]), ("v", kv.v[l])):
+            got = pk.to_contiguous(l, which)[:, :, :40]
+            assert torch.equal(got, ref)
+    c = pk.c()
+    assert c.block_tokens == 16 and c.max_blocks == 3 and c.num_blocks == 13
+    assert c.block_table == pk.table.data_ptr() and c.max_pos == 33
+    assert kv.c().block_table is None
