@@ -149,6 +149,17 @@ class _RowsKV:
                     self.table.data_ptr(), PagedKVCache.BLOCK, self.max_blocks, self.num_blocks)
 
 
+def prefill_rows(pos0, prompts):
+    """Host side of prefill: one row per prompt token — (sequence of the row, its position
+    pos0[seq] + i, its token) — and the row of each sequence's last prompt token."""
+    import numpy as np
+    lens = [len(p) for p in prompts]
+    seq = np.concatenate([np.full(n, b) for b, n in enumerate(lens)]).astype(np.int64)
+    pos = np.concatenate([int(pos0[b]) + np.arange(n) for b, n in enumerate(lens)]).astype(np.int32)
+    toks = np.concatenate([np.asarray(p, dtype=np.int32) for p in prompts])
+    return seq, pos, toks, np.cumsum(lens) - 1
+
+
 def prefill(ctx: "Context", kv: "PagedKVCache", prompts, stream=None, logits=None,
             layer_inputs=None):
     """Prefill as ONE ragged decode step: every prompt token of every
@@ -163,16 +174,13 @@ def prefill(ctx: "Context", kv: "PagedKVCache", prompts, stream=None, logits=Non
     import torch
     dev = kv.k.device
     lens = [len(p) for p in prompts]
-    pos0 = kv.pos[:len(prompts)].cpu().numpy()
-    seq = np.concatenate([np.full(n, b) for b, n in enumerate(lens)]).astype(np.int64)
-    pos = np.concatenate([pos0[b] + np.arange(n) for b, n in enumerate(lens)]).astype(np.int32)
-    toks = torch.from_numpy(np.concatenate([np.asarray(p, dtype=np.int32) for p in prompts])).to(dev)
+    seq, pos, toks_np, last = prefill_rows(kv.pos[:len(prompts)].cpu().numpy(), prompts)
+    toks = torch.from_numpy(toks_np).to(dev)
     rows = len(seq)
     view = _RowsKV(kv, kv.table[torch.from_numpy(seq).to(dev)].contiguous(),
                    torch.from_numpy(pos).to(dev))
     nxt = torch.zeros(rows, dtype=torch.int32, device=dev)
     ctx.step(toks, nxt, view, batch=rows, logits=logits, layer_inputs=layer_inputs, stream=stream)
-    last = np.cumsum(lens) - 1
     kv.pos[:len(prompts)] += torch.as_tensor(lens, dtype=torch.int32, device=dev)
     kv.max_pos = int(kv.pos[:len(prompts)].max().item())
     return nxt[torch.from_numpy(last).to(dev)], last

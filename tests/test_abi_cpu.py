@@ -198,3 +198,16 @@ def test_paged_kv_binding_layout(sidp):
     assert c.block_tokens == 16 and c.max_blocks == 3 and c.num_blocks == 13
     assert c.block_table == pk.table.data_ptr() and c.max_pos == 33
     assert kv.c().block_table is None
+
+
+def test_prefill_rows():
+    """Prefill's row layout (host logic of paper_2605_28095_b200.prefill): every prompt token is a
+    row at position pos0[b] + i of its sequence; the last row of each sequence gives its next
+    token."""
+    import numpy as np
+    from paper_2605_28095_b200.api import prefill_rows
+    seq, pos, toks, last = prefill_rows(np.array([10, 0, 20]), [[1, 2], [3], [4, 5, 6]])
+    assert seq.tolist() == [0, 0, 1, 2, 2, 2]
+    assert pos.tolist() == [10, 11, 0, 20, 21, 22]
+    assert toks.tolist() == [1, 2, 3, 4, 5, 6]
+    assert last.tolist() == [1, 2, 5]
